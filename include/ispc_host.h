@@ -1,0 +1,110 @@
+/*
+ * ispc_host.h — C-ABI of the reference-side host library (libispc_host.so).
+ *
+ * This library lives on the CALLER side of the boundary declared in ispc.h:
+ * it links the reference search-space library (namespace ispace) unchanged
+ * and exposes, as plain C, what a driver needs to walk the space and hand
+ * fully specified candidates to the B200 backend:
+ *
+ *   kernel builders       make_axpy / make_matmul / make_outer_product
+ *                         (proj/core/include/ispace/kernels.hpp:110-121)
+ *   space construction    build_gpu_space (gpu_space.hpp:18) with MachineParams
+ *                         (machine.hpp:17-34)
+ *   candidates            make_root / apply_decision / open_choices /
+ *                         fully_specified / digest (candidate.hpp:69-95)
+ *   reconstruction        reconstruct (loop_nest.hpp:52) -> flat ispc_nest
+ *   reference evaluation  emit_source (loop_nest.hpp:62), evaluate
+ *                         (simulate.hpp:33) for cross-checks
+ *   B200 lower bound      ispc_bound (the reference's bound.cpp is a stub;
+ *                         contract SPEC.md:416-457, re-parameterised in seconds)
+ *   branch and bound      ispc_search_run (the reference's search.cpp is a stub;
+ *                         contract SPEC.md:459-514) sharding subtrees over GPUs
+ *
+ * Status convention as in ispc.h. Decisions return 0 (ok), 1 (dead end).
+ */
+#ifndef ISPC_HOST_H
+#define ISPC_HOST_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "ispc.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ispc_space ispc_space;
+typedef struct ispc_cand ispc_cand;
+typedef struct ispc_nest_buf ispc_nest_buf;
+
+/* Space modes: PARITY = the reference's gpu.space and default MachineParams
+ * (candidate counts equal the reference's); B200 = the same space bound to
+ * B200 machine limits (227 KiB shared memory per block). */
+enum ispc_space_mode { ISPC_SPACE_PARITY = 0, ISPC_SPACE_B200 = 1 };
+
+typedef struct {
+  const char* kind;       /* "axpy" | "outer_product" | "matmul"                  */
+  int64_t m, n, k;        /* axpy uses n                                          */
+  int64_t a_stride;       /* matmul: element stride of A (1 = dense)              */
+  int32_t num_factors;    /* strip-mining universes, outermost first              */
+  int32_t factor_len[4];  /* values per universe                                  */
+  int64_t factors[4][32];
+  int32_t mode;           /* ispc_space_mode                                      */
+  int32_t _pad;
+} ispc_kernel_spec;
+
+typedef struct {
+  uint64_t instances;       /* choice instances (enum + integer + counter)        */
+  uint64_t enum_instances, int_instances, counter_instances;
+  uint64_t objects;         /* backbone objects                                   */
+  uint64_t lowerings;
+  uint64_t root_open;       /* open choices at the root                           */
+  uint64_t root_digest;
+  double build_seconds;
+} ispc_space_stats;
+
+int ispc_space_create(const ispc_kernel_spec* spec, ispc_space** out);
+void ispc_space_free(ispc_space* s);
+int ispc_space_stats_get(const ispc_space* s, ispc_space_stats* out);
+int ispc_space_problem(const ispc_space* s, ispc_problem* out); /* matching ispc_problem */
+const char* ispc_host_last_error(void);
+
+int ispc_cand_root(const ispc_space* s, ispc_cand** out);
+ispc_cand* ispc_cand_clone(const ispc_cand* c);
+void ispc_cand_free(ispc_cand* c);
+/* Named decision, in the orientation the names are given (antisymmetric
+ * choices resolved like nest_test.cpp:36-55). 0 ok, 1 dead end, <0 error. */
+int ispc_cand_decide(const ispc_space* s, ispc_cand* c, const char* choice, const char* arg0,
+                     const char* arg1, const char* value);
+int ispc_cand_open_count(const ispc_space* s, const ispc_cand* c);
+int ispc_cand_fully_specified(const ispc_space* s, const ispc_cand* c);
+uint64_t ispc_cand_digest(const ispc_space* s, const ispc_cand* c);
+uint64_t ispc_cand_fired(const ispc_cand* c);
+
+/* First-open depth-first descent, values in index order (nest_test.cpp:57-75). */
+int ispc_cand_first_leaf(const ispc_space* s, const ispc_cand* from, int budget, ispc_cand** out);
+/* Uniform random descent with restart on dead ends: at each step the first
+ * open instance in `order` (NULL: declaration order) gets a uniformly drawn
+ * value. Reports decisions applied and dead ends met. 0 ok, 1 gave up. */
+int ispc_cand_random_leaf(const ispc_space* s, const ispc_cand* from, uint64_t seed, int max_restarts,
+                          ispc_cand** out, int64_t* decisions, int64_t* dead_ends);
+/* Exhaustive first-open enumeration; returns the number of leaves (capped). */
+int64_t ispc_count_leaves(const ispc_space* s, const ispc_cand* from, int64_t cap);
+
+/* reconstruct() + flatten. */
+int ispc_cand_to_nest(const ispc_space* s, const ispc_cand* c, ispc_nest_buf** out);
+const ispc_nest* ispc_nest_buf_get(const ispc_nest_buf* b);
+void ispc_nest_buf_free(ispc_nest_buf* b);
+
+/* Reference-side renderings / costs of the same candidate. */
+int ispc_cand_reference_source(const ispc_space* s, const ispc_cand* c, char* buf, size_t cap, size_t* len);
+/* evaluate(): out = {compute, memory, sync, block_serial, total} cycles. */
+int ispc_cand_simulate(const ispc_space* s, const ispc_cand* c, int64_t out[5]);
+int ispc_cand_serialize(const ispc_space* s, const ispc_cand* c, char* buf, size_t cap, size_t* len);
+int ispc_cand_deserialize(const ispc_space* s, const char* text, ispc_cand** out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISPC_HOST_H */

@@ -1,0 +1,240 @@
+"""ctypes bindings of the two C-ABI libraries (include/ispc.h, include/ispc_host.h).
+
+The libraries are built in-tree by ``__graft_entry__.build()`` (``make`` in
+``csrc/`` and ``host/``). There is no fallback: importing a binding whose
+shared object is missing raises, so a GPU run can never silently evaluate
+candidates anywhere but on the device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIBISPC_PATH = os.path.join(_HERE, "csrc", "libispc.so")
+LIBHOST_PATH = os.path.join(_HERE, "host", "libispc_host.so")
+
+ISPC_NONE = 0xFFFFFFFF
+ABI_VERSION = 1
+
+STATUS = {0: "ok", -1: "arg", -2: "cuda", -3: "nvrtc", -4: "launch", -5: "mismatch",
+          -6: "timeout", -7: "illegal", -8: "nomem", -9: "sticky"}
+OK, E_ARG, E_CUDA, E_NVRTC, E_LAUNCH, E_MISMATCH, E_TIMEOUT, E_ILLEGAL, E_NOMEM, E_STICKY = (
+    0, -1, -2, -3, -4, -5, -6, -7, -8, -9)
+
+PROB_AXPY, PROB_OUTER, PROB_MATMUL, PROB_GEMV, PROB_BATCHED = range(5)
+SPACE_PARITY, SPACE_B200 = 0, 1
+
+
+class AddrTerm(C.Structure):
+    _fields_ = [("dim", C.c_uint32), ("size_dims_begin", C.c_uint32), ("size_dims_count", C.c_uint32),
+                ("_pad", C.c_uint32), ("base", C.c_int64)]
+
+
+class IVar(C.Structure):
+    _fields_ = [("offset", C.c_int64), ("terms_begin", C.c_uint32), ("terms_count", C.c_uint32)]
+
+
+class Operand(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("input", C.c_uint32), ("ivar", C.c_uint32), ("producer", C.c_uint32),
+                ("init", C.c_uint32), ("comm", C.c_uint32), ("pairs_begin", C.c_uint32),
+                ("pairs_count", C.c_uint32), ("reduce_begin", C.c_uint32), ("reduce_count", C.c_uint32),
+                ("value", C.c_int64)]
+
+
+class Inst(C.Structure):
+    _fields_ = [("obj", C.c_uint32), ("op", C.c_uint32), ("region", C.c_uint32), ("ivar", C.c_uint32),
+                ("operands_begin", C.c_uint32), ("operands_count", C.c_uint32), ("dims_begin", C.c_uint32),
+                ("dims_count", C.c_uint32), ("live", C.c_uint32), ("cache", C.c_uint32)]
+
+
+class Region(C.Structure):
+    _fields_ = [("obj", C.c_uint32), ("input", C.c_uint32), ("live", C.c_uint32), ("mem_space", C.c_uint32),
+                ("elems", C.c_int64), ("elem_bytes", C.c_int64)]
+
+
+class Dim(C.Structure):
+    _fields_ = [("obj", C.c_uint32), ("logical", C.c_uint32), ("is_static", C.c_uint32), ("_pad", C.c_uint32),
+                ("size", C.c_int64)]
+
+
+class Comm(C.Structure):
+    _fields_ = [("producer", C.c_uint32), ("consumer", C.c_uint32), ("region", C.c_uint32),
+                ("store", C.c_uint32), ("load", C.c_uint32), ("pairs_begin", C.c_uint32),
+                ("pairs_count", C.c_uint32), ("fired", C.c_uint32)]
+
+
+class Node(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("dim_kind", C.c_uint32), ("thread_level", C.c_int32),
+                ("block_level", C.c_int32), ("inst", C.c_uint32), ("dims_begin", C.c_uint32),
+                ("dims_count", C.c_uint32), ("children_begin", C.c_uint32), ("children_count", C.c_uint32),
+                ("_pad", C.c_uint32), ("size", C.c_int64)]
+
+
+class Nest(C.Structure):
+    _fields_ = [("abi_version", C.c_uint32), ("kernel_name", C.c_char_p), ("num_objects", C.c_uint32),
+                ("object_names", C.POINTER(C.c_char_p)),
+                ("num_insts", C.c_uint32), ("insts", C.POINTER(Inst)),
+                ("num_regions", C.c_uint32), ("regions", C.POINTER(Region)),
+                ("num_dims", C.c_uint32), ("dims", C.POINTER(Dim)),
+                ("num_ivars", C.c_uint32), ("ivars", C.POINTER(IVar)),
+                ("num_terms", C.c_uint32), ("terms", C.POINTER(AddrTerm)),
+                ("num_operands", C.c_uint32), ("operands", C.POINTER(Operand)),
+                ("num_comms", C.c_uint32), ("comms", C.POINTER(Comm)),
+                ("num_inputs", C.c_uint32), ("input_names", C.POINTER(C.c_char_p)),
+                ("pool_size", C.c_uint32), ("pool", C.POINTER(C.c_uint32)),
+                ("num_nodes", C.c_uint32), ("nodes", C.POINTER(Node)),
+                ("roots_begin", C.c_uint32), ("roots_count", C.c_uint32),
+                ("num_thread_levels", C.c_uint32), ("num_block_levels", C.c_uint32),
+                ("thread_shape", C.c_int64 * 3), ("block_shape", C.c_int64 * 3)]
+
+
+class Param(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("index", C.c_uint32), ("is_input", C.c_uint32), ("_pad", C.c_uint32),
+                ("elems", C.c_int64), ("name", C.c_char * 24)]
+
+
+class Launch(C.Structure):
+    _fields_ = [("name", C.c_char * 64), ("grid_x", C.c_uint64), ("block", C.c_uint32 * 3),
+                ("static_smem", C.c_uint32), ("num_params", C.c_uint32), ("params", Param * 32),
+                ("watchdog", C.c_uint32), ("reg_elems", C.c_uint32), ("source_hash", C.c_uint64)]
+
+
+class EmitOpts(C.Structure):
+    _fields_ = [("watchdog", C.c_uint32), ("max_reg_elems", C.c_uint32), ("max_unrolled", C.c_uint32),
+                ("_pad", C.c_uint32)]
+
+
+class Problem(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("_pad", C.c_uint32), ("m", C.c_int64), ("n", C.c_int64),
+                ("k", C.c_int64), ("batch", C.c_int64), ("a_stride", C.c_int64), ("seed", C.c_uint64),
+                ("alpha", C.c_float), ("_pad2", C.c_float)]
+
+
+class TimeOpts(C.Structure):
+    _fields_ = [("warmup", C.c_uint32), ("reps", C.c_uint32), ("flush_l2", C.c_uint32), ("check", C.c_uint32),
+                ("bit_exact", C.c_uint32), ("_pad", C.c_uint32), ("rtol", C.c_double),
+                ("budget_ns", C.c_double)]
+
+
+class TimeResult(C.Structure):
+    _fields_ = [("status", C.c_int), ("_pad", C.c_int), ("median_ns", C.c_double), ("min_ns", C.c_double),
+                ("first_ns", C.c_double), ("max_err", C.c_double), ("mismatches", C.c_int64)]
+
+
+class KernelSpec(C.Structure):
+    _fields_ = [("kind", C.c_char_p), ("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64),
+                ("a_stride", C.c_int64), ("num_factors", C.c_int32), ("factor_len", C.c_int32 * 4),
+                ("factors", (C.c_int64 * 32) * 4), ("mode", C.c_int32), ("_pad", C.c_int32)]
+
+
+class SpaceStats(C.Structure):
+    _fields_ = [("instances", C.c_uint64), ("enum_instances", C.c_uint64), ("int_instances", C.c_uint64),
+                ("counter_instances", C.c_uint64), ("objects", C.c_uint64), ("lowerings", C.c_uint64),
+                ("root_open", C.c_uint64), ("root_digest", C.c_uint64), ("build_seconds", C.c_double)]
+
+
+# Every symbol include/ispc.h declares, with its ctypes signature.
+ISPC_SYMBOLS = {
+    "ispc_emit_cuda": (C.c_int, [C.POINTER(Nest), C.POINTER(EmitOpts), C.c_char_p, C.c_char_p, C.c_size_t,
+                                 C.POINTER(C.c_size_t), C.POINTER(Launch)]),
+    "ispc_cuda_prelude": (C.c_char_p, []),
+    "ispc_emit_pseudo": (C.c_int, [C.POINTER(Nest), C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "ispc_compile": (C.c_int, [C.POINTER(C.c_char_p), C.c_int, C.c_char_p, C.POINTER(C.c_void_p)]),
+    "ispc_module_cubin": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
+    "ispc_module_log": (C.c_char_p, [C.c_void_p]),
+    "ispc_module_free": (None, [C.c_void_p]),
+    "ispc_dev_open": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "ispc_dev_close": (None, [C.c_void_p]),
+    "ispc_last_error": (C.c_char_p, [C.c_void_p]),
+    "ispc_dev_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                C.POINTER(C.c_int)]),
+    "ispc_bind_problem": (C.c_int, [C.c_void_p, C.POINTER(Problem)]),
+    "ispc_problem_region": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_uint64), C.POINTER(C.c_int64)]),
+    "ispc_module_load": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]),
+    "ispc_module_unload": (C.c_int, [C.c_void_p, C.c_int]),
+    "ispc_launch_timed": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(Launch), C.POINTER(TimeOpts),
+                                    C.POINTER(TimeResult)]),
+    "ispc_check": (C.c_int, [C.c_void_p, C.c_double, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                             C.POINTER(C.c_int)]),
+    "ispc_read_region": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t]),
+    "ispc_read_expected": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t]),
+    "ispc_evaluate": (C.c_int, [C.c_void_p, C.POINTER(Nest), C.POINTER(EmitOpts), C.POINTER(TimeOpts),
+                                C.POINTER(TimeResult), C.POINTER(Launch)]),
+}
+
+HOST_SYMBOLS = {
+    "ispc_space_create": (C.c_int, [C.POINTER(KernelSpec), C.POINTER(C.c_void_p)]),
+    "ispc_space_free": (None, [C.c_void_p]),
+    "ispc_space_stats_get": (C.c_int, [C.c_void_p, C.POINTER(SpaceStats)]),
+    "ispc_space_problem": (C.c_int, [C.c_void_p, C.POINTER(Problem)]),
+    "ispc_host_last_error": (C.c_char_p, []),
+    "ispc_cand_root": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "ispc_cand_clone": (C.c_void_p, [C.c_void_p]),
+    "ispc_cand_free": (None, [C.c_void_p]),
+    "ispc_cand_decide": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p]),
+    "ispc_cand_open_count": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "ispc_cand_fully_specified": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "ispc_cand_digest": (C.c_uint64, [C.c_void_p, C.c_void_p]),
+    "ispc_cand_fired": (C.c_uint64, [C.c_void_p]),
+    "ispc_cand_first_leaf": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "ispc_cand_random_leaf": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p),
+                                        C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "ispc_count_leaves": (C.c_int64, [C.c_void_p, C.c_void_p, C.c_int64]),
+    "ispc_cand_to_nest": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "ispc_nest_buf_get": (C.POINTER(Nest), [C.c_void_p]),
+    "ispc_nest_buf_free": (None, [C.c_void_p]),
+    "ispc_cand_reference_source": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_size_t,
+                                             C.POINTER(C.c_size_t)]),
+    "ispc_cand_simulate": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
+    "ispc_cand_serialize": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "ispc_cand_deserialize": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p)]),
+}
+
+_libs: dict[str, C.CDLL] = {}
+
+
+def _load(path: str, symbols: dict) -> C.CDLL:
+    if path in _libs:
+        return _libs[path]
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is not built; run __graft_entry__.build() (no CPU fallback exists)")
+    lib = C.CDLL(path, mode=C.RTLD_GLOBAL)
+    for name, (res, args) in symbols.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _libs[path] = lib
+    return lib
+
+
+def ispc() -> C.CDLL:
+    return _load(LIBISPC_PATH, ISPC_SYMBOLS)
+
+
+def host() -> C.CDLL:
+    ispc()  # the host library links libispc; load it first with its signatures
+    return _load(LIBHOST_PATH, HOST_SYMBOLS)
+
+
+def read_text(fn, *args) -> str:
+    """Calls a (..., char* buf, size_t cap, size_t* len) entry point twice."""
+    n = C.c_size_t(0)
+    rc = fn(*args, None, 0, C.byref(n))
+    if rc != 0:
+        raise RuntimeError(last_error())
+    buf = C.create_string_buffer(n.value + 1)
+    rc = fn(*args, buf, n.value + 1, C.byref(n))
+    if rc != 0:
+        raise RuntimeError(last_error())
+    return buf.value.decode()
+
+
+def last_error(dev=None) -> str:
+    e = ispc().ispc_last_error(dev)
+    return e.decode() if e else ""
+
+
+def host_error() -> str:
+    e = host().ispc_host_last_error()
+    return e.decode() if e else ""

@@ -1,0 +1,308 @@
+"""Python mirror of the reference's evaluation-path API over the two C ABIs.
+
+``Space`` / ``Candidate`` drive the reference search space (libispc_host:
+build_gpu_space, make_root, apply_decision, reconstruct). ``Device`` is the
+B200 backend (libispc: emit sm_100a CUDA, NVRTC, timed launch, on-device
+check). ``Device.evaluate(nest)`` is the drop-in for the reference's
+``evaluate(kernel, nest, machine)`` (proj/core/include/ispace/simulate.hpp:33):
+same input (a reconstructed schedule), a measured time instead of simulated
+cycles.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+from . import _native as N
+
+
+# ---------------------------------------------------------------- search space
+class Space:
+    """A kernel backbone bound to the GPU decision space (gpu_space.hpp:15-18)."""
+
+    def __init__(self, kind: str, *, m: int = 0, n: int = 0, k: int = 0, a_stride: int = 1,
+                 factors: list[list[int]] | None = None, mode: int = N.SPACE_PARITY):
+        factors = factors or []
+        spec = N.KernelSpec()
+        self._kind = kind.encode()
+        spec.kind = self._kind
+        spec.m, spec.n, spec.k, spec.a_stride = m, n, k, a_stride
+        if len(factors) > 4:
+            raise ValueError("at most 4 strip-mining universes")
+        spec.num_factors = len(factors)
+        for i, u in enumerate(factors):
+            if not 0 < len(u) <= 32:
+                raise ValueError("a universe holds 1..32 sizes")
+            spec.factor_len[i] = len(u)
+            for j, v in enumerate(u):
+                spec.factors[i][j] = v
+        spec.mode = mode
+        self.kind, self.m, self.n, self.k, self.a_stride, self.factors, self.mode = (
+            kind, m, n, k, a_stride, factors, mode)
+        h = C.c_void_p()
+        rc = N.host().ispc_space_create(C.byref(spec), C.byref(h))
+        if rc != 0:
+            raise ValueError(N.host_error())
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.host().ispc_space_free(self._h)
+            self._h = None
+
+    def stats(self) -> dict:
+        s = N.SpaceStats()
+        N.host().ispc_space_stats_get(self._h, C.byref(s))
+        return {f: getattr(s, f) for f, _ in N.SpaceStats._fields_}
+
+    def problem(self) -> N.Problem:
+        p = N.Problem()
+        if N.host().ispc_space_problem(self._h, C.byref(p)) != 0:
+            raise ValueError(N.host_error())
+        return p
+
+    def root(self) -> "Candidate":
+        h = C.c_void_p()
+        N.host().ispc_cand_root(self._h, C.byref(h))
+        return Candidate(self, h)
+
+    def deserialize(self, text: str) -> "Candidate":
+        h = C.c_void_p()
+        if N.host().ispc_cand_deserialize(self._h, text.encode(), C.byref(h)) != 0:
+            raise ValueError(N.host_error())
+        return Candidate(self, h)
+
+
+class DeadEnd(Exception):
+    pass
+
+
+class Candidate:
+    """A (partially) specified implementation (candidate.hpp:54-59)."""
+
+    def __init__(self, space: Space, h):
+        self.space, self._h = space, h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.host().ispc_cand_free(self._h)
+            self._h = None
+
+    def clone(self) -> "Candidate":
+        return Candidate(self.space, C.c_void_p(N.host().ispc_cand_clone(self._h)))
+
+    def decide(self, choice: str, args: list[str], value: str) -> "Candidate":
+        a0 = args[0].encode() if len(args) > 0 else None
+        a1 = args[1].encode() if len(args) > 1 else None
+        rc = N.host().ispc_cand_decide(self.space._h, self._h, choice.encode(), a0, a1, value.encode())
+        if rc == 1:
+            raise DeadEnd(f"{choice}({', '.join(args)}) = {value}")
+        if rc != 0:
+            raise ValueError(N.host_error())
+        return self
+
+    @property
+    def open_count(self) -> int:
+        return N.host().ispc_cand_open_count(self.space._h, self._h)
+
+    @property
+    def fully_specified(self) -> bool:
+        return bool(N.host().ispc_cand_fully_specified(self.space._h, self._h))
+
+    @property
+    def digest(self) -> int:
+        return N.host().ispc_cand_digest(self.space._h, self._h)
+
+    @property
+    def fired(self) -> int:
+        return N.host().ispc_cand_fired(self._h)
+
+    def first_leaf(self, budget: int = 100000) -> "Candidate":
+        h = C.c_void_p()
+        if N.host().ispc_cand_first_leaf(self.space._h, self._h, budget, C.byref(h)) != 0:
+            raise DeadEnd("no leaf within budget")
+        return Candidate(self.space, h)
+
+    def random_leaf(self, seed: int, max_restarts: int = 1000) -> tuple["Candidate", int, int]:
+        h = C.c_void_p()
+        dec, dead = C.c_int64(), C.c_int64()
+        rc = N.host().ispc_cand_random_leaf(self.space._h, self._h, seed, max_restarts, C.byref(h),
+                                            C.byref(dec), C.byref(dead))
+        if rc != 0:
+            raise DeadEnd("random descent gave up")
+        return Candidate(self.space, h), dec.value, dead.value
+
+    def count_leaves(self, cap: int = 10 ** 7) -> int:
+        return N.host().ispc_count_leaves(self.space._h, self._h, cap)
+
+    def nest(self) -> "NestHandle":
+        h = C.c_void_p()
+        if N.host().ispc_cand_to_nest(self.space._h, self._h, C.byref(h)) != 0:
+            raise ValueError(N.host_error())
+        return NestHandle(h)
+
+    def reference_source(self) -> str:
+        return N.read_text(N.host().ispc_cand_reference_source, self.space._h, self._h)
+
+    def simulate(self) -> dict:
+        out = (C.c_int64 * 5)()
+        if N.host().ispc_cand_simulate(self.space._h, self._h, out) != 0:
+            raise ValueError(N.host_error())
+        return dict(zip(("compute", "memory", "sync", "block_serial", "total"), list(out)))
+
+    def serialize(self) -> str:
+        return N.read_text(N.host().ispc_cand_serialize, self.space._h, self._h)
+
+
+class NestHandle:
+    """Flat ispc_nest of a reconstructed schedule (owned by libispc_host)."""
+
+    def __init__(self, h):
+        self._h = h
+        self.nest = N.host().ispc_nest_buf_get(h)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.host().ispc_nest_buf_free(self._h)
+            self._h = None
+
+    def pseudo(self) -> str:
+        return N.read_text(N.ispc().ispc_emit_pseudo, self.nest)
+
+    def cuda(self, fn_name: str | None = None, watchdog: int = 2) -> tuple[str, N.Launch]:
+        opts = N.EmitOpts(watchdog=watchdog)
+        L = N.Launch()
+        n = C.c_size_t()
+        nm = fn_name.encode() if fn_name else None
+        rc = N.ispc().ispc_emit_cuda(self.nest, C.byref(opts), nm, None, 0, C.byref(n), C.byref(L))
+        if rc != 0:
+            raise EmitError(rc, N.last_error())
+        buf = C.create_string_buffer(n.value + 1)
+        rc = N.ispc().ispc_emit_cuda(self.nest, C.byref(opts), nm, buf, n.value + 1, C.byref(n), C.byref(L))
+        if rc != 0:
+            raise EmitError(rc, N.last_error())
+        return buf.value.decode(), L
+
+
+class EmitError(Exception):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{N.STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+# ---------------------------------------------------------------- compilation
+class Module:
+    def __init__(self, h):
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.ispc().ispc_module_free(self._h)
+            self._h = None
+
+    def cubin(self) -> bytes:
+        p, n = C.c_void_p(), C.c_size_t()
+        N.ispc().ispc_module_cubin(self._h, C.byref(p), C.byref(n))
+        return C.string_at(p, n.value)
+
+
+def compile_sources(srcs: list[str], arch: str = "sm_100a") -> Module:
+    arr = (C.c_char_p * len(srcs))(*[s.encode() for s in srcs])
+    h = C.c_void_p()
+    rc = N.ispc().ispc_compile(arr, len(srcs), arch.encode(), C.byref(h))
+    if rc != 0:
+        raise EmitError(rc, N.last_error())
+    return Module(h)
+
+
+# ---------------------------------------------------------------- device
+@dataclass
+class Measurement:
+    status: str
+    median_ns: float
+    min_ns: float
+    first_ns: float
+    max_err: float
+    mismatches: int
+    launch: N.Launch | None = field(default=None, repr=False)
+
+
+class Device:
+    """One B200 (ispc_dev)."""
+
+    def __init__(self, ordinal: int = 0):
+        h = C.c_void_p()
+        rc = N.ispc().ispc_dev_open(ordinal, C.byref(h))
+        if rc != 0:
+            raise RuntimeError(f"ispc_dev_open({ordinal}): {N.last_error()}")
+        self._h = h
+        self.ordinal = ordinal
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.ispc().ispc_dev_close(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def error(self) -> str:
+        return N.last_error(self._h)
+
+    def info(self) -> dict:
+        sm, l2, hbm, clk = C.c_int(), C.c_int64(), C.c_int64(), C.c_int()
+        N.ispc().ispc_dev_info(self._h, C.byref(sm), C.byref(l2), C.byref(hbm), C.byref(clk))
+        return {"sm_count": sm.value, "l2_bytes": l2.value, "hbm_bytes": hbm.value, "sm_clock_khz": clk.value}
+
+    def bind(self, problem: N.Problem):
+        rc = N.ispc().ispc_bind_problem(self._h, C.byref(problem))
+        if rc != 0:
+            raise RuntimeError(self.error())
+
+    def read(self, name: str, count: int, expected: bool = False):
+        import numpy as np
+        out = np.empty(count, dtype=np.float32)
+        fn = N.ispc().ispc_read_expected if expected else N.ispc().ispc_read_region
+        rc = fn(self._h, name.encode(), out.ctypes.data_as(C.c_void_p), out.nbytes)
+        if rc != 0:
+            raise RuntimeError(self.error())
+        return out
+
+    def load(self, module: Module) -> int:
+        h = C.c_int()
+        rc = N.ispc().ispc_module_load(self._h, module._h, C.byref(h))
+        if rc != 0:
+            raise RuntimeError(self.error())
+        return h.value
+
+    def unload(self, handle: int):
+        N.ispc().ispc_module_unload(self._h, handle)
+
+    @staticmethod
+    def _opts(warmup, reps, flush_l2, check, bit_exact, rtol, budget_ns):
+        return N.TimeOpts(warmup=warmup, reps=reps, flush_l2=int(flush_l2), check=int(check),
+                          bit_exact=int(bit_exact), rtol=rtol, budget_ns=budget_ns)
+
+    def launch(self, handle: int, launch: N.Launch, *, warmup=1, reps=3, flush_l2=False, check=True,
+               bit_exact=True, rtol=1e-5, budget_ns=2e9) -> Measurement:
+        r = N.TimeResult()
+        rc = N.ispc().ispc_launch_timed(self._h, handle, C.byref(launch),
+                                        C.byref(self._opts(warmup, reps, flush_l2, check, bit_exact, rtol,
+                                                           budget_ns)), C.byref(r))
+        if rc != 0:
+            return Measurement(N.STATUS.get(rc, str(rc)), float("inf"), float("inf"), float("inf"), 0.0, -1,
+                               launch)
+        return Measurement(N.STATUS.get(r.status, str(r.status)), r.median_ns, r.min_ns, r.first_ns, r.max_err,
+                           r.mismatches, launch)
+
+    def evaluate(self, nest: NestHandle, *, watchdog=2, warmup=1, reps=3, flush_l2=False, check=True,
+                 bit_exact=True, rtol=1e-5, budget_ns=2e9) -> Measurement:
+        r = N.TimeResult()
+        L = N.Launch()
+        eo = N.EmitOpts(watchdog=watchdog)
+        rc = N.ispc().ispc_evaluate(self._h, nest.nest, C.byref(eo),
+                                    C.byref(self._opts(warmup, reps, flush_l2, check, bit_exact, rtol, budget_ns)),
+                                    C.byref(r), C.byref(L))
+        if rc != 0:
+            return Measurement(N.STATUS.get(rc, str(rc)), float("inf"), float("inf"), float("inf"), 0.0, -1, L)
+        return Measurement(N.STATUS.get(r.status, str(r.status)), r.median_ns, r.min_ns, r.first_ns, r.max_err,
+                           r.mismatches, L)

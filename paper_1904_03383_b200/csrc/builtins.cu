@@ -1,0 +1,165 @@
+// Fixed device kernels of the runtime (compiled ahead of time for sm_100a):
+//   * seeded input generation (bit-identical to oracle/numeric.c's generator)
+//   * golden kernels: the expected outputs of each problem, written as plain
+//     sequential-order loops over the backbone semantics (kernels.cpp:373-488)
+//     so every parity-mode schedule must match them bit for bit
+//   * on-device output comparison
+//   * globaltimer probe for the watchdog's host<->device clock offset
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "builtins.hpp"
+
+namespace ispc {
+
+__host__ __device__ inline uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Uniform in [-1, 1) on a 2^-23 grid: exactly representable, so the CPU
+// oracle reproduces every bit.
+__device__ inline float input_value(uint64_t seed, uint32_t tag, uint64_t i) {
+  uint64_t h = splitmix64(splitmix64(seed ^ (uint64_t(tag) << 48)) + i);
+  int32_t m = int32_t(h >> 40);  // 24 bits
+  return float(m - 8388608) * 1.1920928955078125e-07f;
+}
+
+__global__ void fill_kernel(float* p, int64_t n, uint64_t seed, uint32_t tag) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = input_value(seed, tag, i);
+}
+
+__global__ void axpy_golden(const float* x, const float* y, float* z, int64_t n, float alpha) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    z[i] = __fadd_rn(__fmul_rn(alpha, x[i]), y[i]);
+}
+
+__global__ void outer_golden(const float* a, const float* b, float* c, int64_t m, int64_t n) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < m * n; t += int64_t(gridDim.x) * blockDim.x)
+    c[t] = __fmul_rn(a[t / n], b[t % n]);
+}
+
+// C[i + j*m] = sum_k A[i*s + k*m*s] * B[k + j*kk], k ascending from a 0 init.
+// A tile of B columns is staged in shared memory; the per-element operation
+// order is the sequential one regardless of staging.
+__global__ void matmul_golden(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ c,
+                              int64_t m, int64_t n, int64_t kk, int64_t s, int64_t batch_stride_a,
+                              int64_t batch_stride_b, int64_t batch_stride_c) {
+  const int64_t bz = blockIdx.z;
+  a += bz * batch_stride_a;
+  b += bz * batch_stride_b;
+  c += bz * batch_stride_c;
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  int64_t j = blockIdx.y;
+  if (j >= n) return;
+  __shared__ float bs[1024];
+  float acc = 0.0f;
+  for (int64_t k0 = 0; k0 < kk; k0 += 1024) {
+    int64_t kn = kk - k0 < 1024 ? kk - k0 : 1024;
+    __syncthreads();
+    for (int64_t t = threadIdx.x; t < kn; t += blockDim.x) bs[t] = b[k0 + t + j * kk];
+    __syncthreads();
+    if (i < m)
+      for (int64_t k = 0; k < kn; ++k) acc = __fmaf_rn(a[i * s + (k0 + k) * m * s], bs[k], acc);
+  }
+  if (i < m) c[i + j * m] = acc;
+}
+
+// y[i] = sum_j A[i + j*m] * x[j], j ascending (gemv backbone order).
+__global__ void gemv_golden(const float* __restrict__ a, const float* __restrict__ x, float* __restrict__ y,
+                            int64_t m, int64_t n) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= m) return;
+  float acc = 0.0f;
+  for (int64_t j = 0; j < n; ++j) acc = __fmaf_rn(a[i + j * m], x[j], acc);
+  y[i] = acc;
+}
+
+struct CmpOut {
+  unsigned long long mismatches;
+  unsigned int max_err_bits;  // float bits of the max relative error (>= 0)
+  unsigned int pad;
+};
+
+__global__ void compare_kernel(const float* out, const float* exp, int64_t n, int bit_exact, float rtol,
+                               CmpOut* res) {
+  unsigned long long bad = 0;
+  float worst = 0.0f;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    float o = out[i], e = exp[i];
+    float den = fabsf(e) > 1e-30f ? fabsf(e) : 1e-30f;
+    float err = fabsf(o - e) / den;
+    if (o != o) err = __int_as_float(0x7f800000);  // NaN output (unwritten) -> inf
+    bool diff = bit_exact ? (__float_as_uint(o) != __float_as_uint(e)) : !(err <= rtol);
+    bad += diff;
+    worst = fmaxf(worst, err);
+  }
+  for (int off = 16; off; off >>= 1) {
+    bad += __shfl_xor_sync(0xffffffffu, bad, off);
+    worst = fmaxf(worst, __shfl_xor_sync(0xffffffffu, worst, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (bad) atomicAdd(&res->mismatches, bad);
+    atomicMax(&res->max_err_bits, __float_as_uint(worst));
+  }
+}
+
+__global__ void timer_kernel(unsigned long long* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
+}
+
+namespace {
+int grid_for(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  return int(g < 1 ? 1 : g);
+}
+}  // namespace
+
+cudaError_t launch_fill(float* p, int64_t n, uint64_t seed, uint32_t tag, cudaStream_t s) {
+  fill_kernel<<<grid_for(n), 256, 0, s>>>(p, n, seed, tag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_axpy_golden(const float* x, const float* y, float* z, int64_t n, float alpha,
+                               cudaStream_t s) {
+  axpy_golden<<<grid_for(n), 256, 0, s>>>(x, y, z, n, alpha);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_outer_golden(const float* a, const float* b, float* c, int64_t m, int64_t n,
+                                cudaStream_t s) {
+  outer_golden<<<grid_for(m * n), 256, 0, s>>>(a, b, c, m, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_matmul_golden(const float* a, const float* b, float* c, int64_t m, int64_t n, int64_t k,
+                                 int64_t a_stride, int64_t batch, cudaStream_t s) {
+  dim3 grid(unsigned((m + 127) / 128), unsigned(n), unsigned(batch));
+  matmul_golden<<<grid, 128, 0, s>>>(a, b, c, m, n, k, a_stride, m * k * a_stride, k * n, m * n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemv_golden(const float* a, const float* x, float* y, int64_t m, int64_t n,
+                               cudaStream_t s) {
+  gemv_golden<<<unsigned((m + 127) / 128), 128, 0, s>>>(a, x, y, m, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compare(const float* out, const float* exp, int64_t n, int bit_exact, float rtol,
+                           void* dev_res, cudaStream_t s) {
+  compare_kernel<<<grid_for(n), 256, 0, s>>>(out, exp, n, bit_exact, rtol, static_cast<CmpOut*>(dev_res));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_timer(unsigned long long* out, cudaStream_t s) {
+  timer_kernel<<<1, 1, 0, s>>>(out);
+  return cudaGetLastError();
+}
+
+}  // namespace ispc

@@ -1,0 +1,621 @@
+// Runtime half of libispc: NVRTC compilation to sm_100a cubins, module
+// management, problem binding (seeded inputs, golden expected outputs, GLOBAL
+// temporary scratch), CUDA-event-timed launches with a device watchdog, and
+// on-device output checks. Replaces the reference's analytic evaluate()
+// (proj/core/src/simulate.cpp:118-133) with a measurement on a B200.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "builtins.hpp"
+#include "ispc.h"
+#include "nest_view.hpp"
+
+namespace ispc {
+std::string emit_cuda_kernel(const NestView& v, const ispc_emit_opts& opts, const std::string& fn,
+                             ispc_launch& L);
+}
+
+struct ispc_module {
+  std::vector<char> cubin;
+  std::string log;
+};
+
+namespace {
+
+struct Buffer {
+  float* ptr = nullptr;
+  int64_t elems = 0;
+};
+
+struct Loaded {
+  CUmodule mod = nullptr;
+  std::unordered_map<std::string, CUfunction> fns;
+  CUdeviceptr timeout_flag = 0;
+};
+
+
+// Driver API entry points, resolved through the runtime at first device open
+// so the library loads (and its symbols can be inspected) on hosts without a
+// CUDA driver.
+struct DriverTable {
+  decltype(&::cuCtxGetCurrent) CtxGetCurrent = nullptr;
+  decltype(&::cuDeviceGet) DeviceGet = nullptr;
+  decltype(&::cuFuncSetAttribute) FuncSetAttribute = nullptr;
+  decltype(&::cuGetErrorName) GetErrorName = nullptr;
+  decltype(&::cuInit) Init = nullptr;
+  decltype(&::cuLaunchKernel) LaunchKernel = nullptr;
+  decltype(&::cuMemcpyDtoH) MemcpyDtoH = nullptr;
+  decltype(&::cuModuleGetFunction) ModuleGetFunction = nullptr;
+  decltype(&::cuModuleGetGlobal) ModuleGetGlobal = nullptr;
+  decltype(&::cuModuleLoadData) ModuleLoadData = nullptr;
+  decltype(&::cuModuleUnload) ModuleUnload = nullptr;
+  decltype(&::cuMemsetD32Async) MemsetD32Async = nullptr;
+};
+DriverTable drv;
+
+bool resolve_driver(std::string& why) {
+  static std::once_flag once;
+  static bool ok = false;
+  static std::string err;
+  std::call_once(once, [] {
+    ok = true;
+    auto get = [](const char* sym, void** fp) {
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(sym, fp, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess) {
+        ok = false;
+        err += std::string(sym) + " ";
+      }
+    };
+    get("cuCtxGetCurrent", reinterpret_cast<void**>(&drv.CtxGetCurrent));
+    get("cuDeviceGet", reinterpret_cast<void**>(&drv.DeviceGet));
+    get("cuFuncSetAttribute", reinterpret_cast<void**>(&drv.FuncSetAttribute));
+    get("cuGetErrorName", reinterpret_cast<void**>(&drv.GetErrorName));
+    get("cuInit", reinterpret_cast<void**>(&drv.Init));
+    get("cuLaunchKernel", reinterpret_cast<void**>(&drv.LaunchKernel));
+    get("cuMemcpyDtoH", reinterpret_cast<void**>(&drv.MemcpyDtoH));
+    get("cuModuleGetFunction", reinterpret_cast<void**>(&drv.ModuleGetFunction));
+    get("cuModuleGetGlobal", reinterpret_cast<void**>(&drv.ModuleGetGlobal));
+    get("cuModuleLoadData", reinterpret_cast<void**>(&drv.ModuleLoadData));
+    get("cuModuleUnload", reinterpret_cast<void**>(&drv.ModuleUnload));
+    get("cuMemsetD32Async", reinterpret_cast<void**>(&drv.MemsetD32Async));
+  });
+  if (!ok) why = "CUDA driver entry points unavailable: " + err;
+  return ok;
+}
+
+double host_ns() {
+  return double(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                    std::chrono::steady_clock::now().time_since_epoch())
+                    .count());
+}
+
+}  // namespace
+
+struct ispc_dev {
+  int ordinal = 0;
+  CUdevice cu_dev = 0;
+  CUcontext ctx = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::string err;
+  int sm_count = 0, sm_clock_khz = 0;
+  int64_t l2_bytes = 0, hbm_bytes = 0;
+  double gt_offset_ns = 0;  // device globaltimer - host steady clock
+  void* flush = nullptr;
+  size_t flush_bytes = 0;
+  void* cmp_res = nullptr;
+  unsigned long long* timer_buf = nullptr;
+
+  ispc_problem prob{};
+  bool bound = false;
+  std::map<std::string, Buffer> regions;  // inputs and outputs by name
+  std::map<std::string, Buffer> expected;  // golden outputs by name
+  std::vector<std::string> outputs;
+  std::vector<Buffer> scratch;
+
+  std::map<int, Loaded> modules;
+  int next_handle = 1;
+};
+
+namespace {
+unsigned flush_counter_ = 0;
+}
+
+namespace {
+
+int fail(ispc_dev* d, int code, const std::string& msg) {
+  if (d) d->err = msg;
+  ispc::set_thread_error(msg);
+  return code;
+}
+
+bool sticky(cudaError_t e) {
+  return e == cudaErrorIllegalAddress || e == cudaErrorLaunchFailure || e == cudaErrorIllegalInstruction ||
+         e == cudaErrorMisalignedAddress || e == cudaErrorInvalidAddressSpace || e == cudaErrorInvalidPc ||
+         e == cudaErrorHardwareStackError || e == cudaErrorAssert || e == cudaErrorLaunchTimeout;
+}
+
+int cuda_fail(ispc_dev* d, cudaError_t e, const char* what) {
+  return fail(d, sticky(e) ? ISPC_E_STICKY : ISPC_E_CUDA,
+              std::string(what) + ": " + cudaGetErrorName(e) + " " + cudaGetErrorString(e));
+}
+
+int cu_fail(ispc_dev* d, CUresult r, const char* what) {
+  const char* name = nullptr;
+  if (drv.GetErrorName) drv.GetErrorName(r, &name);
+  bool st = r == CUDA_ERROR_ILLEGAL_ADDRESS || r == CUDA_ERROR_LAUNCH_FAILED ||
+            r == CUDA_ERROR_ILLEGAL_INSTRUCTION || r == CUDA_ERROR_MISALIGNED_ADDRESS ||
+            r == CUDA_ERROR_HARDWARE_STACK_ERROR || r == CUDA_ERROR_ASSERT;
+  int code = st ? ISPC_E_STICKY
+                : (r == CUDA_ERROR_LAUNCH_OUT_OF_RESOURCES || r == CUDA_ERROR_INVALID_VALUE) ? ISPC_E_LAUNCH
+                                                                                                : ISPC_E_CUDA;
+  return fail(d, code, std::string(what) + ": " + (name ? name : "CUDA error"));
+}
+
+#define CK(d, expr)                                   \
+  do {                                                \
+    cudaError_t e_ = (expr);                          \
+    if (e_ != cudaSuccess) return cuda_fail(d, e_, #expr); \
+  } while (0)
+#define CU(d, expr)                                   \
+  do {                                                \
+    CUresult r_ = (expr);                             \
+    if (r_ != CUDA_SUCCESS) return cu_fail(d, r_, #expr); \
+  } while (0)
+
+int bind_ctx(ispc_dev* d) {
+  CK(d, cudaSetDevice(d->ordinal));
+  return ISPC_OK;
+}
+
+uint32_t tag_of(const std::string& name) { return uint32_t(static_cast<unsigned char>(name[0])); }
+
+int alloc(ispc_dev* d, Buffer& b, int64_t elems) {
+  b.elems = elems;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&b.ptr), size_t(std::max<int64_t>(elems, 1)) * 4);
+  if (e != cudaSuccess) {
+    b.ptr = nullptr;
+    cudaGetLastError();
+    return fail(d, ISPC_E_NOMEM, "cudaMalloc of " + std::to_string(elems * 4) + " bytes failed");
+  }
+  return ISPC_OK;
+}
+
+void free_problem(ispc_dev* d) {
+  for (auto& [k, b] : d->regions) cudaFree(b.ptr);
+  for (auto& [k, b] : d->expected) cudaFree(b.ptr);
+  for (auto& b : d->scratch) cudaFree(b.ptr);
+  d->regions.clear();
+  d->expected.clear();
+  d->scratch.clear();
+  d->outputs.clear();
+  d->bound = false;
+}
+
+int calibrate_timer(ispc_dev* d) {
+  double best_gap = 1e30;
+  for (int i = 0; i < 5; ++i) {
+    double t0 = host_ns();
+    CK(d, ispc::launch_timer(d->timer_buf, d->stream));
+    CK(d, cudaStreamSynchronize(d->stream));
+    double t1 = host_ns();
+    unsigned long long gt = 0;
+    CK(d, cudaMemcpy(&gt, d->timer_buf, 8, cudaMemcpyDeviceToHost));
+    if (t1 - t0 < best_gap) {
+      best_gap = t1 - t0;
+      d->gt_offset_ns = double(gt) - 0.5 * (t0 + t1);
+    }
+  }
+  return ISPC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ispc_last_error(const ispc_dev* d) { return d ? d->err.c_str() : ispc::thread_error(); }
+
+int ispc_dev_open(int ordinal, ispc_dev** out) {
+  if (!out) return fail(nullptr, ISPC_E_ARG, "null out");
+  auto d = std::make_unique<ispc_dev>();
+  d->ordinal = ordinal;
+  CK(d.get(), cudaSetDevice(ordinal));
+  CK(d.get(), cudaFree(nullptr));  // create the primary context
+  std::string why;
+  if (!resolve_driver(why)) return fail(d.get(), ISPC_E_CUDA, why);
+  CU(d.get(), drv.Init(0));
+  CU(d.get(), drv.DeviceGet(&d->cu_dev, ordinal));
+  CU(d.get(), drv.CtxGetCurrent(&d->ctx));
+  CK(d.get(), cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+  CK(d.get(), cudaEventCreate(&d->ev0));
+  CK(d.get(), cudaEventCreate(&d->ev1));
+  cudaDeviceProp p{};
+  CK(d.get(), cudaGetDeviceProperties(&p, ordinal));
+  d->sm_count = p.multiProcessorCount;
+  d->l2_bytes = p.l2CacheSize;
+  d->hbm_bytes = int64_t(p.totalGlobalMem);
+  int clk = 0;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, ordinal);
+  d->sm_clock_khz = clk;
+  d->flush_bytes = size_t(std::max<int64_t>(d->l2_bytes, 64 << 20)) * 2;
+  CK(d.get(), cudaMalloc(&d->flush, d->flush_bytes));
+  CK(d.get(), cudaMalloc(&d->cmp_res, sizeof(ispc::CmpResult)));
+  CK(d.get(), cudaMalloc(reinterpret_cast<void**>(&d->timer_buf), 8));
+  int rc = calibrate_timer(d.get());
+  if (rc) return rc;
+  *out = d.release();
+  return ISPC_OK;
+}
+
+void ispc_dev_close(ispc_dev* d) {
+  if (!d) return;
+  cudaSetDevice(d->ordinal);
+  cudaStreamSynchronize(d->stream);
+  for (auto& [h, m] : d->modules) drv.ModuleUnload(m.mod);
+  free_problem(d);
+  cudaFree(d->flush);
+  cudaFree(d->cmp_res);
+  cudaFree(d->timer_buf);
+  cudaEventDestroy(d->ev0);
+  cudaEventDestroy(d->ev1);
+  cudaStreamDestroy(d->stream);
+  delete d;
+}
+
+int ispc_dev_info(const ispc_dev* d, int* sm_count, int64_t* l2_bytes, int64_t* hbm_bytes, int* sm_clock_khz) {
+  if (!d) return ISPC_E_ARG;
+  if (sm_count) *sm_count = d->sm_count;
+  if (l2_bytes) *l2_bytes = d->l2_bytes;
+  if (hbm_bytes) *hbm_bytes = d->hbm_bytes;
+  if (sm_clock_khz) *sm_clock_khz = d->sm_clock_khz;
+  return ISPC_OK;
+}
+
+int ispc_bind_problem(ispc_dev* d, const ispc_problem* p) {
+  if (!d || !p) return fail(d, ISPC_E_ARG, "null argument");
+  int rc = bind_ctx(d);
+  if (rc) return rc;
+  CK(d, cudaStreamSynchronize(d->stream));
+  free_problem(d);
+  d->prob = *p;
+  struct R {
+    const char* name;
+    int64_t elems;
+    bool input;
+  };
+  std::vector<R> rs;
+  const int64_t m = p->m, n = p->n, k = p->k, s = std::max<int64_t>(p->a_stride, 1);
+  const int64_t batch = std::max<int64_t>(p->batch, 1);
+  switch (p->kind) {
+    case ISPC_PROB_AXPY: rs = {{"x", n, true}, {"y", n, true}, {"z", n, false}}; break;
+    case ISPC_PROB_OUTER: rs = {{"a", m, true}, {"b", n, true}, {"c", m * n, false}}; break;
+    case ISPC_PROB_MATMUL: rs = {{"a", m * k * s, true}, {"b", k * n, true}, {"c", m * n, false}}; break;
+    case ISPC_PROB_GEMV: rs = {{"a", m * n, true}, {"x", n, true}, {"y", m, false}}; break;
+    case ISPC_PROB_BATCHED:
+      rs = {{"a", batch * m * k, true}, {"b", batch * k * n, true}, {"c", batch * m * n, false}};
+      break;
+    default: return fail(d, ISPC_E_ARG, "unknown problem kind");
+  }
+  for (const R& r : rs) {
+    if (r.elems <= 0) return fail(d, ISPC_E_ARG, std::string("empty region ") + r.name);
+    Buffer b;
+    if ((rc = alloc(d, b, r.elems))) return rc;
+    d->regions[r.name] = b;
+    if (r.input) {
+      CK(d, ispc::launch_fill(b.ptr, b.elems, p->seed, tag_of(r.name), d->stream));
+    } else {
+      Buffer e;
+      if ((rc = alloc(d, e, r.elems))) return rc;
+      d->expected[r.name] = e;
+      d->outputs.push_back(r.name);
+    }
+  }
+  auto R_ = [&](const char* nm) { return d->regions.at(nm).ptr; };
+  auto E_ = [&](const char* nm) { return d->expected.at(nm).ptr; };
+  switch (p->kind) {
+    case ISPC_PROB_AXPY: CK(d, ispc::launch_axpy_golden(R_("x"), R_("y"), E_("z"), n, p->alpha, d->stream)); break;
+    case ISPC_PROB_OUTER: CK(d, ispc::launch_outer_golden(R_("a"), R_("b"), E_("c"), m, n, d->stream)); break;
+    case ISPC_PROB_MATMUL:
+      CK(d, ispc::launch_matmul_golden(R_("a"), R_("b"), E_("c"), m, n, k, s, 1, d->stream));
+      break;
+    case ISPC_PROB_GEMV: CK(d, ispc::launch_gemv_golden(R_("a"), R_("x"), E_("y"), m, n, d->stream)); break;
+    case ISPC_PROB_BATCHED:
+      CK(d, ispc::launch_matmul_golden(R_("a"), R_("b"), E_("c"), m, n, k, 1, batch, d->stream));
+      break;
+  }
+  CK(d, cudaStreamSynchronize(d->stream));
+  d->bound = true;
+  return ISPC_OK;
+}
+
+int ispc_problem_region(ispc_dev* d, const char* name, uint64_t* dev_ptr, int64_t* elems) {
+  if (!d || !name) return ISPC_E_ARG;
+  auto it = d->regions.find(name);
+  if (it == d->regions.end()) return fail(d, ISPC_E_ARG, std::string("no region ") + name);
+  if (dev_ptr) *dev_ptr = reinterpret_cast<uint64_t>(it->second.ptr);
+  if (elems) *elems = it->second.elems;
+  return ISPC_OK;
+}
+
+int ispc_read_region(ispc_dev* d, const char* name, void* host, size_t bytes) {
+  if (!d || !name || !host) return ISPC_E_ARG;
+  int rc = bind_ctx(d);
+  if (rc) return rc;
+  auto it = d->regions.find(name);
+  if (it == d->regions.end()) return fail(d, ISPC_E_ARG, std::string("no region ") + name);
+  size_t n = std::min(bytes, size_t(it->second.elems) * 4);
+  CK(d, cudaStreamSynchronize(d->stream));
+  CK(d, cudaMemcpy(host, it->second.ptr, n, cudaMemcpyDeviceToHost));
+  return ISPC_OK;
+}
+
+int ispc_read_expected(ispc_dev* d, const char* name, void* host, size_t bytes) {
+  if (!d || !name || !host) return ISPC_E_ARG;
+  int rc = bind_ctx(d);
+  if (rc) return rc;
+  auto it = d->expected.find(name);
+  if (it == d->expected.end()) return fail(d, ISPC_E_ARG, std::string("no expected output ") + name);
+  size_t n = std::min(bytes, size_t(it->second.elems) * 4);
+  CK(d, cudaStreamSynchronize(d->stream));
+  CK(d, cudaMemcpy(host, it->second.ptr, n, cudaMemcpyDeviceToHost));
+  return ISPC_OK;
+}
+
+// ---- compilation --------------------------------------------------------------
+
+int ispc_compile(const char* const* srcs, int n, const char* arch, ispc_module** out) {
+  if (!srcs || n <= 0 || !out) return fail(nullptr, ISPC_E_ARG, "bad compile arguments");
+  std::string text = ispc_cuda_prelude();
+  for (int i = 0; i < n; ++i) {
+    if (!srcs[i]) return fail(nullptr, ISPC_E_ARG, "null source");
+    text += srcs[i];
+    text += "\n";
+  }
+  auto m = std::make_unique<ispc_module>();
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, text.c_str(), "ispc_candidates.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+    return fail(nullptr, ISPC_E_NVRTC, "nvrtcCreateProgram failed");
+  std::string arch_opt = std::string("--gpu-architecture=") + (arch ? arch : "sm_100a");
+  const char* opts[] = {arch_opt.c_str(), "--device-as-default-execution-space", "--std=c++17"};
+  nvrtcResult r = nvrtcCompileProgram(prog, 3, opts);
+  size_t log_size = 0;
+  nvrtcGetProgramLogSize(prog, &log_size);
+  m->log.resize(log_size);
+  if (log_size) nvrtcGetProgramLog(prog, m->log.data());
+  if (!m->log.empty() && m->log.back() == 0) m->log.pop_back();
+  if (r != NVRTC_SUCCESS) {
+    std::string msg = std::string("NVRTC: ") + nvrtcGetErrorString(r) + "\n" + m->log;
+    nvrtcDestroyProgram(&prog);
+    return fail(nullptr, ISPC_E_NVRTC, msg);
+  }
+  size_t cubin_size = 0;
+  if (nvrtcGetCUBINSize(prog, &cubin_size) != NVRTC_SUCCESS || cubin_size == 0) {
+    nvrtcDestroyProgram(&prog);
+    return fail(nullptr, ISPC_E_NVRTC, "NVRTC produced no cubin (is the arch a real sm_?)");
+  }
+  m->cubin.resize(cubin_size);
+  nvrtcGetCUBIN(prog, m->cubin.data());
+  nvrtcDestroyProgram(&prog);
+  *out = m.release();
+  return ISPC_OK;
+}
+
+int ispc_module_cubin(const ispc_module* m, const void** data, size_t* size) {
+  if (!m) return ISPC_E_ARG;
+  if (data) *data = m->cubin.data();
+  if (size) *size = m->cubin.size();
+  return ISPC_OK;
+}
+
+const char* ispc_module_log(const ispc_module* m) { return m ? m->log.c_str() : ""; }
+void ispc_module_free(ispc_module* m) { delete m; }
+
+int ispc_module_load(ispc_dev* d, const ispc_module* m, int* handle) {
+  if (!d || !m || !handle) return fail(d, ISPC_E_ARG, "null argument");
+  int rc = bind_ctx(d);
+  if (rc) return rc;
+  Loaded L;
+  CU(d, drv.ModuleLoadData(&L.mod, m->cubin.data()));
+  size_t sz = 0;
+  if (drv.ModuleGetGlobal(&L.timeout_flag, &sz, L.mod, "ispc_timeout_flag") != CUDA_SUCCESS) L.timeout_flag = 0;
+  *handle = d->next_handle++;
+  d->modules[*handle] = std::move(L);
+  return ISPC_OK;
+}
+
+int ispc_module_unload(ispc_dev* d, int handle) {
+  if (!d) return ISPC_E_ARG;
+  auto it = d->modules.find(handle);
+  if (it == d->modules.end()) return fail(d, ISPC_E_ARG, "unknown module handle");
+  bind_ctx(d);
+  drv.ModuleUnload(it->second.mod);
+  d->modules.erase(it);
+  return ISPC_OK;
+}
+
+// ---- check ----------------------------------------------------------------------
+
+int ispc_check(ispc_dev* d, double rtol, int bit_exact, double* max_err, int64_t* mismatches, int* ok) {
+  if (!d || !d->bound) return fail(d, ISPC_E_ARG, "no problem bound");
+  int rc = bind_ctx(d);
+  if (rc) return rc;
+  double worst = 0;
+  int64_t bad = 0;
+  for (const std::string& o : d->outputs) {
+    CK(d, cudaMemsetAsync(d->cmp_res, 0, sizeof(ispc::CmpResult), d->stream));
+    const Buffer& out = d->regions.at(o);
+    const Buffer& exp = d->expected.at(o);
+    CK(d, ispc::launch_compare(out.ptr, exp.ptr, out.elems, bit_exact, float(rtol), d->cmp_res, d->stream));
+    ispc::CmpResult h{};
+    CK(d, cudaMemcpyAsync(&h, d->cmp_res, sizeof(h), cudaMemcpyDeviceToHost, d->stream));
+    CK(d, cudaStreamSynchronize(d->stream));
+    float e;
+    std::memcpy(&e, &h.max_err_bits, 4);
+    worst = std::max(worst, double(e));
+    bad += int64_t(h.mismatches);
+  }
+  if (max_err) *max_err = worst;
+  if (mismatches) *mismatches = bad;
+  if (ok) *ok = bad == 0;
+  return ISPC_OK;
+}
+
+// ---- timed launch -------------------------------------------------------------------
+
+int ispc_launch_timed(ispc_dev* d, int handle, const ispc_launch* L, const ispc_time_opts* o,
+                      ispc_time_result* res) {
+  if (!d || !L || !o || !res) return fail(d, ISPC_E_ARG, "null argument");
+  if (!d->bound) return fail(d, ISPC_E_ARG, "no problem bound");
+  std::memset(res, 0, sizeof(*res));
+  int rc = bind_ctx(d);
+  if (rc) return rc;
+  auto mit = d->modules.find(handle);
+  if (mit == d->modules.end()) return fail(d, ISPC_E_ARG, "unknown module handle");
+  Loaded& mod = mit->second;
+  CUfunction fn;
+  auto fit = mod.fns.find(L->name);
+  if (fit == mod.fns.end()) {
+    CU(d, drv.ModuleGetFunction(&fn, mod.mod, L->name));
+    if (L->static_smem > 48 * 1024)
+      CU(d, drv.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, int(L->static_smem)));
+    mod.fns[L->name] = fn;
+  } else {
+    fn = fit->second;
+  }
+  if (L->grid_x == 0 || L->grid_x > 0x7fffffffull) return fail(d, ISPC_E_ILLEGAL, "grid out of range");
+
+  // bind parameters: problem regions by name, temporaries from scratch
+  std::vector<uint64_t> store(L->num_params, 0);
+  std::vector<void*> args(L->num_params);
+  size_t next_scratch = 0;
+  int deadline_slot = -1;
+  for (uint32_t i = 0; i < L->num_params; ++i) {
+    const ispc_param& prm = L->params[i];
+    args[i] = &store[i];
+    if (prm.kind == ISPC_PARAM_REGION) {
+      if (prm.is_input) {
+        auto it = d->regions.find(prm.name);
+        if (it == d->regions.end())
+          return fail(d, ISPC_E_ARG, std::string("kernel region '") + prm.name + "' not in the bound problem");
+        if (it->second.elems < prm.elems)
+          return fail(d, ISPC_E_ARG, std::string("region '") + prm.name + "' smaller than the kernel's");
+        store[i] = reinterpret_cast<uint64_t>(it->second.ptr);
+      } else {
+        if (next_scratch == d->scratch.size()) d->scratch.push_back(Buffer{});
+        Buffer& b = d->scratch[next_scratch++];
+        if (b.elems < prm.elems) {
+          cudaFree(b.ptr);
+          b = Buffer{};
+          if ((rc = alloc(d, b, prm.elems))) return rc;
+        }
+        store[i] = reinterpret_cast<uint64_t>(b.ptr);
+      }
+    } else if (prm.kind == ISPC_PARAM_INPUT) {
+      if (std::strcmp(prm.name, "alpha") != 0)
+        return fail(d, ISPC_E_ARG, std::string("unknown scalar input ") + prm.name);
+      float a = d->prob.alpha;
+      std::memcpy(&store[i], &a, 4);
+    } else {
+      deadline_slot = int(i);
+    }
+  }
+  const double budget = o->budget_ns > 0 ? o->budget_ns : 2e9;
+  unsigned int smem = L->static_smem;
+  auto launch_once = [&](float* ms, bool flush) -> int {
+    if (flush) CK(d, cudaMemsetAsync(d->flush, int(flush_counter_++ & 0xff), d->flush_bytes, d->stream));
+    if (deadline_slot >= 0) store[deadline_slot] = uint64_t(host_ns() + d->gt_offset_ns + budget);
+    CK(d, cudaEventRecord(d->ev0, d->stream));
+    CU(d, drv.LaunchKernel(fn, unsigned(L->grid_x), 1, 1, L->block[0], L->block[1], L->block[2], smem,
+                         reinterpret_cast<CUstream>(d->stream), args.data(), nullptr));
+    CK(d, cudaEventRecord(d->ev1, d->stream));
+    CK(d, cudaEventSynchronize(d->ev1));
+    CK(d, cudaEventElapsedTime(ms, d->ev0, d->ev1));
+    return ISPC_OK;
+  };
+  auto timed_out = [&](bool* out) -> int {
+    *out = false;
+    if (!mod.timeout_flag) return ISPC_OK;
+    int flag = 0;
+    CU(d, drv.MemcpyDtoH(&flag, mod.timeout_flag, 4));
+    *out = flag != 0;
+    return ISPC_OK;
+  };
+
+  // first launch: NaN-prefilled outputs, watchdog armed, checked
+  for (const std::string& out : d->outputs) {
+    const Buffer& b = d->regions.at(out);
+    CK(d, cudaMemsetAsync(b.ptr, 0xff, size_t(b.elems) * 4, d->stream));
+  }
+  if (mod.timeout_flag) CU(d, drv.MemsetD32Async(mod.timeout_flag, 0, 1, reinterpret_cast<CUstream>(d->stream)));
+  float ms = 0;
+  if ((rc = launch_once(&ms, o->flush_l2 != 0))) return rc;
+  res->first_ns = double(ms) * 1e6;
+  bool late = false;
+  if ((rc = timed_out(&late))) return rc;
+  if (late) {
+    res->status = ISPC_E_TIMEOUT;
+    res->median_ns = res->min_ns = std::max(res->first_ns, budget);
+    return ISPC_OK;
+  }
+  if (o->check) {
+    int ok = 0;
+    if ((rc = ispc_check(d, o->rtol, int(o->bit_exact), &res->max_err, &res->mismatches, &ok))) return rc;
+    if (!ok) {
+      res->status = ISPC_E_MISMATCH;
+      res->median_ns = res->min_ns = res->first_ns;
+      return ISPC_OK;
+    }
+  }
+  for (uint32_t w = 0; w < o->warmup; ++w)
+    if ((rc = launch_once(&ms, o->flush_l2 != 0))) return rc;
+  std::vector<double> times;
+  for (uint32_t r = 0; r < std::max<uint32_t>(o->reps, 1); ++r) {
+    if ((rc = launch_once(&ms, o->flush_l2 != 0))) return rc;
+    times.push_back(double(ms) * 1e6);
+  }
+  if ((rc = timed_out(&late))) return rc;
+  std::sort(times.begin(), times.end());
+  res->median_ns = times[times.size() / 2];
+  res->min_ns = times.front();
+  res->status = late ? ISPC_E_TIMEOUT : ISPC_OK;
+  return ISPC_OK;
+}
+
+// ---- one-shot evaluate -----------------------------------------------------------------
+
+int ispc_evaluate(ispc_dev* d, const ispc_nest* nest, const ispc_emit_opts* eopts, const ispc_time_opts* topts,
+                  ispc_time_result* res, ispc_launch* launch) {
+  if (!d || !nest || !topts || !res) return fail(d, ISPC_E_ARG, "null argument");
+  ispc_launch L{};
+  size_t len = 0;
+  int rc = ispc_emit_cuda(nest, eopts, nullptr, nullptr, 0, &len, &L);
+  if (rc) return fail(d, rc, ispc::thread_error());
+  std::string src(len + 1, '\0');
+  if ((rc = ispc_emit_cuda(nest, eopts, nullptr, src.data(), src.size(), &len, &L)))
+    return fail(d, rc, ispc::thread_error());
+  src.resize(len);
+  if (launch) *launch = L;
+  const char* srcs[] = {src.c_str()};
+  ispc_module* m = nullptr;
+  if ((rc = ispc_compile(srcs, 1, nullptr, &m))) return fail(d, rc, ispc::thread_error());
+  std::unique_ptr<ispc_module, void (*)(ispc_module*)> guard(m, ispc_module_free);
+  int h = 0;
+  if ((rc = ispc_module_load(d, m, &h))) return rc;
+  rc = ispc_launch_timed(d, h, &L, topts, res);
+  ispc_module_unload(d, h);
+  return rc;
+}
+
+}  // extern "C"
