@@ -306,8 +306,20 @@ int ispc_check(ispc_dev* d, double rtol, int bit_exact, double* max_err, int64_t
 
 /* Copies a region of the bound problem to host memory. */
 int ispc_read_region(ispc_dev* d, const char* name, void* host, size_t bytes);
+/* Overwrites an input region of the bound problem from host memory (pinned
+ * memory copies at full PCIe/C2C speed) and recomputes the expected outputs. */
+int ispc_write_region(ispc_dev* d, const char* name, const void* host, size_t bytes);
 /* Reads the expected output computed by the golden kernels. */
 int ispc_read_expected(ispc_dev* d, const char* name, void* host, size_t bytes);
+
+/* Device-timeline marks on the device's stream (CUDA events, 8 slots):
+ * elapsed milliseconds between two recorded marks. */
+int ispc_dev_mark(ispc_dev* d, int slot);
+int ispc_dev_mark_elapsed(ispc_dev* d, int slot_a, int slot_b, double* ms);
+
+/* Pins (page-locks, portable across devices) host memory the search shares
+ * between GPU workers, e.g. the incumbent bound (cudaHostRegister). */
+int ispc_host_register(void* p, size_t bytes);
 
 /* One-shot replacement of evaluate(): emit + compile + load + timed launch +
  * check. The mirror of CostReport is ispc_time_result (time in ns). */

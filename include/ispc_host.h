@@ -89,6 +89,11 @@ int ispc_cand_first_leaf(const ispc_space* s, const ispc_cand* from, int budget,
  * value. Reports decisions applied and dead ends met. 0 ok, 1 gave up. */
 int ispc_cand_random_leaf(const ispc_space* s, const ispc_cand* from, uint64_t seed, int max_restarts,
                           ispc_cand** out, int64_t* decisions, int64_t* dead_ends);
+/* Same, deciding the open instance that comes first in `order` (comma
+ * separated choice names, e.g. the paper's "size,dim_kind,thread_level,
+ * mem_space,order,cache"). */
+int ispc_cand_random_leaf_ordered(const ispc_space* s, const ispc_cand* from, uint64_t seed, const char* order,
+                                  int max_restarts, ispc_cand** out, int64_t* decisions, int64_t* dead_ends);
 /* Exhaustive first-open enumeration; returns the number of leaves (capped). */
 int64_t ispc_count_leaves(const ispc_space* s, const ispc_cand* from, int64_t cap);
 
@@ -103,6 +108,67 @@ int ispc_cand_reference_source(const ispc_space* s, const ispc_cand* c, char* bu
 int ispc_cand_simulate(const ispc_space* s, const ispc_cand* c, int64_t out[5]);
 int ispc_cand_serialize(const ispc_space* s, const ispc_cand* c, char* buf, size_t cap, size_t* len);
 int ispc_cand_deserialize(const ispc_space* s, const char* text, ispc_cand** out);
+
+/* ---- B200 lower bound (seconds) ------------------------------------------- */
+typedef struct {
+  double total, dram, sm_mem, issue, thread, launch; /* seconds */
+  double dram_bytes, blocks_max, threads_per_block_max;
+} ispc_bound_report;
+/* l2_flushed: inputs start outside L2 (the timing flushes L2 between runs). */
+int ispc_bound(const ispc_space* s, const ispc_cand* c, int l2_flushed, ispc_bound_report* out);
+
+/* ---- bound-pruned search with measured evaluation ------------------------- */
+typedef struct ispc_search ispc_search;
+
+typedef struct {
+  int32_t device;           /* CUDA ordinal of this worker's B200               */
+  int32_t rollout_threads;  /* 0: auto                                          */
+  int32_t compile_threads;  /* 0: auto                                          */
+  int32_t batch;            /* kernels per NVRTC program (0: 8)                 */
+  uint64_t seed;
+  int32_t shard_index;      /* this worker's share of the frontier              */
+  int32_t shard_count;
+  int32_t pruning;          /* 1: bound pruning + p ~ max(T-b,0) rollouts, 0: uniform */
+  int32_t watchdog;         /* emit option (1: always)                          */
+  int32_t reps, warmup;     /* timed / untimed launches per candidate           */
+  int32_t flush_l2;         /* L2 flush before each launch                      */
+  int32_t max_unrolled;     /* emit budget (0: 2048)                            */
+  double budget_factor;     /* watchdog budget = factor x incumbent (0: 3)      */
+  double max_budget_ns;     /* budget before any incumbent (0: 50 ms)           */
+  const char* decision_order; /* comma separated choice names; NULL: paper order */
+  const char* incumbent_shm;  /* POSIX shm name shared by ranks; NULL: process-local */
+  const char* log_path;       /* JSONL evaluation log; NULL: none              */
+} ispc_search_config;
+
+typedef struct {
+  int64_t evaluations;      /* kernels launched on the device                   */
+  int64_t ok, mismatches, timeouts, launch_errors;
+  int64_t illegal, compile_errors, duplicates;
+  int64_t rollouts, dead_rollouts, pruned_children, bound_violations;
+  double best_ns;           /* best measured median (this worker's view)        */
+  double incumbent_ns;      /* shared incumbent (all ranks)                     */
+  double best_bound_ns;     /* bound of the best leaf                           */
+  double time_to_best_s, elapsed_s;
+  double device_step_ms;    /* device-timeline duration of the last step()      */
+  double t_rollout_s, t_compile_s, t_gpu_s; /* busy time per stage (summed over threads) */
+  uint64_t best_hash;
+  int64_t frontier;         /* subtree roots owned by this shard                */
+} ispc_search_stats;
+
+int ispc_search_create(const ispc_space* s, const ispc_search_config* cfg, ispc_search** out);
+/* Runs until `evaluations` more kernels were measured (the pipeline keeps
+ * running between calls). Records device-timeline marks around the step. */
+int ispc_search_step(ispc_search* h, int64_t evaluations);
+int ispc_search_stats_get(const ispc_search* h, ispc_search_stats* out);
+/* Best candidate (reference text serialization) and its CUDA source. */
+int ispc_search_best(const ispc_search* h, char* buf, size_t cap, size_t* len);
+int ispc_search_best_source(const ispc_search* h, char* buf, size_t cap, size_t* len);
+const char* ispc_search_error(const ispc_search* h);
+/* Host <-> device copies of the search's bound problem between steps (the
+ * end-to-end measurement uploads inputs and reads the output every step). */
+int ispc_search_write_region(ispc_search* h, const char* name, const void* host, size_t bytes);
+int ispc_search_read_region(ispc_search* h, const char* name, void* host, size_t bytes);
+void ispc_search_free(ispc_search* h);
 
 #ifdef __cplusplus
 }

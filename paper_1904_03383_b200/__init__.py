@@ -9,6 +9,6 @@ Layers:
                            (include/ispc_host.h)
   api.py                   Python mirror used by tests and bench.py
 """
-from .api import (Candidate, DeadEnd, Device, EmitError, Measurement, Module, NestHandle, Space,  # noqa: F401
+from .api import (Candidate, DeadEnd, Device, EmitError, Measurement, Module, NestHandle, Search, Space,  # noqa: F401
                   compile_sources)
 from . import _native  # noqa: F401

@@ -134,6 +134,30 @@ class SpaceStats(C.Structure):
                 ("root_open", C.c_uint64), ("root_digest", C.c_uint64), ("build_seconds", C.c_double)]
 
 
+class BoundReport(C.Structure):
+    _fields_ = [(f, C.c_double) for f in ("total", "dram", "sm_mem", "issue", "thread", "launch", "dram_bytes",
+                                          "blocks_max", "threads_per_block_max")]
+
+
+class SearchConfig(C.Structure):
+    _fields_ = [("device", C.c_int32), ("rollout_threads", C.c_int32), ("compile_threads", C.c_int32),
+                ("batch", C.c_int32), ("seed", C.c_uint64), ("shard_index", C.c_int32), ("shard_count", C.c_int32),
+                ("pruning", C.c_int32), ("watchdog", C.c_int32), ("reps", C.c_int32), ("warmup", C.c_int32),
+                ("flush_l2", C.c_int32), ("max_unrolled", C.c_int32), ("budget_factor", C.c_double),
+                ("max_budget_ns", C.c_double), ("decision_order", C.c_char_p), ("incumbent_shm", C.c_char_p),
+                ("log_path", C.c_char_p)]
+
+
+class SearchStats(C.Structure):
+    _fields_ = ([(f, C.c_int64) for f in ("evaluations", "ok", "mismatches", "timeouts", "launch_errors",
+                                           "illegal", "compile_errors", "duplicates", "rollouts", "dead_rollouts",
+                                           "pruned_children", "bound_violations")]
+                + [(f, C.c_double) for f in ("best_ns", "incumbent_ns", "best_bound_ns", "time_to_best_s",
+                                             "elapsed_s", "device_step_ms", "t_rollout_s", "t_compile_s",
+                                             "t_gpu_s")]
+                + [("best_hash", C.c_uint64), ("frontier", C.c_int64)])
+
+
 # Every symbol include/ispc.h declares, with its ctypes signature.
 ISPC_SYMBOLS = {
     "ispc_emit_cuda": (C.c_int, [C.POINTER(Nest), C.POINTER(EmitOpts), C.c_char_p, C.c_char_p, C.c_size_t,
@@ -158,7 +182,11 @@ ISPC_SYMBOLS = {
     "ispc_check": (C.c_int, [C.c_void_p, C.c_double, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                              C.POINTER(C.c_int)]),
     "ispc_read_region": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t]),
+    "ispc_write_region": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t]),
     "ispc_read_expected": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t]),
+    "ispc_dev_mark": (C.c_int, [C.c_void_p, C.c_int]),
+    "ispc_dev_mark_elapsed": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double)]),
+    "ispc_host_register": (C.c_int, [C.c_void_p, C.c_size_t]),
     "ispc_evaluate": (C.c_int, [C.c_void_p, C.POINTER(Nest), C.POINTER(EmitOpts), C.POINTER(TimeOpts),
                                 C.POINTER(TimeResult), C.POINTER(Launch)]),
 }
@@ -180,6 +208,8 @@ HOST_SYMBOLS = {
     "ispc_cand_first_leaf": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
     "ispc_cand_random_leaf": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p),
                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "ispc_cand_random_leaf_ordered": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_char_p, C.c_int,
+                                                C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "ispc_count_leaves": (C.c_int64, [C.c_void_p, C.c_void_p, C.c_int64]),
     "ispc_cand_to_nest": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
     "ispc_nest_buf_get": (C.POINTER(Nest), [C.c_void_p]),
@@ -189,6 +219,16 @@ HOST_SYMBOLS = {
     "ispc_cand_simulate": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
     "ispc_cand_serialize": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "ispc_cand_deserialize": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p)]),
+    "ispc_bound": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(BoundReport)]),
+    "ispc_search_create": (C.c_int, [C.c_void_p, C.POINTER(SearchConfig), C.POINTER(C.c_void_p)]),
+    "ispc_search_step": (C.c_int, [C.c_void_p, C.c_int64]),
+    "ispc_search_stats_get": (C.c_int, [C.c_void_p, C.POINTER(SearchStats)]),
+    "ispc_search_best": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "ispc_search_best_source": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "ispc_search_error": (C.c_char_p, [C.c_void_p]),
+    "ispc_search_free": (None, [C.c_void_p]),
+    "ispc_search_write_region": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t]),
+    "ispc_search_read_region": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t]),
 }
 
 _libs: dict[str, C.CDLL] = {}

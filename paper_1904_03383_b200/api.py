@@ -123,11 +123,12 @@ class Candidate:
             raise DeadEnd("no leaf within budget")
         return Candidate(self.space, h)
 
-    def random_leaf(self, seed: int, max_restarts: int = 1000) -> tuple["Candidate", int, int]:
+    def random_leaf(self, seed: int, max_restarts: int = 1000, order: str | None = None
+                    ) -> tuple["Candidate", int, int]:
         h = C.c_void_p()
         dec, dead = C.c_int64(), C.c_int64()
-        rc = N.host().ispc_cand_random_leaf(self.space._h, self._h, seed, max_restarts, C.byref(h),
-                                            C.byref(dec), C.byref(dead))
+        rc = N.host().ispc_cand_random_leaf_ordered(self.space._h, self._h, seed, order.encode() if order else None,
+                                                    max_restarts, C.byref(h), C.byref(dec), C.byref(dead))
         if rc != 0:
             raise DeadEnd("random descent gave up")
         return Candidate(self.space, h), dec.value, dead.value
@@ -152,6 +153,13 @@ class Candidate:
 
     def serialize(self) -> str:
         return N.read_text(N.host().ispc_cand_serialize, self.space._h, self._h)
+
+    def bound(self, l2_flushed: bool = False) -> dict:
+        """B200 lower bound in seconds (host/bound.hpp)."""
+        r = N.BoundReport()
+        if N.host().ispc_bound(self.space._h, self._h, int(l2_flushed), C.byref(r)) != 0:
+            raise ValueError(N.host_error())
+        return {f: getattr(r, f) for f, _ in N.BoundReport._fields_}
 
 
 class NestHandle:
@@ -306,3 +314,61 @@ class Device:
             return Measurement(N.STATUS.get(rc, str(rc)), float("inf"), float("inf"), float("inf"), 0.0, -1, L)
         return Measurement(N.STATUS.get(r.status, str(r.status)), r.median_ns, r.min_ns, r.first_ns, r.max_err,
                            r.mismatches, L)
+
+
+# ---------------------------------------------------------------- search
+class Search:
+    """Bound-pruned Monte-Carlo search with measured evaluation on one B200
+    (libispc_host ispc_search_*). The pipeline keeps running between step()s."""
+
+    PAPER_ORDER = "size,dim_kind,thread_level,mem_space,order,cache"
+
+    def __init__(self, space: Space, *, device: int = 0, seed: int = 1, shard_index: int = 0, shard_count: int = 1,
+                 pruning: bool = True, rollout_threads: int = 0, compile_threads: int = 0, batch: int = 8,
+                 reps: int = 3, warmup: int = 1, flush_l2: bool = False, watchdog: int = 1,
+                 budget_factor: float = 3.0, max_budget_ns: float = 50e6, max_unrolled: int = 2048,
+                 decision_order: str | None = None, incumbent_shm: str | None = None, log_path: str | None = None):
+        self.space = space
+        self._keep = [x.encode() if x else None for x in (decision_order, incumbent_shm, log_path)]
+        cfg = N.SearchConfig(device=device, rollout_threads=rollout_threads, compile_threads=compile_threads,
+                             batch=batch, seed=seed, shard_index=shard_index, shard_count=shard_count,
+                             pruning=int(pruning), watchdog=watchdog, reps=reps, warmup=warmup,
+                             flush_l2=int(flush_l2), max_unrolled=max_unrolled, budget_factor=budget_factor,
+                             max_budget_ns=max_budget_ns, decision_order=self._keep[0],
+                             incumbent_shm=self._keep[1], log_path=self._keep[2])
+        h = C.c_void_p()
+        if N.host().ispc_search_create(space._h, C.byref(cfg), C.byref(h)) != 0:
+            raise RuntimeError(N.host_error())
+        self._h = h
+
+    def step(self, evaluations: int):
+        rc = N.host().ispc_search_step(self._h, evaluations)
+        if rc != 0:
+            raise RuntimeError(N.host().ispc_search_error(self._h).decode())
+
+    def stats(self) -> dict:
+        s = N.SearchStats()
+        N.host().ispc_search_stats_get(self._h, C.byref(s))
+        return {f: getattr(s, f) for f, _ in N.SearchStats._fields_}
+
+    def best(self) -> Candidate | None:
+        text = N.read_text(N.host().ispc_search_best, self._h)
+        return self.space.deserialize(text) if text else None
+
+    def best_source(self) -> str:
+        return N.read_text(N.host().ispc_search_best_source, self._h)
+
+    def write_region(self, name: str, ptr: int, nbytes: int):
+        if N.host().ispc_search_write_region(self._h, name.encode(), C.c_void_p(ptr), nbytes) != 0:
+            raise RuntimeError(N.last_error())
+
+    def read_region(self, name: str, ptr: int, nbytes: int):
+        if N.host().ispc_search_read_region(self._h, name.encode(), C.c_void_p(ptr), nbytes) != 0:
+            raise RuntimeError(N.last_error())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.host().ispc_search_free(self._h)
+            self._h = None
+
+    __del__ = close

@@ -127,6 +127,7 @@ struct ispc_dev {
 
   std::map<int, Loaded> modules;
   int next_handle = 1;
+  cudaEvent_t marks[8] = {};
 };
 
 namespace {
@@ -221,6 +222,28 @@ int calibrate_timer(ispc_dev* d) {
   return ISPC_OK;
 }
 
+// Expected outputs of the bound problem, from the golden kernels.
+int recompute_expected(ispc_dev* d) {
+  const ispc_problem* p = &d->prob;
+  const int64_t m = p->m, n = p->n, k = p->k, s = std::max<int64_t>(p->a_stride, 1);
+  const int64_t batch = std::max<int64_t>(p->batch, 1);
+  auto R_ = [&](const char* nm) { return d->regions.at(nm).ptr; };
+  auto E_ = [&](const char* nm) { return d->expected.at(nm).ptr; };
+  switch (p->kind) {
+    case ISPC_PROB_AXPY: CK(d, ispc::launch_axpy_golden(R_("x"), R_("y"), E_("z"), n, p->alpha, d->stream)); break;
+    case ISPC_PROB_OUTER: CK(d, ispc::launch_outer_golden(R_("a"), R_("b"), E_("c"), m, n, d->stream)); break;
+    case ISPC_PROB_MATMUL:
+      CK(d, ispc::launch_matmul_golden(R_("a"), R_("b"), E_("c"), m, n, k, s, 1, d->stream));
+      break;
+    case ISPC_PROB_GEMV: CK(d, ispc::launch_gemv_golden(R_("a"), R_("x"), E_("y"), m, n, d->stream)); break;
+    case ISPC_PROB_BATCHED:
+      CK(d, ispc::launch_matmul_golden(R_("a"), R_("b"), E_("c"), m, n, k, 1, batch, d->stream));
+      break;
+  }
+  CK(d, cudaStreamSynchronize(d->stream));
+  return ISPC_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -295,20 +318,20 @@ int ispc_bind_problem(ispc_dev* d, const ispc_problem* p) {
     int64_t elems;
     bool input;
   };
-  std::vector<R> rs;
+  R rs_buf[3];
   const int64_t m = p->m, n = p->n, k = p->k, s = std::max<int64_t>(p->a_stride, 1);
   const int64_t batch = std::max<int64_t>(p->batch, 1);
   switch (p->kind) {
-    case ISPC_PROB_AXPY: rs = {{"x", n, true}, {"y", n, true}, {"z", n, false}}; break;
-    case ISPC_PROB_OUTER: rs = {{"a", m, true}, {"b", n, true}, {"c", m * n, false}}; break;
-    case ISPC_PROB_MATMUL: rs = {{"a", m * k * s, true}, {"b", k * n, true}, {"c", m * n, false}}; break;
-    case ISPC_PROB_GEMV: rs = {{"a", m * n, true}, {"x", n, true}, {"y", m, false}}; break;
+    case ISPC_PROB_AXPY: rs_buf[0] = {"x", n, true}, rs_buf[1] = {"y", n, true}, rs_buf[2] = {"z", n, false}; break;
+    case ISPC_PROB_OUTER: rs_buf[0] = {"a", m, true}, rs_buf[1] = {"b", n, true}, rs_buf[2] = {"c", m * n, false}; break;
+    case ISPC_PROB_MATMUL: rs_buf[0] = {"a", m * k * s, true}, rs_buf[1] = {"b", k * n, true}, rs_buf[2] = {"c", m * n, false}; break;
+    case ISPC_PROB_GEMV: rs_buf[0] = {"a", m * n, true}, rs_buf[1] = {"x", n, true}, rs_buf[2] = {"y", m, false}; break;
     case ISPC_PROB_BATCHED:
-      rs = {{"a", batch * m * k, true}, {"b", batch * k * n, true}, {"c", batch * m * n, false}};
+      rs_buf[0] = {"a", batch * m * k, true}, rs_buf[1] = {"b", batch * k * n, true}, rs_buf[2] = {"c", batch * m * n, false};
       break;
     default: return fail(d, ISPC_E_ARG, "unknown problem kind");
   }
-  for (const R& r : rs) {
+  for (const R& r : rs_buf) {
     if (r.elems <= 0) return fail(d, ISPC_E_ARG, std::string("empty region ") + r.name);
     Buffer b;
     if ((rc = alloc(d, b, r.elems))) return rc;
@@ -322,22 +345,8 @@ int ispc_bind_problem(ispc_dev* d, const ispc_problem* p) {
       d->outputs.push_back(r.name);
     }
   }
-  auto R_ = [&](const char* nm) { return d->regions.at(nm).ptr; };
-  auto E_ = [&](const char* nm) { return d->expected.at(nm).ptr; };
-  switch (p->kind) {
-    case ISPC_PROB_AXPY: CK(d, ispc::launch_axpy_golden(R_("x"), R_("y"), E_("z"), n, p->alpha, d->stream)); break;
-    case ISPC_PROB_OUTER: CK(d, ispc::launch_outer_golden(R_("a"), R_("b"), E_("c"), m, n, d->stream)); break;
-    case ISPC_PROB_MATMUL:
-      CK(d, ispc::launch_matmul_golden(R_("a"), R_("b"), E_("c"), m, n, k, s, 1, d->stream));
-      break;
-    case ISPC_PROB_GEMV: CK(d, ispc::launch_gemv_golden(R_("a"), R_("x"), E_("y"), m, n, d->stream)); break;
-    case ISPC_PROB_BATCHED:
-      CK(d, ispc::launch_matmul_golden(R_("a"), R_("b"), E_("c"), m, n, k, 1, batch, d->stream));
-      break;
-  }
-  CK(d, cudaStreamSynchronize(d->stream));
   d->bound = true;
-  return ISPC_OK;
+  return recompute_expected(d);
 }
 
 int ispc_problem_region(ispc_dev* d, const char* name, uint64_t* dev_ptr, int64_t* elems) {
@@ -359,6 +368,19 @@ int ispc_read_region(ispc_dev* d, const char* name, void* host, size_t bytes) {
   CK(d, cudaStreamSynchronize(d->stream));
   CK(d, cudaMemcpy(host, it->second.ptr, n, cudaMemcpyDeviceToHost));
   return ISPC_OK;
+}
+
+int ispc_write_region(ispc_dev* d, const char* name, const void* host, size_t bytes) {
+  if (!d || !name || !host) return ISPC_E_ARG;
+  if (!d->bound) return fail(d, ISPC_E_ARG, "no problem bound");
+  int rc = bind_ctx(d);
+  if (rc) return rc;
+  auto it = d->regions.find(name);
+  if (it == d->regions.end()) return fail(d, ISPC_E_ARG, std::string("no region ") + name);
+  if (d->expected.count(name)) return fail(d, ISPC_E_ARG, std::string("region ") + name + " is an output");
+  size_t n = std::min(bytes, size_t(it->second.elems) * 4);
+  CK(d, cudaMemcpyAsync(it->second.ptr, host, n, cudaMemcpyHostToDevice, d->stream));
+  return recompute_expected(d);
 }
 
 int ispc_read_expected(ispc_dev* d, const char* name, void* host, size_t bytes) {
@@ -590,6 +612,36 @@ int ispc_launch_timed(ispc_dev* d, int handle, const ispc_launch* L, const ispc_
   res->median_ns = times[times.size() / 2];
   res->min_ns = times.front();
   res->status = late ? ISPC_E_TIMEOUT : ISPC_OK;
+  return ISPC_OK;
+}
+
+int ispc_dev_mark(ispc_dev* d, int slot) {
+  if (!d || slot < 0 || slot >= 8) return fail(d, ISPC_E_ARG, "bad mark slot");
+  int rc = bind_ctx(d);
+  if (rc) return rc;
+  if (!d->marks[slot]) CK(d, cudaEventCreate(&d->marks[slot]));
+  CK(d, cudaEventRecord(d->marks[slot], d->stream));
+  return ISPC_OK;
+}
+
+int ispc_dev_mark_elapsed(ispc_dev* d, int a, int b, double* ms) {
+  if (!d || a < 0 || a >= 8 || b < 0 || b >= 8 || !d->marks[a] || !d->marks[b] || !ms)
+    return fail(d, ISPC_E_ARG, "bad mark slots");
+  int rc = bind_ctx(d);
+  if (rc) return rc;
+  CK(d, cudaEventSynchronize(d->marks[b]));
+  float f = 0;
+  CK(d, cudaEventElapsedTime(&f, d->marks[a], d->marks[b]));
+  *ms = f;
+  return ISPC_OK;
+}
+
+int ispc_host_register(void* p, size_t bytes) {
+  cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(nullptr, ISPC_E_CUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e));
+  }
   return ISPC_OK;
 }
 

@@ -196,13 +196,33 @@ int ispc_cand_first_leaf(const ispc_space* s, const ispc_cand* from, int budget,
 
 int ispc_cand_random_leaf(const ispc_space* s, const ispc_cand* from, uint64_t seed, int max_restarts,
                           ispc_cand** out, int64_t* decisions, int64_t* dead_ends) {
+  return ispc_cand_random_leaf_ordered(s, from, seed, nullptr, max_restarts, out, decisions, dead_ends);
+}
+
+int ispc_cand_random_leaf_ordered(const ispc_space* s, const ispc_cand* from, uint64_t seed, const char* order,
+                                  int max_restarts, ispc_cand** out, int64_t* decisions, int64_t* dead_ends) {
   if (!s || !from || !out) return set_err(ISPC_E_ARG, "null argument");
   std::mt19937_64 rng(seed);
+  DecisionOrder ord;
+  if (order) {
+    std::vector<std::string> names;
+    std::string cur;
+    for (const char* p = order;; ++p) {
+      if (*p == ',' || *p == 0) {
+        if (!cur.empty()) names.push_back(cur);
+        cur.clear();
+        if (!*p) break;
+      } else {
+        cur += *p;
+      }
+    }
+    ord = DecisionOrder::from_names(*s->ctx, names);
+  }
   int64_t dec = 0, dead = 0;
   ispace::Candidate leaf;
   bool ok = false;
   for (int attempt = 0; attempt <= max_restarts && !ok; ++attempt) {
-    WalkResult w = random_walk(*s->ctx, from->c, rng, leaf, nullptr);
+    WalkResult w = random_walk(*s->ctx, from->c, rng, leaf, order ? &ord : nullptr);
     dec += w.decisions;
     if (w.ok) ok = true;
     else ++dead;

@@ -1,0 +1,570 @@
+#include "search.hpp"
+
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <sstream>
+
+#include "adapter.hpp"
+#include "ispace/loop_nest.hpp"
+
+namespace ispc_host {
+
+using namespace ispace;
+
+// ---- incumbent -------------------------------------------------------------
+
+void Incumbent::open(const char* shm_name) {
+  if (shm_name && *shm_name) {
+    int fd = shm_open(shm_name, O_CREAT | O_RDWR, 0600);
+    if (fd >= 0) {
+      map_bytes = 4096;
+      if (ftruncate(fd, off_t(map_bytes)) == 0) {
+        void* p = mmap(nullptr, map_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+        if (p != MAP_FAILED) {
+          map = p;
+          cell = static_cast<std::atomic<uint64_t>*>(p);  // zero-filled: no incumbent yet
+          ispc_host_register(p, map_bytes);                 // pinned host memory
+        }
+      }
+      close(fd);
+    }
+  }
+  if (!cell) {
+    local = std::make_unique<std::atomic<uint64_t>>(0);
+    cell = local.get();
+  }
+}
+
+Incumbent::~Incumbent() {
+  if (map) munmap(map, map_bytes);
+}
+
+double Incumbent::seconds() const {
+  uint64_t v = cell->load(std::memory_order_acquire);
+  return v == 0 ? std::numeric_limits<double>::infinity() : double(v) * 1e-9;
+}
+
+bool Incumbent::offer(uint64_t ns) {
+  if (ns == 0) ns = 1;
+  uint64_t cur = cell->load(std::memory_order_acquire);
+  while (cur == 0 || ns < cur)
+    if (cell->compare_exchange_weak(cur, ns, std::memory_order_acq_rel)) return true;
+  return false;
+}
+
+// ---- search ------------------------------------------------------------------
+
+namespace {
+
+std::vector<std::string> split(const std::string& s) {
+  std::vector<std::string> out;
+  std::stringstream ss(s);
+  std::string tok;
+  while (std::getline(ss, tok, ','))
+    if (!tok.empty()) out.push_back(tok);
+  return out;
+}
+
+const char* kPaperOrder = "size,dim_kind,thread_level,mem_space,order,cache";
+
+}  // namespace
+
+double Search::now() const {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(space), cfg_(cfg) {
+  order_text_ = cfg.decision_order ? cfg.decision_order : kPaperOrder;
+  shm_text_ = cfg.incumbent_shm ? cfg.incumbent_shm : "";
+  log_text_ = cfg.log_path ? cfg.log_path : "";
+  cfg_.decision_order = order_text_.c_str();
+  if (cfg_.shard_count <= 0) cfg_.shard_count = 1;
+  if (cfg_.batch <= 0) cfg_.batch = 8;
+  if (cfg_.budget_factor <= 0) cfg_.budget_factor = 3.0;
+  if (cfg_.max_budget_ns <= 0) cfg_.max_budget_ns = 50e6;
+  if (cfg_.reps <= 0) cfg_.reps = 3;
+  if (cfg_.max_unrolled <= 0) cfg_.max_unrolled = 2048;
+  unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+  if (cfg_.rollout_threads <= 0) cfg_.rollout_threads = int(std::max(1u, hw / 4));
+  if (cfg_.compile_threads <= 0) cfg_.compile_threads = int(std::max(1u, hw - unsigned(cfg_.rollout_threads) - 1));
+  machine_.l2_flushed = cfg_.flush_l2 != 0;
+  machine_.max_unrolled = cfg_.max_unrolled;
+  model_ = std::make_unique<BoundModel>(space_->kernel, *space_->ctx, machine_);
+  order_ = DecisionOrder::from_names(*space_->ctx, split(order_text_));
+  inc_.open(shm_text_.empty() ? nullptr : shm_text_.c_str());
+  if (!log_text_.empty()) log_ = std::fopen(log_text_.c_str(), "w");
+  expand_frontier();
+
+  st_.best_ns = std::numeric_limits<double>::infinity();
+  t0_ = now();
+  if (cfg_.device < 0) return;  // dry run: rollouts + emission + NVRTC, no device
+  int rc = ispc_dev_open(cfg_.device, &dev_);
+  if (rc) throw std::runtime_error(std::string("ispc_dev_open: ") + ispc_last_error(nullptr));
+  ispc_problem p{};
+  if (ispc_space_problem(space_, &p) != 0) throw std::runtime_error("no problem for this space");
+  if ((rc = ispc_bind_problem(dev_, &p))) throw std::runtime_error(std::string("bind: ") + ispc_last_error(dev_));
+  st_.best_ns = std::numeric_limits<double>::infinity();
+  t0_ = now();
+}
+
+Search::~Search() {
+  stop_ = true;
+  cv_work_.notify_all();
+  cv_batch_.notify_all();
+  cv_done_.notify_all();
+  for (auto& t : threads_) t.join();
+  for (auto& b : batch_q_) ispc_module_free(b->module);
+  if (dev_) ispc_dev_close(dev_);
+  if (log_) std::fclose(log_);
+}
+
+// Deterministic breadth-first expansion of the first decisions; shard i keeps
+// frontier nodes i, i + S, ... Every rank computes the same frontier.
+void Search::expand_frontier() {
+  const SpaceContext& ctx = *space_->ctx;
+  std::vector<Candidate> frontier{space_->root};
+  const size_t want = size_t(16) * size_t(cfg_.shard_count);
+  for (int depth = 0; depth < 64 && frontier.size() < want; ++depth) {
+    std::vector<Candidate> next;
+    bool grew = false;
+    for (const Candidate& c : frontier) {
+      std::uint32_t inst = order_.pick(ctx, c);
+      if (inst == kNoInstance) {
+        next.push_back(c);
+        continue;
+      }
+      Mask m = c.dom[inst];
+      for (int v = 0; v < kMaxDomainBits; ++v) {
+        if (!mask_has(m, v)) continue;
+        Candidate child;
+        if (apply_decision(ctx, c, inst, v, child) == PropStatus::Ok) next.push_back(std::move(child));
+      }
+      grew = true;
+    }
+    if (!grew || next.empty()) break;
+    frontier = std::move(next);
+  }
+  for (size_t i = size_t(cfg_.shard_index); i < frontier.size(); i += size_t(cfg_.shard_count))
+    subtrees_.push_back(frontier[i]);
+  if (subtrees_.empty()) subtrees_.push_back(space_->root);  // tiny spaces: every shard searches all
+  st_.frontier = int64_t(subtrees_.size());
+}
+
+bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound) {
+  const SpaceContext& ctx = *space_->ctx;
+  Candidate cur = subtrees_[size_t(subtree_cursor_++ % subtrees_.size())];
+  const bool prune = cfg_.pruning != 0;
+  for (;;) {
+    std::uint32_t inst = order_.pick(ctx, cur);
+    if (inst == kNoInstance) {
+      leaf_bound = model_->bound(cur).total;
+      leaf = std::move(cur);
+      return true;
+    }
+    const double T = prune ? inc_.seconds() : std::numeric_limits<double>::infinity();
+    Mask m = cur.dom[inst];
+    std::vector<Candidate> kids;
+    std::vector<double> w;
+    for (int v = 0; v < kMaxDomainBits; ++v) {
+      if (!mask_has(m, v)) continue;
+      Candidate child;
+      if (apply_decision(ctx, cur, inst, v, child) != PropStatus::Ok) continue;
+      double weight = 1.0;
+      if (prune) {
+        double b = model_->bound(child).total;
+        if (!std::isfinite(b) || b >= T) {  // unrunnable, or cannot beat the incumbent
+          ++pruned_;
+          continue;
+        }
+        if (std::isfinite(T)) weight = T - b;
+      }
+      kids.push_back(std::move(child));
+      w.push_back(weight);
+    }
+    if (kids.empty()) return false;
+    std::discrete_distribution<size_t> pick(w.begin(), w.end());
+    cur = std::move(kids[pick(rng)]);
+  }
+}
+
+void Search::rollout_worker(int tid) {
+  std::mt19937_64 rng(cfg_.seed + 7919ull * uint64_t(tid) + 104729ull * uint64_t(cfg_.shard_index));
+  const size_t cap = size_t(cfg_.batch) * size_t(cfg_.compile_threads) * 3;
+  ispc_emit_opts eo{};
+  eo.watchdog = uint32_t(cfg_.watchdog);
+  eo.max_unrolled = uint32_t(cfg_.max_unrolled);
+  while (!stop_) {
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_work_.wait(lk, [&] { return stop_ || work_q_.size() < cap; });
+      if (stop_) return;
+    }
+    double t = now();
+    auto w = std::make_unique<Work>();
+    bool ok = rollout(rng, w->leaf, w->bound_s);
+    ++rollouts_;
+    if (!ok) {
+      ++dead_rollouts_;
+      t_rollout_.fetch_add(now() - t);
+      continue;
+    }
+    try {
+      LoopNest l = reconstruct(space_->kernel, *space_->ctx, w->leaf);
+      w->nest = flatten(space_->kernel, l);
+    } catch (const std::exception&) {
+      ++illegal_;
+      t_rollout_.fetch_add(now() - t);
+      continue;
+    }
+    size_t len = 0;
+    int rc = ispc_emit_cuda(&w->nest->nest, &eo, nullptr, nullptr, 0, &len, &w->launch);
+    if (rc == ISPC_OK) {
+      w->src.assign(len + 1, '\0');
+      rc = ispc_emit_cuda(&w->nest->nest, &eo, nullptr, w->src.data(), w->src.size(), &len, &w->launch);
+      w->src.resize(len);
+    }
+    t_rollout_.fetch_add(now() - t);
+    if (rc != ISPC_OK) {
+      ++illegal_;
+      continue;
+    }
+    w->digest = digest(*space_->ctx, w->leaf);
+    std::lock_guard<std::mutex> lk(mu_);
+    if (!seen_hash_.insert(w->launch.source_hash).second) {
+      ++duplicates_;
+      continue;
+    }
+    work_q_.push_back(std::move(w));
+    cv_batch_.notify_all();
+  }
+}
+
+void Search::compile_worker(int tid) {
+  (void)tid;
+  const size_t cap = size_t(cfg_.compile_threads) * 2 + 2;
+  while (!stop_) {
+    std::vector<std::unique_ptr<Work>> items;
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_batch_.wait(lk, [&] { return stop_ || (!work_q_.empty() && batch_q_.size() < cap); });
+      if (stop_) return;
+      // give the rollouts a moment to fill a whole batch
+      if (work_q_.size() < size_t(cfg_.batch))
+        cv_batch_.wait_for(lk, std::chrono::milliseconds(5),
+                           [&] { return stop_ || work_q_.size() >= size_t(cfg_.batch); });
+      while (!work_q_.empty() && items.size() < size_t(cfg_.batch)) {
+        items.push_back(std::move(work_q_.front()));
+        work_q_.pop_front();
+      }
+      cv_work_.notify_all();
+    }
+    if (items.empty()) continue;
+    double t = now();
+    std::vector<const char*> srcs;
+    for (auto& w : items) srcs.push_back(w->src.c_str());
+    ispc_module* m = nullptr;
+    int rc = ispc_compile(srcs.data(), int(srcs.size()), "sm_100a", &m);
+    std::vector<std::unique_ptr<CompiledBatch>> out;
+    if (rc == ISPC_OK) {
+      auto b = std::make_unique<CompiledBatch>();
+      b->items = std::move(items);
+      b->module = m;
+      out.push_back(std::move(b));
+    } else {
+      // isolate the failing kernel(s)
+      for (auto& w : items) {
+        const char* one[] = {w->src.c_str()};
+        ispc_module* m1 = nullptr;
+        if (ispc_compile(one, 1, "sm_100a", &m1) != ISPC_OK) {
+          ++compile_errors_;
+          continue;
+        }
+        auto b = std::make_unique<CompiledBatch>();
+        b->items.push_back(std::move(w));
+        b->module = m1;
+        out.push_back(std::move(b));
+      }
+    }
+    t_compile_.fetch_add(now() - t);
+    std::lock_guard<std::mutex> lk(mu_);
+    for (auto& b : out) batch_q_.push_back(std::move(b));
+    cv_done_.notify_all();
+  }
+}
+
+void Search::launch_worker() {
+  bool step_open = false;
+  while (!stop_) {
+    std::unique_ptr<CompiledBatch> b;
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      // the device only works inside step(): outside it the rollouts and
+      // compiles keep filling their bounded queues while the GPU idles
+      cv_done_.wait(lk, [&] { return stop_ || (!batch_q_.empty() && st_.evaluations < target_.load()); });
+      if (stop_) return;
+      launching_ = true;
+      b = std::move(batch_q_.front());
+      batch_q_.pop_front();
+      cv_batch_.notify_all();
+    }
+    double t_busy = now();
+    int h = 0;
+    if (!dev_) {  // dry run: count the compiled kernels as evaluated
+      std::lock_guard<std::mutex> lk(mu_);
+      st_.evaluations += int64_t(b->items.size());
+      ispc_module_free(b->module);
+      launching_ = false;
+      cv_done_.notify_all();
+      continue;
+    }
+    if (ispc_module_load(dev_, b->module, &h) != ISPC_OK) {
+      std::lock_guard<std::mutex> lk(mu_);
+      st_.launch_errors += int64_t(b->items.size());
+      st_.evaluations += int64_t(b->items.size());
+      ispc_module_free(b->module);
+      cv_done_.notify_all();
+      continue;
+    }
+    for (auto& w : b->items) {
+      if (stop_) break;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        if (st_.evaluations >= target_.load()) {
+          launching_ = false;
+          cv_done_.notify_all();
+          cv_done_.wait(lk, [&] { return stop_ || st_.evaluations < target_.load(); });
+          if (stop_) break;
+          launching_ = true;
+        }
+        if (!step_open && st_.evaluations < target_.load()) {
+          ispc_dev_mark(dev_, 0);
+          step_open = true;
+        }
+      }
+      const double T = inc_.seconds();
+      ispc_time_opts to{};
+      to.warmup = uint32_t(std::max(0, cfg_.warmup));
+      to.reps = uint32_t(cfg_.reps);
+      to.flush_l2 = uint32_t(cfg_.flush_l2);
+      to.check = 1;
+      to.bit_exact = 1;
+      to.rtol = 1e-5;
+      to.budget_ns = std::isfinite(T) ? std::min(cfg_.max_budget_ns, std::max(T * 1e9 * cfg_.budget_factor,
+                                                                                T * 1e9 + 20e3))
+                                      : cfg_.max_budget_ns;
+      ispc_time_result r{};
+      int rc = ispc_launch_timed(dev_, h, &w->launch, &to, &r);
+      const double t_now = now() - t0_;
+      std::string status;
+      bool improved = false;
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        ++st_.evaluations;
+        if (rc != ISPC_OK) {
+          ++st_.launch_errors;
+          status = rc == ISPC_E_STICKY ? "sticky" : "launch_error";
+          if (rc == ISPC_E_STICKY) {
+            err_ = ispc_last_error(dev_);
+            stop_ = true;
+          }
+        } else if (r.status == ISPC_E_MISMATCH) {
+          ++st_.mismatches;
+          status = "mismatch";
+        } else if (r.status == ISPC_E_TIMEOUT) {
+          ++st_.timeouts;
+          status = "timeout";
+        } else {
+          ++st_.ok;
+          status = "ok";
+          if (w->bound_s * 1e9 > r.median_ns * (1 + 1e-9)) ++st_.bound_violations;
+          inc_.offer(uint64_t(std::llround(r.median_ns)));
+          if (r.median_ns < st_.best_ns) {
+            improved = true;
+            st_.best_ns = r.median_ns;
+            st_.best_bound_ns = w->bound_s * 1e9;
+            st_.time_to_best_s = t_now;
+            st_.best_hash = w->launch.source_hash;
+            best_text_ = serialize_text(*space_->ctx, w->leaf);
+            best_src_ = w->src;
+            best_launch_ = w->launch;
+          }
+        }
+        if (log_) {
+          std::fprintf(log_,
+                       "{\"i\": %lld, \"t\": %.4f, \"status\": \"%s\", \"median_ns\": %.1f, \"bound_ns\": %.1f, "
+                       "\"incumbent_ns\": %.1f, \"hash\": \"%016llx\", \"digest\": \"%016llx\", \"best\": %s}\n",
+                       (long long)st_.evaluations, t_now, status.c_str(), rc == ISPC_OK ? r.median_ns : -1.0,
+                       w->bound_s * 1e9, inc_.seconds() * 1e9, (unsigned long long)w->launch.source_hash,
+                       (unsigned long long)w->digest, improved ? "true" : "false");
+        }
+        if (step_open && st_.evaluations >= target_.load()) {
+          ispc_dev_mark(dev_, 1);
+          double ms = 0;
+          ispc_dev_mark_elapsed(dev_, 0, 1, &ms);
+          st_.device_step_ms = ms;
+          step_open = false;
+        }
+      }
+      cv_done_.notify_all();
+    }
+    ispc_module_unload(dev_, h);
+    ispc_module_free(b->module);
+    std::lock_guard<std::mutex> lk(mu_);
+    st_.t_gpu_s += now() - t_busy;
+    launching_ = false;
+    cv_done_.notify_all();
+  }
+}
+
+int Search::region_io(const char* name, void* host, size_t bytes, bool upload) {
+  std::unique_lock<std::mutex> lk(mu_);
+  cv_done_.wait(lk, [&] { return stop_ || !launching_; });  // device idle between steps
+  return upload ? ispc_write_region(dev_, name, host, bytes) : ispc_read_region(dev_, name, host, bytes);
+}
+
+void Search::start() {
+  for (int i = 0; i < cfg_.rollout_threads; ++i) threads_.emplace_back([this, i] { rollout_worker(i); });
+  for (int i = 0; i < cfg_.compile_threads; ++i) threads_.emplace_back([this, i] { compile_worker(i); });
+  threads_.emplace_back([this] { launch_worker(); });
+  pipeline_started_ = true;
+}
+
+int Search::step(int64_t evaluations) {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    target_ = st_.evaluations + evaluations;
+  }
+  if (!pipeline_started_) start();
+  std::unique_lock<std::mutex> lk(mu_);
+  cv_done_.wait(lk, [&] { return stop_ || st_.evaluations >= target_.load(); });
+  if (stop_ && !err_.empty()) return ISPC_E_STICKY;
+  return ISPC_OK;
+}
+
+ispc_search_stats Search::stats() const {
+  std::lock_guard<std::mutex> lk(const_cast<std::mutex&>(mu_));
+  ispc_search_stats s = st_;
+  s.rollouts = rollouts_;
+  s.dead_rollouts = dead_rollouts_;
+  s.pruned_children = pruned_;
+  s.illegal = illegal_;
+  s.duplicates = duplicates_;
+  s.compile_errors = compile_errors_;
+  s.t_rollout_s = t_rollout_;
+  s.t_compile_s = t_compile_;
+  s.incumbent_ns = inc_.seconds() * 1e9;
+  s.elapsed_s = now() - t0_;
+  return s;
+}
+
+std::string Search::best_candidate() const {
+  std::lock_guard<std::mutex> lk(const_cast<std::mutex&>(mu_));
+  return best_text_;
+}
+
+std::string Search::best_source() const {
+  std::lock_guard<std::mutex> lk(const_cast<std::mutex&>(mu_));
+  return best_src_;
+}
+
+}  // namespace ispc_host
+
+// ---- C-ABI -----------------------------------------------------------------------
+
+using namespace ispc_host;
+
+struct ispc_search {
+  std::unique_ptr<Search> s;
+  std::string err;
+};
+
+extern "C" {
+
+int ispc_bound(const ispc_space* s, const ispc_cand* c, int l2_flushed, ispc_bound_report* out) {
+  try {
+    if (!s || !c || !out) return set_err(ISPC_E_ARG, "null argument");
+    B200Machine m;
+    m.l2_flushed = l2_flushed != 0;
+    BoundModel bm(s->kernel, *s->ctx, m);
+    BoundReport r = bm.bound(c->c);
+    out->total = r.total;
+    out->dram = r.dram;
+    out->sm_mem = r.sm_mem;
+    out->issue = r.issue;
+    out->thread = r.thread;
+    out->launch = r.launch;
+    out->dram_bytes = r.dram_bytes;
+    out->blocks_max = r.blocks_max;
+    out->threads_per_block_max = r.threads_per_block_max;
+    return ISPC_OK;
+  } catch (const std::exception& e) {
+    return set_err(ISPC_E_ARG, e.what());
+  }
+}
+
+int ispc_search_create(const ispc_space* s, const ispc_search_config* cfg, ispc_search** out) {
+  try {
+    if (!s || !cfg || !out) return set_err(ISPC_E_ARG, "null argument");
+    auto h = std::make_unique<ispc_search>();
+    h->s = std::make_unique<Search>(s, *cfg);
+    *out = h.release();
+    return ISPC_OK;
+  } catch (const std::exception& e) {
+    return set_err(ISPC_E_CUDA, e.what());
+  }
+}
+
+int ispc_search_step(ispc_search* h, int64_t evaluations) {
+  if (!h) return set_err(ISPC_E_ARG, "null search");
+  int rc = h->s->step(evaluations);
+  if (rc) h->err = h->s->error();
+  return rc;
+}
+
+int ispc_search_stats_get(const ispc_search* h, ispc_search_stats* out) {
+  if (!h || !out) return set_err(ISPC_E_ARG, "null argument");
+  *out = h->s->stats();
+  return ISPC_OK;
+}
+
+static int put(const std::string& s, char* buf, size_t cap, size_t* len) {
+  if (len) *len = s.size();
+  if (buf && cap) {
+    size_t k = s.size() < cap - 1 ? s.size() : cap - 1;
+    std::memcpy(buf, s.data(), k);
+    buf[k] = 0;
+  }
+  return ISPC_OK;
+}
+
+int ispc_search_best(const ispc_search* h, char* buf, size_t cap, size_t* len) {
+  if (!h) return set_err(ISPC_E_ARG, "null search");
+  return put(h->s->best_candidate(), buf, cap, len);
+}
+
+int ispc_search_best_source(const ispc_search* h, char* buf, size_t cap, size_t* len) {
+  if (!h) return set_err(ISPC_E_ARG, "null search");
+  return put(h->s->best_source(), buf, cap, len);
+}
+
+const char* ispc_search_error(const ispc_search* h) { return h ? h->err.c_str() : ""; }
+
+int ispc_search_write_region(ispc_search* h, const char* name, const void* host, size_t bytes) {
+  if (!h || !name || !host) return set_err(ISPC_E_ARG, "null argument");
+  return h->s->region_io(name, const_cast<void*>(host), bytes, true);
+}
+
+int ispc_search_read_region(ispc_search* h, const char* name, void* host, size_t bytes) {
+  if (!h || !name || !host) return set_err(ISPC_E_ARG, "null argument");
+  return h->s->region_io(name, host, bytes, false);
+}
+
+void ispc_search_free(ispc_search* h) { delete h; }
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// Bound-pruned Monte-Carlo search over the reference's decision space with
+// measured evaluation on a B200 (the reference's search.cpp is a stub,
+// proj/core/src/search.cpp:1; contract SPEC.md:459-514).
+//
+// Pipeline (one process per GPU):
+//   rollout threads   descend from this shard's subtree roots in the fixed
+//                     decision order (size, dim_kind, thread_level, mem_space,
+//                     order, cache). At each decision every
+//                     child is propagated (apply_decision) and bounded; children
+//                     with bound >= incumbent T are pruned and the rest drawn with
+//                     p ~ max(T - b, 0). Leaves are
+//                     reconstructed, flattened and emitted as sm_100a CUDA.
+//   compile threads   batch emitted kernels into NVRTC programs (sm_100a cubins)
+//   launch thread     loads each cubin on the device, times every kernel with a
+//                     watchdog budget of max(T x factor) and checks it on device,
+//                     then CAS-mins the incumbent
+// Sharding: the first levels of the tree are expanded deterministically into a
+// frontier; shard i owns frontier nodes i, i+S, i+2S, ... (disjoint subtrees,
+// no collective). The incumbent is one 64-bit cell in POSIX shared memory
+// (pinned through libispc), read by every rank before pruning.
+#pragma once
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_set>
+#include <vector>
+
+#include "adapter.hpp"
+#include "bound.hpp"
+#include "host_internal.hpp"
+#include "ispc.h"
+#include "ispc_host.h"
+
+namespace ispc_host {
+
+struct Incumbent {
+  std::atomic<uint64_t>* cell = nullptr;  // best measured time, ns (UINT64_MAX: none)
+  void* map = nullptr;
+  size_t map_bytes = 0;
+  std::unique_ptr<std::atomic<uint64_t>> local;
+  void open(const char* shm_name);
+  ~Incumbent();
+  double seconds() const;
+  bool offer(uint64_t ns);  // true when it became the new best
+};
+
+struct Work {
+  ispace::Candidate leaf;
+  std::unique_ptr<NestBuf> nest;
+  std::string src;
+  ispc_launch launch{};
+  double bound_s = 0;
+  uint64_t digest = 0;
+};
+
+struct CompiledBatch {
+  std::vector<std::unique_ptr<Work>> items;
+  ispc_module* module = nullptr;
+};
+
+class Search {
+ public:
+  Search(const ispc_space* space, const ispc_search_config& cfg);
+  ~Search();
+  int step(int64_t evaluations);
+  ispc_search_stats stats() const;
+  std::string best_candidate() const;
+  std::string best_source() const;
+  ispc_launch best_launch() const;
+  std::string error() const { return err_; }
+  // host <-> device copy of a problem region while the device is idle
+  int region_io(const char* name, void* host, size_t bytes, bool upload);
+
+ private:
+  const ispc_space* space_;
+  ispc_search_config cfg_;
+  std::string order_text_, shm_text_, log_text_;
+  B200Machine machine_;
+  std::unique_ptr<BoundModel> model_;
+  DecisionOrder order_;
+  std::vector<ispace::Candidate> subtrees_;
+  Incumbent inc_;
+  ispc_dev* dev_ = nullptr;
+  std::string err_;
+  FILE* log_ = nullptr;
+
+  // pipeline
+  std::mutex mu_;
+  std::condition_variable cv_work_, cv_batch_, cv_done_;
+  std::deque<std::unique_ptr<Work>> work_q_;
+  std::deque<std::unique_ptr<CompiledBatch>> batch_q_;
+  std::unordered_set<uint64_t> seen_hash_;
+  std::vector<std::thread> threads_;
+  std::atomic<bool> stop_{false};
+  std::atomic<int64_t> target_{0};
+  std::atomic<uint64_t> subtree_cursor_{0};
+  bool pipeline_started_ = false;
+  bool launching_ = false;  // guarded by mu_
+
+  // statistics (guarded by mu_ unless atomic)
+  ispc_search_stats st_{};
+  std::atomic<int64_t> rollouts_{0}, dead_rollouts_{0}, pruned_{0}, illegal_{0}, duplicates_{0};
+  std::atomic<int64_t> compile_errors_{0};
+  std::atomic<double> t_rollout_{0}, t_compile_{0};
+  double t0_ = 0;
+  std::string best_text_, best_src_;
+  ispc_launch best_launch_{};
+
+  void expand_frontier();
+  bool rollout(std::mt19937_64& rng, ispace::Candidate& leaf, double& leaf_bound);
+  void rollout_worker(int tid);
+  void compile_worker(int tid);
+  void launch_worker();
+  void start();
+  double now() const;
+};
+
+}  // namespace ispc_host

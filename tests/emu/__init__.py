@@ -29,8 +29,8 @@ def _entry(launch) -> str:
             args.append(f"*(unsigned long long*)a[{i}]")
     name = launch.name.decode()
     b = list(launch.block)
-    return (f'extern "C" void emu_entry(void** a) {{\n'
-            f'  emu_launch({launch.grid_x}u, {b[0]}u, {b[1]}u, {b[2]}u, [&] {{ {name}({", ".join(args)}); }});\n'
+    return (f'extern "C" int emu_entry(void** a) {{\n'
+            f'  return emu_launch({launch.grid_x}u, {b[0]}u, {b[1]}u, {b[2]}u, [&] {{ {name}({", ".join(args)}); }});\n'
             f'}}\n')
 
 
@@ -48,6 +48,7 @@ def build(src: str, launch) -> C.CDLL:
         os.replace(so + ".tmp", so)
     lib = C.CDLL(so)
     lib.emu_entry.argtypes = [C.POINTER(C.c_void_p)]
+    lib.emu_entry.restype = C.c_int
     return lib
 
 
@@ -75,5 +76,13 @@ def run(src: str, launch, regions: dict[str, np.ndarray], alpha: float = 1.5) ->
             v = C.c_uint64(2 ** 63)
             keep.append(v)
             ptrs[i] = C.cast(C.pointer(v), C.c_void_p)
-    lib.emu_entry(ptrs)
+    rc = lib.emu_entry(ptrs)
+    if rc == 1:
+        raise RuntimeError("emulated kernel deadlocked at a barrier")
+    if rc == 2:
+        raise TooLong("kernel exceeds the emulation budget of barrier phases")
     return regions
+
+
+class TooLong(Exception):
+    pass

@@ -1,21 +1,23 @@
 // CPU emulation of the CUDA subset the ispc emitter produces — TEST
-// INFRASTRUCTURE ONLY. Every CUDA thread of a block runs as a std::thread;
-// __syncthreads() is a std::barrier, so barrier placement bugs show up as
-// data races exactly like on the device. Blocks run one after another.
+// INFRASTRUCTURE ONLY. Every CUDA thread of a block runs as a user-space fiber
+// (ucontext) on one OS thread; __syncthreads() parks the fiber until every
+// fiber of the block arrived, so barrier placement decides which values a
+// fiber can observe exactly as on the device. Fibers run in a fixed order
+// between barriers (deterministic). Blocks run one after another.
 #pragma once
-#include <atomic>
-#include <barrier>
+#include <ucontext.h>
+
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
-#include <thread>
+#include <functional>
 #include <vector>
 
 struct emu_dim3 {
   unsigned x = 1, y = 1, z = 1;
 };
-inline thread_local emu_dim3 threadIdx, blockIdx;
-inline emu_dim3 blockDim, gridDim;
+inline emu_dim3 threadIdx, blockIdx, blockDim, gridDim;
 
 struct float2 {
   float x, y;
@@ -26,18 +28,27 @@ struct float4 {
 inline float2 make_float2(float a, float b) { return {a, b}; }
 inline float4 make_float4(float a, float b, float c, float d) { return {a, b, c, d}; }
 
-inline std::barrier<>* emu_bar = nullptr;
-inline std::atomic<int> emu_or{0};
-inline void __syncthreads() { emu_bar->arrive_and_wait(); }
+struct EmuSched {
+  ucontext_t main;
+  std::vector<ucontext_t> ctx;
+  std::vector<char*> stacks;
+  std::vector<int> state;  // 0 runnable, 1 at barrier, 2 done
+  int cur = -1;
+  int or_accum = 0, or_result = 0;
+  std::function<void()> kernel;
+};
+inline EmuSched* emu_s = nullptr;
+
+inline void emu_yield_barrier() {
+  EmuSched& s = *emu_s;
+  s.state[size_t(s.cur)] = 1;
+  swapcontext(&s.ctx[size_t(s.cur)], &s.main);
+}
+inline void __syncthreads() { emu_yield_barrier(); }
 inline int __syncthreads_or(int p) {
-  emu_bar->arrive_and_wait();
-  if (p) emu_or.store(1);
-  emu_bar->arrive_and_wait();
-  int r = emu_or.load();
-  emu_bar->arrive_and_wait();
-  emu_or.store(0);  // every thread resets; all read r before this phase
-  emu_bar->arrive_and_wait();
-  return r;
+  if (p) emu_s->or_accum = 1;
+  emu_yield_barrier();
+  return emu_s->or_result;
 }
 
 template <class T>
@@ -80,21 +91,66 @@ inline int ispc_timeout_flag = 0;
 inline unsigned long long ispc_now() { return 0; }
 alignas(16) inline float ispc_smem[1 << 16];
 
+inline void emu_fiber_entry() {
+  emu_s->kernel();
+  emu_s->state[size_t(emu_s->cur)] = 2;
+  swapcontext(&emu_s->ctx[size_t(emu_s->cur)], &emu_s->main);
+}
+
+// Returns 0 on success, 1 when fibers deadlock (some finished while others
+// wait at a barrier), 2 when the kernel exceeds `max_phases` barrier phases
+// (too long to emulate).
 template <class F>
-void emu_launch(unsigned grid, unsigned bx, unsigned by, unsigned bz, F&& kernel) {
+int emu_launch(unsigned grid, unsigned bx, unsigned by, unsigned bz, F&& kernel, long max_phases = 20000) {
   blockDim = {bx, by, bz};
   gridDim = {grid, 1, 1};
-  unsigned nt = bx * by * bz;
-  for (unsigned b = 0; b < grid; ++b) {
-    std::barrier<> bar(nt);
-    emu_bar = &bar;
-    std::vector<std::thread> ts;
-    for (unsigned t = 0; t < nt; ++t)
-      ts.emplace_back([&, t] {
-        blockIdx = {b, 0, 0};
+  const unsigned nt = bx * by * bz;
+  const size_t stack = 256 * 1024;
+  EmuSched s;
+  emu_s = &s;
+  s.kernel = kernel;
+  s.ctx.resize(nt);
+  s.state.assign(nt, 0);
+  for (unsigned t = 0; t < nt; ++t) s.stacks.push_back(static_cast<char*>(std::malloc(stack)));
+  int rc = 0;
+  for (unsigned b = 0; b < grid && !rc; ++b) {
+    blockIdx = {b, 0, 0};
+    for (unsigned t = 0; t < nt; ++t) {
+      getcontext(&s.ctx[t]);
+      s.ctx[t].uc_stack.ss_sp = s.stacks[t];
+      s.ctx[t].uc_stack.ss_size = stack;
+      s.ctx[t].uc_link = nullptr;
+      makecontext(&s.ctx[t], emu_fiber_entry, 0);
+      s.state[t] = 0;
+    }
+    for (;;) {
+      for (unsigned t = 0; t < nt; ++t) {
+        if (s.state[t] != 0) continue;
+        s.cur = int(t);
         threadIdx = {t % bx, (t / bx) % by, t / (bx * by)};
-        kernel();
-      });
-    for (auto& th : ts) th.join();
+        swapcontext(&s.main, &s.ctx[t]);
+      }
+      unsigned done = 0, waiting = 0;
+      for (unsigned t = 0; t < nt; ++t) {
+        done += s.state[t] == 2;
+        waiting += s.state[t] == 1;
+      }
+      if (done == nt) break;
+      if (done && waiting) {
+        rc = 1;
+        break;
+      }
+      if (--max_phases < 0) {
+        rc = 2;
+        break;
+      }
+      s.or_result = s.or_accum;
+      s.or_accum = 0;
+      for (unsigned t = 0; t < nt; ++t)
+        if (s.state[t] == 1) s.state[t] = 0;
+    }
   }
+  for (char* p : s.stacks) std::free(p);
+  emu_s = nullptr;
+  return rc;
 }
