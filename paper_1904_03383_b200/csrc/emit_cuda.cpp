@@ -508,7 +508,7 @@ class CudaEmitter {
   // --- statements -------------------------------------------------------------------
   std::ostringstream os_;
   int depth_ = 1;
-  int watch_loops_ = 0;  // LOOP nesting depth, for the watchdog poll
+  static constexpr int64_t kPollWork = 4096;  // instructions between deadline polls
   bool watchdog_ = false;
 
   void put(const std::string& s) { os_ << std::string(2 * depth_, ' ') << s << "\n"; }
@@ -599,9 +599,31 @@ class CudaEmitter {
     }
   }
 
-  void watchdog_poll(const std::string& var) {
+  // Sequential instruction count of one thread through a subtree (LOOP,
+  // UNROLL and VECTOR multiply; BLOCK / THREAD run in parallel).
+  int64_t work(uint32_t idx) const {
+    const ispc_node& nd = v_.node(idx);
+    if (nd.kind == ISPC_NODE_INST) return 1;
+    if (nd.kind != ISPC_NODE_DIM) return 0;
+    int64_t w = 0;
+    for (uint32_t j = 0; j < nd.children_count; ++j) w += work(nd.children_begin + j);
+    if (nd.dim_kind == ISPC_BLOCK || nd.dim_kind == ISPC_THREAD) return w;
+    return std::min<int64_t>(w * nd.size, int64_t(1) << 50);
+  }
+
+  // Every LOOP whose total work exceeds kPollWork polls the deadline about
+  // once per kPollWork instructions of its body, so no thread runs more than
+  // ~kPollWork instructions between two polls at any depth. Loop bounds are
+  // uniform across the block, so the polls (and their __syncthreads_or) are
+  // reached by every thread the same number of times.
+  void watchdog_poll(uint32_t idx, const std::string& var) {
     if (!watchdog_) return;
-    put("if ((" + var + " & 63) == 0) {");
+    const ispc_node& nd = v_.node(idx);
+    int64_t body = std::max<int64_t>(1, work(idx) / nd.size);
+    if (body * nd.size < kPollWork) return;
+    int64_t every = 1;
+    while (every * body < kPollWork) every <<= 1;
+    put(every == 1 ? std::string("{") : "if ((" + var + " & " + std::to_string(every - 1) + ") == 0) {");
     ++depth_;
     put("bool ispc_late = ispc_now() > ispc_deadline;");
     if (any_barrier()) put("ispc_late = __syncthreads_or(ispc_late);");
@@ -627,11 +649,10 @@ class CudaEmitter {
         put("#pragma unroll 1");
         put("for (int " + var + " = 0; " + var + " < " + sz + "; ++" + var + ") {");
         ++depth_;
-        if (watch_loops_++ == 0) watchdog_poll(var);
+        watchdog_poll(idx, var);
         env_[idx] = Idx{false, 0, var};
         emit_children(idx, nd.children_begin, nd.children_count);
         env_.erase(idx);
-        --watch_loops_;
         --depth_;
         put("}");
         return;
