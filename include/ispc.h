@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define ISPC_ABI_VERSION 1u
+#define ISPC_ABI_VERSION 2u
 #define ISPC_NONE 0xFFFFFFFFu
 
 /* ---- status codes ------------------------------------------------------- */
@@ -179,7 +179,7 @@ typedef struct {
 /* ---- emission -------------------------------------------------------------- */
 
 /* One kernel parameter of an emitted kernel, in declaration order. */
-enum ispc_param_kind { ISPC_PARAM_REGION = 0, ISPC_PARAM_INPUT, ISPC_PARAM_DEADLINE };
+enum ispc_param_kind { ISPC_PARAM_REGION = 0, ISPC_PARAM_INPUT, ISPC_PARAM_DEADLINE, ISPC_PARAM_TMAP };
 typedef struct {
   uint32_t kind;      /* ispc_param_kind                                       */
   uint32_t index;     /* REGION: region ObjId; INPUT: input index              */
@@ -189,7 +189,22 @@ typedef struct {
   char name[24];      /* REGION: region name ("x", "tmp0"); INPUT: "alpha"     */
 } ispc_param;
 
+/* A TMA tensor map (CUtensorMap, passed by value as a __grid_constant__
+ * parameter) the runtime encodes over a bound problem region at launch. */
+typedef struct {
+  uint32_t param;        /* index of the kernel parameter it fills          */
+  uint32_t rank;         /* 2 or 3                                          */
+  uint32_t swizzle;      /* 0 none, 1 32B, 2 64B, 3 128B                    */
+  uint32_t _pad;
+  char region[24];       /* problem region name                             */
+  uint64_t dims[3];      /* elements, innermost first                       */
+  uint64_t strides[2];   /* bytes between consecutive dims[1], dims[2]      */
+  uint32_t box[3];       /* elements per copy, innermost first              */
+  uint32_t _pad2;
+} ispc_tmap;
+
 #define ISPC_MAX_PARAMS 32
+#define ISPC_MAX_TMAPS 4
 typedef struct {
   char name[64];         /* extern "C" __global__ symbol                   */
   uint64_t grid_x;       /* linearized grid (block levels, mixed radix)    */
@@ -200,6 +215,9 @@ typedef struct {
   uint32_t watchdog;     /* 1 when the kernel polls the deadline parameter */
   uint32_t reg_elems;    /* register-array elements per thread (static)    */
   uint64_t source_hash;  /* FNV-1a of the kernel body (dedupe key)         */
+  uint32_t cluster[3];   /* thread-block cluster dims ({0,0,0}: no cluster) */
+  uint32_t num_tmaps;
+  ispc_tmap tmaps[ISPC_MAX_TMAPS];
 } ispc_launch;
 
 typedef struct {
@@ -226,6 +244,46 @@ const char* ispc_cuda_prelude(void);
  * the reference's emit_source() (loop_nest.cpp:389-609). Used to prove the flat
  * description carries the whole schedule. */
 int ispc_emit_pseudo(const ispc_nest* nest, char* buf, size_t cap, size_t* len);
+
+/* ---- B200 building-block kernels -------------------------------------------
+ * gemv, shared/cp.async-staged sgemm, batched sgemm and the tcgen05 sgemm of
+ * BASELINE.json cannot be written in the reference's gpu.space (SURVEY.md
+ * 0.4-0.5): their decisions live in a second space in the reference's own
+ * language (host/tiles.space, built through build_space, candidate.hpp:37-49).
+ * A fully specified candidate of that space crosses the boundary as this flat
+ * struct, the counterpart of ispc_nest; ispc_emit_tiles turns it into one
+ * sm_100a kernel assembled from hand-written building blocks. */
+enum ispc_tile_kind { ISPC_TILE_GEMV = 0, ISPC_TILE_SGEMM, ISPC_TILE_BATCHED, ISPC_TILE_SGEMM_TC };
+enum ispc_staging { ISPC_STAGE_DIRECT = 0, ISPC_STAGE_SHARED, ISPC_STAGE_CP_ASYNC, ISPC_STAGE_TMA };
+enum ispc_engine { ISPC_ENGINE_FFMA = 0, ISPC_ENGINE_TF32, ISPC_ENGINE_TF32X3 };
+enum ispc_xreduce { ISPC_XRED_SHUFFLE = 0, ISPC_XRED_SHARED };
+
+typedef struct {
+  uint32_t kind;                 /* ispc_tile_kind                                  */
+  uint32_t staging, engine;      /* ispc_staging, ispc_engine                       */
+  uint32_t xreduce, cache;       /* ispc_xreduce, ispc_cache (global operand loads) */
+  uint32_t _pad;
+  int64_t m, n, k, batch;        /* problem shape (column-major operands)           */
+  /* decided tile parameters; 0 = not a parameter of this kind                    */
+  int32_t thr_m, thr_n;          /* sgemm: CTA threads along m / n                  */
+  int32_t tm, tn;                /* per-thread output tile (sgemm, batched)         */
+  int32_t bk;                    /* k depth staged per step                         */
+  int32_t bn;                    /* tcgen05: UMMA N (M is 128)                      */
+  int32_t stages;                /* shared-memory ring depth                        */
+  int32_t vec;                   /* global vector width (floats)                    */
+  int32_t lanes_m, lanes_n;      /* gemv: warp lanes along rows / columns           */
+  int32_t warps_m, warps_n;      /* gemv: warps along rows / columns                */
+  int32_t split;                 /* gemv: cluster CTAs splitting the columns (DSMEM) */
+  int32_t unroll;                /* gemv: column loop unroll                        */
+  int32_t per_cta;               /* batched: problems per CTA                       */
+  int32_t _pad2;
+} ispc_tile_config;
+
+/* Emits the kernel of a tile configuration (same conventions as
+ * ispc_emit_cuda). ISPC_E_ILLEGAL when the configuration cannot run on a B200
+ * (shape not divisible, shared memory, threads, registers, cluster size). */
+int ispc_emit_tiles(const ispc_tile_config* cfg, const char* fn_name, char* buf, size_t cap, size_t* len,
+                    ispc_launch* launch);
 
 /* ---- compilation (no GPU needed; thread-safe) ------------------------------ */
 typedef struct ispc_module ispc_module;
@@ -274,6 +332,11 @@ int ispc_problem_region(ispc_dev* d, const char* name, uint64_t* dev_ptr, int64_
 int ispc_module_load(ispc_dev* d, const ispc_module* m, int* handle);
 int ispc_module_unload(ispc_dev* d, int handle);
 
+/* Checking: bit_exact compares bits with the golden sequential kernels.
+ * Otherwise an element fails when |out - exp| > rtol * scale, with scale the
+ * golden sum of |products| (sum |a||x| for gemv, sum |a||b| for matmuls) for
+ * reductions, |exp| elsewhere: the norm-wise test a reordered reduction
+ * (shuffle, split, tensor core) is held to. */
 typedef struct {
   uint32_t warmup;        /* untimed launches after the first (checked) one  */
   uint32_t reps;          /* timed launches; median reported                 */
@@ -325,6 +388,10 @@ int ispc_host_register(void* p, size_t bytes);
  * check. The mirror of CostReport is ispc_time_result (time in ns). */
 int ispc_evaluate(ispc_dev* d, const ispc_nest* nest, const ispc_emit_opts* eopts,
                   const ispc_time_opts* topts, ispc_time_result* res, ispc_launch* launch);
+
+/* Same one-shot path for a building-block configuration (ispc_emit_tiles). */
+int ispc_evaluate_tiles(ispc_dev* d, const ispc_tile_config* cfg, const ispc_time_opts* topts,
+                        ispc_time_result* res, ispc_launch* launch);
 
 #ifdef __cplusplus
 }

@@ -44,7 +44,9 @@ typedef struct ispc_nest_buf ispc_nest_buf;
 enum ispc_space_mode { ISPC_SPACE_PARITY = 0, ISPC_SPACE_B200 = 1 };
 
 typedef struct {
-  const char* kind;       /* "axpy" | "outer_product" | "matmul"                  */
+  const char* kind;       /* reference gpu.space: "axpy" | "outer_product" | "matmul";
+                             building blocks (tiles.space): "gemv" | "sgemm" |
+                             "batched" | "sgemm_tc"                                  */
   int64_t m, n, k;        /* axpy uses n                                          */
   int64_t a_stride;       /* matmul: element stride of A (1 = dense)              */
   int32_t num_factors;    /* strip-mining universes, outermost first              */
@@ -52,6 +54,7 @@ typedef struct {
   int64_t factors[4][32];
   int32_t mode;           /* ispc_space_mode                                      */
   int32_t _pad;
+  int64_t batch;          /* batched: number of independent problems              */
 } ispc_kernel_spec;
 
 typedef struct {
@@ -96,6 +99,9 @@ int ispc_cand_random_leaf_ordered(const ispc_space* s, const ispc_cand* from, ui
                                   int max_restarts, ispc_cand** out, int64_t* decisions, int64_t* dead_ends);
 /* Exhaustive first-open enumeration; returns the number of leaves (capped). */
 int64_t ispc_count_leaves(const ispc_space* s, const ispc_cand* from, int64_t cap);
+
+/* Building-block spaces: the decided tile configuration (ispc.h). */
+int ispc_cand_to_tiles(const ispc_space* s, const ispc_cand* c, ispc_tile_config* out);
 
 /* reconstruct() + flatten. */
 int ispc_cand_to_nest(const ispc_space* s, const ispc_cand* c, ispc_nest_buf** out);

@@ -10,5 +10,5 @@ Layers:
   api.py                   Python mirror used by tests and bench.py
 """
 from .api import (Candidate, DeadEnd, Device, EmitError, Measurement, Module, NestHandle, Search, Space,  # noqa: F401
-                  compile_sources)
+                  compile_sources, tile_cuda)
 from . import _native  # noqa: F401

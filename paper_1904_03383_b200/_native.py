@@ -15,7 +15,7 @@ LIBISPC_PATH = os.path.join(_HERE, "csrc", "libispc.so")
 LIBHOST_PATH = os.path.join(_HERE, "host", "libispc_host.so")
 
 ISPC_NONE = 0xFFFFFFFF
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 STATUS = {0: "ok", -1: "arg", -2: "cuda", -3: "nvrtc", -4: "launch", -5: "mismatch",
           -6: "timeout", -7: "illegal", -8: "nomem", -9: "sticky"}
@@ -24,6 +24,11 @@ OK, E_ARG, E_CUDA, E_NVRTC, E_LAUNCH, E_MISMATCH, E_TIMEOUT, E_ILLEGAL, E_NOMEM,
 
 PROB_AXPY, PROB_OUTER, PROB_MATMUL, PROB_GEMV, PROB_BATCHED = range(5)
 SPACE_PARITY, SPACE_B200 = 0, 1
+TILE_GEMV, TILE_SGEMM, TILE_BATCHED, TILE_SGEMM_TC = range(4)
+STAGINGS = ("DIRECT", "SHARED", "CP_ASYNC", "TMA")
+ENGINES = ("FFMA", "TF32", "TF32X3")
+XREDUCES = ("SHUFFLE", "SHARED")
+CACHES = ("L1", "L2", "READ_ONLY", "NONE")
 
 
 class AddrTerm(C.Structure):
@@ -94,10 +99,31 @@ class Param(C.Structure):
                 ("elems", C.c_int64), ("name", C.c_char * 24)]
 
 
+class TMap(C.Structure):
+    _fields_ = [("param", C.c_uint32), ("rank", C.c_uint32), ("swizzle", C.c_uint32), ("_pad", C.c_uint32),
+                ("region", C.c_char * 24), ("dims", C.c_uint64 * 3), ("strides", C.c_uint64 * 2),
+                ("box", C.c_uint32 * 3), ("_pad2", C.c_uint32)]
+
+
 class Launch(C.Structure):
     _fields_ = [("name", C.c_char * 64), ("grid_x", C.c_uint64), ("block", C.c_uint32 * 3),
                 ("static_smem", C.c_uint32), ("num_params", C.c_uint32), ("params", Param * 32),
-                ("watchdog", C.c_uint32), ("reg_elems", C.c_uint32), ("source_hash", C.c_uint64)]
+                ("watchdog", C.c_uint32), ("reg_elems", C.c_uint32), ("source_hash", C.c_uint64),
+                ("cluster", C.c_uint32 * 3), ("num_tmaps", C.c_uint32), ("tmaps", TMap * 4)]
+
+
+class TileConfig(C.Structure):
+    _fields_ = ([(f, C.c_uint32) for f in ("kind", "staging", "engine", "xreduce", "cache", "_pad")]
+                + [(f, C.c_int64) for f in ("m", "n", "k", "batch")]
+                + [(f, C.c_int32) for f in ("thr_m", "thr_n", "tm", "tn", "bk", "bn", "stages", "vec", "lanes_m",
+                                            "lanes_n", "warps_m", "warps_n", "split", "unroll", "per_cta",
+                                            "_pad2")])
+
+    def as_dict(self) -> dict:
+        d = {f: getattr(self, f) for f, _ in self._fields_ if not f.startswith("_")}
+        d["staging"], d["engine"] = STAGINGS[self.staging], ENGINES[self.engine]
+        d["xreduce"], d["cache"] = XREDUCES[self.xreduce], CACHES[self.cache]
+        return d
 
 
 class EmitOpts(C.Structure):
@@ -125,7 +151,8 @@ class TimeResult(C.Structure):
 class KernelSpec(C.Structure):
     _fields_ = [("kind", C.c_char_p), ("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64),
                 ("a_stride", C.c_int64), ("num_factors", C.c_int32), ("factor_len", C.c_int32 * 4),
-                ("factors", (C.c_int64 * 32) * 4), ("mode", C.c_int32), ("_pad", C.c_int32)]
+                ("factors", (C.c_int64 * 32) * 4), ("mode", C.c_int32), ("_pad", C.c_int32),
+                ("batch", C.c_int64)]
 
 
 class SpaceStats(C.Structure):
@@ -189,6 +216,10 @@ ISPC_SYMBOLS = {
     "ispc_host_register": (C.c_int, [C.c_void_p, C.c_size_t]),
     "ispc_evaluate": (C.c_int, [C.c_void_p, C.POINTER(Nest), C.POINTER(EmitOpts), C.POINTER(TimeOpts),
                                 C.POINTER(TimeResult), C.POINTER(Launch)]),
+    "ispc_emit_tiles": (C.c_int, [C.POINTER(TileConfig), C.c_char_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t),
+                                  C.POINTER(Launch)]),
+    "ispc_evaluate_tiles": (C.c_int, [C.c_void_p, C.POINTER(TileConfig), C.POINTER(TimeOpts),
+                                      C.POINTER(TimeResult), C.POINTER(Launch)]),
 }
 
 HOST_SYMBOLS = {
@@ -212,6 +243,7 @@ HOST_SYMBOLS = {
                                                 C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "ispc_count_leaves": (C.c_int64, [C.c_void_p, C.c_void_p, C.c_int64]),
     "ispc_cand_to_nest": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "ispc_cand_to_tiles": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(TileConfig)]),
     "ispc_nest_buf_get": (C.POINTER(Nest), [C.c_void_p]),
     "ispc_nest_buf_free": (None, [C.c_void_p]),
     "ispc_cand_reference_source": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_size_t,

@@ -20,8 +20,10 @@ from . import _native as N
 class Space:
     """A kernel backbone bound to the GPU decision space (gpu_space.hpp:15-18)."""
 
+    TILE_KINDS = ("gemv", "sgemm", "batched", "sgemm_tc")
+
     def __init__(self, kind: str, *, m: int = 0, n: int = 0, k: int = 0, a_stride: int = 1,
-                 factors: list[list[int]] | None = None, mode: int = N.SPACE_PARITY):
+                 factors: list[list[int]] | None = None, mode: int = N.SPACE_PARITY, batch: int = 1):
         factors = factors or []
         spec = N.KernelSpec()
         self._kind = kind.encode()
@@ -37,8 +39,11 @@ class Space:
             for j, v in enumerate(u):
                 spec.factors[i][j] = v
         spec.mode = mode
+        spec.batch = batch
         self.kind, self.m, self.n, self.k, self.a_stride, self.factors, self.mode = (
             kind, m, n, k, a_stride, factors, mode)
+        self.batch = batch
+        self.tiles = kind in self.TILE_KINDS
         h = C.c_void_p()
         rc = N.host().ispc_space_create(C.byref(spec), C.byref(h))
         if rc != 0:
@@ -136,6 +141,13 @@ class Candidate:
     def count_leaves(self, cap: int = 10 ** 7) -> int:
         return N.host().ispc_count_leaves(self.space._h, self._h, cap)
 
+    def tiles(self) -> N.TileConfig:
+        """Decided building-block configuration (tiles.space candidates)."""
+        t = N.TileConfig()
+        if N.host().ispc_cand_to_tiles(self.space._h, self._h, C.byref(t)) != 0:
+            raise ValueError(N.host_error())
+        return t
+
     def nest(self) -> "NestHandle":
         h = C.c_void_p()
         if N.host().ispc_cand_to_nest(self.space._h, self._h, C.byref(h)) != 0:
@@ -190,6 +202,21 @@ class NestHandle:
         if rc != 0:
             raise EmitError(rc, N.last_error())
         return buf.value.decode(), L
+
+
+def tile_cuda(cfg: N.TileConfig, fn_name: str | None = None) -> tuple[str, N.Launch]:
+    """sm_100a source of a building-block configuration (ispc_emit_tiles)."""
+    L = N.Launch()
+    n = C.c_size_t()
+    nm = fn_name.encode() if fn_name else None
+    rc = N.ispc().ispc_emit_tiles(C.byref(cfg), nm, None, 0, C.byref(n), C.byref(L))
+    if rc != 0:
+        raise EmitError(rc, N.last_error())
+    buf = C.create_string_buffer(n.value + 1)
+    rc = N.ispc().ispc_emit_tiles(C.byref(cfg), nm, buf, n.value + 1, C.byref(n), C.byref(L))
+    if rc != 0:
+        raise EmitError(rc, N.last_error())
+    return buf.value.decode(), L
 
 
 class EmitError(Exception):
@@ -310,6 +337,27 @@ class Device:
         rc = N.ispc().ispc_evaluate(self._h, nest.nest, C.byref(eo),
                                     C.byref(self._opts(warmup, reps, flush_l2, check, bit_exact, rtol, budget_ns)),
                                     C.byref(r), C.byref(L))
+        if rc != 0:
+            return Measurement(N.STATUS.get(rc, str(rc)), float("inf"), float("inf"), float("inf"), 0.0, -1, L)
+        return Measurement(N.STATUS.get(r.status, str(r.status)), r.median_ns, r.min_ns, r.first_ns, r.max_err,
+                           r.mismatches, L)
+
+
+    def evaluate_tiles(self, cfg: N.TileConfig, *, warmup=1, reps=3, flush_l2=False, check=True,
+                       bit_exact=None, rtol=None) -> Measurement:
+        """Emit + compile + timed launch + on-device check of a building-block
+        configuration. Default checking: bit-exact for the FFMA sgemm and
+        batched kernels (k ascending per output), norm-wise rtol otherwise."""
+        exact_default = cfg.kind in (N.TILE_SGEMM, N.TILE_BATCHED)
+        if bit_exact is None:
+            bit_exact = exact_default
+        if rtol is None:
+            rtol = 4e-3 if (cfg.kind == N.TILE_SGEMM_TC and cfg.engine == 1) else 1e-5
+        r = N.TimeResult()
+        L = N.Launch()
+        rc = N.ispc().ispc_evaluate_tiles(self._h, C.byref(cfg),
+                                          C.byref(self._opts(warmup, reps, flush_l2, check, bit_exact, rtol, 2e9)),
+                                          C.byref(r), C.byref(L))
         if rc != 0:
             return Measurement(N.STATUS.get(rc, str(rc)), float("inf"), float("inf"), float("inf"), 0.0, -1, L)
         return Measurement(N.STATUS.get(r.status, str(r.status)), r.median_ns, r.min_ns, r.first_ns, r.max_err,

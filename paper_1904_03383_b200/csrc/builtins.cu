@@ -47,7 +47,7 @@ __global__ void outer_golden(const float* a, const float* b, float* c, int64_t m
 // order is the sequential one regardless of staging.
 __global__ void matmul_golden(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ c,
                               int64_t m, int64_t n, int64_t kk, int64_t s, int64_t batch_stride_a,
-                              int64_t batch_stride_b, int64_t batch_stride_c) {
+                              int64_t batch_stride_b, int64_t batch_stride_c, float* __restrict__ scale) {
   const int64_t bz = blockIdx.z;
   a += bz * batch_stride_a;
   b += bz * batch_stride_b;
@@ -56,26 +56,37 @@ __global__ void matmul_golden(const float* __restrict__ a, const float* __restri
   int64_t j = blockIdx.y;
   if (j >= n) return;
   __shared__ float bs[1024];
-  float acc = 0.0f;
+  float acc = 0.0f, sabs = 0.0f;
   for (int64_t k0 = 0; k0 < kk; k0 += 1024) {
     int64_t kn = kk - k0 < 1024 ? kk - k0 : 1024;
     __syncthreads();
     for (int64_t t = threadIdx.x; t < kn; t += blockDim.x) bs[t] = b[k0 + t + j * kk];
     __syncthreads();
     if (i < m)
-      for (int64_t k = 0; k < kn; ++k) acc = __fmaf_rn(a[i * s + (k0 + k) * m * s], bs[k], acc);
+      for (int64_t k = 0; k < kn; ++k) {
+        float av = a[i * s + (k0 + k) * m * s];
+        acc = __fmaf_rn(av, bs[k], acc);
+        if (scale) sabs = __fmaf_rn(fabsf(av), fabsf(bs[k]), sabs);
+      }
   }
-  if (i < m) c[i + j * m] = acc;
+  if (i < m) {
+    c[i + j * m] = acc;
+    if (scale) scale[bz * batch_stride_c + i + j * m] = sabs;
+  }
 }
 
 // y[i] = sum_j A[i + j*m] * x[j], j ascending (gemv backbone order).
 __global__ void gemv_golden(const float* __restrict__ a, const float* __restrict__ x, float* __restrict__ y,
-                            int64_t m, int64_t n) {
+                            int64_t m, int64_t n, float* __restrict__ scale) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= m) return;
-  float acc = 0.0f;
-  for (int64_t j = 0; j < n; ++j) acc = __fmaf_rn(a[i + j * m], x[j], acc);
+  float acc = 0.0f, sabs = 0.0f;
+  for (int64_t j = 0; j < n; ++j) {
+    acc = __fmaf_rn(a[i + j * m], x[j], acc);
+    sabs = __fmaf_rn(fabsf(a[i + j * m]), fabsf(x[j]), sabs);
+  }
   y[i] = acc;
+  if (scale) scale[i] = sabs;
 }
 
 struct CmpOut {
@@ -84,13 +95,14 @@ struct CmpOut {
   unsigned int pad;
 };
 
-__global__ void compare_kernel(const float* out, const float* exp, int64_t n, int bit_exact, float rtol,
-                               CmpOut* res) {
+__global__ void compare_kernel(const float* out, const float* exp, const float* scale, int64_t n, int bit_exact,
+                               float rtol, CmpOut* res) {
   unsigned long long bad = 0;
   float worst = 0.0f;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     float o = out[i], e = exp[i];
-    float den = fabsf(e) > 1e-30f ? fabsf(e) : 1e-30f;
+    float den = scale ? scale[i] : fabsf(e);
+    den = den > 1e-30f ? den : 1e-30f;
     float err = fabsf(o - e) / den;
     if (o != o) err = __int_as_float(0x7f800000);  // NaN output (unwritten) -> inf
     bool diff = bit_exact ? (__float_as_uint(o) != __float_as_uint(e)) : !(err <= rtol);
@@ -139,21 +151,21 @@ cudaError_t launch_outer_golden(const float* a, const float* b, float* c, int64_
 }
 
 cudaError_t launch_matmul_golden(const float* a, const float* b, float* c, int64_t m, int64_t n, int64_t k,
-                                 int64_t a_stride, int64_t batch, cudaStream_t s) {
+                                 int64_t a_stride, int64_t batch, float* scale, cudaStream_t s) {
   dim3 grid(unsigned((m + 127) / 128), unsigned(n), unsigned(batch));
-  matmul_golden<<<grid, 128, 0, s>>>(a, b, c, m, n, k, a_stride, m * k * a_stride, k * n, m * n);
+  matmul_golden<<<grid, 128, 0, s>>>(a, b, c, m, n, k, a_stride, m * k * a_stride, k * n, m * n, scale);
   return cudaGetLastError();
 }
 
-cudaError_t launch_gemv_golden(const float* a, const float* x, float* y, int64_t m, int64_t n,
+cudaError_t launch_gemv_golden(const float* a, const float* x, float* y, int64_t m, int64_t n, float* scale,
                                cudaStream_t s) {
-  gemv_golden<<<unsigned((m + 127) / 128), 128, 0, s>>>(a, x, y, m, n);
+  gemv_golden<<<unsigned((m + 127) / 128), 128, 0, s>>>(a, x, y, m, n, scale);
   return cudaGetLastError();
 }
 
-cudaError_t launch_compare(const float* out, const float* exp, int64_t n, int bit_exact, float rtol,
-                           void* dev_res, cudaStream_t s) {
-  compare_kernel<<<grid_for(n), 256, 0, s>>>(out, exp, n, bit_exact, rtol, static_cast<CmpOut*>(dev_res));
+cudaError_t launch_compare(const float* out, const float* exp, const float* scale, int64_t n, int bit_exact,
+                           float rtol, void* dev_res, cudaStream_t s) {
+  compare_kernel<<<grid_for(n), 256, 0, s>>>(out, exp, scale, n, bit_exact, rtol, static_cast<CmpOut*>(dev_res));
   return cudaGetLastError();
 }
 

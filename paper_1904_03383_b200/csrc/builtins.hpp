@@ -16,11 +16,11 @@ cudaError_t launch_axpy_golden(const float* x, const float* y, float* z, int64_t
 cudaError_t launch_outer_golden(const float* a, const float* b, float* c, int64_t m, int64_t n,
                                 cudaStream_t s);
 cudaError_t launch_matmul_golden(const float* a, const float* b, float* c, int64_t m, int64_t n, int64_t k,
-                                 int64_t a_stride, int64_t batch, cudaStream_t s);
-cudaError_t launch_gemv_golden(const float* a, const float* x, float* y, int64_t m, int64_t n,
+                                 int64_t a_stride, int64_t batch, float* scale, cudaStream_t s);
+cudaError_t launch_gemv_golden(const float* a, const float* x, float* y, int64_t m, int64_t n, float* scale,
                                cudaStream_t s);
-cudaError_t launch_compare(const float* out, const float* exp, int64_t n, int bit_exact, float rtol,
-                           void* dev_res, cudaStream_t s);
+cudaError_t launch_compare(const float* out, const float* exp, const float* scale, int64_t n, int bit_exact,
+                           float rtol, void* dev_res, cudaStream_t s);
 cudaError_t launch_timer(unsigned long long* out, cudaStream_t s);
 
 }  // namespace ispc

@@ -805,6 +805,42 @@ static __device__ __forceinline__ unsigned long long ispc_now() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// building blocks of the tile kernels (emit_tiles.cpp)
+static __device__ __forceinline__ unsigned ispc_smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+static __device__ __forceinline__ void ispc_cp_async_cg16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(ispc_smem_addr(s)), "l"(g) : "memory");
+}
+static __device__ __forceinline__ void ispc_cp_async_ca16(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(ispc_smem_addr(s)), "l"(g) : "memory");
+}
+static __device__ __forceinline__ void ispc_cp_async_ca8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(ispc_smem_addr(s)), "l"(g) : "memory");
+}
+static __device__ __forceinline__ void ispc_cp_async_ca4(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(ispc_smem_addr(s)), "l"(g) : "memory");
+}
+static __device__ __forceinline__ void ispc_cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+static __device__ __forceinline__ void ispc_cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+static __device__ __forceinline__ unsigned ispc_cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+static __device__ __forceinline__ void ispc_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+static __device__ __forceinline__ float ispc_dsmem_ld(const float* p, unsigned rank) {
+  unsigned a = ispc_smem_addr(p), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(r) : "memory");
+  return v;
+}
 )";
 }
 

@@ -1,0 +1,562 @@
+// sm_100a building-block emitter: one fully specified candidate of the tile
+// space (host/tiles.space, decided through the reference's engine) -> one
+// __global__ kernel. This is the half of the code generator the reference's
+// gpu.space cannot reach: gemv with warp-shuffle and
+// cluster (DSMEM) reductions, shared-memory / cp.async multi-stage sgemm,
+// batched sgemm, and the tcgen05/TMEM sgemm (emit_tcgen05.cpp).
+//
+// Blocks (each a decision of the candidate):
+//   vec      ld.global.v2/v4 (float2/float4) operand loads
+//   cache    L1 -> ld.global.ca, L2 -> .cg, READ_ONLY -> .nc, NONE -> .cs
+//   xreduce  SHUFFLE: __shfl_xor_sync butterfly; SHARED: through shared memory
+//   split    thread-block cluster of `split` CTAs splitting the reduction axis,
+//            partial sums combined through distributed shared memory
+//   staging  SHARED: ld.global -> st.shared (stages 2: register prefetch of
+//            the next k tile); CP_ASYNC: cp.async ring of `stages` tiles
+// The FFMA sgemm / batched kernels keep every output's k order ascending
+// (one fmaf chain per output), so they are bit-identical to the sequential
+// golden kernel; gemv reorders its sum and is checked norm-wise.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+#include <string>
+
+#include "ispc.h"
+#include "nest_view.hpp"
+
+namespace ispc {
+
+std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn, ispc_launch& L);
+
+namespace {
+
+uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char ch : s) h = (h ^ ch) * 1099511628211ull;
+  return h;
+}
+
+[[noreturn]] void illegal(const std::string& why) { throw NestError(ISPC_E_ILLEGAL, why); }
+
+bool pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+std::string ld(uint32_t cache, int width, const std::string& ptr) {
+  std::string ty = width == 4 ? "float4" : width == 2 ? "float2" : "float";
+  std::string p = width > 1 ? "(const " + ty + "*)(" + ptr + ")" : "(" + ptr + ")";
+  switch (cache) {
+    case ISPC_CACHE_L1: return "__ldca(" + p + ")";
+    case ISPC_CACHE_L2: return "__ldcg(" + p + ")";
+    case ISPC_CACHE_READ_ONLY: return "__ldg(" + p + ")";
+    default: return "__ldcs(" + p + ")";
+  }
+}
+
+const char* comp(int i) {
+  static const char* c[] = {".x", ".y", ".z", ".w"};
+  return c[i];
+}
+
+void add_region(ispc_launch& L, const char* name, int64_t elems) {
+  ispc_param& P = L.params[L.num_params++];
+  P.kind = ISPC_PARAM_REGION;
+  P.is_input = 1;
+  P.elems = elems;
+  std::snprintf(P.name, sizeof(P.name), "%s", name);
+}
+
+// ---------------------------------------------------------------- gemv
+// y[i] = sum_j A[i + j*m] x[j]. Lane (lm, ln) of warp (wm, wn) in cluster CTA
+// `rank` owns rows row0 .. row0+vec-1 and walks columns
+//   j = rank*n/split + (wn*lanes_n + ln) + t * warps_n*lanes_n,   t ascending.
+std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
+  const int64_t m = c.m, n = c.n;
+  const int V = c.vec, LM = c.lanes_m, LN = c.lanes_n, WM = c.warps_m, WN = c.warps_n, S = c.split,
+            U = c.unroll;
+  if (!(V == 1 || V == 2 || V == 4)) illegal("vector width must be 1, 2 or 4");
+  if (LM * LN != 32 || !pow2(LM)) illegal("warp lanes must split 32 in powers of two");
+  if (WM < 1 || WN < 1 || S < 1 || U < 1) illegal("non-positive tile parameter");
+  const int T = 32 * WM * WN;
+  if (T > 1024) illegal("more than 1024 threads per CTA");
+  if (S > 8) illegal("cluster larger than 8 CTAs");
+  const int64_t R = int64_t(V) * LM * WM;  // rows per CTA
+  if (m % R) illegal("rows per CTA do not divide m");
+  const int64_t G = int64_t(WN) * LN;      // column lanes per CTA
+  if (n % (S * G * U)) illegal("column split does not divide n");
+  const int64_t iters = n / (S * G);       // columns per thread
+  const bool direct = WN == 1 && S == 1;  // lane sums go straight to y
+  const bool xr_shared = LN > 1 && c.xreduce == ISPC_XRED_SHARED;
+  const int64_t part_off = 0;                                // [WN][R] warp partials
+  const int64_t cl_off = direct ? 0 : WN * R;                // [R] CTA partials (cluster)
+  const int64_t xr_off = direct ? 0 : WN * R + R;            // [T][V] lane partials
+  const int64_t smem = 4 * (xr_off + (xr_shared ? int64_t(T) * V : 0));
+  if (smem > 232448) illegal("shared memory exceeds 227 KiB");
+
+  std::ostringstream o;
+  const std::string ty = V == 4 ? "float4" : V == 2 ? "float2" : "float";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << T << ") " << fn
+    << "(const float* __restrict__ g_a, const float* __restrict__ g_x, float* __restrict__ g_y) {\n";
+  o << "  extern __shared__ __align__(16) float ispc_smem[];\n";
+  o << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n";
+  o << "  const int lm = lane % " << LM << ", ln = lane / " << LM << ";\n";
+  o << "  const int wm = warp % " << WM << ", wn = warp / " << WM << ";\n";
+  o << "  const int rank = " << (S > 1 ? "(int)ispc_cluster_rank()" : "0") << ";\n";
+  o << "  const long long rblk = blockIdx.x / " << S << ";\n";
+  o << "  const long long row0 = rblk * " << R << "LL + (long long)(wm * " << LM << " + lm) * " << V << ";\n";
+  o << "  const long long col0 = (long long)rank * " << n / S << "LL + wn * " << LN << " + ln;\n";
+  o << "  const float* pa = g_a + row0 + col0 * " << m << "LL;\n";
+  o << "  const float* px = g_x + col0;\n";
+  o << "  float acc[" << V << "];\n";
+  o << "  #pragma unroll\n  for (int v = 0; v < " << V << "; ++v) acc[v] = 0.0f;\n";
+  o << "  #pragma unroll 1\n  for (long long t = 0; t < " << iters << "LL; t += " << U << ") {\n";
+  o << "    " << ty << " av[" << U << "];\n    float xv[" << U << "];\n";
+  o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; ++u) {\n";
+  o << "      av[u] = " << ld(c.cache, V, "pa + (t + u) * " + std::to_string(G * m) + "LL") << ";\n";
+  o << "      xv[u] = __ldg(px + (t + u) * " << G << "LL);\n";
+  o << "    }\n";
+  o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; ++u) {\n";
+  if (V == 1) o << "      acc[0] = __fmaf_rn(av[u], xv[u], acc[0]);\n";
+  else
+    for (int v = 0; v < V; ++v) o << "      acc[" << v << "] = __fmaf_rn(av[u]" << comp(v) << ", xv[u], acc[" << v << "]);\n";
+  o << "    }\n  }\n";
+  // (1) lanes sharing rows (ln) -> lane ln == 0
+  if (LN > 1) {
+    if (c.xreduce == ISPC_XRED_SHUFFLE) {
+      o << "  #pragma unroll\n  for (int off = " << LM << "; off < 32; off <<= 1) {\n";
+      o << "    #pragma unroll\n    for (int v = 0; v < " << V << "; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);\n";
+      o << "  }\n";
+    } else {
+      o << "  {\n    float* xr = ispc_smem + " << xr_off << ";\n";
+      o << "    #pragma unroll\n    for (int v = 0; v < " << V << "; ++v) xr[tid * " << V << " + v] = acc[v];\n";
+      o << "    __syncwarp();\n";
+      o << "    if (ln == 0) {\n";
+      o << "      for (int q = 1; q < " << LN << "; ++q)\n";
+      o << "        #pragma unroll\n        for (int v = 0; v < " << V << "; ++v) acc[v] += xr[(tid + q * " << LM << ") * " << V << " + v];\n";
+      o << "    }\n  }\n";
+    }
+  }
+  L.static_smem = uint32_t(smem);
+  if (direct) {
+    o << "  if (ln == 0) {\n";
+    if (V == 1) o << "    g_y[row0] = acc[0];\n";
+    else {
+      o << "    *(" << ty << "*)(g_y + row0) = make_" << ty << "(";
+      for (int v = 0; v < V; ++v) o << (v ? ", " : "") << "acc[" << v << "]";
+      o << ");\n";
+    }
+    o << "  }\n}\n";
+  } else {
+    // (2) warps sharing rows (wn), ascending wn
+    o << "  float* part = ispc_smem + " << part_off << ";\n";
+    o << "  if (ln == 0) {\n";
+    o << "    #pragma unroll\n    for (int v = 0; v < " << V << "; ++v) part[wn * " << R << " + (wm * " << LM
+      << " + lm) * " << V << " + v] = acc[v];\n  }\n";
+    o << "  __syncthreads();\n";
+    o << "  float* csum = ispc_smem + " << cl_off << ";\n";
+    o << "  for (int r = tid; r < " << R << "; r += " << T << ") {\n";
+    o << "    float s = part[r];\n";
+    o << "    for (int w = 1; w < " << WN << "; ++w) s += part[w * " << R << " + r];\n";
+    if (S == 1) o << "    g_y[rblk * " << R << "LL + r] = s;\n";
+    else o << "    csum[r] = s;\n";
+    o << "  }\n";
+    if (S > 1) {
+      // (3) CTAs of the cluster, ascending rank, through distributed shared memory
+      o << "  ispc_cluster_sync();\n";
+      o << "  for (int r = tid; r < " << R << "; r += " << T << ") {\n";
+      o << "    if (r % " << S << " != rank) continue;\n";
+      o << "    float s = 0.0f;\n";
+      o << "    #pragma unroll\n    for (int q = 0; q < " << S << "; ++q) s += ispc_dsmem_ld(csum + r, q);\n";
+      o << "    g_y[rblk * " << R << "LL + r] = s;\n";
+      o << "  }\n";
+      o << "  ispc_cluster_sync();\n";
+      L.cluster[0] = uint32_t(S);
+      L.cluster[1] = L.cluster[2] = 1;
+    }
+    o << "}\n";
+  }
+  L.grid_x = uint64_t(m / R * S);
+  L.block[0] = uint32_t(T);
+  L.block[1] = L.block[2] = 1;
+  add_region(L, "a", m * n);
+  add_region(L, "x", n);
+  add_region(L, "y", m);
+  L.params[2].is_input = 1;
+  L.reg_elems = uint32_t(V * (U + 1) + U);
+  return o.str();
+}
+
+// ---------------------------------------------------------------- sgemm (FFMA)
+// C = A B, column-major: A[i + k*M], B[k + j*K], C[i + j*M]. CTA tile
+// BM x BN = (thr_m*tm) x (thr_n*tn); thread (tx, ty) owns rows
+// bm*BM + tx*tm .. +tm and columns bn*BN + ty*tn .. +tn. Shared tiles per
+// stage: As[bk][BM] (m contiguous) and Bs[BN][bk+4] (k contiguous), both
+// filled with contiguous global chunks (no transposes), read as float4
+// along m (A) and along k (B: four k steps at once).
+struct GemmShape {
+  int TX, TY, TM, TN, BK, S, V, T;
+  int64_t BM, BN, ldb;  // ldb: Bs row pitch
+  int64_t a_tile, b_tile, stage_floats;
+};
+
+GemmShape gemm_shape(const ispc_tile_config& c, int64_t M, int64_t N, int64_t K) {
+  GemmShape g{};
+  g.TX = c.thr_m, g.TY = c.thr_n, g.TM = c.tm, g.TN = c.tn, g.BK = c.bk, g.V = c.vec;
+  g.S = std::max(1, c.stages);
+  if (g.TX < 1 || g.TY < 1 || g.TM < 1 || g.TN < 1 || g.BK < 1) illegal("non-positive tile parameter");
+  if (!(g.V == 1 || g.V == 2 || g.V == 4)) illegal("vector width must be 1, 2 or 4");
+  g.T = g.TX * g.TY;
+  if (g.T > 1024) illegal("more than 1024 threads per CTA");
+  g.BM = int64_t(g.TX) * g.TM;
+  g.BN = int64_t(g.TY) * g.TN;
+  if (M % g.BM || N % g.BN) illegal("CTA tile does not divide the output");
+  if (K % g.BK) illegal("k depth does not divide K");
+  if (g.BK % 4 && g.BK != 1 && g.BK != 2) illegal("k depth must be 1, 2 or a multiple of 4");
+  if (g.BM % g.V || g.BK % g.V) illegal("vector width does not divide the staged tiles");
+  if (int64_t(g.TM) * g.TN > 256) illegal("more than 256 accumulators per thread");
+  g.ldb = g.BK + (g.BK >= 4 ? 4 : 0);
+  g.a_tile = int64_t(g.BK) * g.BM;
+  g.b_tile = g.BN * g.ldb;
+  g.stage_floats = g.a_tile + g.b_tile;
+  if (g.stage_floats * g.S * 4 > 232448) illegal("shared-memory ring exceeds 227 KiB");
+  return g;
+}
+
+// Per-thread compute on one staged k tile: As (m contiguous), Bs (k contiguous).
+void gemm_compute(std::ostringstream& o, const GemmShape& g, const std::string& As, const std::string& Bs,
+                  const std::string& indent) {
+  const int KG = g.BK >= 4 ? 4 : g.BK;  // k steps read at once from Bs
+  const int AV = g.TM % 4 == 0 ? 4 : g.TM % 2 == 0 ? 2 : 1;
+  o << indent << "#pragma unroll\n" << indent << "for (int kq = 0; kq < " << g.BK << "; kq += " << KG << ") {\n";
+  o << indent << "  float ra[" << KG << "][" << g.TM << "], rb[" << g.TN << "][" << KG << "];\n";
+  o << indent << "  #pragma unroll\n" << indent << "  for (int q = 0; q < " << KG << "; ++q) {\n";
+  o << indent << "    #pragma unroll\n" << indent << "    for (int i = 0; i < " << g.TM << "; i += " << AV << ") {\n";
+  if (AV == 4)
+    o << indent << "      float4 t = *(const float4*)(" << As << " + (kq + q) * " << g.BM << " + tx * " << g.TM
+      << " + i);\n"
+      << indent << "      ra[q][i] = t.x; ra[q][i + 1] = t.y; ra[q][i + 2] = t.z; ra[q][i + 3] = t.w;\n";
+  else if (AV == 2)
+    o << indent << "      float2 t = *(const float2*)(" << As << " + (kq + q) * " << g.BM << " + tx * " << g.TM
+      << " + i);\n"
+      << indent << "      ra[q][i] = t.x; ra[q][i + 1] = t.y;\n";
+  else
+    o << indent << "      ra[q][i] = " << As << "[(kq + q) * " << g.BM << " + tx * " << g.TM << " + i];\n";
+  o << indent << "    }\n" << indent << "  }\n";
+  o << indent << "  #pragma unroll\n" << indent << "  for (int j = 0; j < " << g.TN << "; ++j) {\n";
+  if (KG == 4)
+    o << indent << "    float4 t = *(const float4*)(" << Bs << " + (ty * " << g.TN << " + j) * " << g.ldb
+      << " + kq);\n"
+      << indent << "    rb[j][0] = t.x; rb[j][1] = t.y; rb[j][2] = t.z; rb[j][3] = t.w;\n";
+  else
+    o << indent << "    #pragma unroll\n" << indent << "    for (int q = 0; q < " << KG << "; ++q) rb[j][q] = "
+      << Bs << "[(ty * " << g.TN << " + j) * " << g.ldb << " + kq + q];\n";
+  o << indent << "  }\n";
+  o << indent << "  #pragma unroll\n" << indent << "  for (int q = 0; q < " << KG << "; ++q)\n";
+  o << indent << "    #pragma unroll\n" << indent << "    for (int j = 0; j < " << g.TN << "; ++j)\n";
+  o << indent << "      #pragma unroll\n" << indent << "      for (int i = 0; i < " << g.TM << "; ++i)\n";
+  o << indent << "        acc[j][i] = __fmaf_rn(ra[q][i], rb[j][q], acc[j][i]);\n";
+  o << indent << "}\n";
+}
+
+// Issues the copies of k tile `kt` into stage buffer `buf` (cp.async) or
+// loads it into registers / stores it (SHARED).
+void gemm_copy_cp_async(std::ostringstream& o, const GemmShape& g, const ispc_tile_config& c, int64_t M, int64_t K,
+                        const std::string& pa, const std::string& pb, const std::string& kt, const std::string& buf,
+                        const std::string& indent) {
+  const int V = g.V;
+  const std::string cp = V == 4 ? (c.cache == ISPC_CACHE_L1 ? "ispc_cp_async_ca16" : "ispc_cp_async_cg16")
+                                : V == 2 ? "ispc_cp_async_ca8" : "ispc_cp_async_ca4";
+  const int64_t a_chunks = g.a_tile / V, b_chunks = int64_t(g.BN) * g.BK / V;
+  o << indent << "{\n";
+  o << indent << "  float* sA = ispc_smem + (" << buf << ") * " << g.stage_floats << ";\n";
+  o << indent << "  float* sB = sA + " << g.a_tile << ";\n";
+  o << indent << "  const long long k0 = (long long)(" << kt << ") * " << g.BK << ";\n";
+  o << indent << "  #pragma unroll\n" << indent << "  for (int ch = tid; ch < " << a_chunks << "; ch += " << g.T << ") {\n";
+  o << indent << "    const int kk = ch / " << g.BM / V << ", mm = (ch % " << g.BM / V << ") * " << V << ";\n";
+  o << indent << "    " << cp << "(sA + kk * " << g.BM << " + mm, " << pa << " + mm + (k0 + kk) * " << M << "LL);\n";
+  o << indent << "  }\n";
+  o << indent << "  #pragma unroll\n" << indent << "  for (int ch = tid; ch < " << b_chunks << "; ch += " << g.T << ") {\n";
+  o << indent << "    const int nn = ch / " << g.BK / V << ", kk = (ch % " << g.BK / V << ") * " << V << ";\n";
+  o << indent << "    " << cp << "(sB + nn * " << g.ldb << " + kk, " << pb << " + k0 + kk + (long long)nn * " << K
+    << "LL);\n";
+  o << indent << "  }\n";
+  o << indent << "}\n";
+}
+
+std::string sgemm(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
+  const int64_t M = c.m, N = c.n, K = c.k;
+  GemmShape g = gemm_shape(c, M, N, K);
+  if (c.staging != ISPC_STAGE_SHARED && c.staging != ISPC_STAGE_CP_ASYNC)
+    illegal("FFMA sgemm stages operands through shared memory (SHARED or CP_ASYNC)");
+  if (c.staging == ISPC_STAGE_SHARED && g.S > 2) illegal("SHARED staging is single or double buffered");
+  const int64_t KT = K / g.BK;
+  const int V = g.V;
+  const std::string vty = V == 4 ? "float4" : V == 2 ? "float2" : "float";
+  std::ostringstream o;
+  o << "extern \"C\" __global__ void __launch_bounds__(" << g.T << ") " << fn
+    << "(const float* __restrict__ g_a, const float* __restrict__ g_b, float* __restrict__ g_c) {\n";
+  o << "  extern __shared__ __align__(16) float ispc_smem[];\n";
+  o << "  const int tid = threadIdx.x, tx = tid % " << g.TX << ", ty = tid / " << g.TX << ";\n";
+  o << "  const long long bm = blockIdx.x % " << M / g.BM << ", bn = blockIdx.x / " << M / g.BM << ";\n";
+  o << "  const float* pa = g_a + bm * " << g.BM << "LL;\n";
+  o << "  const float* pb = g_b + bn * " << g.BN << "LL * " << K << "LL;\n";
+  o << "  float acc[" << g.TN << "][" << g.TM << "];\n";
+  o << "  #pragma unroll\n  for (int j = 0; j < " << g.TN << "; ++j)\n    #pragma unroll\n    for (int i = 0; i < "
+    << g.TM << "; ++i) acc[j][i] = 0.0f;\n";
+  if (c.staging == ISPC_STAGE_CP_ASYNC) {
+    const int S = g.S;
+    if (S == 1) {
+      o << "  #pragma unroll 1\n  for (int kt = 0; kt < " << KT << "; ++kt) {\n";
+      gemm_copy_cp_async(o, g, c, M, K, "pa", "pb", "kt", "0", "    ");
+      o << "    ispc_cp_async_commit();\n    ispc_cp_async_wait<0>();\n    __syncthreads();\n";
+      gemm_compute(o, g, "ispc_smem", "(ispc_smem + " + std::to_string(g.a_tile) + ")", "    ");
+      o << "    __syncthreads();\n  }\n";
+    } else {
+      o << "  #pragma unroll\n  for (int s = 0; s < " << S - 1 << "; ++s) {\n";
+      o << "    if (s < " << KT << ") {\n";
+      gemm_copy_cp_async(o, g, c, M, K, "pa", "pb", "s", "s", "      ");
+      o << "    }\n    ispc_cp_async_commit();\n  }\n";
+      o << "  #pragma unroll 1\n  for (int kt = 0; kt < " << KT << "; ++kt) {\n";
+      o << "    ispc_cp_async_wait<" << S - 2 << ">();\n    __syncthreads();\n";
+      o << "    {\n      const int nk = kt + " << S - 1 << ";\n      if (nk < " << KT << ") {\n";
+      gemm_copy_cp_async(o, g, c, M, K, "pa", "pb", "nk", "nk % " + std::to_string(S), "        ");
+      o << "      }\n      ispc_cp_async_commit();\n    }\n";
+      o << "    const float* sA = ispc_smem + (kt % " << S << ") * " << g.stage_floats << ";\n";
+      gemm_compute(o, g, "sA", "(sA + " + std::to_string(g.a_tile) + ")", "    ");
+      o << "  }\n";
+      o << "  ispc_cp_async_wait<0>();\n";
+    }
+  } else {
+    // SHARED: global -> registers -> shared; stages 2 prefetches tile kt+1
+    // into registers while tile kt is computed
+    const int64_t a_chunks = g.a_tile / V, b_chunks = int64_t(g.BN) * g.BK / V;
+    const int64_t ra_n = (a_chunks + g.T - 1) / g.T, rb_n = (b_chunks + g.T - 1) / g.T;
+    auto load_regs = [&](const std::string& kt, const std::string& ind) {
+      o << ind << "{\n" << ind << "  const long long k0 = (long long)(" << kt << ") * " << g.BK << ";\n";
+      o << ind << "  #pragma unroll\n" << ind << "  for (int r = 0; r < " << ra_n << "; ++r) {\n";
+      o << ind << "    const int ch = tid + r * " << g.T << ";\n";
+      o << ind << "    if (ch < " << a_chunks << ") {\n";
+      o << ind << "      const int kk = ch / " << g.BM / V << ", mm = (ch % " << g.BM / V << ") * " << V << ";\n";
+      o << ind << "      pfa[r] = " << ld(c.cache, V, "pa + mm + (k0 + kk) * " + std::to_string(M) + "LL") << ";\n";
+      o << ind << "    }\n" << ind << "  }\n";
+      o << ind << "  #pragma unroll\n" << ind << "  for (int r = 0; r < " << rb_n << "; ++r) {\n";
+      o << ind << "    const int ch = tid + r * " << g.T << ";\n";
+      o << ind << "    if (ch < " << b_chunks << ") {\n";
+      o << ind << "      const int nn = ch / " << g.BK / V << ", kk = (ch % " << g.BK / V << ") * " << V << ";\n";
+      o << ind << "      pfb[r] = " << ld(c.cache, V, "pb + k0 + kk + (long long)nn * " + std::to_string(K) + "LL")
+        << ";\n";
+      o << ind << "    }\n" << ind << "  }\n" << ind << "}\n";
+    };
+    auto store_regs = [&](const std::string& buf, const std::string& ind) {
+      o << ind << "{\n" << ind << "  float* sA = ispc_smem + (" << buf << ") * " << g.stage_floats << ";\n";
+      o << ind << "  float* sB = sA + " << g.a_tile << ";\n";
+      o << ind << "  #pragma unroll\n" << ind << "  for (int r = 0; r < " << ra_n << "; ++r) {\n";
+      o << ind << "    const int ch = tid + r * " << g.T << ";\n";
+      o << ind << "    if (ch < " << a_chunks << ") {\n";
+      o << ind << "      const int kk = ch / " << g.BM / V << ", mm = (ch % " << g.BM / V << ") * " << V << ";\n";
+      o << ind << "      *(" << vty << "*)(sA + kk * " << g.BM << " + mm) = pfa[r];\n";
+      o << ind << "    }\n" << ind << "  }\n";
+      o << ind << "  #pragma unroll\n" << ind << "  for (int r = 0; r < " << rb_n << "; ++r) {\n";
+      o << ind << "    const int ch = tid + r * " << g.T << ";\n";
+      o << ind << "    if (ch < " << b_chunks << ") {\n";
+      o << ind << "      const int nn = ch / " << g.BK / V << ", kk = (ch % " << g.BK / V << ") * " << V << ";\n";
+      o << ind << "      *(" << vty << "*)(sB + nn * " << g.ldb << " + kk) = pfb[r];\n";
+      o << ind << "    }\n" << ind << "  }\n" << ind << "}\n";
+    };
+    o << "  " << vty << " pfa[" << ra_n << "], pfb[" << rb_n << "];\n";
+    if (g.S == 1) {
+      o << "  #pragma unroll 1\n  for (int kt = 0; kt < " << KT << "; ++kt) {\n";
+      load_regs("kt", "    ");
+      store_regs("0", "    ");
+      o << "    __syncthreads();\n";
+      gemm_compute(o, g, "ispc_smem", "(ispc_smem + " + std::to_string(g.a_tile) + ")", "    ");
+      o << "    __syncthreads();\n  }\n";
+    } else {
+      load_regs("0", "  ");
+      store_regs("0", "  ");
+      o << "  __syncthreads();\n";
+      o << "  #pragma unroll 1\n  for (int kt = 0; kt < " << KT << "; ++kt) {\n";
+      o << "    if (kt + 1 < " << KT << ") {\n";
+      load_regs("kt + 1", "      ");
+      o << "    }\n";
+      o << "    const float* sA = ispc_smem + (kt & 1) * " << g.stage_floats << ";\n";
+      gemm_compute(o, g, "sA", "(sA + " + std::to_string(g.a_tile) + ")", "    ");
+      o << "    if (kt + 1 < " << KT << ") {\n";
+      store_regs("(kt + 1) & 1", "      ");
+      o << "    }\n    __syncthreads();\n  }\n";
+    }
+  }
+  // epilogue: C[i + j*M], vectors along m
+  const int EV = g.TM % 4 == 0 ? 4 : g.TM % 2 == 0 ? 2 : 1;
+  const std::string ety = EV == 4 ? "float4" : EV == 2 ? "float2" : "float";
+  o << "  float* pc = g_c + (bm * " << g.BM << "LL + tx * " << g.TM << ") + (bn * " << g.BN << "LL + ty * " << g.TN
+    << ") * " << M << "LL;\n";
+  o << "  #pragma unroll\n  for (int j = 0; j < " << g.TN << "; ++j)\n";
+  o << "    #pragma unroll\n    for (int i = 0; i < " << g.TM << "; i += " << EV << ")\n";
+  if (EV == 1) o << "      pc[i + j * " << M << "LL] = acc[j][i];\n";
+  else {
+    o << "      *(" << ety << "*)(pc + i + j * " << M << "LL) = make_" << ety << "(";
+    for (int e = 0; e < EV; ++e) o << (e ? ", " : "") << "acc[j][i + " << e << "]";
+    o << ");\n";
+  }
+  o << "}\n";
+  L.grid_x = uint64_t(M / g.BM * (N / g.BN));
+  L.block[0] = uint32_t(g.T);
+  L.block[1] = L.block[2] = 1;
+  L.static_smem = uint32_t(g.stage_floats * g.S * 4);
+  add_region(L, "a", M * K);
+  add_region(L, "b", K * N);
+  add_region(L, "c", M * N);
+  L.reg_elems = uint32_t(g.TM * g.TN);
+  return o.str();
+}
+
+// ---------------------------------------------------------------- batched sgemm
+// batch x (C_b = A_b B_b), each column-major and densely packed:
+// A_b = a + b*M*K, B_b = b + b*K*N, C_b = c + b*M*N. A CTA holds `per_cta`
+// problems; each problem gets (M/tm)*(N/tn) threads owning a tm x tn output
+// tile. DIRECT reads operands from global (L1); SHARED stages bk-deep slices
+// of every problem's A and B cooperatively. k ascending per output (bit-exact).
+std::string batched(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
+  const int64_t M = c.m, N = c.n, K = c.k, B = c.batch;
+  const int P = c.per_cta, TM = c.tm, TN = c.tn, BK = c.bk;
+  if (P < 1 || TM < 1 || TN < 1 || BK < 1) illegal("non-positive tile parameter");
+  if (M % TM || N % TN) illegal("thread tile does not divide the problem");
+  if (B % P) illegal("problems per CTA do not divide the batch");
+  if (K % BK) illegal("k depth does not divide K");
+  const int64_t TPX = M / TM, TPY = N / TN, TP = TPX * TPY, T = TP * P;
+  if (T > 1024) illegal("more than 1024 threads per CTA");
+  if (T < 32) illegal("fewer than 32 threads per CTA");
+  if (int64_t(TM) * TN > 64) illegal("more than 64 accumulators per thread");
+  const bool sh = c.staging == ISPC_STAGE_SHARED;
+  if (!sh && c.staging != ISPC_STAGE_DIRECT) illegal("batched stages through registers or shared memory");
+  const int64_t ldb = BK + (BK % 4 == 0 ? 4 : 1);
+  const int64_t per_prob = BK * M + N * ldb;  // floats per problem slice
+  const int64_t smem = sh ? per_prob * P * 4 : 0;
+  if (smem > 232448) illegal("shared memory exceeds 227 KiB");
+  const int V = c.vec;
+  if (!(V == 1 || V == 2 || V == 4)) illegal("vector width must be 1, 2 or 4");
+  if (sh && (M % V || BK % V)) illegal("vector width does not divide the staged slices");
+  std::ostringstream o;
+  o << "extern \"C\" __global__ void __launch_bounds__(" << T << ") " << fn
+    << "(const float* __restrict__ g_a, const float* __restrict__ g_b, float* __restrict__ g_c) {\n";
+  o << "  extern __shared__ __align__(16) float ispc_smem[];\n";
+  o << "  const int tid = threadIdx.x, p = tid / " << TP << ", lt = tid % " << TP << ";\n";
+  o << "  const int tx = lt % " << TPX << ", ty = lt / " << TPX << ";\n";
+  o << "  const long long prob = (long long)blockIdx.x * " << P << " + p;\n";
+  o << "  const float* pa = g_a + prob * " << M * K << "LL;\n";
+  o << "  const float* pb = g_b + prob * " << K * N << "LL;\n";
+  o << "  float acc[" << TN << "][" << TM << "];\n";
+  o << "  #pragma unroll\n  for (int j = 0; j < " << TN << "; ++j)\n    #pragma unroll\n    for (int i = 0; i < " << TM
+    << "; ++i) acc[j][i] = 0.0f;\n";
+  o << "  #pragma unroll 1\n  for (int k0 = 0; k0 < " << K << "; k0 += " << BK << ") {\n";
+  if (sh) {
+    const std::string vty = V == 4 ? "float4" : V == 2 ? "float2" : "float";
+    o << "    __syncthreads();\n";
+    // every thread of the CTA copies chunks of all problems' slices
+    const int64_t a_ch = BK * M / V, b_ch = N * BK / V;
+    o << "    for (int ch = tid; ch < " << P * (a_ch + b_ch) << "; ch += " << T << ") {\n";
+    o << "      const int q = ch / " << a_ch + b_ch << ", r = ch % " << a_ch + b_ch << ";\n";
+    o << "      const long long qb = (long long)blockIdx.x * " << P << " + q;\n";
+    o << "      float* s = ispc_smem + q * " << per_prob << ";\n";
+    o << "      if (r < " << a_ch << ") {\n";
+    o << "        const int kk = r / " << M / V << ", mm = (r % " << M / V << ") * " << V << ";\n";
+    o << "        *(" << vty << "*)(s + kk * " << M << " + mm) = "
+      << ld(c.cache, V, "g_a + qb * " + std::to_string(M * K) + "LL + mm + (k0 + kk) * " + std::to_string(M) + "LL")
+      << ";\n";
+    o << "      } else {\n        const int r2 = r - " << a_ch << ";\n";
+    o << "        const int nn = r2 / " << BK / V << ", kk = (r2 % " << BK / V << ") * " << V << ";\n";
+    o << "        " << vty << " v = "
+      << ld(c.cache, V, "g_b + qb * " + std::to_string(K * N) + "LL + k0 + kk + (long long)nn * " + std::to_string(K) + "LL")
+      << ";\n";
+    if (V == 1) o << "        s[" << BK * M << " + nn * " << ldb << " + kk] = v;\n";
+    else
+      for (int e = 0; e < V; ++e)
+        o << "        s[" << BK * M << " + nn * " << ldb << " + kk + " << e << "] = v" << comp(e) << ";\n";
+    o << "      }\n    }\n    __syncthreads();\n";
+    o << "    const float* sa = ispc_smem + p * " << per_prob << ";\n";
+    o << "    const float* sb = sa + " << BK * M << ";\n";
+    o << "    #pragma unroll\n    for (int kk = 0; kk < " << BK << "; ++kk) {\n";
+    o << "      float ra[" << TM << "], rb[" << TN << "];\n";
+    o << "      #pragma unroll\n      for (int i = 0; i < " << TM << "; ++i) ra[i] = sa[kk * " << M << " + tx * " << TM
+      << " + i];\n";
+    o << "      #pragma unroll\n      for (int j = 0; j < " << TN << "; ++j) rb[j] = sb[(ty * " << TN << " + j) * "
+      << ldb << " + kk];\n";
+  } else {
+    o << "    #pragma unroll\n    for (int kk = 0; kk < " << BK << "; ++kk) {\n";
+    o << "      float ra[" << TM << "], rb[" << TN << "];\n";
+    o << "      #pragma unroll\n      for (int i = 0; i < " << TM << "; ++i) ra[i] = "
+      << ld(c.cache, 1, "pa + tx * " + std::to_string(TM) + " + i + (k0 + kk) * " + std::to_string(M) + "LL") << ";\n";
+    o << "      #pragma unroll\n      for (int j = 0; j < " << TN << "; ++j) rb[j] = "
+      << ld(c.cache, 1, "pb + k0 + kk + (long long)(ty * " + std::to_string(TN) + " + j) * " + std::to_string(K) + "LL")
+      << ";\n";
+  }
+  o << "      #pragma unroll\n      for (int j = 0; j < " << TN << "; ++j)\n";
+  o << "        #pragma unroll\n        for (int i = 0; i < " << TM << "; ++i) acc[j][i] = __fmaf_rn(ra[i], rb[j], acc[j][i]);\n";
+  o << "    }\n  }\n";
+  o << "  float* pc = g_c + prob * " << M * N << "LL + tx * " << TM << " + (long long)(ty * " << TN << ") * " << M << "LL;\n";
+  o << "  #pragma unroll\n  for (int j = 0; j < " << TN << "; ++j)\n";
+  o << "    #pragma unroll\n    for (int i = 0; i < " << TM << "; ++i) pc[i + j * " << M << "] = acc[j][i];\n";
+  o << "}\n";
+  L.grid_x = uint64_t(B / P);
+  L.block[0] = uint32_t(T);
+  L.block[1] = L.block[2] = 1;
+  L.static_smem = uint32_t(smem);
+  add_region(L, "a", B * M * K);
+  add_region(L, "b", B * K * N);
+  add_region(L, "c", B * M * N);
+  L.reg_elems = uint32_t(TM * TN);
+  return o.str();
+}
+
+}  // namespace
+
+std::string emit_tile_kernel(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
+  std::memset(&L, 0, sizeof(L));
+  std::snprintf(L.name, sizeof(L.name), "%s", fn.c_str());
+  if (c.m <= 0 || c.n <= 0 || (c.kind != ISPC_TILE_GEMV && c.k <= 0)) illegal("empty problem");
+  std::string src;
+  switch (c.kind) {
+    case ISPC_TILE_GEMV: src = gemv(c, fn, L); break;
+    case ISPC_TILE_SGEMM: src = sgemm(c, fn, L); break;
+    case ISPC_TILE_BATCHED: src = batched(c, fn, L); break;
+    case ISPC_TILE_SGEMM_TC: src = emit_tcgen05_kernel(c, fn, L); break;
+    default: throw NestError(ISPC_E_ARG, "unknown tile kind");
+  }
+  if (L.static_smem > 232448) illegal("shared memory exceeds 227 KiB");
+  L.source_hash = fnv1a(src);
+  return src;
+}
+
+}  // namespace ispc
+
+extern "C" int ispc_emit_tiles(const ispc_tile_config* cfg, const char* fn_name, char* buf, size_t cap,
+                               size_t* len, ispc_launch* launch) {
+  try {
+    if (!cfg || !launch) throw ispc::NestError(ISPC_E_ARG, "null argument");
+    std::string fn = fn_name ? fn_name : "ispc_tile_kernel";
+    std::string src = ispc::emit_tile_kernel(*cfg, fn, *launch);
+    if (!fn_name) {
+      char name[64];
+      std::snprintf(name, sizeof(name), "ispc_t%016llx", (unsigned long long)launch->source_hash);
+      size_t p = 0;
+      while ((p = src.find(fn, p)) != std::string::npos) {
+        src.replace(p, fn.size(), name);
+        p += std::strlen(name);
+      }
+      std::snprintf(launch->name, sizeof(launch->name), "%s", name);
+    }
+    if (len) *len = src.size();
+    if (buf && cap) {
+      size_t k = src.size() < cap - 1 ? src.size() : cap - 1;
+      std::memcpy(buf, src.data(), k);
+      buf[k] = 0;
+    }
+    return ISPC_OK;
+  } catch (const ispc::NestError& e) {
+    ispc::set_thread_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    ispc::set_thread_error(e.what());
+    return ISPC_E_ARG;
+  }
+}

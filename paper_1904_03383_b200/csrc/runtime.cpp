@@ -62,6 +62,8 @@ struct DriverTable {
   decltype(&::cuModuleLoadData) ModuleLoadData = nullptr;
   decltype(&::cuModuleUnload) ModuleUnload = nullptr;
   decltype(&::cuMemsetD32Async) MemsetD32Async = nullptr;
+  decltype(&::cuLaunchKernelEx) LaunchKernelEx = nullptr;
+  decltype(&::cuTensorMapEncodeTiled) TensorMapEncodeTiled = nullptr;
 };
 DriverTable drv;
 
@@ -90,6 +92,8 @@ bool resolve_driver(std::string& why) {
     get("cuModuleLoadData", reinterpret_cast<void**>(&drv.ModuleLoadData));
     get("cuModuleUnload", reinterpret_cast<void**>(&drv.ModuleUnload));
     get("cuMemsetD32Async", reinterpret_cast<void**>(&drv.MemsetD32Async));
+    get("cuLaunchKernelEx", reinterpret_cast<void**>(&drv.LaunchKernelEx));
+    get("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&drv.TensorMapEncodeTiled));
   });
   if (!ok) why = "CUDA driver entry points unavailable: " + err;
   return ok;
@@ -122,6 +126,7 @@ struct ispc_dev {
   bool bound = false;
   std::map<std::string, Buffer> regions;  // inputs and outputs by name
   std::map<std::string, Buffer> expected;  // golden outputs by name
+  std::map<std::string, Buffer> scale;     // golden sum of |products| per output element (reductions)
   std::vector<std::string> outputs;
   std::vector<Buffer> scratch;
 
@@ -197,9 +202,11 @@ int alloc(ispc_dev* d, Buffer& b, int64_t elems) {
 void free_problem(ispc_dev* d) {
   for (auto& [k, b] : d->regions) cudaFree(b.ptr);
   for (auto& [k, b] : d->expected) cudaFree(b.ptr);
+  for (auto& [k, b] : d->scale) cudaFree(b.ptr);
   for (auto& b : d->scratch) cudaFree(b.ptr);
   d->regions.clear();
   d->expected.clear();
+  d->scale.clear();
   d->scratch.clear();
   d->outputs.clear();
   d->bound = false;
@@ -229,15 +236,16 @@ int recompute_expected(ispc_dev* d) {
   const int64_t batch = std::max<int64_t>(p->batch, 1);
   auto R_ = [&](const char* nm) { return d->regions.at(nm).ptr; };
   auto E_ = [&](const char* nm) { return d->expected.at(nm).ptr; };
+  auto S_ = [&](const char* nm) { return d->scale.count(nm) ? d->scale.at(nm).ptr : nullptr; };
   switch (p->kind) {
     case ISPC_PROB_AXPY: CK(d, ispc::launch_axpy_golden(R_("x"), R_("y"), E_("z"), n, p->alpha, d->stream)); break;
     case ISPC_PROB_OUTER: CK(d, ispc::launch_outer_golden(R_("a"), R_("b"), E_("c"), m, n, d->stream)); break;
     case ISPC_PROB_MATMUL:
-      CK(d, ispc::launch_matmul_golden(R_("a"), R_("b"), E_("c"), m, n, k, s, 1, d->stream));
+      CK(d, ispc::launch_matmul_golden(R_("a"), R_("b"), E_("c"), m, n, k, s, 1, S_("c"), d->stream));
       break;
-    case ISPC_PROB_GEMV: CK(d, ispc::launch_gemv_golden(R_("a"), R_("x"), E_("y"), m, n, d->stream)); break;
+    case ISPC_PROB_GEMV: CK(d, ispc::launch_gemv_golden(R_("a"), R_("x"), E_("y"), m, n, S_("y"), d->stream)); break;
     case ISPC_PROB_BATCHED:
-      CK(d, ispc::launch_matmul_golden(R_("a"), R_("b"), E_("c"), m, n, k, 1, batch, d->stream));
+      CK(d, ispc::launch_matmul_golden(R_("a"), R_("b"), E_("c"), m, n, k, 1, batch, S_("c"), d->stream));
       break;
   }
   CK(d, cudaStreamSynchronize(d->stream));
@@ -343,6 +351,11 @@ int ispc_bind_problem(ispc_dev* d, const ispc_problem* p) {
       if ((rc = alloc(d, e, r.elems))) return rc;
       d->expected[r.name] = e;
       d->outputs.push_back(r.name);
+      if (p->kind == ISPC_PROB_MATMUL || p->kind == ISPC_PROB_GEMV || p->kind == ISPC_PROB_BATCHED) {
+        Buffer sc;
+        if ((rc = alloc(d, sc, r.elems))) return rc;
+        d->scale[r.name] = sc;
+      }
     }
   }
   d->bound = true;
@@ -479,7 +492,9 @@ int ispc_check(ispc_dev* d, double rtol, int bit_exact, double* max_err, int64_t
     CK(d, cudaMemsetAsync(d->cmp_res, 0, sizeof(ispc::CmpResult), d->stream));
     const Buffer& out = d->regions.at(o);
     const Buffer& exp = d->expected.at(o);
-    CK(d, ispc::launch_compare(out.ptr, exp.ptr, out.elems, bit_exact, float(rtol), d->cmp_res, d->stream));
+    auto sc = d->scale.find(o);
+    const float* scale = (!bit_exact && sc != d->scale.end()) ? sc->second.ptr : nullptr;
+    CK(d, ispc::launch_compare(out.ptr, exp.ptr, scale, out.elems, bit_exact, float(rtol), d->cmp_res, d->stream));
     ispc::CmpResult h{};
     CK(d, cudaMemcpyAsync(&h, d->cmp_res, sizeof(h), cudaMemcpyDeviceToHost, d->stream));
     CK(d, cudaStreamSynchronize(d->stream));
@@ -521,6 +536,7 @@ int ispc_launch_timed(ispc_dev* d, int handle, const ispc_launch* L, const ispc_
   // bind parameters: problem regions by name, temporaries from scratch
   std::vector<uint64_t> store(L->num_params, 0);
   std::vector<void*> args(L->num_params);
+  std::vector<CUtensorMap> tmaps(L->num_tmaps);
   size_t next_scratch = 0;
   int deadline_slot = -1;
   for (uint32_t i = 0; i < L->num_params; ++i) {
@@ -549,18 +565,62 @@ int ispc_launch_timed(ispc_dev* d, int handle, const ispc_launch* L, const ispc_
         return fail(d, ISPC_E_ARG, std::string("unknown scalar input ") + prm.name);
       float a = d->prob.alpha;
       std::memcpy(&store[i], &a, 4);
+    } else if (prm.kind == ISPC_PARAM_TMAP) {
+      const ispc_tmap* tm = nullptr;
+      uint32_t ti = 0;
+      for (; ti < L->num_tmaps && ti < ISPC_MAX_TMAPS; ++ti)
+        if (L->tmaps[ti].param == i) {
+          tm = &L->tmaps[ti];
+          break;
+        }
+      if (!tm) return fail(d, ISPC_E_ARG, "tensor-map parameter without a descriptor");
+      auto it = d->regions.find(tm->region);
+      if (it == d->regions.end())
+        return fail(d, ISPC_E_ARG, std::string("tensor map over unknown region ") + tm->region);
+      if (tm->rank < 2 || tm->rank > 3) return fail(d, ISPC_E_ARG, "tensor map rank");
+      cuuint64_t dims[3] = {tm->dims[0], tm->dims[1], tm->dims[2]};
+      cuuint64_t strides[2] = {tm->strides[0], tm->strides[1]};
+      cuuint32_t box[3] = {tm->box[0], tm->box[1], tm->box[2]};
+      cuuint32_t estr[3] = {1, 1, 1};
+      static const CUtensorMapSwizzle sw[4] = {CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                                               CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_SWIZZLE_128B};
+      CU(d, drv.TensorMapEncodeTiled(&tmaps[ti], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, tm->rank, it->second.ptr, dims,
+                                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw[tm->swizzle & 3],
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+      args[i] = &tmaps[ti];
     } else {
       deadline_slot = int(i);
     }
   }
   const double budget = o->budget_ns > 0 ? o->budget_ns : 2e9;
+  const bool clustered = L->cluster[0] * std::max(1u, L->cluster[1]) * std::max(1u, L->cluster[2]) > 1;
+  if (clustered && L->grid_x % L->cluster[0] != 0) return fail(d, ISPC_E_ILLEGAL, "grid not a multiple of the cluster");
   unsigned int smem = L->static_smem;
   auto launch_once = [&](float* ms, bool flush) -> int {
     if (flush) CK(d, cudaMemsetAsync(d->flush, int(flush_counter_++ & 0xff), d->flush_bytes, d->stream));
     if (deadline_slot >= 0) store[deadline_slot] = uint64_t(host_ns() + d->gt_offset_ns + budget);
     CK(d, cudaEventRecord(d->ev0, d->stream));
-    CU(d, drv.LaunchKernel(fn, unsigned(L->grid_x), 1, 1, L->block[0], L->block[1], L->block[2], smem,
-                         reinterpret_cast<CUstream>(d->stream), args.data(), nullptr));
+    if (clustered) {
+      CUlaunchConfig cfg{};
+      cfg.gridDimX = unsigned(L->grid_x);
+      cfg.gridDimY = cfg.gridDimZ = 1;
+      cfg.blockDimX = L->block[0];
+      cfg.blockDimY = L->block[1];
+      cfg.blockDimZ = L->block[2];
+      cfg.sharedMemBytes = smem;
+      cfg.hStream = reinterpret_cast<CUstream>(d->stream);
+      CUlaunchAttribute attr{};
+      attr.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+      attr.value.clusterDim.x = L->cluster[0];
+      attr.value.clusterDim.y = std::max(1u, L->cluster[1]);
+      attr.value.clusterDim.z = std::max(1u, L->cluster[2]);
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      CU(d, drv.LaunchKernelEx(&cfg, fn, args.data(), nullptr));
+    } else {
+      CU(d, drv.LaunchKernel(fn, unsigned(L->grid_x), 1, 1, L->block[0], L->block[1], L->block[2], smem,
+                             reinterpret_cast<CUstream>(d->stream), args.data(), nullptr));
+    }
     CK(d, cudaEventRecord(d->ev1, d->stream));
     CK(d, cudaEventSynchronize(d->ev1));
     CK(d, cudaEventElapsedTime(ms, d->ev0, d->ev1));
@@ -657,6 +717,28 @@ int ispc_evaluate(ispc_dev* d, const ispc_nest* nest, const ispc_emit_opts* eopt
   std::string src(len + 1, '\0');
   if ((rc = ispc_emit_cuda(nest, eopts, nullptr, src.data(), src.size(), &len, &L)))
     return fail(d, rc, ispc::thread_error());
+  src.resize(len);
+  if (launch) *launch = L;
+  const char* srcs[] = {src.c_str()};
+  ispc_module* m = nullptr;
+  if ((rc = ispc_compile(srcs, 1, nullptr, &m))) return fail(d, rc, ispc::thread_error());
+  std::unique_ptr<ispc_module, void (*)(ispc_module*)> guard(m, ispc_module_free);
+  int h = 0;
+  if ((rc = ispc_module_load(d, m, &h))) return rc;
+  rc = ispc_launch_timed(d, h, &L, topts, res);
+  ispc_module_unload(d, h);
+  return rc;
+}
+
+int ispc_evaluate_tiles(ispc_dev* d, const ispc_tile_config* cfg, const ispc_time_opts* topts,
+                        ispc_time_result* res, ispc_launch* launch) {
+  if (!d || !cfg || !topts || !res) return fail(d, ISPC_E_ARG, "null argument");
+  ispc_launch L{};
+  size_t len = 0;
+  int rc = ispc_emit_tiles(cfg, nullptr, nullptr, 0, &len, &L);
+  if (rc) return fail(d, rc, ispc::thread_error());
+  std::string src(len + 1, '\0');
+  if ((rc = ispc_emit_tiles(cfg, nullptr, src.data(), src.size(), &len, &L))) return fail(d, rc, ispc::thread_error());
   src.resize(len);
   if (launch) *launch = L;
   const char* srcs[] = {src.c_str()};

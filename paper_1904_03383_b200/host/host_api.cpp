@@ -95,9 +95,15 @@ int ispc_space_create(const ispc_kernel_spec* spec, ispc_space** out) {
       if (spec->factor_len[i] <= 0 || spec->factor_len[i] > 32) return set_err(ISPC_E_ARG, "bad factor list");
       ks.factors.emplace_back(spec->factors[i], spec->factors[i] + spec->factor_len[i]);
     }
-    s->kernel = ispace::build_kernel(ks);
-    s->mp = machine_for(spec->mode);
-    ispace::BuildResult br = ispace::build_gpu_space(s->kernel, s->mp);
+    ispace::BuildResult br;
+    if (is_tile_kind(s->kind)) {
+      s->tiles = std::make_unique<TileFamily>(make_family(s->kind, spec->m, spec->n, spec->k, spec->batch));
+      br = build_tile_space(*s->tiles);
+    } else {
+      s->kernel = ispace::build_kernel(ks);
+      s->mp = machine_for(spec->mode);
+      br = ispace::build_gpu_space(s->kernel, s->mp);
+    }
     if (!br.ctx) {
       std::string msg = "space build failed";
       for (const auto& d : br.diagnostics) msg += "\n" + d.message;
@@ -149,7 +155,12 @@ int ispc_space_problem(const ispc_space* s, ispc_problem* p) {
   p->batch = 1;
   if (k == "axpy") p->kind = ISPC_PROB_AXPY;
   else if (k == "outer_product") p->kind = ISPC_PROB_OUTER;
-  else if (k == "matmul") p->kind = ISPC_PROB_MATMUL;
+  else if (k == "matmul" || k == "sgemm" || k == "sgemm_tc") p->kind = ISPC_PROB_MATMUL;
+  else if (k == "gemv") p->kind = ISPC_PROB_GEMV;
+  else if (k == "batched") {
+    p->kind = ISPC_PROB_BATCHED;
+    p->batch = s->spec.batch;
+  }
   else return set_err(ISPC_E_ARG, "no problem for kernel kind " + k);
   return ISPC_OK;
 }
@@ -241,9 +252,21 @@ int64_t ispc_count_leaves(const ispc_space* s, const ispc_cand* from, int64_t ca
   return n;
 }
 
+int ispc_cand_to_tiles(const ispc_space* s, const ispc_cand* c, ispc_tile_config* out) {
+  try {
+    if (!s || !c || !out) return set_err(ISPC_E_ARG, "null argument");
+    if (!s->tiles) return set_err(ISPC_E_ARG, "not a building-block space (use ispc_cand_to_nest)");
+    *out = tile_config(*s->tiles, *s->ctx, c->c);
+    return ISPC_OK;
+  } catch (const std::exception& e) {
+    return set_err(ISPC_E_ARG, e.what());
+  }
+}
+
 int ispc_cand_to_nest(const ispc_space* s, const ispc_cand* c, ispc_nest_buf** out) {
   try {
     if (!s || !c || !out) return set_err(ISPC_E_ARG, "null argument");
+    if (s->tiles) return set_err(ISPC_E_ARG, "building-block spaces have no loop nest (use ispc_cand_to_tiles)");
     ispace::LoopNest l = ispace::reconstruct(s->kernel, *s->ctx, c->c);
     auto nb = std::make_unique<ispc_nest_buf>();
     nb->b = flatten(s->kernel, l);
@@ -269,6 +292,7 @@ static int put_text(const std::string& s, char* buf, size_t cap, size_t* len) {
 
 int ispc_cand_reference_source(const ispc_space* s, const ispc_cand* c, char* buf, size_t cap, size_t* len) {
   try {
+    if (s->tiles) return set_err(ISPC_E_ARG, "building-block spaces have no reference pseudo-source");
     ispace::LoopNest l = ispace::reconstruct(s->kernel, *s->ctx, c->c);
     return put_text(ispace::emit_source(s->kernel, l), buf, cap, len);
   } catch (const std::exception& e) {
@@ -278,6 +302,7 @@ int ispc_cand_reference_source(const ispc_space* s, const ispc_cand* c, char* bu
 
 int ispc_cand_simulate(const ispc_space* s, const ispc_cand* c, int64_t out[5]) {
   try {
+    if (s->tiles) return set_err(ISPC_E_ARG, "building-block spaces have no reference simulation");
     ispace::LoopNest l = ispace::reconstruct(s->kernel, *s->ctx, c->c);
     ispace::CostReport r = ispace::evaluate(s->kernel, l, s->mp);
     out[0] = r.compute;

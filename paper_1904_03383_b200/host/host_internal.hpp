@@ -11,6 +11,7 @@
 #include "ispace/kernels.hpp"
 #include "ispace/machine.hpp"
 #include "ispc_host.h"
+#include "tiles.hpp"
 
 struct ispc_space {
   ispc_kernel_spec spec{};
@@ -20,6 +21,9 @@ struct ispc_space {
   std::shared_ptr<const ispace::SpaceContext> ctx;
   ispace::Candidate root;
   double build_seconds = 0;
+  // building-block kinds (gemv, sgemm, batched, sgemm_tc): the tiles.space
+  // family; `kernel` stays empty for them
+  std::unique_ptr<ispc_host::TileFamily> tiles;
 };
 
 struct ispc_cand {

@@ -72,6 +72,8 @@ std::vector<std::string> split(const std::string& s) {
 }
 
 const char* kPaperOrder = "size,dim_kind,thread_level,mem_space,order,cache";
+// building-block spaces: the engine and staging shape everything below them
+const char* kTileOrder = "engine,staging,tile,xreduce,cache";
 
 }  // namespace
 
@@ -80,7 +82,7 @@ double Search::now() const {
 }
 
 Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(space), cfg_(cfg) {
-  order_text_ = cfg.decision_order ? cfg.decision_order : kPaperOrder;
+  order_text_ = cfg.decision_order ? cfg.decision_order : space->tiles ? kTileOrder : kPaperOrder;
   shm_text_ = cfg.incumbent_shm ? cfg.incumbent_shm : "";
   log_text_ = cfg.log_path ? cfg.log_path : "";
   cfg_.decision_order = order_text_.c_str();
@@ -95,7 +97,7 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
   if (cfg_.compile_threads <= 0) cfg_.compile_threads = int(std::max(1u, hw - unsigned(cfg_.rollout_threads) - 1));
   machine_.l2_flushed = cfg_.flush_l2 != 0;
   machine_.max_unrolled = cfg_.max_unrolled;
-  model_ = std::make_unique<BoundModel>(space_->kernel, *space_->ctx, machine_);
+  if (!space_->tiles) model_ = std::make_unique<BoundModel>(space_->kernel, *space_->ctx, machine_);
   order_ = DecisionOrder::from_names(*space_->ctx, split(order_text_));
   inc_.open(shm_text_.empty() ? nullptr : shm_text_.c_str());
   if (!log_text_.empty()) log_ = std::fopen(log_text_.c_str(), "w");
@@ -156,6 +158,11 @@ void Search::expand_frontier() {
   st_.frontier = int64_t(subtrees_.size());
 }
 
+double Search::bound_total(const Candidate& c) const {
+  if (space_->tiles) return tile_bound(*space_->tiles, *space_->ctx, c).total;
+  return model_->bound(c).total;
+}
+
 bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound) {
   const SpaceContext& ctx = *space_->ctx;
   Candidate cur = subtrees_[size_t(subtree_cursor_++ % subtrees_.size())];
@@ -163,7 +170,7 @@ bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound) 
   for (;;) {
     std::uint32_t inst = order_.pick(ctx, cur);
     if (inst == kNoInstance) {
-      leaf_bound = model_->bound(cur).total;
+      leaf_bound = bound_total(cur);
       leaf = std::move(cur);
       return true;
     }
@@ -177,7 +184,7 @@ bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound) 
       if (apply_decision(ctx, cur, inst, v, child) != PropStatus::Ok) continue;
       double weight = 1.0;
       if (prune) {
-        double b = model_->bound(child).total;
+        double b = bound_total(child);
         if (!std::isfinite(b) || b >= T) {  // unrunnable, or cannot beat the incumbent
           ++pruned_;
           continue;
@@ -214,20 +221,41 @@ void Search::rollout_worker(int tid) {
       t_rollout_.fetch_add(now() - t);
       continue;
     }
-    try {
-      LoopNest l = reconstruct(space_->kernel, *space_->ctx, w->leaf);
-      w->nest = flatten(space_->kernel, l);
-    } catch (const std::exception&) {
-      ++illegal_;
-      t_rollout_.fetch_add(now() - t);
-      continue;
-    }
+    int rc = ISPC_OK;
     size_t len = 0;
-    int rc = ispc_emit_cuda(&w->nest->nest, &eo, nullptr, nullptr, 0, &len, &w->launch);
-    if (rc == ISPC_OK) {
-      w->src.assign(len + 1, '\0');
-      rc = ispc_emit_cuda(&w->nest->nest, &eo, nullptr, w->src.data(), w->src.size(), &len, &w->launch);
-      w->src.resize(len);
+    if (space_->tiles) {
+      // building-block leaf: decided tile configuration -> sm_100a kernel
+      ispc_tile_config tc{};
+      try {
+        tc = tile_config(*space_->tiles, *space_->ctx, w->leaf);
+      } catch (const std::exception&) {
+        ++illegal_;
+        t_rollout_.fetch_add(now() - t);
+        continue;
+      }
+      w->bit_exact = space_->tiles->bit_exact();
+      w->rtol = space_->tiles->rtol();
+      rc = ispc_emit_tiles(&tc, nullptr, nullptr, 0, &len, &w->launch);
+      if (rc == ISPC_OK) {
+        w->src.assign(len + 1, '\0');
+        rc = ispc_emit_tiles(&tc, nullptr, w->src.data(), w->src.size(), &len, &w->launch);
+        w->src.resize(len);
+      }
+    } else {
+      try {
+        LoopNest l = reconstruct(space_->kernel, *space_->ctx, w->leaf);
+        w->nest = flatten(space_->kernel, l);
+      } catch (const std::exception&) {
+        ++illegal_;
+        t_rollout_.fetch_add(now() - t);
+        continue;
+      }
+      rc = ispc_emit_cuda(&w->nest->nest, &eo, nullptr, nullptr, 0, &len, &w->launch);
+      if (rc == ISPC_OK) {
+        w->src.assign(len + 1, '\0');
+        rc = ispc_emit_cuda(&w->nest->nest, &eo, nullptr, w->src.data(), w->src.size(), &len, &w->launch);
+        w->src.resize(len);
+      }
     }
     t_rollout_.fetch_add(now() - t);
     if (rc != ISPC_OK) {
@@ -353,8 +381,8 @@ void Search::launch_worker() {
       to.reps = uint32_t(cfg_.reps);
       to.flush_l2 = uint32_t(cfg_.flush_l2);
       to.check = 1;
-      to.bit_exact = 1;
-      to.rtol = 1e-5;
+      to.bit_exact = w->bit_exact ? 1 : 0;
+      to.rtol = w->rtol;
       to.budget_ns = std::isfinite(T) ? std::min(cfg_.max_budget_ns, std::max(T * 1e9 * cfg_.budget_factor,
                                                                                 T * 1e9 + 20e3))
                                       : cfg_.max_budget_ns;
@@ -489,6 +517,17 @@ extern "C" {
 int ispc_bound(const ispc_space* s, const ispc_cand* c, int l2_flushed, ispc_bound_report* out) {
   try {
     if (!s || !c || !out) return set_err(ISPC_E_ARG, "null argument");
+    if (s->tiles) {
+      TileBoundReport r = tile_bound(*s->tiles, *s->ctx, c->c);
+      std::memset(out, 0, sizeof(*out));
+      out->total = r.total;
+      out->dram = r.dram;
+      out->issue = r.compute;
+      out->launch = r.launch;
+      out->dram_bytes = r.dram_bytes;
+      out->blocks_max = r.ctas;
+      return ISPC_OK;
+    }
     B200Machine m;
     m.l2_flushed = l2_flushed != 0;
     BoundModel bm(s->kernel, *s->ctx, m);

@@ -57,6 +57,8 @@ struct Work {
   ispc_launch launch{};
   double bound_s = 0;
   uint64_t digest = 0;
+  bool bit_exact = true;  // parity-mode and FFMA sgemm outputs: identical bits
+  double rtol = 1e-5;     // otherwise: |out - exp| <= rtol * sum |products|
 };
 
 struct CompiledBatch {
@@ -112,6 +114,7 @@ class Search {
   std::string best_text_, best_src_;
   ispc_launch best_launch_{};
 
+  double bound_total(const ispace::Candidate& c) const;
   void expand_frontier();
   bool rollout(std::mt19937_64& rng, ispace::Candidate& leaf, double& leaf_bound);
   void rollout_worker(int tid);

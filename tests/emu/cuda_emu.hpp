@@ -87,6 +87,31 @@ inline float __fmaf_rn(float a, float b, float c) { return std::fmaf(a, b, c); }
 #define __align__(x)
 #define __restrict__ __restrict
 
+// warp-level exchange and the tile kernels' building blocks. The emulated
+// kernels call these uniformly across the block, so a block-wide phase
+// boundary stands in for the warp-wide one.
+inline float emu_xchg[1024];
+inline unsigned emu_tid() { return threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z); }
+inline float __shfl_xor_sync(unsigned, float v, int off) {
+  const unsigned t = emu_tid();
+  emu_xchg[t] = v;
+  emu_yield_barrier();
+  float r = emu_xchg[t ^ unsigned(off)];
+  emu_yield_barrier();
+  return r;
+}
+inline void __syncwarp() { emu_yield_barrier(); }
+inline void ispc_cp_async_cg16(void* s, const void* g) { std::memcpy(s, g, 16); }
+inline void ispc_cp_async_ca16(void* s, const void* g) { std::memcpy(s, g, 16); }
+inline void ispc_cp_async_ca8(void* s, const void* g) { std::memcpy(s, g, 8); }
+inline void ispc_cp_async_ca4(void* s, const void* g) { std::memcpy(s, g, 4); }
+inline void ispc_cp_async_commit() {}
+template <int N>
+inline void ispc_cp_async_wait() {}
+inline unsigned ispc_cluster_rank() { return 0; }  // clusters of one CTA only
+inline void ispc_cluster_sync() { emu_yield_barrier(); }
+inline float ispc_dsmem_ld(const float* p, unsigned) { return *p; }
+
 inline int ispc_timeout_flag = 0;
 inline unsigned long long ispc_now() { return 0; }
 alignas(16) inline float ispc_smem[1 << 16];

@@ -1,0 +1,170 @@
+"""Building-block spaces (host/tiles.space through the reference's
+build_space): space construction, propagation facts, the B200 lower bound,
+and the emitted kernels executed by the CPU emulator against the oracle
+(bit-exact for the FFMA sgemm / batched kernels, norm-wise 1e-5 against the
+fp64 oracle for the reordered gemv)."""
+import numpy as np
+import pytest
+
+from paper_1904_03383_b200 import DeadEnd, EmitError, Space, tile_cuda
+from paper_1904_03383_b200 import _native as N
+from tests import emu
+from tests.oracle_lib import Oracle
+
+SEED = 0x190403383
+
+
+def _leaves(space, n, order=None):
+    root = space.root()
+    out = []
+    for seed in range(n):
+        try:
+            leaf, _, _ = root.random_leaf(seed, order=order)
+        except DeadEnd:
+            continue
+        out.append(leaf)
+    return out
+
+
+@pytest.mark.parametrize("kind,kw", [
+    ("gemv", dict(m=4096, n=4096)),
+    ("sgemm", dict(m=1024, n=1024, k=1024)),
+    ("batched", dict(m=32, n=32, k=64, batch=512)),
+    ("sgemm_tc", dict(m=4096, n=4096, k=4096)),
+])
+def test_space_builds_and_is_deterministic(kind, kw):
+    a, b = Space(kind, **kw), Space(kind, **kw)
+    sa, sb = a.stats(), b.stats()
+    assert sa["root_digest"] == sb["root_digest"]
+    assert sa["instances"] > 0 and sa["root_open"] > 0
+    leaf = a.root().first_leaf()
+    assert leaf.fully_specified
+    assert leaf.digest == b.deserialize(leaf.serialize()).digest
+
+
+def test_gemv_lane_split_propagates():
+    """warp_lanes() == 32: deciding lanes_m fixes lanes_n through the counter."""
+    s = Space("gemv", m=256, n=256)
+    c = s.root()
+    c.decide("tile", ["lanes_m"], "8")
+    with pytest.raises(DeadEnd):
+        c.clone().decide("tile", ["lanes_n"], "8")
+    c.clone().decide("tile", ["lanes_n"], "4")
+    leaf = c.first_leaf()
+    t = leaf.tiles()
+    assert t.lanes_m * t.lanes_n == 32
+
+
+def test_sgemm_thread_and_register_counters():
+    s = Space("sgemm", m=256, n=256, k=64)
+    for leaf in _leaves(s, 40):
+        t = leaf.tiles()
+        assert 32 <= t.thr_m * t.thr_n <= 1024
+        assert t.tm * t.tn <= 128
+        assert N.STAGINGS[t.staging] in ("SHARED", "CP_ASYNC") and N.ENGINES[t.engine] == "FFMA"
+    c = s.root()
+    c.decide("tile", ["thr_m"], "256")
+    with pytest.raises(DeadEnd):
+        c.clone().decide("tile", ["thr_n"], "8")  # 2048 threads
+
+
+def test_tcgen05_space_is_tma_only():
+    s = Space("sgemm_tc", m=512, n=512, k=512)
+    for leaf in _leaves(s, 10):
+        t = leaf.tiles()
+        assert N.STAGINGS[t.staging] == "TMA" and N.ENGINES[t.engine] in ("TF32", "TF32X3")
+
+
+@pytest.mark.parametrize("kind,kw", [
+    ("gemv", dict(m=4096, n=4096)),
+    ("sgemm", dict(m=1024, n=1024, k=1024)),
+    ("batched", dict(m=32, n=32, k=64, batch=512)),
+])
+def test_bound_is_monotone_along_descents(kind, kw):
+    s = Space(kind, **kw)
+    root = s.root()
+    b0 = root.bound()["total"]
+    assert b0 > 0
+    for leaf in _leaves(s, 8):
+        bl = leaf.bound()["total"]
+        assert bl >= b0 * (1 - 1e-12)
+
+
+def _regions(orc, p):
+    nan = lambda n: np.full(n, np.nan, dtype=np.float32)  # noqa: E731
+    if p.kind == 3:
+        return {"a": orc.fill(p.m * p.n, p.seed, "a"), "x": orc.fill(p.n, p.seed, "x"), "y": nan(p.m)}
+    bt = max(int(p.batch), 1)
+    return {"a": orc.fill(bt * p.m * p.k, p.seed, "a"), "b": orc.fill(bt * p.k * p.n, p.seed, "b"),
+            "c": nan(bt * p.m * p.n)}
+
+
+def _emulate_all(space, want, max_threads=256, n=30):
+    orc = Oracle()
+    p = space.problem()
+    checked = 0
+    for leaf in _leaves(space, n):
+        t = leaf.tiles()
+        try:
+            src, L = tile_cuda(t, "k_emu")
+        except EmitError:
+            continue
+        if L.block[0] > max_threads or (L.cluster[0] > 1):
+            continue
+        regs = _regions(orc, p)
+        emu.run(src, L, regs)
+        want(regs, t)
+        checked += 1
+    return checked
+
+
+def test_sgemm_kernels_bit_exact_on_emulator():
+    s = Space("sgemm", m=32, n=32, k=32)
+    orc = Oracle()
+    p = s.problem()
+    r = _regions(orc, p)
+    ref = orc.matmul(r["a"], r["b"], 32, 32, 32)
+
+    def want(regs, t):
+        assert np.array_equal(regs["c"].view(np.uint32), ref.view(np.uint32)), t.as_dict()
+
+    assert _emulate_all(s, want) >= 5
+
+
+def test_batched_kernels_bit_exact_on_emulator():
+    s = Space("batched", m=8, n=8, k=16, batch=8)
+    orc = Oracle()
+    p = s.problem()
+    r = _regions(orc, p)
+    ref = orc.batched(r["a"], r["b"], 8, 8, 8, 16)
+
+    def want(regs, t):
+        assert np.array_equal(regs["c"].view(np.uint32), ref.view(np.uint32)), t.as_dict()
+
+    assert _emulate_all(s, want) >= 5
+
+
+def test_gemv_kernels_normwise_on_emulator():
+    s = Space("gemv", m=128, n=128)
+    orc = Oracle()
+    p = s.problem()
+    r = _regions(orc, p)
+    y64, scale = orc.gemv_f64(r["a"], r["x"], 128, 128)
+
+    def want(regs, t):
+        err = np.abs(regs["y"].astype(np.float64) - y64) / np.maximum(scale, 1e-30)
+        assert np.all(np.isfinite(regs["y"])) and err.max() <= 1e-5, (t.as_dict(), err.max())
+
+    assert _emulate_all(s, want, max_threads=1024, n=60) >= 5
+
+
+def test_illegal_configurations_are_rejected():
+    s = Space("gemv", m=64, n=64)
+    t = s.root().first_leaf().tiles()
+    t.split = 16
+    with pytest.raises(EmitError):
+        tile_cuda(t)
+    t = Space("sgemm", m=64, n=64, k=64).root().first_leaf().tiles()
+    t.bk = 3
+    with pytest.raises(EmitError):
+        tile_cuda(t)
