@@ -13,7 +13,14 @@ through the C-ABI. `roofline` = the best kernel found, re-timed without the
 watchdog. `cpu_baseline` = the reference's own CPU search + simulated
 evaluation (oracle/_ref/ref_cpu_bench) on this host.
 
+`configs` (rank 0, after the headline): the other BASELINE.json shapes, each a
+bounded search of the building-block space (gemv 4096^2, sgemm 1024^3,
+batched 512 x 32x32x64 sharded over ranks, tcgen05 sgemm 4096^3): best
+kernel re-timed with an L2 flush before every launch, its roofline fraction,
+and cuBLAS (through torch) on the same shape.
+
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--configs all|none|gemv,sgemm,batched,sgemm_tc]
 """
 from __future__ import annotations
 
@@ -36,14 +43,6 @@ METRIC = "candidates evaluated/s (best-kernel GB/s vs HBM roofline in `roofline`
 WORKLOAD = "axpy fp32 n=2^26: full search + evaluation (paper factors {2,4}x{2..1024}, reference gpu.space)"
 REF_CPU_BENCH = os.path.join(ROOT, "oracle", "_ref", "ref_cpu_bench")
 PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r01_axpy_best_ncu.json")
-
-
-def peaks() -> dict:
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(p):
-        d = json.load(open(p))
-        return {"hbm_gbs": d["hbm_gbs"], "source": "measured"}
-    return {"hbm_gbs": 6650.0, "source": "fallback"}
 
 
 class Clocks:
@@ -125,35 +124,6 @@ def cpu_baseline(seconds: float, threads: int) -> dict | None:
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
-def cublas_axpy_gbs() -> float | None:
-    """cuBLAS Saxpy on the same n (reads x, y, writes y: the same 12 B/element)."""
-    try:
-        import ctypes as C
-
-        import torch
-        lib = C.CDLL("libcublas.so.12")
-        h = C.c_void_p()
-        lib.cublasCreate_v2(C.byref(h))
-        x = torch.rand(N_AXPY, device="cuda")
-        y = torch.rand(N_AXPY, device="cuda")
-        alpha = C.c_float(1.5)
-        stream = torch.cuda.current_stream().cuda_stream
-        lib.cublasSetStream_v2(h, C.c_void_p(stream))
-        times = []
-        for i in range(13):
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            lib.cublasSaxpy_v2(h, N_AXPY, C.byref(alpha), C.c_void_p(x.data_ptr()), 1, C.c_void_p(y.data_ptr()), 1)
-            e.record()
-            torch.cuda.synchronize()
-            if i >= 3:
-                times.append(s.elapsed_time(e))
-        lib.cublasDestroy_v2(h)
-        return BYTES_PER_RUN / (statistics.median(times) * 1e-3) / 1e9
-    except Exception:
-        return None
-
-
 def run_reference(args, world, rank):
     """`--impl reference`: the reference's CPU search + simulated evaluation on
     this host's cores (rank 0 only), on our metric/config."""
@@ -179,6 +149,53 @@ def run_reference(args, world, rank):
     print(json.dumps(line))
 
 
+CONFIG_SPACES = {
+    # kind: (Space kwargs, evaluations, flush L2 while searching)
+    "gemv": (dict(m=4096, n=4096), 96, True),
+    "sgemm": (dict(m=1024, n=1024, k=1024), 96, False),
+    "batched": (dict(m=32, n=32, k=64, batch=512), 64, True),
+    "sgemm_tc": (dict(m=4096, n=4096, k=4096), 30, False),
+}
+
+
+def run_configs(kinds, args, local, world, rank) -> dict:
+    """Bounded searches over the other BASELINE shapes; batched is sharded
+    along its batch across ranks (64 problems per GPU at 8 GPUs), the others
+    run on rank 0 only (replicas would repeat the same search)."""
+    from paper_1904_03383_b200 import Search, Space
+    from paper_1904_03383_b200.measure import cublas_reference, retime_best
+    out = {}
+    for kind in kinds:
+        kw, evals, flush = CONFIG_SPACES[kind]
+        kw = dict(kw)
+        if kind == "batched":
+            kw["batch"] = kw["batch"] // world
+        elif rank != 0:
+            continue
+        t0 = time.perf_counter()
+        try:
+            space = Space(kind, **kw)
+            s = Search(space, device=local, seed=0x1904 + rank, reps=3, warmup=1, flush_l2=flush)
+            s.step(evals)
+            st = s.stats()
+            best = s.best()
+            s.close()
+        except Exception as e:  # report, keep the headline
+            out[kind] = {"error": str(e)}
+            continue
+        res = {"shape": kw, "evaluated": st["evaluations"], "ok": st["ok"], "mismatches": st["mismatches"],
+               "illegal": st["illegal"], "exhausted": bool(st["exhausted"]), "time_to_best_s": st["time_to_best_s"],
+               "search_s": round(time.perf_counter() - t0, 2)}
+        if best is not None:
+            r = retime_best(space, best, reps=20, ordinal=local)
+            res["best"] = r
+            res["best_config"] = best.tiles().as_dict()
+        if rank == 0:
+            res["cublas"] = cublas_reference(space)
+        out[kind] = res
+    return out
+
+
 def run_ours(args, world, rank, local):
     import numpy as np
     import torch
@@ -201,6 +218,7 @@ def run_ours(args, world, rank, local):
     barrier(world)
     torch.cuda.synchronize()
     dev_ms = []
+    ev0 = search.stats()["evaluations"]
     t_wall = time.perf_counter()
     with Clocks(local) as clk:
         for _ in range(args.steps):
@@ -209,9 +227,10 @@ def run_ours(args, world, rank, local):
     wall = time.perf_counter() - t_wall
     torch.cuda.synchronize()
     barrier(world)
-    dev_s = sum(dev_ms) * 1e-3
+    evals_here = search.stats()["evaluations"] - ev0
+    dev_s = max(sum(dev_ms) * 1e-3, 1e-9)
     (dev_s_max,) = allreduce([dev_s], "max", world)
-    (evals_total,) = allreduce([float(E * args.steps)], "sum", world)
+    (evals_total,) = allreduce([float(evals_here)], "sum", world)
     value = evals_total / dev_s_max
 
     # ---- end to end: host buffers through the C-ABI every step ----
@@ -222,6 +241,7 @@ def run_ours(args, world, rank, local):
     search.read_region("y", yh.data_ptr(), yh.nbytes)
     e2e_steps = max(2, args.steps // 2)
     barrier(world)
+    ev1 = search.stats()["evaluations"]
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         search.write_region("x", xh.data_ptr(), xh.nbytes)
@@ -230,7 +250,7 @@ def run_ours(args, world, rank, local):
         search.read_region("z", zh.data_ptr(), zh.nbytes)
     e2e_wall = time.perf_counter() - t0
     (e2e_max,) = allreduce([e2e_wall], "max", world)
-    (e2e_evals,) = allreduce([float(E * e2e_steps)], "sum", world)
+    (e2e_evals,) = allreduce([float(search.stats()["evaluations"] - ev1)], "sum", world)
     e2e_value = e2e_evals / e2e_max
 
     st = search.stats()
@@ -238,30 +258,30 @@ def run_ours(args, world, rank, local):
     best_src = search.best_source()
     search.close()
 
+    configs = {}
+    if args.configs != "none":
+        want = ["gemv", "sgemm", "batched", "sgemm_tc"] if args.configs == "all" else args.configs.split(",")
+        configs = run_configs(want, args, local, world, rank)
     if rank != 0:
         return
 
-    # ---- roofline: the best kernel, re-timed without the watchdog ----
-    pk = peaks()
+    # ---- roofline: the best kernel, re-timed (no watchdog, L2 flushed) ----
+    from paper_1904_03383_b200.measure import cublas_reference, retime_best
     roofline = None
     best_info = {}
     if best is not None:
-        dev = Device(local)
-        dev.bind(space.problem())
-        m = dev.evaluate(best.nest(), watchdog=0, reps=20, warmup=3)
-        dev.close()
-        if m.status == "ok":
-            gbs = BYTES_PER_RUN / m.median_ns
+        r = retime_best(space, best, reps=20, ordinal=local)
+        if r.get("status") == "ok":
+            roofline = dict(r["roofline"])
             traffic = None
             if os.path.exists(PROFILE_SUMMARY):
                 traffic = json.load(open(PROFILE_SUMMARY)).get("dram_bytes_per_launch")
-            roofline = {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                        "frac": round(gbs / pk["hbm_gbs"], 4), "traffic": traffic,
-                        "algorithmic_bytes_per_launch": BYTES_PER_RUN, "kernel_us": round(m.median_ns / 1e3, 2),
-                        "peak_source": pk["source"]}
-            best_info = {"kernel_us": m.median_ns / 1e3, "gbs": gbs, "search_median_us": st["best_ns"] / 1e3,
-                         "bound_us": st["best_bound_ns"] / 1e3, "time_to_best_s": st["time_to_best_s"]}
-    cub = cublas_axpy_gbs()
+            roofline["traffic"] = traffic
+            roofline["kernel_us"] = r["kernel_us"]
+            best_info = {"kernel_us": r["kernel_us"], "search_median_us": st["best_ns"] / 1e3,
+                         "bound_us": st["best_bound_ns"] / 1e3, "time_to_best_s": st["time_to_best_s"],
+                         "grid": r["grid"], "block": r["block"]}
+    cub = cublas_reference(space)
     cpu = None
     if not args.no_cpu_baseline:
         res = cpu_baseline(args.cpu_seconds, os.cpu_count() or 1)
@@ -284,7 +304,8 @@ def run_ours(args, world, rank, local):
         "gpu_launches": int(evals_total * per_eval_launches),
         "clocks": clk.summary(),
         "best_kernel": best_info,
-        "cublas_saxpy_gbs": round(cub, 1) if cub else None,
+        "cublas_axpy": cub,
+        "configs": configs,
         "search": {k: st[k] for k in ("evaluations", "ok", "mismatches", "timeouts", "launch_errors", "illegal",
                                       "compile_errors", "duplicates", "rollouts", "dead_rollouts",
                                       "pruned_children", "bound_violations", "frontier", "t_rollout_s",
@@ -307,6 +328,7 @@ def main():
     ap.add_argument("--batch", type=int, default=8, help="kernels per NVRTC program")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--configs", default="all", help="all | none | comma list of gemv,sgemm,batched,sgemm_tc")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":

@@ -159,6 +159,7 @@ typedef struct {
   double t_rollout_s, t_compile_s, t_gpu_s; /* busy time per stage (summed over threads) */
   uint64_t best_hash;
   int64_t frontier;         /* subtree roots owned by this shard                */
+  int64_t exhausted;        /* 1: no new kernel survives pruning in this shard  */
 } ispc_search_stats;
 
 int ispc_search_create(const ispc_space* s, const ispc_search_config* cfg, ispc_search** out);

@@ -182,7 +182,7 @@ class SearchStats(C.Structure):
                 + [(f, C.c_double) for f in ("best_ns", "incumbent_ns", "best_bound_ns", "time_to_best_s",
                                              "elapsed_s", "device_step_ms", "t_rollout_s", "t_compile_s",
                                              "t_gpu_s")]
-                + [("best_hash", C.c_uint64), ("frontier", C.c_int64)])
+                + [("best_hash", C.c_uint64), ("frontier", C.c_int64), ("exhausted", C.c_int64)])
 
 
 # Every symbol include/ispc.h declares, with its ctypes signature.

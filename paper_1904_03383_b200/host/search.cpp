@@ -200,6 +200,13 @@ bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound) 
   }
 }
 
+void Search::note_fruitless() {
+  if (++fruitless_ >= kExhaust && !exhausted_.exchange(true)) {
+    std::lock_guard<std::mutex> lk(mu_);
+    cv_done_.notify_all();
+  }
+}
+
 void Search::rollout_worker(int tid) {
   std::mt19937_64 rng(cfg_.seed + 7919ull * uint64_t(tid) + 104729ull * uint64_t(cfg_.shard_index));
   const size_t cap = size_t(cfg_.batch) * size_t(cfg_.compile_threads) * 3;
@@ -219,6 +226,8 @@ void Search::rollout_worker(int tid) {
     if (!ok) {
       ++dead_rollouts_;
       t_rollout_.fetch_add(now() - t);
+      note_fruitless();
+      if (exhausted_) std::this_thread::sleep_for(std::chrono::milliseconds(1));
       continue;
     }
     int rc = ISPC_OK;
@@ -231,6 +240,7 @@ void Search::rollout_worker(int tid) {
       } catch (const std::exception&) {
         ++illegal_;
         t_rollout_.fetch_add(now() - t);
+        note_fruitless();
         continue;
       }
       w->bit_exact = space_->tiles->bit_exact();
@@ -248,6 +258,7 @@ void Search::rollout_worker(int tid) {
       } catch (const std::exception&) {
         ++illegal_;
         t_rollout_.fetch_add(now() - t);
+        note_fruitless();
         continue;
       }
       rc = ispc_emit_cuda(&w->nest->nest, &eo, nullptr, nullptr, 0, &len, &w->launch);
@@ -260,14 +271,20 @@ void Search::rollout_worker(int tid) {
     t_rollout_.fetch_add(now() - t);
     if (rc != ISPC_OK) {
       ++illegal_;
+      note_fruitless();
       continue;
     }
     w->digest = digest(*space_->ctx, w->leaf);
-    std::lock_guard<std::mutex> lk(mu_);
+    std::unique_lock<std::mutex> lk(mu_);
     if (!seen_hash_.insert(w->launch.source_hash).second) {
       ++duplicates_;
+      lk.unlock();
+      note_fruitless();
+      if (exhausted_) std::this_thread::sleep_for(std::chrono::milliseconds(1));
       continue;
     }
+    fruitless_ = 0;
+    exhausted_ = false;
     work_q_.push_back(std::move(w));
     cv_batch_.notify_all();
   }
@@ -327,7 +344,7 @@ void Search::compile_worker(int tid) {
 }
 
 void Search::launch_worker() {
-  bool step_open = false;
+  bool& step_open = step_open_;
   while (!stop_) {
     std::unique_ptr<CompiledBatch> b;
     {
@@ -430,6 +447,7 @@ void Search::launch_worker() {
                        (long long)st_.evaluations, t_now, status.c_str(), rc == ISPC_OK ? r.median_ns : -1.0,
                        w->bound_s * 1e9, inc_.seconds() * 1e9, (unsigned long long)w->launch.source_hash,
                        (unsigned long long)w->digest, improved ? "true" : "false");
+          std::fflush(log_);
         }
         if (step_open && st_.evaluations >= target_.load()) {
           ispc_dev_mark(dev_, 1);
@@ -470,7 +488,17 @@ int Search::step(int64_t evaluations) {
   }
   if (!pipeline_started_) start();
   std::unique_lock<std::mutex> lk(mu_);
-  cv_done_.wait(lk, [&] { return stop_ || st_.evaluations >= target_.load(); });
+  auto drained = [&] { return exhausted_ && work_q_.empty() && batch_q_.empty() && !launching_; };
+  while (!(stop_ || st_.evaluations >= target_.load() || drained()))
+    cv_done_.wait_for(lk, std::chrono::milliseconds(50));
+  if (step_open_) {  // close the device-timeline step of an exhausted search
+    ispc_dev_mark(dev_, 1);
+    double ms = 0;
+    ispc_dev_mark_elapsed(dev_, 0, 1, &ms);
+    st_.device_step_ms = ms;
+    step_open_ = false;
+  }
+  target_ = st_.evaluations;
   if (stop_ && !err_.empty()) return ISPC_E_STICKY;
   return ISPC_OK;
 }
@@ -487,6 +515,7 @@ ispc_search_stats Search::stats() const {
   s.t_rollout_s = t_rollout_;
   s.t_compile_s = t_compile_;
   s.incumbent_ns = inc_.seconds() * 1e9;
+  s.exhausted = exhausted_ ? 1 : 0;
   s.elapsed_s = now() - t0_;
   return s;
 }

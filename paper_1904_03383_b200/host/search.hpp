@@ -104,11 +104,19 @@ class Search {
   std::atomic<uint64_t> subtree_cursor_{0};
   bool pipeline_started_ = false;
   bool launching_ = false;  // guarded by mu_
+  bool step_open_ = false;  // guarded by mu_: device mark 0 recorded for this step
 
   // statistics (guarded by mu_ unless atomic)
   ispc_search_stats st_{};
   std::atomic<int64_t> rollouts_{0}, dead_rollouts_{0}, pruned_{0}, illegal_{0}, duplicates_{0};
   std::atomic<int64_t> compile_errors_{0};
+  // consecutive rollouts (all threads) that queued no new kernel: dead ends,
+  // illegal or duplicate leaves. Past kExhaust the shard's subtrees are
+  // exhausted under the current incumbent and step() returns early.
+  static constexpr int64_t kExhaust = 3000;
+  std::atomic<int64_t> fruitless_{0};
+  std::atomic<bool> exhausted_{false};
+  void note_fruitless();
   std::atomic<double> t_rollout_{0}, t_compile_{0};
   double t0_ = 0;
   std::string best_text_, best_src_;

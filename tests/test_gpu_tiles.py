@@ -1,0 +1,157 @@
+"""GPU parity of the building-block kernels (tiles.space candidates emitted by
+ispc_emit_tiles, compiled by NVRTC for sm_100a, launched through the C-ABI).
+
+  sgemm / batched (FFMA, k ascending per output)  bit-exact vs the oracle
+  gemv (shuffle / shared / DSMEM-cluster sums)     |y - y64| <= 1e-5 * sum|a||x|
+  sgemm_tc TF32 / 3xTF32                           4e-3 / 1e-5 of sum|a||b|
+
+Small shapes are read back and compared with the CPU oracle; BASELINE shapes
+are checked on the device against the golden sequential kernels (themselves
+pinned to the oracle by test_golden_kernels_match_oracle)."""
+import numpy as np
+import pytest
+
+from paper_1904_03383_b200 import DeadEnd, Device, Space
+from paper_1904_03383_b200 import _native as N
+from tests.oracle_lib import Oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    d = Device(0)
+    yield d
+    d.close()
+
+
+def _leaves(space, n):
+    root = space.root()
+    for seed in range(n):
+        try:
+            leaf, _, _ = root.random_leaf(seed)
+        except DeadEnd:
+            continue
+        yield leaf
+
+
+def _run_many(dev, space, n, min_ok):
+    dev.bind(space.problem())
+    counts = {"ok": 0, "illegal": 0}
+    for leaf in _leaves(space, n):
+        t = leaf.tiles()
+        m = dev.evaluate_tiles(t, reps=1, warmup=0)
+        if m.status == "illegal":
+            counts["illegal"] += 1
+            continue
+        assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
+        counts["ok"] += 1
+    assert counts["ok"] >= min_ok, counts
+    return counts
+
+
+def test_golden_gemv_and_batched_match_oracle(dev):
+    orc = Oracle()
+    for space in (Space("gemv", m=256, n=128), Space("batched", m=8, n=16, k=32, batch=6)):
+        p = space.problem()
+        dev.bind(p)
+        for name, ref in orc.expected(p).items():
+            got = dev.read(name, ref.size, expected=True)
+            assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), name
+
+
+def test_gemv_small_readback(dev):
+    orc = Oracle()
+    space = Space("gemv", m=512, n=256)
+    p = space.problem()
+    dev.bind(p)
+    a, x = orc.fill(512 * 256, p.seed, "a"), orc.fill(256, p.seed, "x")
+    y64, scale = orc.gemv_f64(a, x, 512, 256)
+    ok = 0
+    for leaf in _leaves(space, 40):
+        m = dev.evaluate_tiles(leaf.tiles(), reps=1, warmup=0)
+        if m.status == "illegal":
+            continue
+        assert m.status == "ok", (leaf.tiles().as_dict(), m, dev.error())
+        y = dev.read("y", 512).astype(np.float64)
+        assert np.max(np.abs(y - y64) / np.maximum(scale, 1e-30)) <= 1e-5
+        ok += 1
+    assert ok >= 10
+
+
+def test_gemv_baseline_shape(dev):
+    _run_many(dev, Space("gemv", m=4096, n=4096), 40, 15)
+
+
+def test_gemv_cluster_split_is_exercised(dev):
+    space = Space("gemv", m=4096, n=4096)
+    dev.bind(space.problem())
+    c = space.root()
+    c.decide("tile", ["split"], "8")
+    c.decide("tile", ["warps_n"], "2")
+    leaf = c.first_leaf()
+    t = leaf.tiles()
+    m = dev.evaluate_tiles(t, reps=3)
+    assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
+    assert m.launch.cluster[0] == 8
+
+
+def test_sgemm_small_readback_bit_exact(dev):
+    orc = Oracle()
+    space = Space("sgemm", m=128, n=64, k=32)
+    p = space.problem()
+    dev.bind(p)
+    ref = orc.expected(p)["c"]
+    ok = 0
+    for leaf in _leaves(space, 40):
+        m = dev.evaluate_tiles(leaf.tiles(), reps=1, warmup=0)
+        if m.status == "illegal":
+            continue
+        assert m.status == "ok", (leaf.tiles().as_dict(), m, dev.error())
+        got = dev.read("c", ref.size)
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), leaf.tiles().as_dict()
+        ok += 1
+    assert ok >= 10
+
+
+def test_sgemm_baseline_shape(dev):
+    _run_many(dev, Space("sgemm", m=1024, n=1024, k=1024), 30, 10)
+
+
+def test_batched_baseline_shape(dev):
+    _run_many(dev, Space("batched", m=32, n=32, k=64, batch=512), 40, 10)
+
+
+def test_batched_small_readback_bit_exact(dev):
+    orc = Oracle()
+    space = Space("batched", m=32, n=32, k=64, batch=16)
+    p = space.problem()
+    dev.bind(p)
+    ref = orc.expected(p)["c"]
+    ok = 0
+    for leaf in _leaves(space, 30):
+        m = dev.evaluate_tiles(leaf.tiles(), reps=1, warmup=0)
+        if m.status == "illegal":
+            continue
+        assert m.status == "ok", (leaf.tiles().as_dict(), m, dev.error())
+        got = dev.read("c", ref.size)
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+        ok += 1
+    assert ok >= 5
+
+
+@pytest.mark.parametrize("engine", ["TF32", "TF32X3"])
+def test_tcgen05_sgemm(dev, engine):
+    space = Space("sgemm_tc", m=512, n=512, k=256)
+    dev.bind(space.problem())
+    ok = 0
+    for leaf in _leaves(space, 40):
+        t = leaf.tiles()
+        if N.ENGINES[t.engine] != engine:
+            continue
+        m = dev.evaluate_tiles(t, reps=1, warmup=0)
+        if m.status == "illegal" and "not available" in dev.error():
+            pytest.skip("tcgen05 kernel not built")
+        assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
+        ok += 1
+    assert ok >= 1
