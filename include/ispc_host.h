@@ -176,6 +176,12 @@ const char* ispc_search_error(const ispc_search* h);
 int ispc_search_write_region(ispc_search* h, const char* name, const void* host, size_t bytes);
 int ispc_search_read_region(ispc_search* h, const char* name, void* host, size_t bytes);
 void ispc_search_free(ispc_search* h);
+/* Digests of this shard's subtree roots (disjoint across shards); returns the
+ * count, writes at most `cap`. */
+int64_t ispc_search_frontier(const ispc_search* h, uint64_t* digests, int64_t cap);
+/* Offers a measured time to the shared incumbent (CAS-min across ranks);
+ * 1 when it became the new incumbent. Used by external evaluators and tests. */
+int ispc_search_offer(ispc_search* h, double ns);
 
 #ifdef __cplusplus
 }

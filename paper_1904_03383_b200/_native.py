@@ -261,6 +261,8 @@ HOST_SYMBOLS = {
     "ispc_search_free": (None, [C.c_void_p]),
     "ispc_search_write_region": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t]),
     "ispc_search_read_region": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t]),
+    "ispc_search_frontier": (C.c_int64, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64]),
+    "ispc_search_offer": (C.c_int, [C.c_void_p, C.c_double]),
 }
 
 _libs: dict[str, C.CDLL] = {}

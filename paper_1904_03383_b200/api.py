@@ -414,6 +414,17 @@ class Search:
         if N.host().ispc_search_read_region(self._h, name.encode(), C.c_void_p(ptr), nbytes) != 0:
             raise RuntimeError(N.last_error())
 
+    def frontier(self) -> list[int]:
+        """Digests of this shard's subtree roots."""
+        n = N.host().ispc_search_frontier(self._h, None, 0)
+        buf = (C.c_uint64 * max(n, 1))()
+        N.host().ispc_search_frontier(self._h, buf, n)
+        return list(buf)[:n]
+
+    def offer(self, ns: float) -> bool:
+        """CAS-min a measured time into the shared incumbent."""
+        return bool(N.host().ispc_search_offer(self._h, ns))
+
     def close(self):
         if getattr(self, "_h", None):
             N.host().ispc_search_free(self._h)

@@ -188,7 +188,9 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
 // ---------------------------------------------------------------- sgemm (FFMA)
 // C = A B, column-major: A[i + k*M], B[k + j*K], C[i + j*M]. CTA tile
 // BM x BN = (thr_m*tm) x (thr_n*tn); thread (tx, ty) owns rows
-// bm*BM + tx*tm .. +tm and columns bn*BN + ty*tn .. +tn. Shared tiles per
+// bm*BM + tx*tm .. +tm (contiguous: float4 smem reads and C stores) and the
+// columns bn*BN + ty + j*thr_n, j < tn (interleaved, so the Bs rows a warp
+// reads fall in distinct banks). Shared tiles per
 // stage: As[bk][BM] (m contiguous) and Bs[BN][bk+4] (k contiguous), both
 // filled with contiguous global chunks (no transposes), read as float4
 // along m (A) and along k (B: four k steps at once).
@@ -243,12 +245,12 @@ void gemm_compute(std::ostringstream& o, const GemmShape& g, const std::string& 
   o << indent << "    }\n" << indent << "  }\n";
   o << indent << "  #pragma unroll\n" << indent << "  for (int j = 0; j < " << g.TN << "; ++j) {\n";
   if (KG == 4)
-    o << indent << "    float4 t = *(const float4*)(" << Bs << " + (ty * " << g.TN << " + j) * " << g.ldb
+    o << indent << "    float4 t = *(const float4*)(" << Bs << " + (ty + j * " << g.TY << ") * " << g.ldb
       << " + kq);\n"
       << indent << "    rb[j][0] = t.x; rb[j][1] = t.y; rb[j][2] = t.z; rb[j][3] = t.w;\n";
   else
     o << indent << "    #pragma unroll\n" << indent << "    for (int q = 0; q < " << KG << "; ++q) rb[j][q] = "
-      << Bs << "[(ty * " << g.TN << " + j) * " << g.ldb << " + kq + q];\n";
+      << Bs << "[(ty + j * " << g.TY << ") * " << g.ldb << " + kq + q];\n";
   o << indent << "  }\n";
   o << indent << "  #pragma unroll\n" << indent << "  for (int q = 0; q < " << KG << "; ++q)\n";
   o << indent << "    #pragma unroll\n" << indent << "    for (int j = 0; j < " << g.TN << "; ++j)\n";
@@ -388,13 +390,13 @@ std::string sgemm(const ispc_tile_config& c, const std::string& fn, ispc_launch&
   // epilogue: C[i + j*M], vectors along m
   const int EV = g.TM % 4 == 0 ? 4 : g.TM % 2 == 0 ? 2 : 1;
   const std::string ety = EV == 4 ? "float4" : EV == 2 ? "float2" : "float";
-  o << "  float* pc = g_c + (bm * " << g.BM << "LL + tx * " << g.TM << ") + (bn * " << g.BN << "LL + ty * " << g.TN
-    << ") * " << M << "LL;\n";
+  o << "  float* pc = g_c + (bm * " << g.BM << "LL + tx * " << g.TM << ") + (bn * " << g.BN << "LL + ty) * " << M
+    << "LL;\n";
   o << "  #pragma unroll\n  for (int j = 0; j < " << g.TN << "; ++j)\n";
   o << "    #pragma unroll\n    for (int i = 0; i < " << g.TM << "; i += " << EV << ")\n";
-  if (EV == 1) o << "      pc[i + j * " << M << "LL] = acc[j][i];\n";
+  if (EV == 1) o << "      pc[i + (long long)j * " << int64_t(g.TY) * M << "LL] = acc[j][i];\n";
   else {
-    o << "      *(" << ety << "*)(pc + i + j * " << M << "LL) = make_" << ety << "(";
+    o << "      *(" << ety << "*)(pc + i + (long long)j * " << int64_t(g.TY) * M << "LL) = make_" << ety << "(";
     for (int e = 0; e < EV; ++e) o << (e ? ", " : "") << "acc[j][i + " << e << "]";
     o << ");\n";
   }

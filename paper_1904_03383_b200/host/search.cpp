@@ -520,6 +520,12 @@ ispc_search_stats Search::stats() const {
   return s;
 }
 
+std::vector<uint64_t> Search::frontier_digests() const {
+  std::vector<uint64_t> d;
+  for (const Candidate& c : subtrees_) d.push_back(digest(*space_->ctx, c));
+  return d;
+}
+
 std::string Search::best_candidate() const {
   std::lock_guard<std::mutex> lk(const_cast<std::mutex&>(mu_));
   return best_text_;
@@ -634,5 +640,17 @@ int ispc_search_read_region(ispc_search* h, const char* name, void* host, size_t
 }
 
 void ispc_search_free(ispc_search* h) { delete h; }
+
+int64_t ispc_search_frontier(const ispc_search* h, uint64_t* digests, int64_t cap) {
+  if (!h) return set_err(ISPC_E_ARG, "null search");
+  std::vector<uint64_t> d = h->s->frontier_digests();
+  for (int64_t i = 0; i < cap && i < int64_t(d.size()); ++i) digests[i] = d[size_t(i)];
+  return int64_t(d.size());
+}
+
+int ispc_search_offer(ispc_search* h, double ns) {
+  if (!h) return set_err(ISPC_E_ARG, "null search");
+  return h->s->offer(ns) ? 1 : 0;
+}
 
 }  // extern "C"

@@ -76,6 +76,8 @@ class Search {
   std::string best_source() const;
   ispc_launch best_launch() const;
   std::string error() const { return err_; }
+  std::vector<uint64_t> frontier_digests() const;
+  bool offer(double ns) { return inc_.offer(uint64_t(ns < 1 ? 1 : ns)); }
   // host <-> device copy of a problem region while the device is idle
   int region_io(const char* name, void* host, size_t bytes, bool upload);
 

@@ -1,0 +1,73 @@
+"""The N > 1 path on CPU: world-size-2 gloo process group, one search shard
+per rank (device=-1: rollouts, emission and NVRTC run, no device). Shards own
+disjoint subtrees of the same deterministic frontier, and the incumbent cell
+in POSIX shared memory is seen by every rank (no collective on the data
+path; gloo only carries the test's own checks)."""
+import os
+import uuid
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from tests.conftest import ROOT
+
+
+def _worker(rank, world, port, shm, kind, kw, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1904_03383_b200 import Search, Space
+        space = Space(kind, **kw)
+        s = Search(space, device=-1, seed=7, shard_index=rank, shard_count=world, incumbent_shm=shm,
+                   rollout_threads=1, compile_threads=1)
+        mine = s.frontier()
+        every = [None] * world
+        dist.all_gather_object(every, mine)
+        dist.barrier()
+        if rank == 0:
+            s.offer(12345.0)
+        dist.barrier()
+        seen = s.stats()["incumbent_ns"]
+        dist.barrier()
+        if rank == 1:
+            s.offer(99999.0)  # worse: must not replace
+            s.offer(777.0)    # better: must replace for everyone
+        dist.barrier()
+        after = s.stats()["incumbent_ns"]
+        s.close()
+        q.put((rank, every, seen, after))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,kw", [
+    ("axpy", dict(n=1 << 20, factors=[[2, 4], [32, 64, 128, 256]])),
+    ("sgemm", dict(m=256, n=256, k=64)),
+])
+def test_two_rank_shards_and_shared_incumbent(kind, kw):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + (os.getpid() % 1000)
+    shm = f"/ispc_test_{uuid.uuid4().hex[:12]}"
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, shm, kind, kw, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    every = res[0][1]
+    a, b = set(every[0]), set(every[1])
+    assert a and b and not (a & b), "shards must own disjoint subtrees"
+    assert every == res[1][1]
+    for _, _, seen, after in res:
+        assert seen == pytest.approx(12345.0)
+        assert after == pytest.approx(777.0)
+    try:
+        os.unlink("/dev/shm" + shm)
+    except OSError:
+        pass
