@@ -73,7 +73,10 @@ enum ispc_operand_kind {
 };
 enum ispc_dim_kind { ISPC_LOOP = 0, ISPC_BLOCK, ISPC_THREAD, ISPC_UNROLL, ISPC_VECTOR };
 enum ispc_mem_space { ISPC_GLOBAL = 0, ISPC_SHARED };
-enum ispc_cache { ISPC_CACHE_L1 = 0, ISPC_CACHE_L2, ISPC_CACHE_READ_ONLY, ISPC_CACHE_NONE };
+enum ispc_cache {
+  ISPC_CACHE_L1 = 0, ISPC_CACHE_L2, ISPC_CACHE_READ_ONLY, ISPC_CACHE_NONE,
+  ISPC_CACHE_STREAM /* building blocks only: ld.global.nc.L1::no_allocate.L2::256B */
+};
 enum ispc_node_kind { ISPC_NODE_DIM = 0, ISPC_NODE_INST, ISPC_NODE_BARRIER };
 
 typedef struct {

@@ -28,7 +28,7 @@ TILE_GEMV, TILE_SGEMM, TILE_BATCHED, TILE_SGEMM_TC = range(4)
 STAGINGS = ("DIRECT", "SHARED", "CP_ASYNC", "TMA")
 ENGINES = ("FFMA", "TF32", "TF32X3")
 XREDUCES = ("SHUFFLE", "SHARED")
-CACHES = ("L1", "L2", "READ_ONLY", "NONE")
+CACHES = ("L1", "L2", "READ_ONLY", "NONE", "STREAM")
 
 
 class AddrTerm(C.Structure):

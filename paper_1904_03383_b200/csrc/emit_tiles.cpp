@@ -7,7 +7,8 @@
 //
 // Blocks (each a decision of the candidate):
 //   vec      ld.global.v2/v4 (float2/float4) operand loads
-//   cache    L1 -> ld.global.ca, L2 -> .cg, READ_ONLY -> .nc, NONE -> .cs
+//   cache    L1 -> ld.global.ca, L2 -> .cg, READ_ONLY -> .nc, NONE -> .cs,
+//            STREAM -> ld.global.nc.L1::no_allocate.L2::256B
 //   xreduce  SHUFFLE: __shfl_xor_sync butterfly; SHARED: through shared memory
 //   split    thread-block cluster of `split` CTAs splitting the reduction axis,
 //            partial sums combined through distributed shared memory
@@ -48,6 +49,7 @@ std::string ld(uint32_t cache, int width, const std::string& ptr) {
     case ISPC_CACHE_L1: return "__ldca(" + p + ")";
     case ISPC_CACHE_L2: return "__ldcg(" + p + ")";
     case ISPC_CACHE_READ_ONLY: return "__ldg(" + p + ")";
+    case ISPC_CACHE_STREAM: return "ispc_ld_stream(" + p + ")";
     default: return "__ldcs(" + p + ")";
   }
 }

@@ -65,6 +65,7 @@ inline void emu_st(T* p, T v) {
 #define __ldcg(p) emu_ld(p)
 #define __ldcs(p) emu_ld(p)
 #define __ldg(p) emu_ld(p)
+#define ispc_ld_stream(p) emu_ld(p)
 #define __stwb(p, v) emu_st(p, v)
 #define __stcg(p, v) emu_st(p, v)
 #define __stcs(p, v) emu_st(p, v)
