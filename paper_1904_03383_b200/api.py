@@ -348,7 +348,7 @@ class Device:
         """Emit + compile + timed launch + on-device check of a building-block
         configuration. Default checking: bit-exact for the FFMA sgemm and
         batched kernels (k ascending per output), norm-wise rtol otherwise."""
-        exact_default = cfg.kind in (N.TILE_SGEMM, N.TILE_BATCHED)
+        exact_default = (cfg.kind == N.TILE_SGEMM and cfg.split <= 1) or cfg.kind == N.TILE_BATCHED
         if bit_exact is None:
             bit_exact = exact_default
         if rtol is None:

@@ -850,6 +850,14 @@ static __device__ __forceinline__ unsigned ispc_cluster_rank() {
 static __device__ __forceinline__ void ispc_cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
+static __device__ __forceinline__ float4 ispc_dsmem_ld4(const float* p, unsigned rank) {
+  unsigned a = ispc_smem_addr(p), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(r) : "memory");
+  return v;
+}
 static __device__ __forceinline__ float ispc_dsmem_ld(const float* p, unsigned rank) {
   unsigned a = ispc_smem_addr(p), r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));

@@ -292,7 +292,14 @@ std::string sgemm(const ispc_tile_config& c, const std::string& fn, ispc_launch&
   if (c.staging != ISPC_STAGE_SHARED && c.staging != ISPC_STAGE_CP_ASYNC)
     illegal("FFMA sgemm stages operands through shared memory (SHARED or CP_ASYNC)");
   if (c.staging == ISPC_STAGE_SHARED && g.S > 2) illegal("SHARED staging is single or double buffered");
-  const int64_t KT = K / g.BK;
+  // split-K over a thread-block cluster: CTA `rank` of the cluster walks
+  // k in [rank*K/SP, (rank+1)*K/SP); partial tiles are summed through
+  // distributed shared memory in rank order (norm-wise checked, not bit-exact)
+  const int SP = std::max(1, c.split);
+  if (SP > 8) illegal("cluster larger than 8 CTAs");
+  if (K % (int64_t(SP) * g.BK)) illegal("split-K slices do not divide K");
+  if ((g.BM * g.BN) % (4 * SP)) illegal("partial tile does not split across the cluster");
+  const int64_t KT = K / (int64_t(SP) * g.BK);
   const int V = g.V;
   const std::string vty = V == 4 ? "float4" : V == 2 ? "float2" : "float";
   std::ostringstream o;
@@ -300,9 +307,12 @@ std::string sgemm(const ispc_tile_config& c, const std::string& fn, ispc_launch&
     << "(const float* __restrict__ g_a, const float* __restrict__ g_b, float* __restrict__ g_c) {\n";
   o << "  extern __shared__ __align__(16) float ispc_smem[];\n";
   o << "  const int tid = threadIdx.x, tx = tid % " << g.TX << ", ty = tid / " << g.TX << ";\n";
-  o << "  const long long bm = blockIdx.x % " << M / g.BM << ", bn = blockIdx.x / " << M / g.BM << ";\n";
-  o << "  const float* pa = g_a + bm * " << g.BM << "LL;\n";
-  o << "  const float* pb = g_b + bn * " << g.BN << "LL * " << K << "LL;\n";
+  o << "  const long long tile = blockIdx.x / " << SP << ";\n";
+  o << "  const int rank = " << (SP > 1 ? "(int)ispc_cluster_rank()" : "0") << ";\n";
+  o << "  const long long bm = tile % " << M / g.BM << ", bn = tile / " << M / g.BM << ";\n";
+  o << "  const long long kbase = (long long)rank * " << K / SP << "LL;\n";
+  o << "  const float* pa = g_a + bm * " << g.BM << "LL + kbase * " << M << "LL;\n";
+  o << "  const float* pb = g_b + bn * " << g.BN << "LL * " << K << "LL + kbase;\n";
   o << "  float acc[" << g.TN << "][" << g.TM << "];\n";
   o << "  #pragma unroll\n  for (int j = 0; j < " << g.TN << "; ++j)\n    #pragma unroll\n    for (int i = 0; i < "
     << g.TM << "; ++i) acc[j][i] = 0.0f;\n";
@@ -392,21 +402,44 @@ std::string sgemm(const ispc_tile_config& c, const std::string& fn, ispc_launch&
   // epilogue: C[i + j*M], vectors along m
   const int EV = g.TM % 4 == 0 ? 4 : g.TM % 2 == 0 ? 2 : 1;
   const std::string ety = EV == 4 ? "float4" : EV == 2 ? "float2" : "float";
-  o << "  float* pc = g_c + (bm * " << g.BM << "LL + tx * " << g.TM << ") + (bn * " << g.BN << "LL + ty) * " << M
-    << "LL;\n";
-  o << "  #pragma unroll\n  for (int j = 0; j < " << g.TN << "; ++j)\n";
-  o << "    #pragma unroll\n    for (int i = 0; i < " << g.TM << "; i += " << EV << ")\n";
-  if (EV == 1) o << "      pc[i + (long long)j * " << int64_t(g.TY) * M << "LL] = acc[j][i];\n";
-  else {
-    o << "      *(" << ety << "*)(pc + i + (long long)j * " << int64_t(g.TY) * M << "LL) = make_" << ety << "(";
-    for (int e = 0; e < EV; ++e) o << (e ? ", " : "") << "acc[j][i + " << e << "]";
-    o << ");\n";
+  if (SP == 1) {
+    o << "  float* pc = g_c + (bm * " << g.BM << "LL + tx * " << g.TM << ") + (bn * " << g.BN << "LL + ty) * " << M
+      << "LL;\n";
+    o << "  #pragma unroll\n  for (int j = 0; j < " << g.TN << "; ++j)\n";
+    o << "    #pragma unroll\n    for (int i = 0; i < " << g.TM << "; i += " << EV << ")\n";
+    if (EV == 1) o << "      pc[i + (long long)j * " << int64_t(g.TY) * M << "LL] = acc[j][i];\n";
+    else {
+      o << "      *(" << ety << "*)(pc + i + (long long)j * " << int64_t(g.TY) * M << "LL) = make_" << ety << "(";
+      for (int e = 0; e < EV; ++e) o << (e ? ", " : "") << "acc[j][i + " << e << "]";
+      o << ");\n";
+    }
+  } else {
+    // partial tile P[col][row] (BN x BM, rows contiguous) in this CTA's shared
+    // memory; CTA `rank` then sums slice `rank` of every CTA's P and stores it
+    const int64_t tile_elems = g.BM * g.BN, slice = tile_elems / SP;
+    o << "  __syncthreads();\n";
+    o << "  float* P = ispc_smem;\n";
+    o << "  #pragma unroll\n  for (int j = 0; j < " << g.TN << "; ++j)\n";
+    o << "    #pragma unroll\n    for (int i = 0; i < " << g.TM << "; ++i) P[(ty + j * " << g.TY << ") * " << g.BM
+      << " + tx * " << g.TM << " + i] = acc[j][i];\n";
+    o << "  ispc_cluster_sync();\n";
+    o << "  for (int e = rank * " << slice << " + tid * 4; e < (rank + 1) * " << slice << "; e += " << 4 * g.T << ") {\n";
+    o << "    float4 s = ispc_dsmem_ld4(P + e, 0);\n";
+    o << "    #pragma unroll\n    for (int q = 1; q < " << SP << "; ++q) {\n";
+    o << "      const float4 t = ispc_dsmem_ld4(P + e, q);\n";
+    o << "      s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;\n    }\n";
+    o << "    const int col = e / " << g.BM << ", row = e % " << g.BM << ";\n";
+    o << "    *(float4*)(g_c + bm * " << g.BM << "LL + row + (bn * " << g.BN << "LL + col) * " << M << "LL) = s;\n";
+    o << "  }\n";
+    o << "  ispc_cluster_sync();\n";
+    L.cluster[0] = uint32_t(SP);
+    L.cluster[1] = L.cluster[2] = 1;
   }
   o << "}\n";
-  L.grid_x = uint64_t(M / g.BM * (N / g.BN));
+  L.grid_x = uint64_t(M / g.BM * (N / g.BN) * SP);
   L.block[0] = uint32_t(g.T);
   L.block[1] = L.block[2] = 1;
-  L.static_smem = uint32_t(g.stage_floats * g.S * 4);
+  L.static_smem = uint32_t(std::max<int64_t>(g.stage_floats * g.S, SP > 1 ? g.BM * g.BN : 0) * 4);
   add_region(L, "a", M * K);
   add_region(L, "b", K * N);
   add_region(L, "c", M * N);

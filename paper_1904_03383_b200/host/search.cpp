@@ -243,7 +243,7 @@ void Search::rollout_worker(int tid) {
         note_fruitless();
         continue;
       }
-      w->bit_exact = space_->tiles->bit_exact();
+      w->bit_exact = tile_bit_exact(tc);
       w->rtol = space_->tiles->rtol();
       rc = ispc_emit_tiles(&tc, nullptr, nullptr, 0, &len, &w->launch);
       if (rc == ISPC_OK) {

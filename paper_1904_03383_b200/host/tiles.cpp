@@ -57,6 +57,12 @@ const char* tiles_space_text() { return kTilesSpaceText; }
 
 bool TileFamily::bit_exact() const { return kind == ISPC_TILE_SGEMM || kind == ISPC_TILE_BATCHED; }
 
+bool tile_bit_exact(const ispc_tile_config& t) {
+  // FFMA kernels that keep one k-ascending chain per output; split-K sums
+  // cluster partials and is checked norm-wise
+  return (t.kind == ISPC_TILE_SGEMM && t.split <= 1) || t.kind == ISPC_TILE_BATCHED;
+}
+
 double TileFamily::rtol() const {
   // FFMA reorderings (gemv) and 3xTF32 are held to 1e-5 of sum |a||b|; plain
   // TF32 rounds operands to 10 mantissa bits (2^-11 relative each)
@@ -93,9 +99,11 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     TileParam tm = P("tm", dividing(pow2_upto(1, 16), m)), tn = P("tn", dividing(pow2_upto(1, 16), n));
     TileParam bk = P("bk", dividing({4, 8, 16, 32}, k)), st = P("stages", {1, 2, 3, 4});
     TileParam vec = P("vec", {1, 2, 4});
+    TileParam split = P("split", dividing({1, 2, 4, 8}, k));
     tx.thread = ty.thread = true;
     tm.acc = tn.acc = true;
-    f.params = {tx, ty, tm, tn, bk, st, vec};
+    split.cluster = true;
+    f.params = {tx, ty, tm, tn, bk, st, vec, split};
     f.min_threads = 32;
     f.max_acc = 128;
     pre("staging", {"SHARED", "CP_ASYNC"});
@@ -271,8 +279,8 @@ TileBoundReport tile_bound(const TileFamily& f, const SpaceContext& ctx, const C
       b.dram_bytes = 4 * (M * K + K * N + M * N);
       flops = 2 * M * N * K;
       if (f.kind == ISPC_TILE_SGEMM) {
-        b.ctas = M / (lo("thr_m") * lo("tm")) * (N / (lo("thr_n") * lo("tn")));
-        per_thread = lo("tm") * lo("tn") * K;
+        b.ctas = M / (lo("thr_m") * lo("tm")) * (N / (lo("thr_n") * lo("tn"))) * hi("split");
+        per_thread = lo("tm") * lo("tn") * K / hi("split");
       } else {
         b.ctas = M / 128 * (N / lo("bn"));
       }

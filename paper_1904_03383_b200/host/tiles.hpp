@@ -43,6 +43,10 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
 
 bool is_tile_kind(const std::string& kind);
 
+// Checking rule of one configuration: bit-exact for FFMA kernels with one
+// k-ascending fmaf chain per output, norm-wise (TileFamily::rtol) otherwise.
+bool tile_bit_exact(const ispc_tile_config& t);
+
 const char* tiles_space_text();
 
 // Builds the space (null ctx + diagnostics on failure, like build_gpu_space).

@@ -112,6 +112,7 @@ inline void ispc_cp_async_wait() {}
 inline unsigned ispc_cluster_rank() { return 0; }  // clusters of one CTA only
 inline void ispc_cluster_sync() { emu_yield_barrier(); }
 inline float ispc_dsmem_ld(const float* p, unsigned) { return *p; }
+inline float4 ispc_dsmem_ld4(const float* p, unsigned) { return emu_ld(reinterpret_cast<const float4*>(p)); }
 
 inline int ispc_timeout_flag = 0;
 inline unsigned long long ispc_now() { return 0; }

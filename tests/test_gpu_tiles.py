@@ -155,3 +155,25 @@ def test_tcgen05_sgemm(dev, engine):
         assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
         ok += 1
     assert ok >= 1
+
+
+@pytest.mark.parametrize("split", ["2", "4", "8"])
+def test_sgemm_split_k_cluster(dev, split):
+    """Split-K over a cluster, partials summed through DSMEM (norm-wise 1e-5)."""
+    space = Space("sgemm", m=1024, n=1024, k=1024)
+    dev.bind(space.problem())
+    root = space.root().decide("tile", ["split"], split)
+    ok = 0
+    for seed in range(20):
+        try:
+            leaf, _, _ = root.random_leaf(seed)
+        except DeadEnd:
+            continue
+        t = leaf.tiles()
+        m = dev.evaluate_tiles(t, reps=1, warmup=0)
+        if m.status == "illegal":
+            continue
+        assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
+        assert m.launch.cluster[0] == int(split)
+        ok += 1
+    assert ok >= 3

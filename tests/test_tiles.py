@@ -14,8 +14,8 @@ from tests.oracle_lib import Oracle
 SEED = 0x190403383
 
 
-def _leaves(space, n, order=None):
-    root = space.root()
+def _leaves(space, n, order=None, root=None):
+    root = root or space.root()
     out = []
     for seed in range(n):
         try:
@@ -99,11 +99,11 @@ def _regions(orc, p):
             "c": nan(bt * p.m * p.n)}
 
 
-def _emulate_all(space, want, max_threads=256, n=30):
+def _emulate_all(space, want, max_threads=256, n=30, root=None):
     orc = Oracle()
     p = space.problem()
     checked = 0
-    for leaf in _leaves(space, n):
+    for leaf in _leaves(space, n, root=root):
         t = leaf.tiles()
         try:
             src, L = tile_cuda(t, "k_emu")
@@ -128,7 +128,8 @@ def test_sgemm_kernels_bit_exact_on_emulator():
     def want(regs, t):
         assert np.array_equal(regs["c"].view(np.uint32), ref.view(np.uint32)), t.as_dict()
 
-    assert _emulate_all(s, want) >= 5
+    # clusters (split-K) need concurrent CTAs: checked on the GPU
+    assert _emulate_all(s, want, root=s.root().decide("tile", ["split"], "1")) >= 5
 
 
 def test_batched_kernels_bit_exact_on_emulator():
