@@ -158,6 +158,15 @@ CONFIG_SPACES = {
 }
 
 
+def save_best(kind, kw, cand):
+    """Keeps the best candidate (reference text serialization) for
+    tools/profile_best.py (ncu captures of exactly this kernel)."""
+    d = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(d):
+        with open(os.path.join(d, f"best_{kind}.json"), "w") as f:
+            json.dump({"kind": kind, "space": kw, "candidate": cand.serialize()}, f)
+
+
 def run_configs(kinds, args, local, world, rank) -> dict:
     """Bounded searches over the other BASELINE shapes; batched is sharded
     along its batch across ranks (64 problems per GPU at 8 GPUs), the others
@@ -190,6 +199,7 @@ def run_configs(kinds, args, local, world, rank) -> dict:
             r = retime_best(space, best, reps=20, ordinal=local)
             res["best"] = r
             res["best_config"] = best.tiles().as_dict()
+            save_best(kind, kw, best)
         if rank == 0:
             res["cublas"] = cublas_reference(space)
         out[kind] = res
@@ -257,6 +267,8 @@ def run_ours(args, world, rank, local):
     best = search.best()
     best_src = search.best_source()
     search.close()
+    if best is not None and rank == 0:
+        save_best("axpy", {"n": N_AXPY, "factors": FACTORS}, best)
 
     configs = {}
     if args.configs != "none":
