@@ -19,8 +19,12 @@
 //   B  K-major (k contiguous, as in memory): row n = 32 k (128 B), 8-row
 //      atoms, SBO = 1 KiB; the k step inside the 128-B row advances the
 //      descriptor start by 32 B
-// TF32X3 (split operands, three MMAs) is a separate engine value; this build
-// implements TF32.
+// TF32X3 (engine value): 256 threads; warps 4-7 split every landed stage in
+// place, x -> big = cvt.rna.tf32(x) (exactly representable) and, in a second
+// buffer of the same swizzled layout, small = x - big; they fence the writes
+// to the async proxy and arrive on conv[s]. The MMA lane then issues
+// big*big + big*small + small*big per k step (fp32-level accuracy from the
+// TF32 pipe). The epilogue splits the columns between warps w and w+4.
 #include <cstdio>
 #include <cstring>
 #include <sstream>
@@ -69,6 +73,14 @@ static __device__ __forceinline__ void ispc_mma_tf32(unsigned tmem, unsigned lon
       " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem), "l"(da), "l"(db), "r"(idesc),
       "r"(accumulate) : "memory");
 }
+static __device__ __forceinline__ void ispc_mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+static __device__ __forceinline__ float ispc_tf32_rna(float x) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
 static __device__ __forceinline__ void ispc_mma_commit(unsigned bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -90,15 +102,18 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   const int64_t M = c.m, N = c.n, K = c.k;
   const int BN = c.bn, S = c.stages;
   if (c.staging != ISPC_STAGE_TMA) illegal("the tensor-core tile reads TMA-staged operands");
-  if (c.engine == ISPC_ENGINE_TF32X3) illegal("TF32X3 engine not implemented in this build");
-  if (c.engine != ISPC_ENGINE_TF32) illegal("tcgen05 kernel needs a tensor engine");
+  if (c.engine != ISPC_ENGINE_TF32 && c.engine != ISPC_ENGINE_TF32X3) illegal("tcgen05 kernel needs a tensor engine");
+  const bool X3 = c.engine == ISPC_ENGINE_TF32X3;
+  const int T = X3 ? 256 : 128;
   if (!(BN == 64 || BN == 128 || BN == 256)) illegal("UMMA N must be 64, 128 or 256");
   if (S < 2 || S > 8) illegal("TMA ring depth must be 2..8");
   if (M % 128 || N % BN || K % 32) illegal("shape not divisible by the 128 x BN x 32 tile");
   if (M > (int64_t(1) << 31) || K > (int64_t(1) << 31)) illegal("shape too large for the tensor maps");
-  const int64_t a_bytes = 128 * 32 * 4, b_bytes = int64_t(BN) * 32 * 4, stage = a_bytes + b_bytes;
+  const int64_t a_bytes = 128 * 32 * 4, b_bytes = int64_t(BN) * 32 * 4, tma_bytes = a_bytes + b_bytes;
+  const int64_t stage = tma_bytes * (X3 ? 2 : 1);  // [A big][B big]([A small][B small])
   const int64_t bar_off = S * stage;
-  const int64_t smem = bar_off + (2 * S + 2) * 8 + 1024;  // + slack to 1 KiB-align the base
+  const int nbar = 3 * S + 1;                     // full[S], empty[S], conv[S], acc
+  const int64_t smem = bar_off + (nbar + 1) * 8 + 1024;  // + slack to 1 KiB-align the base
   if (smem > 232448) illegal("TMA ring exceeds 227 KiB of shared memory");
   const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (unsigned(BN >> 3) << 17) |
                          (unsigned(128 >> 4) << 24);
@@ -106,18 +121,20 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
 
   std::ostringstream o;
   o << tcgen05_prelude();
-  o << "extern \"C\" __global__ void __launch_bounds__(128, 1) " << fn
+  o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", 1) " << fn
     << "(const __grid_constant__ ispc_tmap_t tm_a, const __grid_constant__ ispc_tmap_t tm_b, float* __restrict__ g_c) {\n";
   o << "  extern __shared__ __align__(1024) unsigned char ispc_smem_raw[];\n";
   o << "  const unsigned raw = ispc_smem_addr(ispc_smem_raw);\n";
   o << "  const unsigned base = (raw + 1023u) & ~1023u;\n";
-  o << "  const unsigned bars = base + " << bar_off << "u;  // full[S], empty[S], acc, tmem slot\n";
+  o << "  const unsigned bars = base + " << bar_off << "u;  // full[S], empty[S], conv[S], acc, tmem slot\n";
   o << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
   o << "  const int m_blk = blockIdx.x % " << MB << ", n_blk = blockIdx.x / " << MB << ";\n";
   o << "  unsigned char* gen = ispc_smem_raw + (base - raw);\n";
-  o << "  unsigned* tmem_slot = (unsigned*)(gen + " << bar_off + (2 * S + 1) * 8 << ");\n";
+  o << "  unsigned* tmem_slot = (unsigned*)(gen + " << bar_off + nbar * 8 << ");\n";
+  o << "  const unsigned acc_bar = bars + " << 8 * 3 * S << "u;\n";
   o << "  if (threadIdx.x == 0) {\n";
-  o << "    for (int s = 0; s < " << 2 * S + 1 << "; ++s) ispc_mbar_init(bars + 8u * s, 1);\n";
+  o << "    for (int s = 0; s < " << nbar << "; ++s) ispc_mbar_init(bars + 8u * s, (s >= " << 2 * S << " && s < "
+    << 3 * S << ") ? 128u : 1u);\n";
   o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
   o << "    asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&tm_a) : \"memory\");\n";
   o << "    asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&tm_b) : \"memory\");\n";
@@ -138,7 +155,7 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   o << "      if (kb >= " << S << ") ispc_mbar_wait(bars + 8u * (" << S << " + s), ((kb / " << S << ") + 1) & 1);\n";
   o << "      const unsigned full = bars + 8u * s;\n";
   o << "      const unsigned sa = base + s * " << stage << "u, sb = sa + " << a_bytes << "u;\n";
-  o << "      ispc_mbar_expect_tx(full, " << stage << "u);\n";
+  o << "      ispc_mbar_expect_tx(full, " << tma_bytes << "u);\n";
   o << "      #pragma unroll\n";
   o << "      for (int i = 0; i < 4; ++i) ispc_tma_2d(sa + i * 4096u, &tm_a, m_blk * 128 + i * 32, kb * 32, full);\n";
   o << "      ispc_tma_2d(sb, &tm_b, kb * 32, n_blk * " << BN << ", full);\n";
@@ -147,29 +164,63 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   // MMA issuer
   o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
   o << "      const int s = kb % " << S << ";\n";
-  o << "      ispc_mbar_wait(bars + 8u * s, (kb / " << S << ") & 1);\n";
+  o << "      ispc_mbar_wait(bars + 8u * (" << (X3 ? 2 * S : 0) << " + s), (kb / " << S << ") & 1);\n";
   o << "      asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
   o << "      const unsigned sa = base + s * " << stage << "u, sb = sa + " << a_bytes << "u;\n";
   o << "      #pragma unroll\n";
   o << "      for (int kk = 0; kk < 4; ++kk) {\n";
   o << "        const unsigned long long da = ispc_umma_desc(sa + kk * 1024u, 4096u, 1024u);\n";
   o << "        const unsigned long long db = ispc_umma_desc(sb + kk * 32u, 16u, 1024u);\n";
-  o << "        ispc_mma_tf32(tmem, da, db, " << idesc << "u, (kb | kk) != 0);\n";
+  if (X3) {
+    o << "        const unsigned long long das = ispc_umma_desc(sa + " << tma_bytes << "u + kk * 1024u, 4096u, 1024u);\n";
+    o << "        const unsigned long long dbs = ispc_umma_desc(sb + " << tma_bytes << "u + kk * 32u, 16u, 1024u);\n";
+    o << "        ispc_mma_tf32(tmem, das, db, " << idesc << "u, (kb | kk) != 0);\n";
+    o << "        ispc_mma_tf32(tmem, da, dbs, " << idesc << "u, 1u);\n";
+    o << "        ispc_mma_tf32(tmem, da, db, " << idesc << "u, 1u);\n";
+  } else {
+    o << "        ispc_mma_tf32(tmem, da, db, " << idesc << "u, (kb | kk) != 0);\n";
+  }
   o << "      }\n";
   o << "      ispc_mma_commit(bars + 8u * (" << S << " + s));\n";
   o << "    }\n";
-  o << "    ispc_mma_commit(bars + " << 16 * S << "u);\n";
-  o << "  }\n";
-  o << "  __syncwarp();\n";
+  o << "    ispc_mma_commit(acc_bar);\n";
+  o << "  }";
+  if (X3) {
+    // converters: warps 4-7 split each landed stage into big / small parts
+    o << " else if (warp >= 4) {\n";
+    o << "    const int t = threadIdx.x - 128;\n";
+    o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
+    o << "      const int s = kb % " << S << ";\n";
+    o << "      ispc_mbar_wait(bars + 8u * s, (kb / " << S << ") & 1);\n";
+    o << "      float4* big = (float4*)(gen + s * " << stage << ");\n";
+    o << "      float4* small = (float4*)(gen + s * " << stage << " + " << tma_bytes << ");\n";
+    o << "      #pragma unroll 4\n";
+    o << "      for (int i = t; i < " << tma_bytes / 16 << "; i += 128) {\n";
+    o << "        const float4 x = big[i];\n";
+    o << "        float4 hi, lo;\n";
+    o << "        hi.x = ispc_tf32_rna(x.x); hi.y = ispc_tf32_rna(x.y); hi.z = ispc_tf32_rna(x.z); hi.w = ispc_tf32_rna(x.w);\n";
+    o << "        lo.x = x.x - hi.x; lo.y = x.y - hi.y; lo.z = x.z - hi.z; lo.w = x.w - hi.w;\n";
+    o << "        big[i] = hi;\n";
+    o << "        small[i] = lo;\n";
+    o << "      }\n";
+    o << "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
+    o << "      ispc_mbar_arrive(bars + 8u * (" << 2 * S << " + s));\n";
+    o << "    }\n";
+    o << "  }";
+  }
+  o << "\n  __syncwarp();\n";
   // epilogue
-  o << "  ispc_mbar_wait(bars + " << 16 * S << "u, 0);\n";
+  // epilogue: TMEM lane group = warp % 4; X3 splits the columns between w, w+4
+  const int cols = X3 ? BN / 2 : BN;
+  o << "  ispc_mbar_wait(acc_bar, 0);\n";
   o << "  asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
-  o << "  const long long row = (long long)m_blk * 128 + warp * 32 + lane;\n";
+  o << "  const int lg = warp & 3, c_begin = (warp >> 2) * " << cols << ";\n";
+  o << "  const long long row = (long long)m_blk * 128 + lg * 32 + lane;\n";
   o << "  float* pc = g_c + row + (long long)n_blk * " << BN << " * " << M << "LL;\n";
   o << "  #pragma unroll 1\n";
-  o << "  for (int c0 = 0; c0 < " << BN << "; c0 += 32) {\n";
+  o << "  for (int c0 = c_begin; c0 < c_begin + " << cols << "; c0 += 32) {\n";
   o << "    unsigned r[32];\n";
-  o << "    ISPC_TMEM_LD32(tmem + ((unsigned)(warp * 32) << 16) + c0, r);\n";
+  o << "    ISPC_TMEM_LD32(tmem + ((unsigned)(lg * 32) << 16) + c0, r);\n";
   o << "    asm volatile(\"tcgen05.wait::ld.sync.aligned;\" ::: \"memory\");\n";
   o << "    #pragma unroll\n";
   o << "    for (int j = 0; j < 32; ++j) pc[(long long)(c0 + j) * " << M << "LL] = __uint_as_float(r[j]);\n";
@@ -182,7 +233,7 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   o << "}\n";
 
   L.grid_x = uint64_t(MB * (N / BN));
-  L.block[0] = 128;
+  L.block[0] = uint32_t(T);
   L.block[1] = L.block[2] = 1;
   L.static_smem = uint32_t(smem);
   // parameters: tensor maps over a and b, region c
