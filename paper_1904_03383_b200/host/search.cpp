@@ -189,7 +189,9 @@ bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound) 
           ++pruned_;
           continue;
         }
-        if (std::isfinite(T)) weight = T - b;
+        // p ~ max(T - b, 0); before the first measurement
+        // there is no T, and the bound itself ranks the children (p ~ 1/b)
+        weight = std::isfinite(T) ? T - b : 1.0 / std::max(b, 1e-12);
       }
       kids.push_back(std::move(child));
       w.push_back(weight);
