@@ -1,0 +1,24 @@
+#!/bin/bash
+# One gpurun call's worth of evidence: GPU tests, the bench line, the ncu
+# launch list of a short bench run and full ncu captures of each best kernel.
+# Usage (under gpurun): bash tools/gpu_round.sh <tag> [skip-tests]
+set -u
+TAG=${1:-r01}
+OUT=gpurun_out
+mkdir -p $OUT
+if [ "${2:-}" != "skip-tests" ]; then
+  timeout 1200 python -m pytest tests -m gpu -q > $OUT/${TAG}_pytest.log 2>&1; echo "pytest=$?" >> $OUT/${TAG}_pytest.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/${TAG}_smoke.log 2>&1; echo "smoke=$?" >> $OUT/${TAG}_smoke.log
+fi
+timeout 1500 python bench.py --steps 5 --warmup 3 > $OUT/${TAG}_bench.log 2>&1; echo "bench=$?" >> $OUT/${TAG}_bench.log
+nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/${TAG}_smi_after.csv 2>&1
+# launch list (cold-cache, serialised: compare shares, not absolutes)
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/${TAG}_launches.csv \
+  python bench.py --steps 1 --warmup 1 --per-step 16 --configs none --no-cpu-baseline > $OUT/${TAG}_ncu_bench.log 2>&1
+for k in axpy gemv sgemm batched sgemm_tc; do
+  if [ -f $OUT/best_$k.json ]; then
+    timeout 600 ncu --set full --import-source on --clock-control none -k regex:^ispc_[kt] -s 4 -c 1 \
+      -o $OUT/${TAG}_prof_$k -f python tools/profile_best.py $k > $OUT/${TAG}_prof_$k.log 2>&1
+  fi
+done
+echo done > $OUT/${TAG}_done.txt
