@@ -81,7 +81,7 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     TileParam vec = P("vec", dividing({1, 2, 4}, m));
     TileParam lm = P("lanes_m", pow2_upto(1, 32)), ln = P("lanes_n", dividing(pow2_upto(1, 32), n));
     TileParam wm = P("warps_m", pow2_upto(1, 8)), wn = P("warps_n", dividing(pow2_upto(1, 32), n));
-    TileParam split = P("split", dividing({1, 2, 4, 8}, n)), unroll = P("unroll", dividing({1, 2, 4, 8}, n));
+    TileParam split = P("split", dividing({1, 2, 4, 8}, n)), unroll = P("unroll", dividing({1, 2, 4, 8, 16}, n));
     lm.thread = ln.thread = wm.thread = wn.thread = true;
     lm.warp = ln.warp = true;
     vec.acc = unroll.acc = true;
@@ -89,7 +89,7 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     f.params = {vec, lm, ln, wm, wn, split, unroll};
     f.min_threads = 32;
     f.warp_lanes = 32;
-    f.max_acc = 32;
+    f.max_acc = 64;
     pre("staging", {"DIRECT"});
     pre("engine", {"FFMA"});
   } else if (kind == "sgemm") {
