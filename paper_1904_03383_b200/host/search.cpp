@@ -4,6 +4,7 @@
 #include <sys/mman.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -443,12 +444,15 @@ void Search::launch_worker() {
           }
         }
         if (log_) {
+          std::string compact = improved ? best_text_ : std::string();
+          std::replace(compact.begin(), compact.end(), '\n', ' ');
           std::fprintf(log_,
                        "{\"i\": %lld, \"t\": %.4f, \"status\": \"%s\", \"median_ns\": %.1f, \"bound_ns\": %.1f, "
-                       "\"incumbent_ns\": %.1f, \"hash\": \"%016llx\", \"digest\": \"%016llx\", \"best\": %s}\n",
+                       "\"incumbent_ns\": %.1f, \"hash\": \"%016llx\", \"digest\": \"%016llx\", \"best\": %s%s%s}\n",
                        (long long)st_.evaluations, t_now, status.c_str(), rc == ISPC_OK ? r.median_ns : -1.0,
                        w->bound_s * 1e9, inc_.seconds() * 1e9, (unsigned long long)w->launch.source_hash,
-                       (unsigned long long)w->digest, improved ? "true" : "false");
+                       (unsigned long long)w->digest, improved ? "true" : "false",
+                       improved ? ", \"candidate\": " : "", compact.c_str());
           std::fflush(log_);
         }
         if (step_open && st_.evaluations >= target_.load()) {

@@ -169,3 +169,15 @@ def test_illegal_configurations_are_rejected():
     t.bk = 3
     with pytest.raises(EmitError):
         tile_cuda(t)
+
+
+def test_cli_codegen_and_bound(capsys):
+    from paper_1904_03383_b200 import cli
+    assert cli.main(["codegen", "sgemm", "--m", "64", "--n", "64", "--k", "64", "--seed", "2"]) == 0
+    src = capsys.readouterr().out
+    assert "__global__" in src and "__fmaf_rn" in src
+    assert cli.main(["bound", "gemv", "--m", "4096", "--n", "4096", "--root"]) == 0
+    b = __import__("json").loads(capsys.readouterr().out)
+    assert b["dram"] > 8e-6 and b["total"] >= b["dram"]
+    assert cli.main(["codegen", "axpy", "--n", "1024", "--factors", "4", "2,8,32", "--seed", "1"]) == 0
+    assert "__global__" in capsys.readouterr().out
