@@ -19,7 +19,7 @@ import argparse
 import json
 import sys
 
-from .api import DeadEnd, Search, Space, tile_cuda
+from .api import DeadEnd, EmitError, Search, Space, tile_cuda
 
 
 def _space(a) -> Space:
@@ -53,14 +53,22 @@ def cmd_explore(a) -> int:
 
 
 def cmd_codegen(a) -> int:
+    """Source of the given candidate, or of the first runnable random leaf
+    from --seed on (the space admits leaves a B200 cannot run)."""
     space = _space(a)
-    c = _candidate(space, a)
-    if space.tiles:
-        src, _ = tile_cuda(c.tiles())
-    else:
-        src, _ = c.nest().cuda()
-    sys.stdout.write(src)
-    return 0
+    last = None
+    for attempt in range(1 if a.candidate else 100):
+        a2 = argparse.Namespace(**{**vars(a), "seed": a.seed + attempt})
+        try:
+            c = _candidate(space, a2)
+            src, _ = tile_cuda(c.tiles()) if space.tiles else c.nest().cuda()
+        except (EmitError, DeadEnd) as e:
+            last = e
+            continue
+        sys.stdout.write(src)
+        return 0
+    print(f"no runnable leaf: {last}", file=sys.stderr)
+    return 3
 
 
 def cmd_bound(a) -> int:
