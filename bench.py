@@ -331,6 +331,8 @@ def run_ours(args, world, rank, local):
 
 
 def main():
+    import faulthandler
+    faulthandler.dump_traceback_later(float(os.environ.get("BENCH_STACK_DUMP_S", "900")), exit=False)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -101,6 +102,7 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
   if (!space_->tiles) model_ = std::make_unique<BoundModel>(space_->kernel, *space_->ctx, machine_);
   order_ = DecisionOrder::from_names(*space_->ctx, split(order_text_));
   inc_.open(shm_text_.empty() ? nullptr : shm_text_.c_str());
+  trace_ = std::getenv("ISPC_TRACE") != nullptr;
   if (!log_text_.empty()) log_ = std::fopen(log_text_.c_str(), "w");
   expand_frontier();
 
@@ -396,6 +398,11 @@ void Search::launch_worker() {
         }
       }
       const double T = inc_.seconds();
+      if (trace_)
+        std::fprintf(stderr, "[ispc] launch %lld %s grid=%llu block=%u,%u,%u smem=%u wd=%u\n",
+                     (long long)st_.evaluations + 1, w->launch.name, (unsigned long long)w->launch.grid_x,
+                     w->launch.block[0], w->launch.block[1], w->launch.block[2], w->launch.static_smem,
+                     w->launch.watchdog);
       ispc_time_opts to{};
       to.warmup = uint32_t(std::max(0, cfg_.warmup));
       to.reps = uint32_t(cfg_.reps);
@@ -446,10 +453,11 @@ void Search::launch_worker() {
         if (log_) {
           std::string compact = improved ? best_text_ : std::string();
           std::replace(compact.begin(), compact.end(), '\n', ' ');
+          const double logged_ns = rc == ISPC_OK && std::isfinite(r.median_ns) ? r.median_ns : -1.0;
           std::fprintf(log_,
                        "{\"i\": %lld, \"t\": %.4f, \"status\": \"%s\", \"median_ns\": %.1f, \"bound_ns\": %.1f, "
                        "\"incumbent_ns\": %.1f, \"hash\": \"%016llx\", \"digest\": \"%016llx\", \"best\": %s%s%s}\n",
-                       (long long)st_.evaluations, t_now, status.c_str(), rc == ISPC_OK ? r.median_ns : -1.0,
+                       (long long)st_.evaluations, t_now, status.c_str(), logged_ns,
                        w->bound_s * 1e9, inc_.seconds() * 1e9, (unsigned long long)w->launch.source_hash,
                        (unsigned long long)w->digest, improved ? "true" : "false",
                        improved ? ", \"candidate\": " : "", compact.c_str());

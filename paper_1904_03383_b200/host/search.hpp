@@ -107,6 +107,7 @@ class Search {
   bool pipeline_started_ = false;
   bool launching_ = false;  // guarded by mu_
   bool step_open_ = false;  // guarded by mu_: device mark 0 recorded for this step
+  bool trace_ = false;      // ISPC_TRACE: one stderr line per launch
 
   // statistics (guarded by mu_ unless atomic)
   ispc_search_stats st_{};
