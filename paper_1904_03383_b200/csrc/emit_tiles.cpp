@@ -453,7 +453,89 @@ std::string sgemm(const ispc_tile_config& c, const std::string& fn, ispc_launch&
 // problems; each problem gets (M/tm)*(N/tn) threads owning a tm x tn output
 // tile. DIRECT reads operands from global (L1); SHARED stages bk-deep slices
 // of every problem's A and B cooperatively. k ascending per output (bit-exact).
+// CP_ASYNC batched: every thread of the CTA works on one problem at a time;
+// the CTA walks its `per_cta` problems in order through a 2-stage cp.async
+// ring, so problem q+1's operands land while problem q is computed. Whole-K
+// slices: A_b (M x K, m contiguous) and B_b stored n-major with k contiguous
+// (row pitch K + 4). k ascending per output (bit-exact).
+std::string batched_pipelined(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
+  const int64_t M = c.m, N = c.n, K = c.k, B = c.batch;
+  const int P = c.per_cta, TM = c.tm, TN = c.tn;
+  if (P < 1 || TM < 1 || TN < 1) illegal("non-positive tile parameter");
+  if (M % TM || N % TN) illegal("thread tile does not divide the problem");
+  if (B % P) illegal("problems per CTA do not divide the batch");
+  const int64_t TPX = M / TM, TPY = N / TN, T = TPX * TPY;
+  if (T > 1024) illegal("more than 1024 threads per CTA");
+  if (T < 32) illegal("fewer than 32 threads per CTA");
+  if (int64_t(TM) * TN > 64) illegal("more than 64 accumulators per thread");
+  const int V = c.vec;
+  if (!(V == 1 || V == 2 || V == 4)) illegal("vector width must be 1, 2 or 4");
+  if (M % V || K % V) illegal("vector width does not divide the problem");
+  const int64_t ldb = K + 4, stage = M * K + N * ldb;
+  const int64_t smem = 2 * stage * 4;
+  if (smem > 232448) illegal("shared memory exceeds 227 KiB");
+  const std::string cp = V == 4 ? (c.cache == ISPC_CACHE_L1 ? "ispc_cp_async_ca16" : "ispc_cp_async_cg16")
+                                : V == 2 ? "ispc_cp_async_ca8" : "ispc_cp_async_ca4";
+  const int64_t a_ch = M * K / V, b_ch = N * K / V;
+  std::ostringstream o;
+  o << "extern \"C\" __global__ void __launch_bounds__(" << T << ") " << fn
+    << "(const float* __restrict__ g_a, const float* __restrict__ g_b, float* __restrict__ g_c) {\n";
+  o << "  extern __shared__ __align__(16) float ispc_smem[];\n";
+  o << "  const int tid = threadIdx.x, tx = tid % " << TPX << ", ty = tid / " << TPX << ";\n";
+  o << "  const long long first = (long long)blockIdx.x * " << P << ";\n";
+  auto issue = [&](const std::string& q, const std::string& ind) {
+    o << ind << "{\n";
+    o << ind << "  float* sa = ispc_smem + ((" << q << ") & 1) * " << stage << ";\n";
+    o << ind << "  float* sb = sa + " << M * K << ";\n";
+    o << ind << "  const float* ga = g_a + (first + (" << q << ")) * " << M * K << "LL;\n";
+    o << ind << "  const float* gb = g_b + (first + (" << q << ")) * " << K * N << "LL;\n";
+    o << ind << "  for (int ch = tid; ch < " << a_ch << "; ch += " << T << ") " << cp << "(sa + ch * " << V
+      << ", ga + ch * " << V << ");\n";
+    o << ind << "  for (int ch = tid; ch < " << b_ch << "; ch += " << T << ") {\n";
+    o << ind << "    const int nn = ch / " << K / V << ", kk = (ch % " << K / V << ") * " << V << ";\n";
+    o << ind << "    " << cp << "(sb + nn * " << ldb << " + kk, gb + nn * " << K << " + kk);\n";
+    o << ind << "  }\n" << ind << "}\n";
+  };
+  issue("0", "  ");
+  o << "  ispc_cp_async_commit();\n";
+  o << "  #pragma unroll 1\n  for (int q = 0; q < " << P << "; ++q) {\n";
+  o << "    if (q + 1 < " << P << ") {\n";
+  issue("q + 1", "      ");
+  o << "    }\n    ispc_cp_async_commit();\n";
+  o << "    ispc_cp_async_wait<1>();\n    __syncthreads();\n";
+  o << "    const float* sa = ispc_smem + (q & 1) * " << stage << ";\n";
+  o << "    const float* sb = sa + " << M * K << ";\n";
+  o << "    float acc[" << TN << "][" << TM << "];\n";
+  o << "    #pragma unroll\n    for (int j = 0; j < " << TN << "; ++j)\n      #pragma unroll\n      for (int i = 0; i < "
+    << TM << "; ++i) acc[j][i] = 0.0f;\n";
+  o << "    #pragma unroll 4\n    for (int k = 0; k < " << K << "; ++k) {\n";
+  o << "      float ra[" << TM << "], rb[" << TN << "];\n";
+  o << "      #pragma unroll\n      for (int i = 0; i < " << TM << "; ++i) ra[i] = sa[k * " << M << " + tx * " << TM
+    << " + i];\n";
+  o << "      #pragma unroll\n      for (int j = 0; j < " << TN << "; ++j) rb[j] = sb[(ty + j * " << TPY << ") * "
+    << ldb << " + k];\n";
+  o << "      #pragma unroll\n      for (int j = 0; j < " << TN << "; ++j)\n";
+  o << "        #pragma unroll\n        for (int i = 0; i < " << TM << "; ++i) acc[j][i] = __fmaf_rn(ra[i], rb[j], acc[j][i]);\n";
+  o << "    }\n";
+  o << "    float* pc = g_c + (first + q) * " << M * N << "LL + tx * " << TM << ";\n";
+  o << "    #pragma unroll\n    for (int j = 0; j < " << TN << "; ++j)\n";
+  o << "      #pragma unroll\n      for (int i = 0; i < " << TM << "; ++i) pc[i + (ty + j * " << TPY << ") * " << M
+    << "] = acc[j][i];\n";
+  o << "    __syncthreads();\n  }\n";
+  o << "  ispc_cp_async_wait<0>();\n}\n";
+  L.grid_x = uint64_t(B / P);
+  L.block[0] = uint32_t(T);
+  L.block[1] = L.block[2] = 1;
+  L.static_smem = uint32_t(smem);
+  add_region(L, "a", B * M * K);
+  add_region(L, "b", B * K * N);
+  add_region(L, "c", B * M * N);
+  L.reg_elems = uint32_t(TM * TN);
+  return o.str();
+}
+
 std::string batched(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
+  if (c.staging == ISPC_STAGE_CP_ASYNC) return batched_pipelined(c, fn, L);
   const int64_t M = c.m, N = c.n, K = c.k, B = c.batch;
   const int P = c.per_cta, TM = c.tm, TN = c.tn, BK = c.bk;
   if (P < 1 || TM < 1 || TN < 1 || BK < 1) illegal("non-positive tile parameter");

@@ -120,7 +120,7 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     f.params = {pc, tm, tn, bk, vec};
     f.min_threads = 1;
     f.max_acc = 64;
-    pre("staging", {"DIRECT", "SHARED"});
+    pre("staging", {"DIRECT", "SHARED", "CP_ASYNC"});
     pre("engine", {"FFMA"});
     pre("xreduce", {"SHUFFLE"});
   } else if (kind == "sgemm_tc") {
