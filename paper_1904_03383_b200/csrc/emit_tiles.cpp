@@ -91,7 +91,18 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
   const int64_t part_off = 0;                                // [WN][R] warp partials
   const int64_t cl_off = direct ? 0 : WN * R;                // [R] CTA partials (cluster)
   const int64_t xr_off = direct ? 0 : WN * R + R;            // [T][V] lane partials
-  const int64_t smem = 4 * (xr_off + (xr_shared ? int64_t(T) * V : 0));
+  // CP_ASYNC staging: a ring of `stages` tiles of R rows x bk columns (column
+  // segments of R contiguous floats) filled by 16-byte cp.async copies
+  const bool staged = c.staging == ISPC_STAGE_CP_ASYNC;
+  if (!staged && c.staging != ISPC_STAGE_DIRECT) illegal("gemv reads A directly or through a cp.async ring");
+  const int64_t CB = staged ? c.bk : 0, ST = staged ? c.stages : 0;
+  if (staged) {
+    if (ST < 2 || CB < 1) illegal("cp.async ring needs >= 2 stages of >= 1 column");
+    if (R % 4) illegal("cp.async column segments need rows per CTA divisible by 4");
+    if (CB % G || (n / S) % CB) illegal("stage columns do not split across column lanes / the CTA slice");
+  }
+  const int64_t ring_off = (xr_off + (xr_shared ? int64_t(T) * V : 0) + 3) / 4 * 4;
+  const int64_t smem = 4 * (staged ? ring_off + ST * R * CB : ring_off);
   if (smem > 232448) illegal("shared memory exceeds 227 KiB");
 
   std::ostringstream o;
@@ -110,17 +121,54 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
   o << "  const float* px = g_x + col0;\n";
   o << "  float acc[" << V << "];\n";
   o << "  #pragma unroll\n  for (int v = 0; v < " << V << "; ++v) acc[v] = 0.0f;\n";
-  o << "  #pragma unroll 1\n  for (long long t = 0; t < " << iters << "LL; t += " << U << ") {\n";
-  o << "    " << ty << " av[" << U << "];\n    float xv[" << U << "];\n";
-  o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; ++u) {\n";
-  o << "      av[u] = " << ld(c.cache, V, "pa + (t + u) * " + std::to_string(G * m) + "LL") << ";\n";
-  o << "      xv[u] = __ldg(px + (t + u) * " << G << "LL);\n";
-  o << "    }\n";
-  o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; ++u) {\n";
-  if (V == 1) o << "      acc[0] = __fmaf_rn(av[u], xv[u], acc[0]);\n";
-  else
-    for (int v = 0; v < V; ++v) o << "      acc[" << v << "] = __fmaf_rn(av[u]" << comp(v) << ", xv[u], acc[" << v << "]);\n";
-  o << "    }\n  }\n";
+  if (!staged) {
+    o << "  #pragma unroll 1\n  for (long long t = 0; t < " << iters << "LL; t += " << U << ") {\n";
+    o << "    " << ty << " av[" << U << "];\n    float xv[" << U << "];\n";
+    o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; ++u) {\n";
+    o << "      av[u] = " << ld(c.cache, V, "pa + (t + u) * " + std::to_string(G * m) + "LL") << ";\n";
+    o << "      xv[u] = __ldg(px + (t + u) * " << G << "LL);\n";
+    o << "    }\n";
+    o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; ++u) {\n";
+    if (V == 1) o << "      acc[0] = __fmaf_rn(av[u], xv[u], acc[0]);\n";
+    else
+      for (int v = 0; v < V; ++v)
+        o << "      acc[" << v << "] = __fmaf_rn(av[u]" << comp(v) << ", xv[u], acc[" << v << "]);\n";
+    o << "    }\n  }\n";
+  } else {
+    const int64_t KT = n / S / CB, chunks = R * CB / 4;
+    const std::string cp = c.cache == ISPC_CACHE_L1 ? "ispc_cp_async_ca16" : "ispc_cp_async_cg16";
+    o << "  float* ring = ispc_smem + " << ring_off << ";\n";
+    o << "  const float* pa_cta = g_a + rblk * " << R << "LL + (long long)rank * " << n / S << "LL * " << m << "LL;\n";
+    o << "  const float* px_cta = g_x + (long long)rank * " << n / S << "LL;\n";
+    o << "  const int cl = wn * " << LN << " + ln, rl = (wm * " << LM << " + lm) * " << V << ";\n";
+    auto issue = [&](const std::string& kt, const std::string& slot, const std::string& ind) {
+      o << ind << "for (int ch = threadIdx.x; ch < " << chunks << "; ch += " << T << ") {\n";
+      o << ind << "  const int cc = ch / " << R / 4 << ", rr = (ch % " << R / 4 << ") * 4;\n";
+      o << ind << "  " << cp << "(ring + (" << slot << ") * " << R * CB << " + cc * " << R << " + rr, pa_cta + rr + ((long long)("
+        << kt << ") * " << CB << " + cc) * " << m << "LL);\n";
+      o << ind << "}\n";
+    };
+    o << "  #pragma unroll\n  for (int s = 0; s < " << ST - 1 << "; ++s) {\n";
+    o << "    if (s < " << KT << ") {\n";
+    issue("s", "s", "      ");
+    o << "    }\n    ispc_cp_async_commit();\n  }\n";
+    o << "  #pragma unroll 1\n  for (int kt = 0; kt < " << KT << "; ++kt) {\n";
+    o << "    ispc_cp_async_wait<" << ST - 2 << ">();\n    __syncthreads();\n";
+    o << "    {\n      const int nk = kt + " << ST - 1 << ";\n      if (nk < " << KT << ") {\n";
+    issue("nk", "nk % " + std::to_string(ST), "        ");
+    o << "      }\n      ispc_cp_async_commit();\n    }\n";
+    o << "    const float* st = ring + (kt % " << ST << ") * " << R * CB << ";\n";
+    o << "    #pragma unroll\n    for (int t = 0; t < " << CB / G << "; ++t) {\n";
+    o << "      const int cc = cl + t * " << G << ";\n";
+    o << "      const float xv = __ldg(px_cta + kt * " << CB << " + cc);\n";
+    o << "      const " << ty << " av = *(const " << ty << "*)(st + cc * " << R << " + rl);\n";
+    if (V == 1) o << "      acc[0] = __fmaf_rn(av, xv, acc[0]);\n";
+    else
+      for (int v = 0; v < V; ++v)
+        o << "      acc[" << v << "] = __fmaf_rn(av" << comp(v) << ", xv, acc[" << v << "]);\n";
+    o << "    }\n  }\n";
+    o << "  ispc_cp_async_wait<0>();\n";
+  }
   // (1) lanes sharing rows (ln) -> lane ln == 0
   if (LN > 1) {
     if (c.xreduce == ISPC_XRED_SHUFFLE) {

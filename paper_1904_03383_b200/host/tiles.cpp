@@ -82,15 +82,17 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     TileParam lm = P("lanes_m", pow2_upto(1, 32)), ln = P("lanes_n", dividing(pow2_upto(1, 32), n));
     TileParam wm = P("warps_m", pow2_upto(1, 8)), wn = P("warps_n", dividing(pow2_upto(1, 32), n));
     TileParam split = P("split", dividing({1, 2, 4, 8}, n)), unroll = P("unroll", dividing({1, 2, 4, 8, 16}, n));
+    TileParam bk = P("bk", {1, 8, 16, 32, 64, 128}), st = P("stages", {1, 2, 3, 4});
     lm.thread = ln.thread = wm.thread = wn.thread = true;
     lm.warp = ln.warp = true;
     vec.acc = unroll.acc = true;
     split.cluster = true;
-    f.params = {vec, lm, ln, wm, wn, split, unroll};
+    bk.stage = st.stage = true;
+    f.params = {vec, lm, ln, wm, wn, split, unroll, bk, st};
     f.min_threads = 32;
     f.warp_lanes = 32;
     f.max_acc = 64;
-    pre("staging", {"DIRECT"});
+    pre("staging", {"DIRECT", "CP_ASYNC"});
     pre("engine", {"FFMA"});
   } else if (kind == "sgemm") {
     if (m <= 0 || n <= 0 || k <= 0) throw std::invalid_argument("sgemm needs m, n, k > 0");
@@ -156,6 +158,7 @@ BuildResult build_tile_space(const TileFamily& f) {
     if (p.warp) bb.add_to_set("WarpParams", o);
     if (p.acc) bb.add_to_set("AccParams", o);
     if (p.cluster) bb.add_to_set("ClusterParams", o);
+    if (p.stage) bb.add_to_set("StageParams", o);
     (*values)[o] = p.values;
   }
   for (const auto& [outer, inner] : f.covers) {
@@ -164,7 +167,7 @@ BuildResult build_tile_space(const TileFamily& f) {
     bb.add_to_param_set("CoverOuter", c, bb.find(outer));
     bb.add_to_param_set("CoverInner", c, bb.find(inner));
   }
-  for (const char* s : {"ThreadParams", "WarpParams", "AccParams", "ClusterParams", "Covers"})
+  for (const char* s : {"ThreadParams", "WarpParams", "AccParams", "ClusterParams", "StageParams", "Covers"})
     if (!bb.sets.count(s)) bb.sets[s] = {};
 
   Providers pv;

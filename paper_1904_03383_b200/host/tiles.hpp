@@ -20,7 +20,7 @@ namespace ispc_host {
 struct TileParam {
   std::string name;
   std::vector<std::int64_t> values;
-  bool thread = false, warp = false, acc = false, cluster = false;
+  bool thread = false, warp = false, acc = false, cluster = false, stage = false;
 };
 
 struct TileFamily {
