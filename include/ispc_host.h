@@ -144,6 +144,8 @@ typedef struct {
   const char* decision_order; /* comma separated choice names; NULL: paper order */
   const char* incumbent_shm;  /* POSIX shm name shared by ranks; NULL: process-local */
   const char* log_path;       /* JSONL evaluation log; NULL: none              */
+  int32_t tree_depth;         /* TAG-MCTS tree over the first decisions (0: 12, <0: off) */
+  int32_t _pad;
 } ispc_search_config;
 
 typedef struct {

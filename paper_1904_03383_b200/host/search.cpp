@@ -103,6 +103,7 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
   order_ = DecisionOrder::from_names(*space_->ctx, split(order_text_));
   inc_.open(shm_text_.empty() ? nullptr : shm_text_.c_str());
   trace_ = std::getenv("ISPC_TRACE") != nullptr;
+  tree_depth_ = cfg_.tree_depth < 0 ? 0 : cfg_.tree_depth == 0 ? 12 : cfg_.tree_depth;
   if (!log_text_.empty()) log_ = std::fopen(log_text_.c_str(), "w");
   expand_frontier();
 
@@ -166,10 +167,135 @@ double Search::bound_total(const Candidate& c) const {
   return model_->bound(c).total;
 }
 
-bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound) {
+// TAG selection (threshold ascent): with s_i the number of child i's
+// samples among the kTop best times seen by the shard, n_i its visits and
+// alpha = ln(2 N kTop / delta), pick argmax (s_i + alpha + sqrt(2 s_i alpha +
+// alpha^2)) / n_i; unvisited children first (drawn by bound, p ~ 1/b).
+// Children whose bound reached the incumbent are skipped.
+int Search::select_child(MctsNode& n, double T, std::mt19937_64& rng) {
+  const double thr = top_.size() >= kTop ? top_.back() : std::numeric_limits<double>::infinity();
+  const double alpha = std::log(2.0 * double(std::max<int64_t>(n.total, 1)) * double(kTop) / 0.01);
+  std::vector<int> fresh;
+  std::vector<double> fresh_w;
+  int best = -1;
+  double best_h = -1;
+  for (size_t i = 0; i < n.kid_cand.size(); ++i) {
+    if (!(n.kid_bound[i] < T)) continue;
+    if (n.kids[i] && n.kids[i]->dead) continue;
+    if (n.visits[i] == 0) {
+      fresh.push_back(int(i));
+      fresh_w.push_back(1.0 / std::max(n.kid_bound[i], 1e-12));
+      continue;
+    }
+    double si = 0;
+    for (double t : n.times[i]) si += (t <= thr) ? 1 : 0;
+    double h = (si + alpha + std::sqrt(2 * si * alpha + alpha * alpha)) / double(n.visits[i]);
+    if (h > best_h) best_h = h, best = int(i);
+  }
+  if (!fresh.empty()) {
+    std::discrete_distribution<size_t> pick(fresh_w.begin(), fresh_w.end());
+    return fresh[pick(rng)];
+  }
+  return best;
+}
+
+void Search::backprop(const std::vector<std::pair<MctsNode*, int>>& path, double ns) {
+  std::lock_guard<std::mutex> lk(tree_mu_);
+  if (std::isfinite(ns)) {
+    top_.insert(std::upper_bound(top_.begin(), top_.end(), ns), ns);
+    if (top_.size() > kTop) top_.pop_back();
+  }
+  for (auto& [node, i] : path) {
+    if (std::isfinite(ns)) node->times[size_t(i)].push_back(ns);
+  }
+}
+
+bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound,
+                     std::vector<std::pair<MctsNode*, int>>& path) {
   const SpaceContext& ctx = *space_->ctx;
-  Candidate cur = subtrees_[size_t(subtree_cursor_++ % subtrees_.size())];
+  const size_t root_i = size_t(subtree_cursor_++ % subtrees_.size());
   const bool prune = cfg_.pruning != 0;
+  path.clear();
+  Candidate cur;
+  // ---- in-tree descent (TAG) over the first tree_depth_ decisions ----
+  MctsNode* node = nullptr;
+  if (tree_depth_ > 0) {
+    std::lock_guard<std::mutex> lk(tree_mu_);
+    if (tree_roots_.size() != subtrees_.size()) {
+      tree_roots_.clear();
+      for (const Candidate& c : subtrees_) {
+        tree_roots_.push_back(std::make_unique<MctsNode>());
+        tree_roots_.back()->cand = c;
+      }
+    }
+    node = tree_roots_[root_i].get();
+  }
+  int depth = 0;
+  while (node && depth < tree_depth_) {
+    const double T = prune ? inc_.seconds() : std::numeric_limits<double>::infinity();
+    if (!node->expanded) {
+      // expand outside the lock (propagation dominates), install under it
+      std::uint32_t inst = order_.pick(ctx, node->cand);
+      std::vector<Candidate> kc;
+      std::vector<double> kb;
+      if (inst != kNoInstance) {
+        Mask m = node->cand.dom[inst];
+        for (int v = 0; v < kMaxDomainBits; ++v) {
+          if (!mask_has(m, v)) continue;
+          Candidate child;
+          if (apply_decision(ctx, node->cand, inst, v, child) != PropStatus::Ok) continue;
+          double b = bound_total(child);
+          if (!std::isfinite(b)) {
+            ++pruned_;
+            continue;
+          }
+          kc.push_back(std::move(child));
+          kb.push_back(b);
+        }
+      }
+      std::lock_guard<std::mutex> lk(tree_mu_);
+      if (!node->expanded) {
+        if (inst == kNoInstance) {  // a leaf inside the tree
+          node->expanded = true;
+        } else {
+          node->kid_cand = std::move(kc);
+          node->kid_bound = std::move(kb);
+          node->kids.resize(node->kid_cand.size());
+          node->visits.assign(node->kid_cand.size(), 0);
+          node->times.assign(node->kid_cand.size(), {});
+          node->expanded = true;
+          if (node->kid_cand.empty()) node->dead = true;
+        }
+      }
+    }
+    std::lock_guard<std::mutex> lk(tree_mu_);
+    if (node->kid_cand.empty()) {
+      if (node->dead) return false;
+      break;  // fully specified inside the tree
+    }
+    int i = select_child(*node, T, rng);
+    if (i < 0) {  // every child pruned or dead under the current incumbent
+      node->dead = node->dead || !std::isfinite(T);
+      ++pruned_;
+      return false;
+    }
+    ++node->visits[size_t(i)];
+    ++node->total;
+    path.emplace_back(node, i);
+    if (!node->kids[size_t(i)]) {
+      node->kids[size_t(i)] = std::make_unique<MctsNode>();
+      node->kids[size_t(i)]->cand = node->kid_cand[size_t(i)];
+    }
+    node = node->kids[size_t(i)].get();
+    ++depth;
+  }
+  if (node) {
+    std::lock_guard<std::mutex> lk(tree_mu_);
+    cur = node->cand;
+  } else {
+    cur = subtrees_[root_i];
+  }
+  // ---- rollout below the tree: p ~ max(T - b, 0) ----
   for (;;) {
     std::uint32_t inst = order_.pick(ctx, cur);
     if (inst == kNoInstance) {
@@ -226,7 +352,7 @@ void Search::rollout_worker(int tid) {
     }
     double t = now();
     auto w = std::make_unique<Work>();
-    bool ok = rollout(rng, w->leaf, w->bound_s);
+    bool ok = rollout(rng, w->leaf, w->bound_s, w->path);
     ++rollouts_;
     if (!ok) {
       ++dead_rollouts_;
@@ -449,6 +575,11 @@ void Search::launch_worker() {
             best_src_ = w->src;
             best_launch_ = w->launch;
           }
+        }
+        if (!w->path.empty()) {
+          const double ns = (rc == ISPC_OK && r.status == ISPC_OK) ? r.median_ns
+                                                                  : std::numeric_limits<double>::infinity();
+          backprop(w->path, ns);
         }
         if (log_) {
           std::string compact = improved ? best_text_ : std::string();

@@ -50,8 +50,25 @@ struct Incumbent {
   bool offer(uint64_t ns);  // true when it became the new best
 };
 
+// One node of the Monte-Carlo tree over the first `tree_depth` decisions of
+// a shard. Children are the propagated
+// values of the node's next decision that survived pruning; per child the
+// search keeps the visit count and the measured times of the leaves below
+// it, for the TAG (threshold ascent on graphs) selection rule.
+struct MctsNode {
+  ispace::Candidate cand;
+  bool expanded = false, dead = false;
+  std::vector<ispace::Candidate> kid_cand;
+  std::vector<double> kid_bound;
+  std::vector<std::unique_ptr<MctsNode>> kids;
+  std::vector<int64_t> visits;
+  std::vector<std::vector<double>> times;  // measured ns of leaves below each child
+  int64_t total = 0;
+};
+
 struct Work {
   ispace::Candidate leaf;
+  std::vector<std::pair<MctsNode*, int>> path;  // tree edges taken (TAG back-propagation)
   std::unique_ptr<NestBuf> nest;
   std::string src;
   ispc_launch launch{};
@@ -127,7 +144,16 @@ class Search {
 
   double bound_total(const ispace::Candidate& c) const;
   void expand_frontier();
-  bool rollout(std::mt19937_64& rng, ispace::Candidate& leaf, double& leaf_bound);
+  bool rollout(std::mt19937_64& rng, ispace::Candidate& leaf, double& leaf_bound,
+               std::vector<std::pair<MctsNode*, int>>& path);
+  // TAG-MCTS state (guarded by tree_mu_)
+  std::mutex tree_mu_;
+  std::vector<std::unique_ptr<MctsNode>> tree_roots_;
+  std::vector<double> top_;  // the kTop best measured times (ns), ascending
+  static constexpr size_t kTop = 16;
+  int tree_depth_ = 12;
+  int select_child(MctsNode& n, double T, std::mt19937_64& rng);
+  void backprop(const std::vector<std::pair<MctsNode*, int>>& path, double ns);
   void rollout_worker(int tid);
   void compile_worker(int tid);
   void launch_worker();
