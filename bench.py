@@ -185,7 +185,7 @@ def run_configs(kinds, args, local, world, rank) -> dict:
         try:
             space = Space(kind, **kw)
             s = Search(space, device=local, seed=0x1904 + rank, reps=3, warmup=1, flush_l2=flush)
-            s.step(evals)
+            s.step(evals, max_seconds=4 * args.step_timeout)
             st = s.stats()
             best = s.best()
             s.close()
@@ -221,8 +221,9 @@ def run_ours(args, world, rank, local):
     search = Search(space, device=local, seed=0x1904 + rank, shard_index=rank, shard_count=world,
                     reps=3, warmup=1, batch=args.batch, incumbent_shm=shm, log_path=log)
     E = args.per_step
+    stalled = 0
     for _ in range(args.warmup):
-        search.step(E)
+        stalled += not search.step(E, max_seconds=args.step_timeout)
 
     # ---- timed steps (inputs resident in HBM) ----
     barrier(world)
@@ -232,7 +233,7 @@ def run_ours(args, world, rank, local):
     t_wall = time.perf_counter()
     with Clocks(local) as clk:
         for _ in range(args.steps):
-            search.step(E)
+            stalled += not search.step(E, max_seconds=args.step_timeout)
             dev_ms.append(search.stats()["device_step_ms"])
     wall = time.perf_counter() - t_wall
     torch.cuda.synchronize()
@@ -256,7 +257,7 @@ def run_ours(args, world, rank, local):
     for _ in range(e2e_steps):
         search.write_region("x", xh.data_ptr(), xh.nbytes)
         search.write_region("y", yh.data_ptr(), yh.nbytes)
-        search.step(E)
+        stalled += not search.step(E, max_seconds=args.step_timeout)
         search.read_region("z", zh.data_ptr(), zh.nbytes)
     e2e_wall = time.perf_counter() - t0
     (e2e_max,) = allreduce([e2e_wall], "max", world)
@@ -323,6 +324,7 @@ def run_ours(args, world, rank, local):
                                       "pruned_children", "bound_violations", "frontier", "t_rollout_s",
                                       "t_compile_s", "t_gpu_s")},
         "wall_s": round(wall, 3),
+        "stalled_steps": stalled,
     }
     print(json.dumps(line))
     if os.path.isdir(os.path.join(ROOT, "gpurun_out")) and best_src:
@@ -343,6 +345,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--configs", default="all", help="all | none | comma list of gemv,sgemm,batched,sgemm_tc")
+    ap.add_argument("--step-timeout", type=float, default=60.0, help="wall seconds a search step may take")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":

@@ -138,7 +138,7 @@ typedef struct {
   int32_t watchdog;         /* emit option (1: always)                          */
   int32_t reps, warmup;     /* timed / untimed launches per candidate           */
   int32_t flush_l2;         /* L2 flush before each launch                      */
-  int32_t max_unrolled;     /* emit budget (0: 2048)                            */
+  int32_t max_unrolled;     /* emit budget (0: 512)                             */
   double budget_factor;     /* watchdog budget = factor x incumbent (0: 3)      */
   double max_budget_ns;     /* budget before any incumbent (0: 50 ms)           */
   const char* decision_order; /* comma separated choice names; NULL: paper order */
@@ -168,6 +168,9 @@ int ispc_search_create(const ispc_space* s, const ispc_search_config* cfg, ispc_
 /* Runs until `evaluations` more kernels were measured (the pipeline keeps
  * running between calls). Records device-timeline marks around the step. */
 int ispc_search_step(ispc_search* h, int64_t evaluations);
+/* Same with a wall-clock deadline: returns ISPC_E_TIMEOUT when fewer kernels
+ * could be produced and measured in `max_seconds` (0: no deadline). */
+int ispc_search_step_for(ispc_search* h, int64_t evaluations, double max_seconds);
 int ispc_search_stats_get(const ispc_search* h, ispc_search_stats* out);
 /* Best candidate (reference text serialization) and its CUDA source. */
 int ispc_search_best(const ispc_search* h, char* buf, size_t cap, size_t* len);

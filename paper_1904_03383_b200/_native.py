@@ -254,6 +254,7 @@ HOST_SYMBOLS = {
     "ispc_bound": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(BoundReport)]),
     "ispc_search_create": (C.c_int, [C.c_void_p, C.POINTER(SearchConfig), C.POINTER(C.c_void_p)]),
     "ispc_search_step": (C.c_int, [C.c_void_p, C.c_int64]),
+    "ispc_search_step_for": (C.c_int, [C.c_void_p, C.c_int64, C.c_double]),
     "ispc_search_stats_get": (C.c_int, [C.c_void_p, C.POINTER(SearchStats)]),
     "ispc_search_best": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "ispc_search_best_source": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),

@@ -374,7 +374,7 @@ class Search:
     def __init__(self, space: Space, *, device: int = 0, seed: int = 1, shard_index: int = 0, shard_count: int = 1,
                  pruning: bool = True, rollout_threads: int = 0, compile_threads: int = 0, batch: int = 8,
                  reps: int = 3, warmup: int = 1, flush_l2: bool = False, watchdog: int = 1,
-                 budget_factor: float = 3.0, max_budget_ns: float = 50e6, max_unrolled: int = 2048,
+                 budget_factor: float = 3.0, max_budget_ns: float = 50e6, max_unrolled: int = 512,
                  decision_order: str | None = None, incumbent_shm: str | None = None, log_path: str | None = None,
                  tree_depth: int = 0):
         self.space = space
@@ -390,10 +390,15 @@ class Search:
             raise RuntimeError(N.host_error())
         self._h = h
 
-    def step(self, evaluations: int):
-        rc = N.host().ispc_search_step(self._h, evaluations)
+    def step(self, evaluations: int, max_seconds: float = 0.0) -> bool:
+        """Measures `evaluations` more kernels; False when `max_seconds`
+        passed first (the pipeline could not produce them in time)."""
+        rc = N.host().ispc_search_step_for(self._h, evaluations, max_seconds)
+        if rc == N.E_TIMEOUT:
+            return False
         if rc != 0:
             raise RuntimeError(N.host().ispc_search_error(self._h).decode())
+        return True
 
     def stats(self) -> dict:
         s = N.SearchStats()

@@ -14,6 +14,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -622,7 +623,20 @@ int ispc_launch_timed(ispc_dev* d, int handle, const ispc_launch* L, const ispc_
                              reinterpret_cast<CUstream>(d->stream), args.data(), nullptr));
     }
     CK(d, cudaEventRecord(d->ev1, d->stream));
-    CK(d, cudaEventSynchronize(d->ev1));
+    // host-side guard: a kernel that outlives every device-side watchdog would
+    // wedge the context; report it as a context-killing fault instead of
+    // blocking forever (the device must be reopened, i.e. the process exits)
+    const double t_wait = host_ns();
+    const double limit_ns = std::max(5e9, 40.0 * budget);
+    for (;;) {
+      cudaError_t q = cudaEventQuery(d->ev1);
+      if (q == cudaSuccess) break;
+      if (q != cudaErrorNotReady) return cuda_fail(d, q, "kernel");
+      if (host_ns() - t_wait > limit_ns)
+        return fail(d, ISPC_E_STICKY, std::string("kernel ") + L->name + " still running after " +
+                                          std::to_string(int(limit_ns / 1e9)) + " s (host guard)");
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
     CK(d, cudaEventElapsedTime(ms, d->ev0, d->ev1));
     return ISPC_OK;
   };

@@ -47,7 +47,7 @@ struct B200Machine {
   bool l2_flushed = false;  // inputs start outside L2 (timed with an L2 flush)
   // per-thread budgets of the emitter (ispc_emit_opts); exceeding them makes
   // every completion unrunnable, i.e. an infinite bound
-  double max_reg_elems = 512;
+  double max_reg_elems = 160;
   double max_unrolled = 16384;
 };
 

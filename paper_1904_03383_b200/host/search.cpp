@@ -93,7 +93,7 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
   if (cfg_.budget_factor <= 0) cfg_.budget_factor = 3.0;
   if (cfg_.max_budget_ns <= 0) cfg_.max_budget_ns = 50e6;
   if (cfg_.reps <= 0) cfg_.reps = 3;
-  if (cfg_.max_unrolled <= 0) cfg_.max_unrolled = 2048;
+  if (cfg_.max_unrolled <= 0) cfg_.max_unrolled = 512;
   unsigned hw = std::max(2u, std::thread::hardware_concurrency());
   if (cfg_.rollout_threads <= 0) cfg_.rollout_threads = int(std::max(1u, hw / 4));
   if (cfg_.compile_threads <= 0) cfg_.compile_threads = int(std::max(1u, hw - unsigned(cfg_.rollout_threads) - 1));
@@ -344,6 +344,7 @@ void Search::rollout_worker(int tid) {
   ispc_emit_opts eo{};
   eo.watchdog = uint32_t(cfg_.watchdog);
   eo.max_unrolled = uint32_t(cfg_.max_unrolled);
+  eo.max_reg_elems = 160;  // register arrays beyond this spill on a 255-register thread anyway
   while (!stop_) {
     {
       std::unique_lock<std::mutex> lk(mu_);
@@ -446,6 +447,13 @@ void Search::compile_worker(int tid) {
     for (auto& w : items) srcs.push_back(w->src.c_str());
     ispc_module* m = nullptr;
     int rc = ispc_compile(srcs.data(), int(srcs.size()), "sm_100a", &m);
+    if (trace_) {
+      size_t bytes = 0;
+      for (auto& w : items) bytes += w->src.size();
+      std::fprintf(stderr, "[ispc] compile %zu kernels (%zu B of source) in %.3f s rc=%d first=%s\n", items.size(), bytes,
+                   now() - t, rc, items.front()->launch.name);
+      std::fflush(stderr);
+    }
     std::vector<std::unique_ptr<CompiledBatch>> out;
     if (rc == ISPC_OK) {
       auto b = std::make_unique<CompiledBatch>();
@@ -524,11 +532,19 @@ void Search::launch_worker() {
         }
       }
       const double T = inc_.seconds();
-      if (trace_)
+      if (trace_) {
         std::fprintf(stderr, "[ispc] launch %lld %s grid=%llu block=%u,%u,%u smem=%u wd=%u\n",
                      (long long)st_.evaluations + 1, w->launch.name, (unsigned long long)w->launch.grid_x,
                      w->launch.block[0], w->launch.block[1], w->launch.block[2], w->launch.static_smem,
                      w->launch.watchdog);
+        std::fflush(stderr);
+        if (const char* dir = std::getenv("ISPC_TRACE_DIR")) {  // the kernel source, for post-mortems
+          if (FILE* f = std::fopen((std::string(dir) + "/" + w->launch.name + ".cu").c_str(), "w")) {
+            std::fputs(w->src.c_str(), f);
+            std::fclose(f);
+          }
+        }
+      }
       ispc_time_opts to{};
       to.warmup = uint32_t(std::max(0, cfg_.warmup));
       to.reps = uint32_t(cfg_.reps);
@@ -626,7 +642,7 @@ void Search::start() {
   pipeline_started_ = true;
 }
 
-int Search::step(int64_t evaluations) {
+int Search::step(int64_t evaluations, double max_seconds) {
   {
     std::lock_guard<std::mutex> lk(mu_);
     target_ = st_.evaluations + evaluations;
@@ -634,8 +650,19 @@ int Search::step(int64_t evaluations) {
   if (!pipeline_started_) start();
   std::unique_lock<std::mutex> lk(mu_);
   auto drained = [&] { return exhausted_ && work_q_.empty() && batch_q_.empty() && !launching_; };
-  while (!(stop_ || st_.evaluations >= target_.load() || drained()))
+  const double t_end = max_seconds > 0 ? now() + max_seconds : std::numeric_limits<double>::infinity();
+  bool late = false;
+  while (!(stop_ || st_.evaluations >= target_.load() || drained())) {
+    if (now() > t_end) {  // the pipeline starved (rollouts/compiles slower than the deadline)
+      late = true;
+      break;
+    }
     cv_done_.wait_for(lk, std::chrono::milliseconds(50));
+  }
+  if (late) {
+    // stop launching for this step once the in-flight kernel returns
+    cv_done_.wait(lk, [&] { return stop_ || !launching_; });
+  }
   if (step_open_) {  // close the device-timeline step of an exhausted search
     ispc_dev_mark(dev_, 1);
     double ms = 0;
@@ -645,7 +672,7 @@ int Search::step(int64_t evaluations) {
   }
   target_ = st_.evaluations;
   if (stop_ && !err_.empty()) return ISPC_E_STICKY;
-  return ISPC_OK;
+  return late ? ISPC_E_TIMEOUT : ISPC_OK;
 }
 
 ispc_search_stats Search::stats() const {
@@ -739,10 +766,13 @@ int ispc_search_create(const ispc_space* s, const ispc_search_config* cfg, ispc_
   }
 }
 
-int ispc_search_step(ispc_search* h, int64_t evaluations) {
+int ispc_search_step(ispc_search* h, int64_t evaluations) { return ispc_search_step_for(h, evaluations, 0); }
+
+int ispc_search_step_for(ispc_search* h, int64_t evaluations, double max_seconds) {
   if (!h) return set_err(ISPC_E_ARG, "null search");
-  int rc = h->s->step(evaluations);
-  if (rc) h->err = h->s->error();
+  int rc = h->s->step(evaluations, max_seconds);
+  if (rc == ISPC_E_TIMEOUT) h->err = "step deadline reached before the evaluation target";
+  else if (rc) h->err = h->s->error();
   return rc;
 }
 

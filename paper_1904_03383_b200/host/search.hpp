@@ -87,7 +87,7 @@ class Search {
  public:
   Search(const ispc_space* space, const ispc_search_config& cfg);
   ~Search();
-  int step(int64_t evaluations);
+  int step(int64_t evaluations, double max_seconds = 0);
   ispc_search_stats stats() const;
   std::string best_candidate() const;
   std::string best_source() const;

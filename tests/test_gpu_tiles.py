@@ -102,14 +102,22 @@ def test_sgemm_small_readback_bit_exact(dev):
     p = space.problem()
     dev.bind(p)
     ref = orc.expected(p)["c"]
+    a = orc.fill(128 * 32, p.seed, "a").reshape(32, 128).T.astype(np.float64)
+    b = orc.fill(32 * 64, p.seed, "b").reshape(64, 32).T.astype(np.float64)
+    c64 = (a @ b).T.ravel()
+    scale = (np.abs(a) @ np.abs(b)).T.ravel()
     ok = 0
     for leaf in _leaves(space, 40):
-        m = dev.evaluate_tiles(leaf.tiles(), reps=1, warmup=0)
+        t = leaf.tiles()
+        m = dev.evaluate_tiles(t, reps=1, warmup=0)
         if m.status == "illegal":
             continue
-        assert m.status == "ok", (leaf.tiles().as_dict(), m, dev.error())
+        assert m.status == "ok", (t.as_dict(), m, dev.error())
         got = dev.read("c", ref.size)
-        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), leaf.tiles().as_dict()
+        if t.split > 1:  # split-K sums cluster partials: norm-wise
+            assert np.max(np.abs(got - c64) / scale) <= 1e-5, t.as_dict()
+        else:
+            assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), t.as_dict()
         ok += 1
     assert ok >= 10
 
