@@ -97,6 +97,12 @@ int ispc_cand_random_leaf(const ispc_space* s, const ispc_cand* from, uint64_t s
  * mem_space,order,cache"). */
 int ispc_cand_random_leaf_ordered(const ispc_space* s, const ispc_cand* from, uint64_t seed, const char* order,
                                   int max_restarts, ispc_cand** out, int64_t* decisions, int64_t* dead_ends);
+/* Knuth's tree-size estimator (the reference's tree_size.cpp is a stub;
+ * SPEC.md:516-567): `probes` random descents from `from` branching like
+ * ispc_count_leaves (or by `order`). out = {leaves, leaves_stderr, nodes,
+ * dead-end probe ratio, probes}. */
+int ispc_estimate_tree(const ispc_space* s, const ispc_cand* from, int64_t probes, uint64_t seed, const char* order,
+                       double out[5]);
 /* Exhaustive first-open enumeration; returns the number of leaves (capped). */
 int64_t ispc_count_leaves(const ispc_space* s, const ispc_cand* from, int64_t cap);
 

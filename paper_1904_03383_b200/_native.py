@@ -242,6 +242,8 @@ HOST_SYMBOLS = {
     "ispc_cand_random_leaf_ordered": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_char_p, C.c_int,
                                                 C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "ispc_count_leaves": (C.c_int64, [C.c_void_p, C.c_void_p, C.c_int64]),
+    "ispc_estimate_tree": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_uint64, C.c_char_p,
+                                     C.POINTER(C.c_double)]),
     "ispc_cand_to_nest": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
     "ispc_cand_to_tiles": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(TileConfig)]),
     "ispc_nest_buf_get": (C.POINTER(Nest), [C.c_void_p]),

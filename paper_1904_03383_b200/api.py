@@ -138,6 +138,14 @@ class Candidate:
             raise DeadEnd("random descent gave up")
         return Candidate(self.space, h), dec.value, dead.value
 
+    def estimate_tree(self, probes: int = 1000, seed: int = 1, order: str | None = None) -> dict:
+        """Knuth's estimate of the subtree below this candidate."""
+        out = (C.c_double * 5)()
+        rc = N.host().ispc_estimate_tree(self.space._h, self._h, probes, seed, order.encode() if order else None, out)
+        if rc != 0:
+            raise ValueError(N.host_error())
+        return dict(zip(("leaves", "leaves_stderr", "nodes", "dead_probe_ratio", "probes"), list(out)))
+
     def count_leaves(self, cap: int = 10 ** 7) -> int:
         return N.host().ispc_count_leaves(self.space._h, self._h, cap)
 

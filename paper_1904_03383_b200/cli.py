@@ -6,6 +6,7 @@ proj/tools/src/main.cpp:1; its commands are specified at SPEC.md:569-604).
   python -m paper_1904_03383_b200.cli codegen  sgemm --m 1024 --n 1024 --k 1024 [--candidate c.json] [--seed 3]
   python -m paper_1904_03383_b200.cli bound    matmul --m 64 --n 64 --k 64 --factors 2,4 [--candidate c.json]
   python -m paper_1904_03383_b200.cli replay   run.jsonl axpy --n 1048576 --factors 2,4 32,64,128
+  python -m paper_1904_03383_b200.cli estimate matmul --m 256 --n 256 --k 32 --factors 2,4,8,16,32 2,4 --probes 500
 
 `codegen` and `bound` need no GPU. `explore` and `replay` run on cuda device
 `--device`. A candidate file holds the reference's text serialization
@@ -78,6 +79,13 @@ def cmd_bound(a) -> int:
     return 0
 
 
+def cmd_estimate(a) -> int:
+    """Knuth's estimate of the space size (the reference's tree_size is a stub)."""
+    space = _space(a)
+    print(json.dumps(space.root().estimate_tree(a.probes, seed=a.seed, order=a.order)))
+    return 0
+
+
 def cmd_replay(a) -> int:
     from .api import Device
     space = _space(a)
@@ -126,6 +134,11 @@ def main(argv=None) -> int:
     p.add_argument("--root", action="store_true")
     p.add_argument("--l2-flushed", action="store_true")
     p.set_defaults(fn=cmd_bound)
+    p = sub.add_parser("estimate")
+    common(p)
+    p.add_argument("--probes", type=int, default=1000)
+    p.add_argument("--order", default=None)
+    p.set_defaults(fn=cmd_estimate)
     p = sub.add_parser("replay")
     p.add_argument("log_file")
     common(p)

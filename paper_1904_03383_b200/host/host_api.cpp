@@ -252,6 +252,38 @@ int64_t ispc_count_leaves(const ispc_space* s, const ispc_cand* from, int64_t ca
   return n;
 }
 
+int ispc_estimate_tree(const ispc_space* s, const ispc_cand* from, int64_t probes, uint64_t seed, const char* order,
+                       double out[5]) {
+  try {
+    if (!s || !from || !out || probes <= 0) return set_err(ISPC_E_ARG, "bad argument");
+    std::mt19937_64 rng(seed);
+    DecisionOrder ord;
+    if (order) {
+      std::vector<std::string> names;
+      std::string cur;
+      for (const char* p = order;; ++p) {
+        if (*p == ',' || *p == 0) {
+          if (!cur.empty()) names.push_back(cur);
+          cur.clear();
+          if (!*p) break;
+        } else {
+          cur += *p;
+        }
+      }
+      ord = DecisionOrder::from_names(*s->ctx, names);
+    }
+    TreeEstimate e = knuth_estimate(*s->ctx, from->c, probes, rng, order ? &ord : nullptr);
+    out[0] = e.leaves;
+    out[1] = e.leaves_stderr;
+    out[2] = e.nodes;
+    out[3] = e.dead_probe_ratio;
+    out[4] = double(e.probes);
+    return ISPC_OK;
+  } catch (const std::exception& e) {
+    return set_err(ISPC_E_ARG, e.what());
+  }
+}
+
 int ispc_cand_to_tiles(const ispc_space* s, const ispc_cand* c, ispc_tile_config* out) {
   try {
     if (!s || !c || !out) return set_err(ISPC_E_ARG, "null argument");

@@ -62,4 +62,11 @@ bool first_leaf(const ispace::SpaceContext& ctx, const ispace::Candidate& root, 
                 int* budget);
 void count_leaves(const ispace::SpaceContext& ctx, const ispace::Candidate& c, int64_t& n, int64_t cap);
 
+struct TreeEstimate {
+  double leaves = 0, leaves_stderr = 0, nodes = 0, dead_probe_ratio = 0;
+  int64_t probes = 0;
+};
+TreeEstimate knuth_estimate(const ispace::SpaceContext& ctx, const ispace::Candidate& from, int64_t probes,
+                            std::mt19937_64& rng, const DecisionOrder* order);
+
 }  // namespace ispc_host

@@ -95,3 +95,11 @@ def test_serialization_round_trip_keeps_digest():
     leaf, _, _ = space.root().random_leaf(3)
     again = space.deserialize(leaf.serialize())
     assert again.digest == leaf.digest and again.fully_specified
+
+
+def test_knuth_estimate_matches_exact_count():
+    """Knuth's estimator over the same first-open tree count_leaves walks."""
+    s = Space("outer_product", m=2, n=2)
+    est = s.root().estimate_tree(20000, seed=3)
+    assert abs(est["leaves"] - 768) <= 4 * est["leaves_stderr"] + 1e-9
+    assert est["dead_probe_ratio"] == 0.0
