@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -424,8 +425,22 @@ int ispc_compile(const char* const* srcs, int n, const char* arch, ispc_module**
   if (nvrtcCreateProgram(&prog, text.c_str(), "ispc_candidates.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
     return fail(nullptr, ISPC_E_NVRTC, "nvrtcCreateProgram failed");
   std::string arch_opt = std::string("--gpu-architecture=") + (arch ? arch : "sm_100a");
-  const char* opts[] = {arch_opt.c_str(), "--device-as-default-execution-space", "--std=c++17"};
-  nvrtcResult r = nvrtcCompileProgram(prog, 3, opts);
+  std::vector<std::string> extra;  // ISPC_NVRTC_OPTS: space separated extra options (tuning experiments)
+  if (const char* e = std::getenv("ISPC_NVRTC_OPTS")) {
+    std::string cur;
+    for (const char* p = e;; ++p) {
+      if (*p == ' ' || *p == 0) {
+        if (!cur.empty()) extra.push_back(cur);
+        cur.clear();
+        if (!*p) break;
+      } else {
+        cur += *p;
+      }
+    }
+  }
+  std::vector<const char*> opts = {arch_opt.c_str(), "--device-as-default-execution-space", "--std=c++17"};
+  for (const std::string& x : extra) opts.push_back(x.c_str());
+  nvrtcResult r = nvrtcCompileProgram(prog, int(opts.size()), opts.data());
   size_t log_size = 0;
   nvrtcGetProgramLogSize(prog, &log_size);
   m->log.resize(log_size);
