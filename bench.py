@@ -158,6 +158,21 @@ CONFIG_SPACES = {
 }
 
 
+def safe_step(search, evals, seconds) -> bool:
+    """One search step; a context-killing fault (reported by the runtime)
+    ends the step instead of the benchmark."""
+    try:
+        return search.step(evals, max_seconds=seconds)
+    except RuntimeError:
+        return False
+
+
+def N_error(search) -> str | None:
+    from paper_1904_03383_b200 import _native as N
+    e = N.host().ispc_search_error(search._h)
+    return e.decode() if e else None
+
+
 def save_best(kind, kw, cand):
     """Keeps the best candidate (reference text serialization) for
     tools/profile_best.py (ncu captures of exactly this kernel)."""
@@ -167,42 +182,56 @@ def save_best(kind, kw, cand):
             json.dump({"kind": kind, "space": kw, "candidate": cand.serialize()}, f)
 
 
-def run_configs(kinds, args, local, world, rank) -> dict:
-    """Bounded searches over the other BASELINE shapes; batched is sharded
-    along its batch across ranks (64 problems per GPU at 8 GPUs), the others
-    run on rank 0 only (replicas would repeat the same search)."""
+def config_worker(args) -> None:
+    """One bounded search over one BASELINE shape (a child process, so a
+    context-killing fault of one candidate cannot take the others down)."""
     from paper_1904_03383_b200 import Search, Space
     from paper_1904_03383_b200.measure import cublas_reference, retime_best
+    kind = args.config_worker
+    kw, evals, flush = CONFIG_SPACES[kind]
+    kw = dict(kw)
+    if kind == "batched":
+        kw["batch"] = kw["batch"] // max(args.batch_div, 1)
+    t0 = time.perf_counter()
+    space = Space(kind, **kw)
+    s = Search(space, device=args.ordinal, seed=0x1904 + args.ordinal, reps=3, warmup=1, flush_l2=flush)
+    done = s.step(evals, max_seconds=4 * args.step_timeout)
+    st = s.stats()
+    best = s.best()
+    s.close()
+    res = {"shape": kw, "evaluated": st["evaluations"], "ok": st["ok"], "mismatches": st["mismatches"],
+           "illegal": st["illegal"], "launch_errors": st["launch_errors"], "exhausted": bool(st["exhausted"]),
+           "deadline_hit": not done, "time_to_best_s": round(st["time_to_best_s"], 3),
+           "bound_violations": st["bound_violations"], "search_s": round(time.perf_counter() - t0, 2)}
+    if best is not None:
+        res["best"] = retime_best(space, best, reps=20, ordinal=args.ordinal)
+        res["best_config"] = best.tiles().as_dict()
+        save_best(kind, kw, best)
+    if args.with_cublas:
+        res["cublas"] = cublas_reference(space)
+    print("CONFIG_RESULT " + json.dumps(res))
+
+
+def run_configs(kinds, args, local, world, rank) -> dict:
+    """Bounded searches over the other BASELINE shapes, each in a child
+    process; batched is sharded along its batch across ranks (64 problems per
+    GPU at 8 GPUs), the others run on rank 0 only (replicas would repeat the
+    same search)."""
     out = {}
     for kind in kinds:
-        kw, evals, flush = CONFIG_SPACES[kind]
-        kw = dict(kw)
-        if kind == "batched":
-            kw["batch"] = kw["batch"] // world
-        elif rank != 0:
+        if kind != "batched" and rank != 0:
             continue
-        t0 = time.perf_counter()
-        try:
-            space = Space(kind, **kw)
-            s = Search(space, device=local, seed=0x1904 + rank, reps=3, warmup=1, flush_l2=flush)
-            s.step(evals, max_seconds=4 * args.step_timeout)
-            st = s.stats()
-            best = s.best()
-            s.close()
-        except Exception as e:  # report, keep the headline
-            out[kind] = {"error": str(e)}
-            continue
-        res = {"shape": kw, "evaluated": st["evaluations"], "ok": st["ok"], "mismatches": st["mismatches"],
-               "illegal": st["illegal"], "exhausted": bool(st["exhausted"]), "time_to_best_s": st["time_to_best_s"],
-               "search_s": round(time.perf_counter() - t0, 2)}
-        if best is not None:
-            r = retime_best(space, best, reps=20, ordinal=local)
-            res["best"] = r
-            res["best_config"] = best.tiles().as_dict()
-            save_best(kind, kw, best)
+        cmd = [sys.executable, os.path.abspath(__file__), "--config-worker", kind, "--ordinal", str(local),
+               "--batch-div", str(world), "--step-timeout", str(args.step_timeout)]
         if rank == 0:
-            res["cublas"] = cublas_reference(space)
-        out[kind] = res
+            cmd.append("--with-cublas")
+        try:
+            p = subprocess.run(cmd, capture_output=True, text=True, timeout=8 * args.step_timeout + 300)
+            lines = [l for l in p.stdout.splitlines() if l.startswith("CONFIG_RESULT ")]
+            out[kind] = json.loads(lines[-1][len("CONFIG_RESULT "):]) if lines else {
+                "error": (p.stderr.strip().splitlines() or ["no output"])[-1][:300], "rc": p.returncode}
+        except subprocess.TimeoutExpired:
+            out[kind] = {"error": "config search timed out"}
     return out
 
 
@@ -223,7 +252,7 @@ def run_ours(args, world, rank, local):
     E = args.per_step
     stalled = 0
     for _ in range(args.warmup):
-        stalled += not search.step(E, max_seconds=args.step_timeout)
+        stalled += not safe_step(search, E, args.step_timeout)
 
     # ---- timed steps (inputs resident in HBM) ----
     barrier(world)
@@ -233,7 +262,7 @@ def run_ours(args, world, rank, local):
     t_wall = time.perf_counter()
     with Clocks(local) as clk:
         for _ in range(args.steps):
-            stalled += not search.step(E, max_seconds=args.step_timeout)
+            stalled += not safe_step(search, E, args.step_timeout)
             dev_ms.append(search.stats()["device_step_ms"])
     wall = time.perf_counter() - t_wall
     torch.cuda.synchronize()
@@ -257,7 +286,7 @@ def run_ours(args, world, rank, local):
     for _ in range(e2e_steps):
         search.write_region("x", xh.data_ptr(), xh.nbytes)
         search.write_region("y", yh.data_ptr(), yh.nbytes)
-        stalled += not search.step(E, max_seconds=args.step_timeout)
+        stalled += not safe_step(search, E, args.step_timeout)
         search.read_region("z", zh.data_ptr(), zh.nbytes)
     e2e_wall = time.perf_counter() - t0
     (e2e_max,) = allreduce([e2e_wall], "max", world)
@@ -267,6 +296,7 @@ def run_ours(args, world, rank, local):
     st = search.stats()
     best = search.best()
     best_src = search.best_source()
+    search_error = N_error(search)
     search.close()
     if best is not None and rank == 0:
         save_best("axpy", {"n": N_AXPY, "factors": FACTORS}, best)
@@ -283,7 +313,11 @@ def run_ours(args, world, rank, local):
     roofline = None
     best_info = {}
     if best is not None:
-        r = retime_best(space, best, reps=20, ordinal=local)
+        try:
+            r = retime_best(space, best, reps=20, ordinal=local)
+        except RuntimeError as e:  # the context died under a faulting candidate
+            r = {"status": "error", "error": str(e)}
+            best_info = {"error": str(e)}
         if r.get("status") == "ok":
             roofline = dict(r["roofline"])
             traffic = None
@@ -294,7 +328,10 @@ def run_ours(args, world, rank, local):
             best_info = {"kernel_us": r["kernel_us"], "search_median_us": st["best_ns"] / 1e3,
                          "bound_us": st["best_bound_ns"] / 1e3, "time_to_best_s": st["time_to_best_s"],
                          "grid": r["grid"], "block": r["block"]}
-    cub = cublas_reference(space)
+    try:
+        cub = cublas_reference(space)
+    except Exception as e:  # noqa: BLE001 - reported, not fatal
+        cub = {"error": str(e)}
     cpu = None
     if not args.no_cpu_baseline:
         res = cpu_baseline(args.cpu_seconds, os.cpu_count() or 1)
@@ -325,6 +362,7 @@ def run_ours(args, world, rank, local):
                                       "t_compile_s", "t_gpu_s")},
         "wall_s": round(wall, 3),
         "stalled_steps": stalled,
+        "search_error": search_error,
     }
     print(json.dumps(line))
     if os.path.isdir(os.path.join(ROOT, "gpurun_out")) and best_src:
@@ -346,7 +384,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--configs", default="all", help="all | none | comma list of gemv,sgemm,batched,sgemm_tc")
     ap.add_argument("--step-timeout", type=float, default=60.0, help="wall seconds a search step may take")
+    ap.add_argument("--config-worker", default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--ordinal", type=int, default=0, help=argparse.SUPPRESS)
+    ap.add_argument("--batch-div", type=int, default=1, help=argparse.SUPPRESS)
+    ap.add_argument("--with-cublas", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.config_worker:
+        import torch
+        torch.cuda.set_device(args.ordinal)
+        config_worker(args)
+        return
     world, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, world, rank)

@@ -104,19 +104,22 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   if (c.staging != ISPC_STAGE_TMA) illegal("the tensor-core tile reads TMA-staged operands");
   if (c.engine != ISPC_ENGINE_TF32 && c.engine != ISPC_ENGINE_TF32X3) illegal("tcgen05 kernel needs a tensor engine");
   const bool X3 = c.engine == ISPC_ENGINE_TF32X3;
-  const int T = X3 ? 256 : 128;
+  const int T = 256;
   if (!(BN == 64 || BN == 128 || BN == 256)) illegal("UMMA N must be 64, 128 or 256");
   if (S < 2 || S > 8) illegal("TMA ring depth must be 2..8");
   if (M % 128 || N % BN || K % 32) illegal("shape not divisible by the 128 x BN x 32 tile");
   if (M > (int64_t(1) << 31) || K > (int64_t(1) << 31)) illegal("shape too large for the tensor maps");
+  // stage: [A as landed, m contiguous][B, k contiguous][A k contiguous]
+  //        (X3: [A small][B small]); every part 1 KiB aligned
   const int64_t a_bytes = 128 * 32 * 4, b_bytes = int64_t(BN) * 32 * 4, tma_bytes = a_bytes + b_bytes;
-  const int64_t stage = tma_bytes * (X3 ? 2 : 1);  // [A big][B big]([A small][B small])
+  const int64_t off_b = a_bytes, off_ak = a_bytes + b_bytes, off_aks = off_ak + a_bytes, off_bs = off_aks + a_bytes;
+  const int64_t stage = off_ak + a_bytes + (X3 ? a_bytes + b_bytes : 0);
   const int64_t bar_off = S * stage;
-  const int nbar = 3 * S + 1;                     // full[S], empty[S], conv[S], acc
+  const int nbar = 3 * S + 1;  // full[S], empty[S], conv[S], acc
   const int64_t smem = bar_off + (nbar + 1) * 8 + 1024;  // + slack to 1 KiB-align the base
   if (smem > 232448) illegal("TMA ring exceeds 227 KiB of shared memory");
-  const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (unsigned(BN >> 3) << 17) |
-                         (unsigned(128 >> 4) << 24);
+  // kind::tf32, fp32 accumulate, A and B K-major, N = BN, M = 128
+  const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(128 >> 4) << 24);
   const int64_t KB = K / 32, MB = M / 128;
 
   std::ostringstream o;
@@ -154,26 +157,26 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   o << "      const int s = kb % " << S << ";\n";
   o << "      if (kb >= " << S << ") ispc_mbar_wait(bars + 8u * (" << S << " + s), ((kb / " << S << ") + 1) & 1);\n";
   o << "      const unsigned full = bars + 8u * s;\n";
-  o << "      const unsigned sa = base + s * " << stage << "u, sb = sa + " << a_bytes << "u;\n";
+  o << "      const unsigned sa = base + s * " << stage << "u;\n";
   o << "      ispc_mbar_expect_tx(full, " << tma_bytes << "u);\n";
   o << "      #pragma unroll\n";
   o << "      for (int i = 0; i < 4; ++i) ispc_tma_2d(sa + i * 4096u, &tm_a, m_blk * 128 + i * 32, kb * 32, full);\n";
-  o << "      ispc_tma_2d(sb, &tm_b, kb * 32, n_blk * " << BN << ", full);\n";
+  o << "      ispc_tma_2d(sa + " << off_b << "u, &tm_b, kb * 32, n_blk * " << BN << ", full);\n";
   o << "    }\n";
   o << "  } else if (warp == 1 && lane == 0) {\n";
-  // MMA issuer
+  // MMA issuer: A and B K-major, 128-byte swizzle: SBO = 1 KiB (8 rows), +32 B per K=8 step
   o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
   o << "      const int s = kb % " << S << ";\n";
-  o << "      ispc_mbar_wait(bars + 8u * (" << (X3 ? 2 * S : 0) << " + s), (kb / " << S << ") & 1);\n";
+  o << "      ispc_mbar_wait(bars + 8u * (" << 2 * S << " + s), (kb / " << S << ") & 1);\n";
   o << "      asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
-  o << "      const unsigned sa = base + s * " << stage << "u, sb = sa + " << a_bytes << "u;\n";
+  o << "      const unsigned sa = base + s * " << stage << "u;\n";
   o << "      #pragma unroll\n";
   o << "      for (int kk = 0; kk < 4; ++kk) {\n";
-  o << "        const unsigned long long da = ispc_umma_desc(sa + kk * 1024u, 4096u, 1024u);\n";
-  o << "        const unsigned long long db = ispc_umma_desc(sb + kk * 32u, 16u, 1024u);\n";
+  o << "        const unsigned long long da = ispc_umma_desc(sa + " << off_ak << "u + kk * 32u, 16u, 1024u);\n";
+  o << "        const unsigned long long db = ispc_umma_desc(sa + " << off_b << "u + kk * 32u, 16u, 1024u);\n";
   if (X3) {
-    o << "        const unsigned long long das = ispc_umma_desc(sa + " << tma_bytes << "u + kk * 1024u, 4096u, 1024u);\n";
-    o << "        const unsigned long long dbs = ispc_umma_desc(sb + " << tma_bytes << "u + kk * 32u, 16u, 1024u);\n";
+    o << "        const unsigned long long das = ispc_umma_desc(sa + " << off_aks << "u + kk * 32u, 16u, 1024u);\n";
+    o << "        const unsigned long long dbs = ispc_umma_desc(sa + " << off_bs << "u + kk * 32u, 16u, 1024u);\n";
     o << "        ispc_mma_tf32(tmem, das, db, " << idesc << "u, (kb | kk) != 0);\n";
     o << "        ispc_mma_tf32(tmem, da, dbs, " << idesc << "u, 1u);\n";
     o << "        ispc_mma_tf32(tmem, da, db, " << idesc << "u, 1u);\n";
@@ -184,34 +187,54 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   o << "      ispc_mma_commit(bars + 8u * (" << S << " + s));\n";
   o << "    }\n";
   o << "    ispc_mma_commit(acc_bar);\n";
-  o << "  }";
+  o << "  } else if (warp >= 4) {\n";
+  // converters: the tf32 tensor path reads K-major operands only, so A (m
+  // contiguous in memory) is transposed in shared memory, row m = thread
+  o << "    const int m = threadIdx.x - 128;\n";
+  o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
+  o << "      const int s = kb % " << S << ";\n";
+  o << "      ispc_mbar_wait(bars + 8u * s, (kb / " << S << ") & 1);\n";
+  o << "      unsigned char* st = gen + s * " << stage << ";\n";
+  o << "      const unsigned src_row = (m >> 5) * 4096u + (m & 3) * 4u;\n";
+  o << "      const unsigned dst_row = (m >> 3) * 1024u + (m & 7) * 128u;\n";
+  o << "      #pragma unroll\n";
+  o << "      for (int kq = 0; kq < 8; ++kq) {\n";
+  o << "        float v[4];\n";
+  o << "        #pragma unroll\n";
+  o << "        for (int i = 0; i < 4; ++i) {\n";
+  o << "          const int k = kq * 4 + i;\n";
+  o << "          v[i] = *(const float*)(st + src_row + (k >> 3) * 1024u + (k & 7) * 128u + ((((m & 31) >> 2) ^ (k & 7)) << 4));\n";
+  o << "        }\n";
+  o << "        const unsigned dst = dst_row + ((kq ^ (m & 7)) << 4);\n";
   if (X3) {
-    // converters: warps 4-7 split each landed stage into big / small parts
-    o << " else if (warp >= 4) {\n";
-    o << "    const int t = threadIdx.x - 128;\n";
-    o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
-    o << "      const int s = kb % " << S << ";\n";
-    o << "      ispc_mbar_wait(bars + 8u * s, (kb / " << S << ") & 1);\n";
-    o << "      float4* big = (float4*)(gen + s * " << stage << ");\n";
-    o << "      float4* small = (float4*)(gen + s * " << stage << " + " << tma_bytes << ");\n";
+    o << "        float4 hi, lo;\n";
+    o << "        hi.x = ispc_tf32_rna(v[0]); hi.y = ispc_tf32_rna(v[1]); hi.z = ispc_tf32_rna(v[2]); hi.w = ispc_tf32_rna(v[3]);\n";
+    o << "        lo.x = v[0] - hi.x; lo.y = v[1] - hi.y; lo.z = v[2] - hi.z; lo.w = v[3] - hi.w;\n";
+    o << "        *(float4*)(st + " << off_ak << " + dst) = hi;\n";
+    o << "        *(float4*)(st + " << off_aks << " + dst) = lo;\n";
+  } else {
+    o << "        *(float4*)(st + " << off_ak << " + dst) = make_float4(v[0], v[1], v[2], v[3]);\n";
+  }
+  o << "      }\n";
+  if (X3) {
     o << "      #pragma unroll 4\n";
-    o << "      for (int i = t; i < " << tma_bytes / 16 << "; i += 128) {\n";
-    o << "        const float4 x = big[i];\n";
+    o << "      for (int i = m; i < " << b_bytes / 16 << "; i += 128) {\n";
+    o << "        float4* pb = (float4*)(st + " << off_b << ") + i;\n";
+    o << "        const float4 x = *pb;\n";
     o << "        float4 hi, lo;\n";
     o << "        hi.x = ispc_tf32_rna(x.x); hi.y = ispc_tf32_rna(x.y); hi.z = ispc_tf32_rna(x.z); hi.w = ispc_tf32_rna(x.w);\n";
     o << "        lo.x = x.x - hi.x; lo.y = x.y - hi.y; lo.z = x.z - hi.z; lo.w = x.w - hi.w;\n";
-    o << "        big[i] = hi;\n";
-    o << "        small[i] = lo;\n";
+    o << "        *pb = hi;\n";
+    o << "        *((float4*)(st + " << off_bs << ") + i) = lo;\n";
     o << "      }\n";
-    o << "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
-    o << "      ispc_mbar_arrive(bars + 8u * (" << 2 * S << " + s));\n";
-    o << "    }\n";
-    o << "  }";
   }
-  o << "\n  __syncwarp();\n";
-  // epilogue
-  // epilogue: TMEM lane group = warp % 4; X3 splits the columns between w, w+4
-  const int cols = X3 ? BN / 2 : BN;
+  o << "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
+  o << "      ispc_mbar_arrive(bars + 8u * (" << 2 * S << " + s));\n";
+  o << "    }\n";
+  o << "  }\n";
+  o << "  __syncwarp();\n";
+  // epilogue: TMEM lane group = warp % 4, column half = warp / 4
+  const int cols = BN / 2;
   o << "  ispc_mbar_wait(acc_bar, 0);\n";
   o << "  asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
   o << "  const int lg = warp & 3, c_begin = (warp >> 2) * " << cols << ";\n";

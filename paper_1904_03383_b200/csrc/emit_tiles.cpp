@@ -471,14 +471,23 @@ std::string sgemm(const ispc_tile_config& c, const std::string& fn, ispc_launch&
     o << "    #pragma unroll\n    for (int i = 0; i < " << g.TM << "; ++i) P[(ty + j * " << g.TY << ") * " << g.BM
       << " + tx * " << g.TM << " + i] = acc[j][i];\n";
     o << "  ispc_cluster_sync();\n";
-    o << "  for (int e = rank * " << slice << " + tid * 4; e < (rank + 1) * " << slice << "; e += " << 4 * g.T << ") {\n";
-    o << "    float4 s = ispc_dsmem_ld4(P + e, 0);\n";
-    o << "    #pragma unroll\n    for (int q = 1; q < " << SP << "; ++q) {\n";
-    o << "      const float4 t = ispc_dsmem_ld4(P + e, q);\n";
-    o << "      s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;\n    }\n";
-    o << "    const int col = e / " << g.BM << ", row = e % " << g.BM << ";\n";
-    o << "    *(float4*)(g_c + bm * " << g.BM << "LL + row + (bn * " << g.BN << "LL + col) * " << M << "LL) = s;\n";
-    o << "  }\n";
+    if (g.BM % 4 == 0) {  // four rows of one column per step: aligned float4 everywhere
+      o << "  for (int e = rank * " << slice << " + tid * 4; e < (rank + 1) * " << slice << "; e += " << 4 * g.T << ") {\n";
+      o << "    float4 s = ispc_dsmem_ld4(P + e, 0);\n";
+      o << "    #pragma unroll\n    for (int q = 1; q < " << SP << "; ++q) {\n";
+      o << "      const float4 t = ispc_dsmem_ld4(P + e, q);\n";
+      o << "      s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;\n    }\n";
+      o << "    const int col = e / " << g.BM << ", row = e % " << g.BM << ";\n";
+      o << "    *(float4*)(g_c + bm * " << g.BM << "LL + row + (bn * " << g.BN << "LL + col) * " << M << "LL) = s;\n";
+      o << "  }\n";
+    } else {
+      o << "  for (int e = rank * " << slice << " + tid; e < (rank + 1) * " << slice << "; e += " << g.T << ") {\n";
+      o << "    float s = ispc_dsmem_ld(P + e, 0);\n";
+      o << "    #pragma unroll\n    for (int q = 1; q < " << SP << "; ++q) s += ispc_dsmem_ld(P + e, q);\n";
+      o << "    const int col = e / " << g.BM << ", row = e % " << g.BM << ";\n";
+      o << "    g_c[bm * " << g.BM << "LL + row + (bn * " << g.BN << "LL + col) * " << M << "LL] = s;\n";
+      o << "  }\n";
+    }
     o << "  ispc_cluster_sync();\n";
     L.cluster[0] = uint32_t(SP);
     L.cluster[1] = L.cluster[2] = 1;

@@ -8,6 +8,8 @@
 //       emitter assumes TMA produces
 //   P5  P4 with the operands landed by TMA (cuTensorMapEncodeTiled), plus a
 //       byte-compare of the landed tiles against P4's layout
+//   P6  A and B both K-major with the 128-byte swizzle (the layout the kernel
+//       builds by transposing A in shared memory)
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o tc_probe tc_probe.cu -lcuda
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -127,6 +129,7 @@ __global__ void __launch_bounds__(128, 1) probe(int mode, const float* A, const 
           unsigned off;
           if (mode == 2) off = (m / 8) * 256 + (k / 4) * 128 + (m % 8) * 16 + (k % 4) * 4;
           else if (mode == 3) off = (m / 4) * 128 + (k % 8) * 16 + (m % 4) * 4;
+          else if (mode == 6) off = (m / 8) * 1024 + (m % 8) * 128 + ((((k % 32) / 4) ^ (m % 8)) * 16) + (k % 4) * 4;
           else off = (m / 32) * 4096 + (k / 8) * 1024 + (k % 8) * 128 + ((((m % 32) / 4) ^ (k % 8)) * 16) + (m % 4) * 4;
           *(float*)(gen + off) = v;
         }
@@ -143,7 +146,7 @@ __global__ void __launch_bounds__(128, 1) probe(int mode, const float* A, const 
     }
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const unsigned amaj = (mode == 3 || mode >= 4) ? 1u : 0u;
+      const unsigned amaj = (mode == 3 || mode == 4 || mode == 5) ? 1u : 0u;
       const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (amaj << 15) | (0u << 16) | ((64u >> 3) << 17) |
                              ((128u >> 4) << 24);
       if (mode == 2) {
@@ -151,6 +154,9 @@ __global__ void __launch_bounds__(128, 1) probe(int mode, const float* A, const 
       } else if (mode == 3) {
         // MN-major, no swizzle: SBO = stride between 4-element MN core matrices, LBO = next 8 k
         mma(tmem, desc(base, 1024, 128, 0), desc(base + 16384, 128, 256, 0), idesc, 0);
+      } else if (mode == 6) {
+        for (int kk = 0; kk < 4; ++kk)
+          mma(tmem, desc(base + kk * 32u, 16, 1024, 2), desc(base + 16384 + kk * 32u, 16, 1024, 2), idesc, kk != 0);
       } else {
         for (int kk = 0; kk < 4; ++kk)
           mma(tmem, desc(base + kk * 1024u, 4096, 1024, 2), desc(base + 16384 + kk * 32u, 16, 1024, 2), idesc,
@@ -204,7 +210,7 @@ int main() {
   }
   CK(cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000));
   std::vector<unsigned> land4(16384 / 4 + 64 * 32);
-  for (int mode = 1; mode <= 5; ++mode) {
+  for (int mode = 1; mode <= 6; ++mode) {
     CK(cudaMemset(dO, 0xff, M * N * 4));
     CK(cudaMemset(dD, 0, 65536 * 4));
     probe<<<1, 128, 70000>>>(mode, dA, dB, dO, M, N, K, ta, tb, dD);
