@@ -192,7 +192,8 @@ int Search::select_child(MctsNode& n, double T, std::mt19937_64& rng) {
     double h = (si + alpha + std::sqrt(2 * si * alpha + alpha * alpha)) / double(n.visits[i]);
     if (h > best_h) best_h = h, best = int(i);
   }
-  if (!fresh.empty()) {
+  if (!fresh.empty()) {  // the lowest bound first half of the time, else p ~ 1/b
+    if (rng() & 1) return fresh[size_t(std::max_element(fresh_w.begin(), fresh_w.end()) - fresh_w.begin())];
     std::discrete_distribution<size_t> pick(fresh_w.begin(), fresh_w.end());
     return fresh[pick(rng)];
   }
@@ -326,8 +327,16 @@ bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound,
       w.push_back(weight);
     }
     if (kids.empty()) return false;
-    std::discrete_distribution<size_t> pick(w.begin(), w.end());
-    cur = std::move(kids[pick(rng)]);
+    // half of the draws follow the bound greedily (the most promising child,
+    // lowest b), the other half sample p ~ max(T - b, 0) / 1/b
+    size_t choice;
+    if (prune && (rng() & 1)) {
+      choice = size_t(std::max_element(w.begin(), w.end()) - w.begin());
+    } else {
+      std::discrete_distribution<size_t> pick(w.begin(), w.end());
+      choice = pick(rng);
+    }
+    cur = std::move(kids[choice]);
   }
 }
 
