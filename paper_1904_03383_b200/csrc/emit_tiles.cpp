@@ -29,6 +29,7 @@
 namespace ispc {
 
 std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn, ispc_launch& L);
+const char* tcgen05_prelude();
 
 namespace {
 
@@ -93,22 +94,27 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
   const int64_t xr_off = direct ? 0 : WN * R + R;            // [T][V] lane partials
   // CP_ASYNC staging: a ring of `stages` tiles of R rows x bk columns (column
   // segments of R contiguous floats) filled by 16-byte cp.async copies
-  const bool staged = c.staging == ISPC_STAGE_CP_ASYNC;
-  if (!staged && c.staging != ISPC_STAGE_DIRECT) illegal("gemv reads A directly or through a cp.async ring");
+  const bool tma = c.staging == ISPC_STAGE_TMA;
+  const bool staged = c.staging == ISPC_STAGE_CP_ASYNC || tma;
+  if (!staged && c.staging != ISPC_STAGE_DIRECT) illegal("gemv reads A directly or through a cp.async / TMA ring");
   const int64_t CB = staged ? c.bk : 0, ST = staged ? c.stages : 0;
   if (staged) {
-    if (ST < 2 || CB < 1) illegal("cp.async ring needs >= 2 stages of >= 1 column");
-    if (R % 4) illegal("cp.async column segments need rows per CTA divisible by 4");
+    if (ST < 2 || CB < 1) illegal("the staging ring needs >= 2 stages of >= 1 column");
+    if (R % 4) illegal("staged column segments need rows per CTA divisible by 4");
     if (CB % G || (n / S) % CB) illegal("stage columns do not split across column lanes / the CTA slice");
+    if (tma && (R > 256 || CB > 256)) illegal("TMA boxes hold at most 256 elements per dimension");
   }
-  const int64_t ring_off = (xr_off + (xr_shared ? int64_t(T) * V : 0) + 3) / 4 * 4;
-  const int64_t smem = 4 * (staged ? ring_off + ST * R * CB : ring_off);
+  // ring 128-byte aligned (TMA destination), then full[ST] / empty[ST] mbarriers
+  const int64_t ring_off = (xr_off + (xr_shared ? int64_t(T) * V : 0) + 31) / 32 * 32;
+  const int64_t smem = 4 * (staged ? ring_off + ST * R * CB : ring_off) + (tma ? 16 * ST : 0);
   if (smem > 232448) illegal("shared memory exceeds 227 KiB");
 
   std::ostringstream o;
   const std::string ty = V == 4 ? "float4" : V == 2 ? "float2" : "float";
+  if (tma) o << tcgen05_prelude();
   o << "extern \"C\" __global__ void __launch_bounds__(" << T << ") " << fn
-    << "(const float* __restrict__ g_a, const float* __restrict__ g_x, float* __restrict__ g_y) {\n";
+    << "(const float* __restrict__ g_a, const float* __restrict__ g_x, float* __restrict__ g_y"
+    << (tma ? ", const __grid_constant__ ispc_tmap_t tm_a" : "") << ") {\n";
   o << "  extern __shared__ __align__(16) float ispc_smem[];\n";
   o << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n";
   o << "  const int lm = lane % " << LM << ", ln = lane / " << LM << ";\n";
@@ -134,6 +140,49 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
       for (int v = 0; v < V; ++v)
         o << "      acc[" << v << "] = __fmaf_rn(av[u]" << comp(v) << ", xv[u], acc[" << v << "]);\n";
     o << "    }\n  }\n";
+  } else if (tma) {
+    // TMA ring: thread 0 lands one {R rows x CB columns} box per stage
+    // (mbarrier expect-tx); every thread releases the stage through empty[s]
+    const int64_t KT = n / S / CB, box_bytes = R * CB * 4;
+    o << "  float* ring = ispc_smem + " << ring_off << ";\n";
+    o << "  const unsigned ring_s = ispc_smem_addr(ring);\n";
+    o << "  const unsigned bars = ring_s + " << ST * box_bytes << "u;  // full[ST], empty[ST]\n";
+    o << "  const int row_c = (int)(rblk * " << R << "), col_c = rank * " << n / S << ";\n";
+    o << "  const float* px_cta = g_x + col_c;\n";
+    o << "  const int cl = wn * " << LN << " + ln, rl = (wm * " << LM << " + lm) * " << V << ";\n";
+    o << "  if (tid == 0) {\n";
+    o << "    for (int s = 0; s < " << ST << "; ++s) { ispc_mbar_init(bars + 8u * s, 1u); ispc_mbar_init(bars + 8u * ("
+      << ST << " + s), " << T << "u); }\n";
+    o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
+    o << "  }\n  __syncthreads();\n";
+    o << "  if (tid == 0) {\n";
+    o << "    for (int s = 0; s < " << ST - 1 << " && s < " << KT << "; ++s) {\n";
+    o << "      ispc_mbar_expect_tx(bars + 8u * s, " << box_bytes << "u);\n";
+    o << "      ispc_tma_2d(ring_s + s * " << box_bytes << "u, &tm_a, row_c, col_c + s * " << CB << ", bars + 8u * s);\n";
+    o << "    }\n  }\n";
+    o << "  #pragma unroll 1\n  for (int kt = 0; kt < " << KT << "; ++kt) {\n";
+    o << "    if (tid == 0) {\n";
+    o << "      const int nk = kt + " << ST - 1 << ";\n";
+    o << "      if (nk < " << KT << ") {\n";
+    o << "        const int slot = nk % " << ST << ";\n";
+    o << "        if (kt >= 1) ispc_mbar_wait(bars + 8u * (" << ST << " + slot), ((kt - 1) / " << ST << ") & 1);\n";
+    o << "        ispc_mbar_expect_tx(bars + 8u * slot, " << box_bytes << "u);\n";
+    o << "        ispc_tma_2d(ring_s + slot * " << box_bytes << "u, &tm_a, row_c, col_c + nk * " << CB
+      << ", bars + 8u * slot);\n";
+    o << "      }\n    }\n";
+    o << "    ispc_mbar_wait(bars + 8u * (kt % " << ST << "), (kt / " << ST << ") & 1);\n";
+    o << "    const float* st = ring + (kt % " << ST << ") * " << R * CB << ";\n";
+    o << "    #pragma unroll\n    for (int t = 0; t < " << CB / G << "; ++t) {\n";
+    o << "      const int cc = cl + t * " << G << ";\n";
+    o << "      const float xv = __ldg(px_cta + kt * " << CB << " + cc);\n";
+    o << "      const " << ty << " av = *(const " << ty << "*)(st + cc * " << R << " + rl);\n";
+    if (V == 1) o << "      acc[0] = __fmaf_rn(av, xv, acc[0]);\n";
+    else
+      for (int v = 0; v < V; ++v)
+        o << "      acc[" << v << "] = __fmaf_rn(av" << comp(v) << ", xv, acc[" << v << "]);\n";
+    o << "    }\n";
+    o << "    ispc_mbar_arrive(bars + 8u * (" << ST << " + kt % " << ST << "));\n";
+    o << "  }\n";
   } else {
     const int64_t KT = n / S / CB, chunks = R * CB / 4;
     const std::string cp = c.cache == ISPC_CACHE_L1 ? "ispc_cp_async_ca16" : "ispc_cp_async_cg16";
@@ -231,6 +280,20 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
   add_region(L, "x", n);
   add_region(L, "y", m);
   L.params[2].is_input = 1;
+  if (tma) {
+    ispc_param& P = L.params[L.num_params++];
+    P.kind = ISPC_PARAM_TMAP;
+    P.is_input = 1;
+    std::snprintf(P.name, sizeof(P.name), "a");
+    ispc_tmap& tm = L.tmaps[L.num_tmaps++];
+    tm.param = 3;
+    tm.rank = 2;
+    tm.swizzle = 0;
+    std::snprintf(tm.region, sizeof(tm.region), "a");
+    tm.dims[0] = uint64_t(m), tm.dims[1] = uint64_t(n);
+    tm.strides[0] = uint64_t(m) * 4;
+    tm.box[0] = uint32_t(R), tm.box[1] = uint32_t(CB);
+  }
   L.reg_elems = uint32_t(V * (U + 1) + U);
   return o.str();
 }

@@ -92,7 +92,7 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     f.min_threads = 32;
     f.warp_lanes = 32;
     f.max_acc = 64;
-    pre("staging", {"DIRECT", "CP_ASYNC"});
+    pre("staging", {"DIRECT", "CP_ASYNC", "TMA"});
     pre("engine", {"FFMA"});
   } else if (kind == "sgemm") {
     if (m <= 0 || n <= 0 || k <= 0) throw std::invalid_argument("sgemm needs m, n, k > 0");

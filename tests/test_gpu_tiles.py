@@ -83,6 +83,27 @@ def test_gemv_baseline_shape(dev):
     _run_many(dev, Space("gemv", m=4096, n=4096), 40, 15)
 
 
+@pytest.mark.parametrize("staging", ["CP_ASYNC", "TMA"])
+def test_gemv_staged_rings(dev, staging):
+    """cp.async and TMA (mbarrier expect-tx) column rings, norm-wise 1e-5."""
+    space = Space("gemv", m=4096, n=4096)
+    dev.bind(space.problem())
+    root = space.root().decide("staging", ["kernel"], staging)
+    ok = 0
+    for seed in range(30):
+        try:
+            leaf, _, _ = root.random_leaf(seed)
+        except DeadEnd:
+            continue
+        t = leaf.tiles()
+        m = dev.evaluate_tiles(t, reps=1, warmup=0)
+        if m.status == "illegal":
+            continue
+        assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
+        ok += 1
+    assert ok >= 5
+
+
 def test_gemv_cluster_split_is_exercised(dev):
     space = Space("gemv", m=4096, n=4096)
     dev.bind(space.problem())

@@ -109,8 +109,8 @@ def _emulate_all(space, want, max_threads=256, n=30, root=None):
             src, L = tile_cuda(t, "k_emu")
         except EmitError:
             continue
-        if L.block[0] > max_threads or (L.cluster[0] > 1):
-            continue
+        if L.block[0] > max_threads or L.cluster[0] > 1 or L.num_tmaps:
+            continue  # clusters and TMA need the device (tests/test_gpu_tiles.py)
         regs = _regions(orc, p)
         emu.run(src, L, regs)
         want(regs, t)
