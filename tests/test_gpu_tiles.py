@@ -206,3 +206,19 @@ def test_sgemm_split_k_cluster(dev, split):
         assert m.launch.cluster[0] == int(split)
         ok += 1
     assert ok >= 3
+
+
+def test_cli_explore_then_replay(tmp_path, capsys):
+    """explore writes the JSONL log (improving lines carry the candidate);
+    replay re-measures every logged improvement through the C-ABI."""
+    import json
+
+    from paper_1904_03383_b200 import cli
+    log = tmp_path / "gemv.jsonl"
+    args = ["gemv", "--m", "1024", "--n", "1024"]
+    assert cli.main(["explore", *args, "--evals", "16", "--log", str(log)]) == 0
+    out = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert out["evaluations"] >= 1 and out["ok"] >= 1
+    assert cli.main(["replay", str(log), *args]) == 0
+    rows = [json.loads(l) for l in capsys.readouterr().out.strip().splitlines()]
+    assert rows and all(r["status"] == "ok" for r in rows)
