@@ -499,7 +499,8 @@ void Search::launch_worker() {
       std::unique_lock<std::mutex> lk(mu_);
       // the device only works inside step(): outside it the rollouts and
       // compiles keep filling their bounded queues while the GPU idles
-      cv_done_.wait(lk, [&] { return stop_ || (!batch_q_.empty() && st_.evaluations < target_.load()); });
+      while (!(stop_ || (!batch_q_.empty() && st_.evaluations < target_.load())))
+        cv_done_.wait_for(lk, std::chrono::milliseconds(20));
       if (stop_) return;
       launching_ = true;
       b = std::move(batch_q_.front());
@@ -531,7 +532,7 @@ void Search::launch_worker() {
         if (st_.evaluations >= target_.load()) {
           launching_ = false;
           cv_done_.notify_all();
-          cv_done_.wait(lk, [&] { return stop_ || st_.evaluations < target_.load(); });
+          while (!(stop_ || st_.evaluations < target_.load())) cv_done_.wait_for(lk, std::chrono::milliseconds(20));
           if (stop_) break;
           launching_ = true;
         }
@@ -656,6 +657,9 @@ int Search::step(int64_t evaluations, double max_seconds) {
     std::lock_guard<std::mutex> lk(mu_);
     target_ = st_.evaluations + evaluations;
   }
+  // wake the launch thread: it sleeps on cv_done_ between steps, and with
+  // full queues nothing else would notify it
+  cv_done_.notify_all();
   if (!pipeline_started_) start();
   std::unique_lock<std::mutex> lk(mu_);
   auto drained = [&] { return exhausted_ && work_q_.empty() && batch_q_.empty() && !launching_; };

@@ -128,7 +128,7 @@ def test_sgemm_small_readback_bit_exact(dev):
     c64 = (a @ b).T.ravel()
     scale = (np.abs(a) @ np.abs(b)).T.ravel()
     ok = 0
-    for leaf in _leaves(space, 40):
+    for leaf in _leaves(space, 120):
         t = leaf.tiles()
         m = dev.evaluate_tiles(t, reps=1, warmup=0)
         if m.status == "illegal":
@@ -179,8 +179,8 @@ def test_tcgen05_sgemm(dev, engine):
         if N.ENGINES[t.engine] != engine:
             continue
         m = dev.evaluate_tiles(t, reps=1, warmup=0)
-        if m.status == "illegal" and "not implemented" in dev.error():
-            pytest.skip(dev.error())
+        if m.status == "illegal":  # e.g. a ring deeper than 227 KiB
+            continue
         assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
         ok += 1
     assert ok >= 1
