@@ -119,6 +119,18 @@ __global__ void compare_kernel(const float* out, const float* exp, const float* 
   }
 }
 
+// Reads the flush buffer after it was written: the written (dirty) lines are
+// written back here, so the timed kernel starts on a clean L2 that holds none
+// of its inputs.
+__global__ void flush_read_kernel(const uint4* __restrict__ p, int64_t n, unsigned* sink) {
+  unsigned acc = 0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    uint4 v = __ldcg(p + i);
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x9e3779b9u) *sink = acc;  // practically never: keeps the loads alive
+}
+
 __global__ void timer_kernel(unsigned long long* out) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -166,6 +178,12 @@ cudaError_t launch_gemv_golden(const float* a, const float* x, float* y, int64_t
 cudaError_t launch_compare(const float* out, const float* exp, const float* scale, int64_t n, int bit_exact,
                            float rtol, void* dev_res, cudaStream_t s) {
   compare_kernel<<<grid_for(n), 256, 0, s>>>(out, exp, scale, n, bit_exact, rtol, static_cast<CmpOut*>(dev_res));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flush_read(const void* p, size_t bytes, void* sink, cudaStream_t s) {
+  flush_read_kernel<<<148 * 8, 512, 0, s>>>(static_cast<const uint4*>(p), int64_t(bytes / 16),
+                                            static_cast<unsigned*>(sink));
   return cudaGetLastError();
 }
 

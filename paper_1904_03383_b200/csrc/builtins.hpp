@@ -22,5 +22,6 @@ cudaError_t launch_gemv_golden(const float* a, const float* x, float* y, int64_t
 cudaError_t launch_compare(const float* out, const float* exp, const float* scale, int64_t n, int bit_exact,
                            float rtol, void* dev_res, cudaStream_t s);
 cudaError_t launch_timer(unsigned long long* out, cudaStream_t s);
+cudaError_t launch_flush_read(const void* p, size_t bytes, void* sink, cudaStream_t s);
 
 }  // namespace ispc

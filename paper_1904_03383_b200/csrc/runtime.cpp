@@ -613,7 +613,10 @@ int ispc_launch_timed(ispc_dev* d, int handle, const ispc_launch* L, const ispc_
   if (clustered && L->grid_x % L->cluster[0] != 0) return fail(d, ISPC_E_ILLEGAL, "grid not a multiple of the cluster");
   unsigned int smem = L->static_smem;
   auto launch_once = [&](float* ms, bool flush) -> int {
-    if (flush) CK(d, cudaMemsetAsync(d->flush, int(flush_counter_++ & 0xff), d->flush_bytes, d->stream));
+    if (flush) {  // write a buffer larger than L2, then read it back (clean L2, no pending write-backs)
+      CK(d, cudaMemsetAsync(d->flush, int(flush_counter_++ & 0xff), d->flush_bytes, d->stream));
+      CK(d, ispc::launch_flush_read(d->flush, d->flush_bytes, d->cmp_res, d->stream));
+    }
     if (deadline_slot >= 0) store[deadline_slot] = uint64_t(host_ns() + d->gt_offset_ns + budget);
     CK(d, cudaEventRecord(d->ev0, d->stream));
     if (clustered) {

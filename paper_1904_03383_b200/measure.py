@@ -91,8 +91,9 @@ def _time(fn, reps=20, flush=None) -> float:
     import torch
     times = []
     for i in range(reps + 3):
-        if flush is not None:
+        if flush is not None:  # same flush as the runtime: write, then read back (clean L2)
             flush.fill_(i & 0xff)
+            flush.view(torch.int32).max()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         fn()

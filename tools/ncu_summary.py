@@ -60,11 +60,20 @@ def main():
             x = r.get(k)
             return x["value"] if isinstance(x, dict) else x
 
-        rd, wr = val("dram__bytes_read.sum"), val("dram__bytes_write.sum")
-        ur = r.get("dram__bytes_read.sum", {}).get("unit", "byte") if isinstance(r.get("dram__bytes_read.sum"), dict) else "byte"
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(ur, 1)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+
+        def nbytes(k):
+            x = r.get(k)
+            if not isinstance(x, dict):
+                return None
+            return x["value"] * scale.get(x["unit"], 1)
+
+        rd, wr = nbytes("dram__bytes_read.sum"), nbytes("dram__bytes_write.sum")
         if rd is not None and wr is not None:
-            summary["dram_bytes_per_launch"] = (rd + wr) * scale
+            summary["dram_bytes_per_launch"] = rd + wr
+        t = r.get("gpu__time_duration.sum")
+        if isinstance(t, dict):
+            summary["duration_us"] = t["value"] * {"ns": 1e-3, "us": 1, "ms": 1e3, "s": 1e6}.get(t["unit"], 1)
         summary["kernel"] = val("Kernel Name")
     json.dump(summary, open(out, "w"), indent=1)
     print(json.dumps({k: v for k, v in summary.items() if k != "launches"}))
