@@ -224,6 +224,16 @@ struct Reader {
       if (mask_has(c.dom[i], int(v))) lo = std::min(lo, u[v]), hi = std::max(hi, u[v]);
     return {lo, hi};
   }
+  // remaining values of a tile parameter ({} when absent)
+  std::vector<std::int64_t> remaining(const std::string& name) const {
+    std::vector<std::int64_t> out;
+    std::uint32_t i = inst_of(ch_tile, name);
+    if (i == kNoInstance) return out;
+    const auto& u = ctx.table.universe_of(i);
+    for (size_t v = 0; v < u.size(); ++v)
+      if (mask_has(c.dom[i], int(v))) out.push_back(u[v]);
+    return out;
+  }
   std::int64_t value(const std::string& name) const {
     std::uint32_t i = inst_of(ch_tile, name);
     if (i == kNoInstance) return 0;
@@ -307,6 +317,23 @@ TileBoundReport tile_bound(const TileFamily& f, const SpaceContext& ctx, const C
     b.compute = flops / (sms * kFfmaPerSmClk * 2 * kFmax);
   }
   if (!tensor) b.compute = std::max(b.compute, per_thread / kFmax);
+  if (f.kind == ISPC_TILE_SGEMM) {
+    // shared-memory operand traffic: per k step a warp reads tm values for
+    // each of its min(thr_m, 32) distinct rows and tn values for each of its
+    // max(1, 32/thr_m) distinct columns (equal addresses broadcast), i.e.
+    // (tm*min(tx,32) + tn*max(1,32/tx)) * 4 B per 32*tm*tn FMAs, at 128 B per
+    // clock per SM; minimised over the values still open
+    double best = std::numeric_limits<double>::infinity();
+    for (std::int64_t tx : r.remaining("thr_m"))
+      for (std::int64_t tm : r.remaining("tm"))
+        for (std::int64_t tn : r.remaining("tn")) {
+          double per_fma = (double(tm) * double(std::min<std::int64_t>(tx, 32)) +
+                            double(tn) * double(std::max<std::int64_t>(1, 32 / std::max<std::int64_t>(tx, 1)))) *
+                           4.0 / (32.0 * double(tm) * double(tn));
+          best = std::min(best, per_fma);
+        }
+    if (std::isfinite(best)) b.compute = std::max(b.compute, flops / 2 * best / (sms * 128.0 * kFmax));
+  }
   b.launch = kLaunch;
   b.total = std::max({b.dram, b.compute, b.launch});
   if (fully_specified(ctx, c)) {
