@@ -42,7 +42,6 @@ BYTES_PER_RUN = 12 * N_AXPY  # x, y read + z written, fp32
 METRIC = "candidates evaluated/s (best-kernel GB/s vs HBM roofline in `roofline`)"
 WORKLOAD = "axpy fp32 n=2^26: full search + evaluation (paper factors {2,4}x{2..1024}, reference gpu.space)"
 REF_CPU_BENCH = os.path.join(ROOT, "oracle", "_ref", "ref_cpu_bench")
-PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r01_axpy_best_ncu.json")
 
 
 class Clocks:
@@ -320,10 +319,8 @@ def run_ours(args, world, rank, local):
             best_info = {"error": str(e)}
         if r.get("status") == "ok":
             roofline = dict(r["roofline"])
-            traffic = None
-            if os.path.exists(PROFILE_SUMMARY):
-                traffic = json.load(open(PROFILE_SUMMARY)).get("dram_bytes_per_launch")
-            roofline["traffic"] = traffic
+            roofline["traffic"] = r.get("traffic")  # ncu capture of this exact kernel, when in profiles/
+            roofline["kernel"] = r.get("kernel")
             roofline["kernel_us"] = r["kernel_us"]
             best_info = {"kernel_us": r["kernel_us"], "search_median_us": st["best_ns"] / 1e3,
                          "bound_us": st["best_bound_ns"] / 1e3, "time_to_best_s": st["time_to_best_s"],

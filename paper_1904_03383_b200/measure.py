@@ -77,9 +77,29 @@ def retime_best(space, cand, reps: int = 20, dev=None, ordinal: int = 0) -> dict
         return {"status": m.status}
     r = {"status": "ok", "kernel_us": round(m.median_ns / 1e3, 3), "min_us": round(m.min_ns / 1e3, 3),
          "max_err": m.max_err, "grid": int(m.launch.grid_x), "block": list(m.launch.block)[:1][0],
-         "smem": int(m.launch.static_smem), "cluster": int(m.launch.cluster[0])}
+         "smem": int(m.launch.static_smem), "cluster": int(m.launch.cluster[0]),
+         "kernel": m.launch.name.decode()}
+    r["traffic"] = traffic_of(r["kernel"])
     r["roofline"] = roofline(space, m.median_ns)
     return r
+
+
+def traffic_of(kernel: str) -> float | None:
+    """DRAM read+write bytes per launch of `kernel` from an ncu --set full
+    capture summarised under profiles/ (None when this exact kernel was not
+    captured)."""
+    d = os.path.join(ROOT, "profiles")
+    if not os.path.isdir(d):
+        return None
+    for f in sorted(os.listdir(d), reverse=True):
+        if f.endswith("_ncu.json"):
+            try:
+                j = json.load(open(os.path.join(d, f)))
+            except (OSError, ValueError):
+                continue
+            if j.get("kernel") == kernel:
+                return j.get("dram_bytes_per_launch")
+    return None
 
 
 def _flush_buf():
