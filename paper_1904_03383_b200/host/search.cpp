@@ -149,7 +149,11 @@ void Search::expand_frontier() {
       for (int v = 0; v < kMaxDomainBits; ++v) {
         if (!mask_has(m, v)) continue;
         Candidate child;
-        if (apply_decision(ctx, c, inst, v, child) == PropStatus::Ok) next.push_back(std::move(child));
+        if (apply_decision(ctx, c, inst, v, child) != PropStatus::Ok) continue;
+        // unrunnable subtrees (infinite bound, e.g. a ring beyond 227 KiB)
+        // never enter the frontier
+        if (cfg_.pruning && !std::isfinite(bound_total(child))) continue;
+        next.push_back(std::move(child));
       }
       grew = true;
     }
@@ -378,7 +382,8 @@ void Search::rollout_worker(int tid) {
       ispc_tile_config tc{};
       try {
         tc = tile_config(*space_->tiles, *space_->ctx, w->leaf);
-      } catch (const std::exception&) {
+      } catch (const std::exception& e) {
+        if (trace_) std::fprintf(stderr, "[ispc] leaf without a tile config: %s\n", e.what());
         ++illegal_;
         t_rollout_.fetch_add(now() - t);
         note_fruitless();
@@ -411,6 +416,7 @@ void Search::rollout_worker(int tid) {
     }
     t_rollout_.fetch_add(now() - t);
     if (rc != ISPC_OK) {
+      if (trace_) std::fprintf(stderr, "[ispc] illegal leaf: %s\n", ispc_last_error(nullptr));
       ++illegal_;
       note_fruitless();
       continue;
@@ -448,6 +454,7 @@ void Search::compile_worker(int tid) {
         items.push_back(std::move(work_q_.front()));
         work_q_.pop_front();
       }
+      if (!items.empty()) ++compiling_;
       cv_work_.notify_all();
     }
     if (items.empty()) continue;
@@ -487,6 +494,7 @@ void Search::compile_worker(int tid) {
     t_compile_.fetch_add(now() - t);
     std::lock_guard<std::mutex> lk(mu_);
     for (auto& b : out) batch_q_.push_back(std::move(b));
+    --compiling_;
     cv_done_.notify_all();
   }
 }
@@ -662,7 +670,9 @@ int Search::step(int64_t evaluations, double max_seconds) {
   cv_done_.notify_all();
   if (!pipeline_started_) start();
   std::unique_lock<std::mutex> lk(mu_);
-  auto drained = [&] { return exhausted_ && work_q_.empty() && batch_q_.empty() && !launching_; };
+  auto drained = [&] {
+    return exhausted_ && work_q_.empty() && batch_q_.empty() && compiling_.load() == 0 && !launching_;
+  };
   const double t_end = max_seconds > 0 ? now() + max_seconds : std::numeric_limits<double>::infinity();
   bool late = false;
   while (!(stop_ || st_.evaluations >= target_.load() || drained())) {

@@ -136,6 +136,7 @@ class Search {
   static constexpr int64_t kExhaust = 3000;
   std::atomic<int64_t> fruitless_{0};
   std::atomic<bool> exhausted_{false};
+  std::atomic<int> compiling_{0};  // batches inside NVRTC right now
   void note_fruitless();
   std::atomic<double> t_rollout_{0}, t_compile_{0};
   double t0_ = 0;
