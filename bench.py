@@ -176,7 +176,7 @@ def save_best(kind, kw, cand):
     """Keeps the best candidate (reference text serialization) for
     tools/profile_best.py (ncu captures of exactly this kernel)."""
     d = os.path.join(ROOT, "gpurun_out")
-    if os.path.isdir(d):
+    if os.path.isdir(d) and not os.environ.get("BENCH_NO_SAVE_BEST"):
         with open(os.path.join(d, f"best_{kind}.json"), "w") as f:
             json.dump({"kind": kind, "space": kw, "candidate": cand.serialize()}, f)
 
