@@ -300,8 +300,10 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
 
 // ---------------------------------------------------------------- sgemm (FFMA)
 // C = A B, column-major: A[i + k*M], B[k + j*K], C[i + j*M]. CTA tile
-// BM x BN = (thr_m*tm) x (thr_n*tn); thread (tx, ty) owns rows
-// bm*BM + tx*tm .. +tm (contiguous: float4 smem reads and C stores) and the
+// BM x BN = (thr_m*tm) x (thr_n*tn); thread (tx, ty) owns the rows
+// bm*BM + (i/v)*thr_m*v + tx*v + i%v, i < tm, v = the vector width that
+// divides tm (groups of v contiguous rows, interleaved across threads: a
+// warp's float4 smem reads are contiguous, C stores stay vectorised) and the
 // columns bn*BN + ty + j*thr_n, j < tn (interleaved, so the Bs rows a warp
 // reads fall in distinct banks). Shared tiles per
 // stage: As[bk][BM] (m contiguous) and Bs[BN][bk+4] (k contiguous), both
@@ -346,15 +348,15 @@ void gemm_compute(std::ostringstream& o, const GemmShape& g, const std::string& 
   o << indent << "  #pragma unroll\n" << indent << "  for (int q = 0; q < " << KG << "; ++q) {\n";
   o << indent << "    #pragma unroll\n" << indent << "    for (int i = 0; i < " << g.TM << "; i += " << AV << ") {\n";
   if (AV == 4)
-    o << indent << "      float4 t = *(const float4*)(" << As << " + (kq + q) * " << g.BM << " + tx * " << g.TM
-      << " + i);\n"
+    o << indent << "      float4 t = *(const float4*)(" << As << " + (kq + q) * " << g.BM << " + (i / 4) * " << g.TX * 4
+      << " + tx * 4);\n"
       << indent << "      ra[q][i] = t.x; ra[q][i + 1] = t.y; ra[q][i + 2] = t.z; ra[q][i + 3] = t.w;\n";
   else if (AV == 2)
-    o << indent << "      float2 t = *(const float2*)(" << As << " + (kq + q) * " << g.BM << " + tx * " << g.TM
-      << " + i);\n"
+    o << indent << "      float2 t = *(const float2*)(" << As << " + (kq + q) * " << g.BM << " + (i / 2) * " << g.TX * 2
+      << " + tx * 2);\n"
       << indent << "      ra[q][i] = t.x; ra[q][i + 1] = t.y;\n";
   else
-    o << indent << "      ra[q][i] = " << As << "[(kq + q) * " << g.BM << " + tx * " << g.TM << " + i];\n";
+    o << indent << "      ra[q][i] = " << As << "[(kq + q) * " << g.BM << " + i * " << g.TX << " + tx];\n";
   o << indent << "    }\n" << indent << "  }\n";
   o << indent << "  #pragma unroll\n" << indent << "  for (int j = 0; j < " << g.TN << "; ++j) {\n";
   if (KG == 4)
@@ -514,13 +516,14 @@ std::string sgemm(const ispc_tile_config& c, const std::string& fn, ispc_launch&
   const int EV = g.TM % 4 == 0 ? 4 : g.TM % 2 == 0 ? 2 : 1;
   const std::string ety = EV == 4 ? "float4" : EV == 2 ? "float2" : "float";
   if (SP == 1) {
-    o << "  float* pc = g_c + (bm * " << g.BM << "LL + tx * " << g.TM << ") + (bn * " << g.BN << "LL + ty) * " << M
+    o << "  float* pc = g_c + (bm * " << g.BM << "LL + tx * " << EV << ") + (bn * " << g.BN << "LL + ty) * " << M
       << "LL;\n";
     o << "  #pragma unroll\n  for (int j = 0; j < " << g.TN << "; ++j)\n";
     o << "    #pragma unroll\n    for (int i = 0; i < " << g.TM << "; i += " << EV << ")\n";
-    if (EV == 1) o << "      pc[i + (long long)j * " << int64_t(g.TY) * M << "LL] = acc[j][i];\n";
+    if (EV == 1) o << "      pc[i * " << g.TX << " + (long long)j * " << int64_t(g.TY) * M << "LL] = acc[j][i];\n";
     else {
-      o << "      *(" << ety << "*)(pc + i + (long long)j * " << int64_t(g.TY) * M << "LL) = make_" << ety << "(";
+      o << "      *(" << ety << "*)(pc + (i / " << EV << ") * " << g.TX * EV << " + (long long)j * " << int64_t(g.TY) * M
+        << "LL) = make_" << ety << "(";
       for (int e = 0; e < EV; ++e) o << (e ? ", " : "") << "acc[j][i + " << e << "]";
       o << ");\n";
     }
@@ -532,7 +535,7 @@ std::string sgemm(const ispc_tile_config& c, const std::string& fn, ispc_launch&
     o << "  float* P = ispc_smem;\n";
     o << "  #pragma unroll\n  for (int j = 0; j < " << g.TN << "; ++j)\n";
     o << "    #pragma unroll\n    for (int i = 0; i < " << g.TM << "; ++i) P[(ty + j * " << g.TY << ") * " << g.BM
-      << " + tx * " << g.TM << " + i] = acc[j][i];\n";
+      << " + (i / " << EV << ") * " << g.TX * EV << " + tx * " << EV << " + i % " << EV << "] = acc[j][i];\n";
     o << "  ispc_cluster_sync();\n";
     if (g.BM % 4 == 0) {  // four rows of one column per step: aligned float4 everywhere
       o << "  for (int e = rank * " << slice << " + tid * 4; e < (rank + 1) * " << slice << "; e += " << 4 * g.T << ") {\n";
