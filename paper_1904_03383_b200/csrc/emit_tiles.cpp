@@ -181,6 +181,9 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
       for (int v = 0; v < V; ++v)
         o << "      acc[" << v << "] = __fmaf_rn(av" << comp(v) << ", xv, acc[" << v << "]);\n";
     o << "    }\n";
+    // order this thread's generic-proxy reads of the slot before the TMA
+    // (async proxy) that will overwrite it once every thread arrived
+    o << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
     o << "    ispc_mbar_arrive(bars + 8u * (" << ST << " + kt % " << ST << "));\n";
     o << "  }\n";
   } else {

@@ -35,6 +35,18 @@ def main():
                           **{k: d[k] for k in ("vec", "lanes_m", "lanes_n", "warps_m", "warps_n", "split", "bk",
                                                "stages", "xreduce")}}), flush=True)
         bad += m.status != "ok"
+    # the two configurations that failed before the proxy fence, ten times each
+    for cfg in ({"vec": "2", "lanes_m": "1", "warps_m": "8", "warps_n": "1", "split": "2", "bk": "64", "stages": "4"},
+                {"vec": "4", "lanes_m": "2", "warps_m": "4", "warps_n": "8", "split": "8", "bk": "128", "stages": "3"}):
+        c = space.root().decide("staging", ["kernel"], "TMA").decide("xreduce", ["kernel"], "SHUFFLE")
+        for k, v in cfg.items():
+            c.decide("tile", [k], v)
+        t = c.first_leaf().tiles()
+        res = []
+        for _ in range(10):
+            m = dev.evaluate_tiles(t, reps=1, warmup=0)
+            res.append((m.status, m.mismatches))
+        print(json.dumps({"cfg": cfg, "runs": res}), flush=True)
     dev.close()
     print("bad", bad)
 
