@@ -150,9 +150,9 @@ def run_reference(args, world, rank):
 
 CONFIG_SPACES = {
     # kind: (Space kwargs, evaluations, flush L2 while searching)
-    "gemv": (dict(m=4096, n=4096), 512, True),
-    "sgemm": (dict(m=1024, n=1024, k=1024), 512, False),
-    "batched": (dict(m=32, n=32, k=64, batch=512), 256, True),
+    "gemv": (dict(m=4096, n=4096), 1024, True),
+    "sgemm": (dict(m=1024, n=1024, k=1024), 1536, False),
+    "batched": (dict(m=32, n=32, k=64, batch=512), 512, True),
     "sgemm_tc": (dict(m=4096, n=4096, k=4096), 30, False),
 }
 
