@@ -154,6 +154,7 @@ CONFIG_SPACES = {
     "sgemm": (dict(m=1024, n=1024, k=1024), 1536, False),
     "batched": (dict(m=32, n=32, k=64, batch=512), 512, True),
     "sgemm_tc": (dict(m=4096, n=4096, k=4096), 30, False),
+    "sgemm_tc_x3": (dict(m=4096, n=4096, k=4096), 30, False),
 }
 
 
@@ -302,7 +303,8 @@ def run_ours(args, world, rank, local):
 
     configs = {}
     if args.configs != "none":
-        want = ["gemv", "sgemm", "batched", "sgemm_tc"] if args.configs == "all" else args.configs.split(",")
+        want = (["gemv", "sgemm", "batched", "sgemm_tc", "sgemm_tc_x3"] if args.configs == "all"
+                else args.configs.split(","))
         configs = run_configs(want, args, local, world, rank)
     if rank != 0:
         return

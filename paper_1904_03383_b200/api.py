@@ -20,7 +20,7 @@ from . import _native as N
 class Space:
     """A kernel backbone bound to the GPU decision space (gpu_space.hpp:15-18)."""
 
-    TILE_KINDS = ("gemv", "sgemm", "batched", "sgemm_tc")
+    TILE_KINDS = ("gemv", "sgemm", "batched", "sgemm_tc", "sgemm_tc_x3")
 
     def __init__(self, kind: str, *, m: int = 0, n: int = 0, k: int = 0, a_stride: int = 1,
                  factors: list[list[int]] | None = None, mode: int = N.SPACE_PARITY, batch: int = 1):

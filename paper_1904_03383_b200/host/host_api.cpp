@@ -155,7 +155,7 @@ int ispc_space_problem(const ispc_space* s, ispc_problem* p) {
   p->batch = 1;
   if (k == "axpy") p->kind = ISPC_PROB_AXPY;
   else if (k == "outer_product") p->kind = ISPC_PROB_OUTER;
-  else if (k == "matmul" || k == "sgemm" || k == "sgemm_tc") p->kind = ISPC_PROB_MATMUL;
+  else if (k == "matmul" || k == "sgemm" || k == "sgemm_tc" || k == "sgemm_tc_x3") p->kind = ISPC_PROB_MATMUL;
   else if (k == "gemv") p->kind = ISPC_PROB_GEMV;
   else if (k == "batched") {
     p->kind = ISPC_PROB_BATCHED;

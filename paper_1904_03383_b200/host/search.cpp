@@ -390,7 +390,7 @@ void Search::rollout_worker(int tid) {
         continue;
       }
       w->bit_exact = tile_bit_exact(tc);
-      w->rtol = space_->tiles->rtol();
+      w->rtol = tc.kind == ISPC_TILE_SGEMM_TC && tc.engine == ISPC_ENGINE_TF32X3 ? 1e-5 : space_->tiles->rtol();
       rc = ispc_emit_tiles(&tc, nullptr, nullptr, 0, &len, &w->launch);
       if (rc == ISPC_OK) {
         w->src.assign(len + 1, '\0');

@@ -30,6 +30,7 @@ struct TileFamily {
   std::vector<std::pair<std::string, std::string>> covers;  // (outer, inner)
   std::vector<ispace::PreRestriction> pre;
   std::int64_t min_threads = 1, warp_lanes = 1, max_acc = 256, max_cluster = 8;
+  bool x3_only = false;  // sgemm_tc_x3
 
   // checking rule of this kind's outputs
   bool bit_exact() const;

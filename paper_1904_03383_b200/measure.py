@@ -36,7 +36,7 @@ def work(space) -> dict:
         return {"bytes": 4 * b * (m * k + k * n + m * n), "flops": 2 * b * m * n * k, "bound": "hbm"}
     if kind in ("sgemm", "matmul"):
         return {"bytes": 4 * (m * k + k * n + m * n), "flops": 2 * m * n * k, "bound": "fp32"}
-    if kind == "sgemm_tc":
+    if kind in ("sgemm_tc", "sgemm_tc_x3"):
         return {"bytes": 4 * (m * k + k * n + m * n), "flops": 2 * m * n * k, "bound": "tensor"}
     raise ValueError(kind)
 
@@ -152,7 +152,7 @@ def cublas_reference(space, reps: int = 20) -> dict | None:
     elif kind == "batched":
         a, bb = torch.rand(b, k, m, device="cuda"), torch.rand(b, n, k, device="cuda")
         out["sgemm_strided_batched"] = _time(lambda: torch.bmm(a.transpose(1, 2), bb.transpose(1, 2)), reps, flush)
-    elif kind == "sgemm_tc":
+    elif kind in ("sgemm_tc", "sgemm_tc_x3"):
         a, bb = torch.rand(k, m, device="cuda"), torch.rand(n, k, device="cuda")
         out["sgemm_fp32"] = _time(lambda: torch.mm(a.t(), bb.t()), reps, flush)
         torch.backends.cuda.matmul.allow_tf32 = True

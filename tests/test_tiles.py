@@ -31,6 +31,7 @@ def _leaves(space, n, order=None, root=None):
     ("sgemm", dict(m=1024, n=1024, k=1024)),
     ("batched", dict(m=32, n=32, k=64, batch=512)),
     ("sgemm_tc", dict(m=4096, n=4096, k=4096)),
+    ("sgemm_tc_x3", dict(m=4096, n=4096, k=4096)),
 ])
 def test_space_builds_and_is_deterministic(kind, kw):
     a, b = Space(kind, **kw), Space(kind, **kw)
