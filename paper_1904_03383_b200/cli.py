@@ -37,7 +37,8 @@ def _candidate(space: Space, a):
 
 def cmd_explore(a) -> int:
     space = _space(a)
-    s = Search(space, device=a.device, seed=a.seed, log_path=a.log, flush_l2=a.kind in ("gemv", "batched"))
+    s = Search(space, device=a.device, seed=a.seed, log_path=a.log, flush_l2=a.kind in ("gemv", "batched"),
+               decision_order=a.decision_order)
     s.step(a.evals)
     st = s.stats()
     best = s.best()
@@ -125,6 +126,7 @@ def main(argv=None) -> int:
     p.add_argument("--device", type=int, default=0)
     p.add_argument("--log")
     p.add_argument("--out", help="write the best candidate's serialization here")
+    p.add_argument("--decision-order", default=None, help="comma separated choice names (default: paper order)")
     p.set_defaults(fn=cmd_explore)
     p = sub.add_parser("codegen")
     common(p)
