@@ -346,7 +346,10 @@ typedef struct {
   uint32_t flush_l2;      /* 1: write an L2-sized buffer before every launch */
   uint32_t check;         /* 1: verify outputs after the first launch        */
   uint32_t bit_exact;     /* 1: require identical bits, else rtol            */
-  uint32_t _pad;
+  uint32_t rotate;        /* >= 2: timed launches run back to back over this
+                             many copies of the inputs (inputs larger than L2
+                             in aggregate), mean per launch; else one launch
+                             per event pair                                   */
   double rtol;            /* relative tolerance when !bit_exact              */
   double budget_ns;       /* watchdog budget per launch (0: 2 s)             */
 } ispc_time_opts;

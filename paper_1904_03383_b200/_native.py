@@ -139,7 +139,7 @@ class Problem(C.Structure):
 
 class TimeOpts(C.Structure):
     _fields_ = [("warmup", C.c_uint32), ("reps", C.c_uint32), ("flush_l2", C.c_uint32), ("check", C.c_uint32),
-                ("bit_exact", C.c_uint32), ("_pad", C.c_uint32), ("rtol", C.c_double),
+                ("bit_exact", C.c_uint32), ("rotate", C.c_uint32), ("rtol", C.c_double),
                 ("budget_ns", C.c_double)]
 
 

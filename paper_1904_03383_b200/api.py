@@ -321,9 +321,9 @@ class Device:
         N.ispc().ispc_module_unload(self._h, handle)
 
     @staticmethod
-    def _opts(warmup, reps, flush_l2, check, bit_exact, rtol, budget_ns):
+    def _opts(warmup, reps, flush_l2, check, bit_exact, rtol, budget_ns, rotate=0):
         return N.TimeOpts(warmup=warmup, reps=reps, flush_l2=int(flush_l2), check=int(check),
-                          bit_exact=int(bit_exact), rtol=rtol, budget_ns=budget_ns)
+                          bit_exact=int(bit_exact), rtol=rtol, budget_ns=budget_ns, rotate=rotate)
 
     def launch(self, handle: int, launch: N.Launch, *, warmup=1, reps=3, flush_l2=False, check=True,
                bit_exact=True, rtol=1e-5, budget_ns=2e9) -> Measurement:
@@ -338,12 +338,13 @@ class Device:
                            r.mismatches, launch)
 
     def evaluate(self, nest: NestHandle, *, watchdog=2, warmup=1, reps=3, flush_l2=False, check=True,
-                 bit_exact=True, rtol=1e-5, budget_ns=2e9) -> Measurement:
+                 bit_exact=True, rtol=1e-5, budget_ns=2e9, rotate=0) -> Measurement:
         r = N.TimeResult()
         L = N.Launch()
         eo = N.EmitOpts(watchdog=watchdog)
         rc = N.ispc().ispc_evaluate(self._h, nest.nest, C.byref(eo),
-                                    C.byref(self._opts(warmup, reps, flush_l2, check, bit_exact, rtol, budget_ns)),
+                                    C.byref(self._opts(warmup, reps, flush_l2, check, bit_exact, rtol, budget_ns,
+                                                       rotate)),
                                     C.byref(r), C.byref(L))
         if rc != 0:
             return Measurement(N.STATUS.get(rc, str(rc)), float("inf"), float("inf"), float("inf"), 0.0, -1, L)
@@ -352,7 +353,7 @@ class Device:
 
 
     def evaluate_tiles(self, cfg: N.TileConfig, *, warmup=1, reps=3, flush_l2=False, check=True,
-                       bit_exact=None, rtol=None) -> Measurement:
+                       bit_exact=None, rtol=None, rotate=0) -> Measurement:
         """Emit + compile + timed launch + on-device check of a building-block
         configuration. Default checking: bit-exact for the FFMA sgemm and
         batched kernels (k ascending per output), norm-wise rtol otherwise."""
@@ -364,7 +365,8 @@ class Device:
         r = N.TimeResult()
         L = N.Launch()
         rc = N.ispc().ispc_evaluate_tiles(self._h, C.byref(cfg),
-                                          C.byref(self._opts(warmup, reps, flush_l2, check, bit_exact, rtol, 2e9)),
+                                          C.byref(self._opts(warmup, reps, flush_l2, check, bit_exact, rtol, 2e9,
+                                                             rotate)),
                                           C.byref(r), C.byref(L))
         if rc != 0:
             return Measurement(N.STATUS.get(rc, str(rc)), float("inf"), float("inf"), float("inf"), 0.0, -1, L)
