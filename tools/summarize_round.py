@@ -69,9 +69,10 @@ def main():
     if sh:
         res["launch_shares"] = sh
         json.dump(sh, open(os.path.join(PROF, f"{tag}_launch_shares.json"), "w"), indent=1)
-    for k in ("axpy", "gemv", "sgemm", "batched", "sgemm_tc"):
-        rep = os.path.join(OUT, f"{tag}_prof_{k}.ncu-rep")
-        if os.path.exists(rep):
+    for f in sorted(os.listdir(OUT)):
+        if f.startswith(f"{tag}_prof_") and f.endswith(".ncu-rep"):
+            k = f[len(f"{tag}_prof_"):-len(".ncu-rep")]
+            rep = os.path.join(OUT, f)
             dst = os.path.join(PROF, f"{tag}_{k}_ncu.json")
             subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep, dst], check=False)
     print(json.dumps({k: v for k, v in res.items() if k != "bench"}, indent=1))
