@@ -150,8 +150,8 @@ def run_reference(args, world, rank):
 
 CONFIG_SPACES = {
     # name: (space kind, Space kwargs, evaluations, flush L2 while searching)
-    "gemv": ("gemv", dict(m=4096, n=4096), 1024, True),
-    "sgemm": ("sgemm", dict(m=1024, n=1024, k=1024), 1536, False),
+    "gemv": ("gemv", dict(m=4096, n=4096), 2048, True),
+    "sgemm": ("sgemm", dict(m=1024, n=1024, k=1024), 4096, False),
     "batched": ("batched", dict(m=32, n=32, k=64, batch=512), 512, True),
     "sgemm_tc": ("sgemm_tc", dict(m=4096, n=4096, k=4096), 30, False),
     "sgemm_tc_x3": ("sgemm_tc_x3", dict(m=4096, n=4096, k=4096), 30, False),
