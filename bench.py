@@ -150,6 +150,9 @@ def run_reference(args, world, rank):
 
 CONFIG_SPACES = {
     # name: (space kind, Space kwargs, evaluations, flush L2 while searching)
+    # axpy 2^26 on the elementwise streaming building block (the headline
+    # searches the reference's own gpu.space for the same computation)
+    "axpy_stream": ("axpy_stream", dict(n=1 << 26), 256, False),
     "gemv": ("gemv", dict(m=4096, n=4096), 2048, True),
     "sgemm": ("sgemm", dict(m=1024, n=1024, k=1024), 4096, False),
     "batched": ("batched", dict(m=32, n=32, k=64, batch=512), 512, True),

@@ -256,7 +256,7 @@ int ispc_emit_pseudo(const ispc_nest* nest, char* buf, size_t cap, size_t* len);
  * A fully specified candidate of that space crosses the boundary as this flat
  * struct, the counterpart of ispc_nest; ispc_emit_tiles turns it into one
  * sm_100a kernel assembled from hand-written building blocks. */
-enum ispc_tile_kind { ISPC_TILE_GEMV = 0, ISPC_TILE_SGEMM, ISPC_TILE_BATCHED, ISPC_TILE_SGEMM_TC };
+enum ispc_tile_kind { ISPC_TILE_GEMV = 0, ISPC_TILE_SGEMM, ISPC_TILE_BATCHED, ISPC_TILE_SGEMM_TC, ISPC_TILE_AXPY };
 enum ispc_staging { ISPC_STAGE_DIRECT = 0, ISPC_STAGE_SHARED, ISPC_STAGE_CP_ASYNC, ISPC_STAGE_TMA };
 enum ispc_engine { ISPC_ENGINE_FFMA = 0, ISPC_ENGINE_TF32, ISPC_ENGINE_TF32X3 };
 enum ispc_xreduce { ISPC_XRED_SHUFFLE = 0, ISPC_XRED_SHARED };
@@ -279,6 +279,8 @@ typedef struct {
   int32_t split;                 /* gemv: cluster CTAs splitting the columns (DSMEM) */
   int32_t unroll;                /* gemv: column loop unroll                        */
   int32_t per_cta;               /* batched: problems per CTA                       */
+  int32_t threads;               /* axpy stream: threads per CTA                    */
+  int32_t grid;                  /* axpy stream: CTAs (0: one vector group per thread) */
   int32_t _pad2;
 } ispc_tile_config;
 

@@ -24,7 +24,7 @@ OK, E_ARG, E_CUDA, E_NVRTC, E_LAUNCH, E_MISMATCH, E_TIMEOUT, E_ILLEGAL, E_NOMEM,
 
 PROB_AXPY, PROB_OUTER, PROB_MATMUL, PROB_GEMV, PROB_BATCHED = range(5)
 SPACE_PARITY, SPACE_B200 = 0, 1
-TILE_GEMV, TILE_SGEMM, TILE_BATCHED, TILE_SGEMM_TC = range(4)
+TILE_GEMV, TILE_SGEMM, TILE_BATCHED, TILE_SGEMM_TC, TILE_AXPY = range(5)
 STAGINGS = ("DIRECT", "SHARED", "CP_ASYNC", "TMA")
 ENGINES = ("FFMA", "TF32", "TF32X3")
 XREDUCES = ("SHUFFLE", "SHARED")
@@ -117,7 +117,7 @@ class TileConfig(C.Structure):
                 + [(f, C.c_int64) for f in ("m", "n", "k", "batch")]
                 + [(f, C.c_int32) for f in ("thr_m", "thr_n", "tm", "tn", "bk", "bn", "stages", "vec", "lanes_m",
                                             "lanes_n", "warps_m", "warps_n", "split", "unroll", "per_cta",
-                                            "_pad2")])
+                                            "threads", "grid", "_pad2")])
 
     def as_dict(self) -> dict:
         d = {f: getattr(self, f) for f, _ in self._fields_ if not f.startswith("_")}

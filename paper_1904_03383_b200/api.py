@@ -20,7 +20,7 @@ from . import _native as N
 class Space:
     """A kernel backbone bound to the GPU decision space (gpu_space.hpp:15-18)."""
 
-    TILE_KINDS = ("gemv", "sgemm", "batched", "sgemm_tc", "sgemm_tc_x3")
+    TILE_KINDS = ("gemv", "sgemm", "batched", "sgemm_tc", "sgemm_tc_x3", "axpy_stream")
 
     def __init__(self, kind: str, *, m: int = 0, n: int = 0, k: int = 0, a_stride: int = 1,
                  factors: list[list[int]] | None = None, mode: int = N.SPACE_PARITY, batch: int = 1):
@@ -357,7 +357,7 @@ class Device:
         """Emit + compile + timed launch + on-device check of a building-block
         configuration. Default checking: bit-exact for the FFMA sgemm and
         batched kernels (k ascending per output), norm-wise rtol otherwise."""
-        exact_default = (cfg.kind == N.TILE_SGEMM and cfg.split <= 1) or cfg.kind == N.TILE_BATCHED
+        exact_default = (cfg.kind == N.TILE_SGEMM and cfg.split <= 1) or cfg.kind in (N.TILE_BATCHED, N.TILE_AXPY)
         if bit_exact is None:
             bit_exact = exact_default
         if rtol is None:

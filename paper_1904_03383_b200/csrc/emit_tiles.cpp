@@ -753,18 +753,79 @@ std::string batched(const ispc_tile_config& c, const std::string& fn, ispc_launc
   return o.str();
 }
 
+// ---------------------------------------------------------------- axpy stream
+// z = alpha*x + y (mul then add, each rounded: the backbone's two
+// instructions, kernels.cpp:397-403). Vector group c (vec floats) of a
+// grid-stride walk: c = (blockIdx.x*unroll + u)*threads + tid, so a warp
+// touches 32 consecutive vectors per load; `unroll` groups in flight per
+// thread; grid = `grid` CTAs (0: exactly one group per thread).
+std::string axpy_stream(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
+  const int64_t n = c.n;
+  const int V = c.vec, T = c.threads, U = c.unroll;
+  if (!(V == 1 || V == 2 || V == 4)) illegal("vector width must be 1, 2 or 4");
+  if (T < 32 || T > 1024 || T % 32) illegal("threads per CTA must be a multiple of 32 up to 1024");
+  if (U < 1) illegal("non-positive unroll");
+  if (n % V) illegal("vector width does not divide n");
+  const int64_t groups = n / V, per_cta = int64_t(T) * U;
+  const int64_t grid = c.grid > 0 ? c.grid : (groups + per_cta - 1) / per_cta;
+  if (grid > 0x7fffffffLL) illegal("grid exceeds 2^31-1 CTAs");
+  const std::string ty = V == 4 ? "float4" : V == 2 ? "float2" : "float";
+  const bool stream_st = c.cache == ISPC_CACHE_NONE || c.cache == ISPC_CACHE_STREAM;
+  std::ostringstream o;
+  o << "extern \"C\" __global__ void __launch_bounds__(" << T << ") " << fn
+    << "(const float* __restrict__ g_x, const float* __restrict__ g_y, float* __restrict__ g_z, const float p_alpha) {\n";
+  o << "  const " << ty << "* __restrict__ vx = (const " << ty << "*)g_x;\n";
+  o << "  const " << ty << "* __restrict__ vy = (const " << ty << "*)g_y;\n";
+  o << "  " << ty << "* __restrict__ vz = (" << ty << "*)g_z;\n";
+  o << "  #pragma unroll 1\n";
+  o << "  for (long long c0 = (long long)blockIdx.x * " << per_cta << "LL + threadIdx.x; c0 < " << groups
+    << "LL; c0 += (long long)gridDim.x * " << per_cta << "LL) {\n";
+  o << "    " << ty << " xv[" << U << "], yv[" << U << "];\n";
+  o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; ++u) {\n";
+  o << "      const long long g = c0 + u * " << T << ";\n";
+  o << "      if (g < " << groups << "LL) { xv[u] = " << ld(c.cache, V, "vx + g") << "; yv[u] = "
+    << ld(c.cache, V, "vy + g") << "; }\n";
+  o << "    }\n";
+  o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; ++u) {\n";
+  o << "      const long long g = c0 + u * " << T << ";\n";
+  o << "      if (g < " << groups << "LL) {\n";
+  o << "        " << ty << " r;\n";
+  if (V == 1) o << "        r = __fadd_rn(__fmul_rn(p_alpha, xv[u]), yv[u]);\n";
+  else
+    for (int v = 0; v < V; ++v)
+      o << "        r" << comp(v) << " = __fadd_rn(__fmul_rn(p_alpha, xv[u]" << comp(v) << "), yv[u]" << comp(v)
+        << ");\n";
+  o << "        " << (stream_st ? "__stcs(vz + g, r);" : "vz[g] = r;") << "\n";
+  o << "      }\n    }\n  }\n}\n";
+  L.grid_x = uint64_t(grid);
+  L.block[0] = uint32_t(T);
+  L.block[1] = L.block[2] = 1;
+  add_region(L, "x", n);
+  add_region(L, "y", n);
+  add_region(L, "z", n);
+  ispc_param& P = L.params[L.num_params++];
+  P.kind = ISPC_PARAM_INPUT;
+  P.index = 0;
+  std::snprintf(P.name, sizeof(P.name), "alpha");
+  L.reg_elems = uint32_t(2 * V * U);
+  return o.str();
+}
+
 }  // namespace
 
 std::string emit_tile_kernel(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
   std::memset(&L, 0, sizeof(L));
   std::snprintf(L.name, sizeof(L.name), "%s", fn.c_str());
-  if (c.m <= 0 || c.n <= 0 || (c.kind != ISPC_TILE_GEMV && c.k <= 0)) illegal("empty problem");
+  if (c.n <= 0 || (c.kind != ISPC_TILE_AXPY && c.m <= 0) ||
+      (c.kind != ISPC_TILE_GEMV && c.kind != ISPC_TILE_AXPY && c.k <= 0))
+    illegal("empty problem");
   std::string src;
   switch (c.kind) {
     case ISPC_TILE_GEMV: src = gemv(c, fn, L); break;
     case ISPC_TILE_SGEMM: src = sgemm(c, fn, L); break;
     case ISPC_TILE_BATCHED: src = batched(c, fn, L); break;
     case ISPC_TILE_SGEMM_TC: src = emit_tcgen05_kernel(c, fn, L); break;
+    case ISPC_TILE_AXPY: src = axpy_stream(c, fn, L); break;
     default: throw NestError(ISPC_E_ARG, "unknown tile kind");
   }
   if (L.static_smem > 232448) illegal("shared memory exceeds 227 KiB");

@@ -153,7 +153,7 @@ int ispc_space_problem(const ispc_space* s, ispc_problem* p) {
   p->k = s->spec.k;
   p->a_stride = s->spec.a_stride > 0 ? s->spec.a_stride : 1;
   p->batch = 1;
-  if (k == "axpy") p->kind = ISPC_PROB_AXPY;
+  if (k == "axpy" || k == "axpy_stream") p->kind = ISPC_PROB_AXPY;
   else if (k == "outer_product") p->kind = ISPC_PROB_OUTER;
   else if (k == "matmul" || k == "sgemm" || k == "sgemm_tc" || k == "sgemm_tc_x3") p->kind = ISPC_PROB_MATMUL;
   else if (k == "gemv") p->kind = ISPC_PROB_GEMV;

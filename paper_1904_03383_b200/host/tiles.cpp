@@ -50,17 +50,20 @@ constexpr double kLaunch = 1e-6;
 }  // namespace
 
 bool is_tile_kind(const std::string& k) {
-  return k == "gemv" || k == "sgemm" || k == "batched" || k == "sgemm_tc" || k == "sgemm_tc_x3";
+  return k == "gemv" || k == "sgemm" || k == "batched" || k == "sgemm_tc" || k == "sgemm_tc_x3" ||
+         k == "axpy_stream";
 }
 
 const char* tiles_space_text() { return kTilesSpaceText; }
 
-bool TileFamily::bit_exact() const { return kind == ISPC_TILE_SGEMM || kind == ISPC_TILE_BATCHED; }
+bool TileFamily::bit_exact() const {
+  return kind == ISPC_TILE_SGEMM || kind == ISPC_TILE_BATCHED || kind == ISPC_TILE_AXPY;
+}
 
 bool tile_bit_exact(const ispc_tile_config& t) {
   // FFMA kernels that keep one k-ascending chain per output; split-K sums
   // cluster partials and is checked norm-wise
-  return (t.kind == ISPC_TILE_SGEMM && t.split <= 1) || t.kind == ISPC_TILE_BATCHED;
+  return (t.kind == ISPC_TILE_SGEMM && t.split <= 1) || t.kind == ISPC_TILE_BATCHED || t.kind == ISPC_TILE_AXPY;
 }
 
 double TileFamily::rtol() const {
@@ -140,6 +143,21 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     else pre("engine", {"TF32", "TF32X3"});
     pre("xreduce", {"SHUFFLE"});
     pre("cache", {"L2"});
+  } else if (kind == "axpy_stream") {
+    // the elementwise streaming block for axpy (the parity space's axpy is
+    // the reference's own gpu.space; this one is B200 building blocks only)
+    if (n <= 0) throw std::invalid_argument("axpy_stream needs n > 0");
+    f.kind = ISPC_TILE_AXPY;
+    TileParam vec = P("vec", dividing({1, 2, 4}, n)), thr = P("threads", pow2_upto(32, 1024));
+    TileParam unroll = P("unroll", {1, 2, 4, 8}), grid = P("grid", {0, 148, 296, 592, 1184, 2368, 4736});
+    thr.thread = true;
+    vec.acc = unroll.acc = true;
+    f.params = {vec, thr, unroll, grid};
+    f.min_threads = 32;
+    f.max_acc = 32;
+    pre("staging", {"DIRECT"});
+    pre("engine", {"FFMA"});
+    pre("xreduce", {"SHUFFLE"});
   } else {
     throw std::invalid_argument("not a building-block kernel kind: " + kind);
   }
@@ -274,6 +292,8 @@ ispc_tile_config tile_config(const TileFamily& f, const SpaceContext& ctx, const
   t.stages = v("stages"), t.vec = v("vec"), t.lanes_m = v("lanes_m"), t.lanes_n = v("lanes_n");
   t.warps_m = v("warps_m"), t.warps_n = v("warps_n"), t.split = v("split"), t.unroll = v("unroll");
   t.per_cta = v("per_cta");
+  t.threads = v("threads");
+  t.grid = v("grid");
   return t;
 }
 
@@ -301,6 +321,11 @@ TileBoundReport tile_bound(const TileFamily& f, const SpaceContext& ctx, const C
       } else {
         b.ctas = M / 128 * (N / lo("bn"));
       }
+      break;
+    case ISPC_TILE_AXPY:
+      b.dram_bytes = 12 * N;
+      flops = 2 * N;
+      b.ctas = N / (lo("vec") * lo("threads") * lo("unroll"));
       break;
     case ISPC_TILE_BATCHED:
       b.dram_bytes = 4 * B * (M * K + K * N + M * N);

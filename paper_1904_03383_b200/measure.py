@@ -28,7 +28,7 @@ def work(space) -> dict:
     """Algorithmic bytes and flops of one launch of the space's kernel."""
     m, n, k, b = space.m, space.n, space.k, max(space.batch, 1)
     kind = space.kind
-    if kind == "axpy":
+    if kind in ("axpy", "axpy_stream"):
         return {"bytes": 12 * n, "flops": 2 * n, "bound": "hbm"}
     if kind == "gemv":
         return {"bytes": 4 * (m * n + m + n), "flops": 2 * m * n, "bound": "hbm"}
@@ -71,7 +71,7 @@ def rotation(space, l2_bytes: int) -> int:
 
 def output_bytes(space) -> int:
     m, n, b = space.m, space.n, max(space.batch, 1)
-    if space.kind == "axpy":
+    if space.kind in ("axpy", "axpy_stream"):
         return 4 * n
     if space.kind == "gemv":
         return 4 * m
@@ -167,7 +167,7 @@ def cublas_reference(space, reps: int = 20) -> dict | None:
             return lambda: fn(*ts)
         return make
 
-    if kind == "axpy":
+    if kind in ("axpy", "axpy_stream"):
         out["axpy"] = _time_rotating(mk([(n,), (n,)], lambda x, y: y.add_(x, alpha=1.5)), rot)
     elif kind == "gemv":
         out["sgemv"] = _time_rotating(mk([(n, m), (n,)], lambda at, x: torch.mv(at.t(), x)), rot)

@@ -222,3 +222,7 @@ def test_cli_explore_then_replay(tmp_path, capsys):
     assert cli.main(["replay", str(log), *args]) == 0
     rows = [json.loads(l) for l in capsys.readouterr().out.strip().splitlines()]
     assert rows and all(r["status"] == "ok" for r in rows)
+
+
+def test_axpy_stream_full_size_bit_exact(dev):
+    _run_many(dev, Space("axpy_stream", n=1 << 26), 30, 10)

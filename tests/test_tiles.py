@@ -182,3 +182,22 @@ def test_cli_codegen_and_bound(capsys):
     assert b["dram"] > 8e-6 and b["total"] >= b["dram"]
     assert cli.main(["codegen", "axpy", "--n", "1024", "--factors", "4", "2,8,32", "--seed", "1"]) == 0
     assert "__global__" in capsys.readouterr().out
+
+
+def test_axpy_stream_bit_exact_on_emulator():
+    s = Space("axpy_stream", n=4096)
+    orc = Oracle()
+    p = s.problem()
+    x, y = orc.fill(4096, p.seed, "x"), orc.fill(4096, p.seed, "y")
+    ref = orc.axpy(x, y, p.alpha)
+    checked = 0
+    for leaf in _leaves(s, 40):
+        t = leaf.tiles()
+        if t.grid == 0 or t.threads > 256:
+            continue  # keep the fiber emulation small
+        src, L = tile_cuda(t, "k_emu")
+        regs = {"x": x.copy(), "y": y.copy(), "z": np.full(4096, np.nan, dtype=np.float32)}
+        emu.run(src, L, regs, p.alpha)
+        assert np.array_equal(regs["z"].view(np.uint32), ref.view(np.uint32)), t.as_dict()
+        checked += 1
+    assert checked >= 3
