@@ -15,7 +15,7 @@ nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/${
 # launch list (cold-cache, serialised: compare shares, not absolutes)
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/${TAG}_launches.csv \
   env BENCH_NO_SAVE_BEST=1 python bench.py --steps 1 --warmup 1 --per-step 16 --configs none --no-cpu-baseline > $OUT/${TAG}_ncu_bench.log 2>&1
-for k in axpy gemv sgemm batched sgemm_tc sgemm_tc_x3 sgemm_1024_x3; do
+for k in axpy axpy_stream gemv sgemm batched sgemm_tc sgemm_tc_x3 sgemm_1024_x3; do
   if [ -f $OUT/best_$k.json ]; then
     timeout 600 ncu --set full --import-source on --clock-control none -k regex:^ispc_[kt] -s 4 -c 1 \
       -o $OUT/${TAG}_prof_$k -f python tools/profile_best.py $k > $OUT/${TAG}_prof_$k.log 2>&1
