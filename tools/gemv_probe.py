@@ -9,16 +9,18 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 CFGS = [
-    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=32, warps_m=1, warps_n=4, split=8, unroll=8),
-    dict(staging="DIRECT", cache="STREAM", vec=4, lanes_m=32, warps_m=1, warps_n=4, split=8, unroll=8),
-    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=32, warps_m=2, warps_n=2, split=8, unroll=16),
-    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=32, warps_m=1, warps_n=8, split=4, unroll=4),
-    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=16, warps_m=1, warps_n=8, split=8, unroll=8),
-    dict(staging="DIRECT", cache="NONE", vec=2, lanes_m=32, warps_m=1, warps_n=8, split=8, unroll=16),
-    dict(staging="TMA", cache="L2", vec=4, lanes_m=32, warps_m=1, warps_n=4, split=8, bk=32, stages=4),
-    dict(staging="TMA", cache="L2", vec=4, lanes_m=32, warps_m=2, warps_n=2, split=8, bk=64, stages=3),
-    dict(staging="TMA", cache="L2", vec=4, lanes_m=16, warps_m=2, warps_n=4, split=8, bk=32, stages=6),
-    dict(staging="CP_ASYNC", cache="L2", vec=4, lanes_m=32, warps_m=1, warps_n=4, split=8, bk=32, stages=4),
+    # long contiguous column segments (512 B per warp) with many loads in flight
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=32, warps_m=1, warps_n=8, split=8, unroll=16),
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=32, warps_m=1, warps_n=16, split=8, unroll=8),
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=32, warps_m=1, warps_n=32, split=8, unroll=4),
+    dict(staging="DIRECT", cache="STREAM", vec=4, lanes_m=32, warps_m=1, warps_n=16, split=8, unroll=16),
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=16, warps_m=1, warps_n=16, split=8, unroll=16),
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=8, warps_m=1, warps_n=8, split=8, unroll=16),
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=8, warps_m=1, warps_n=16, split=8, unroll=8),
+    dict(staging="TMA", cache="L2", vec=4, lanes_m=32, warps_m=1, warps_n=8, split=8, bk=64, stages=4),
+    dict(staging="TMA", cache="L2", vec=4, lanes_m=32, warps_m=1, warps_n=4, split=8, bk=128, stages=4),
+    dict(staging="TMA", cache="L2", vec=4, lanes_m=32, warps_m=2, warps_n=4, split=8, bk=64, stages=3),
+    dict(staging="CP_ASYNC", cache="L2", vec=4, lanes_m=32, warps_m=1, warps_n=8, split=8, bk=64, stages=4),
 ]
 
 
