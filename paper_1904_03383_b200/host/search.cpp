@@ -95,6 +95,11 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
   if (cfg_.reps <= 0) cfg_.reps = 3;
   if (cfg_.max_unrolled <= 0) cfg_.max_unrolled = 512;
   unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+  // one process per GPU: the ranks of this node share its cores
+  if (const char* lws = std::getenv("LOCAL_WORLD_SIZE")) {
+    const int ranks = std::atoi(lws);
+    if (ranks > 1) hw = std::max(2u, hw / unsigned(ranks));
+  }
   // measured on the B200 boxes (16 cores): propagation-heavy rollouts cost
   // ~2x the CPU of NVRTC per produced kernel, so they get ~5/8 of the cores
   if (cfg_.rollout_threads <= 0) cfg_.rollout_threads = int(std::max(1u, hw * 5 / 8));
