@@ -109,18 +109,20 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   if (S < 2 || S > 8) illegal("TMA ring depth must be 2..8");
   if (M % 128 || N % BN || K % 32) illegal("shape not divisible by the 128 x BN x 32 tile");
   if (M > (int64_t(1) << 31) || K > (int64_t(1) << 31)) illegal("shape too large for the tensor maps");
-  // stage: [A as landed, m contiguous][B, k contiguous][A k contiguous]
-  //        (X3: [A small][B small]); every part 1 KiB aligned
+  // TMA ring stage: [A as landed, m contiguous][B, k contiguous]([B small])
+  // transposed-A ring, 2 slots: [A k contiguous]([A small]); 1 KiB aligned parts
   const int64_t a_bytes = 128 * 32 * 4, b_bytes = int64_t(BN) * 32 * 4, tma_bytes = a_bytes + b_bytes;
-  const int64_t off_b = a_bytes, off_ak = a_bytes + b_bytes, off_aks = off_ak + a_bytes, off_bs = off_aks + a_bytes;
-  const int64_t stage = off_ak + a_bytes + (X3 ? a_bytes + b_bytes : 0);
-  const int64_t bar_off = S * stage;
-  const int nbar = 3 * S + 1;  // full[S], empty[S], conv[S], acc
+  const int64_t off_b = a_bytes, off_bs = a_bytes + b_bytes;
+  const int64_t stage = tma_bytes + (X3 ? b_bytes : 0);
+  const int64_t slot = a_bytes * (X3 ? 2 : 1);
+  const int64_t ak_off = S * stage, bar_off = ak_off + 2 * slot;
+  const int nbar = 2 * S + 4 + 1;  // full[S], empty[S], conv[2], akfree[2], acc
   const int64_t smem = bar_off + (nbar + 1) * 8 + 1024;  // + slack to 1 KiB-align the base
   if (smem > 232448) illegal("TMA ring exceeds 227 KiB of shared memory");
   // kind::tf32, fp32 accumulate, A and B K-major, N = BN, M = 128
   const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(128 >> 4) << 24);
   const int64_t KB = K / 32, MB = M / 128;
+  const unsigned FULL = 0, EMPTY = 8u * S, CONV = 16u * S, AKFREE = 16u * S + 16, ACC = 16u * S + 32;
 
   std::ostringstream o;
   o << tcgen05_prelude();
@@ -129,15 +131,15 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   o << "  extern __shared__ __align__(1024) unsigned char ispc_smem_raw[];\n";
   o << "  const unsigned raw = ispc_smem_addr(ispc_smem_raw);\n";
   o << "  const unsigned base = (raw + 1023u) & ~1023u;\n";
-  o << "  const unsigned bars = base + " << bar_off << "u;  // full[S], empty[S], conv[S], acc, tmem slot\n";
+  o << "  const unsigned bars = base + " << bar_off << "u;  // full[S], empty[S], conv[2], akfree[2], acc, tmem slot\n";
+  o << "  const unsigned ak = base + " << ak_off << "u;     // transposed-A slots\n";
   o << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
   o << "  const int m_blk = blockIdx.x % " << MB << ", n_blk = blockIdx.x / " << MB << ";\n";
   o << "  unsigned char* gen = ispc_smem_raw + (base - raw);\n";
   o << "  unsigned* tmem_slot = (unsigned*)(gen + " << bar_off + nbar * 8 << ");\n";
-  o << "  const unsigned acc_bar = bars + " << 8 * 3 * S << "u;\n";
   o << "  if (threadIdx.x == 0) {\n";
-  o << "    for (int s = 0; s < " << nbar << "; ++s) ispc_mbar_init(bars + 8u * s, (s >= " << 2 * S << " && s < "
-    << 3 * S << ") ? 128u : 1u);\n";
+  o << "    for (int s = 0; s < " << nbar << "; ++s)\n";
+  o << "      ispc_mbar_init(bars + 8u * s, (s >= " << 2 * S << " && s < " << 2 * S + 2 << ") ? 128u : 1u);\n";
   o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
   o << "    asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&tm_a) : \"memory\");\n";
   o << "    asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&tm_b) : \"memory\");\n";
@@ -151,12 +153,12 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   o << "  __syncthreads();\n";
   o << "  asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
   o << "  const unsigned tmem = *(volatile unsigned*)tmem_slot;\n";
-  // producer
+  // producer: TMA ring of S stages
   o << "  if (warp == 0 && lane == 0) {\n";
   o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
   o << "      const int s = kb % " << S << ";\n";
-  o << "      if (kb >= " << S << ") ispc_mbar_wait(bars + 8u * (" << S << " + s), ((kb / " << S << ") + 1) & 1);\n";
-  o << "      const unsigned full = bars + 8u * s;\n";
+  o << "      if (kb >= " << S << ") ispc_mbar_wait(bars + " << EMPTY << "u + 8u * s, ((kb / " << S << ") + 1) & 1);\n";
+  o << "      const unsigned full = bars + " << FULL << "u + 8u * s;\n";
   o << "      const unsigned sa = base + s * " << stage << "u;\n";
   o << "      ispc_mbar_expect_tx(full, " << tma_bytes << "u);\n";
   o << "      #pragma unroll\n";
@@ -164,19 +166,20 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   o << "      ispc_tma_2d(sa + " << off_b << "u, &tm_b, kb * 32, n_blk * " << BN << ", full);\n";
   o << "    }\n";
   o << "  } else if (warp == 1 && lane == 0) {\n";
-  // MMA issuer: A and B K-major, 128-byte swizzle: SBO = 1 KiB (8 rows), +32 B per K=8 step
+  // MMA issuer: A (transposed slot) and B (TMA stage), both K-major 128-B swizzle
   o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
-  o << "      const int s = kb % " << S << ";\n";
-  o << "      ispc_mbar_wait(bars + 8u * (" << 2 * S << " + s), (kb / " << S << ") & 1);\n";
+  o << "      const int s = kb % " << S << ", a2 = kb & 1;\n";
+  o << "      ispc_mbar_wait(bars + " << CONV << "u + 8u * a2, (kb >> 1) & 1);\n";
   o << "      asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
-  o << "      const unsigned sa = base + s * " << stage << "u;\n";
+  o << "      const unsigned sb = base + s * " << stage << "u + " << off_b << "u;\n";
+  o << "      const unsigned sk = ak + a2 * " << slot << "u;\n";
   o << "      #pragma unroll\n";
   o << "      for (int kk = 0; kk < 4; ++kk) {\n";
-  o << "        const unsigned long long da = ispc_umma_desc(sa + " << off_ak << "u + kk * 32u, 16u, 1024u);\n";
-  o << "        const unsigned long long db = ispc_umma_desc(sa + " << off_b << "u + kk * 32u, 16u, 1024u);\n";
+  o << "        const unsigned long long da = ispc_umma_desc(sk + kk * 32u, 16u, 1024u);\n";
+  o << "        const unsigned long long db = ispc_umma_desc(sb + kk * 32u, 16u, 1024u);\n";
   if (X3) {
-    o << "        const unsigned long long das = ispc_umma_desc(sa + " << off_aks << "u + kk * 32u, 16u, 1024u);\n";
-    o << "        const unsigned long long dbs = ispc_umma_desc(sa + " << off_bs << "u + kk * 32u, 16u, 1024u);\n";
+    o << "        const unsigned long long das = ispc_umma_desc(sk + " << a_bytes << "u + kk * 32u, 16u, 1024u);\n";
+    o << "        const unsigned long long dbs = ispc_umma_desc(sb + " << b_bytes << "u + kk * 32u, 16u, 1024u);\n";
     o << "        ispc_mma_tf32(tmem, das, db, " << idesc << "u, (kb | kk) != 0);\n";
     o << "        ispc_mma_tf32(tmem, da, dbs, " << idesc << "u, 1u);\n";
     o << "        ispc_mma_tf32(tmem, da, db, " << idesc << "u, 1u);\n";
@@ -184,17 +187,21 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
     o << "        ispc_mma_tf32(tmem, da, db, " << idesc << "u, (kb | kk) != 0);\n";
   }
   o << "      }\n";
-  o << "      ispc_mma_commit(bars + 8u * (" << S << " + s));\n";
+  o << "      ispc_mma_commit(bars + " << EMPTY << "u + 8u * s);   // TMA stage free\n";
+  o << "      ispc_mma_commit(bars + " << AKFREE << "u + 8u * a2);  // transposed slot free\n";
   o << "    }\n";
-  o << "    ispc_mma_commit(acc_bar);\n";
+  o << "    ispc_mma_commit(bars + " << ACC << "u);\n";
   o << "  } else if (warp >= 4) {\n";
-  // converters: the tf32 tensor path reads K-major operands only, so A (m
-  // contiguous in memory) is transposed in shared memory, row m = thread
+  // converters: the tf32 tensor path reads K-major operands only (MN-major
+  // descriptors read zeros on sm_100a, tools/tc_probe.cu), so every landed A
+  // tile is transposed into a 2-slot K-major ring, row m = thread
   o << "    const int m = threadIdx.x - 128;\n";
   o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
-  o << "      const int s = kb % " << S << ";\n";
-  o << "      ispc_mbar_wait(bars + 8u * s, (kb / " << S << ") & 1);\n";
+  o << "      const int s = kb % " << S << ", a2 = kb & 1;\n";
+  o << "      ispc_mbar_wait(bars + " << FULL << "u + 8u * s, (kb / " << S << ") & 1);\n";
+  o << "      if (kb >= 2) ispc_mbar_wait(bars + " << AKFREE << "u + 8u * a2, ((kb >> 1) + 1) & 1);\n";
   o << "      unsigned char* st = gen + s * " << stage << ";\n";
+  o << "      unsigned char* sk = gen + " << ak_off << " + a2 * " << slot << ";\n";
   o << "      const unsigned src_row = (m >> 5) * 4096u + (m & 3) * 4u;\n";
   o << "      const unsigned dst_row = (m >> 3) * 1024u + (m & 7) * 128u;\n";
   o << "      #pragma unroll\n";
@@ -210,13 +217,13 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
     o << "        float4 hi, lo;\n";
     o << "        hi.x = ispc_tf32_rna(v[0]); hi.y = ispc_tf32_rna(v[1]); hi.z = ispc_tf32_rna(v[2]); hi.w = ispc_tf32_rna(v[3]);\n";
     o << "        lo.x = v[0] - hi.x; lo.y = v[1] - hi.y; lo.z = v[2] - hi.z; lo.w = v[3] - hi.w;\n";
-    o << "        *(float4*)(st + " << off_ak << " + dst) = hi;\n";
-    o << "        *(float4*)(st + " << off_aks << " + dst) = lo;\n";
+    o << "        *(float4*)(sk + dst) = hi;\n";
+    o << "        *(float4*)(sk + " << a_bytes << " + dst) = lo;\n";
   } else {
-    o << "        *(float4*)(st + " << off_ak << " + dst) = make_float4(v[0], v[1], v[2], v[3]);\n";
+    o << "        *(float4*)(sk + dst) = make_float4(v[0], v[1], v[2], v[3]);\n";
   }
   o << "      }\n";
-  if (X3) {
+  if (X3) {  // B split in place (big) + small part beside it in the TMA stage
     o << "      #pragma unroll 4\n";
     o << "      for (int i = m; i < " << b_bytes / 16 << "; i += 128) {\n";
     o << "        float4* pb = (float4*)(st + " << off_b << ") + i;\n";
@@ -229,13 +236,13 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
     o << "      }\n";
   }
   o << "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
-  o << "      ispc_mbar_arrive(bars + 8u * (" << 2 * S << " + s));\n";
+  o << "      ispc_mbar_arrive(bars + " << CONV << "u + 8u * a2);\n";
   o << "    }\n";
   o << "  }\n";
   o << "  __syncwarp();\n";
   // epilogue: TMEM lane group = warp % 4, column half = warp / 4
   const int cols = BN / 2;
-  o << "  ispc_mbar_wait(acc_bar, 0);\n";
+  o << "  ispc_mbar_wait(bars + " << ACC << "u, 0);\n";
   o << "  asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
   o << "  const int lg = warp & 3, c_begin = (warp >> 2) * " << cols << ";\n";
   o << "  const long long row = (long long)m_blk * 128 + lg * 32 + lane;\n";
