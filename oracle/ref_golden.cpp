@@ -214,6 +214,11 @@ int main(int argc, char** argv) {
   add("matmul_16x8x4", "matmul", 16, 8, 4, {{2}, {2, 4}}, 1);
   add("strided_matmul_8x4x4_s3", "matmul", 8, 4, 4, {{2}}, 3);
   add("matmul_12x6x5", "matmul", 12, 6, 5, {{3}}, 1);
+  // gemv and batched have no reference builder (kernel_test.cpp:351); their
+  // semantics are the reference matmul's with n = 1 (y = A x, A column-major)
+  // and a sequence of independent matmuls: pinned through these cases
+  add("gemv_as_matmul_32x1x24", "matmul", 32, 1, 24, {}, 1);
+  add("gemv_as_matmul_64x1x100", "matmul", 64, 1, 100, {}, 1);
 
   FILE* f = std::fopen(argv[1], "w");
   std::fprintf(f, "{\n  \"generator\": \"oracle/ref_golden.cpp (reference Kernel interpreted via eval_addr)\",\n");
