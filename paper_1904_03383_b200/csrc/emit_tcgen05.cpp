@@ -2,29 +2,31 @@
 // matmul contraction (BASELINE.json config 5), C = A B with fp32 column-major
 // operands on the TF32 tensor pipe, fp32 accumulation in tensor memory.
 //
-// One CTA computes a 128 x BN tile of C with 128 threads:
-//   warp 0 lane 0  TMA producer: per k block (32 deep) one 3-D box of A and
-//                  one 2-D box of B into stage s of a `stages`-deep ring,
-//                  completion counted on full[s] (mbarrier expect_tx)
-//   warp 1         allocates BN TMEM columns; lane 0 issues 4 x
-//                  tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=BN, K=8)
-//                  per k block and tcgen05.commit's empty[s] back to the
-//                  producer, then the accumulator barrier
-//   warps 0-3      epilogue: tcgen05.ld 32x32b.x32 (warp w owns TMEM lanes
-//                  32w..32w+31 = rows), coalesced column-major stores
-// Shared-memory operand layouts (UMMA canonical forms, 128-byte swizzle):
-//   A  MN-major (m contiguous, as in memory): atoms of 32 m x 8 k (1 KiB);
-//      four TMA boxes {32 m, 32 k} land k rows of 128 B per 32 m, so
-//      SBO (next 8 k) = 1 KiB and LBO (next 32 m) = 4 KiB
-//   B  K-major (k contiguous, as in memory): row n = 32 k (128 B), 8-row
-//      atoms, SBO = 1 KiB; the k step inside the 128-B row advances the
-//      descriptor start by 32 B
-// TF32X3 (engine value): 256 threads; warps 4-7 split every landed stage in
-// place, x -> big = cvt.rna.tf32(x) (exactly representable) and, in a second
-// buffer of the same swizzled layout, small = x - big; they fence the writes
-// to the async proxy and arrive on conv[s]. The MMA lane then issues
-// big*big + big*small + small*big per k step (fp32-level accuracy from the
-// TF32 pipe). The epilogue splits the columns between warps w and w+4.
+// One CTA (split = 1) or a cluster pair (split = 2, cta_group::2, UMMA M = 256
+// over two SMs) computes a UMMA_M x BN tile of C with 256 threads per CTA:
+//   warp 0 lane 0  producer: per k block (32 deep) TMA boxes of this CTA's
+//                  B rows (BN / split of them) and, for staging TMA, its 128
+//                  A rows into stage s of a `stages`-deep ring; full[s]
+//                  counts the bytes (mbarrier expect_tx)
+//   warps 4-7      converters, row m = thread: tf32 UMMA reads K-major
+//                  operands only (MN-major reads zeros on sm_100a,
+//                  tools/tc_probe.cu) and A is m-contiguous, so each k block
+//                  of A is written K-major (128-B swizzle) into the stage:
+//                  staging TMA transposes the landed box, staging SHARED
+//                  loads A from global memory one k block ahead in
+//                  registers. TF32X3 also splits x -> big = cvt.rna.tf32(x),
+//                  small = x - big for A and (in place) B. They fence to the
+//                  async proxy and arrive on conv[s] (the leader's, remotely,
+//                  for a pair)
+//   warp 1         allocates BN TMEM columns; lane 0 of the (leader) CTA
+//                  issues 4 (x3 for TF32X3) tcgen05.mma per k block and
+//                  commits empty[s] (multicast to both CTAs of a pair), then
+//                  the accumulator barrier
+//   warps 0-7      epilogue: tcgen05.ld 32x32b.x32 (lane group = warp % 4,
+//                  column half = warp / 4), coalesced column-major stores
+// Operand descriptors: K-major, 128-B swizzle, rows of 32 tf32 (128 B),
+// 8-row atoms, SBO = 1 KiB; the k step inside the row advances the start
+// address by 32 B.
 #include <cstdio>
 #include <cstring>
 #include <sstream>
@@ -53,6 +55,12 @@ static __device__ __forceinline__ void ispc_mbar_wait(unsigned bar, unsigned par
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra ISPC_WAIT_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
 }
+static __device__ __forceinline__ void ispc_mbar_wait_cluster(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n ISPC_WAITC_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra ISPC_WAITC_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
+}
 static __device__ __forceinline__ void ispc_mbar_expect_tx(unsigned bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
@@ -75,6 +83,23 @@ static __device__ __forceinline__ void ispc_mma_tf32(unsigned tmem, unsigned lon
 }
 static __device__ __forceinline__ void ispc_mbar_arrive(unsigned bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+static __device__ __forceinline__ void ispc_mbar_arrive_rank(unsigned bar, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(bar), "r"(rank));
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+}
+static __device__ __forceinline__ void ispc_mma_tf32_pair(unsigned tmem, unsigned long long da, unsigned long long db,
+                                                          unsigned idesc, unsigned accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem), "l"(da), "l"(db), "r"(idesc),
+      "r"(accumulate) : "memory");
+}
+static __device__ __forceinline__ void ispc_mma_commit_pair(unsigned bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((unsigned short)3) : "memory");
 }
 static __device__ __forceinline__ float ispc_tf32_rna(float x) {
   unsigned r;
@@ -100,60 +125,80 @@ static __device__ __forceinline__ void ispc_mma_commit(unsigned bar) {
 
 std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
   const int64_t M = c.m, N = c.n, K = c.k;
-  const int BN = c.bn, S = c.stages;
-  if (c.staging != ISPC_STAGE_TMA) illegal("the tensor-core tile reads TMA-staged operands");
+  const int BN = c.bn, S = c.stages, PAIR = c.split > 1 ? c.split : 1;
+  if (c.staging != ISPC_STAGE_TMA && c.staging != ISPC_STAGE_SHARED)
+    illegal("the tensor-core tile stages A by TMA or through registers, B by TMA");
   if (c.engine != ISPC_ENGINE_TF32 && c.engine != ISPC_ENGINE_TF32X3) illegal("tcgen05 kernel needs a tensor engine");
-  const bool X3 = c.engine == ISPC_ENGINE_TF32X3;
+  const bool X3 = c.engine == ISPC_ENGINE_TF32X3, A_TMA = c.staging == ISPC_STAGE_TMA;
   const int T = 256;
   if (!(BN == 64 || BN == 128 || BN == 256)) illegal("UMMA N must be 64, 128 or 256");
+  if (PAIR != 1 && PAIR != 2) illegal("tcgen05 pairs at most two CTAs (cta_group::2)");
   if (S < 2 || S > 8) illegal("TMA ring depth must be 2..8");
-  if (M % 128 || N % BN || K % 32) illegal("shape not divisible by the 128 x BN x 32 tile");
-  if (M > (int64_t(1) << 31) || K > (int64_t(1) << 31)) illegal("shape too large for the tensor maps");
-  // TMA ring stage: [A as landed, m contiguous][B, k contiguous]([B small])
-  // transposed-A ring, 2 slots: [A k contiguous]([A small]); 1 KiB aligned parts
-  const int64_t a_bytes = 128 * 32 * 4, b_bytes = int64_t(BN) * 32 * 4, tma_bytes = a_bytes + b_bytes;
-  const int64_t off_b = a_bytes, off_bs = a_bytes + b_bytes;
-  const int64_t stage = tma_bytes + (X3 ? b_bytes : 0);
-  const int64_t slot = a_bytes * (X3 ? 2 : 1);
-  const int64_t ak_off = S * stage, bar_off = ak_off + 2 * slot;
-  const int nbar = 2 * S + 4 + 1;  // full[S], empty[S], conv[2], akfree[2], acc
+  const int UM = 128 * PAIR, BNL = BN / PAIR;  // MMA M; B rows each CTA of the pair lands
+  if (M % UM || N % BN || K % 32) illegal("shape not divisible by the UMMA_M x BN x 32 tile");
+  if (M > (int64_t(1) << 31) || K > (int64_t(1) << 31) || N > (int64_t(1) << 31))
+    illegal("shape too large for the tensor maps");
+  // ring stage (1 KiB aligned parts): ([A as landed, m contiguous]) [B half,
+  // k contiguous] [A k contiguous, written by the converters] ([B small] [A small])
+  const int64_t a_bytes = 128 * 32 * 4, b_bytes = int64_t(BNL) * 32 * 4;
+  const int64_t off_b = A_TMA ? a_bytes : 0, off_ak = off_b + b_bytes, off_bs = off_ak + a_bytes;
+  const int64_t off_as = off_bs + b_bytes;
+  const int64_t tma_bytes = off_b + b_bytes;
+  const int64_t stage = off_ak + a_bytes + (X3 ? b_bytes + a_bytes : 0);
+  const int64_t bar_off = S * stage;
+  const int nbar = 3 * S + 1;  // full[S], empty[S], conv[S], acc
   const int64_t smem = bar_off + (nbar + 1) * 8 + 1024;  // + slack to 1 KiB-align the base
   if (smem > 232448) illegal("TMA ring exceeds 227 KiB of shared memory");
-  // kind::tf32, fp32 accumulate, A and B K-major, N = BN, M = 128
-  const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(128 >> 4) << 24);
-  const int64_t KB = K / 32, MB = M / 128;
-  const unsigned FULL = 0, EMPTY = 8u * S, CONV = 16u * S, AKFREE = 16u * S + 16, ACC = 16u * S + 32;
+  // kind::tf32, fp32 accumulate, A and B K-major, N = BN, M = 128 per CTA
+  const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(UM >> 4) << 24);
+  const int64_t KB = K / 32, MB = M / UM;
+  const unsigned FULL = 0, EMPTY = 8u * S, CONV = 16u * S, ACC = 24u * S;
+  const char* cg = PAIR == 2 ? "2" : "1";
 
   std::ostringstream o;
   o << tcgen05_prelude();
   o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", 1) " << fn
-    << "(const __grid_constant__ ispc_tmap_t tm_a, const __grid_constant__ ispc_tmap_t tm_b, float* __restrict__ g_c) {\n";
+    << "(const __grid_constant__ ispc_tmap_t tm_a, const __grid_constant__ ispc_tmap_t tm_b, "
+       "const float* __restrict__ g_a, float* __restrict__ g_c) {\n";
   o << "  extern __shared__ __align__(1024) unsigned char ispc_smem_raw[];\n";
   o << "  const unsigned raw = ispc_smem_addr(ispc_smem_raw);\n";
   o << "  const unsigned base = (raw + 1023u) & ~1023u;\n";
-  o << "  const unsigned bars = base + " << bar_off << "u;  // full[S], empty[S], conv[2], akfree[2], acc, tmem slot\n";
-  o << "  const unsigned ak = base + " << ak_off << "u;     // transposed-A slots\n";
+  o << "  const unsigned bars = base + " << bar_off << "u;  // full[S], empty[S], conv[S], acc, tmem slot\n";
   o << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
-  o << "  const int m_blk = blockIdx.x % " << MB << ", n_blk = blockIdx.x / " << MB << ";\n";
+  if (PAIR == 2) {
+    o << "  unsigned rank;\n";
+    o << "  asm volatile(\"mov.u32 %0, %%cluster_ctarank;\" : \"=r\"(rank));\n";
+    o << "  const int pair = blockIdx.x >> 1;\n";
+  } else {
+    o << "  const unsigned rank = 0;\n";
+    o << "  const int pair = blockIdx.x;\n";
+  }
+  o << "  const int m_blk = pair % " << MB << ", n_blk = pair / " << MB << ";\n";
+  o << "  const int m_base = m_blk * " << UM << " + rank * 128;\n";
   o << "  unsigned char* gen = ispc_smem_raw + (base - raw);\n";
   o << "  unsigned* tmem_slot = (unsigned*)(gen + " << bar_off + nbar * 8 << ");\n";
   o << "  if (threadIdx.x == 0) {\n";
   o << "    for (int s = 0; s < " << nbar << "; ++s)\n";
-  o << "      ispc_mbar_init(bars + 8u * s, (s >= " << 2 * S << " && s < " << 2 * S + 2 << ") ? 128u : 1u);\n";
+  o << "      ispc_mbar_init(bars + 8u * s, (s >= " << 2 * S << " && s < " << 3 * S << ") ? " << PAIR << "u : 1u);\n";
   o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
-  o << "    asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&tm_a) : \"memory\");\n";
+  if (A_TMA) o << "    asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&tm_a) : \"memory\");\n";
   o << "    asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&tm_b) : \"memory\");\n";
   o << "  }\n";
   o << "  if (warp == 1) {\n";
-  o << "    asm volatile(\"tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], " << BN
+  o << "    asm volatile(\"tcgen05.alloc.cta_group::" << cg << ".sync.aligned.shared::cta.b32 [%0], " << BN
     << ";\" ::\"r\"(ispc_smem_addr(tmem_slot)) : \"memory\");\n";
-  o << "    asm volatile(\"tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\" ::: \"memory\");\n";
+  o << "    asm volatile(\"tcgen05.relinquish_alloc_permit.cta_group::" << cg << ".sync.aligned;\" ::: \"memory\");\n";
   o << "  }\n";
   o << "  asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n";
-  o << "  __syncthreads();\n";
+  if (PAIR == 2) {  // barriers of both CTAs initialised before any remote arrive / multicast commit
+    o << "  asm volatile(\"barrier.cluster.arrive.release.aligned;\\n barrier.cluster.wait.acquire.aligned;\" ::: "
+         "\"memory\");\n";
+  } else {
+    o << "  __syncthreads();\n";
+  }
   o << "  asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
   o << "  const unsigned tmem = *(volatile unsigned*)tmem_slot;\n";
-  // producer: TMA ring of S stages
+  // producer: TMA ring of S stages (this CTA's own A rows and B half)
   o << "  if (warp == 0 && lane == 0) {\n";
   o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
   o << "      const int s = kb % " << S << ";\n";
@@ -161,66 +206,82 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   o << "      const unsigned full = bars + " << FULL << "u + 8u * s;\n";
   o << "      const unsigned sa = base + s * " << stage << "u;\n";
   o << "      ispc_mbar_expect_tx(full, " << tma_bytes << "u);\n";
-  o << "      #pragma unroll\n";
-  o << "      for (int i = 0; i < 4; ++i) ispc_tma_2d(sa + i * 4096u, &tm_a, m_blk * 128 + i * 32, kb * 32, full);\n";
-  o << "      ispc_tma_2d(sa + " << off_b << "u, &tm_b, kb * 32, n_blk * " << BN << ", full);\n";
+  if (A_TMA) {
+    o << "      #pragma unroll\n";
+    o << "      for (int i = 0; i < 4; ++i) ispc_tma_2d(sa + i * 4096u, &tm_a, m_base + i * 32, kb * 32, full);\n";
+  }
+  o << "      ispc_tma_2d(sa + " << off_b << "u, &tm_b, kb * 32, n_blk * " << BN << " + rank * " << BNL
+    << ", full);\n";
   o << "    }\n";
-  o << "  } else if (warp == 1 && lane == 0) {\n";
-  // MMA issuer: A (transposed slot) and B (TMA stage), both K-major 128-B swizzle
+  o << "  } else if (warp == 1 && lane == 0 && rank == 0) {\n";
+  // MMA issuer (the pair's leader): A (transposed slot) and B (TMA stage),
+  // both K-major 128-B swizzle; with cta_group::2 the same smem offsets in
+  // the peer CTA supply rows 128..255 of A and the second half of B
   o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
-  o << "      const int s = kb % " << S << ", a2 = kb & 1;\n";
-  o << "      ispc_mbar_wait(bars + " << CONV << "u + 8u * a2, (kb >> 1) & 1);\n";
+  o << "      const int s = kb % " << S << ";\n";
+  o << "      ispc_mbar_wait(bars + " << CONV << "u + 8u * s, (kb / " << S << ") & 1);\n";
   o << "      asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
   o << "      const unsigned sb = base + s * " << stage << "u + " << off_b << "u;\n";
-  o << "      const unsigned sk = ak + a2 * " << slot << "u;\n";
+  o << "      const unsigned sk = base + s * " << stage << "u + " << off_ak << "u;\n";
+  const char* mma = PAIR == 2 ? "ispc_mma_tf32_pair" : "ispc_mma_tf32";
+  const char* commit = PAIR == 2 ? "ispc_mma_commit_pair" : "ispc_mma_commit";
   o << "      #pragma unroll\n";
   o << "      for (int kk = 0; kk < 4; ++kk) {\n";
   o << "        const unsigned long long da = ispc_umma_desc(sk + kk * 32u, 16u, 1024u);\n";
   o << "        const unsigned long long db = ispc_umma_desc(sb + kk * 32u, 16u, 1024u);\n";
   if (X3) {
-    o << "        const unsigned long long das = ispc_umma_desc(sk + " << a_bytes << "u + kk * 32u, 16u, 1024u);\n";
-    o << "        const unsigned long long dbs = ispc_umma_desc(sb + " << b_bytes << "u + kk * 32u, 16u, 1024u);\n";
-    o << "        ispc_mma_tf32(tmem, das, db, " << idesc << "u, (kb | kk) != 0);\n";
-    o << "        ispc_mma_tf32(tmem, da, dbs, " << idesc << "u, 1u);\n";
-    o << "        ispc_mma_tf32(tmem, da, db, " << idesc << "u, 1u);\n";
+    o << "        const unsigned long long das = ispc_umma_desc(sk + " << off_as - off_ak << "u + kk * 32u, 16u, 1024u);\n";
+    o << "        const unsigned long long dbs = ispc_umma_desc(sb + " << off_bs - off_b << "u + kk * 32u, 16u, 1024u);\n";
+    o << "        " << mma << "(tmem, das, db, " << idesc << "u, (kb | kk) != 0);\n";
+    o << "        " << mma << "(tmem, da, dbs, " << idesc << "u, 1u);\n";
+    o << "        " << mma << "(tmem, da, db, " << idesc << "u, 1u);\n";
   } else {
-    o << "        ispc_mma_tf32(tmem, da, db, " << idesc << "u, (kb | kk) != 0);\n";
+    o << "        " << mma << "(tmem, da, db, " << idesc << "u, (kb | kk) != 0);\n";
   }
   o << "      }\n";
-  o << "      ispc_mma_commit(bars + " << EMPTY << "u + 8u * s);   // TMA stage free\n";
-  o << "      ispc_mma_commit(bars + " << AKFREE << "u + 8u * a2);  // transposed slot free\n";
+  o << "      " << commit << "(bars + " << EMPTY << "u + 8u * s);   // stage free (both CTAs of a pair)\n";
   o << "    }\n";
-  o << "    ispc_mma_commit(bars + " << ACC << "u);\n";
+  o << "    " << commit << "(bars + " << ACC << "u);\n";
   o << "  } else if (warp >= 4) {\n";
   // converters: the tf32 tensor path reads K-major operands only (MN-major
-  // descriptors read zeros on sm_100a, tools/tc_probe.cu), so every landed A
-  // tile is transposed into a 2-slot K-major ring, row m = thread
+  // descriptors read zeros on sm_100a, tools/tc_probe.cu), so every A tile
+  // is rewritten K-major into its ring stage, row m = thread; staging TMA
+  // transposes the landed swizzled box, staging SHARED loads A straight from
+  // global memory (coalesced along m, one k block ahead in registers)
   o << "    const int m = threadIdx.x - 128;\n";
+  if (!A_TMA) {
+    o << "    const float* pa = g_a + m_base + m;\n";
+    o << "    float v[32];\n";
+    o << "    #pragma unroll\n";
+    o << "    for (int k = 0; k < 32; ++k) v[k] = __ldg(pa + (long long)k * " << M << "LL);\n";
+  }
   o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
-  o << "      const int s = kb % " << S << ", a2 = kb & 1;\n";
+  o << "      const int s = kb % " << S << ";\n";
   o << "      ispc_mbar_wait(bars + " << FULL << "u + 8u * s, (kb / " << S << ") & 1);\n";
-  o << "      if (kb >= 2) ispc_mbar_wait(bars + " << AKFREE << "u + 8u * a2, ((kb >> 1) + 1) & 1);\n";
   o << "      unsigned char* st = gen + s * " << stage << ";\n";
-  o << "      unsigned char* sk = gen + " << ak_off << " + a2 * " << slot << ";\n";
-  o << "      const unsigned src_row = (m >> 5) * 4096u + (m & 3) * 4u;\n";
+  o << "      unsigned char* sk = st + " << off_ak << ";\n";
+  if (A_TMA) o << "      const unsigned src_row = (m >> 5) * 4096u + (m & 3) * 4u;\n";
   o << "      const unsigned dst_row = (m >> 3) * 1024u + (m & 7) * 128u;\n";
   o << "      #pragma unroll\n";
   o << "      for (int kq = 0; kq < 8; ++kq) {\n";
-  o << "        float v[4];\n";
+  o << "        float w[4];\n";
   o << "        #pragma unroll\n";
   o << "        for (int i = 0; i < 4; ++i) {\n";
   o << "          const int k = kq * 4 + i;\n";
-  o << "          v[i] = *(const float*)(st + src_row + (k >> 3) * 1024u + (k & 7) * 128u + ((((m & 31) >> 2) ^ (k & 7)) << 4));\n";
+  if (A_TMA)
+    o << "          w[i] = *(const float*)(st + src_row + (k >> 3) * 1024u + (k & 7) * 128u + ((((m & 31) >> 2) ^ (k & 7)) << 4));\n";
+  else
+    o << "          w[i] = v[k];\n";
   o << "        }\n";
   o << "        const unsigned dst = dst_row + ((kq ^ (m & 7)) << 4);\n";
   if (X3) {
     o << "        float4 hi, lo;\n";
-    o << "        hi.x = ispc_tf32_rna(v[0]); hi.y = ispc_tf32_rna(v[1]); hi.z = ispc_tf32_rna(v[2]); hi.w = ispc_tf32_rna(v[3]);\n";
-    o << "        lo.x = v[0] - hi.x; lo.y = v[1] - hi.y; lo.z = v[2] - hi.z; lo.w = v[3] - hi.w;\n";
+    o << "        hi.x = ispc_tf32_rna(w[0]); hi.y = ispc_tf32_rna(w[1]); hi.z = ispc_tf32_rna(w[2]); hi.w = ispc_tf32_rna(w[3]);\n";
+    o << "        lo.x = w[0] - hi.x; lo.y = w[1] - hi.y; lo.z = w[2] - hi.z; lo.w = w[3] - hi.w;\n";
     o << "        *(float4*)(sk + dst) = hi;\n";
-    o << "        *(float4*)(sk + " << a_bytes << " + dst) = lo;\n";
+    o << "        *(float4*)(sk + " << off_as - off_ak << " + dst) = lo;\n";
   } else {
-    o << "        *(float4*)(sk + dst) = make_float4(v[0], v[1], v[2], v[3]);\n";
+    o << "        *(float4*)(sk + dst) = make_float4(w[0], w[1], w[2], w[3]);\n";
   }
   o << "      }\n";
   if (X3) {  // B split in place (big) + small part beside it in the TMA stage
@@ -235,8 +296,21 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
     o << "        *((float4*)(st + " << off_bs << ") + i) = lo;\n";
     o << "      }\n";
   }
+  // one arrive per CTA after the converter warps meet on named barrier 1
+  // (a release.cluster arrive per thread costs a cluster-scope membar each)
   o << "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
-  o << "      ispc_mbar_arrive(bars + " << CONV << "u + 8u * a2);\n";
+  o << "      asm volatile(\"bar.sync 1, 128;\" ::: \"memory\");\n";
+  if (PAIR == 2)  // the leader's conv barrier counts both CTAs
+    o << "      if (m == 0) ispc_mbar_arrive_rank(bars + " << CONV << "u + 8u * s, 0u);\n";
+  else
+    o << "      if (m == 0) ispc_mbar_arrive(bars + " << CONV << "u + 8u * s);\n";
+  if (!A_TMA) {  // next k block's A, issued after the arrive so its release does not wait on the loads
+    o << "      if (kb + 1 < " << KB << ") {\n";
+    o << "        const float* pn = pa + (long long)(kb + 1) * 32 * " << M << "LL;\n";
+    o << "        #pragma unroll\n";
+    o << "        for (int k = 0; k < 32; ++k) v[k] = __ldg(pn + (long long)k * " << M << "LL);\n";
+    o << "      }\n";
+  }
   o << "    }\n";
   o << "  }\n";
   o << "  __syncwarp();\n";
@@ -245,7 +319,7 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   o << "  ispc_mbar_wait(bars + " << ACC << "u, 0);\n";
   o << "  asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
   o << "  const int lg = warp & 3, c_begin = (warp >> 2) * " << cols << ";\n";
-  o << "  const long long row = (long long)m_blk * 128 + lg * 32 + lane;\n";
+  o << "  const long long row = (long long)m_base + lg * 32 + lane;\n";
   o << "  float* pc = g_c + row + (long long)n_blk * " << BN << " * " << M << "LL;\n";
   o << "  #pragma unroll 1\n";
   o << "  for (int c0 = c_begin; c0 < c_begin + " << cols << "; c0 += 32) {\n";
@@ -256,25 +330,39 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   o << "    for (int j = 0; j < 32; ++j) pc[(long long)(c0 + j) * " << M << "LL] = __uint_as_float(r[j]);\n";
   o << "  }\n";
   o << "  asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n";
-  o << "  __syncthreads();\n";
+  if (PAIR == 2)  // neither CTA frees TMEM or exits while its peer may still touch it
+    o << "  asm volatile(\"barrier.cluster.arrive.release.aligned;\\n barrier.cluster.wait.acquire.aligned;\" ::: "
+         "\"memory\");\n";
+  else
+    o << "  __syncthreads();\n";
   o << "  if (warp == 1) {\n";
-  o << "    asm volatile(\"tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, " << BN << ";\" ::\"r\"(tmem) : \"memory\");\n";
+  o << "    asm volatile(\"tcgen05.dealloc.cta_group::" << cg << ".sync.aligned.b32 %0, " << BN
+    << ";\" ::\"r\"(tmem) : \"memory\");\n";
   o << "  }\n";
   o << "}\n";
 
-  L.grid_x = uint64_t(MB * (N / BN));
+  L.grid_x = uint64_t(MB * (N / BN) * PAIR);
   L.block[0] = uint32_t(T);
   L.block[1] = L.block[2] = 1;
   L.static_smem = uint32_t(smem);
-  // parameters: tensor maps over a and b, region c
-  L.num_params = 3;
+  if (PAIR == 2) {
+    L.cluster[0] = 2;
+    L.cluster[1] = L.cluster[2] = 1;
+  }
+  // parameters: tensor maps over a and b, region a (register-staged A), region c
+  L.num_params = 4;
   for (int i = 0; i < 2; ++i) {
     ispc_param& P = L.params[i];
     P.kind = ISPC_PARAM_TMAP;
     P.is_input = 1;
     std::snprintf(P.name, sizeof(P.name), "%s", i == 0 ? "a" : "b");
   }
-  ispc_param& Pc = L.params[2];
+  ispc_param& Pa = L.params[2];
+  Pa.kind = ISPC_PARAM_REGION;
+  Pa.is_input = 1;
+  Pa.elems = M * K;
+  std::snprintf(Pa.name, sizeof(Pa.name), "a");
+  ispc_param& Pc = L.params[3];
   Pc.kind = ISPC_PARAM_REGION;
   Pc.is_input = 1;
   Pc.elems = M * N;
@@ -295,7 +383,7 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   std::snprintf(tb.region, sizeof(tb.region), "b");
   tb.dims[0] = uint64_t(K), tb.dims[1] = uint64_t(N);
   tb.strides[0] = uint64_t(K) * 4;
-  tb.box[0] = 32, tb.box[1] = uint32_t(BN);
+  tb.box[0] = 32, tb.box[1] = uint32_t(BNL);
   L.reg_elems = 32;
   return o.str();
 }

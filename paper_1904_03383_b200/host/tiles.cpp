@@ -134,11 +134,16 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     if (m <= 0 || n <= 0 || k <= 0) throw std::invalid_argument("sgemm_tc needs m, n, k > 0");
     f.kind = ISPC_TILE_SGEMM_TC;
     f.x3_only = kind == "sgemm_tc_x3";
-    TileParam bn = P("bn", dividing({64, 128, 256}, n)), st = P("stages", {2, 3, 4, 5, 6});
-    f.params = {bn, st};
+    // split = CTAs sharing one UMMA (cta_group::2 pairs two SMs on M = 256)
+    TileParam bn = P("bn", dividing({64, 128, 256}, n)), st = P("stages", {2, 3, 4, 5, 6, 8});
+    TileParam pair = P("split", m % 256 == 0 ? std::vector<std::int64_t>{1, 2} : std::vector<std::int64_t>{1});
+    pair.cluster = true;
+    f.params = {bn, st, pair};
     f.min_threads = 1;
     f.max_acc = 1;
-    pre("staging", {"TMA"});
+    f.max_cluster = 2;
+    // A by TMA (transposed in shared memory) or through registers; B by TMA
+    pre("staging", {"TMA", "SHARED"});
     if (f.x3_only) pre("engine", {"TF32X3"});
     else pre("engine", {"TF32", "TF32X3"});
     pre("xreduce", {"SHUFFLE"});

@@ -186,6 +186,32 @@ def test_tcgen05_sgemm(dev, engine):
     assert ok >= 1
 
 
+@pytest.mark.parametrize("engine", ["TF32", "TF32X3"])
+@pytest.mark.parametrize("staging", ["TMA", "SHARED"])
+@pytest.mark.parametrize("pair", ["1", "2"])
+def test_tcgen05_staging_and_pairs(dev, engine, staging, pair):
+    """A staged by TMA or through registers; one CTA per UMMA or a
+    cta_group::2 pair (M = 256 over two SMs, B split between them)."""
+    space = Space("sgemm_tc", m=512, n=768, k=192)
+    dev.bind(space.problem())
+    ok = 0
+    for bn in ("64", "128", "256"):
+        c = space.root()
+        try:
+            c.decide("engine", ["kernel"], engine).decide("staging", ["kernel"], staging)
+            c.decide("tile", ["split"], pair).decide("tile", ["bn"], bn).decide("tile", ["stages"], "3")
+        except (DeadEnd, ValueError):
+            continue
+        t = c.first_leaf().tiles()
+        m = dev.evaluate_tiles(t, reps=1, warmup=0)
+        if m.status == "illegal":
+            continue
+        assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
+        assert m.launch.cluster[0] == (2 if pair == "2" else 0)
+        ok += 1
+    assert ok >= 1
+
+
 @pytest.mark.parametrize("split", ["2", "4", "8"])
 def test_sgemm_split_k_cluster(dev, split):
     """Split-K over a cluster, partials summed through DSMEM (norm-wise 1e-5)."""

@@ -69,11 +69,18 @@ def test_sgemm_thread_and_register_counters():
         c.clone().decide("tile", ["thr_n"], "8")  # 2048 threads
 
 
-def test_tcgen05_space_is_tma_only():
+def test_tcgen05_space_stages_in_shared_memory():
     s = Space("sgemm_tc", m=512, n=512, k=512)
     for leaf in _leaves(s, 10):
         t = leaf.tiles()
-        assert N.STAGINGS[t.staging] == "TMA" and N.ENGINES[t.engine] in ("TF32", "TF32X3")
+        assert N.STAGINGS[t.staging] in ("TMA", "SHARED") and N.ENGINES[t.engine] in ("TF32", "TF32X3")
+        assert t.split in (1, 2)
+    # cta_group::2 pairs need M divisible by 256
+    s2 = Space("sgemm_tc", m=384, n=512, k=512)
+    assert all(leaf.tiles().split == 1 for leaf in _leaves(s2, 6))
+    c = s.root().decide("tile", ["split"], "2").first_leaf()
+    src, L = tile_cuda(c.tiles(), "k_pair")
+    assert "cta_group::2" in src and L.cluster[0] == 2 and L.grid_x == (512 // 256) * (512 // c.tiles().bn) * 2
 
 
 @pytest.mark.parametrize("kind,kw", [
