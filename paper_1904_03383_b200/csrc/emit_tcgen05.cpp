@@ -101,6 +101,29 @@ static __device__ __forceinline__ void ispc_mma_commit_pair(unsigned bar) {
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
       "h"((unsigned short)3) : "memory");
 }
+static __device__ __forceinline__ void ispc_mma_tf32_ts(unsigned tmem, unsigned ta, unsigned long long db,
+                                                        unsigned idesc, unsigned accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem), "r"(ta), "l"(db), "r"(idesc),
+      "r"(accumulate) : "memory");
+}
+static __device__ __forceinline__ void ispc_mma_tf32_ts_pair(unsigned tmem, unsigned ta, unsigned long long db,
+                                                             unsigned idesc, unsigned accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem), "r"(ta), "l"(db), "r"(idesc),
+      "r"(accumulate) : "memory");
+}
+#define ISPC_TMEM_ST32(taddr, v)                                                                              \
+  asm volatile(                                                                                              \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16," \
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"                                    \
+      ::"r"(taddr), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),   \
+        "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]),         \
+        "f"(v[16]), "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]),       \
+        "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])        \
+      : "memory")
 static __device__ __forceinline__ float ispc_tf32_rna(float x) {
   unsigned r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -138,18 +161,23 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   if (M % UM || N % BN || K % 32) illegal("shape not divisible by the UMMA_M x BN x 32 tile");
   if (M > (int64_t(1) << 31) || K > (int64_t(1) << 31) || N > (int64_t(1) << 31))
     illegal("shape too large for the tensor maps");
-  // ring stage (1 KiB aligned parts): ([A as landed, m contiguous]) [B half,
-  // k contiguous] [A k contiguous, written by the converters] ([B small] [A small])
+  // tensor memory: accumulator in columns [0, BN), then one A slot per ring
+  // stage (32 columns = 32 k of this CTA's 128 rows; 64 with A small)
+  const int a_cols = X3 ? 64 : 32;
+  const int need_cols = BN + S * a_cols;
+  if (need_cols > 512) illegal("accumulator + A slots exceed 512 TMEM columns");
+  int tcols = 32;
+  while (tcols < need_cols) tcols *= 2;
+  // smem ring stage (1 KiB aligned parts): ([A as landed, m contiguous]) [B rows, k contiguous] ([B small])
   const int64_t a_bytes = 128 * 32 * 4, b_bytes = int64_t(BNL) * 32 * 4;
-  const int64_t off_b = A_TMA ? a_bytes : 0, off_ak = off_b + b_bytes, off_bs = off_ak + a_bytes;
-  const int64_t off_as = off_bs + b_bytes;
+  const int64_t off_b = A_TMA ? a_bytes : 0, off_bs = off_b + b_bytes;
   const int64_t tma_bytes = off_b + b_bytes;
-  const int64_t stage = off_ak + a_bytes + (X3 ? b_bytes + a_bytes : 0);
+  const int64_t stage = tma_bytes + (X3 ? b_bytes : 0);
   const int64_t bar_off = S * stage;
   const int nbar = 3 * S + 1;  // full[S], empty[S], conv[S], acc
   const int64_t smem = bar_off + (nbar + 1) * 8 + 1024;  // + slack to 1 KiB-align the base
   if (smem > 232448) illegal("TMA ring exceeds 227 KiB of shared memory");
-  // kind::tf32, fp32 accumulate, A and B K-major, N = BN, M = 128 per CTA
+  // kind::tf32, fp32 accumulate, K-major operands, N = BN, M = UMMA_M
   const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(UM >> 4) << 24);
   const int64_t KB = K / 32, MB = M / UM;
   const unsigned FULL = 0, EMPTY = 8u * S, CONV = 16u * S, ACC = 24u * S;
@@ -185,7 +213,7 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   o << "    asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&tm_b) : \"memory\");\n";
   o << "  }\n";
   o << "  if (warp == 1) {\n";
-  o << "    asm volatile(\"tcgen05.alloc.cta_group::" << cg << ".sync.aligned.shared::cta.b32 [%0], " << BN
+  o << "    asm volatile(\"tcgen05.alloc.cta_group::" << cg << ".sync.aligned.shared::cta.b32 [%0], " << tcols
     << ";\" ::\"r\"(ispc_smem_addr(tmem_slot)) : \"memory\");\n";
   o << "    asm volatile(\"tcgen05.relinquish_alloc_permit.cta_group::" << cg << ".sync.aligned;\" ::: \"memory\");\n";
   o << "  }\n";
@@ -198,7 +226,7 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   }
   o << "  asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
   o << "  const unsigned tmem = *(volatile unsigned*)tmem_slot;\n";
-  // producer: TMA ring of S stages (this CTA's own A rows and B half)
+  // producer: TMA ring of S stages (this CTA's own A rows and B rows)
   o << "  if (warp == 0 && lane == 0) {\n";
   o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
   o << "      const int s = kb % " << S << ";\n";
@@ -214,44 +242,42 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
     << ", full);\n";
   o << "    }\n";
   o << "  } else if (warp == 1 && lane == 0 && rank == 0) {\n";
-  // MMA issuer (the pair's leader): A (transposed slot) and B (TMA stage),
-  // both K-major 128-B swizzle; with cta_group::2 the same smem offsets in
-  // the peer CTA supply rows 128..255 of A and the second half of B
+  // MMA issuer (the pair's leader): A from tensor memory (slot s), B from the
+  // smem stage (K-major, 128-B swizzle); with cta_group::2 the same TMEM and
+  // smem addresses in the peer CTA supply rows 128..255 and the second half of B
+  const char* mma = PAIR == 2 ? "ispc_mma_tf32_ts_pair" : "ispc_mma_tf32_ts";
+  const char* commit = PAIR == 2 ? "ispc_mma_commit_pair" : "ispc_mma_commit";
   o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
   o << "      const int s = kb % " << S << ";\n";
   o << "      ispc_mbar_wait(bars + " << CONV << "u + 8u * s, (kb / " << S << ") & 1);\n";
   o << "      asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
   o << "      const unsigned sb = base + s * " << stage << "u + " << off_b << "u;\n";
-  o << "      const unsigned sk = base + s * " << stage << "u + " << off_ak << "u;\n";
-  const char* mma = PAIR == 2 ? "ispc_mma_tf32_pair" : "ispc_mma_tf32";
-  const char* commit = PAIR == 2 ? "ispc_mma_commit_pair" : "ispc_mma_commit";
+  o << "      const unsigned ta = tmem + " << BN << "u + s * " << a_cols << "u;\n";
   o << "      #pragma unroll\n";
   o << "      for (int kk = 0; kk < 4; ++kk) {\n";
-  o << "        const unsigned long long da = ispc_umma_desc(sk + kk * 32u, 16u, 1024u);\n";
   o << "        const unsigned long long db = ispc_umma_desc(sb + kk * 32u, 16u, 1024u);\n";
   if (X3) {
-    o << "        const unsigned long long das = ispc_umma_desc(sk + " << off_as - off_ak << "u + kk * 32u, 16u, 1024u);\n";
     o << "        const unsigned long long dbs = ispc_umma_desc(sb + " << off_bs - off_b << "u + kk * 32u, 16u, 1024u);\n";
-    o << "        " << mma << "(tmem, das, db, " << idesc << "u, (kb | kk) != 0);\n";
-    o << "        " << mma << "(tmem, da, dbs, " << idesc << "u, 1u);\n";
-    o << "        " << mma << "(tmem, da, db, " << idesc << "u, 1u);\n";
+    o << "        " << mma << "(tmem, ta + 32u + kk * 8u, db, " << idesc << "u, (kb | kk) != 0);\n";
+    o << "        " << mma << "(tmem, ta + kk * 8u, dbs, " << idesc << "u, 1u);\n";
+    o << "        " << mma << "(tmem, ta + kk * 8u, db, " << idesc << "u, 1u);\n";
   } else {
-    o << "        " << mma << "(tmem, da, db, " << idesc << "u, (kb | kk) != 0);\n";
+    o << "        " << mma << "(tmem, ta + kk * 8u, db, " << idesc << "u, (kb | kk) != 0);\n";
   }
   o << "      }\n";
-  o << "      " << commit << "(bars + " << EMPTY << "u + 8u * s);   // stage free (both CTAs of a pair)\n";
+  o << "      " << commit << "(bars + " << EMPTY << "u + 8u * s);   // stage + A slot free (both CTAs of a pair)\n";
   o << "    }\n";
   o << "    " << commit << "(bars + " << ACC << "u);\n";
   o << "  } else if (warp >= 4) {\n";
-  // converters: the tf32 tensor path reads K-major operands only (MN-major
-  // descriptors read zeros on sm_100a, tools/tc_probe.cu), so every A tile
-  // is rewritten K-major into its ring stage, row m = thread; staging TMA
-  // transposes the landed swizzled box, staging SHARED loads A straight from
-  // global memory (coalesced along m, one k block ahead in registers)
+  // converters, row m = thread = TMEM lane: A is m-contiguous, so each thread
+  // holds its row's 32 k values of a k block in registers (a transposed read
+  // of the landed TMA box, or straight from global memory one k block ahead)
+  // and tcgen05.st's them into the stage's A slot (TF32X3: big and small)
   o << "    const int m = threadIdx.x - 128;\n";
+  o << "    const unsigned trow = (unsigned)((warp & 3) * 32) << 16;\n";
+  o << "    float v[32];\n";
   if (!A_TMA) {
     o << "    const float* pa = g_a + m_base + m;\n";
-    o << "    float v[32];\n";
     o << "    #pragma unroll\n";
     o << "    for (int k = 0; k < 32; ++k) v[k] = __ldg(pa + (long long)k * " << M << "LL);\n";
   }
@@ -259,46 +285,37 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   o << "      const int s = kb % " << S << ";\n";
   o << "      ispc_mbar_wait(bars + " << FULL << "u + 8u * s, (kb / " << S << ") & 1);\n";
   o << "      unsigned char* st = gen + s * " << stage << ";\n";
-  o << "      unsigned char* sk = st + " << off_ak << ";\n";
-  if (A_TMA) o << "      const unsigned src_row = (m >> 5) * 4096u + (m & 3) * 4u;\n";
-  o << "      const unsigned dst_row = (m >> 3) * 1024u + (m & 7) * 128u;\n";
-  o << "      #pragma unroll\n";
-  o << "      for (int kq = 0; kq < 8; ++kq) {\n";
-  o << "        float w[4];\n";
-  o << "        #pragma unroll\n";
-  o << "        for (int i = 0; i < 4; ++i) {\n";
-  o << "          const int k = kq * 4 + i;\n";
-  if (A_TMA)
-    o << "          w[i] = *(const float*)(st + src_row + (k >> 3) * 1024u + (k & 7) * 128u + ((((m & 31) >> 2) ^ (k & 7)) << 4));\n";
-  else
-    o << "          w[i] = v[k];\n";
-  o << "        }\n";
-  o << "        const unsigned dst = dst_row + ((kq ^ (m & 7)) << 4);\n";
-  if (X3) {
-    o << "        float4 hi, lo;\n";
-    o << "        hi.x = ispc_tf32_rna(w[0]); hi.y = ispc_tf32_rna(w[1]); hi.z = ispc_tf32_rna(w[2]); hi.w = ispc_tf32_rna(w[3]);\n";
-    o << "        lo.x = w[0] - hi.x; lo.y = w[1] - hi.y; lo.z = w[2] - hi.z; lo.w = w[3] - hi.w;\n";
-    o << "        *(float4*)(sk + dst) = hi;\n";
-    o << "        *(float4*)(sk + " << off_as - off_ak << " + dst) = lo;\n";
-  } else {
-    o << "        *(float4*)(sk + dst) = make_float4(w[0], w[1], w[2], w[3]);\n";
+  if (A_TMA) {
+    o << "      const unsigned src_row = (m >> 5) * 4096u + (m & 3) * 4u;\n";
+    o << "      #pragma unroll\n";
+    o << "      for (int k = 0; k < 32; ++k)\n";
+    o << "        v[k] = *(const float*)(st + src_row + (k >> 3) * 1024u + (k & 7) * 128u + ((((m & 31) >> 2) ^ (k & 7)) << 4));\n";
   }
-  o << "      }\n";
-  if (X3) {  // B split in place (big) + small part beside it in the TMA stage
+  o << "      const unsigned ta = tmem + trow + " << BN << "u + s * " << a_cols << "u;\n";
+  if (X3) {
+    o << "      float lo[32];\n";
+    o << "      #pragma unroll\n";
+    o << "      for (int k = 0; k < 32; ++k) { const float h = ispc_tf32_rna(v[k]); lo[k] = v[k] - h; v[k] = h; }\n";
+    o << "      ISPC_TMEM_ST32(ta, v);\n";
+    o << "      ISPC_TMEM_ST32(ta + 32u, lo);\n";
+    // B split in place (big) + small part beside it in the TMA stage
     o << "      #pragma unroll 4\n";
     o << "      for (int i = m; i < " << b_bytes / 16 << "; i += 128) {\n";
     o << "        float4* pb = (float4*)(st + " << off_b << ") + i;\n";
     o << "        const float4 x = *pb;\n";
-    o << "        float4 hi, lo;\n";
+    o << "        float4 hi, l4;\n";
     o << "        hi.x = ispc_tf32_rna(x.x); hi.y = ispc_tf32_rna(x.y); hi.z = ispc_tf32_rna(x.z); hi.w = ispc_tf32_rna(x.w);\n";
-    o << "        lo.x = x.x - hi.x; lo.y = x.y - hi.y; lo.z = x.z - hi.z; lo.w = x.w - hi.w;\n";
+    o << "        l4.x = x.x - hi.x; l4.y = x.y - hi.y; l4.z = x.z - hi.z; l4.w = x.w - hi.w;\n";
     o << "        *pb = hi;\n";
-    o << "        *((float4*)(st + " << off_bs << ") + i) = lo;\n";
+    o << "        *((float4*)(st + " << off_bs << ") + i) = l4;\n";
     o << "      }\n";
+    o << "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
+  } else {
+    o << "      ISPC_TMEM_ST32(ta, v);\n";
   }
+  o << "      asm volatile(\"tcgen05.wait::st.sync.aligned;\" ::: \"memory\");\n";
+  o << "      asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n";
   // one arrive per CTA after the converter warps meet on named barrier 1
-  // (a release.cluster arrive per thread costs a cluster-scope membar each)
-  o << "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
   o << "      asm volatile(\"bar.sync 1, 128;\" ::: \"memory\");\n";
   if (PAIR == 2)  // the leader's conv barrier counts both CTAs
     o << "      if (m == 0) ispc_mbar_arrive_rank(bars + " << CONV << "u + 8u * s, 0u);\n";
@@ -336,7 +353,7 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   else
     o << "  __syncthreads();\n";
   o << "  if (warp == 1) {\n";
-  o << "    asm volatile(\"tcgen05.dealloc.cta_group::" << cg << ".sync.aligned.b32 %0, " << BN
+  o << "    asm volatile(\"tcgen05.dealloc.cta_group::" << cg << ".sync.aligned.b32 %0, " << tcols
     << ";\" ::\"r\"(tmem) : \"memory\");\n";
   o << "  }\n";
   o << "}\n";
