@@ -326,11 +326,11 @@ class Device:
                           bit_exact=int(bit_exact), rtol=rtol, budget_ns=budget_ns, rotate=rotate)
 
     def launch(self, handle: int, launch: N.Launch, *, warmup=1, reps=3, flush_l2=False, check=True,
-               bit_exact=True, rtol=1e-5, budget_ns=2e9) -> Measurement:
+               bit_exact=True, rtol=1e-5, budget_ns=2e9, rotate=0) -> Measurement:
         r = N.TimeResult()
         rc = N.ispc().ispc_launch_timed(self._h, handle, C.byref(launch),
                                         C.byref(self._opts(warmup, reps, flush_l2, check, bit_exact, rtol,
-                                                           budget_ns)), C.byref(r))
+                                                           budget_ns, rotate)), C.byref(r))
         if rc != 0:
             return Measurement(N.STATUS.get(rc, str(rc)), float("inf"), float("inf"), float("inf"), 0.0, -1,
                                launch)

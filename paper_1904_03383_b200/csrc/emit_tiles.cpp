@@ -72,6 +72,153 @@ void add_region(ispc_launch& L, const char* name, int64_t elems) {
 // y[i] = sum_j A[i + j*m] x[j]. Lane (lm, ln) of warp (wm, wn) in cluster CTA
 // `rank` owns rows row0 .. row0+vec-1 and walks columns
 //   j = rank*n/split + (wn*lanes_n + ln) + t * warps_n*lanes_n,   t ascending.
+// Persistent TMA gemv (grid > 0): `grid` CTAs (grid / split clusters) walk
+// the row blocks rb = rb0, rb0 + clusters, ... of R rows; thread 0 streams the
+// CTA's {R rows x bk columns} boxes of every row block it owns through one
+// continuous ring (the TMA for the next row block is in flight while this
+// one is reduced), so the grid is sized to the 148 SMs instead of to the
+// matrix and no SM idles in a partial last wave.
+std::string gemv_tma_persistent(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
+  const int64_t m = c.m, n = c.n;
+  const int V = c.vec, LM = c.lanes_m, LN = c.lanes_n, WM = c.warps_m, WN = c.warps_n, S = c.split;
+  const int T = 32 * WM * WN;
+  const int64_t R = int64_t(V) * LM * WM, G = int64_t(WN) * LN, NRB = m / R;
+  const int64_t CB = c.bk, ST = c.stages, KT = n / S / CB, box_bytes = R * CB * 4;
+  if (c.grid % S) illegal("persistent grid is not a whole number of clusters");
+  const bool xr_shared = LN > 1 && c.xreduce == ISPC_XRED_SHARED;
+  const int64_t part_off = 0, cl_off = WN * R, xr_off = WN * R + R;
+  const int64_t ring_off = (xr_off + (xr_shared ? int64_t(T) * V : 0) + 31) / 32 * 32;
+  const int64_t smem = 4 * (ring_off + ST * R * CB) + 16 * ST;
+  if (smem > 232448) illegal("shared memory exceeds 227 KiB");
+  const std::string ty = V == 4 ? "float4" : V == 2 ? "float2" : "float";
+  std::ostringstream o;
+  o << tcgen05_prelude();
+  o << "extern \"C\" __global__ void __launch_bounds__(" << T << ") " << fn
+    << "(const float* __restrict__ g_a, const float* __restrict__ g_x, float* __restrict__ g_y, "
+       "const __grid_constant__ ispc_tmap_t tm_a) {\n";
+  o << "  extern __shared__ __align__(128) float ispc_smem[];\n";
+  o << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n";
+  o << "  const int lm = lane % " << LM << ", ln = lane / " << LM << ";\n";
+  o << "  const int wm = warp % " << WM << ", wn = warp / " << WM << ";\n";
+  o << "  const int rank = " << (S > 1 ? "(int)ispc_cluster_rank()" : "0") << ";\n";
+  o << "  const int cl = wn * " << LN << " + ln, rl = (wm * " << LM << " + lm) * " << V << ";\n";
+  o << "  const int col_c = rank * " << n / S << ";\n";
+  o << "  const float* px_cta = g_x + col_c;\n";
+  o << "  const int stride = gridDim.x / " << S << ", rb0 = blockIdx.x / " << S << ";\n";
+  o << "  const int my_it = rb0 < " << NRB << " ? (" << NRB - 1 << " - rb0) / stride + 1 : 0;\n";
+  o << "  const int total = my_it * " << KT << ";\n";
+  o << "  float* ring = ispc_smem + " << ring_off << ";\n";
+  o << "  const unsigned ring_s = ispc_smem_addr(ring);\n";
+  o << "  const unsigned bars = ring_s + " << ST * box_bytes << "u;  // full[ST], empty[ST]\n";
+  o << "  if (tid == 0) {\n";
+  o << "    for (int s = 0; s < " << ST << "; ++s) { ispc_mbar_init(bars + 8u * s, 1u); ispc_mbar_init(bars + 8u * ("
+    << ST << " + s), " << T / 32 << "u); }\n";
+  o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
+  o << "    asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&tm_a) : \"memory\");\n";
+  o << "    for (int g = 0; g < " << ST - 1 << " && g < total; ++g) {\n";
+  o << "      ispc_mbar_expect_tx(bars + 8u * g, " << box_bytes << "u);\n";
+  o << "      ispc_tma_2d(ring_s + g * " << box_bytes << "u, &tm_a, (rb0 + (g / " << KT << ") * stride) * " << R
+    << ", col_c + (g % " << KT << ") * " << CB << ", bars + 8u * g);\n";
+  o << "    }\n  }\n  __syncthreads();\n";
+  o << "  float acc[" << V << "];\n";
+  o << "  #pragma unroll 1\n  for (int g = 0; g < total; ++g) {\n";
+  o << "    const int kt = g % " << KT << ";\n";
+  o << "    if (kt == 0) {\n      #pragma unroll\n      for (int v = 0; v < " << V << "; ++v) acc[v] = 0.0f;\n    }\n";
+  o << "    if (tid == 0) {\n";
+  o << "      const int ng = g + " << ST - 1 << ";\n";
+  o << "      if (ng < total) {\n";
+  o << "        const int slot = ng % " << ST << ";\n";
+  o << "        if (g >= 1) ispc_mbar_wait(bars + 8u * (" << ST << " + slot), ((g - 1) / " << ST << ") & 1);\n";
+  o << "        ispc_mbar_expect_tx(bars + 8u * slot, " << box_bytes << "u);\n";
+  o << "        ispc_tma_2d(ring_s + slot * " << box_bytes << "u, &tm_a, (rb0 + (ng / " << KT << ") * stride) * " << R
+    << ", col_c + (ng % " << KT << ") * " << CB << ", bars + 8u * slot);\n";
+  o << "      }\n    }\n";
+  o << "    ispc_mbar_wait(bars + 8u * (g % " << ST << "), (g / " << ST << ") & 1);\n";
+  o << "    const float* st = ring + (g % " << ST << ") * " << R * CB << ";\n";
+  o << "    #pragma unroll\n    for (int t = 0; t < " << CB / G << "; ++t) {\n";
+  o << "      const int cc = cl + t * " << G << ";\n";
+  o << "      const float xv = __ldg(px_cta + kt * " << CB << " + cc);\n";
+  o << "      const " << ty << " av = *(const " << ty << "*)(st + cc * " << R << " + rl);\n";
+  if (V == 1) o << "      acc[0] = __fmaf_rn(av, xv, acc[0]);\n";
+  else
+    for (int v = 0; v < V; ++v) o << "      acc[" << v << "] = __fmaf_rn(av" << comp(v) << ", xv, acc[" << v << "]);\n";
+  o << "    }\n";
+  o << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
+  o << "    __syncwarp();\n";
+  o << "    if (lane == 0) ispc_mbar_arrive(bars + 8u * (" << ST << " + g % " << ST << "));  // one arrive per warp\n";
+  o << "    if (kt != " << KT - 1 << ") continue;\n";
+  o << "    const long long rblk = rb0 + (long long)(g / " << KT << ") * stride;\n";
+  // (1) lanes sharing rows, (2) warps sharing rows, (3) the cluster's CTAs
+  o << "    float r_acc[" << V << "];\n";
+  o << "    #pragma unroll\n    for (int v = 0; v < " << V << "; ++v) r_acc[v] = acc[v];\n";
+  if (LN > 1) {
+    if (c.xreduce == ISPC_XRED_SHUFFLE) {
+      o << "    #pragma unroll\n    for (int off = " << LM << "; off < 32; off <<= 1) {\n";
+      o << "      #pragma unroll\n      for (int v = 0; v < " << V
+        << "; ++v) r_acc[v] += __shfl_xor_sync(0xffffffffu, r_acc[v], off);\n";
+      o << "    }\n";
+    } else {
+      o << "    {\n      float* xr = ispc_smem + " << xr_off << ";\n";
+      o << "      #pragma unroll\n      for (int v = 0; v < " << V << "; ++v) xr[tid * " << V << " + v] = r_acc[v];\n";
+      o << "      __syncwarp();\n";
+      o << "      if (ln == 0) {\n";
+      o << "        for (int q = 1; q < " << LN << "; ++q)\n";
+      o << "          #pragma unroll\n          for (int v = 0; v < " << V << "; ++v) r_acc[v] += xr[(tid + q * " << LM
+        << ") * " << V << " + v];\n";
+      o << "      }\n      __syncwarp();\n    }\n";
+    }
+  }
+  o << "    float* part = ispc_smem + " << part_off << ";\n";
+  o << "    if (ln == 0) {\n";
+  o << "      #pragma unroll\n      for (int v = 0; v < " << V << "; ++v) part[wn * " << R << " + (wm * " << LM
+    << " + lm) * " << V << " + v] = r_acc[v];\n    }\n";
+  o << "    __syncthreads();\n";
+  o << "    float* csum = ispc_smem + " << cl_off << ";\n";
+  o << "    for (int r = tid; r < " << R << "; r += " << T << ") {\n";
+  o << "      float s = part[r];\n";
+  o << "      for (int w = 1; w < " << WN << "; ++w) s += part[w * " << R << " + r];\n";
+  if (S == 1) o << "      g_y[rblk * " << R << "LL + r] = s;\n";
+  else o << "      csum[r] = s;\n";
+  o << "    }\n";
+  if (S > 1) {
+    o << "    ispc_cluster_sync();\n";
+    o << "    for (int r = tid; r < " << R << "; r += " << T << ") {\n";
+    o << "      if (r % " << S << " != rank) continue;\n";
+    o << "      float s = 0.0f;\n";
+    o << "      #pragma unroll\n      for (int q = 0; q < " << S << "; ++q) s += ispc_dsmem_ld(csum + r, q);\n";
+    o << "      g_y[rblk * " << R << "LL + r] = s;\n";
+    o << "    }\n";
+    o << "    ispc_cluster_sync();\n";
+    L.cluster[0] = uint32_t(S);
+    L.cluster[1] = L.cluster[2] = 1;
+  } else {
+    o << "    __syncthreads();\n";
+  }
+  o << "  }\n}\n";
+  L.static_smem = uint32_t(smem);
+  L.grid_x = uint64_t(c.grid);
+  L.block[0] = uint32_t(T);
+  L.block[1] = L.block[2] = 1;
+  add_region(L, "a", m * n);
+  add_region(L, "x", n);
+  add_region(L, "y", m);
+  L.params[2].is_input = 1;
+  ispc_param& P = L.params[L.num_params++];
+  P.kind = ISPC_PARAM_TMAP;
+  P.is_input = 1;
+  std::snprintf(P.name, sizeof(P.name), "a");
+  ispc_tmap& tm = L.tmaps[L.num_tmaps++];
+  tm.param = 3;
+  tm.rank = 2;
+  tm.swizzle = 0;
+  std::snprintf(tm.region, sizeof(tm.region), "a");
+  tm.dims[0] = uint64_t(m), tm.dims[1] = uint64_t(n);
+  tm.strides[0] = uint64_t(m) * 4;
+  tm.box[0] = uint32_t(R), tm.box[1] = uint32_t(CB);
+  L.reg_elems = uint32_t(2 * V + 2);
+  return o.str();
+}
+
 std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
   const int64_t m = c.m, n = c.n;
   const int V = c.vec, LM = c.lanes_m, LN = c.lanes_n, WM = c.warps_m, WN = c.warps_n, S = c.split,
@@ -104,6 +251,12 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
     if (CB % G || (n / S) % CB) illegal("stage columns do not split across column lanes / the CTA slice");
     if (tma && (R > 256 || CB > 256)) illegal("TMA boxes hold at most 256 elements per dimension");
   }
+  const bool persist = c.grid > 0;
+  if (persist) {
+    if (tma) return gemv_tma_persistent(c, fn, L);
+    if (staged) illegal("the cp.async ring does not stream across row blocks (persistent grid)");
+    if (c.grid % S) illegal("persistent grid is not a whole number of clusters");
+  }
   // ring 128-byte aligned (TMA destination), then full[ST] / empty[ST] mbarriers
   const int64_t ring_off = (xr_off + (xr_shared ? int64_t(T) * V : 0) + 31) / 32 * 32;
   const int64_t smem = 4 * (staged ? ring_off + ST * R * CB : ring_off) + (tma ? 16 * ST : 0);
@@ -120,7 +273,11 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
   o << "  const int lm = lane % " << LM << ", ln = lane / " << LM << ";\n";
   o << "  const int wm = warp % " << WM << ", wn = warp / " << WM << ";\n";
   o << "  const int rank = " << (S > 1 ? "(int)ispc_cluster_rank()" : "0") << ";\n";
-  o << "  const long long rblk = blockIdx.x / " << S << ";\n";
+  if (persist)  // persistent: the cluster walks row blocks rblk, rblk + clusters, ...
+    o << "  for (long long rblk = blockIdx.x / " << S << "; rblk < " << m / R << "LL; rblk += gridDim.x / " << S
+      << ") {\n";
+  else
+    o << "  const long long rblk = blockIdx.x / " << S << ";\n";
   o << "  const long long row0 = rblk * " << R << "LL + (long long)(wm * " << LM << " + lm) * " << V << ";\n";
   o << "  const long long col0 = (long long)rank * " << n / S << "LL + wn * " << LN << " + ln;\n";
   o << "  const float* pa = g_a + row0 + col0 * " << m << "LL;\n";
@@ -246,7 +403,9 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
       for (int v = 0; v < V; ++v) o << (v ? ", " : "") << "acc[" << v << "]";
       o << ");\n";
     }
-    o << "  }\n}\n";
+    o << "  }\n";
+    if (persist) o << "  }\n";
+    o << "}\n";
   } else {
     // (2) warps sharing rows (wn), ascending wn
     o << "  float* part = ispc_smem + " << part_off << ";\n";
@@ -273,10 +432,13 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
       o << "  ispc_cluster_sync();\n";
       L.cluster[0] = uint32_t(S);
       L.cluster[1] = L.cluster[2] = 1;
+    } else if (persist) {
+      o << "  __syncthreads();  // partials reused by the next row block\n";
     }
+    if (persist) o << "  }\n";
     o << "}\n";
   }
-  L.grid_x = uint64_t(m / R * S);
+  L.grid_x = persist ? uint64_t(c.grid) : uint64_t(m / R * S);
   L.block[0] = uint32_t(T);
   L.block[1] = L.block[2] = 1;
   add_region(L, "a", m * n);

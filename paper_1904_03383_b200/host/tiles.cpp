@@ -85,13 +85,15 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     TileParam lm = P("lanes_m", pow2_upto(1, 32)), ln = P("lanes_n", dividing(pow2_upto(1, 32), n));
     TileParam wm = P("warps_m", pow2_upto(1, 8)), wn = P("warps_n", dividing(pow2_upto(1, 32), n));
     TileParam split = P("split", dividing({1, 2, 4, 8}, n)), unroll = P("unroll", dividing({1, 2, 4, 8, 16}, n));
-    TileParam bk = P("bk", {1, 8, 16, 32, 64, 128}), st = P("stages", {1, 2, 3, 4});
+    TileParam bk = P("bk", {1, 8, 16, 32, 64, 128, 256}), st = P("stages", {1, 2, 3, 4, 6, 8});
+    TileParam grid = P("grid", {0});  // persistent grids (148 x k) measured slower here: DESIGN.md 8
+    grid.persist = true;
     lm.thread = ln.thread = wm.thread = wn.thread = true;
     lm.warp = ln.warp = true;
     vec.acc = unroll.acc = true;
     split.cluster = true;
     bk.stage = st.stage = true;
-    f.params = {vec, lm, ln, wm, wn, split, unroll, bk, st};
+    f.params = {vec, lm, ln, wm, wn, split, unroll, bk, st, grid};
     f.min_threads = 32;
     f.warp_lanes = 32;
     f.max_acc = 64;
@@ -186,6 +188,7 @@ BuildResult build_tile_space(const TileFamily& f) {
     if (p.acc) bb.add_to_set("AccParams", o);
     if (p.cluster) bb.add_to_set("ClusterParams", o);
     if (p.stage) bb.add_to_set("StageParams", o);
+    if (p.persist) bb.add_to_set("PersistParams", o);
     (*values)[o] = p.values;
   }
   for (const auto& [outer, inner] : f.covers) {
@@ -194,7 +197,8 @@ BuildResult build_tile_space(const TileFamily& f) {
     bb.add_to_param_set("CoverOuter", c, bb.find(outer));
     bb.add_to_param_set("CoverInner", c, bb.find(inner));
   }
-  for (const char* s : {"ThreadParams", "WarpParams", "AccParams", "ClusterParams", "StageParams", "Covers"})
+  for (const char* s : {"ThreadParams", "WarpParams", "AccParams", "ClusterParams", "StageParams", "PersistParams",
+                        "Covers"})
     if (!bb.sets.count(s)) bb.sets[s] = {};
 
   Providers pv;
@@ -314,6 +318,7 @@ TileBoundReport tile_bound(const TileFamily& f, const SpaceContext& ctx, const C
       b.dram_bytes = 4 * (M * N + M + N);
       flops = 2 * M * N;
       b.ctas = M / (lo("vec") * lo("lanes_m") * lo("warps_m")) * hi("split");
+      if (lo("grid") > 0) b.ctas = std::min(b.ctas, hi("grid"));
       per_thread = N / (hi("split") * hi("warps_n") * hi("lanes_n")) * lo("vec");
       break;
     case ISPC_TILE_SGEMM:

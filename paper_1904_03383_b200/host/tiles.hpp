@@ -21,6 +21,7 @@ struct TileParam {
   std::string name;
   std::vector<std::int64_t> values;
   bool thread = false, warp = false, acc = false, cluster = false, stage = false;
+  bool persist = false;  // persistent grid size (0 = one CTA per tile)
 };
 
 struct TileFamily {

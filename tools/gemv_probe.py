@@ -21,6 +21,24 @@ CFGS = [
     dict(staging="TMA", cache="L2", vec=4, lanes_m=32, warps_m=1, warps_n=4, split=8, bk=128, stages=4),
     dict(staging="TMA", cache="L2", vec=4, lanes_m=32, warps_m=2, warps_n=4, split=8, bk=64, stages=3),
     dict(staging="CP_ASYNC", cache="L2", vec=4, lanes_m=32, warps_m=1, warps_n=8, split=8, bk=64, stages=4),
+    # the r16 search's best (DIRECT, 256 CTAs of 1024 threads, cluster split 8)
+    dict(staging="DIRECT", cache="L1", xreduce="SHARED", vec=4, lanes_m=16, warps_m=2, warps_n=16, split=8, unroll=2),
+    # persistent TMA rings: 37 clusters x 7 row blocks of 16 rows (grid sized to the SMs)
+    dict(staging="TMA", cache="L2", vec=4, lanes_m=4, warps_m=1, warps_n=8, split=4, bk=128, stages=8, grid=148),
+    dict(staging="TMA", cache="L2", vec=4, lanes_m=4, warps_m=1, warps_n=16, split=4, bk=128, stages=8, grid=148),
+    dict(staging="TMA", cache="L2", vec=4, lanes_m=4, warps_m=1, warps_n=8, split=8, bk=128, stages=4, grid=296),
+    dict(staging="TMA", cache="L2", vec=4, lanes_m=4, warps_m=1, warps_n=8, split=4, bk=256, stages=6, grid=148),
+    dict(staging="TMA", cache="L2", vec=4, lanes_m=4, warps_m=1, warps_n=4, split=4, bk=64, stages=8, grid=148),
+    dict(staging="TMA", cache="L2", vec=4, lanes_m=8, warps_m=1, warps_n=8, split=4, bk=128, stages=6, grid=148),
+    dict(staging="TMA", cache="L2", vec=4, lanes_m=4, warps_m=1, warps_n=8, split=4, bk=128, stages=4, grid=296),
+    # persistent direct loads: 37 clusters x 7 row blocks of 16 rows
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=4, warps_m=1, warps_n=16, split=8, unroll=4, grid=296),
+    dict(staging="DIRECT", cache="L1", vec=4, lanes_m=4, warps_m=1, warps_n=16, split=8, unroll=4, grid=296),
+    dict(staging="DIRECT", cache="STREAM", vec=4, lanes_m=4, warps_m=1, warps_n=16, split=8, unroll=4, grid=296),
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=4, warps_m=1, warps_n=32, split=4, unroll=4, grid=148),
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=4, warps_m=1, warps_n=8, split=8, unroll=8, grid=296),
+    dict(staging="DIRECT", cache="NONE", vec=2, lanes_m=8, warps_m=1, warps_n=16, split=8, unroll=8, grid=296),
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=4, warps_m=1, warps_n=32, split=8, unroll=2, grid=296),
 ]
 
 
@@ -35,7 +53,7 @@ def main():
         c = space.root()
         try:
             for k, v in cfg.items():
-                if k in ("staging", "cache"):
+                if k in ("staging", "cache", "xreduce"):
                     c.decide(k, ["kernel"], v)
                 else:
                     c.decide("tile", [k], str(v))
