@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import time
 import sys
 
 from .api import DeadEnd, EmitError, Search, Space, tile_cuda
@@ -38,13 +39,17 @@ def _candidate(space: Space, a):
 def cmd_explore(a) -> int:
     space = _space(a)
     s = Search(space, device=a.device, seed=a.seed, log_path=a.log, flush_l2=a.kind in ("gemv", "batched"),
-               decision_order=a.decision_order)
+               decision_order=a.decision_order, tree_depth=a.tree_depth)
+    t0 = time.perf_counter()
     s.step(a.evals)
+    wall = time.perf_counter() - t0
     st = s.stats()
     best = s.best()
     out = {"evaluations": st["evaluations"], "ok": st["ok"], "best_us": st["best_ns"] / 1e3,
            "bound_us": st["best_bound_ns"] / 1e3, "time_to_best_s": st["time_to_best_s"],
-           "bound_violations": st["bound_violations"], "exhausted": bool(st["exhausted"])}
+           "bound_violations": st["bound_violations"], "exhausted": bool(st["exhausted"]),
+           "evals_per_s": round(st["evaluations"] / max(wall, 1e-9), 1), "dead_rollouts": st["dead_rollouts"],
+           "rollouts": st["rollouts"]}
     if best is not None and space.tiles:
         out["config"] = best.tiles().as_dict()
     print(json.dumps(out))
@@ -127,6 +132,7 @@ def main(argv=None) -> int:
     p.add_argument("--log")
     p.add_argument("--out", help="write the best candidate's serialization here")
     p.add_argument("--decision-order", default=None, help="comma separated choice names (default: paper order)")
+    p.add_argument("--tree-depth", type=int, default=0, help="decisions kept in the Monte-Carlo tree (0: 12)")
     p.set_defaults(fn=cmd_explore)
     p = sub.add_parser("codegen")
     common(p)

@@ -110,6 +110,17 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
   order_ = DecisionOrder::from_names(*space_->ctx, split(order_text_));
   inc_.open(shm_text_.empty() ? nullptr : shm_text_.c_str());
   trace_ = std::getenv("ISPC_TRACE") != nullptr;
+  if (const char* g = std::getenv("ISPC_GREEDY")) {
+    const std::string v(g);
+    greedy_mode_ = v == "first" ? 0 : v == "off" ? 2 : 1;
+  }
+  if (const char* gp = std::getenv("ISPC_GREEDY_P")) greedy_p_ = std::clamp(std::atof(gp), 0.0, 1.0);
+  if (const char* q = std::getenv("ISPC_ELITE_Q")) elite_q_ = std::clamp(std::atof(q), 0.0, 1.0);
+  if (const char* mu = std::getenv("ISPC_ELITE_MUT")) elite_mut_ = std::max(0.0, std::atof(mu));
+  if (const char* r = std::getenv("ISPC_ROLLOUT")) {
+    const std::string v(r);
+    rollout_mode_ = v == "deep" ? 1 : v == "ancestor" ? 2 : 0;
+  }
   tree_depth_ = cfg_.tree_depth < 0 ? 0 : cfg_.tree_depth == 0 ? 12 : cfg_.tree_depth;
   if (!log_text_.empty()) log_ = std::fopen(log_text_.c_str(), "w");
   expand_frontier();
@@ -223,12 +234,30 @@ void Search::backprop(const std::vector<std::pair<MctsNode*, int>>& path, double
 }
 
 bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound,
-                     std::vector<std::pair<MctsNode*, int>>& path) {
+                     std::vector<std::pair<MctsNode*, int>>& path, size_t& root_out) {
   const SpaceContext& ctx = *space_->ctx;
-  const size_t root_i = size_t(subtree_cursor_++ % subtrees_.size());
+  size_t root_i = size_t(subtree_cursor_++ % subtrees_.size());
   const bool prune = cfg_.pruning != 0;
   path.clear();
   Candidate cur;
+  // ---- elite-guided: follow a measured leaf's decisions, deviate at a few ----
+  Candidate elite;
+  bool guided = false;
+  double p_mut = 0;
+  if (elite_q_ > 0 && double(rng() % 4096) < elite_q_ * 4096.0) {
+    std::lock_guard<std::mutex> lk(elite_mu_);
+    if (!elites_.empty()) {
+      // rank-biased pick: the incumbent half of the time, else any elite
+      const size_t e = (rng() & 1) ? 0 : size_t(rng() % elites_.size());
+      elite = elites_[e].leaf;
+      root_i = elites_[e].root;
+      guided = true;
+      const double depth = double(std::max<int64_t>(decisions_per_leaf_.load(), 1));
+      p_mut = std::min(1.0, elite_mut_ / depth);
+    }
+  }
+  root_out = root_i;
+  if (guided) return descend(rng, subtrees_[root_i], &elite, p_mut, leaf, leaf_bound, nullptr);
   // ---- in-tree descent (TAG) over the first tree_depth_ decisions ----
   MctsNode* node = nullptr;
   if (tree_depth_ > 0) {
@@ -286,8 +315,8 @@ bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound,
       break;  // fully specified inside the tree
     }
     int i = select_child(*node, T, rng);
-    if (i < 0) {  // every child pruned or dead under the current incumbent
-      node->dead = node->dead || !std::isfinite(T);
+    if (i < 0) {  // every child dead, or pruned by the incumbent (which only falls): for good
+      node->dead = true;
       ++pruned_;
       return false;
     }
@@ -307,48 +336,159 @@ bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound,
   } else {
     cur = subtrees_[root_i];
   }
-  // ---- rollout below the tree: p ~ max(T - b, 0) ----
+  return descend(rng, std::move(cur), nullptr, 0.0, leaf, leaf_bound, node);
+}
+
+// ---- rollout below the tree: p ~ max(T - b, 0), with backtracking ----
+  // A descent that dead-ends (every child infeasible or bound >= incumbent)
+  // or reaches a leaf it already produced returns to the deepest frame with
+  // an untried child instead of starting over from the root, so the prefix's
+  // propagation is reused; siblings are re-checked against the incumbent
+  // when they are taken. A subtree the walk exhausts within its expansion
+  // budget is marked dead in the tree above it.
+// With `guide`, each decision takes the guide leaf's value when that child
+// is still feasible and unpruned, except with probability p_mut (and always
+// when it is not), where it samples like an exploring rollout.
+bool Search::descend(std::mt19937_64& rng, Candidate cur, const Candidate* guide, double p_mut, Candidate& leaf,
+                     double& leaf_bound, MctsNode* node) {
+  const SpaceContext& ctx = *space_->ctx;
+  const bool prune = cfg_.pruning != 0;
+  int64_t decisions = 0;
+  struct Frame {
+    std::vector<Candidate> kids;
+    std::vector<double> w, b;
+  };
+  std::vector<Frame> stack;
+  int budget = rollout_mode_ == 0 ? std::numeric_limits<int>::max() : kRolloutExpansions;
+  bool cut = false, dead_end = false;
   for (;;) {
     std::uint32_t inst = order_.pick(ctx, cur);
-    if (inst == kNoInstance) {
-      leaf_bound = bound_total(cur);
-      leaf = std::move(cur);
-      return true;
-    }
     const double T = prune ? inc_.seconds() : std::numeric_limits<double>::infinity();
-    Mask m = cur.dom[inst];
-    std::vector<Candidate> kids;
-    std::vector<double> w;
-    for (int v = 0; v < kMaxDomainBits; ++v) {
-      if (!mask_has(m, v)) continue;
-      Candidate child;
-      if (apply_decision(ctx, cur, inst, v, child) != PropStatus::Ok) continue;
-      double weight = 1.0;
-      if (prune) {
-        double b = bound_total(child);
-        if (!std::isfinite(b) || b >= T) {  // unrunnable, or cannot beat the incumbent
-          ++pruned_;
-          continue;
-        }
-        // p ~ max(T - b, 0); before the first measurement
-        // there is no T, and the bound itself ranks the children (p ~ 1/b)
-        weight = std::isfinite(T) ? T - b : 1.0 / std::max(b, 1e-12);
+    if (inst == kNoInstance) {
+      const uint64_t d = digest(ctx, cur);
+      bool fresh;
+      {
+        std::lock_guard<std::mutex> lk(seen_leaf_mu_);
+        fresh = seen_leaf_.insert(d).second;
       }
-      kids.push_back(std::move(child));
-      w.push_back(weight);
-    }
-    if (kids.empty()) return false;
-    // half of the draws follow the bound greedily (the most promising child,
-    // lowest b), the other half sample p ~ max(T - b, 0) / 1/b
-    size_t choice;
-    if (prune && (rng() & 1)) {
-      choice = size_t(std::max_element(w.begin(), w.end()) - w.begin());
+      if (fresh) {
+        if (!guide) {  // running estimate of the decisions a rollout makes below its start
+          const int64_t old = decisions_per_leaf_.load();
+          decisions_per_leaf_.store(old == 0 ? decisions : (3 * old + decisions + 2) / 4);
+        }
+        leaf_bound = bound_total(cur);
+        leaf = std::move(cur);
+        return true;
+      }
+      dead_end = rollout_mode_ == 0;  // produced before: a restart treats it as a dead end
+    } else if (budget > 0) {
+      --budget;
+      Mask m = cur.dom[inst];
+      ++decisions;
+      // guided: the guide's value alone (one propagation) unless this
+      // decision mutates or that child is infeasible / pruned
+      const int want = guide ? decided_value(*guide, inst) : -1;
+      if (want >= 0 && mask_has(m, want) && double(rng() % 4096) >= p_mut * 4096.0) {
+        Candidate child;
+        if (apply_decision(ctx, cur, inst, want, child) == PropStatus::Ok) {
+          const double b = prune ? bound_total(child) : 0.0;
+          if (!prune || (std::isfinite(b) && b < T)) {
+            cur = std::move(child);
+            continue;
+          }
+        }
+      }
+      Frame f;
+      for (int v = 0; v < kMaxDomainBits; ++v) {
+        if (!mask_has(m, v)) continue;
+        Candidate child;
+        if (apply_decision(ctx, cur, inst, v, child) != PropStatus::Ok) continue;
+        double weight = 1.0, b = 0.0;
+        if (prune) {
+          b = bound_total(child);
+          if (!std::isfinite(b) || b >= T) {  // unrunnable, or cannot beat the incumbent
+            ++pruned_;
+            continue;
+          }
+          // p ~ max(T - b, 0); before the first measurement
+          // there is no T, and the bound itself ranks the children (p ~ 1/b)
+          weight = std::isfinite(T) ? T - b : 1.0 / std::max(b, 1e-12);
+        }
+        f.kids.push_back(std::move(child));
+        f.w.push_back(weight);
+        f.b.push_back(b);
+      }
+      if (!f.kids.empty()) {
+        stack.push_back(std::move(f));
+      } else {
+        dead_end = true;
+      }
     } else {
-      std::discrete_distribution<size_t> pick(w.begin(), w.end());
-      choice = pick(rng);
+      cut = true;
+      break;
     }
-    cur = std::move(kids[choice]);
+    // a dead end resumes from a uniformly drawn ancestor frame (diversity
+    // close to a restart, prefix propagation reused); a leaf produced before
+    // resumes from the deepest frame (a live region: its siblings)
+    if (rollout_mode_ == 0 && dead_end) break;  // restart: a fresh descent from the tree next time
+    if (dead_end && rollout_mode_ == 2 && stack.size() > 1) stack.resize(1 + size_t(rng() % stack.size()));
+    dead_end = false;
+    // take an untried child of the deepest frame that still has one
+    bool took = false;
+    while (!stack.empty() && !took) {
+      Frame& f = stack.back();
+      if (prune) {  // drop siblings the incumbent has overtaken since the frame was built
+        for (size_t k = f.kids.size(); k-- > 0;)
+          if (f.b[k] >= T) {
+            f.kids.erase(f.kids.begin() + long(k)), f.w.erase(f.w.begin() + long(k)), f.b.erase(f.b.begin() + long(k));
+            ++pruned_;
+          }
+      }
+      if (f.kids.empty()) {
+        stack.pop_back();
+        continue;
+      }
+      // half of the draws follow the bound greedily (the most promising child,
+      // lowest b), the other half sample p ~ max(T - b, 0) / 1/b
+      size_t choice;
+      if (prune && greedy_mode_ != 2 && double(rng() % 4096) < greedy_p_ * 4096.0) {
+        choice = size_t(std::max_element(f.w.begin(), f.w.end()) - f.w.begin());
+        if (greedy_mode_ == 1) {  // uniformly among the children tied at the best weight
+          const double top = f.w[choice];
+          size_t ties = 0;
+          for (double x : f.w) ties += x >= top;
+          size_t r = size_t(rng() % ties);
+          for (size_t k = 0; k < f.w.size(); ++k)
+            if (f.w[k] >= top && r-- == 0) {
+              choice = k;
+              break;
+            }
+        }
+      } else {
+        std::discrete_distribution<size_t> pick(f.w.begin(), f.w.end());
+        choice = pick(rng);
+      }
+      cur = std::move(f.kids[choice]);
+      f.kids.erase(f.kids.begin() + long(choice));
+      f.w.erase(f.w.begin() + long(choice));
+      f.b.erase(f.b.begin() + long(choice));
+      took = true;
+    }
+    if (!took) break;  // the whole subtree below the tree node is spent
   }
+  if (rollout_mode_ != 0 && !cut && node && tree_depth_ > 0) {  // exhausted exactly: skip it from now on
+    std::lock_guard<std::mutex> lk(tree_mu_);
+    node->dead = true;
+  }
+  return false;
+}
+
+void Search::note_elite(double ns, size_t root, const Candidate& leaf) {
+  std::lock_guard<std::mutex> lk(elite_mu_);
+  if (elites_.size() >= kElite && ns >= elites_.back().ns) return;
+  auto at = std::upper_bound(elites_.begin(), elites_.end(), ns, [](double x, const Elite& e) { return x < e.ns; });
+  elites_.insert(at, Elite{ns, root, leaf});
+  if (elites_.size() > kElite) elites_.pop_back();
 }
 
 void Search::note_fruitless() {
@@ -373,7 +513,7 @@ void Search::rollout_worker(int tid) {
     }
     double t = now();
     auto w = std::make_unique<Work>();
-    bool ok = rollout(rng, w->leaf, w->bound_s, w->path);
+    bool ok = rollout(rng, w->leaf, w->bound_s, w->path, w->root);
     ++rollouts_;
     if (!ok) {
       ++dead_rollouts_;
@@ -617,6 +757,7 @@ void Search::launch_worker() {
             best_launch_ = w->launch;
           }
         }
+        if (rc == ISPC_OK && r.status == ISPC_OK && std::isfinite(r.median_ns)) note_elite(r.median_ns, w->root, w->leaf);
         if (!w->path.empty()) {
           const double ns = (rc == ISPC_OK && r.status == ISPC_OK) ? r.median_ns
                                                                   : std::numeric_limits<double>::infinity();

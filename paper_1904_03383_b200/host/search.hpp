@@ -74,6 +74,7 @@ struct Work {
   ispc_launch launch{};
   double bound_s = 0;
   uint64_t digest = 0;
+  size_t root = 0;  // index of the shard subtree the leaf came from
   bool bit_exact = true;  // parity-mode and FFMA sgemm outputs: identical bits
   double rtol = 1e-5;     // otherwise: |out - exp| <= rtol * sum |products|
 };
@@ -117,6 +118,11 @@ class Search {
   std::deque<std::unique_ptr<Work>> work_q_;
   std::deque<std::unique_ptr<CompiledBatch>> batch_q_;
   std::unordered_set<uint64_t> seen_hash_;
+  // digests of every leaf a rollout has produced: a rollout that reaches one
+  // again backtracks to an untried sibling instead of re-emitting it
+  std::unordered_set<uint64_t> seen_leaf_;
+  std::mutex seen_leaf_mu_;
+  static constexpr int kRolloutExpansions = 96;  // node expansions one rollout may spend backtracking
   std::vector<std::thread> threads_;
   std::atomic<bool> stop_{false};
   std::atomic<int64_t> target_{0};
@@ -125,6 +131,31 @@ class Search {
   bool launching_ = false;  // guarded by mu_
   bool step_open_ = false;  // guarded by mu_: device mark 0 recorded for this step
   bool trace_ = false;      // ISPC_TRACE: one stderr line per launch
+  // ISPC_ROLLOUT: what a rollout does at a dead end or an already produced
+  // leaf: 0 "restart" from the tree (the paper's rollout), 1 "deep" (resume
+  // from the deepest frame with an untried child), 2 "ancestor" (resume from
+  // a uniformly drawn ancestor frame)
+  int rollout_mode_ = 0;
+  // ISPC_GREEDY: the greedy half of the rollout draws takes the lowest-bound
+  // child; ties (many children share the DRAM floor) go to 0 "first" in value
+  // order, 1 "random"; 2 "off" samples every draw p ~ max(T - b, 0)
+  int greedy_mode_ = 1;
+  double greedy_p_ = 0.5;  // ISPC_GREEDY_P: share of greedy draws
+  // elite-guided rollouts (ISPC_ELITE_Q, ISPC_ELITE_MUT): a share q of the
+  // rollouts copies the decisions of one of the kElite best measured leaves,
+  // deviating at ~mut randomly drawn decisions (local search around the
+  // incumbents; the rest explore through the tree as before)
+  static constexpr size_t kElite = 8;
+  double elite_q_ = 0.0, elite_mut_ = 2.0;  // off: measured worse
+  struct Elite {
+    double ns;
+    size_t root;
+    ispace::Candidate leaf;
+  };
+  std::vector<Elite> elites_;  // ascending ns, under elite_mu_
+  std::mutex elite_mu_;
+  std::atomic<int64_t> decisions_per_leaf_{0};  // running estimate of the decisions below a subtree root
+  void note_elite(double ns, size_t root, const ispace::Candidate& leaf);
 
   // statistics (guarded by mu_ unless atomic)
   ispc_search_stats st_{};
@@ -146,7 +177,9 @@ class Search {
   double bound_total(const ispace::Candidate& c) const;
   void expand_frontier();
   bool rollout(std::mt19937_64& rng, ispace::Candidate& leaf, double& leaf_bound,
-               std::vector<std::pair<MctsNode*, int>>& path);
+               std::vector<std::pair<MctsNode*, int>>& path, size_t& root_out);
+  bool descend(std::mt19937_64& rng, ispace::Candidate cur, const ispace::Candidate* guide, double p_mut,
+               ispace::Candidate& leaf, double& leaf_bound, MctsNode* node);
   // TAG-MCTS state (guarded by tree_mu_)
   std::mutex tree_mu_;
   std::vector<std::unique_ptr<MctsNode>> tree_roots_;

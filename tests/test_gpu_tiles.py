@@ -68,7 +68,7 @@ def test_gemv_small_readback(dev):
     a, x = orc.fill(512 * 256, p.seed, "a"), orc.fill(256, p.seed, "x")
     y64, scale = orc.gemv_f64(a, x, 512, 256)
     ok = 0
-    for leaf in _leaves(space, 40):
+    for leaf in _leaves(space, 80):
         m = dev.evaluate_tiles(leaf.tiles(), reps=1, warmup=0)
         if m.status == "illegal":
             continue
