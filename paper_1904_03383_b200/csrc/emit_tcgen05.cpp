@@ -146,8 +146,49 @@ static __device__ __forceinline__ void ispc_mma_commit(unsigned bar) {
 )";
 }
 
+void tc_params(ispc_launch& L, int64_t M, int64_t N, int64_t K, int BNL) {
+  // parameters: tensor maps over a and b, region a (register-staged A), region c
+  L.num_params = 4;
+  for (int i = 0; i < 2; ++i) {
+    ispc_param& P = L.params[i];
+    P.kind = ISPC_PARAM_TMAP;
+    P.is_input = 1;
+    std::snprintf(P.name, sizeof(P.name), "%s", i == 0 ? "a" : "b");
+  }
+  ispc_param& Pa = L.params[2];
+  Pa.kind = ISPC_PARAM_REGION;
+  Pa.is_input = 1;
+  Pa.elems = M * K;
+  std::snprintf(Pa.name, sizeof(Pa.name), "a");
+  ispc_param& Pc = L.params[3];
+  Pc.kind = ISPC_PARAM_REGION;
+  Pc.is_input = 1;
+  Pc.elems = M * N;
+  std::snprintf(Pc.name, sizeof(Pc.name), "c");
+  L.num_tmaps = 2;
+  ispc_tmap& ta = L.tmaps[0];
+  ta.param = 0;
+  ta.rank = 2;
+  ta.swizzle = 3;
+  std::snprintf(ta.region, sizeof(ta.region), "a");
+  ta.dims[0] = uint64_t(M), ta.dims[1] = uint64_t(K);
+  ta.strides[0] = uint64_t(M) * 4;
+  ta.box[0] = 32, ta.box[1] = 32;
+  ispc_tmap& tb = L.tmaps[1];
+  tb.param = 1;
+  tb.rank = 2;
+  tb.swizzle = 3;
+  std::snprintf(tb.region, sizeof(tb.region), "b");
+  tb.dims[0] = uint64_t(K), tb.dims[1] = uint64_t(N);
+  tb.strides[0] = uint64_t(K) * 4;
+  tb.box[0] = 32, tb.box[1] = uint32_t(BNL);
+}
+
+std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string& fn, ispc_launch& L);
+
 std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
   const int64_t M = c.m, N = c.n, K = c.k;
+  if (c.grid > 0) return emit_tcgen05_persistent(c, fn, L);
   const int BN = c.bn, S = c.stages, PAIR = c.split > 1 ? c.split : 1;
   if (c.staging != ISPC_STAGE_TMA && c.staging != ISPC_STAGE_SHARED)
     illegal("the tensor-core tile stages A by TMA or through registers, B by TMA");
@@ -366,41 +407,257 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
     L.cluster[0] = 2;
     L.cluster[1] = L.cluster[2] = 1;
   }
-  // parameters: tensor maps over a and b, region a (register-staged A), region c
-  L.num_params = 4;
-  for (int i = 0; i < 2; ++i) {
-    ispc_param& P = L.params[i];
-    P.kind = ISPC_PARAM_TMAP;
-    P.is_input = 1;
-    std::snprintf(P.name, sizeof(P.name), "%s", i == 0 ? "a" : "b");
+  tc_params(L, M, N, K, BNL);
+  L.reg_elems = 32;
+  return o.str();
+}
+
+// Persistent variant (grid > 0): `grid` CTAs (grid / split clusters) walk the
+// UMMA_M x BN output tiles t = cluster, cluster + clusters, ... (m fastest);
+// every role keeps one running k-block counter across tiles, so the TMA ring
+// and the converters run ahead into the next tile, and the accumulator is
+// double-buffered in tensor memory: four dedicated epilogue warps (8-11)
+// drain tile i's buffer while the MMA lane fills the other with tile i+1.
+// Barriers: full[S], empty[S], conv[S] as in the one-tile kernel, plus
+// accfull[2] (MMA commit -> epilogue) and accempty[2] (epilogue -> the
+// leader's MMA lane; one arrive per CTA after the epilogue warps meet).
+// The 1 x 4 wave tail of a one-tile-per-CTA grid (512 tiles over 148 SMs =
+// 3.46 waves at 4096^3, BN 256) becomes 7 rounds of 74 pair tiles at BN 128.
+std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
+  const int64_t M = c.m, N = c.n, K = c.k;
+  const int BN = c.bn, S = c.stages, PAIR = c.split > 1 ? c.split : 1;
+  if (c.staging != ISPC_STAGE_TMA && c.staging != ISPC_STAGE_SHARED)
+    illegal("the tensor-core tile stages A by TMA or through registers, B by TMA");
+  if (c.engine != ISPC_ENGINE_TF32 && c.engine != ISPC_ENGINE_TF32X3) illegal("tcgen05 kernel needs a tensor engine");
+  const bool X3 = c.engine == ISPC_ENGINE_TF32X3, A_TMA = c.staging == ISPC_STAGE_TMA;
+  const int T = 384;
+  if (!(BN == 64 || BN == 128 || BN == 256)) illegal("UMMA N must be 64, 128 or 256");
+  if (PAIR != 1 && PAIR != 2) illegal("tcgen05 pairs at most two CTAs (cta_group::2)");
+  if (S < 2 || S > 8) illegal("TMA ring depth must be 2..8");
+  if (c.grid % PAIR) illegal("persistent grid is not a whole number of CTA pairs");
+  const int UM = 128 * PAIR, BNL = BN / PAIR;
+  if (M % UM || N % BN || K % 32) illegal("shape not divisible by the UMMA_M x BN x 32 tile");
+  if (M > (int64_t(1) << 31) || K > (int64_t(1) << 31) || N > (int64_t(1) << 31))
+    illegal("shape too large for the tensor maps");
+  const int a_cols = X3 ? 64 : 32;
+  const int need_cols = 2 * BN + S * a_cols;
+  if (need_cols > 512) illegal("two accumulators + A slots exceed 512 TMEM columns");
+  int tcols = 32;
+  while (tcols < need_cols) tcols *= 2;
+  const int64_t a_bytes = 128 * 32 * 4, b_bytes = int64_t(BNL) * 32 * 4;
+  const int64_t off_b = A_TMA ? a_bytes : 0, off_bs = off_b + b_bytes;
+  const int64_t tma_bytes = off_b + b_bytes;
+  const int64_t stage = tma_bytes + (X3 ? b_bytes : 0);
+  const int64_t bar_off = S * stage;
+  const int nbar = 3 * S + 4;  // full[S], empty[S], conv[S], accfull[2], accempty[2]
+  const int64_t smem = bar_off + (nbar + 1) * 8 + 1024;
+  if (smem > 232448) illegal("TMA ring exceeds 227 KiB of shared memory");
+  const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(UM >> 4) << 24);
+  const int64_t KB = K / 32, MB = M / UM, TILES = MB * (N / BN);
+  const unsigned FULL = 0, EMPTY = 8u * S, CONV = 16u * S, AFULL = 24u * S, AEMPTY = 24u * S + 16;
+  const char* cg = PAIR == 2 ? "2" : "1";
+  const char* mma = PAIR == 2 ? "ispc_mma_tf32_ts_pair" : "ispc_mma_tf32_ts";
+  const char* commit = PAIR == 2 ? "ispc_mma_commit_pair" : "ispc_mma_commit";
+
+  std::ostringstream o;
+  o << tcgen05_prelude();
+  o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", 1) " << fn
+    << "(const __grid_constant__ ispc_tmap_t tm_a, const __grid_constant__ ispc_tmap_t tm_b, "
+       "const float* __restrict__ g_a, float* __restrict__ g_c) {\n";
+  o << "  extern __shared__ __align__(1024) unsigned char ispc_smem_raw[];\n";
+  o << "  const unsigned raw = ispc_smem_addr(ispc_smem_raw);\n";
+  o << "  const unsigned base = (raw + 1023u) & ~1023u;\n";
+  o << "  const unsigned bars = base + " << bar_off << "u;\n";
+  o << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
+  if (PAIR == 2) {
+    o << "  unsigned rank;\n";
+    o << "  asm volatile(\"mov.u32 %0, %%cluster_ctarank;\" : \"=r\"(rank));\n";
+  } else {
+    o << "  const unsigned rank = 0;\n";
   }
-  ispc_param& Pa = L.params[2];
-  Pa.kind = ISPC_PARAM_REGION;
-  Pa.is_input = 1;
-  Pa.elems = M * K;
-  std::snprintf(Pa.name, sizeof(Pa.name), "a");
-  ispc_param& Pc = L.params[3];
-  Pc.kind = ISPC_PARAM_REGION;
-  Pc.is_input = 1;
-  Pc.elems = M * N;
-  std::snprintf(Pc.name, sizeof(Pc.name), "c");
-  L.num_tmaps = 2;
-  ispc_tmap& ta = L.tmaps[0];
-  ta.param = 0;
-  ta.rank = 2;
-  ta.swizzle = 3;
-  std::snprintf(ta.region, sizeof(ta.region), "a");
-  ta.dims[0] = uint64_t(M), ta.dims[1] = uint64_t(K);
-  ta.strides[0] = uint64_t(M) * 4;
-  ta.box[0] = 32, ta.box[1] = 32;
-  ispc_tmap& tb = L.tmaps[1];
-  tb.param = 1;
-  tb.rank = 2;
-  tb.swizzle = 3;
-  std::snprintf(tb.region, sizeof(tb.region), "b");
-  tb.dims[0] = uint64_t(K), tb.dims[1] = uint64_t(N);
-  tb.strides[0] = uint64_t(K) * 4;
-  tb.box[0] = 32, tb.box[1] = uint32_t(BNL);
+  o << "  const int cl = blockIdx.x / " << PAIR << ", ncl = gridDim.x / " << PAIR << ";\n";
+  o << "  const int my_tiles = cl < " << TILES << " ? (" << TILES - 1 << " - cl) / ncl + 1 : 0;\n";
+  o << "  unsigned char* gen = ispc_smem_raw + (base - raw);\n";
+  o << "  unsigned* tmem_slot = (unsigned*)(gen + " << bar_off + nbar * 8 << ");\n";
+  o << "  if (threadIdx.x == 0) {\n";
+  o << "    for (int s = 0; s < " << nbar << "; ++s) {\n";
+  o << "      const bool per_cta = (s >= " << 2 * S << " && s < " << 3 * S << ") || s >= " << 3 * S + 2 << ";\n";
+  o << "      ispc_mbar_init(bars + 8u * s, per_cta ? " << PAIR << "u : 1u);\n";
+  o << "    }\n";
+  o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
+  if (A_TMA) o << "    asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&tm_a) : \"memory\");\n";
+  o << "    asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&tm_b) : \"memory\");\n";
+  o << "  }\n";
+  o << "  if (warp == 1) {\n";
+  o << "    asm volatile(\"tcgen05.alloc.cta_group::" << cg << ".sync.aligned.shared::cta.b32 [%0], " << tcols
+    << ";\" ::\"r\"(ispc_smem_addr(tmem_slot)) : \"memory\");\n";
+  o << "    asm volatile(\"tcgen05.relinquish_alloc_permit.cta_group::" << cg << ".sync.aligned;\" ::: \"memory\");\n";
+  o << "  }\n";
+  o << "  asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n";
+  if (PAIR == 2)
+    o << "  asm volatile(\"barrier.cluster.arrive.release.aligned;\\n barrier.cluster.wait.acquire.aligned;\" ::: "
+         "\"memory\");\n";
+  else
+    o << "  __syncthreads();\n";
+  o << "  asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
+  o << "  const unsigned tmem = *(volatile unsigned*)tmem_slot;\n";
+  // producer
+  o << "  if (warp == 0 && lane == 0) {\n";
+  o << "    int g = 0;\n";
+  o << "    for (int i = 0; i < my_tiles; ++i) {\n";
+  o << "      const int t = cl + i * ncl, m_blk = t % " << MB << ", n_blk = t / " << MB << ";\n";
+  o << "      const int m_base = m_blk * " << UM << " + rank * 128;\n";
+  o << "      for (int kb = 0; kb < " << KB << "; ++kb, ++g) {\n";
+  o << "        const int s = g % " << S << ";\n";
+  o << "        if (g >= " << S << ") ispc_mbar_wait(bars + " << EMPTY << "u + 8u * s, ((g / " << S << ") + 1) & 1);\n";
+  o << "        const unsigned full = bars + " << FULL << "u + 8u * s;\n";
+  o << "        const unsigned sa = base + s * " << stage << "u;\n";
+  o << "        ispc_mbar_expect_tx(full, " << tma_bytes << "u);\n";
+  if (A_TMA) {
+    o << "        #pragma unroll\n";
+    o << "        for (int q = 0; q < 4; ++q) ispc_tma_2d(sa + q * 4096u, &tm_a, m_base + q * 32, kb * 32, full);\n";
+  }
+  o << "        ispc_tma_2d(sa + " << off_b << "u, &tm_b, kb * 32, n_blk * " << BN << " + rank * " << BNL
+    << ", full);\n";
+  o << "      }\n    }\n";
+  o << "  } else if (warp == 1 && lane == 0 && rank == 0) {\n";
+  // MMA issuer
+  o << "    int g = 0;\n";
+  o << "    for (int i = 0; i < my_tiles; ++i) {\n";
+  o << "      const int ab = i & 1;\n";
+  o << "      if (i >= 2) ispc_mbar_wait(bars + " << AEMPTY << "u + 8u * ab, ((i >> 1) + 1) & 1);\n";
+  o << "      asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
+  o << "      const unsigned acc = tmem + ab * " << BN << "u;\n";
+  o << "      for (int kb = 0; kb < " << KB << "; ++kb, ++g) {\n";
+  o << "        const int s = g % " << S << ";\n";
+  o << "        ispc_mbar_wait(bars + " << CONV << "u + 8u * s, (g / " << S << ") & 1);\n";
+  o << "        asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
+  o << "        const unsigned sb = base + s * " << stage << "u + " << off_b << "u;\n";
+  o << "        const unsigned ta = tmem + " << 2 * BN << "u + s * " << a_cols << "u;\n";
+  o << "        #pragma unroll\n";
+  o << "        for (int kk = 0; kk < 4; ++kk) {\n";
+  o << "          const unsigned long long db = ispc_umma_desc(sb + kk * 32u, 16u, 1024u);\n";
+  if (X3) {
+    o << "          const unsigned long long dbs = ispc_umma_desc(sb + " << off_bs - off_b
+      << "u + kk * 32u, 16u, 1024u);\n";
+    o << "          " << mma << "(acc, ta + 32u + kk * 8u, db, " << idesc << "u, (kb | kk) != 0);\n";
+    o << "          " << mma << "(acc, ta + kk * 8u, dbs, " << idesc << "u, 1u);\n";
+    o << "          " << mma << "(acc, ta + kk * 8u, db, " << idesc << "u, 1u);\n";
+  } else {
+    o << "          " << mma << "(acc, ta + kk * 8u, db, " << idesc << "u, (kb | kk) != 0);\n";
+  }
+  o << "        }\n";
+  o << "        " << commit << "(bars + " << EMPTY << "u + 8u * s);\n";
+  o << "      }\n";
+  o << "      " << commit << "(bars + " << AFULL << "u + 8u * ab);  // tile done: epilogue may drain\n";
+  o << "    }\n";
+  o << "  } else if (warp >= 4 && warp < 8) {\n";
+  // converters
+  o << "    const int m = threadIdx.x - 128;\n";
+  o << "    const unsigned trow = (unsigned)((warp & 3) * 32) << 16;\n";
+  o << "    float v[32];\n";
+  o << "    int g = 0;\n";
+  o << "    for (int i = 0; i < my_tiles; ++i) {\n";
+  o << "      const int t = cl + i * ncl, m_blk = t % " << MB << ";\n";
+  o << "      const int m_base = m_blk * " << UM << " + rank * 128;\n";
+  if (!A_TMA) {
+    o << "      const float* pa = g_a + m_base + m;\n";
+    o << "      #pragma unroll\n";
+    o << "      for (int k = 0; k < 32; ++k) v[k] = __ldg(pa + (long long)k * " << M << "LL);\n";
+  }
+  o << "      for (int kb = 0; kb < " << KB << "; ++kb, ++g) {\n";
+  o << "        const int s = g % " << S << ";\n";
+  o << "        ispc_mbar_wait(bars + " << FULL << "u + 8u * s, (g / " << S << ") & 1);\n";
+  o << "        unsigned char* st = gen + s * " << stage << ";\n";
+  if (A_TMA) {
+    o << "        const unsigned src_row = (m >> 5) * 4096u + (m & 3) * 4u;\n";
+    o << "        #pragma unroll\n";
+    o << "        for (int k = 0; k < 32; ++k)\n";
+    o << "          v[k] = *(const float*)(st + src_row + (k >> 3) * 1024u + (k & 7) * 128u + ((((m & 31) >> 2) ^ (k & 7)) << 4));\n";
+  }
+  o << "        const unsigned ta = tmem + trow + " << 2 * BN << "u + s * " << a_cols << "u;\n";
+  if (X3) {
+    o << "        float lo[32];\n";
+    o << "        #pragma unroll\n";
+    o << "        for (int k = 0; k < 32; ++k) { const float h = ispc_tf32_rna(v[k]); lo[k] = v[k] - h; v[k] = h; }\n";
+    o << "        ISPC_TMEM_ST32(ta, v);\n";
+    o << "        ISPC_TMEM_ST32(ta + 32u, lo);\n";
+    o << "        #pragma unroll 4\n";
+    o << "        for (int q = m; q < " << b_bytes / 16 << "; q += 128) {\n";
+    o << "          float4* pb = (float4*)(st + " << off_b << ") + q;\n";
+    o << "          const float4 x = *pb;\n";
+    o << "          float4 hi, l4;\n";
+    o << "          hi.x = ispc_tf32_rna(x.x); hi.y = ispc_tf32_rna(x.y); hi.z = ispc_tf32_rna(x.z); hi.w = ispc_tf32_rna(x.w);\n";
+    o << "          l4.x = x.x - hi.x; l4.y = x.y - hi.y; l4.z = x.z - hi.z; l4.w = x.w - hi.w;\n";
+    o << "          *pb = hi;\n";
+    o << "          *((float4*)(st + " << off_bs << ") + q) = l4;\n";
+    o << "        }\n";
+    o << "        asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
+  } else {
+    o << "        ISPC_TMEM_ST32(ta, v);\n";
+  }
+  o << "        asm volatile(\"tcgen05.wait::st.sync.aligned;\" ::: \"memory\");\n";
+  o << "        asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n";
+  o << "        asm volatile(\"bar.sync 1, 128;\" ::: \"memory\");\n";
+  if (PAIR == 2)
+    o << "        if (m == 0) ispc_mbar_arrive_rank(bars + " << CONV << "u + 8u * s, 0u);\n";
+  else
+    o << "        if (m == 0) ispc_mbar_arrive(bars + " << CONV << "u + 8u * s);\n";
+  if (!A_TMA) {
+    o << "        if (kb + 1 < " << KB << ") {\n";
+    o << "          const float* pn = pa + (long long)(kb + 1) * 32 * " << M << "LL;\n";
+    o << "          #pragma unroll\n";
+    o << "          for (int k = 0; k < 32; ++k) v[k] = __ldg(pn + (long long)k * " << M << "LL);\n";
+    o << "        }\n";
+  }
+  o << "      }\n    }\n";
+  o << "  } else if (warp >= 8) {\n";
+  // epilogue warps: lane group = warp % 4
+  o << "    const int lg = warp & 3;\n";
+  o << "    for (int i = 0; i < my_tiles; ++i) {\n";
+  o << "      const int t = cl + i * ncl, m_blk = t % " << MB << ", n_blk = t / " << MB << ", ab = i & 1;\n";
+  o << "      ispc_mbar_wait(bars + " << AFULL << "u + 8u * ab, (i >> 1) & 1);\n";
+  o << "      asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
+  o << "      const long long row = (long long)m_blk * " << UM << " + rank * 128 + lg * 32 + lane;\n";
+  o << "      float* pc = g_c + row + (long long)n_blk * " << BN << " * " << M << "LL;\n";
+  o << "      #pragma unroll 1\n";
+  o << "      for (int c0 = 0; c0 < " << BN << "; c0 += 32) {\n";
+  o << "        unsigned r[32];\n";
+  o << "        ISPC_TMEM_LD32(tmem + ((unsigned)(lg * 32) << 16) + ab * " << BN << "u + c0, r);\n";
+  o << "        asm volatile(\"tcgen05.wait::ld.sync.aligned;\" ::: \"memory\");\n";
+  o << "        #pragma unroll\n";
+  o << "        for (int j = 0; j < 32; ++j) pc[(long long)(c0 + j) * " << M << "LL] = __uint_as_float(r[j]);\n";
+  o << "      }\n";
+  o << "      asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n";
+  o << "      asm volatile(\"bar.sync 2, 128;\" ::: \"memory\");\n";
+  if (PAIR == 2)
+    o << "      if (warp == 8 && lane == 0) ispc_mbar_arrive_rank(bars + " << AEMPTY << "u + 8u * ab, 0u);\n";
+  else
+    o << "      if (warp == 8 && lane == 0) ispc_mbar_arrive(bars + " << AEMPTY << "u + 8u * ab);\n";
+  o << "    }\n";
+  o << "  }\n";
+  o << "  __syncwarp();\n";
+  o << "  asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n";
+  if (PAIR == 2)
+    o << "  asm volatile(\"barrier.cluster.arrive.release.aligned;\\n barrier.cluster.wait.acquire.aligned;\" ::: "
+         "\"memory\");\n";
+  else
+    o << "  __syncthreads();\n";
+  o << "  if (warp == 1) {\n";
+  o << "    asm volatile(\"tcgen05.dealloc.cta_group::" << cg << ".sync.aligned.b32 %0, " << tcols
+    << ";\" ::\"r\"(tmem) : \"memory\");\n";
+  o << "  }\n";
+  o << "}\n";
+
+  L.grid_x = uint64_t(c.grid);
+  L.block[0] = uint32_t(T);
+  L.block[1] = L.block[2] = 1;
+  L.static_smem = uint32_t(smem);
+  if (PAIR == 2) {
+    L.cluster[0] = 2;
+    L.cluster[1] = L.cluster[2] = 1;
+  }
+  tc_params(L, M, N, K, BNL);
   L.reg_elems = 32;
   return o.str();
 }

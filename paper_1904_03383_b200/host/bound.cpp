@@ -83,6 +83,7 @@ BoundModel::BoundModel(const Kernel& k, const SpaceContext& ctx, const B200Machi
     r.instances = 1;
     for (ObjId l : logicals) r.instances *= double(k.logicals.at(l).extent);
     r.memory = ii.op == Op::Load || ii.op == Op::Store;
+    r.load = ii.op == Op::Load;
     r.region = ii.region;
     insts_.push_back(r);
   }
@@ -220,7 +221,7 @@ BoundReport BoundModel::bound(const Candidate& c) const {
   const double lanes = std::min(32.0, threads);
 
   // instructions that exist in every completion
-  double warp_insts = 0, thread_trips = 0;
+  double warp_insts = 0, thread_trips = 0, load_chain = 0;
   std::map<ObjId, double> region_touch;  // bytes each input region must move
   for (const InstRec& r : insts_) {
     if (r.lowering != kNoLowering && !((c.fired >> r.lowering) & 1u)) continue;
@@ -234,6 +235,12 @@ BoundReport BoundModel::bound(const Candidate& c) const {
     double pack = packable ? (r.memory ? 4.0 : 2.0) : 1.0;
     warp_insts += std::ceil(r.instances / (lanes * pack));
     thread_trips += seq / pack;
+    if (r.load) {  // trips of the dimensions certainly rolled loops around this load
+      double trips = 1;
+      for (std::size_t d : r.dims)
+        if (is(d, v_loop_)) trips *= lo[d];
+      load_chain = std::max(load_chain, trips);
+    }
     if (r.memory) {
       double& t = region_touch[r.region];
       t = std::max(t, r.instances * 4.0);
@@ -258,7 +265,7 @@ BoundReport BoundModel::bound(const Candidate& c) const {
   rep.dram = dram_bytes / m_.hbm_bytes_per_s;
   rep.sm_mem = (input_bytes + tmp_lsu) / (sms * m_.sm_bytes_per_cycle * f);
   rep.issue = warp_insts / (sms * m_.issue_per_sm_cycle * f);
-  rep.thread = thread_trips / f;
+  rep.thread = std::max(thread_trips, load_chain * m_.min_load_latency_cycles) / f;
   rep.launch = m_.launch_floor_s;
   rep.total = std::max({rep.dram, rep.sm_mem, rep.issue, rep.thread, rep.launch});
   return rep;

@@ -49,6 +49,11 @@ struct B200Machine {
   // every completion unrunnable, i.e. an infinite bound
   double max_reg_elems = 160;
   double max_unrolled = 16384;
+  // a loaded value is consumed in the iteration that loads it, and the
+  // emitter keeps LOOP dimensions rolled (#pragma unroll 1): each trip of the
+  // LOOP dimensions around a load waits at least the fastest load latency
+  // (LDS 29 cycles, L1 hit 31.8; B300_MICROARCH.md)
+  double min_load_latency_cycles = 29;
 };
 
 // Why a subtree can never run correctly on the device (bound = +inf).
@@ -81,6 +86,7 @@ class BoundModel {
     std::vector<std::size_t> dims;  // indices into dims_
     double instances;               // product of logical extents
     bool memory;
+    bool load;
     ispace::ObjId region;
   };
   struct PairRec {

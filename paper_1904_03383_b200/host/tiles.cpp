@@ -139,8 +139,10 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     // split = CTAs sharing one UMMA (cta_group::2 pairs two SMs on M = 256)
     TileParam bn = P("bn", dividing({64, 128, 256}, n)), st = P("stages", {2, 3, 4, 5, 6, 8});
     TileParam pair = P("split", m % 256 == 0 ? std::vector<std::int64_t>{1, 2} : std::vector<std::int64_t>{1});
+    TileParam grid = P("grid", {0, 148});  // 0: one tile per CTA (pair); 148: persistent, one CTA per SM
     pair.cluster = true;
-    f.params = {bn, st, pair};
+    grid.persist = true;
+    f.params = {bn, st, pair, grid};
     f.min_threads = 1;
     f.max_acc = 1;
     f.max_cluster = 2;
@@ -330,6 +332,7 @@ TileBoundReport tile_bound(const TileFamily& f, const SpaceContext& ctx, const C
         per_thread = lo("tm") * lo("tn") * K / hi("split");
       } else {
         b.ctas = M / 128 * (N / lo("bn"));
+        if (lo("grid") > 0) b.ctas = std::min(b.ctas, hi("grid"));
       }
       break;
     case ISPC_TILE_AXPY:

@@ -212,6 +212,29 @@ def test_tcgen05_staging_and_pairs(dev, engine, staging, pair):
     assert ok >= 1
 
 
+@pytest.mark.parametrize("engine", ["TF32", "TF32X3"])
+@pytest.mark.parametrize("pair", ["1", "2"])
+def test_tcgen05_persistent(dev, engine, pair):
+    """Persistent grid (148 CTAs): several tiles per CTA through one running
+    ring and a double-buffered TMEM accumulator."""
+    space = Space("sgemm_tc", m=2048, n=2048, k=96)
+    dev.bind(space.problem())
+    ok = 0
+    for staging, bn in (("TMA", "64"), ("SHARED", "128")):
+        c = space.root()
+        c.decide("engine", ["kernel"], engine).decide("staging", ["kernel"], staging)
+        c.decide("tile", ["split"], pair).decide("tile", ["bn"], bn).decide("tile", ["stages"], "4")
+        c.decide("tile", ["grid"], "148")
+        t = c.first_leaf().tiles()
+        m = dev.evaluate_tiles(t, reps=2, warmup=1)
+        if m.status == "illegal":
+            continue
+        assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
+        assert m.launch.grid_x == 148
+        ok += 1
+    assert ok >= 1
+
+
 @pytest.mark.parametrize("split", ["2", "4", "8"])
 def test_sgemm_split_k_cluster(dev, split):
     """Split-K over a cluster, partials summed through DSMEM (norm-wise 1e-5)."""

@@ -21,12 +21,13 @@ def main():
     dev = Device(0)
     dev.bind(space.problem())
     rows = []
-    for st, eng, pair, bn, stg in itertools.product(["TMA", "SHARED"], engines, ["1", "2"], ["128", "256"],
-                                                    ["2", "3", "4", "5", "6", "8"]):
+    grids = sys.argv[5].split(",") if len(sys.argv) > 5 else ["0", "148"]
+    for st, eng, pair, bn, stg, grid in itertools.product(["TMA", "SHARED"], engines, ["1", "2"], ["128", "256"],
+                                                          ["2", "3", "4", "6", "8"], grids):
         c = space.root()
         try:
             c.decide("staging", ["kernel"], st).decide("engine", ["kernel"], eng).decide("tile", ["split"], pair)
-            c.decide("tile", ["bn"], bn).decide("tile", ["stages"], stg)
+            c.decide("tile", ["bn"], bn).decide("tile", ["stages"], stg).decide("tile", ["grid"], grid)
             t = c.first_leaf().tiles()
         except (DeadEnd, ValueError):
             continue
@@ -34,7 +35,7 @@ def main():
         r = runs[-1]
         us = min(x.median_ns for x in runs) / 1e3 if all(x.status == "ok" for x in runs) else None
         tf = 2.0 * m * n * k / (us * 1e-6) / 1e12 if us else None
-        row = dict(staging=st, engine=eng, pair=pair, bn=bn, stages=stg, status=r.status, us=us,
+        row = dict(staging=st, engine=eng, pair=pair, bn=bn, stages=stg, grid=grid, status=r.status, us=us,
                    tflops=tf and round(tf, 1), mismatches=r.mismatches, max_err=r.max_err)
         if r.status not in ("ok", "illegal"):
             row["error"] = dev.error()
