@@ -124,6 +124,12 @@ static __device__ __forceinline__ void ispc_mma_tf32_ts_pair(unsigned tmem, unsi
         "f"(v[16]), "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]),       \
         "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])        \
       : "memory")
+#define ISPC_TMEM_ST16(taddr, v)                                                                              \
+  asm volatile(                                                                                              \
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" \
+      ::"r"(taddr), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),   \
+        "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])          \
+      : "memory")
 static __device__ __forceinline__ float ispc_tf32_rna(float x) {
   unsigned r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -430,7 +436,7 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
     illegal("the tensor-core tile stages A by TMA or through registers, B by TMA");
   if (c.engine != ISPC_ENGINE_TF32 && c.engine != ISPC_ENGINE_TF32X3) illegal("tcgen05 kernel needs a tensor engine");
   const bool X3 = c.engine == ISPC_ENGINE_TF32X3, A_TMA = c.staging == ISPC_STAGE_TMA;
-  const int T = 384;
+  const int T = 512;  // + warps 12-15: a second converter group (k 16..31 of each block)
   if (!(BN == 64 || BN == 128 || BN == 256)) illegal("UMMA N must be 64, 128 or 256");
   if (PAIR != 1 && PAIR != 2) illegal("tcgen05 pairs at most two CTAs (cta_group::2)");
   if (S < 2 || S > 8) illegal("TMA ring depth must be 2..8");
@@ -551,19 +557,20 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   o << "      }\n";
   o << "      " << commit << "(bars + " << AFULL << "u + 8u * ab);  // tile done: epilogue may drain\n";
   o << "    }\n";
-  o << "  } else if (warp >= 4 && warp < 8) {\n";
-  // converters
-  o << "    const int m = threadIdx.x - 128;\n";
+  o << "  } else if ((warp >= 4 && warp < 8) || warp >= 12) {\n";
+  // converters: two groups of 4 warps, group kh owns k = 16 kh .. 16 kh + 15
+  // of every k block (row m = TMEM lane of warp % 4)
+  o << "    const int m = threadIdx.x & 127, kh = warp >= 12 ? 1 : 0, ct = kh * 128 + m;\n";
   o << "    const unsigned trow = (unsigned)((warp & 3) * 32) << 16;\n";
-  o << "    float v[32];\n";
+  o << "    float v[16];\n";
   o << "    int g = 0;\n";
   o << "    for (int i = 0; i < my_tiles; ++i) {\n";
   o << "      const int t = cl + i * ncl, m_blk = t % " << MB << ";\n";
   o << "      const int m_base = m_blk * " << UM << " + rank * 128;\n";
   if (!A_TMA) {
-    o << "      const float* pa = g_a + m_base + m;\n";
+    o << "      const float* pa = g_a + m_base + m + (long long)kh * 16 * " << M << "LL;\n";
     o << "      #pragma unroll\n";
-    o << "      for (int k = 0; k < 32; ++k) v[k] = __ldg(pa + (long long)k * " << M << "LL);\n";
+    o << "      for (int k = 0; k < 16; ++k) v[k] = __ldg(pa + (long long)k * " << M << "LL);\n";
   }
   o << "      for (int kb = 0; kb < " << KB << "; ++kb, ++g) {\n";
   o << "        const int s = g % " << S << ";\n";
@@ -572,18 +579,20 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   if (A_TMA) {
     o << "        const unsigned src_row = (m >> 5) * 4096u + (m & 3) * 4u;\n";
     o << "        #pragma unroll\n";
-    o << "        for (int k = 0; k < 32; ++k)\n";
-    o << "          v[k] = *(const float*)(st + src_row + (k >> 3) * 1024u + (k & 7) * 128u + ((((m & 31) >> 2) ^ (k & 7)) << 4));\n";
+    o << "        for (int q = 0; q < 16; ++q) {\n";
+    o << "          const int k = kh * 16 + q;\n";
+    o << "          v[q] = *(const float*)(st + src_row + (k >> 3) * 1024u + (k & 7) * 128u + ((((m & 31) >> 2) ^ (k & 7)) << 4));\n";
+    o << "        }\n";
   }
-  o << "        const unsigned ta = tmem + trow + " << 2 * BN << "u + s * " << a_cols << "u;\n";
+  o << "        const unsigned ta = tmem + trow + " << 2 * BN << "u + s * " << a_cols << "u + kh * 16u;\n";
   if (X3) {
-    o << "        float lo[32];\n";
+    o << "        float lo[16];\n";
     o << "        #pragma unroll\n";
-    o << "        for (int k = 0; k < 32; ++k) { const float h = ispc_tf32_rna(v[k]); lo[k] = v[k] - h; v[k] = h; }\n";
-    o << "        ISPC_TMEM_ST32(ta, v);\n";
-    o << "        ISPC_TMEM_ST32(ta + 32u, lo);\n";
+    o << "        for (int k = 0; k < 16; ++k) { const float h = ispc_tf32_rna(v[k]); lo[k] = v[k] - h; v[k] = h; }\n";
+    o << "        ISPC_TMEM_ST16(ta, v);\n";
+    o << "        ISPC_TMEM_ST16(ta + 32u, lo);\n";
     o << "        #pragma unroll 4\n";
-    o << "        for (int q = m; q < " << b_bytes / 16 << "; q += 128) {\n";
+    o << "        for (int q = ct; q < " << b_bytes / 16 << "; q += 256) {\n";
     o << "          float4* pb = (float4*)(st + " << off_b << ") + q;\n";
     o << "          const float4 x = *pb;\n";
     o << "          float4 hi, l4;\n";
@@ -594,24 +603,24 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
     o << "        }\n";
     o << "        asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
   } else {
-    o << "        ISPC_TMEM_ST32(ta, v);\n";
+    o << "        ISPC_TMEM_ST16(ta, v);\n";
   }
   o << "        asm volatile(\"tcgen05.wait::st.sync.aligned;\" ::: \"memory\");\n";
   o << "        asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n";
-  o << "        asm volatile(\"bar.sync 1, 128;\" ::: \"memory\");\n";
+  o << "        asm volatile(\"bar.sync 1, 256;\" ::: \"memory\");\n";
   if (PAIR == 2)
-    o << "        if (m == 0) ispc_mbar_arrive_rank(bars + " << CONV << "u + 8u * s, 0u);\n";
+    o << "        if (ct == 0) ispc_mbar_arrive_rank(bars + " << CONV << "u + 8u * s, 0u);\n";
   else
-    o << "        if (m == 0) ispc_mbar_arrive(bars + " << CONV << "u + 8u * s);\n";
+    o << "        if (ct == 0) ispc_mbar_arrive(bars + " << CONV << "u + 8u * s);\n";
   if (!A_TMA) {
     o << "        if (kb + 1 < " << KB << ") {\n";
     o << "          const float* pn = pa + (long long)(kb + 1) * 32 * " << M << "LL;\n";
     o << "          #pragma unroll\n";
-    o << "          for (int k = 0; k < 32; ++k) v[k] = __ldg(pn + (long long)k * " << M << "LL);\n";
+    o << "          for (int k = 0; k < 16; ++k) v[k] = __ldg(pn + (long long)k * " << M << "LL);\n";
     o << "        }\n";
   }
   o << "      }\n    }\n";
-  o << "  } else if (warp >= 8) {\n";
+  o << "  } else if (warp >= 8 && warp < 12) {\n";
   // epilogue warps: lane group = warp % 4
   o << "    const int lg = warp & 3;\n";
   o << "    for (int i = 0; i < my_tiles; ++i) {\n";

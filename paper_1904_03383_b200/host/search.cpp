@@ -381,6 +381,10 @@ bool Search::descend(std::mt19937_64& rng, Candidate cur, const Candidate* guide
         return true;
       }
       dead_end = rollout_mode_ == 0;  // produced before: a restart treats it as a dead end
+      if (decisions == 0 && node) {  // the tree node itself is that leaf: never select it again
+        std::lock_guard<std::mutex> lk(tree_mu_);
+        node->dead = true;
+      }
     } else if (budget > 0) {
       --budget;
       Mask m = cur.dom[inst];
