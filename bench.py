@@ -90,6 +90,12 @@ def dist_setup():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        # more ranks than visible GPUs (a smoke test of the sharded path on
+        # one device): ranks share devices round-robin instead of failing
+        import torch
+        n = torch.cuda.device_count()
+        if n > 0:
+            local %= n
         import torch.distributed as dist
         dist.init_process_group("gloo")
     return world, rank, local
@@ -156,11 +162,14 @@ CONFIG_SPACES = {
     "gemv": ("gemv", dict(m=4096, n=4096), 2048, True),
     "sgemm": ("sgemm", dict(m=1024, n=1024, k=1024), 4096, False),
     "batched": ("batched", dict(m=32, n=32, k=64, batch=512), 512, True),
-    "sgemm_tc": ("sgemm_tc", dict(m=4096, n=4096, k=4096), 30, False),
-    "sgemm_tc_x3": ("sgemm_tc_x3", dict(m=4096, n=4096, k=4096), 30, False),
+    # the tcgen05 spaces hold 192 / 96 runnable leaves (staging x engine x
+    # bn x stages x pair x persistent grid); the bound prunes 3xTF32 leaves
+    # from the TF32 search once a TF32 kernel is measured
+    "sgemm_tc": ("sgemm_tc", dict(m=4096, n=4096, k=4096), 160, False),
+    "sgemm_tc_x3": ("sgemm_tc_x3", dict(m=4096, n=4096, k=4096), 96, False),
     # the 1024^3 sgemm on the tensor pipe with fp32-level accuracy (3xTF32,
     # checked at 1e-5 of sum |a||b|), beside the FFMA search and cuBLAS FP32
-    "sgemm_1024_x3": ("sgemm_tc_x3", dict(m=1024, n=1024, k=1024), 30, False),
+    "sgemm_1024_x3": ("sgemm_tc_x3", dict(m=1024, n=1024, k=1024), 96, False),
 }
 
 

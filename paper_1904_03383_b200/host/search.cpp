@@ -115,6 +115,7 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
     greedy_mode_ = v == "first" ? 0 : v == "off" ? 2 : 1;
   }
   if (const char* gp = std::getenv("ISPC_GREEDY_P")) greedy_p_ = std::clamp(std::atof(gp), 0.0, 1.0);
+  if (const char* lp = std::getenv("ISPC_LEAFB_P")) leafb_p_ = std::clamp(std::atof(lp), 0.0, 1.0);
   if (const char* q = std::getenv("ISPC_ELITE_Q")) elite_q_ = std::clamp(std::atof(q), 0.0, 1.0);
   if (const char* mu = std::getenv("ISPC_ELITE_MUT")) elite_mut_ = std::max(0.0, std::atof(mu));
   if (const char* r = std::getenv("ISPC_ROLLOUT")) {
@@ -214,6 +215,17 @@ int Search::select_child(MctsNode& n, double T, std::mt19937_64& rng) {
     double h = (si + alpha + std::sqrt(2 * si * alpha + alpha * alpha)) / double(n.visits[i]);
     if (h > best_h) best_h = h, best = int(i);
   }
+  if (fresh.empty() && leafb_p_ > 0 && double(rng() % 4096) < leafb_p_ * 4096.0) {
+    // the child whose subtree produced the lowest-bound leaf (ties at random)
+    double lb = std::numeric_limits<double>::infinity();
+    std::vector<int> at;
+    for (size_t i = 0; i < n.kid_cand.size(); ++i) {
+      if (!(n.kid_bound[i] < T) || (n.kids[i] && n.kids[i]->dead) || !std::isfinite(n.leaf_min[i])) continue;
+      if (n.leaf_min[i] < lb * (1 - 1e-9)) lb = n.leaf_min[i], at.clear();
+      if (n.leaf_min[i] <= lb * (1 + 1e-9)) at.push_back(int(i));
+    }
+    if (!at.empty()) return at[size_t(rng() % at.size())];
+  }
   if (!fresh.empty()) {  // the lowest bound first half of the time, else p ~ 1/b
     if (rng() & 1) return fresh[size_t(std::max_element(fresh_w.begin(), fresh_w.end()) - fresh_w.begin())];
     std::discrete_distribution<size_t> pick(fresh_w.begin(), fresh_w.end());
@@ -304,6 +316,7 @@ bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound,
           node->kids.resize(node->kid_cand.size());
           node->visits.assign(node->kid_cand.size(), 0);
           node->times.assign(node->kid_cand.size(), {});
+          node->leaf_min.assign(node->kid_cand.size(), std::numeric_limits<double>::infinity());
           node->expanded = true;
           if (node->kid_cand.empty()) node->dead = true;
         }
@@ -336,7 +349,12 @@ bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound,
   } else {
     cur = subtrees_[root_i];
   }
-  return descend(rng, std::move(cur), nullptr, 0.0, leaf, leaf_bound, node);
+  const bool ok = descend(rng, std::move(cur), nullptr, 0.0, leaf, leaf_bound, node);
+  if (ok && !path.empty()) {
+    std::lock_guard<std::mutex> lk(tree_mu_);
+    for (auto& [pn, i] : path) pn->leaf_min[size_t(i)] = std::min(pn->leaf_min[size_t(i)], leaf_bound);
+  }
+  return ok;
 }
 
 // ---- rollout below the tree: p ~ max(T - b, 0), with backtracking ----
