@@ -271,16 +271,18 @@ typedef struct {
   int32_t thr_m, thr_n;          /* sgemm: CTA threads along m / n                  */
   int32_t tm, tn;                /* per-thread output tile (sgemm, batched)         */
   int32_t bk;                    /* k depth staged per step                         */
-  int32_t bn;                    /* tcgen05: UMMA N (M is 128)                      */
+  int32_t bn;                    /* tcgen05: UMMA N (M is 128 per CTA)              */
   int32_t stages;                /* shared-memory ring depth                        */
   int32_t vec;                   /* global vector width (floats)                    */
   int32_t lanes_m, lanes_n;      /* gemv: warp lanes along rows / columns           */
   int32_t warps_m, warps_n;      /* gemv: warps along rows / columns                */
-  int32_t split;                 /* gemv: cluster CTAs splitting the columns (DSMEM) */
+  int32_t split;                 /* gemv: cluster CTAs splitting the columns (DSMEM);
+                                    sgemm: split-K cluster; tcgen05: 2 = cta_group::2 pair */
   int32_t unroll;                /* gemv: column loop unroll                        */
   int32_t per_cta;               /* batched: problems per CTA                       */
   int32_t threads;               /* axpy stream: threads per CTA                    */
-  int32_t grid;                  /* axpy stream: CTAs (0: one vector group per thread) */
+  int32_t grid;                  /* axpy stream: CTAs (0: one vector group per thread);
+                                    tcgen05 / gemv: persistent CTAs (0: one tile each) */
   int32_t _pad2;
 } ispc_tile_config;
 

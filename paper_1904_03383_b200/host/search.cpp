@@ -739,9 +739,13 @@ void Search::launch_worker() {
       to.check = 1;
       to.bit_exact = w->bit_exact ? 1 : 0;
       to.rtol = w->rtol;
+      // before the first measurement: 50x the leaf's own bound (>= 2 ms) for
+      // the first 64 evaluations, then the cap (a schedule 50x off its bound
+      // is not worth waiting 50 ms for while any incumbent is missing)
       to.budget_ns = std::isfinite(T) ? std::min(cfg_.max_budget_ns, std::max(T * 1e9 * cfg_.budget_factor,
                                                                                 T * 1e9 + 20e3))
-                                      : cfg_.max_budget_ns;
+                     : st_.evaluations < 64 ? std::min(cfg_.max_budget_ns, std::max(2e6, 50.0 * w->bound_s * 1e9))
+                                            : cfg_.max_budget_ns;
       ispc_time_result r{};
       int rc = ispc_launch_timed(dev_, h, &w->launch, &to, &r);
       const double t_now = now() - t0_;

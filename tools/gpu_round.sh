@@ -12,6 +12,13 @@ if [ "${2:-}" != "skip-tests" ]; then
 fi
 timeout 1500 python bench.py --steps 5 --warmup 3 > $OUT/${TAG}_bench.log 2>&1; echo "bench=$?" >> $OUT/${TAG}_bench.log
 nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/${TAG}_smi_after.csv 2>&1
+# the sharded path end to end: 2 ranks (sharing this one GPU), headline only
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29531 \
+  bench.py --gpus 2 --steps 2 --warmup 1 --configs none --no-cpu-baseline > $OUT/${TAG}_bench_2rank.log 2>&1
+echo "bench2=$?" >> $OUT/${TAG}_bench_2rank.log
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29532 \
+  bench.py --impl reference --gpus 2 --steps 2 --warmup 1 > $OUT/${TAG}_bench_ref_2rank.log 2>&1
+echo "ref2=$?" >> $OUT/${TAG}_bench_ref_2rank.log
 # launch list (cold-cache, serialised: compare shares, not absolutes)
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/${TAG}_launches.csv \
   env BENCH_NO_SAVE_BEST=1 python bench.py --steps 1 --warmup 1 --per-step 16 --configs none --no-cpu-baseline > $OUT/${TAG}_ncu_bench.log 2>&1
