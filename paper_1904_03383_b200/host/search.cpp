@@ -116,6 +116,7 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
   }
   if (const char* gp = std::getenv("ISPC_GREEDY_P")) greedy_p_ = std::clamp(std::atof(gp), 0.0, 1.0);
   if (const char* lp = std::getenv("ISPC_LEAFB_P")) leafb_p_ = std::clamp(std::atof(lp), 0.0, 1.0);
+  if (const char* sh = std::getenv("ISPC_SHARP")) sharp_ = std::max(0.0, std::atof(sh));
   if (const char* q = std::getenv("ISPC_ELITE_Q")) elite_q_ = std::clamp(std::atof(q), 0.0, 1.0);
   if (const char* mu = std::getenv("ISPC_ELITE_MUT")) elite_mut_ = std::max(0.0, std::atof(mu));
   if (const char* r = std::getenv("ISPC_ROLLOUT")) {
@@ -486,6 +487,12 @@ bool Search::descend(std::mt19937_64& rng, Candidate cur, const Candidate* guide
               break;
             }
         }
+      } else if (prune && sharp_ > 0) {
+        const double bmin = std::max(*std::min_element(f.b.begin(), f.b.end()), 1e-12);
+        std::vector<double> w2(f.w.size());
+        for (size_t k = 0; k < w2.size(); ++k) w2[k] = f.w[k] * std::exp(-sharp_ * (f.b[k] - bmin) / bmin);
+        std::discrete_distribution<size_t> pick(w2.begin(), w2.end());
+        choice = pick(rng);
       } else {
         std::discrete_distribution<size_t> pick(f.w.begin(), f.w.end());
         choice = pick(rng);

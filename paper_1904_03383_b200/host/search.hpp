@@ -141,13 +141,17 @@ class Search {
   // child; ties (many children share the DRAM floor) go to 0 "first" in value
   // order, 1 "random"; 2 "off" samples every draw p ~ max(T - b, 0)
   int greedy_mode_ = 1;
-  double greedy_p_ = 0.5;  // ISPC_GREEDY_P: share of greedy draws
+  double greedy_p_ = 0.9;  // ISPC_GREEDY_P: share of greedy draws (0.5 in the first version)
   // ISPC_LEAFB_P: share of in-tree selections (once every child was visited)
   // that take the child with the smallest leaf bound produced below it; the
   // rest use the TAG score. Leaves of low bound are rare and run fast (the
   // fused axpy schedules: bound 88 µs, measured 117-125 µs), which a score of
   // measured top-16 times alone learns slowly.
   double leafb_p_ = 0.5;
+  // ISPC_SHARP (gamma): the sampled draws weight a child by
+  // max(T - b, 0) * exp(-gamma (b - b_min) / b_min), b_min the lowest bound
+  // among the siblings; 0 = the paper's p ~ max(T - b, 0)
+  double sharp_ = 8.0;
   // elite-guided rollouts (ISPC_ELITE_Q, ISPC_ELITE_MUT): a share q of the
   // rollouts copies the decisions of one of the kElite best measured leaves,
   // deviating at ~mut randomly drawn decisions (local search around the
