@@ -796,7 +796,7 @@ void Search::launch_worker() {
                                                                   : std::numeric_limits<double>::infinity();
           backprop(w->path, ns);
         }
-        if (log_) {
+        if (log_) {  // JSON: -1 for "no value" (no incumbent yet, no time)
           std::string compact = improved ? best_text_ : std::string();
           std::replace(compact.begin(), compact.end(), '\n', ' ');
           const double logged_ns = rc == ISPC_OK && std::isfinite(r.median_ns) ? r.median_ns : -1.0;
@@ -804,7 +804,8 @@ void Search::launch_worker() {
                        "{\"i\": %lld, \"t\": %.4f, \"status\": \"%s\", \"median_ns\": %.1f, \"bound_ns\": %.1f, "
                        "\"incumbent_ns\": %.1f, \"hash\": \"%016llx\", \"digest\": \"%016llx\", \"best\": %s%s%s}\n",
                        (long long)st_.evaluations, t_now, status.c_str(), logged_ns,
-                       w->bound_s * 1e9, inc_.seconds() * 1e9, (unsigned long long)w->launch.source_hash,
+                       w->bound_s * 1e9, std::isfinite(inc_.seconds()) ? inc_.seconds() * 1e9 : -1.0,
+                       (unsigned long long)w->launch.source_hash,
                        (unsigned long long)w->digest, improved ? "true" : "false",
                        improved ? ", \"candidate\": " : "", compact.c_str());
           std::fflush(log_);
