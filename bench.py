@@ -162,10 +162,10 @@ CONFIG_SPACES = {
     "gemv": ("gemv", dict(m=4096, n=4096), 2048, True),
     "sgemm": ("sgemm", dict(m=1024, n=1024, k=1024), 4096, False),
     "batched": ("batched", dict(m=32, n=32, k=64, batch=512), 512, True),
-    # the tcgen05 spaces hold 192 / 96 runnable leaves (staging x engine x
-    # bn x stages x pair x persistent grid); the bound prunes 3xTF32 leaves
+    # the tcgen05 spaces hold ~400 / ~200 runnable leaves (staging x engine x
+    # bn x stages x cluster x persistent grid); the bound prunes 3xTF32 leaves
     # from the TF32 search once a TF32 kernel is measured
-    "sgemm_tc": ("sgemm_tc", dict(m=4096, n=4096, k=4096), 160, False),
+    "sgemm_tc": ("sgemm_tc", dict(m=4096, n=4096, k=4096), 240, False),
     "sgemm_tc_x3": ("sgemm_tc_x3", dict(m=4096, n=4096, k=4096), 96, False),
     # the 1024^3 sgemm on the tensor pipe with fp32-level accuracy (3xTF32,
     # checked at 1e-5 of sum |a||b|), beside the FFMA search and cuBLAS FP32

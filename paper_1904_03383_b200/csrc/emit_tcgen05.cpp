@@ -130,6 +130,17 @@ static __device__ __forceinline__ void ispc_mma_tf32_ts_pair(unsigned tmem, unsi
       ::"r"(taddr), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),   \
         "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])          \
       : "memory")
+static __device__ __forceinline__ void ispc_mma_commit_mask(unsigned bar, unsigned short mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"(mask) : "memory");
+}
+static __device__ __forceinline__ void ispc_tma_2d_mc(unsigned dst, const ispc_tmap_t* map, int c0, int c1, unsigned bar,
+                                                      unsigned short mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(bar), "h"(mask) : "memory");
+}
 static __device__ __forceinline__ float ispc_tf32_rna(float x) {
   unsigned r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -431,18 +442,23 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
 // 3.46 waves at 4096^3, BN 256) becomes 7 rounds of 74 pair tiles at BN 128.
 std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
   const int64_t M = c.m, N = c.n, K = c.k;
-  const int BN = c.bn, S = c.stages, PAIR = c.split > 1 ? c.split : 1;
+  // split: 1 = one CTA per tile, 2 = a cta_group::2 pair, 4 = two pairs in a
+  // cluster of 4 on adjacent n-blocks of one m-block, each A box landed once
+  // per pair member rank and multicast to both pairs (TMA .multicast::cluster)
+  const int CL = c.split > 1 ? c.split : 1, BN = c.bn, S = c.stages, PAIR = CL >= 2 ? 2 : 1;
+  const bool QUAD = CL == 4;
   if (c.staging != ISPC_STAGE_TMA && c.staging != ISPC_STAGE_SHARED)
     illegal("the tensor-core tile stages A by TMA or through registers, B by TMA");
   if (c.engine != ISPC_ENGINE_TF32 && c.engine != ISPC_ENGINE_TF32X3) illegal("tcgen05 kernel needs a tensor engine");
   const bool X3 = c.engine == ISPC_ENGINE_TF32X3, A_TMA = c.staging == ISPC_STAGE_TMA;
   const int T = 512;  // + warps 12-15: a second converter group (k 16..31 of each block)
   if (!(BN == 64 || BN == 128 || BN == 256)) illegal("UMMA N must be 64, 128 or 256");
-  if (PAIR != 1 && PAIR != 2) illegal("tcgen05 pairs at most two CTAs (cta_group::2)");
+  if (CL != 1 && CL != 2 && CL != 4) illegal("tcgen05 clusters are 1, a pair, or two pairs");
+  if (QUAD && c.staging != ISPC_STAGE_TMA) illegal("A multicast needs the TMA-staged A");
   if (S < 2 || S > 8) illegal("TMA ring depth must be 2..8");
-  if (c.grid % PAIR) illegal("persistent grid is not a whole number of CTA pairs");
+  if (c.grid % CL) illegal("persistent grid is not a whole number of clusters");
   const int UM = 128 * PAIR, BNL = BN / PAIR;
-  if (M % UM || N % BN || K % 32) illegal("shape not divisible by the UMMA_M x BN x 32 tile");
+  if (M % UM || N % (BN * (QUAD ? 2 : 1)) || K % 32) illegal("shape not divisible by the UMMA_M x BN x 32 tile");
   if (M > (int64_t(1) << 31) || K > (int64_t(1) << 31) || N > (int64_t(1) << 31))
     illegal("shape too large for the tensor maps");
   const int a_cols = X3 ? 64 : 32;
@@ -459,11 +475,15 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   const int64_t smem = bar_off + (nbar + 1) * 8 + 1024;
   if (smem > 232448) illegal("TMA ring exceeds 227 KiB of shared memory");
   const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(UM >> 4) << 24);
-  const int64_t KB = K / 32, MB = M / UM, TILES = MB * (N / BN);
+  const int64_t KB = K / 32, MB = M / UM, TILES = MB * (N / BN / (QUAD ? 2 : 1));  // QUAD: tile pairs
   const unsigned FULL = 0, EMPTY = 8u * S, CONV = 16u * S, AFULL = 24u * S, AEMPTY = 24u * S + 16;
   const char* cg = PAIR == 2 ? "2" : "1";
   const char* mma = PAIR == 2 ? "ispc_mma_tf32_ts_pair" : "ispc_mma_tf32_ts";
   const char* commit = PAIR == 2 ? "ispc_mma_commit_pair" : "ispc_mma_commit";
+  auto commit_to = [&](const std::string& bar, const char* mask) {  // both pairs (QUAD) or the own pair
+    if (QUAD) return std::string("ispc_mma_commit_mask(") + bar + ", " + mask + ")";
+    return std::string(commit) + "(" + bar + ")";
+  };
 
   std::ostringstream o;
   o << tcgen05_prelude();
@@ -481,14 +501,17 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   } else {
     o << "  const unsigned rank = 0;\n";
   }
-  o << "  const int cl = blockIdx.x / " << PAIR << ", ncl = gridDim.x / " << PAIR << ";\n";
+  o << "  const int cl = blockIdx.x / " << CL << ", ncl = gridDim.x / " << CL << ";\n";
+  o << "  const unsigned prank = rank & 1u, lead = rank & ~1u, sub = rank >> 1;  // rank in the pair, its leader, the pair\n";
+  o << "  const unsigned short pair_mask = (unsigned short)(3u << (2u * sub));\n";
   o << "  const int my_tiles = cl < " << TILES << " ? (" << TILES - 1 << " - cl) / ncl + 1 : 0;\n";
   o << "  unsigned char* gen = ispc_smem_raw + (base - raw);\n";
   o << "  unsigned* tmem_slot = (unsigned*)(gen + " << bar_off + nbar * 8 << ");\n";
   o << "  if (threadIdx.x == 0) {\n";
   o << "    for (int s = 0; s < " << nbar << "; ++s) {\n";
   o << "      const bool per_cta = (s >= " << 2 * S << " && s < " << 3 * S << ") || s >= " << 3 * S + 2 << ";\n";
-  o << "      ispc_mbar_init(bars + 8u * s, per_cta ? " << PAIR << "u : 1u);\n";
+  o << "      const bool empty = s >= " << S << " && s < " << 2 * S << ";\n";
+  o << "      ispc_mbar_init(bars + 8u * s, per_cta ? " << PAIR << "u : empty ? " << (QUAD ? 2 : 1) << "u : 1u);\n";
   o << "    }\n";
   o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
   if (A_TMA) o << "    asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&tm_a) : \"memory\");\n";
@@ -511,22 +534,27 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   o << "  if (warp == 0 && lane == 0) {\n";
   o << "    int g = 0;\n";
   o << "    for (int i = 0; i < my_tiles; ++i) {\n";
-  o << "      const int t = cl + i * ncl, m_blk = t % " << MB << ", n_blk = t / " << MB << ";\n";
-  o << "      const int m_base = m_blk * " << UM << " + rank * 128;\n";
+  o << "      const int t = cl + i * ncl, m_blk = t % " << MB << ", n_blk = " << (QUAD ? "(t / " + std::to_string(MB) + ") * 2 + sub" : "t / " + std::to_string(MB)) << ";\n";
+  o << "      const int m_base = m_blk * " << UM << " + prank * 128;\n";
   o << "      for (int kb = 0; kb < " << KB << "; ++kb, ++g) {\n";
   o << "        const int s = g % " << S << ";\n";
   o << "        if (g >= " << S << ") ispc_mbar_wait(bars + " << EMPTY << "u + 8u * s, ((g / " << S << ") + 1) & 1);\n";
   o << "        const unsigned full = bars + " << FULL << "u + 8u * s;\n";
   o << "        const unsigned sa = base + s * " << stage << "u;\n";
   o << "        ispc_mbar_expect_tx(full, " << tma_bytes << "u);\n";
-  if (A_TMA) {
+  if (A_TMA && QUAD) {  // this CTA lands boxes 2 sub, 2 sub + 1 in itself and in the other pair's same-rank CTA
+    o << "        const unsigned short amask = (unsigned short)((1u << rank) | (1u << (rank ^ 2u)));\n";
+    o << "        #pragma unroll\n";
+    o << "        for (int q = 2 * sub; q < 2 * sub + 2; ++q)\n";
+    o << "          ispc_tma_2d_mc(sa + q * 4096u, &tm_a, m_base + q * 32, kb * 32, full, amask);\n";
+  } else if (A_TMA) {
     o << "        #pragma unroll\n";
     o << "        for (int q = 0; q < 4; ++q) ispc_tma_2d(sa + q * 4096u, &tm_a, m_base + q * 32, kb * 32, full);\n";
   }
-  o << "        ispc_tma_2d(sa + " << off_b << "u, &tm_b, kb * 32, n_blk * " << BN << " + rank * " << BNL
+  o << "        ispc_tma_2d(sa + " << off_b << "u, &tm_b, kb * 32, n_blk * " << BN << " + prank * " << BNL
     << ", full);\n";
   o << "      }\n    }\n";
-  o << "  } else if (warp == 1 && lane == 0 && rank == 0) {\n";
+  o << "  } else if (warp == 1 && lane == 0 && prank == 0) {\n";
   // MMA issuer
   o << "    int g = 0;\n";
   o << "    for (int i = 0; i < my_tiles; ++i) {\n";
@@ -553,9 +581,10 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
     o << "          " << mma << "(acc, ta + kk * 8u, db, " << idesc << "u, (kb | kk) != 0);\n";
   }
   o << "        }\n";
-  o << "        " << commit << "(bars + " << EMPTY << "u + 8u * s);\n";
+  o << "        " << commit_to("bars + " + std::to_string(EMPTY) + "u + 8u * s", "(unsigned short)15") << ";\n";
   o << "      }\n";
-  o << "      " << commit << "(bars + " << AFULL << "u + 8u * ab);  // tile done: epilogue may drain\n";
+  o << "      " << commit_to("bars + " + std::to_string(AFULL) + "u + 8u * ab", "pair_mask")
+    << ";  // tile done: epilogue may drain\n";
   o << "    }\n";
   o << "  } else if ((warp >= 4 && warp < 8) || warp >= 12) {\n";
   // converters: two groups of 4 warps, group kh owns k = 16 kh .. 16 kh + 15
@@ -566,7 +595,7 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   o << "    int g = 0;\n";
   o << "    for (int i = 0; i < my_tiles; ++i) {\n";
   o << "      const int t = cl + i * ncl, m_blk = t % " << MB << ";\n";
-  o << "      const int m_base = m_blk * " << UM << " + rank * 128;\n";
+  o << "      const int m_base = m_blk * " << UM << " + prank * 128;\n";
   if (!A_TMA) {
     o << "      const float* pa = g_a + m_base + m + (long long)kh * 16 * " << M << "LL;\n";
     o << "      #pragma unroll\n";
@@ -609,7 +638,7 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   o << "        asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n";
   o << "        asm volatile(\"bar.sync 1, 256;\" ::: \"memory\");\n";
   if (PAIR == 2)
-    o << "        if (ct == 0) ispc_mbar_arrive_rank(bars + " << CONV << "u + 8u * s, 0u);\n";
+    o << "        if (ct == 0) ispc_mbar_arrive_rank(bars + " << CONV << "u + 8u * s, lead);\n";
   else
     o << "        if (ct == 0) ispc_mbar_arrive(bars + " << CONV << "u + 8u * s);\n";
   if (!A_TMA) {
@@ -624,10 +653,10 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   // epilogue warps: lane group = warp % 4
   o << "    const int lg = warp & 3;\n";
   o << "    for (int i = 0; i < my_tiles; ++i) {\n";
-  o << "      const int t = cl + i * ncl, m_blk = t % " << MB << ", n_blk = t / " << MB << ", ab = i & 1;\n";
+  o << "      const int t = cl + i * ncl, m_blk = t % " << MB << ", n_blk = " << (QUAD ? "(t / " + std::to_string(MB) + ") * 2 + sub" : "t / " + std::to_string(MB)) << ", ab = i & 1;\n";
   o << "      ispc_mbar_wait(bars + " << AFULL << "u + 8u * ab, (i >> 1) & 1);\n";
   o << "      asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
-  o << "      const long long row = (long long)m_blk * " << UM << " + rank * 128 + lg * 32 + lane;\n";
+  o << "      const long long row = (long long)m_blk * " << UM << " + prank * 128 + lg * 32 + lane;\n";
   o << "      float* pc = g_c + row + (long long)n_blk * " << BN << " * " << M << "LL;\n";
   o << "      #pragma unroll 1\n";
   o << "      for (int c0 = 0; c0 < " << BN << "; c0 += 32) {\n";
@@ -640,7 +669,7 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   o << "      asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n";
   o << "      asm volatile(\"bar.sync 2, 128;\" ::: \"memory\");\n";
   if (PAIR == 2)
-    o << "      if (warp == 8 && lane == 0) ispc_mbar_arrive_rank(bars + " << AEMPTY << "u + 8u * ab, 0u);\n";
+    o << "      if (warp == 8 && lane == 0) ispc_mbar_arrive_rank(bars + " << AEMPTY << "u + 8u * ab, lead);\n";
   else
     o << "      if (warp == 8 && lane == 0) ispc_mbar_arrive(bars + " << AEMPTY << "u + 8u * ab);\n";
   o << "    }\n";
@@ -662,8 +691,8 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   L.block[0] = uint32_t(T);
   L.block[1] = L.block[2] = 1;
   L.static_smem = uint32_t(smem);
-  if (PAIR == 2) {
-    L.cluster[0] = 2;
+  if (CL > 1) {
+    L.cluster[0] = uint32_t(CL);
     L.cluster[1] = L.cluster[2] = 1;
   }
   tc_params(L, M, N, K, BNL);

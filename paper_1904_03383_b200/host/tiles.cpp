@@ -138,14 +138,15 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     f.x3_only = kind == "sgemm_tc_x3";
     // split = CTAs sharing one UMMA (cta_group::2 pairs two SMs on M = 256)
     TileParam bn = P("bn", dividing({64, 128, 256}, n)), st = P("stages", {2, 3, 4, 5, 6, 8});
-    TileParam pair = P("split", m % 256 == 0 ? std::vector<std::int64_t>{1, 2} : std::vector<std::int64_t>{1});
-    TileParam grid = P("grid", {0, 148});  // 0: one tile per CTA (pair); 148: persistent, one CTA per SM
+    // split = 4: two pairs on adjacent n-blocks sharing A by TMA multicast (persistent grid only)
+    TileParam pair = P("split", m % 256 == 0 ? std::vector<std::int64_t>{1, 2, 4} : std::vector<std::int64_t>{1});
+    TileParam grid = P("grid", {0, 128, 144, 148});  // 0: one tile per CTA (pair); else persistent CTAs (<= one per SM)
     pair.cluster = true;
     grid.persist = true;
     f.params = {bn, st, pair, grid};
     f.min_threads = 1;
     f.max_acc = 1;
-    f.max_cluster = 2;
+    f.max_cluster = 4;
     // A by TMA (transposed in shared memory) or through registers; B by TMA
     pre("staging", {"TMA", "SHARED"});
     if (f.x3_only) pre("engine", {"TF32X3"});

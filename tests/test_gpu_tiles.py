@@ -213,10 +213,11 @@ def test_tcgen05_staging_and_pairs(dev, engine, staging, pair):
 
 
 @pytest.mark.parametrize("engine", ["TF32", "TF32X3"])
-@pytest.mark.parametrize("pair", ["1", "2"])
+@pytest.mark.parametrize("pair", ["1", "2", "4"])
 def test_tcgen05_persistent(dev, engine, pair):
     """Persistent grid (148 CTAs): several tiles per CTA through one running
-    ring and a double-buffered TMEM accumulator."""
+    ring and a double-buffered TMEM accumulator; split 4 = two pairs sharing
+    the A boxes by TMA multicast."""
     space = Space("sgemm_tc", m=2048, n=2048, k=96)
     dev.bind(space.problem())
     ok = 0

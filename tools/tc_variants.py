@@ -22,7 +22,8 @@ def main():
     dev.bind(space.problem())
     rows = []
     grids = sys.argv[5].split(",") if len(sys.argv) > 5 else ["0", "148"]
-    for st, eng, pair, bn, stg, grid in itertools.product(["TMA", "SHARED"], engines, ["1", "2"], ["128", "256"],
+    pairs = sys.argv[6].split(",") if len(sys.argv) > 6 else ["1", "2"]
+    for st, eng, pair, bn, stg, grid in itertools.product(["TMA", "SHARED"], engines, pairs, ["128", "256"],
                                                           ["2", "3", "4", "6", "8"], grids):
         c = space.root()
         try:
