@@ -55,12 +55,6 @@ static __device__ __forceinline__ void ispc_mbar_wait(unsigned bar, unsigned par
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra ISPC_WAIT_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
 }
-static __device__ __forceinline__ void ispc_mbar_wait_cluster(unsigned bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n ISPC_WAITC_%=:\n"
-      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra ISPC_WAITC_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
-}
 static __device__ __forceinline__ void ispc_mbar_expect_tx(unsigned bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
@@ -74,13 +68,6 @@ static __device__ __forceinline__ unsigned long long ispc_umma_desc(unsigned add
   return (unsigned long long)((addr >> 4) & 0x3FFF) | ((unsigned long long)((lbo >> 4) & 0x3FFF) << 16) |
          ((unsigned long long)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
 }
-static __device__ __forceinline__ void ispc_mma_tf32(unsigned tmem, unsigned long long da, unsigned long long db,
-                                                     unsigned idesc, unsigned accumulate) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem), "l"(da), "l"(db), "r"(idesc),
-      "r"(accumulate) : "memory");
-}
 static __device__ __forceinline__ void ispc_mbar_arrive(unsigned bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -88,13 +75,6 @@ static __device__ __forceinline__ void ispc_mbar_arrive_rank(unsigned bar, unsig
   unsigned r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(bar), "r"(rank));
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
-}
-static __device__ __forceinline__ void ispc_mma_tf32_pair(unsigned tmem, unsigned long long da, unsigned long long db,
-                                                          unsigned idesc, unsigned accumulate) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem), "l"(da), "l"(db), "r"(idesc),
-      "r"(accumulate) : "memory");
 }
 static __device__ __forceinline__ void ispc_mma_commit_pair(unsigned bar) {
   asm volatile(
