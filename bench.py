@@ -161,7 +161,7 @@ CONFIG_SPACES = {
     "axpy_stream": ("axpy_stream", dict(n=1 << 26), 256, False),
     "gemv": ("gemv", dict(m=4096, n=4096), 2048, True),
     "sgemm": ("sgemm", dict(m=1024, n=1024, k=1024), 4096, False),
-    "batched": ("batched", dict(m=32, n=32, k=64, batch=512), 512, True),
+    "batched": ("batched", dict(m=32, n=32, k=64, batch=512), 1536, True),
     # the tcgen05 spaces hold ~400 / ~200 runnable leaves (staging x engine x
     # bn x stages x cluster x persistent grid); the bound prunes 3xTF32 leaves
     # from the TF32 search once a TF32 kernel is measured
