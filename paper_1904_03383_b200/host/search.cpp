@@ -180,10 +180,12 @@ void Search::expand_frontier() {
     if (!grew || next.empty()) break;
     frontier = std::move(next);
   }
-  for (size_t i = size_t(cfg_.shard_index); i < frontier.size(); i += size_t(cfg_.shard_count))
-    subtrees_.push_back(frontier[i]);
-  if (subtrees_.empty()) subtrees_.push_back(space_->root);  // tiny spaces: every shard searches all
-  st_.frontier = int64_t(subtrees_.size());
+  subtrees_ = std::move(frontier);
+  for (size_t i = size_t(cfg_.shard_index); i < subtrees_.size(); i += size_t(cfg_.shard_count)) mine_.push_back(i);
+  if (mine_.empty()) {  // tiny spaces: every shard searches all
+    for (size_t i = 0; i < subtrees_.size(); ++i) mine_.push_back(i);
+  }
+  st_.frontier = int64_t(mine_.size());
 }
 
 double Search::bound_total(const Candidate& c) const {
@@ -249,7 +251,8 @@ void Search::backprop(const std::vector<std::pair<MctsNode*, int>>& path, double
 bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound,
                      std::vector<std::pair<MctsNode*, int>>& path, size_t& root_out) {
   const SpaceContext& ctx = *space_->ctx;
-  size_t root_i = size_t(subtree_cursor_++ % subtrees_.size());
+  const uint64_t cur_i = subtree_cursor_++;
+  size_t root_i = stealing_ ? size_t(cur_i % subtrees_.size()) : mine_[size_t(cur_i % mine_.size())];
   const bool prune = cfg_.pruning != 0;
   path.clear();
   Candidate cur;
@@ -521,7 +524,14 @@ void Search::note_elite(double ns, size_t root, const Candidate& leaf) {
 }
 
 void Search::note_fruitless() {
-  if (++fruitless_ >= kExhaust && !exhausted_.exchange(true)) {
+  if (++fruitless_ < kExhaust) return;
+  if (cfg_.shard_count > 1 && mine_.size() < subtrees_.size() && !stealing_.exchange(true)) {
+    fruitless_ = 0;  // own shard spent: steal from the whole frontier before giving up
+    if (trace_) std::fprintf(stderr, "[ispc] shard %d spent, stealing from %zu subtrees\n", cfg_.shard_index,
+                             subtrees_.size());
+    return;
+  }
+  if (!exhausted_.exchange(true)) {
     std::lock_guard<std::mutex> lk(mu_);
     cv_done_.notify_all();
   }
@@ -899,7 +909,7 @@ ispc_search_stats Search::stats() const {
 
 std::vector<uint64_t> Search::frontier_digests() const {
   std::vector<uint64_t> d;
-  for (const Candidate& c : subtrees_) d.push_back(digest(*space_->ctx, c));
+  for (size_t i : mine_) d.push_back(digest(*space_->ctx, subtrees_[i]));
   return d;
 }
 

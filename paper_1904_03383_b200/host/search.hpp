@@ -107,7 +107,12 @@ class Search {
   B200Machine machine_;
   std::unique_ptr<BoundModel> model_;
   DecisionOrder order_;
-  std::vector<ispace::Candidate> subtrees_;
+  // every rank computes the same frontier; this shard owns the indices in
+  // mine_ and, once those are spent (exhausted), steals: its rollouts start
+  // from any frontier subtree (stealing_), so no GPU idles while others work
+  std::vector<ispace::Candidate> subtrees_;  // the whole frontier
+  std::vector<size_t> mine_;
+  std::atomic<bool> stealing_{false};
   Incumbent inc_;
   ispc_dev* dev_ = nullptr;
   std::string err_;
