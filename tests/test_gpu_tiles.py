@@ -276,3 +276,20 @@ def test_cli_explore_then_replay(tmp_path, capsys):
 
 def test_axpy_stream_full_size_bit_exact(dev):
     _run_many(dev, Space("axpy_stream", n=1 << 26), 30, 10)
+
+
+@pytest.mark.parametrize("knobs", [{"ISPC_ROLLOUT": "deep"}, {"ISPC_ROLLOUT": "ancestor"},
+                                   {"ISPC_ELITE_Q": "0.5"}, {"ISPC_GREEDY_P": "0.5", "ISPC_SHARP": "0"}])
+def test_search_policy_knobs(monkeypatch, capsys, knobs):
+    """Every rollout policy the experiments in DESIGN.md section 5 compare
+    runs a search to measured, correct kernels with an admissible bound."""
+    import json
+
+    from paper_1904_03383_b200 import cli
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    assert cli.main(["explore", "axpy", "--n", str(1 << 20), "--factors", "2,4", "2,4,8,16,32,64,128,256",
+                     "--evals", "48", "--seed", "5"]) == 0
+    out = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert out["evaluations"] >= 1 and out["ok"] >= 1
+    assert out["bound_violations"] == 0
