@@ -219,6 +219,100 @@ std::string gemv_tma_persistent(const ispc_tile_config& c, const std::string& fn
   return o.str();
 }
 
+// Balanced gemv (staging DIRECT, grid > 0): grid / split clusters, cluster c
+// owns the rows [c RB, (c + 1) RB) with RB = ceil(m / clusters) rounded up to
+// 16, so the 2 x 148 SM slots get equal work although 4096 rows do not split
+// into 148 equal power-of-two blocks (the last cluster holds the remainder).
+// Warp lanes cover 32 x vec consecutive rows of one column (128-512 B per
+// load instruction, lanes past the cluster's last row idle); warps split the
+// CTA's column slice, CTAs of a cluster split the columns; partial sums meet
+// in shared memory, then across the cluster through DSMEM (rank-strided rows).
+std::string gemv_balanced(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
+  const int64_t m = c.m, n = c.n;
+  const int V = c.vec, WM = c.warps_m, WN = c.warps_n, S = c.split, U = c.unroll;
+  if (!(V == 1 || V == 2 || V == 4)) illegal("vector width must be 1, 2 or 4");
+  if (c.lanes_m != 32 || c.lanes_n != 1) illegal("balanced gemv puts all 32 lanes on rows");
+  if (WM < 1 || WN < 1 || S < 1 || U < 1) illegal("non-positive tile parameter");
+  const int T = 32 * WM * WN;
+  if (T > 1024) illegal("more than 1024 threads per CTA");
+  if (S > 8) illegal("cluster larger than 8 CTAs");
+  if (c.grid % S) illegal("grid is not a whole number of clusters");
+  const int64_t NC = c.grid / S;
+  const int64_t RB = ((m + NC - 1) / NC + 15) / 16 * 16;  // rows per cluster
+  const int64_t CAP = int64_t(32) * V * WM;                // rows a CTA's lanes cover
+  if (RB > CAP) illegal("the CTA's lanes do not cover the cluster's rows");
+  if (CAP > 2 * RB) illegal("more than half of the lanes would idle");
+  if (RB % V || m % V) illegal("vector width does not divide the row blocks");
+  if (n % (int64_t(S) * WN * U)) illegal("column split does not divide n");
+  const int64_t iters = n / (int64_t(S) * WN);
+  const int64_t smem = 4 * (int64_t(WN) * CAP + CAP);
+  if (smem > 232448) illegal("shared memory exceeds 227 KiB");
+  const std::string ty = V == 4 ? "float4" : V == 2 ? "float2" : "float";
+  std::ostringstream o;
+  o << "extern \"C\" __global__ void __launch_bounds__(" << T << ") " << fn
+    << "(const float* __restrict__ g_a, const float* __restrict__ g_x, float* __restrict__ g_y) {\n";
+  o << "  extern __shared__ __align__(16) float ispc_smem[];\n";
+  o << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n";
+  o << "  const int wm = warp % " << WM << ", wn = warp / " << WM << ";\n";
+  o << "  const int rank = " << (S > 1 ? "(int)ispc_cluster_rank()" : "0") << ";\n";
+  o << "  const long long row_begin = (long long)(blockIdx.x / " << S << ") * " << RB << "LL;\n";
+  o << "  const long long row_end = row_begin + " << RB << "LL < " << m << "LL ? row_begin + " << RB << "LL : " << m
+    << "LL;\n";
+  o << "  const int rl = (wm * 32 + lane) * " << V << ";\n";
+  o << "  const long long row0 = row_begin + rl;\n";
+  o << "  const long long col0 = (long long)rank * " << n / S << "LL + wn;\n";
+  o << "  float acc[" << V << "];\n";
+  o << "  #pragma unroll\n  for (int v = 0; v < " << V << "; ++v) acc[v] = 0.0f;\n";
+  o << "  if (row0 < row_end) {\n";
+  o << "    const float* pa = g_a + row0 + col0 * " << m << "LL;\n";
+  o << "    const float* px = g_x + col0;\n";
+  o << "    #pragma unroll 1\n    for (long long t = 0; t < " << iters << "LL; t += " << U << ") {\n";
+  o << "      " << ty << " av[" << U << "];\n      float xv[" << U << "];\n";
+  o << "      #pragma unroll\n      for (int u = 0; u < " << U << "; ++u) {\n";
+  o << "        av[u] = " << ld(c.cache, V, "pa + (t + u) * " + std::to_string(int64_t(WN) * m) + "LL") << ";\n";
+  o << "        xv[u] = __ldg(px + (t + u) * " << WN << "LL);\n";
+  o << "      }\n";
+  o << "      #pragma unroll\n      for (int u = 0; u < " << U << "; ++u) {\n";
+  if (V == 1) o << "        acc[0] = __fmaf_rn(av[u], xv[u], acc[0]);\n";
+  else
+    for (int v = 0; v < V; ++v)
+      o << "        acc[" << v << "] = __fmaf_rn(av[u]" << comp(v) << ", xv[u], acc[" << v << "]);\n";
+  o << "      }\n    }\n  }\n";
+  o << "  float* part = ispc_smem;                  // [WN][CAP] warp partials\n";
+  o << "  float* csum = ispc_smem + " << int64_t(WN) * CAP << ";  // [CAP] CTA partials\n";
+  o << "  #pragma unroll\n  for (int v = 0; v < " << V << "; ++v) part[wn * " << CAP << " + rl + v] = acc[v];\n";
+  o << "  __syncthreads();\n";
+  o << "  for (int r = tid; r < " << CAP << "; r += " << T << ") {\n";
+  o << "    float s = part[r];\n";
+  o << "    for (int w = 1; w < " << WN << "; ++w) s += part[w * " << CAP << " + r];\n";
+  if (S == 1) o << "    if (row_begin + r < row_end) g_y[row_begin + r] = s;\n";
+  else o << "    csum[r] = s;\n";
+  o << "  }\n";
+  if (S > 1) {
+    o << "  ispc_cluster_sync();\n";
+    o << "  for (int r = tid; r < " << CAP << "; r += " << T << ") {\n";
+    o << "    if (r % " << S << " != rank || row_begin + r >= row_end) continue;\n";
+    o << "    float s = 0.0f;\n";
+    o << "    #pragma unroll\n    for (int q = 0; q < " << S << "; ++q) s += ispc_dsmem_ld(csum + r, q);\n";
+    o << "    g_y[row_begin + r] = s;\n";
+    o << "  }\n";
+    o << "  ispc_cluster_sync();\n";
+    L.cluster[0] = uint32_t(S);
+    L.cluster[1] = L.cluster[2] = 1;
+  }
+  o << "}\n";
+  L.static_smem = uint32_t(smem);
+  L.grid_x = uint64_t(c.grid);
+  L.block[0] = uint32_t(T);
+  L.block[1] = L.block[2] = 1;
+  add_region(L, "a", m * n);
+  add_region(L, "x", n);
+  add_region(L, "y", m);
+  L.params[2].is_input = 1;
+  L.reg_elems = uint32_t(V * (U + 1) + U);
+  return o.str();
+}
+
 std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
   const int64_t m = c.m, n = c.n;
   const int V = c.vec, LM = c.lanes_m, LN = c.lanes_n, WM = c.warps_m, WN = c.warps_n, S = c.split,
@@ -251,11 +345,10 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
     if (CB % G || (n / S) % CB) illegal("stage columns do not split across column lanes / the CTA slice");
     if (tma && (R > 256 || CB > 256)) illegal("TMA boxes hold at most 256 elements per dimension");
   }
-  const bool persist = c.grid > 0;
-  if (persist) {
+  if (c.grid > 0) {  // the balanced (DIRECT) or persistent (TMA) variants
     if (tma) return gemv_tma_persistent(c, fn, L);
-    if (staged) illegal("the cp.async ring does not stream across row blocks (persistent grid)");
-    if (c.grid % S) illegal("persistent grid is not a whole number of clusters");
+    if (staged) illegal("the cp.async ring does not take a grid size");
+    return gemv_balanced(c, fn, L);
   }
   // ring 128-byte aligned (TMA destination), then full[ST] / empty[ST] mbarriers
   const int64_t ring_off = (xr_off + (xr_shared ? int64_t(T) * V : 0) + 31) / 32 * 32;
@@ -273,11 +366,7 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
   o << "  const int lm = lane % " << LM << ", ln = lane / " << LM << ";\n";
   o << "  const int wm = warp % " << WM << ", wn = warp / " << WM << ";\n";
   o << "  const int rank = " << (S > 1 ? "(int)ispc_cluster_rank()" : "0") << ";\n";
-  if (persist)  // persistent: the cluster walks row blocks rblk, rblk + clusters, ...
-    o << "  for (long long rblk = blockIdx.x / " << S << "; rblk < " << m / R << "LL; rblk += gridDim.x / " << S
-      << ") {\n";
-  else
-    o << "  const long long rblk = blockIdx.x / " << S << ";\n";
+  o << "  const long long rblk = blockIdx.x / " << S << ";\n";
   o << "  const long long row0 = rblk * " << R << "LL + (long long)(wm * " << LM << " + lm) * " << V << ";\n";
   o << "  const long long col0 = (long long)rank * " << n / S << "LL + wn * " << LN << " + ln;\n";
   o << "  const float* pa = g_a + row0 + col0 * " << m << "LL;\n";
@@ -403,9 +492,7 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
       for (int v = 0; v < V; ++v) o << (v ? ", " : "") << "acc[" << v << "]";
       o << ");\n";
     }
-    o << "  }\n";
-    if (persist) o << "  }\n";
-    o << "}\n";
+    o << "  }\n}\n";
   } else {
     // (2) warps sharing rows (wn), ascending wn
     o << "  float* part = ispc_smem + " << part_off << ";\n";
@@ -432,13 +519,10 @@ std::string gemv(const ispc_tile_config& c, const std::string& fn, ispc_launch& 
       o << "  ispc_cluster_sync();\n";
       L.cluster[0] = uint32_t(S);
       L.cluster[1] = L.cluster[2] = 1;
-    } else if (persist) {
-      o << "  __syncthreads();  // partials reused by the next row block\n";
     }
-    if (persist) o << "  }\n";
     o << "}\n";
   }
-  L.grid_x = persist ? uint64_t(c.grid) : uint64_t(m / R * S);
+  L.grid_x = uint64_t(m / R * S);
   L.block[0] = uint32_t(T);
   L.block[1] = L.block[2] = 1;
   add_region(L, "a", m * n);

@@ -86,7 +86,7 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     TileParam wm = P("warps_m", pow2_upto(1, 8)), wn = P("warps_n", dividing(pow2_upto(1, 32), n));
     TileParam split = P("split", dividing({1, 2, 4, 8}, n)), unroll = P("unroll", dividing({1, 2, 4, 8, 16}, n));
     TileParam bk = P("bk", {1, 8, 16, 32, 64, 128, 256}), st = P("stages", {1, 2, 3, 4, 6, 8});
-    TileParam grid = P("grid", {0});  // persistent grids (148 x k) measured slower here: DESIGN.md 8
+    TileParam grid = P("grid", {0});  // > 0 (balanced row blocks / persistent TMA ring) measured slower: DESIGN.md 3
     grid.persist = true;
     lm.thread = ln.thread = wm.thread = wn.thread = true;
     lm.warp = ln.warp = true;

@@ -9,36 +9,22 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 CFGS = [
-    # long contiguous column segments (512 B per warp) with many loads in flight
-    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=32, warps_m=1, warps_n=8, split=8, unroll=16),
-    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=32, warps_m=1, warps_n=16, split=8, unroll=8),
-    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=32, warps_m=1, warps_n=32, split=8, unroll=4),
-    dict(staging="DIRECT", cache="STREAM", vec=4, lanes_m=32, warps_m=1, warps_n=16, split=8, unroll=16),
-    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=16, warps_m=1, warps_n=16, split=8, unroll=16),
-    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=8, warps_m=1, warps_n=8, split=8, unroll=16),
-    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=8, warps_m=1, warps_n=16, split=8, unroll=8),
-    dict(staging="TMA", cache="L2", vec=4, lanes_m=32, warps_m=1, warps_n=8, split=8, bk=64, stages=4),
-    dict(staging="TMA", cache="L2", vec=4, lanes_m=32, warps_m=1, warps_n=4, split=8, bk=128, stages=4),
-    dict(staging="TMA", cache="L2", vec=4, lanes_m=32, warps_m=2, warps_n=4, split=8, bk=64, stages=3),
-    dict(staging="CP_ASYNC", cache="L2", vec=4, lanes_m=32, warps_m=1, warps_n=8, split=8, bk=64, stages=4),
-    # the r16 search's best (DIRECT, 256 CTAs of 1024 threads, cluster split 8)
+    # the r16-r22 searches' best (DIRECT, one-tile-per-CTA)
+    dict(staging="DIRECT", cache="NONE", vec=2, lanes_m=8, warps_m=1, warps_n=32, split=1, unroll=8),
     dict(staging="DIRECT", cache="L1", xreduce="SHARED", vec=4, lanes_m=16, warps_m=2, warps_n=16, split=8, unroll=2),
-    # persistent TMA rings: 37 clusters x 7 row blocks of 16 rows (grid sized to the SMs)
-    dict(staging="TMA", cache="L2", vec=4, lanes_m=4, warps_m=1, warps_n=8, split=4, bk=128, stages=8, grid=148),
-    dict(staging="TMA", cache="L2", vec=4, lanes_m=4, warps_m=1, warps_n=16, split=4, bk=128, stages=8, grid=148),
-    dict(staging="TMA", cache="L2", vec=4, lanes_m=4, warps_m=1, warps_n=8, split=8, bk=128, stages=4, grid=296),
-    dict(staging="TMA", cache="L2", vec=4, lanes_m=4, warps_m=1, warps_n=8, split=4, bk=256, stages=6, grid=148),
-    dict(staging="TMA", cache="L2", vec=4, lanes_m=4, warps_m=1, warps_n=4, split=4, bk=64, stages=8, grid=148),
-    dict(staging="TMA", cache="L2", vec=4, lanes_m=8, warps_m=1, warps_n=8, split=4, bk=128, stages=6, grid=148),
-    dict(staging="TMA", cache="L2", vec=4, lanes_m=4, warps_m=1, warps_n=8, split=4, bk=128, stages=4, grid=296),
-    # persistent direct loads: 37 clusters x 7 row blocks of 16 rows
-    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=4, warps_m=1, warps_n=16, split=8, unroll=4, grid=296),
-    dict(staging="DIRECT", cache="L1", vec=4, lanes_m=4, warps_m=1, warps_n=16, split=8, unroll=4, grid=296),
-    dict(staging="DIRECT", cache="STREAM", vec=4, lanes_m=4, warps_m=1, warps_n=16, split=8, unroll=4, grid=296),
-    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=4, warps_m=1, warps_n=32, split=4, unroll=4, grid=148),
-    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=4, warps_m=1, warps_n=8, split=8, unroll=8, grid=296),
-    dict(staging="DIRECT", cache="NONE", vec=2, lanes_m=8, warps_m=1, warps_n=16, split=8, unroll=8, grid=296),
-    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=4, warps_m=1, warps_n=32, split=8, unroll=2, grid=296),
+    # balanced row blocks: 37 clusters (x 8 or x 4) of ceil(4096 / 37) -> 112 rows
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=32, warps_m=1, warps_n=32, split=8, unroll=4, grid=296),
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=32, warps_m=1, warps_n=32, split=8, unroll=8, grid=296),
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=32, warps_m=1, warps_n=32, split=8, unroll=16, grid=296),
+    dict(staging="DIRECT", cache="STREAM", vec=4, lanes_m=32, warps_m=1, warps_n=32, split=8, unroll=8, grid=296),
+    dict(staging="DIRECT", cache="L1", vec=4, lanes_m=32, warps_m=1, warps_n=32, split=8, unroll=8, grid=296),
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=32, warps_m=1, warps_n=16, split=8, unroll=8, grid=296),
+    dict(staging="DIRECT", cache="NONE", vec=2, lanes_m=32, warps_m=2, warps_n=16, split=8, unroll=8, grid=296),
+    dict(staging="DIRECT", cache="NONE", vec=1, lanes_m=32, warps_m=4, warps_n=8, split=8, unroll=16, grid=296),
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=32, warps_m=1, warps_n=32, split=4, unroll=8, grid=148),
+    dict(staging="DIRECT", cache="NONE", vec=4, lanes_m=32, warps_m=1, warps_n=32, split=4, unroll=16, grid=148),
+    dict(staging="DIRECT", cache="NONE", vec=2, lanes_m=32, warps_m=1, warps_n=32, split=8, unroll=8, grid=592),
+    dict(staging="DIRECT", cache="NONE", vec=2, lanes_m=32, warps_m=1, warps_n=16, split=8, unroll=8, grid=592),
 ]
 
 
