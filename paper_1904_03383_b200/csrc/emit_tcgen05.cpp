@@ -442,8 +442,11 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   if (M > (int64_t(1) << 31) || K > (int64_t(1) << 31) || N > (int64_t(1) << 31))
     illegal("shape too large for the tensor maps");
   const int a_cols = X3 ? 64 : 32;
-  const int need_cols = 2 * BN + S * a_cols;
-  if (need_cols > 512) illegal("two accumulators + A slots exceed 512 TMEM columns");
+  // two accumulator buffers when they fit beside the A slots, else one (the
+  // MMA of tile i + 1 then waits for the epilogue of tile i)
+  const int NB = 2 * BN + S * a_cols <= 512 ? 2 : 1;
+  const int need_cols = NB * BN + S * a_cols;
+  if (need_cols > 512) illegal("accumulator + A slots exceed 512 TMEM columns");
   int tcols = 32;
   while (tcols < need_cols) tcols *= 2;
   const int64_t a_bytes = 128 * 32 * 4, b_bytes = int64_t(BNL) * 32 * 4;
@@ -456,6 +459,13 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   if (smem > 232448) illegal("TMA ring exceeds 227 KiB of shared memory");
   const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(UM >> 4) << 24);
   const int64_t KB = K / 32, MB = M / UM, TILES = MB * (N / BN / (QUAD ? 2 : 1));  // QUAD: tile pairs
+  // tail split: when the last round of full tiles would leave most clusters
+  // idle, its tiles are cut in half along n (UMMA N = BN / 2) and spread over
+  // twice as many clusters
+  const int64_t NCL = c.grid / CL, RFULL = TILES / NCL, REM = TILES - RFULL * NCL;
+  const bool TS = !QUAD && BN == 256 && REM > 0 && 2 * REM <= NCL;
+  const unsigned idesc_half =
+      (1u << 4) | (2u << 7) | (2u << 10) | (unsigned((BN / 2) >> 3) << 17) | (unsigned(UM >> 4) << 24);
   const unsigned FULL = 0, EMPTY = 8u * S, CONV = 16u * S, AFULL = 24u * S, AEMPTY = 24u * S + 16;
   const char* cg = PAIR == 2 ? "2" : "1";
   const char* mma = PAIR == 2 ? "ispc_mma_tf32_ts_pair" : "ispc_mma_tf32_ts";
@@ -484,7 +494,28 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   o << "  const int cl = blockIdx.x / " << CL << ", ncl = gridDim.x / " << CL << ";\n";
   o << "  const unsigned prank = rank & 1u, lead = rank & ~1u, sub = rank >> 1;  // rank in the pair, its leader, the pair\n";
   o << "  const unsigned short pair_mask = (unsigned short)(3u << (2u * sub));\n";
-  o << "  const int my_tiles = cl < " << TILES << " ? (" << TILES - 1 << " - cl) / ncl + 1 : 0;\n";
+  if (TS) {
+    o << "  const int my_tiles = " << RFULL << " + (cl < " << 2 * REM << " ? 1 : 0);\n";
+  } else {
+    o << "  const int my_tiles = cl < " << TILES << " ? (" << TILES - 1 << " - cl) / ncl + 1 : 0;\n";
+  }
+  // tile i of this cluster -> (m block, first column, width)
+  o << "  auto tile_of = [&](int i, int& m_blk, int& n_off, int& width) {\n";
+  if (TS) {
+    o << "    if (i >= " << RFULL << ") {\n";
+    o << "      const int t = " << RFULL * NCL << " + cl / 2;\n";
+    o << "      m_blk = t % " << MB << ";\n";
+    o << "      n_off = (t / " << MB << ") * " << BN << " + (cl & 1) * " << BN / 2 << ";\n";
+    o << "      width = " << BN / 2 << ";\n";
+    o << "      return;\n";
+    o << "    }\n";
+  }
+  o << "    const int t = cl + i * ncl;\n";
+  o << "    m_blk = t % " << MB << ";\n";
+  o << "    n_off = " << (QUAD ? "((t / " + std::to_string(MB) + ") * 2 + sub)" : "(t / " + std::to_string(MB) + ")") << " * "
+    << BN << ";\n";
+  o << "    width = " << BN << ";\n";
+  o << "  };\n";
   o << "  unsigned char* gen = ispc_smem_raw + (base - raw);\n";
   o << "  unsigned* tmem_slot = (unsigned*)(gen + " << bar_off + nbar * 8 << ");\n";
   o << "  if (threadIdx.x == 0) {\n";
@@ -514,7 +545,8 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   o << "  if (warp == 0 && lane == 0) {\n";
   o << "    int g = 0;\n";
   o << "    for (int i = 0; i < my_tiles; ++i) {\n";
-  o << "      const int t = cl + i * ncl, m_blk = t % " << MB << ", n_blk = " << (QUAD ? "(t / " + std::to_string(MB) + ") * 2 + sub" : "t / " + std::to_string(MB)) << ";\n";
+  o << "      int m_blk, n_off, width;\n";
+  o << "      tile_of(i, m_blk, n_off, width);\n";
   o << "      const int m_base = m_blk * " << UM << " + prank * 128;\n";
   o << "      for (int kb = 0; kb < " << KB << "; ++kb, ++g) {\n";
   o << "        const int s = g % " << S << ";\n";
@@ -531,15 +563,20 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
     o << "        #pragma unroll\n";
     o << "        for (int q = 0; q < 4; ++q) ispc_tma_2d(sa + q * 4096u, &tm_a, m_base + q * 32, kb * 32, full);\n";
   }
-  o << "        ispc_tma_2d(sa + " << off_b << "u, &tm_b, kb * 32, n_blk * " << BN << " + prank * " << BNL
-    << ", full);\n";
+  // the box always holds BN / PAIR rows; a half-width tile uses its first half
+  o << "        ispc_tma_2d(sa + " << off_b << "u, &tm_b, kb * 32, n_off + prank * (width / " << PAIR
+    << "), full);\n";
   o << "      }\n    }\n";
   o << "  } else if (warp == 1 && lane == 0 && prank == 0) {\n";
   // MMA issuer
   o << "    int g = 0;\n";
   o << "    for (int i = 0; i < my_tiles; ++i) {\n";
-  o << "      const int ab = i & 1;\n";
-  o << "      if (i >= 2) ispc_mbar_wait(bars + " << AEMPTY << "u + 8u * ab, ((i >> 1) + 1) & 1);\n";
+  o << "      const int ab = i % " << NB << ";\n";
+  o << "      int m_blk, n_off, width;\n";
+  o << "      tile_of(i, m_blk, n_off, width);\n";
+  o << "      const unsigned idesc = width == " << BN << " ? " << idesc << "u : " << idesc_half << "u;\n";
+  o << "      if (i >= " << NB << ") ispc_mbar_wait(bars + " << AEMPTY << "u + 8u * ab, ((i / " << NB
+    << ") + 1) & 1);\n";
   o << "      asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
   o << "      const unsigned acc = tmem + ab * " << BN << "u;\n";
   o << "      for (int kb = 0; kb < " << KB << "; ++kb, ++g) {\n";
@@ -547,7 +584,7 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   o << "        ispc_mbar_wait(bars + " << CONV << "u + 8u * s, (g / " << S << ") & 1);\n";
   o << "        asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
   o << "        const unsigned sb = base + s * " << stage << "u + " << off_b << "u;\n";
-  o << "        const unsigned ta = tmem + " << 2 * BN << "u + s * " << a_cols << "u;\n";
+  o << "        const unsigned ta = tmem + " << NB * BN << "u + s * " << a_cols << "u;\n";
   o << "        #pragma unroll\n";
   o << "        for (int kk = 0; kk < 4; ++kk) {\n";
   o << "          const unsigned long long db = ispc_umma_desc(sb + kk * 32u, 16u, 1024u);\n";
@@ -574,7 +611,8 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   o << "    float v[16];\n";
   o << "    int g = 0;\n";
   o << "    for (int i = 0; i < my_tiles; ++i) {\n";
-  o << "      const int t = cl + i * ncl, m_blk = t % " << MB << ";\n";
+  o << "      int m_blk, n_off, width;\n";
+  o << "      tile_of(i, m_blk, n_off, width);\n";
   o << "      const int m_base = m_blk * " << UM << " + prank * 128;\n";
   if (!A_TMA) {
     o << "      const float* pa = g_a + m_base + m + (long long)kh * 16 * " << M << "LL;\n";
@@ -593,7 +631,7 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
     o << "          v[q] = *(const float*)(st + src_row + (k >> 3) * 1024u + (k & 7) * 128u + ((((m & 31) >> 2) ^ (k & 7)) << 4));\n";
     o << "        }\n";
   }
-  o << "        const unsigned ta = tmem + trow + " << 2 * BN << "u + s * " << a_cols << "u + kh * 16u;\n";
+  o << "        const unsigned ta = tmem + trow + " << NB * BN << "u + s * " << a_cols << "u + kh * 16u;\n";
   if (X3) {
     o << "        float lo[16];\n";
     o << "        #pragma unroll\n";
@@ -633,13 +671,15 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   // epilogue warps: lane group = warp % 4
   o << "    const int lg = warp & 3;\n";
   o << "    for (int i = 0; i < my_tiles; ++i) {\n";
-  o << "      const int t = cl + i * ncl, m_blk = t % " << MB << ", n_blk = " << (QUAD ? "(t / " + std::to_string(MB) + ") * 2 + sub" : "t / " + std::to_string(MB)) << ", ab = i & 1;\n";
-  o << "      ispc_mbar_wait(bars + " << AFULL << "u + 8u * ab, (i >> 1) & 1);\n";
+  o << "      int m_blk, n_off, width;\n";
+  o << "      tile_of(i, m_blk, n_off, width);\n";
+  o << "      const int ab = i % " << NB << ";\n";
+  o << "      ispc_mbar_wait(bars + " << AFULL << "u + 8u * ab, (i / " << NB << ") & 1);\n";
   o << "      asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
   o << "      const long long row = (long long)m_blk * " << UM << " + prank * 128 + lg * 32 + lane;\n";
-  o << "      float* pc = g_c + row + (long long)n_blk * " << BN << " * " << M << "LL;\n";
+  o << "      float* pc = g_c + row + (long long)n_off * " << M << "LL;\n";
   o << "      #pragma unroll 1\n";
-  o << "      for (int c0 = 0; c0 < " << BN << "; c0 += 32) {\n";
+  o << "      for (int c0 = 0; c0 < width; c0 += 32) {\n";
   o << "        unsigned r[32];\n";
   o << "        ISPC_TMEM_LD32(tmem + ((unsigned)(lg * 32) << 16) + ab * " << BN << "u + c0, r);\n";
   o << "        asm volatile(\"tcgen05.wait::ld.sync.aligned;\" ::: \"memory\");\n";

@@ -293,3 +293,24 @@ def test_search_policy_knobs(monkeypatch, capsys, knobs):
     out = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
     assert out["evaluations"] >= 1 and out["ok"] >= 1
     assert out["bound_violations"] == 0
+
+
+@pytest.mark.parametrize("engine", ["TF32", "TF32X3"])
+@pytest.mark.parametrize("pair", ["1", "2"])
+def test_tcgen05_persistent_tail_split(dev, engine, pair):
+    """BN 256 persistent grid with one accumulator: the last, partial round of
+    tiles is cut into half-width tiles (UMMA N = 128) spread over twice as many
+    clusters (160 / 320 tiles over 74 / 148 clusters)."""
+    space = Space("sgemm_tc", m=4096, n=2560, k=64)
+    dev.bind(space.problem())
+    c = space.root()
+    c.decide("engine", ["kernel"], engine).decide("staging", ["kernel"], "TMA")
+    stages = "2" if engine == "TF32X3" else "3"  # 3xTF32 stages carry B big + small
+    c.decide("tile", ["split"], pair).decide("tile", ["bn"], "256").decide("tile", ["stages"], stages)
+    c.decide("tile", ["grid"], "148")
+    t = c.first_leaf().tiles()
+    from paper_1904_03383_b200 import tile_cuda
+    src, _ = tile_cuda(t, "k_ts")
+    assert "width = 128" in src  # the tail split is emitted
+    m = dev.evaluate_tiles(t, reps=2, warmup=1)
+    assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
