@@ -391,7 +391,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--per-step", type=int, default=96, help="candidates evaluated per step")
+    ap.add_argument("--per-step", type=int, default=128, help="candidates evaluated per step")
     ap.add_argument("--batch", type=int, default=8, help="kernels per NVRTC program")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
