@@ -13,7 +13,11 @@
 //   split    thread-block cluster of `split` CTAs splitting the reduction axis,
 //            partial sums combined through distributed shared memory
 //   staging  SHARED: ld.global -> st.shared (stages 2: register prefetch of
-//            the next k tile); CP_ASYNC: cp.async ring of `stages` tiles
+//            the next k tile); CP_ASYNC: cp.async ring of `stages` tiles;
+//            TMA (gemv): cp.async.bulk.tensor ring with full/empty mbarriers
+//   grid     0: one tile per CTA; > 0: gemv balanced row blocks (DIRECT) or a
+//            persistent TMA ring, tcgen05 persistent grids (emit_tcgen05.cpp);
+//            axpy_stream: grid-stride CTAs
 // The FFMA sgemm / batched kernels keep every output's k order ascending
 // (one fmaf chain per output), so they are bit-identical to the sequential
 // golden kernel; gemv reorders its sum and is checked norm-wise.
