@@ -117,6 +117,7 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
   if (const char* gp = std::getenv("ISPC_GREEDY_P")) greedy_p_ = std::clamp(std::atof(gp), 0.0, 1.0);
   if (const char* lp = std::getenv("ISPC_LEAFB_P")) leafb_p_ = std::clamp(std::atof(lp), 0.0, 1.0);
   if (const char* sh = std::getenv("ISPC_SHARP")) sharp_ = std::max(0.0, std::atof(sh));
+  if (const char* lz = std::getenv("ISPC_LAZY")) lazy_greedy_ = std::atoi(lz) != 0;
   if (const char* q = std::getenv("ISPC_ELITE_Q")) elite_q_ = std::clamp(std::atof(q), 0.0, 1.0);
   if (const char* mu = std::getenv("ISPC_ELITE_MUT")) elite_mut_ = std::max(0.0, std::atof(mu));
   if (const char* r = std::getenv("ISPC_ROLLOUT")) {
@@ -383,6 +384,7 @@ bool Search::descend(std::mt19937_64& rng, Candidate cur, const Candidate* guide
   std::vector<Frame> stack;
   int budget = rollout_mode_ == 0 ? std::numeric_limits<int>::max() : kRolloutExpansions;
   bool cut = false, dead_end = false;
+  double cur_b = -1;  // bound of `cur` when known (the child a lazy greedy draw took)
   for (;;) {
     std::uint32_t inst = order_.pick(ctx, cur);
     const double T = prune ? inc_.seconds() : std::numeric_limits<double>::infinity();
@@ -423,6 +425,35 @@ bool Search::descend(std::mt19937_64& rng, Candidate cur, const Candidate* guide
             continue;
           }
         }
+      }
+      // lazy greedy draw (restart mode): children in random order; the bound
+      // is monotone, so a child whose bound equals the parent's is a minimum
+      // and ends the scan early (most decisions leave the bound unchanged);
+      // otherwise the lowest-bound child seen, ties kept at random
+      if (rollout_mode_ == 0 && prune && greedy_mode_ != 2 && lazy_greedy_ &&
+          double(rng() % 4096) < greedy_p_ * 4096.0) {
+        int vals[kMaxDomainBits], nv = 0;
+        for (int v = 0; v < kMaxDomainBits; ++v)
+          if (mask_has(m, v)) vals[nv++] = v;
+        for (int k = nv - 1; k > 0; --k) std::swap(vals[k], vals[size_t(rng() % uint64_t(k + 1))]);
+        const double b_parent = cur_b >= 0 ? cur_b : bound_total(cur);
+        Candidate best_child;
+        double best_b = std::numeric_limits<double>::infinity();
+        for (int k = 0; k < nv; ++k) {
+          Candidate child;
+          if (apply_decision(ctx, cur, inst, vals[k], child) != PropStatus::Ok) continue;
+          const double b = bound_total(child);
+          if (!std::isfinite(b) || b >= T) {
+            ++pruned_;
+            continue;
+          }
+          if (b < best_b) best_b = b, best_child = std::move(child);
+          if (best_b <= b_parent * (1 + 1e-12)) break;
+        }
+        if (!std::isfinite(best_b)) break;  // dead end: restart
+        cur = std::move(best_child);
+        cur_b = best_b;
+        continue;
       }
       Frame f;
       for (int v = 0; v < kMaxDomainBits; ++v) {
@@ -477,7 +508,9 @@ bool Search::descend(std::mt19937_64& rng, Candidate cur, const Candidate* guide
       // half of the draws follow the bound greedily (the most promising child,
       // lowest b), the other half sample p ~ max(T - b, 0) / 1/b
       size_t choice;
-      if (prune && greedy_mode_ != 2 && double(rng() % 4096) < greedy_p_ * 4096.0) {
+      // (with lazy greedy draws the greedy share was drawn above; this is the sampled rest)
+      const bool lazy_drawn = rollout_mode_ == 0 && lazy_greedy_ && greedy_mode_ != 2;
+      if (prune && greedy_mode_ != 2 && !lazy_drawn && double(rng() % 4096) < greedy_p_ * 4096.0) {
         choice = size_t(std::max_element(f.w.begin(), f.w.end()) - f.w.begin());
         if (greedy_mode_ == 1) {  // uniformly among the children tied at the best weight
           const double top = f.w[choice];
@@ -501,6 +534,7 @@ bool Search::descend(std::mt19937_64& rng, Candidate cur, const Candidate* guide
         choice = pick(rng);
       }
       cur = std::move(f.kids[choice]);
+      cur_b = prune ? f.b[choice] : -1;
       f.kids.erase(f.kids.begin() + long(choice));
       f.w.erase(f.w.begin() + long(choice));
       f.b.erase(f.b.begin() + long(choice));

@@ -157,6 +157,7 @@ class Search {
   // max(T - b, 0) * exp(-gamma (b - b_min) / b_min), b_min the lowest bound
   // among the siblings; 0 = the paper's p ~ max(T - b, 0)
   double sharp_ = 8.0;
+  bool lazy_greedy_ = true;  // ISPC_LAZY=0: greedy draws expand every child
   // elite-guided rollouts (ISPC_ELITE_Q, ISPC_ELITE_MUT): a share q of the
   // rollouts copies the decisions of one of the kElite best measured leaves,
   // deviating at ~mut randomly drawn decisions (local search around the
