@@ -118,6 +118,11 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
   if (const char* lp = std::getenv("ISPC_LEAFB_P")) leafb_p_ = std::clamp(std::atof(lp), 0.0, 1.0);
   if (const char* sh = std::getenv("ISPC_SHARP")) sharp_ = std::max(0.0, std::atof(sh));
   if (const char* lz = std::getenv("ISPC_LAZY")) lazy_greedy_ = std::atoi(lz) != 0;
+  // default: on for the reference's loop-nest spaces (where a leaf's bound
+  // separates fused from unfused schedules), off for the building-block
+  // spaces (whose leaves mostly share one bound)
+  aspire_ = space_->tiles ? 0.0 : 1.5;
+  if (const char* as = std::getenv("ISPC_ASPIRE")) aspire_ = std::max(0.0, std::atof(as));
   if (const char* q = std::getenv("ISPC_ELITE_Q")) elite_q_ = std::clamp(std::atof(q), 0.0, 1.0);
   if (const char* mu = std::getenv("ISPC_ELITE_MUT")) elite_mut_ = std::max(0.0, std::atof(mu));
   if (const char* r = std::getenv("ISPC_ROLLOUT")) {
@@ -587,6 +592,12 @@ void Search::rollout_worker(int tid) {
     double t = now();
     auto w = std::make_unique<Work>();
     bool ok = rollout(rng, w->leaf, w->bound_s, w->path, w->root);
+    if (ok && aspire_ > 0) {
+      double lo = min_leaf_bound_.load();
+      while (w->bound_s < lo && !min_leaf_bound_.compare_exchange_weak(lo, w->bound_s)) {
+      }
+      if (w->bound_s > aspire_ * std::min(lo, w->bound_s)) ok = false;  // outside the aspiration band
+    }
     ++rollouts_;
     if (!ok) {
       ++dead_rollouts_;

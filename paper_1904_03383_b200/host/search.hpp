@@ -21,6 +21,7 @@
 #pragma once
 
 #include <atomic>
+#include <limits>
 #include <condition_variable>
 #include <cstdint>
 #include <deque>
@@ -158,6 +159,11 @@ class Search {
   // among the siblings; 0 = the paper's p ~ max(T - b, 0)
   double sharp_ = 8.0;
   bool lazy_greedy_ = true;  // ISPC_LAZY=0: greedy draws expand every child
+  // ISPC_ASPIRE (kappa, 0 = off; 1.5 by default on loop-nest spaces): a leaf
+  // whose bound exceeds kappa x the lowest leaf bound produced so far is not
+  // evaluated (a heuristic filter on top of the admissible b >= T pruning)
+  double aspire_ = 0.0;
+  std::atomic<double> min_leaf_bound_{std::numeric_limits<double>::infinity()};
   // elite-guided rollouts (ISPC_ELITE_Q, ISPC_ELITE_MUT): a share q of the
   // rollouts copies the decisions of one of the kElite best measured leaves,
   // deviating at ~mut randomly drawn decisions (local search around the

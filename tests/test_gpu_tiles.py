@@ -280,7 +280,7 @@ def test_axpy_stream_full_size_bit_exact(dev):
 
 @pytest.mark.parametrize("knobs", [{"ISPC_ROLLOUT": "deep"}, {"ISPC_ROLLOUT": "ancestor"},
                                    {"ISPC_ELITE_Q": "0.5"}, {"ISPC_GREEDY_P": "0.5", "ISPC_SHARP": "0"},
-                                   {"ISPC_LAZY": "0"}])
+                                   {"ISPC_LAZY": "0"}, {"ISPC_ASPIRE": "0"}])
 def test_search_policy_knobs(monkeypatch, capsys, knobs):
     """Every rollout policy the experiments in DESIGN.md section 5 compare
     runs a search to measured, correct kernels with an admissible bound."""
