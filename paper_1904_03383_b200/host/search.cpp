@@ -295,7 +295,7 @@ bool Search::rollout(std::mt19937_64& rng, Candidate& leaf, double& leaf_bound,
   }
   int depth = 0;
   while (node && depth < tree_depth_) {
-    const double T = prune ? inc_.seconds() : std::numeric_limits<double>::infinity();
+    const double T = prune ? prune_threshold() : std::numeric_limits<double>::infinity();
     if (!node->expanded) {
       // expand outside the lock (propagation dominates), install under it
       std::uint32_t inst = order_.pick(ctx, node->cand);
@@ -392,7 +392,7 @@ bool Search::descend(std::mt19937_64& rng, Candidate cur, const Candidate* guide
   double cur_b = -1;  // bound of `cur` when known (the child a lazy greedy draw took)
   for (;;) {
     std::uint32_t inst = order_.pick(ctx, cur);
-    const double T = prune ? inc_.seconds() : std::numeric_limits<double>::infinity();
+    const double T = prune ? prune_threshold() : std::numeric_limits<double>::infinity();
     if (inst == kNoInstance) {
       const uint64_t d = digest(ctx, cur);
       bool fresh;
@@ -552,6 +552,17 @@ bool Search::descend(std::mt19937_64& rng, Candidate cur, const Candidate* guide
     node->dead = true;
   }
   return false;
+}
+
+// Pruning threshold of the rollouts: the incumbent (admissible B&B), and
+// with the aspiration filter also kappa x the lowest leaf bound produced so
+// far, applied to partial candidates too (their bounds never exceed their
+// leaves'), so descents leave the band as early as the bound shows it. Both
+// terms only fall, so what they prune stays pruned.
+double Search::prune_threshold() const {
+  double T = inc_.seconds();
+  if (aspire_ > 0) T = std::min(T, aspire_ * min_leaf_bound_.load());
+  return T;
 }
 
 void Search::note_elite(double ns, size_t root, const Candidate& leaf) {

@@ -164,6 +164,7 @@ class Search {
   // evaluated (a heuristic filter on top of the admissible b >= T pruning)
   double aspire_ = 0.0;
   std::atomic<double> min_leaf_bound_{std::numeric_limits<double>::infinity()};
+  double prune_threshold() const;
   // elite-guided rollouts (ISPC_ELITE_Q, ISPC_ELITE_MUT): a share q of the
   // rollouts copies the decisions of one of the kElite best measured leaves,
   // deviating at ~mut randomly drawn decisions (local search around the
