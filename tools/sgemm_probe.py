@@ -19,7 +19,8 @@ def main():
     rot = rotation(space, dev.info()["l2_bytes"])
     shapes = [(16, 16, 8, 8), (16, 8, 8, 8), (8, 16, 8, 8), (8, 8, 8, 8), (32, 8, 4, 8), (16, 16, 4, 8),
               (16, 4, 16, 8), (32, 4, 8, 8), (16, 16, 8, 4)]
-    for (tx, ty, tm, tn), bk, st, split, staging in itertools.product(shapes, (8, 16), (2, 3), (1, 2, 4),
+    bks = tuple(int(x) for x in os.environ.get("PROBE_BK", "8,16").split(","))
+    for (tx, ty, tm, tn), bk, st, split, staging in itertools.product(shapes, bks, (2, 3), (1, 2, 4),
                                                                        ("CP_ASYNC", "SHARED")):
         if staging == "SHARED" and st != 2:
             continue
