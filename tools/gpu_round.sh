@@ -13,7 +13,7 @@ fi
 timeout 1500 python bench.py --steps 5 --warmup 3 > $OUT/${TAG}_bench.log 2>&1; echo "bench=$?" >> $OUT/${TAG}_bench.log
 nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/${TAG}_smi_after.csv 2>&1
 # the sharded path end to end: 2 ranks (sharing this one GPU), headline only
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29531 \
+BENCH_NO_SAVE_BEST=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29531 \
   bench.py --gpus 2 --steps 2 --warmup 1 --configs none --no-cpu-baseline > $OUT/${TAG}_bench_2rank.log 2>&1
 echo "bench2=$?" >> $OUT/${TAG}_bench_2rank.log
 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29532 \
