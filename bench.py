@@ -159,7 +159,7 @@ CONFIG_SPACES = {
     # axpy 2^26 on the elementwise streaming building block (the headline
     # searches the reference's own gpu.space for the same computation)
     "axpy_stream": ("axpy_stream", dict(n=1 << 26), 256, False),
-    "gemv": ("gemv", dict(m=4096, n=4096), 2048, True),
+    "gemv": ("gemv", dict(m=4096, n=4096), 4096, True),
     "sgemm": ("sgemm", dict(m=1024, n=1024, k=1024), 4096, False),
     "batched": ("batched", dict(m=32, n=32, k=64, batch=512), 1536, True),
     # the tcgen05 spaces hold ~400 / ~200 runnable leaves (staging x engine x
