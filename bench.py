@@ -201,7 +201,7 @@ def config_worker(args) -> None:
     """One bounded search over one BASELINE shape (a child process, so a
     context-killing fault of one candidate cannot take the others down)."""
     from paper_1904_03383_b200 import Search, Space
-    from paper_1904_03383_b200.measure import cublas_reference, retime_best
+    from paper_1904_03383_b200.measure import cublas_reference, retime_best, rotation
     name = args.config_worker
     kind, kw, evals, flush = CONFIG_SPACES[name]
     kw = dict(kw)
@@ -209,7 +209,16 @@ def config_worker(args) -> None:
         kw["batch"] = kw["batch"] // max(args.batch_div, 1)
     t0 = time.perf_counter()
     space = Space(kind, **kw)
-    s = Search(space, device=args.ordinal, seed=0x1904 + args.ordinal, reps=3, warmup=1, flush_l2=flush)
+    # memory-bound shapes whose inputs fit in L2: each candidate is timed over
+    # rotating input copies (the same method as the reported re-time and
+    # cuBLAS), not after an L2 flush, whose single timed launch carries the
+    # launch latency and hides microsecond differences between candidates
+    rot = 0
+    if flush:
+        import torch
+        rot = rotation(space, torch.cuda.get_device_properties(args.ordinal).L2_cache_size)
+    s = Search(space, device=args.ordinal, seed=0x1904 + args.ordinal, reps=3, warmup=1,
+               flush_l2=flush and rot < 2, rotate=rot)
     done = s.step(evals, max_seconds=4 * args.step_timeout)
     st = s.stats()
     best = s.best()

@@ -151,7 +151,8 @@ typedef struct {
   const char* incumbent_shm;  /* POSIX shm name shared by ranks; NULL: process-local */
   const char* log_path;       /* JSONL evaluation log; NULL: none              */
   int32_t tree_depth;         /* TAG-MCTS tree over the first decisions (0: 12, <0: off) */
-  int32_t _pad;
+  int32_t rotate;             /* > 1: time each candidate over this many input copies
+                                 (ispc_time_opts.rotate) instead of L2 flushes */
 } ispc_search_config;
 
 typedef struct {

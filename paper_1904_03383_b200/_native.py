@@ -172,7 +172,7 @@ class SearchConfig(C.Structure):
                 ("pruning", C.c_int32), ("watchdog", C.c_int32), ("reps", C.c_int32), ("warmup", C.c_int32),
                 ("flush_l2", C.c_int32), ("max_unrolled", C.c_int32), ("budget_factor", C.c_double),
                 ("max_budget_ns", C.c_double), ("decision_order", C.c_char_p), ("incumbent_shm", C.c_char_p),
-                ("log_path", C.c_char_p), ("tree_depth", C.c_int32), ("_pad", C.c_int32)]
+                ("log_path", C.c_char_p), ("tree_depth", C.c_int32), ("rotate", C.c_int32)]
 
 
 class SearchStats(C.Structure):

@@ -809,6 +809,7 @@ void Search::launch_worker() {
       to.warmup = uint32_t(std::max(0, cfg_.warmup));
       to.reps = uint32_t(cfg_.reps);
       to.flush_l2 = uint32_t(cfg_.flush_l2);
+      to.rotate = cfg_.rotate > 1 ? uint32_t(cfg_.rotate) : 0u;
       to.check = 1;
       to.bit_exact = w->bit_exact ? 1 : 0;
       to.rtol = w->rtol;
