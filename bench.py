@@ -101,6 +101,20 @@ def dist_setup():
     return world, rank, local
 
 
+def best_over_ranks(world: int, best_ns: float, best_text: str | None, bound_ns: float,
+                    time_to_best_s: float) -> tuple:
+    """(ns, serialized candidate, bound ns, time to best) of the fastest
+    kernel any rank measured: the incumbent is shared through pinned memory,
+    the candidate that set it lives on one rank (gathered over gloo)."""
+    mine = (best_ns, best_text, bound_ns, time_to_best_s)
+    if world == 1:
+        return mine
+    import torch.distributed as dist
+    every = [None] * world
+    dist.all_gather_object(every, mine)
+    return min(every, key=lambda x: x[0])
+
+
 def allreduce(vals: list[float], op: str, world: int) -> list[float]:
     if world == 1:
         return vals
@@ -326,12 +340,9 @@ def run_ours(args, world, rank, local):
     # shared, the candidate that set it lives on one rank)
     g_best = (st["best_ns"], st["best_bound_ns"], st["time_to_best_s"])
     if world > 1:
-        import torch.distributed as dist
-        mine = (st["best_ns"] if best is not None else float("inf"), best.serialize() if best is not None else None,
-                st["best_bound_ns"], st["time_to_best_s"])
-        every = [None] * world
-        dist.all_gather_object(every, mine)
-        top = min(every, key=lambda x: x[0])
+        top = best_over_ranks(world, st["best_ns"] if best is not None else float("inf"),
+                              best.serialize() if best is not None else None, st["best_bound_ns"],
+                              st["time_to_best_s"])
         if top[1] is not None:
             best = space.deserialize(top[1])
             g_best = (top[0], top[2], top[3])

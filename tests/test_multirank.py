@@ -71,3 +71,32 @@ def test_two_rank_shards_and_shared_incumbent(kind, kw):
         os.unlink("/dev/shm" + shm)
     except OSError:
         pass
+
+
+def _best_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        mine = [(500.0, "slow", 88.0, 3.0), (117.0, "fast", 88.0, 4.5)][rank]
+        q.put((rank, bench.best_over_ranks(world, *mine)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_reports_the_best_kernel_over_ranks():
+    """bench.py's JSON line describes the fastest kernel any shard measured,
+    whichever rank holds its candidate."""
+    port = 29000 + (uuid.uuid4().int % 2000)
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_best_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    got = dict(q.get() for _ in range(2))
+    assert got[0] == got[1] == (117.0, "fast", 88.0, 4.5)
+
