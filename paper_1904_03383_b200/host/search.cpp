@@ -100,9 +100,11 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
     const int ranks = std::atoi(lws);
     if (ranks > 1) hw = std::max(2u, hw / unsigned(ranks));
   }
-  // measured on the B200 boxes (16 cores): propagation-heavy rollouts cost
-  // ~2x the CPU of NVRTC per produced kernel, so they get ~5/8 of the cores
-  if (cfg_.rollout_threads <= 0) cfg_.rollout_threads = int(std::max(1u, hw * 5 / 8));
+  // measured on the B200 boxes (16 cores): propagation-heavy rollouts (most
+  // of them dead ends under the aspiration band) cost ~4-5x the CPU of NVRTC
+  // per produced kernel; 11/16 of the cores measured best (10/16: -12%,
+  // 12/16: -16% candidates/s over 4 seeds each)
+  if (cfg_.rollout_threads <= 0) cfg_.rollout_threads = int(std::max(1u, hw * 11 / 16));
   if (cfg_.compile_threads <= 0) cfg_.compile_threads = int(std::max(1u, hw - unsigned(cfg_.rollout_threads) - 1));
   machine_.l2_flushed = cfg_.flush_l2 != 0;
   machine_.max_unrolled = cfg_.max_unrolled;
