@@ -315,3 +315,28 @@ def test_tcgen05_persistent_tail_split(dev, engine, pair):
     assert "width = 128" in src  # the tail split is emitted
     m = dev.evaluate_tiles(t, reps=2, warmup=1)
     assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
+
+
+@pytest.mark.parametrize("cfg", [
+    # balanced row blocks: 37 clusters of 8 CTAs, 112 rows each
+    dict(staging="DIRECT", vec=4, lanes_m=32, lanes_n=1, warps_m=1, warps_n=16, split=8, unroll=8, grid=296),
+    # persistent TMA ring: 37 clusters of 4 CTAs walking 16-row blocks
+    dict(staging="TMA", vec=4, lanes_m=4, lanes_n=8, warps_m=1, warps_n=8, split=4, bk=128, stages=8, grid=148),
+])
+def test_gemv_grid_variants_through_the_abi(dev, cfg):
+    """The gemv variants kept out of the search space (measured slower) stay
+    correct through ispc_evaluate_tiles (norm-wise 1e-5 of sum |a||x|)."""
+    orc = Oracle()
+    space = Space("gemv", m=4096, n=4096)
+    p = space.problem()
+    dev.bind(p)
+    t = space.root().first_leaf().tiles()
+    t.staging = N.STAGINGS.index(cfg.pop("staging"))
+    for k, v in cfg.items():
+        setattr(t, k, v)
+    m = dev.evaluate_tiles(t, reps=2, warmup=1)
+    assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
+    a, x = orc.fill(4096 * 4096, p.seed, "a"), orc.fill(4096, p.seed, "x")
+    y64, scale = orc.gemv_f64(a, x, 4096, 4096)
+    y = dev.read("y", 4096).astype(np.float64)
+    assert np.max(np.abs(y - y64) / np.maximum(scale, 1e-30)) <= 1e-5
