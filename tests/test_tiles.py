@@ -208,3 +208,36 @@ def test_axpy_stream_bit_exact_on_emulator():
         assert np.array_equal(regs["z"].view(np.uint32), ref.view(np.uint32)), t.as_dict()
         checked += 1
     assert checked >= 3
+
+
+def test_tcgen05_cluster_and_grid_rules():
+    """Emitter rules of the tensor-core tile: A multicast needs TMA-staged A,
+    a persistent grid must hold whole clusters, and the BN 256 persistent
+    grid splits its partial last round into half-width tiles."""
+    s = Space("sgemm_tc", m=4096, n=4096, k=4096)
+
+    def leaf(**kv):
+        c = s.root().decide("engine", ["kernel"], "TF32")
+        c.decide("staging", ["kernel"], kv.pop("staging", "TMA"))
+        for k, v in kv.items():
+            c.decide("tile", [k], str(v))
+        return c.first_leaf().tiles()
+
+    with pytest.raises(EmitError):
+        tile_cuda(leaf(staging="SHARED", split=4, grid=148, bn=128, stages=2))
+    src, L = tile_cuda(leaf(split=2, bn=256, stages=4, grid=148))
+    assert "width = 128" in src and L.grid_x == 148 and L.cluster[0] == 2  # 256 tiles = 3 x 74 + 34 halves
+    src, L = tile_cuda(leaf(split=2, bn=256, stages=4, grid=128))
+    assert "width = 128" not in src  # 256 tiles = 4 x 64 exactly: no tail
+    t = leaf(split=2, bn=256, stages=4, grid=128)
+    t.grid = 127  # not a whole number of pairs
+    with pytest.raises(EmitError):
+        tile_cuda(t)
+
+
+def test_gemv_grid_requires_a_streaming_staging():
+    t = Space("gemv", m=4096, n=4096).root().first_leaf().tiles()
+    t.staging = N.STAGINGS.index("CP_ASYNC")
+    t.bk, t.stages, t.grid = 64, 2, 296
+    with pytest.raises(EmitError):
+        tile_cuda(t)
