@@ -159,7 +159,8 @@ def run_reference(args, world, rank):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "candidates/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "evaluator": "reference simulate() (analytic cycles)"},
+        "config": {"workload": WORKLOAD, "evaluator": "reference simulate() (analytic cycles)",
+                   "walk": "seeded uniform first-open descents (oracle/ref_cpu_bench.cpp)"},
         "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": threads, "kind": "reference",
                          "sample": f"{res['leaves']} leaves of seeded uniform descents in {res['seconds']:.1f}s"},
         "e2e": {"value": v, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -273,6 +274,37 @@ def run_configs(kinds, args, local, world, rank) -> dict:
     return out
 
 
+def run_uniform(space, local, rank, world, args) -> dict:
+    """Our evaluator on the reference baseline's walk: seeded uniform
+    first-open descents from the root (oracle/ref_cpu_bench.cpp's), every
+    leaf emitted, compiled, launched, timed and checked; the same candidates
+    the `--impl reference` arm evaluates with simulate()."""
+    from paper_1904_03383_b200 import Search
+    # no uniform leaf may hold the device for long: a schedule still running
+    # after 10 ms is recorded as a timeout (the budget before any incumbent)
+    s = Search(space, device=local, seed=0x190403383, shard_index=rank, shard_count=world, reps=3, warmup=1,
+               batch=args.batch, walk="uniform", max_budget_ns=10e6)
+    safe_step(s, max(8, args.uniform_evals // 4), args.step_timeout)  # warm-up (pipeline fill)
+    barrier(world)
+    ev0 = s.stats()["evaluations"]
+    t0 = time.perf_counter()
+    ok = safe_step(s, args.uniform_evals, args.step_timeout * 2)
+    wall = time.perf_counter() - t0
+    st = s.stats()
+    s.close()
+    n = st["evaluations"] - ev0
+    dev_s = max(st["device_step_ms"] * 1e-3, 1e-9)
+    (dev_max,) = allreduce([dev_s], "max", world)
+    (n_tot,) = allreduce([float(n)], "sum", world)
+    return {"value": round(n_tot / dev_max, 2), "unit": "candidates/s", "wall_rate": round(n / wall, 2),
+            "evaluated": n, "completed": ok,
+            "walk": "seeded uniform first-open descents (the reference arm's walk)",
+            "stats": {k: st[k] for k in ("ok", "timeouts", "mismatches", "launch_errors", "illegal", "duplicates",
+                                         "rollouts", "dead_rollouts", "bound_violations", "t_rollout_s",
+                                         "t_compile_s", "refined")},
+            "best_us": round(st["best_ns"] / 1e3, 3) if st["best_ns"] < float("inf") else None}
+
+
 def run_ours(args, world, rank, local):
     import numpy as np
     import torch
@@ -287,6 +319,7 @@ def run_ours(args, world, rank, local):
         os.path.join(ROOT, "gpurun_out")) else None
     search = Search(space, device=local, seed=0x1904 + rank, shard_index=rank, shard_count=world,
                     reps=3, warmup=1, batch=args.batch, incumbent_shm=shm, log_path=log)
+    busy_ms = []
     E = args.per_step
     stalled = 0
     for _ in range(args.warmup):
@@ -301,11 +334,15 @@ def run_ours(args, world, rank, local):
     with Clocks(local) as clk:
         for _ in range(args.steps):
             stalled += not safe_step(search, E, args.step_timeout)
-            dev_ms.append(search.stats()["device_step_ms"])
+            st_k = search.stats()
+            dev_ms.append(st_k["device_step_ms"])
+            busy_ms.append(st_k["device_busy_ms"])
     wall = time.perf_counter() - t_wall
     torch.cuda.synchronize()
     barrier(world)
-    evals_here = search.stats()["evaluations"] - ev0
+    st_t = search.stats()
+    evals_here = st_t["evaluations"] - ev0
+    refined_here = st_t["refined"]
     dev_s = max(sum(dev_ms) * 1e-3, 1e-9)
     (dev_s_max,) = allreduce([dev_s], "max", world)
     (evals_total,) = allreduce([float(evals_here)], "sum", world)
@@ -336,6 +373,9 @@ def run_ours(args, world, rank, local):
     best_src = search.best_source()
     search_error = N_error(search)
     search.close()
+    uniform = None
+    if args.uniform_evals > 0:
+        uniform = run_uniform(space, local, rank, world, args)
     # the job's best kernel is the best over all shards (the incumbent is
     # shared, the candidate that set it lives on one rank)
     g_best = (st["best_ns"], st["best_bound_ns"], st["time_to_best_s"])
@@ -385,7 +425,9 @@ def run_ours(args, world, rank, local):
             cpu = {"value": res["leaves_per_s"], "unit": "candidates/s", "cores": res["threads"],
                    "kind": "reference",
                    "sample": f"reference CPU search+simulate: {res['leaves']} leaves in {res['seconds']:.1f}s"}
-    per_eval_launches = 1 + 1 + 3 + 1  # checked launch, warmup, reps, compare kernel
+    # per evaluation: ispc_arm + the kernel + the check kernel; per re-timed
+    # one: (warmup + reps) x (ispc_arm + kernel + flag collect)
+    gpu_launches = int(evals_total * 3 + refined_here * (1 + 3) * 3)
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "candidates/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dev_s_max / args.steps * 1e3, 2),
@@ -397,7 +439,7 @@ def run_ours(args, world, rank, local):
                 "h2d_bytes_per_step": 2 * 4 * N_AXPY, "d2h_bytes_per_step": 4 * N_AXPY},
         "roofline": roofline,
         "cpu_baseline": cpu,
-        "gpu_launches": int(evals_total * per_eval_launches),
+        "gpu_launches": gpu_launches,
         "clocks": clk.summary(),
         "best_kernel": best_info,
         "cublas_axpy": cub,
@@ -405,11 +447,18 @@ def run_ours(args, world, rank, local):
         "search": {k: st[k] for k in ("evaluations", "ok", "mismatches", "timeouts", "launch_errors", "illegal",
                                       "compile_errors", "duplicates", "rollouts", "dead_rollouts",
                                       "pruned_children", "bound_violations", "frontier", "t_rollout_s",
-                                      "t_compile_s", "t_gpu_s")},
+                                      "t_compile_s", "t_gpu_s", "refined", "t_launch_host_s")},
+        "device": {"busy_ms_timed": round(sum(busy_ms), 3), "step_ms_timed": round(sum(dev_ms), 3),
+                   "busy_frac": round(sum(busy_ms) / max(sum(dev_ms), 1e-9), 4),
+                   "note": "busy = the timed kernel launches' own event time; the rest of the device "
+                           "timeline is fills, checks, arm kernels and host gaps"},
+        "uniform_walk": uniform,
         "wall_s": round(wall, 3),
         "stalled_steps": stalled,
         "search_error": search_error,
     }
+    if uniform and cpu:
+        uniform["vs_reference_cpu"] = round(uniform["value"] / cpu["value"], 5)
     print(json.dumps(line))
     if os.path.isdir(os.path.join(ROOT, "gpurun_out")) and best_src:
         with open(os.path.join(ROOT, "gpurun_out", "best_axpy_kernel.cu"), "w") as f:
@@ -430,6 +479,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--configs", default="all", help="all | none | comma list of gemv,sgemm,batched,sgemm_tc")
     ap.add_argument("--step-timeout", type=float, default=60.0, help="wall seconds a search step may take")
+    ap.add_argument("--uniform-evals", type=int, default=128,
+                    help="kernels measured on the reference's uniform walk (0: skip)")
     ap.add_argument("--config-worker", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--ordinal", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--batch-div", type=int, default=1, help=argparse.SUPPRESS)

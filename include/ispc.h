@@ -336,6 +336,8 @@ int ispc_bind_problem(ispc_dev* d, const ispc_problem* p);
 /* Region pointer / size of the bound problem by region name ("x", "c", ...). */
 int ispc_problem_region(ispc_dev* d, const char* name, uint64_t* dev_ptr, int64_t* elems);
 
+/* Loading and unloading may be called from any host thread (e.g. compile
+ * threads loading the next module while the device thread launches). */
 int ispc_module_load(ispc_dev* d, const ispc_module* m, int* handle);
 int ispc_module_unload(ispc_dev* d, int handle);
 
@@ -355,7 +357,9 @@ typedef struct {
                              in aggregate), mean per launch; else one launch
                              per event pair                                   */
   double rtol;            /* relative tolerance when !bit_exact              */
-  double budget_ns;       /* watchdog budget per launch (0: 2 s)             */
+  double budget_ns;       /* watchdog budget per launch (0: 2 s); armed on the
+                             device when the launch starts (a rotation group of
+                             R launches gets R budgets)                       */
 } ispc_time_opts;
 
 typedef struct {
@@ -372,6 +376,23 @@ typedef struct {
  * (NaN-prefilled outputs, GLOBAL temporaries from a scratch pool). */
 int ispc_launch_timed(ispc_dev* d, int handle, const ispc_launch* launch,
                       const ispc_time_opts* opts, ispc_time_result* res);
+
+/* Batched evaluation of several kernels of one loaded module with two host
+ * round trips in all (no per-launch synchronisation):
+ *   screen: per item, NaN-filled outputs, one launch timed by CUDA events with
+ *           its watchdog deadline armed on the device right before it, and the
+ *           on-device check (skipped when the watchdog fired) - every item;
+ *   refine: `warmup` + `reps` timed launches (median; rotation groups as in
+ *           ispc_launch_timed) for the items that passed the check and whose
+ *           screened time is <= refine_below_ns (INFINITY: all of them).
+ * A failure to bind or launch one item is reported in its result's status;
+ * the call fails only for errors of the device (ISPC_E_STICKY, ...). */
+typedef struct {
+  const ispc_launch* launch;
+  ispc_time_opts opts;     /* per item: budget, check / bit_exact / rtol, reps */
+} ispc_batch_item;
+int ispc_launch_batch(ispc_dev* d, int handle, int n, const ispc_batch_item* items,
+                      double refine_below_ns, ispc_time_result* res);
 
 /* Compares the bound outputs with the expected outputs on the device. */
 int ispc_check(ispc_dev* d, double rtol, int bit_exact, double* max_err, int64_t* mismatches,
@@ -393,6 +414,7 @@ int ispc_dev_mark_elapsed(ispc_dev* d, int slot_a, int slot_b, double* ms);
 /* Pins (page-locks, portable across devices) host memory the search shares
  * between GPU workers, e.g. the incumbent bound (cudaHostRegister). */
 int ispc_host_register(void* p, size_t bytes);
+int ispc_host_unregister(void* p);
 
 /* One-shot replacement of evaluate(): emit + compile + load + timed launch +
  * check. The mirror of CostReport is ispc_time_result (time in ns). */

@@ -125,6 +125,7 @@ int ispc_cand_deserialize(const ispc_space* s, const char* text, ispc_cand** out
 typedef struct {
   double total, dram, sm_mem, issue, thread, launch; /* seconds */
   double dram_bytes, blocks_max, threads_per_block_max;
+  double dispatch, l1;      /* seconds: block dispatch floor, L1 lines of scattered warp accesses */
 } ispc_bound_report;
 /* l2_flushed: inputs start outside L2 (the timing flushes L2 between runs). */
 int ispc_bound(const ispc_space* s, const ispc_cand* c, int l2_flushed, ispc_bound_report* out);
@@ -153,7 +154,18 @@ typedef struct {
   int32_t tree_depth;         /* TAG-MCTS tree over the first decisions (0: 12, <0: off) */
   int32_t rotate;             /* > 1: time each candidate over this many input copies
                                  (ispc_time_opts.rotate) instead of L2 flushes */
+  double refine_factor;       /* re-time (warmup + reps) only the kernels whose screened
+                                 first launch is <= factor x incumbent (0: 1.25); the
+                                 others keep their single checked launch's time */
+  int32_t walk;               /* ISPC_WALK_SEARCH (default) or ISPC_WALK_UNIFORM          */
+  int32_t _pad;
 } ispc_search_config;
+
+/* ISPC_WALK_UNIFORM: seeded uniform first-open descents from the root, every
+ * leaf evaluated - the walk of the reference's CPU baseline
+ * (oracle/ref_cpu_bench.cpp), so the two arms measure the same candidates'
+ * evaluation; no bound, incumbent pruning, tree or aspiration band. */
+enum { ISPC_WALK_SEARCH = 0, ISPC_WALK_UNIFORM = 1 };
 
 typedef struct {
   int64_t evaluations;      /* kernels launched on the device                   */
@@ -169,6 +181,10 @@ typedef struct {
   uint64_t best_hash;
   int64_t frontier;         /* subtree roots owned by this shard                */
   int64_t exhausted;        /* 1: no new kernel survives pruning in this shard  */
+  int64_t refined;          /* kernels re-timed after their screening launch    */
+  double device_busy_ms;    /* device time of the timed launches in the last step */
+  double t_launch_host_s;   /* launch thread: host time spent per batch outside the
+                               device waits (binding, enqueue, result processing) */
 } ispc_search_stats;
 
 int ispc_search_create(const ispc_space* s, const ispc_search_config* cfg, ispc_search** out);

@@ -148,6 +148,10 @@ class TimeResult(C.Structure):
                 ("first_ns", C.c_double), ("max_err", C.c_double), ("mismatches", C.c_int64)]
 
 
+class BatchItem(C.Structure):
+    _fields_ = [("launch", C.POINTER(Launch)), ("opts", TimeOpts)]
+
+
 class KernelSpec(C.Structure):
     _fields_ = [("kind", C.c_char_p), ("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64),
                 ("a_stride", C.c_int64), ("num_factors", C.c_int32), ("factor_len", C.c_int32 * 4),
@@ -163,7 +167,7 @@ class SpaceStats(C.Structure):
 
 class BoundReport(C.Structure):
     _fields_ = [(f, C.c_double) for f in ("total", "dram", "sm_mem", "issue", "thread", "launch", "dram_bytes",
-                                          "blocks_max", "threads_per_block_max")]
+                                          "blocks_max", "threads_per_block_max", "dispatch", "l1")]
 
 
 class SearchConfig(C.Structure):
@@ -172,7 +176,10 @@ class SearchConfig(C.Structure):
                 ("pruning", C.c_int32), ("watchdog", C.c_int32), ("reps", C.c_int32), ("warmup", C.c_int32),
                 ("flush_l2", C.c_int32), ("max_unrolled", C.c_int32), ("budget_factor", C.c_double),
                 ("max_budget_ns", C.c_double), ("decision_order", C.c_char_p), ("incumbent_shm", C.c_char_p),
-                ("log_path", C.c_char_p), ("tree_depth", C.c_int32), ("rotate", C.c_int32)]
+                ("log_path", C.c_char_p), ("tree_depth", C.c_int32), ("rotate", C.c_int32),
+                ("refine_factor", C.c_double), ("walk", C.c_int32), ("_pad", C.c_int32)]
+
+WALK_SEARCH, WALK_UNIFORM = 0, 1
 
 
 class SearchStats(C.Structure):
@@ -182,7 +189,8 @@ class SearchStats(C.Structure):
                 + [(f, C.c_double) for f in ("best_ns", "incumbent_ns", "best_bound_ns", "time_to_best_s",
                                              "elapsed_s", "device_step_ms", "t_rollout_s", "t_compile_s",
                                              "t_gpu_s")]
-                + [("best_hash", C.c_uint64), ("frontier", C.c_int64), ("exhausted", C.c_int64)])
+                + [("best_hash", C.c_uint64), ("frontier", C.c_int64), ("exhausted", C.c_int64),
+                   ("refined", C.c_int64), ("device_busy_ms", C.c_double), ("t_launch_host_s", C.c_double)])
 
 
 # Every symbol include/ispc.h declares, with its ctypes signature.
@@ -206,6 +214,8 @@ ISPC_SYMBOLS = {
     "ispc_module_unload": (C.c_int, [C.c_void_p, C.c_int]),
     "ispc_launch_timed": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(Launch), C.POINTER(TimeOpts),
                                     C.POINTER(TimeResult)]),
+    "ispc_launch_batch": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(BatchItem), C.c_double,
+                                    C.POINTER(TimeResult)]),
     "ispc_check": (C.c_int, [C.c_void_p, C.c_double, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                              C.POINTER(C.c_int)]),
     "ispc_read_region": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t]),
@@ -214,6 +224,7 @@ ISPC_SYMBOLS = {
     "ispc_dev_mark": (C.c_int, [C.c_void_p, C.c_int]),
     "ispc_dev_mark_elapsed": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "ispc_host_register": (C.c_int, [C.c_void_p, C.c_size_t]),
+    "ispc_host_unregister": (C.c_int, [C.c_void_p]),
     "ispc_evaluate": (C.c_int, [C.c_void_p, C.POINTER(Nest), C.POINTER(EmitOpts), C.POINTER(TimeOpts),
                                 C.POINTER(TimeResult), C.POINTER(Launch)]),
     "ispc_emit_tiles": (C.c_int, [C.POINTER(TileConfig), C.c_char_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t),

@@ -386,7 +386,7 @@ class Search:
                  reps: int = 3, warmup: int = 1, flush_l2: bool = False, watchdog: int = 1,
                  budget_factor: float = 3.0, max_budget_ns: float = 50e6, max_unrolled: int = 512,
                  decision_order: str | None = None, incumbent_shm: str | None = None, log_path: str | None = None,
-                 tree_depth: int = 0, rotate: int = 0):
+                 tree_depth: int = 0, rotate: int = 0, refine_factor: float = 0.0, walk: str = "search"):
         self.space = space
         self._keep = [x.encode() if x else None for x in (decision_order, incumbent_shm, log_path)]
         cfg = N.SearchConfig(device=device, rollout_threads=rollout_threads, compile_threads=compile_threads,
@@ -395,7 +395,8 @@ class Search:
                              flush_l2=int(flush_l2), max_unrolled=max_unrolled, budget_factor=budget_factor,
                              max_budget_ns=max_budget_ns, decision_order=self._keep[0],
                              incumbent_shm=self._keep[1], log_path=self._keep[2], tree_depth=tree_depth,
-                             rotate=rotate)
+                             rotate=rotate, refine_factor=refine_factor,
+                             walk={"search": N.WALK_SEARCH, "uniform": N.WALK_UNIFORM}[walk])
         h = C.c_void_p()
         if N.host().ispc_search_create(space._h, C.byref(cfg), C.byref(h)) != 0:
             raise RuntimeError(N.host_error())

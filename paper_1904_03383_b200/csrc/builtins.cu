@@ -92,7 +92,7 @@ __global__ void gemv_golden(const float* __restrict__ a, const float* __restrict
 struct CmpOut {
   unsigned long long mismatches;
   unsigned int max_err_bits;  // float bits of the max relative error (>= 0)
-  unsigned int pad;
+  unsigned int timeout;
 };
 
 __global__ void compare_kernel(const float* out, const float* exp, const float* scale, int64_t n, int bit_exact,
@@ -117,6 +117,59 @@ __global__ void compare_kernel(const float* out, const float* exp, const float* 
     if (bad) atomicAdd(&res->mismatches, bad);
     atomicMax(&res->max_err_bits, __float_as_uint(worst));
   }
+}
+
+// The same comparison behind the watchdog flag of the kernel just launched
+// (float4 loads when the element count allows; the arithmetic per element is
+// compare_kernel's).
+__device__ __forceinline__ void cmp_one(float o, float e, float den, int bit_exact, float rtol,
+                                        unsigned long long& bad, float& worst) {
+  den = den > 1e-30f ? den : 1e-30f;
+  float err = fabsf(o - e) / den;
+  if (o != o) err = __int_as_float(0x7f800000);
+  bool diff = bit_exact ? (__float_as_uint(o) != __float_as_uint(e)) : !(err <= rtol);
+  bad += diff;
+  worst = fmaxf(worst, err);
+}
+
+__global__ void check_kernel(const float* out, const float* exp, const float* scale, int64_t n, int bit_exact,
+                             float rtol, const int* timeout_flag, CmpOut* res) {
+  if (timeout_flag && *(volatile const int*)timeout_flag) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) res->timeout = 1;
+    return;
+  }
+  unsigned long long bad = 0;
+  float worst = 0.0f;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int64_t t0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if ((n & 3) == 0 && ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(exp) |
+                        reinterpret_cast<uintptr_t>(scale)) & 15) == 0) {
+    const float4* o4 = reinterpret_cast<const float4*>(out);
+    const float4* e4 = reinterpret_cast<const float4*>(exp);
+    const float4* s4 = reinterpret_cast<const float4*>(scale);
+    for (int64_t i = t0; i < n / 4; i += stride) {
+      float4 o = __ldcs(o4 + i), e = __ldcs(e4 + i);
+      float4 d = scale ? __ldcs(s4 + i) : make_float4(fabsf(e.x), fabsf(e.y), fabsf(e.z), fabsf(e.w));
+      cmp_one(o.x, e.x, d.x, bit_exact, rtol, bad, worst);
+      cmp_one(o.y, e.y, d.y, bit_exact, rtol, bad, worst);
+      cmp_one(o.z, e.z, d.z, bit_exact, rtol, bad, worst);
+      cmp_one(o.w, e.w, d.w, bit_exact, rtol, bad, worst);
+    }
+  } else {
+    for (int64_t i = t0; i < n; i += stride) cmp_one(out[i], exp[i], scale ? scale[i] : fabsf(exp[i]), bit_exact, rtol, bad, worst);
+  }
+  for (int off = 16; off; off >>= 1) {
+    bad += __shfl_xor_sync(0xffffffffu, bad, off);
+    worst = fmaxf(worst, __shfl_xor_sync(0xffffffffu, worst, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (bad) atomicAdd(&res->mismatches, bad);
+    atomicMax(&res->max_err_bits, __float_as_uint(worst));
+  }
+}
+
+__global__ void collect_kernel(const int* timeout_flag, CmpOut* res) {
+  if (*(volatile const int*)timeout_flag) res->timeout = 1;
 }
 
 // Reads the flush buffer after it was written: the written (dirty) lines are
@@ -178,6 +231,19 @@ cudaError_t launch_gemv_golden(const float* a, const float* x, float* y, int64_t
 cudaError_t launch_compare(const float* out, const float* exp, const float* scale, int64_t n, int bit_exact,
                            float rtol, void* dev_res, cudaStream_t s) {
   compare_kernel<<<grid_for(n), 256, 0, s>>>(out, exp, scale, n, bit_exact, rtol, static_cast<CmpOut*>(dev_res));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check(const float* out, const float* exp, const float* scale, int64_t n, int bit_exact,
+                         float rtol, const int* timeout_flag, void* slot, cudaStream_t s) {
+  int64_t g = (n / 4 + 255) / 256;
+  g = g < 1 ? 1 : g > 148 * 8 ? 148 * 8 : g;
+  check_kernel<<<unsigned(g), 256, 0, s>>>(out, exp, scale, n, bit_exact, rtol, timeout_flag, static_cast<CmpOut*>(slot));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_collect(const int* timeout_flag, void* slot, cudaStream_t s) {
+  collect_kernel<<<1, 1, 0, s>>>(timeout_flag, static_cast<CmpOut*>(slot));
   return cudaGetLastError();
 }
 

@@ -508,7 +508,12 @@ class CudaEmitter {
   // --- statements -------------------------------------------------------------------
   std::ostringstream os_;
   int depth_ = 1;
-  static constexpr int64_t kPollWork = 4096;  // instructions between deadline polls
+  // instructions between deadline polls: a serial loop of dependent global
+  // accesses runs ~1 us per instruction, so 4096 overshot the budget by
+  // milliseconds (r2: timeouts measured 0.4-8.7 ms against a 0.35 ms budget);
+  // 128 keeps the overshoot near 0.1 ms, and the poll (a %globaltimer read and
+  // a compare every 128 instructions) is noise next to the loop's own work
+  static constexpr int64_t kPollWork = 128;
   bool watchdog_ = false;
 
   void put(const std::string& s) { os_ << std::string(2 * depth_, ' ') << s << "\n"; }
@@ -737,7 +742,9 @@ class CudaEmitter {
       std::snprintf(P.name, sizeof(P.name), "%s", n.input_names[i]);
     }
     if (watchdog_) {
-      plist.push_back("const unsigned long long ispc_deadline");
+      // absolute %globaltimer deadline, or 0: the one ispc_arm() last set on
+      // the device (so queued launches each get their budget from their start)
+      plist.push_back("const unsigned long long ispc_deadline_arg");
       if (L.num_params >= ISPC_MAX_PARAMS) throw NestError(ISPC_E_ILLEGAL, "too many kernel parameters");
       ispc_param& P = L.params[L.num_params++];
       P.kind = ISPC_PARAM_DEADLINE;
@@ -762,6 +769,7 @@ class CudaEmitter {
     }
     if (watchdog_) {
       bool bar = any_barrier();
+      h << "  const unsigned long long ispc_deadline = ispc_deadline_arg ? ispc_deadline_arg : ispc_deadline_at;\n";
       h << "  if (" << (bar ? "__syncthreads_or(ispc_now() > ispc_deadline)" : "ispc_now() > ispc_deadline")
         << ") { ispc_timeout_flag = 1; return; }\n";
     }
@@ -800,10 +808,17 @@ std::string emit_cuda_kernel(const NestView& v, const ispc_emit_opts& opts, cons
 extern "C" const char* ispc_cuda_prelude(void) {
   return R"(// ispc prelude: device helpers shared by every emitted kernel
 __device__ int ispc_timeout_flag;
+__device__ unsigned long long ispc_deadline_at;
 static __device__ __forceinline__ unsigned long long ispc_now() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+// launched on the stream right before a watchdog kernel: its deadline starts
+// when the device reaches it, not when the host enqueued it
+extern "C" __global__ void ispc_arm(unsigned long long budget_ns) {
+  ispc_deadline_at = ispc_now() + budget_ns;
+  ispc_timeout_flag = 0;
 }
 // building blocks of the tile kernels (emit_tiles.cpp)
 static __device__ __forceinline__ unsigned ispc_smem_addr(const void* p) {

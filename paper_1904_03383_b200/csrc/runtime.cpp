@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -45,6 +46,7 @@ struct Loaded {
   CUmodule mod = nullptr;
   std::unordered_map<std::string, CUfunction> fns;
   CUdeviceptr timeout_flag = 0;
+  CUfunction arm = nullptr;  // ispc_arm of the prelude (device-side watchdog deadline)
 };
 
 
@@ -66,6 +68,10 @@ struct DriverTable {
   decltype(&::cuMemsetD32Async) MemsetD32Async = nullptr;
   decltype(&::cuLaunchKernelEx) LaunchKernelEx = nullptr;
   decltype(&::cuTensorMapEncodeTiled) TensorMapEncodeTiled = nullptr;
+  // optional (eager loading of a module's kernels on the thread that loads it)
+  decltype(&::cuModuleGetFunctionCount) ModuleGetFunctionCount = nullptr;
+  decltype(&::cuModuleEnumerateFunctions) ModuleEnumerateFunctions = nullptr;
+  decltype(&::cuFuncLoad) FuncLoad = nullptr;
 };
 DriverTable drv;
 
@@ -96,6 +102,14 @@ bool resolve_driver(std::string& why) {
     get("cuMemsetD32Async", reinterpret_cast<void**>(&drv.MemsetD32Async));
     get("cuLaunchKernelEx", reinterpret_cast<void**>(&drv.LaunchKernelEx));
     get("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&drv.TensorMapEncodeTiled));
+    auto opt = [](const char* sym, void** fp) {
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(sym, fp, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+        *fp = nullptr;
+    };
+    opt("cuModuleGetFunctionCount", reinterpret_cast<void**>(&drv.ModuleGetFunctionCount));
+    opt("cuModuleEnumerateFunctions", reinterpret_cast<void**>(&drv.ModuleEnumerateFunctions));
+    opt("cuFuncLoad", reinterpret_cast<void**>(&drv.FuncLoad));
   });
   if (!ok) why = "CUDA driver entry points unavailable: " + err;
   return ok;
@@ -134,8 +148,12 @@ struct ispc_dev {
   // rotation copies of the input regions (timing with inputs larger than L2)
   std::vector<std::map<std::string, Buffer>> rot;
 
-  std::map<int, Loaded> modules;
+  std::map<int, Loaded> modules;  // guarded by mod_mu (loads may come from compile threads)
+  std::mutex mod_mu;
   int next_handle = 1;
+  std::vector<cudaEvent_t> evpool;  // timing events of batched launches
+  void* slots = nullptr;            // per-item ispc::CmpResult of batched launches
+  size_t slot_cap = 0;
   cudaEvent_t marks[8] = {};
 };
 
@@ -303,6 +321,8 @@ void ispc_dev_close(ispc_dev* d) {
   cudaStreamSynchronize(d->stream);
   for (auto& [h, m] : d->modules) drv.ModuleUnload(m.mod);
   free_problem(d);
+  for (cudaEvent_t e : d->evpool) cudaEventDestroy(e);
+  if (d->slots) cudaFree(d->slots);
   cudaFree(d->flush);
   cudaFree(d->cmp_res);
   cudaFree(d->timer_buf);
@@ -489,6 +509,18 @@ int ispc_module_load(ispc_dev* d, const ispc_module* m, int* handle) {
   CU(d, drv.ModuleLoadData(&L.mod, m->cubin.data()));
   size_t sz = 0;
   if (drv.ModuleGetGlobal(&L.timeout_flag, &sz, L.mod, "ispc_timeout_flag") != CUDA_SUCCESS) L.timeout_flag = 0;
+  if (drv.ModuleGetFunction(&L.arm, L.mod, "ispc_arm") != CUDA_SUCCESS) L.arm = nullptr;
+  // lazy module loading would upload each kernel at its first launch, on the
+  // launching thread; load them all here (a compile thread, off the device's
+  // critical path) instead
+  unsigned nf = 0;
+  if (drv.ModuleGetFunctionCount && drv.ModuleEnumerateFunctions && drv.FuncLoad &&
+      drv.ModuleGetFunctionCount(&nf, L.mod) == CUDA_SUCCESS && nf > 0) {
+    std::vector<CUfunction> fs(nf);
+    if (drv.ModuleEnumerateFunctions(fs.data(), nf, L.mod) == CUDA_SUCCESS)
+      for (CUfunction f : fs) drv.FuncLoad(f);
+  }
+  std::lock_guard<std::mutex> lk(d->mod_mu);
   *handle = d->next_handle++;
   d->modules[*handle] = std::move(L);
   return ISPC_OK;
@@ -496,11 +528,16 @@ int ispc_module_load(ispc_dev* d, const ispc_module* m, int* handle) {
 
 int ispc_module_unload(ispc_dev* d, int handle) {
   if (!d) return ISPC_E_ARG;
-  auto it = d->modules.find(handle);
-  if (it == d->modules.end()) return fail(d, ISPC_E_ARG, "unknown module handle");
   bind_ctx(d);
-  drv.ModuleUnload(it->second.mod);
-  d->modules.erase(it);
+  CUmodule mod = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(d->mod_mu);
+    auto it = d->modules.find(handle);
+    if (it == d->modules.end()) return fail(d, ISPC_E_ARG, "unknown module handle");
+    mod = it->second.mod;
+    d->modules.erase(it);
+  }
+  drv.ModuleUnload(mod);
   return ISPC_OK;
 }
 
@@ -533,47 +570,76 @@ int ispc_check(ispc_dev* d, double rtol, int bit_exact, double* max_err, int64_t
   return ISPC_OK;
 }
 
-// ---- timed launch -------------------------------------------------------------------
+// ---- timed launches -------------------------------------------------------------------
+//
+// A batch of candidates of one module is evaluated with two host round trips
+// in total, however many kernels it holds:
+//   screen   per item: NaN-fill the outputs, [L2 flush], ispc_arm(budget),
+//            event, the kernel, event, check (skipped on the device when the
+//            watchdog fired) into the item's result slot
+//   refine   per item whose screened time is at most `refine_below_ns` and
+//            whose output checked: warmup launches, then `reps` timed groups
+//            (one launch each, or R back-to-back launches over R input copies),
+//            each group armed with its own budget and its watchdog flag
+//            collected into the item's second slot
+// Everything of a phase is enqueued before the host waits once on its last
+// event; the watchdog deadline of each launch is set on the device by
+// ispc_arm (emitted in every module's prelude) right before the launch, so a
+// kernel queued behind others still gets its whole budget.
 
-int ispc_launch_timed(ispc_dev* d, int handle, const ispc_launch* L, const ispc_time_opts* o,
-                      ispc_time_result* res) {
-  if (!d || !L || !o || !res) return fail(d, ISPC_E_ARG, "null argument");
-  if (!d->bound) return fail(d, ISPC_E_ARG, "no problem bound");
-  std::memset(res, 0, sizeof(*res));
-  int rc = bind_ctx(d);
-  if (rc) return rc;
-  auto mit = d->modules.find(handle);
-  if (mit == d->modules.end()) return fail(d, ISPC_E_ARG, "unknown module handle");
-  Loaded& mod = mit->second;
-  CUfunction fn;
+namespace {
+
+struct Bound {  // one kernel with its parameters bound per rotation copy
+  CUfunction fn = nullptr;
+  const ispc_launch* L = nullptr;
+  uint32_t R = 1;
+  std::vector<std::vector<uint64_t>> stores;     // [copy][param]
+  std::vector<std::vector<CUtensorMap>> tmaps;   // [copy][tmap]
+  std::vector<int> tmap_of;                      // param -> tmap index or -1
+  int deadline_slot = -1;
+  bool clustered = false;
+};
+
+int get_function(ispc_dev* d, Loaded& mod, const ispc_launch* L, CUfunction* out) {
   auto fit = mod.fns.find(L->name);
-  if (fit == mod.fns.end()) {
-    CU(d, drv.ModuleGetFunction(&fn, mod.mod, L->name));
-    if (L->static_smem > 48 * 1024)
-      CU(d, drv.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, int(L->static_smem)));
-    mod.fns[L->name] = fn;
-  } else {
-    fn = fit->second;
+  if (fit != mod.fns.end()) {
+    *out = fit->second;
+    return ISPC_OK;
   }
-  if (L->grid_x == 0 || L->grid_x > 0x7fffffffull) return fail(d, ISPC_E_ILLEGAL, "grid out of range");
+  CUfunction fn;
+  CU(d, drv.ModuleGetFunction(&fn, mod.mod, L->name));
+  if (L->static_smem > 48 * 1024)
+    CU(d, drv.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, int(L->static_smem)));
+  mod.fns[L->name] = fn;
+  *out = fn;
+  return ISPC_OK;
+}
 
-  // rotation copies: R sets of the input regions so that back-to-back timed
-  // launches each read inputs that are not L2 resident (copy 0 = originals)
-  const uint32_t R = std::max<uint32_t>(1, std::min<uint32_t>(o->rotate, 16));
-  if (R > 1 && d->rot.size() + 1 < R) {
-    CK(d, cudaStreamSynchronize(d->stream));
-    while (d->rot.size() + 1 < R) {
-      std::map<std::string, Buffer> copy;
-      for (auto& [name, b] : d->regions) {
-        if (d->expected.count(name)) continue;  // outputs are shared
-        Buffer c;
-        if ((rc = alloc(d, c, b.elems))) return rc;
-        CK(d, cudaMemcpy(c.ptr, b.ptr, size_t(b.elems) * 4, cudaMemcpyDeviceToDevice));
-        copy[name] = c;
-      }
-      d->rot.push_back(std::move(copy));
+int ensure_rotation(ispc_dev* d, uint32_t R) {
+  if (R <= 1 || d->rot.size() + 1 >= R) return ISPC_OK;
+  CK(d, cudaStreamSynchronize(d->stream));
+  while (d->rot.size() + 1 < R) {
+    std::map<std::string, Buffer> copy;
+    for (auto& [name, b] : d->regions) {
+      if (d->expected.count(name)) continue;  // outputs are shared
+      Buffer c;
+      int rc = alloc(d, c, b.elems);
+      if (rc) return rc;
+      CK(d, cudaMemcpy(c.ptr, b.ptr, size_t(b.elems) * 4, cudaMemcpyDeviceToDevice));
+      copy[name] = c;
     }
+    d->rot.push_back(std::move(copy));
   }
+  return ISPC_OK;
+}
+
+int bind_kernel(ispc_dev* d, Loaded& mod, const ispc_launch* L, uint32_t rotate, Bound& B) {
+  int rc = get_function(d, mod, L, &B.fn);
+  if (rc) return rc;
+  if (L->grid_x == 0 || L->grid_x > 0x7fffffffull) return fail(d, ISPC_E_ILLEGAL, "grid out of range");
+  B.L = L;
+  B.R = std::max<uint32_t>(1, std::min<uint32_t>(rotate, 16));
+  if ((rc = ensure_rotation(d, B.R))) return rc;
   auto region_ptr = [&](uint32_t copy, const std::string& name) -> float* {
     if (copy > 0) {
       auto it = d->rot[copy - 1].find(name);
@@ -582,16 +648,12 @@ int ispc_launch_timed(ispc_dev* d, int handle, const ispc_launch* L, const ispc_
     auto it = d->regions.find(name);
     return it == d->regions.end() ? nullptr : it->second.ptr;
   };
-
-  // bind parameters (per copy): problem regions by name, temporaries from scratch
-  std::vector<std::vector<uint64_t>> stores(R, std::vector<uint64_t>(L->num_params, 0));
-  std::vector<std::vector<void*>> argv(R, std::vector<void*>(L->num_params));
-  std::vector<std::vector<CUtensorMap>> tmapv(R, std::vector<CUtensorMap>(L->num_tmaps));
+  B.stores.assign(B.R, std::vector<uint64_t>(L->num_params, 0));
+  B.tmaps.assign(B.R, std::vector<CUtensorMap>(L->num_tmaps));
+  B.tmap_of.assign(L->num_params, -1);
   size_t next_scratch = 0;
-  int deadline_slot = -1;
   for (uint32_t i = 0; i < L->num_params; ++i) {
     const ispc_param& prm = L->params[i];
-    for (uint32_t c = 0; c < R; ++c) argv[c][i] = &stores[c][i];
     if (prm.kind == ISPC_PARAM_REGION) {
       if (prm.is_input) {
         auto it = d->regions.find(prm.name);
@@ -599,22 +661,19 @@ int ispc_launch_timed(ispc_dev* d, int handle, const ispc_launch* L, const ispc_
           return fail(d, ISPC_E_ARG, std::string("kernel region '") + prm.name + "' not in the bound problem");
         if (it->second.elems < prm.elems)
           return fail(d, ISPC_E_ARG, std::string("region '") + prm.name + "' smaller than the kernel's");
-        for (uint32_t c = 0; c < R; ++c) stores[c][i] = reinterpret_cast<uint64_t>(region_ptr(c, prm.name));
+        for (uint32_t c = 0; c < B.R; ++c) B.stores[c][i] = reinterpret_cast<uint64_t>(region_ptr(c, prm.name));
       } else {
-        if (next_scratch == d->scratch.size()) d->scratch.push_back(Buffer{});
+        // sized by grow_scratch() for every kernel of the batch beforehand
+        if (next_scratch >= d->scratch.size() || d->scratch[next_scratch].elems < prm.elems)
+          return fail(d, ISPC_E_ARG, "scratch pool not sized for the batch");
         Buffer& b = d->scratch[next_scratch++];
-        if (b.elems < prm.elems) {
-          cudaFree(b.ptr);
-          b = Buffer{};
-          if ((rc = alloc(d, b, prm.elems))) return rc;
-        }
-        for (uint32_t c = 0; c < R; ++c) stores[c][i] = reinterpret_cast<uint64_t>(b.ptr);
+        for (uint32_t c = 0; c < B.R; ++c) B.stores[c][i] = reinterpret_cast<uint64_t>(b.ptr);
       }
     } else if (prm.kind == ISPC_PARAM_INPUT) {
       if (std::strcmp(prm.name, "alpha") != 0)
         return fail(d, ISPC_E_ARG, std::string("unknown scalar input ") + prm.name);
       float a = d->prob.alpha;
-      for (uint32_t c = 0; c < R; ++c) std::memcpy(&stores[c][i], &a, 4);
+      for (uint32_t c = 0; c < B.R; ++c) std::memcpy(&B.stores[c][i], &a, 4);
     } else if (prm.kind == ISPC_PARAM_TMAP) {
       const ispc_tmap* tm = nullptr;
       uint32_t ti = 0;
@@ -633,133 +692,328 @@ int ispc_launch_timed(ispc_dev* d, int handle, const ispc_launch* L, const ispc_
       cuuint32_t estr[3] = {1, 1, 1};
       static const CUtensorMapSwizzle sw[4] = {CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
                                                CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_SWIZZLE_128B};
-      for (uint32_t c = 0; c < R; ++c) {
-        CU(d, drv.TensorMapEncodeTiled(&tmapv[c][ti], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, tm->rank,
+      for (uint32_t c = 0; c < B.R; ++c)
+        CU(d, drv.TensorMapEncodeTiled(&B.tmaps[c][ti], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, tm->rank,
                                        region_ptr(c, tm->region), dims, strides, box, estr,
                                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw[tm->swizzle & 3],
                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
-        argv[c][i] = &tmapv[c][ti];
-      }
+      B.tmap_of[i] = int(ti);
     } else {
-      deadline_slot = int(i);
+      B.deadline_slot = int(i);
     }
   }
-  const double budget = o->budget_ns > 0 ? o->budget_ns : 2e9;
-  const bool clustered = L->cluster[0] * std::max(1u, L->cluster[1]) * std::max(1u, L->cluster[2]) > 1;
-  if (clustered && L->grid_x % L->cluster[0] != 0) return fail(d, ISPC_E_ILLEGAL, "grid not a multiple of the cluster");
-  unsigned int smem = L->static_smem;
-  auto enqueue = [&](uint32_t copy) -> int {
-    void** args = argv[copy].data();
-    if (clustered) {
-      CUlaunchConfig cfg{};
-      cfg.gridDimX = unsigned(L->grid_x);
-      cfg.gridDimY = cfg.gridDimZ = 1;
-      cfg.blockDimX = L->block[0];
-      cfg.blockDimY = L->block[1];
-      cfg.blockDimZ = L->block[2];
-      cfg.sharedMemBytes = smem;
-      cfg.hStream = reinterpret_cast<CUstream>(d->stream);
-      CUlaunchAttribute attr{};
-      attr.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
-      attr.value.clusterDim.x = L->cluster[0];
-      attr.value.clusterDim.y = std::max(1u, L->cluster[1]);
-      attr.value.clusterDim.z = std::max(1u, L->cluster[2]);
-      cfg.attrs = &attr;
-      cfg.numAttrs = 1;
-      CU(d, drv.LaunchKernelEx(&cfg, fn, args, nullptr));
-    } else {
-      CU(d, drv.LaunchKernel(fn, unsigned(L->grid_x), 1, 1, L->block[0], L->block[1], L->block[2], smem,
-                             reinterpret_cast<CUstream>(d->stream), args, nullptr));
-    }
-    return ISPC_OK;
-  };
-  // times `count` launches cycling through the copies, one event pair
-  auto launch_timed_n = [&](float* ms, bool flush, uint32_t count) -> int {
-    if (flush) {  // write a buffer larger than L2, then read it back (clean L2, no pending write-backs)
-      CK(d, cudaMemsetAsync(d->flush, int(flush_counter_++ & 0xff), d->flush_bytes, d->stream));
-      CK(d, ispc::launch_flush_read(d->flush, d->flush_bytes, d->cmp_res, d->stream));
-    }
-    if (deadline_slot >= 0)
-      for (uint32_t c = 0; c < R; ++c) stores[c][deadline_slot] = uint64_t(host_ns() + d->gt_offset_ns + budget);
-    CK(d, cudaEventRecord(d->ev0, d->stream));
-    for (uint32_t k = 0; k < count; ++k)
-      if ((rc = enqueue(k % R))) return rc;
-    CK(d, cudaEventRecord(d->ev1, d->stream));
-    // host-side guard: a kernel that outlives every device-side watchdog would
-    // wedge the context; report it as a context-killing fault instead of
-    // blocking forever (the device must be reopened, i.e. the process exits)
-    const double t_wait = host_ns();
-    const double limit_ns = std::max(5e9, 40.0 * budget);
-    for (;;) {
-      cudaError_t q = cudaEventQuery(d->ev1);
-      if (q == cudaSuccess) break;
-      if (q != cudaErrorNotReady) return cuda_fail(d, q, "kernel");
-      if (host_ns() - t_wait > limit_ns)
-        return fail(d, ISPC_E_STICKY, std::string("kernel ") + L->name + " still running after " +
-                                          std::to_string(int(limit_ns / 1e9)) + " s (host guard)");
-      std::this_thread::sleep_for(std::chrono::microseconds(20));
-    }
-    CK(d, cudaEventElapsedTime(ms, d->ev0, d->ev1));
-    return ISPC_OK;
-  };
-  auto launch_once = [&](float* ms, bool flush) -> int { return launch_timed_n(ms, flush, 1); };
-  auto timed_out = [&](bool* out) -> int {
-    *out = false;
-    if (!mod.timeout_flag) return ISPC_OK;
-    int flag = 0;
-    CU(d, drv.MemcpyDtoH(&flag, mod.timeout_flag, 4));
-    *out = flag != 0;
-    return ISPC_OK;
-  };
+  B.clustered = L->cluster[0] * std::max(1u, L->cluster[1]) * std::max(1u, L->cluster[2]) > 1;
+  if (B.clustered && L->grid_x % L->cluster[0] != 0) return fail(d, ISPC_E_ILLEGAL, "grid not a multiple of the cluster");
+  return ISPC_OK;
+}
 
-  // first launch: NaN-prefilled outputs, watchdog armed, checked
-  for (const std::string& out : d->outputs) {
-    const Buffer& b = d->regions.at(out);
-    CK(d, cudaMemsetAsync(b.ptr, 0xff, size_t(b.elems) * 4, d->stream));
+// Enqueues one launch over rotation copy `copy`. `deadline`: the absolute
+// deadline parameter (0: the device-armed one).
+int enqueue(ispc_dev* d, Bound& B, uint32_t copy, uint64_t deadline) {
+  const ispc_launch* L = B.L;
+  void* args[ISPC_MAX_PARAMS];
+  for (uint32_t i = 0; i < L->num_params; ++i) {
+    if (int(i) == B.deadline_slot) B.stores[copy][i] = deadline;
+    args[i] = B.tmap_of[i] >= 0 ? static_cast<void*>(&B.tmaps[copy][size_t(B.tmap_of[i])])
+                                : static_cast<void*>(&B.stores[copy][i]);
   }
-  if (mod.timeout_flag) CU(d, drv.MemsetD32Async(mod.timeout_flag, 0, 1, reinterpret_cast<CUstream>(d->stream)));
-  float ms = 0;
-  if ((rc = launch_once(&ms, o->flush_l2 != 0))) return rc;
-  res->first_ns = double(ms) * 1e6;
-  bool late = false;
-  if ((rc = timed_out(&late))) return rc;
-  if (late) {
-    res->status = ISPC_E_TIMEOUT;
-    res->median_ns = res->min_ns = std::max(res->first_ns, budget);
-    return ISPC_OK;
-  }
-  if (o->check) {
-    int ok = 0;
-    if ((rc = ispc_check(d, o->rtol, int(o->bit_exact), &res->max_err, &res->mismatches, &ok))) return rc;
-    if (!ok) {
-      res->status = ISPC_E_MISMATCH;
-      res->median_ns = res->min_ns = res->first_ns;
-      return ISPC_OK;
-    }
-  }
-  for (uint32_t w = 0; w < o->warmup; ++w)
-    if ((rc = launch_once(&ms, o->flush_l2 != 0))) return rc;
-  std::vector<double> times;
-  if (R > 1) {
-    // rotation: batches of R back-to-back launches over the R input copies
-    // (each launch reads inputs untouched for R-1 launches, i.e. not in L2);
-    // the launch overhead is amortised, the per-launch time is the batch mean
-    const uint32_t batches = std::max<uint32_t>(1, (std::max<uint32_t>(o->reps, 1) + R - 1) / R);
-    for (uint32_t b = 0; b < batches; ++b) {
-      if ((rc = launch_timed_n(&ms, false, R))) return rc;
-      times.push_back(double(ms) * 1e6 / R);
-    }
+  if (B.clustered) {
+    CUlaunchConfig cfg{};
+    cfg.gridDimX = unsigned(L->grid_x);
+    cfg.gridDimY = cfg.gridDimZ = 1;
+    cfg.blockDimX = L->block[0];
+    cfg.blockDimY = L->block[1];
+    cfg.blockDimZ = L->block[2];
+    cfg.sharedMemBytes = L->static_smem;
+    cfg.hStream = reinterpret_cast<CUstream>(d->stream);
+    CUlaunchAttribute attr{};
+    attr.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+    attr.value.clusterDim.x = L->cluster[0];
+    attr.value.clusterDim.y = std::max(1u, L->cluster[1]);
+    attr.value.clusterDim.z = std::max(1u, L->cluster[2]);
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    CU(d, drv.LaunchKernelEx(&cfg, B.fn, args, nullptr));
   } else {
-    for (uint32_t r = 0; r < std::max<uint32_t>(o->reps, 1); ++r) {
-      if ((rc = launch_once(&ms, o->flush_l2 != 0))) return rc;
-      times.push_back(double(ms) * 1e6);
+    CU(d, drv.LaunchKernel(B.fn, unsigned(L->grid_x), 1, 1, L->block[0], L->block[1], L->block[2], L->static_smem,
+                           reinterpret_cast<CUstream>(d->stream), args, nullptr));
+  }
+  return ISPC_OK;
+}
+
+// Sets the device deadline `budget_ns` from now (when the stream reaches it)
+// and clears the module's watchdog flag. Without an arm kernel (a module not
+// built from the prelude) the deadline is computed on the host instead.
+int arm(ispc_dev* d, Loaded& mod, double budget_ns, uint64_t* host_deadline) {
+  *host_deadline = 0;
+  if (mod.arm) {
+    unsigned long long b = (unsigned long long)std::max(0.0, budget_ns);
+    void* args[1] = {&b};
+    CU(d, drv.LaunchKernel(mod.arm, 1, 1, 1, 1, 1, 1, 0, reinterpret_cast<CUstream>(d->stream), args, nullptr));
+  } else {
+    if (mod.timeout_flag) CU(d, drv.MemsetD32Async(mod.timeout_flag, 0, 1, reinterpret_cast<CUstream>(d->stream)));
+    *host_deadline = uint64_t(host_ns() + d->gt_offset_ns + budget_ns);
+  }
+  return ISPC_OK;
+}
+
+// GLOBAL temporaries come from a per-device pool: the j-th temporary of every
+// kernel shares buffer j (the kernels of a stream never overlap), sized for
+// the largest j-th temporary of the batch before anything is enqueued.
+int grow_scratch(ispc_dev* d, int n, const ispc_batch_item* items) {
+  std::vector<int64_t> need;
+  for (int i = 0; i < n; ++i) {
+    size_t j = 0;
+    const ispc_launch* L = items[i].launch;
+    for (uint32_t p = 0; p < L->num_params; ++p)
+      if (L->params[p].kind == ISPC_PARAM_REGION && !L->params[p].is_input) {
+        if (need.size() <= j) need.push_back(0);
+        need[j] = std::max(need[j], L->params[p].elems);
+        ++j;
+      }
+  }
+  bool synced = false;
+  for (size_t j = 0; j < need.size(); ++j) {
+    if (j == d->scratch.size()) d->scratch.push_back(Buffer{});
+    Buffer& b = d->scratch[j];
+    if (b.elems >= need[j]) continue;
+    if (!synced) {  // the pool may be in use by kernels still queued
+      CK(d, cudaStreamSynchronize(d->stream));
+      synced = true;
+    }
+    cudaFree(b.ptr);
+    b = Buffer{};
+    int rc = alloc(d, b, need[j]);
+    if (rc) return rc;
+  }
+  return ISPC_OK;
+}
+
+cudaEvent_t event_at(ispc_dev* d, size_t i) {
+  while (d->evpool.size() <= i) {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    d->evpool.push_back(e);
+  }
+  return d->evpool[i];
+}
+
+int slots_for(ispc_dev* d, size_t n) {
+  if (d->slot_cap >= n) return ISPC_OK;
+  CK(d, cudaStreamSynchronize(d->stream));
+  if (d->slots) cudaFree(d->slots);
+  d->slots = nullptr;
+  d->slot_cap = 0;
+  size_t cap = std::max<size_t>(64, n);
+  CK(d, cudaMalloc(&d->slots, cap * sizeof(ispc::CmpResult)));
+  d->slot_cap = cap;
+  return ISPC_OK;
+}
+
+// Waits for `ev`, polling so that a kernel outliving every watchdog is
+// reported as a context-killing fault instead of blocking forever.
+int wait_event(ispc_dev* d, cudaEvent_t ev, double limit_ns, const char* what) {
+  const double t_wait = host_ns();
+  for (int spin = 0;; ++spin) {
+    cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) return ISPC_OK;
+    if (q != cudaErrorNotReady) return cuda_fail(d, q, "kernel");
+    if (host_ns() - t_wait > limit_ns)
+      return fail(d, ISPC_E_STICKY, std::string("kernel ") + what + " still running after " +
+                                        std::to_string(int(limit_ns / 1e9)) + " s (host guard)");
+    if (spin < 64) std::this_thread::yield();
+    else std::this_thread::sleep_for(std::chrono::microseconds(10));
+  }
+}
+
+int flush_l2(ispc_dev* d) {
+  // write a buffer larger than L2, then read it back (clean L2, no pending write-backs)
+  CK(d, cudaMemsetAsync(d->flush, int(flush_counter_++ & 0xff), d->flush_bytes, d->stream));
+  CK(d, ispc::launch_flush_read(d->flush, d->flush_bytes, d->cmp_res, d->stream));
+  return ISPC_OK;
+}
+
+}  // namespace
+
+int ispc_launch_batch(ispc_dev* d, int handle, int n, const ispc_batch_item* items, double refine_below_ns,
+                      ispc_time_result* res) {
+  if (!d || n < 0 || (n > 0 && (!items || !res))) return fail(d, ISPC_E_ARG, "null argument");
+  if (!d->bound) return fail(d, ISPC_E_ARG, "no problem bound");
+  if (n == 0) return ISPC_OK;
+  int rc = bind_ctx(d);
+  if (rc) return rc;
+  Loaded* modp = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(d->mod_mu);
+    auto mit = d->modules.find(handle);
+    if (mit == d->modules.end()) return fail(d, ISPC_E_ARG, "unknown module handle");
+    modp = &mit->second;
+  }
+  Loaded& mod = *modp;
+  const int* flag = reinterpret_cast<const int*>(mod.timeout_flag);
+  for (int i = 0; i < n; ++i) {
+    std::memset(&res[i], 0, sizeof(res[i]));
+    if (!items[i].launch) return fail(d, ISPC_E_ARG, "null launch");
+  }
+  if ((rc = slots_for(d, size_t(2 * n)))) return rc;
+  auto* slots = static_cast<ispc::CmpResult*>(d->slots);
+  CK(d, cudaMemsetAsync(slots, 0, size_t(2 * n) * sizeof(ispc::CmpResult), d->stream));
+
+  if ((rc = grow_scratch(d, n, items))) return rc;
+  std::vector<Bound> B(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i)
+    if ((rc = bind_kernel(d, mod, items[i].launch, items[i].opts.rotate, B[size_t(i)]))) {
+      // report the failing item, keep the others
+      res[i].status = rc;
+    }
+
+  // ---- screen -------------------------------------------------------------------
+  double guard_ns = 0;
+  size_t ev = 0;
+  std::vector<size_t> first_ev(size_t(n), SIZE_MAX);
+  for (int i = 0; i < n; ++i) {
+    if (res[i].status) continue;
+    const ispc_time_opts& o = items[i].opts;
+    const double budget = o.budget_ns > 0 ? o.budget_ns : 2e9;
+    for (const std::string& out : d->outputs) {
+      const Buffer& b = d->regions.at(out);
+      CK(d, cudaMemsetAsync(b.ptr, 0xff, size_t(b.elems) * 4, d->stream));
+    }
+    if (o.flush_l2 && (rc = flush_l2(d))) return rc;
+    uint64_t dl = 0;
+    if ((rc = arm(d, mod, budget, &dl))) return rc;
+    cudaEvent_t e0 = event_at(d, ev), e1 = event_at(d, ev + 1);
+    if (!e0 || !e1) return fail(d, ISPC_E_CUDA, "cudaEventCreate failed");
+    first_ev[size_t(i)] = ev;
+    ev += 2;
+    CK(d, cudaEventRecord(e0, d->stream));
+    if ((rc = enqueue(d, B[size_t(i)], 0, dl))) return rc;
+    CK(d, cudaEventRecord(e1, d->stream));
+    guard_ns += std::max(5e9, 40.0 * budget);
+    ispc::CmpResult* slot = slots + i;
+    if (o.check) {
+      for (const std::string& out_name : d->outputs) {
+        const Buffer& out = d->regions.at(out_name);
+        const Buffer& exp = d->expected.at(out_name);
+        auto sc = d->scale.find(out_name);
+        const float* scale = (!o.bit_exact && sc != d->scale.end()) ? sc->second.ptr : nullptr;
+        CK(d, ispc::launch_check(out.ptr, exp.ptr, scale, out.elems, int(o.bit_exact), float(o.rtol), flag, slot,
+                                 d->stream));
+      }
+    } else if (flag) {
+      CK(d, ispc::launch_collect(flag, slot, d->stream));
     }
   }
-  if ((rc = timed_out(&late))) return rc;
-  std::sort(times.begin(), times.end());
-  res->median_ns = times[times.size() / 2];
-  res->min_ns = times.front();
-  res->status = late ? ISPC_E_TIMEOUT : ISPC_OK;
+  if (ev == 0) return ISPC_OK;
+  if ((rc = wait_event(d, d->evpool[ev - 1], guard_ns, items[0].launch->name))) return rc;
+  std::vector<ispc::CmpResult> h(size_t(2 * n));
+  CK(d, cudaMemcpy(h.data(), slots, size_t(n) * sizeof(ispc::CmpResult), cudaMemcpyDeviceToHost));
+  std::vector<char> refine(size_t(n), 0);
+  bool any_refine = false;
+  for (int i = 0; i < n; ++i) {
+    if (res[i].status) continue;
+    const ispc_time_opts& o = items[i].opts;
+    const double budget = o.budget_ns > 0 ? o.budget_ns : 2e9;
+    float ms = 0;
+    CK(d, cudaEventElapsedTime(&ms, d->evpool[first_ev[size_t(i)]], d->evpool[first_ev[size_t(i)] + 1]));
+    res[i].first_ns = double(ms) * 1e6;
+    if (h[size_t(i)].timeout) {
+      res[i].status = ISPC_E_TIMEOUT;
+      res[i].median_ns = res[i].min_ns = std::max(res[i].first_ns, budget);
+      continue;
+    }
+    if (o.check) {
+      float e;
+      std::memcpy(&e, &h[size_t(i)].max_err_bits, 4);
+      res[i].max_err = e;
+      res[i].mismatches = int64_t(h[size_t(i)].mismatches);
+      if (res[i].mismatches) {
+        res[i].status = ISPC_E_MISMATCH;
+        res[i].median_ns = res[i].min_ns = res[i].first_ns;
+        continue;
+      }
+    }
+    res[i].median_ns = res[i].min_ns = res[i].first_ns;
+    if (o.reps > 0 && !(res[i].first_ns > refine_below_ns)) {
+      refine[size_t(i)] = 1;
+      any_refine = true;
+    }
+  }
+  if (!any_refine) return ISPC_OK;
+
+  // ---- refine -------------------------------------------------------------------
+  guard_ns = 0;
+  ev = 0;
+  struct Group {
+    int item;
+    size_t ev;
+    uint32_t count;
+  };
+  std::vector<Group> groups;
+  for (int i = 0; i < n; ++i) {
+    if (!refine[size_t(i)]) continue;
+    const ispc_time_opts& o = items[i].opts;
+    const double budget = o.budget_ns > 0 ? o.budget_ns : 2e9;
+    Bound& b = B[size_t(i)];
+    ispc::CmpResult* slot = slots + n + i;
+    uint64_t dl = 0;
+    for (uint32_t w = 0; w < o.warmup; ++w) {
+      if (o.flush_l2 && (rc = flush_l2(d))) return rc;
+      if ((rc = arm(d, mod, budget, &dl))) return rc;
+      if ((rc = enqueue(d, b, 0, dl))) return rc;
+      if (flag) CK(d, ispc::launch_collect(flag, slot, d->stream));
+      guard_ns += std::max(5e9, 40.0 * budget);
+    }
+    // rotation: groups of R back-to-back launches over the R input copies
+    // (each launch reads inputs untouched for R-1 launches, i.e. not in L2),
+    // mean per launch; else one launch per event pair
+    const uint32_t R = b.R;
+    const uint32_t ngroups = R > 1 ? std::max<uint32_t>(1, (o.reps + R - 1) / R) : o.reps;
+    for (uint32_t g = 0; g < ngroups; ++g) {
+      if (R == 1 && o.flush_l2 && (rc = flush_l2(d))) return rc;
+      if ((rc = arm(d, mod, budget * R, &dl))) return rc;  // R launches share one armed deadline
+      cudaEvent_t e0 = event_at(d, ev), e1 = event_at(d, ev + 1);
+      if (!e0 || !e1) return fail(d, ISPC_E_CUDA, "cudaEventCreate failed");
+      CK(d, cudaEventRecord(e0, d->stream));
+      for (uint32_t k = 0; k < R; ++k)
+        if ((rc = enqueue(d, b, k % R, dl))) return rc;
+      CK(d, cudaEventRecord(e1, d->stream));
+      if (flag) CK(d, ispc::launch_collect(flag, slot, d->stream));
+      groups.push_back(Group{i, ev, R});
+      ev += 2;
+      guard_ns += std::max(5e9, 40.0 * budget * R);
+    }
+  }
+  if (ev == 0) return ISPC_OK;
+  if ((rc = wait_event(d, d->evpool[ev - 1], guard_ns, items[0].launch->name))) return rc;
+  CK(d, cudaMemcpy(h.data() + n, slots + n, size_t(n) * sizeof(ispc::CmpResult), cudaMemcpyDeviceToHost));
+  std::vector<std::vector<double>> times(static_cast<size_t>(n));
+  for (const Group& g : groups) {
+    float ms = 0;
+    CK(d, cudaEventElapsedTime(&ms, d->evpool[g.ev], d->evpool[g.ev + 1]));
+    times[size_t(g.item)].push_back(double(ms) * 1e6 / g.count);
+  }
+  for (int i = 0; i < n; ++i) {
+    if (!refine[size_t(i)] || times[size_t(i)].empty()) continue;
+    std::vector<double>& t = times[size_t(i)];
+    std::sort(t.begin(), t.end());
+    res[i].median_ns = t[t.size() / 2];
+    res[i].min_ns = t.front();
+    if (h[size_t(n + i)].timeout) res[i].status = ISPC_E_TIMEOUT;
+  }
+  return ISPC_OK;
+}
+
+int ispc_launch_timed(ispc_dev* d, int handle, const ispc_launch* L, const ispc_time_opts* o,
+                      ispc_time_result* res) {
+  if (!d || !L || !o || !res) return fail(d, ISPC_E_ARG, "null argument");
+  ispc_batch_item it{};
+  it.launch = L;
+  it.opts = *o;
+  int rc = ispc_launch_batch(d, handle, 1, &it, std::numeric_limits<double>::infinity(), res);
+  if (rc) return rc;
+  // a launch-level failure of the single item is the call's failure
+  if (res->status != ISPC_OK && res->status != ISPC_E_TIMEOUT && res->status != ISPC_E_MISMATCH) return res->status;
   return ISPC_OK;
 }
 
@@ -789,6 +1043,15 @@ int ispc_host_register(void* p, size_t bytes) {
   if (e != cudaSuccess) {
     cudaGetLastError();
     return fail(nullptr, ISPC_E_CUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e));
+  }
+  return ISPC_OK;
+}
+
+int ispc_host_unregister(void* p) {
+  cudaError_t e = cudaHostUnregister(p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(nullptr, ISPC_E_CUDA, std::string("cudaHostUnregister: ") + cudaGetErrorString(e));
   }
   return ISPC_OK;
 }

@@ -85,6 +85,15 @@ BoundModel::BoundModel(const Kernel& k, const SpaceContext& ctx, const B200Machi
     r.memory = ii.op == Op::Load || ii.op == Op::Store;
     r.load = ii.op == Op::Load;
     r.region = ii.region;
+    r.stride_terms.resize(ii.dims.size());
+    if (r.memory && ii.ivar != kNoIndex)
+      for (const AddrTerm& t : k.ivars[ii.ivar].terms)
+        for (std::size_t p = 0; p < ii.dims.size(); ++p)
+          if (ii.dims[p] == t.dim) {
+            std::vector<std::size_t> sd;
+            for (ObjId x : t.size_dims) sd.push_back(dim_index.at(x));
+            r.stride_terms[p].emplace_back(double(t.base), std::move(sd));
+          }
     insts_.push_back(r);
   }
   for (const auto& [id, ii] : k.insts) {
@@ -166,6 +175,7 @@ BoundReport BoundModel::bound(const Candidate& c) const {
     if (fired(p.lowering) && (is(p.src, v_block_) || is(p.dst, v_block_)) && !may_merge(p.src, p.dst))
       return illegal(Illegal::CrossBlock);
   // grid: dims certainly BLOCK that can never fuse multiply the block count
+  double blocks_lo = 1;
   {
     UF pm(nd);
     for (std::size_t a = 0; a < nd; ++a)
@@ -174,7 +184,6 @@ BoundReport BoundModel::bound(const Candidate& c) const {
     std::map<std::size_t, double> comp;
     for (std::size_t d = 0; d < nd; ++d)
       if (is(d, v_block_)) comp[pm.find(d)] = std::max(comp[pm.find(d)], lo[d]);
-    double blocks_lo = 1;
     for (auto& [r, e] : comp) blocks_lo *= e;
     if (blocks_lo > 2147483647.0) return illegal(Illegal::Grid);
   }
@@ -246,6 +255,35 @@ BoundReport BoundModel::bound(const Candidate& c) const {
       t = std::max(t, r.instances * 4.0);
     }
   }
+  // L1 lines of scattered warp accesses (see bound.hpp)
+  double l1_lines = 0;
+  for (const InstRec& r : insts_) {
+    if (!r.memory || !fired(r.lowering)) continue;
+    bool global_region = false;
+    for (const RegionRec& g : regions_)
+      if (g.id == r.region) global_region = g.input || (g.space_inst != kNoInstance && c.dom[g.space_inst] == bit(v_global_));
+    if (!global_region) continue;
+    bool some_thread = false, vec = false;
+    double s_min = 1e300, lanes = 32;
+    for (std::size_t p = 0; p < r.dims.size(); ++p) {
+      const std::size_t d = r.dims[p];
+      if (can(d, v_vector_)) vec = true;
+      if (!can(d, v_thread_)) continue;
+      if (is(d, v_thread_)) some_thread = true;
+      double s = 0;
+      for (const auto& [base, sd] : r.stride_terms[p]) {
+        double m = base;
+        for (std::size_t x : sd) m *= lo[x];
+        s += m;
+      }
+      s_min = std::min(s_min, s);
+      lanes = std::min(lanes, lo[d]);
+    }
+    if (!some_thread || vec || !(s_min >= 2)) continue;
+    const double per_access = s_min >= 32 ? lanes : std::ceil(lanes * s_min / 32.0);
+    l1_lines += r.instances / 32.0 * per_access;
+  }
+
   double input_bytes = 0, tmp_dram = 0, tmp_lsu = 0;
   for (const RegionRec& g : regions_) {
     auto it = region_touch.find(g.id);
@@ -267,7 +305,9 @@ BoundReport BoundModel::bound(const Candidate& c) const {
   rep.issue = warp_insts / (sms * m_.issue_per_sm_cycle * f);
   rep.thread = std::max(thread_trips, load_chain * m_.min_load_latency_cycles) / f;
   rep.launch = m_.launch_floor_s;
-  rep.total = std::max({rep.dram, rep.sm_mem, rep.issue, rep.thread, rep.launch});
+  rep.dispatch = blocks_lo * m_.block_dispatch_s;
+  rep.l1 = l1_lines / (sms * m_.l1_lines_per_cycle * f);
+  rep.total = std::max({rep.dram, rep.sm_mem, rep.issue, rep.thread, rep.launch, rep.dispatch, rep.l1});
   return rep;
 }
 

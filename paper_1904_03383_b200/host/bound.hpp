@@ -20,6 +20,15 @@
 //           BLOCK/THREAD/VECTOR multiplies by its smallest possible extent;
 //           one instruction per cycle at f_max
 //   launch  1 us launch floor
+//   dispatch  the blocks every completion launches x 0.5 ns: the B200's block
+//           dispatch rate, measured with empty blocks (0.517 ns/block for
+//           <= 128 threads, 1.02 ns for 1024; profiles/r2_block_dispatch.log)
+//   l1      cache lines a warp access must touch: when every dim of a global
+//           access that can be the warp's lane (innermost THREAD) dim walks
+//           the address with stride s >= 2 elements, each warp access touches
+//           ceil(lanes x min(s, 32) / 32) 128-byte lines; lines / (active SMs
+//           x 2 lines/cycle x f_max) (the reference's coalescing rule,
+//           simulate.cpp:46-60, priced as L1 wavefronts)
 // bound = max of the terms. All domain reads take the most optimistic value
 // still possible, so narrowing a domain can only raise a term (monotone), and
 // a leaf's bound is below its measured time (admissible; checked on every
@@ -47,13 +56,20 @@ struct B200Machine {
   bool l2_flushed = false;  // inputs start outside L2 (timed with an L2 flush)
   // per-thread budgets of the emitter (ispc_emit_opts); exceeding them makes
   // every completion unrunnable, i.e. an infinite bound
-  double max_reg_elems = 160;
-  double max_unrolled = 16384;
+  // the search's emit budgets (ispc_search_config.max_unrolled default, the
+  // register-array cap it passes to ispc_emit_cuda): one source of truth, so
+  // ispc_bound reports +inf for exactly the leaves the search cannot run
+  static constexpr int kDefaultMaxUnrolled = 512;
+  static constexpr int kMaxRegElems = 160;
+  double max_reg_elems = kMaxRegElems;
+  double max_unrolled = kDefaultMaxUnrolled;
   // a loaded value is consumed in the iteration that loads it, and the
   // emitter keeps LOOP dimensions rolled (#pragma unroll 1): each trip of the
   // LOOP dimensions around a load waits at least the fastest load latency
   // (LDS 29 cycles, L1 hit 31.8; B300_MICROARCH.md)
   double min_load_latency_cycles = 29;
+  double block_dispatch_s = 0.5e-9;  // per block, whatever the block does
+  double l1_lines_per_cycle = 2;     // per SM (the L1 serves ~1 wavefront/clk; 2 keeps a margin)
 };
 
 // Why a subtree can never run correctly on the device (bound = +inf).
@@ -61,7 +77,7 @@ enum class Illegal : int { None = 0, Grid, CrossBlock, Registers, Unrolled };
 
 struct BoundReport {
   Illegal illegal = Illegal::None;
-  double total = 0, dram = 0, sm_mem = 0, issue = 0, thread = 0, launch = 0;
+  double total = 0, dram = 0, sm_mem = 0, issue = 0, thread = 0, launch = 0, dispatch = 0, l1 = 0;
   double dram_bytes = 0;
   double blocks_max = 0, threads_per_block_max = 0;
 };
@@ -88,6 +104,9 @@ class BoundModel {
     bool memory;
     bool load;
     ispace::ObjId region;
+    // per position of `dims`: the address terms of that dim, (base, indices
+    // of the dims whose sizes multiply it) - its element stride
+    std::vector<std::vector<std::pair<double, std::vector<std::size_t>>>> stride_terms;
   };
   struct PairRec {
     std::size_t src, dst;  // dim indices

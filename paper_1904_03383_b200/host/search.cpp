@@ -30,8 +30,8 @@ void Incumbent::open(const char* shm_name) {
         void* p = mmap(nullptr, map_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
         if (p != MAP_FAILED) {
           map = p;
-          cell = static_cast<std::atomic<uint64_t>*>(p);  // zero-filled: no incumbent yet
-          ispc_host_register(p, map_bytes);                 // pinned host memory
+          name = shm_name;
+          cell = static_cast<std::atomic<uint64_t>*>(p);  // zero-filled when created: no incumbent yet
         }
       }
       close(fd);
@@ -43,8 +43,20 @@ void Incumbent::open(const char* shm_name) {
   }
 }
 
+// Page-locks the shared page once the worker's device is selected (so the
+// registration creates no context on another GPU).
+void Incumbent::pin() {
+  if (map && !pinned) pinned = ispc_host_register(map, map_bytes) == ISPC_OK;
+}
+
 Incumbent::~Incumbent() {
-  if (map) munmap(map, map_bytes);
+  if (map) {
+    if (pinned) ispc_host_unregister(map);
+    munmap(map, map_bytes);
+    // every rank unlinks at exit: the name never outlives the job, so a later
+    // job reusing it starts from an empty (zero) cell, not a stale incumbent
+    if (!name.empty()) shm_unlink(name.c_str());
+  }
 }
 
 double Incumbent::seconds() const {
@@ -74,6 +86,26 @@ std::vector<std::string> split(const std::string& s) {
 }
 
 const char* kPaperOrder = "size,dim_kind,thread_level,mem_space,order,cache";
+
+// Structural key of a candidate inside this process (domains, counters,
+// fired lowerings): the rollouts' memo key. The reference's digest()
+// (candidate.cpp:413) hashes the canonical names and values character by
+// character - 68 us per call on the axpy space, more than a propagation -
+// and stays the key of logs and serializations.
+uint64_t fast_key(const Candidate& c) {
+  auto mix = [](uint64_t h, uint64_t w) {
+    h ^= w + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+    h *= 0xff51afd7ed558ccdull;
+    return h ^ (h >> 32);
+  };
+  uint64_t h = mix(0x1904033830ull, c.fired);
+  const size_t n = c.dom.size();
+  size_t i = 0;
+  for (; i + 1 < n; i += 2) h = mix(h, uint64_t(c.dom[i]) | (uint64_t(c.dom[i + 1]) << 32));
+  if (i < n) h = mix(h, c.dom[i]);
+  for (const Interval& v : c.cnt) h = mix(mix(h, uint64_t(v.lo)), uint64_t(v.hi));
+  return h;
+}
 // building-block spaces: the engine and staging shape everything below them
 const char* kTileOrder = "engine,staging,tile,xreduce,cache";
 
@@ -93,25 +125,25 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
   if (cfg_.budget_factor <= 0) cfg_.budget_factor = 3.0;
   if (cfg_.max_budget_ns <= 0) cfg_.max_budget_ns = 50e6;
   if (cfg_.reps <= 0) cfg_.reps = 3;
-  if (cfg_.max_unrolled <= 0) cfg_.max_unrolled = 512;
+  if (cfg_.max_unrolled <= 0) cfg_.max_unrolled = B200Machine::kDefaultMaxUnrolled;
   unsigned hw = std::max(2u, std::thread::hardware_concurrency());
   // one process per GPU: the ranks of this node share its cores
   if (const char* lws = std::getenv("LOCAL_WORLD_SIZE")) {
     const int ranks = std::atoi(lws);
     if (ranks > 1) hw = std::max(2u, hw / unsigned(ranks));
   }
-  // measured on the B200 boxes (16 cores): propagation-heavy rollouts (most
-  // of them dead ends under the aspiration band) cost ~4-5x the CPU of NVRTC
-  // per produced kernel; 11/16 of the cores measured best (10/16: -12%,
-  // 12/16: -16% candidates/s over 4 seeds each)
-  if (cfg_.rollout_threads <= 0) cfg_.rollout_threads = int(std::max(1u, hw * 11 / 16));
-  if (cfg_.compile_threads <= 0) cfg_.compile_threads = int(std::max(1u, hw - unsigned(cfg_.rollout_threads) - 1));
+  // one launch thread; every other core alternates rollouts and NVRTC by
+  // need (worker()); rollout_threads + compile_threads, when given, set the total
+  workers_ = cfg_.rollout_threads > 0 || cfg_.compile_threads > 0
+                 ? std::max(1, std::max(0, cfg_.rollout_threads) + std::max(0, cfg_.compile_threads))
+                 : int(std::max(1u, hw));  // the launch thread mostly waits on the device
   machine_.l2_flushed = cfg_.flush_l2 != 0;
   machine_.max_unrolled = cfg_.max_unrolled;
   if (!space_->tiles) model_ = std::make_unique<BoundModel>(space_->kernel, *space_->ctx, machine_);
   order_ = DecisionOrder::from_names(*space_->ctx, split(order_text_));
   inc_.open(shm_text_.empty() ? nullptr : shm_text_.c_str());
   trace_ = std::getenv("ISPC_TRACE") != nullptr;
+  if (const char* ld = std::getenv("ISPC_LOG_DEADENDS")) log_dead_ = std::atoi(ld) != 0;
   if (const char* g = std::getenv("ISPC_GREEDY")) {
     const std::string v(g);
     greedy_mode_ = v == "first" ? 0 : v == "off" ? 2 : 1;
@@ -132,6 +164,13 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
     rollout_mode_ = v == "deep" ? 1 : v == "ancestor" ? 2 : 0;
   }
   tree_depth_ = cfg_.tree_depth < 0 ? 0 : cfg_.tree_depth == 0 ? 12 : cfg_.tree_depth;
+  refine_factor_ = cfg_.refine_factor > 0 ? cfg_.refine_factor : 1.25;
+  uniform_ = cfg_.walk == ISPC_WALK_UNIFORM;
+  if (uniform_) {  // the reference baseline's walk: no bound, tree or band
+    cfg_.pruning = 0;
+    tree_depth_ = 0;
+    aspire_ = 0;
+  }
   if (!log_text_.empty()) log_ = std::fopen(log_text_.c_str(), "w");
   expand_frontier();
 
@@ -140,6 +179,7 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
   if (cfg_.device < 0) return;  // dry run: rollouts + emission + NVRTC, no device
   int rc = ispc_dev_open(cfg_.device, &dev_);
   if (rc) throw std::runtime_error(std::string("ispc_dev_open: ") + ispc_last_error(nullptr));
+  inc_.pin();
   ispc_problem p{};
   if (ispc_space_problem(space_, &p) != 0) throw std::runtime_error("no problem for this space");
   if ((rc = ispc_bind_problem(dev_, &p))) throw std::runtime_error(std::string("bind: ") + ispc_last_error(dev_));
@@ -153,7 +193,12 @@ Search::~Search() {
   cv_batch_.notify_all();
   cv_done_.notify_all();
   for (auto& t : threads_) t.join();
-  for (auto& b : batch_q_) ispc_module_free(b->module);
+  for (auto& b : batch_q_) {
+    if (dev_ && b->handle) ispc_module_unload(dev_, b->handle);
+    ispc_module_free(b->module);
+  }
+  if (dev_)
+    for (int h : retired_) ispc_module_unload(dev_, h);
   if (dev_) ispc_dev_close(dev_);
   if (log_) std::fclose(log_);
 }
@@ -396,12 +441,13 @@ bool Search::descend(std::mt19937_64& rng, Candidate cur, const Candidate* guide
     std::uint32_t inst = order_.pick(ctx, cur);
     const double T = prune ? prune_threshold() : std::numeric_limits<double>::infinity();
     if (inst == kNoInstance) {
-      const uint64_t d = digest(ctx, cur);
+      const uint64_t d = fast_key(cur);
       bool fresh;
       {
         std::lock_guard<std::mutex> lk(seen_leaf_mu_);
         fresh = seen_leaf_.insert(d).second;
       }
+      dead_.add(d);  // produced: no later rollout needs to reach it again
       if (fresh) {
         if (!guide) {  // running estimate of the decisions a rollout makes below its start
           const int64_t old = decisions_per_leaf_.load();
@@ -450,14 +496,17 @@ bool Search::descend(std::mt19937_64& rng, Candidate cur, const Candidate* guide
           Candidate child;
           if (apply_decision(ctx, cur, inst, vals[k], child) != PropStatus::Ok) continue;
           const double b = bound_total(child);
-          if (!std::isfinite(b) || b >= T) {
+          if (!std::isfinite(b) || b >= T || dead_.has(fast_key(child))) {
             ++pruned_;
             continue;
           }
           if (b < best_b) best_b = b, best_child = std::move(child);
           if (best_b <= b_parent * (1 + 1e-12)) break;
         }
-        if (!std::isfinite(best_b)) break;  // dead end: restart
+        if (!std::isfinite(best_b)) {  // dead end: remember it, restart
+          dead_.add(fast_key(cur));
+          break;
+        }
         cur = std::move(best_child);
         cur_b = best_b;
         continue;
@@ -470,7 +519,8 @@ bool Search::descend(std::mt19937_64& rng, Candidate cur, const Candidate* guide
         double weight = 1.0, b = 0.0;
         if (prune) {
           b = bound_total(child);
-          if (!std::isfinite(b) || b >= T) {  // unrunnable, or cannot beat the incumbent
+          // unrunnable, cannot beat the incumbent, or spent by earlier rollouts
+          if (!std::isfinite(b) || b >= T || dead_.has(fast_key(child))) {
             ++pruned_;
             continue;
           }
@@ -485,6 +535,7 @@ bool Search::descend(std::mt19937_64& rng, Candidate cur, const Candidate* guide
       if (!f.kids.empty()) {
         stack.push_back(std::move(f));
       } else {
+        if (prune) dead_.add(fast_key(cur));  // every child pruned or spent: so is this node
         dead_end = true;
       }
     } else {
@@ -589,159 +640,213 @@ void Search::note_fruitless() {
   }
 }
 
-void Search::rollout_worker(int tid) {
+// One rollout: descend to a leaf (or a dead end), emit its kernel and queue it.
+void Search::rollout_one(int tid, std::mt19937_64& rng, int64_t& k_roll, const ispc_emit_opts& eo) {
+  double t = now();
+  auto w = std::make_unique<Work>();
+  w->tid = tid;
+  w->rollout_no = k_roll++;
+  bool ok;
+  const char* dead_reason = "deadend";
+  if (uniform_) {
+    ok = uniform_walk(rng, w->leaf);
+    if (ok) w->bound_s = bound_total(w->leaf);  // not used to prune: counts bound violations
+  } else {
+    ok = rollout(rng, w->leaf, w->bound_s, w->path, w->root);
+  }
+  if (ok && aspire_ > 0) {
+    double lo = min_leaf_bound_.load();
+    while (w->bound_s < lo && !min_leaf_bound_.compare_exchange_weak(lo, w->bound_s)) {
+    }
+    if (w->bound_s > aspire_ * std::min(lo, w->bound_s)) {  // outside the aspiration band
+      ok = false;
+      dead_reason = "aspiration";
+    }
+  }
+  ++rollouts_;
+  if (!ok) {
+    ++dead_rollouts_;
+    if (log_ && log_dead_) log_dead(tid, w->rollout_no, dead_reason);
+    t_rollout_.fetch_add(now() - t);
+    note_fruitless();
+    if (exhausted_) std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    return;
+  }
+  int rc = ISPC_OK;
+  size_t len = 0;
+  if (space_->tiles) {
+    // building-block leaf: decided tile configuration -> sm_100a kernel
+    ispc_tile_config tc{};
+    try {
+      tc = tile_config(*space_->tiles, *space_->ctx, w->leaf);
+    } catch (const std::exception& e) {
+      if (trace_) std::fprintf(stderr, "[ispc] leaf without a tile config: %s\n", e.what());
+      ++illegal_;
+      if (log_ && log_dead_) log_dead(tid, w->rollout_no, "illegal");
+      t_rollout_.fetch_add(now() - t);
+      note_fruitless();
+      return;
+    }
+    w->bit_exact = tile_bit_exact(tc);
+    w->rtol = tc.kind == ISPC_TILE_SGEMM_TC && tc.engine == ISPC_ENGINE_TF32X3 ? 1e-5 : space_->tiles->rtol();
+    rc = ispc_emit_tiles(&tc, nullptr, nullptr, 0, &len, &w->launch);
+    if (rc == ISPC_OK) {
+      w->src.assign(len + 1, '\0');
+      rc = ispc_emit_tiles(&tc, nullptr, w->src.data(), w->src.size(), &len, &w->launch);
+      w->src.resize(len);
+    }
+  } else {
+    try {
+      LoopNest l = reconstruct(space_->kernel, *space_->ctx, w->leaf);
+      w->nest = flatten(space_->kernel, l);
+    } catch (const std::exception&) {
+      ++illegal_;
+      if (log_ && log_dead_) log_dead(tid, w->rollout_no, "illegal");
+      t_rollout_.fetch_add(now() - t);
+      note_fruitless();
+      return;
+    }
+    rc = ispc_emit_cuda(&w->nest->nest, &eo, nullptr, nullptr, 0, &len, &w->launch);
+    if (rc == ISPC_OK) {
+      w->src.assign(len + 1, '\0');
+      rc = ispc_emit_cuda(&w->nest->nest, &eo, nullptr, w->src.data(), w->src.size(), &len, &w->launch);
+      w->src.resize(len);
+    }
+  }
+  t_rollout_.fetch_add(now() - t);
+  if (rc != ISPC_OK) {
+    if (trace_) std::fprintf(stderr, "[ispc] illegal leaf: %s\n", ispc_last_error(nullptr));
+    ++illegal_;
+    if (log_ && log_dead_) log_dead(tid, w->rollout_no, "illegal");
+    note_fruitless();
+    return;
+  }
+  w->digest = digest(*space_->ctx, w->leaf);
+  std::unique_lock<std::mutex> lk(mu_);
+  if (!seen_hash_.insert(w->launch.source_hash).second) {
+    ++duplicates_;
+    lk.unlock();
+    if (log_ && log_dead_) log_dead(tid, w->rollout_no, "duplicate");
+    note_fruitless();
+    if (exhausted_) std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    return;
+  }
+  fruitless_ = 0;
+  exhausted_ = false;
+  work_q_.push_back(std::move(w));
+  cv_batch_.notify_all();
+}
+
+// Compiles a batch of emitted kernels into one NVRTC program (isolating a
+// failing kernel) and loads the cubin on the device.
+void Search::compile_items(std::vector<std::unique_ptr<Work>> items) {
+  double t = now();
+  std::vector<const char*> srcs;
+  for (auto& w : items) srcs.push_back(w->src.c_str());
+  ispc_module* m = nullptr;
+  int rc = ispc_compile(srcs.data(), int(srcs.size()), "sm_100a", &m);
+  if (trace_) {
+    size_t bytes = 0;
+    for (auto& w : items) bytes += w->src.size();
+    std::fprintf(stderr, "[ispc] compile %zu kernels (%zu B of source) in %.3f s rc=%d first=%s\n", items.size(), bytes,
+                 now() - t, rc, items.front()->launch.name);
+    std::fflush(stderr);
+  }
+  std::vector<std::unique_ptr<CompiledBatch>> out;
+  if (rc == ISPC_OK) {
+    auto b = std::make_unique<CompiledBatch>();
+    b->items = std::move(items);
+    b->module = m;
+    out.push_back(std::move(b));
+  } else {
+    // isolate the failing kernel(s)
+    for (auto& w : items) {
+      const char* one[] = {w->src.c_str()};
+      ispc_module* m1 = nullptr;
+      if (ispc_compile(one, 1, "sm_100a", &m1) != ISPC_OK) {
+        ++compile_errors_;
+        continue;
+      }
+      auto b = std::make_unique<CompiledBatch>();
+      b->items.push_back(std::move(w));
+      b->module = m1;
+      out.push_back(std::move(b));
+    }
+  }
+  // load the cubins here, off the launch thread (module load and the eager
+  // upload of its kernels overlap the device's work on earlier batches)
+  if (dev_)
+    for (auto& b : out) {
+      b->load_rc = ispc_module_load(dev_, b->module, &b->handle);
+      if (b->load_rc != ISPC_OK) b->load_err = ispc_last_error(dev_);
+    }
+  t_compile_.fetch_add(now() - t);
+  std::lock_guard<std::mutex> lk(mu_);
+  for (auto& b : out) batch_q_.push_back(std::move(b));
+  --compiling_;
+  cv_done_.notify_all();
+}
+
+// Every host thread but the launch thread alternates between the two CPU
+// stages by need: it compiles when a whole batch of emitted kernels waits (or
+// any kernel waits while the device has nothing queued), otherwise it runs a
+// rollout while the emitted-kernel queue has room. The split adapts to the
+// walk: pruned rollouts cost ~2-3x the CPU of NVRTC per kernel, uniform
+// leaves the reverse (r2 measurements), so fixed pools left cores idle.
+void Search::worker(int tid) {
+  // uniform walk: thread tid's descents are those of the reference baseline's
+  // thread tid (oracle/ref_cpu_bench.cpp seeds 0x190403383 + 7919 tid)
   std::mt19937_64 rng(cfg_.seed + 7919ull * uint64_t(tid) + 104729ull * uint64_t(cfg_.shard_index));
-  const size_t cap = size_t(cfg_.batch) * size_t(cfg_.compile_threads) * 3;
+  int64_t k_roll = 0;
   ispc_emit_opts eo{};
   eo.watchdog = uint32_t(cfg_.watchdog);
   eo.max_unrolled = uint32_t(cfg_.max_unrolled);
-  eo.max_reg_elems = 160;  // register arrays beyond this spill on a 255-register thread anyway
-  while (!stop_) {
-    {
-      std::unique_lock<std::mutex> lk(mu_);
-      cv_work_.wait(lk, [&] { return stop_ || work_q_.size() < cap; });
-      if (stop_) return;
-    }
-    double t = now();
-    auto w = std::make_unique<Work>();
-    bool ok = rollout(rng, w->leaf, w->bound_s, w->path, w->root);
-    if (ok && aspire_ > 0) {
-      double lo = min_leaf_bound_.load();
-      while (w->bound_s < lo && !min_leaf_bound_.compare_exchange_weak(lo, w->bound_s)) {
-      }
-      if (w->bound_s > aspire_ * std::min(lo, w->bound_s)) ok = false;  // outside the aspiration band
-    }
-    ++rollouts_;
-    if (!ok) {
-      ++dead_rollouts_;
-      t_rollout_.fetch_add(now() - t);
-      note_fruitless();
-      if (exhausted_) std::this_thread::sleep_for(std::chrono::milliseconds(1));
-      continue;
-    }
-    int rc = ISPC_OK;
-    size_t len = 0;
-    if (space_->tiles) {
-      // building-block leaf: decided tile configuration -> sm_100a kernel
-      ispc_tile_config tc{};
-      try {
-        tc = tile_config(*space_->tiles, *space_->ctx, w->leaf);
-      } catch (const std::exception& e) {
-        if (trace_) std::fprintf(stderr, "[ispc] leaf without a tile config: %s\n", e.what());
-        ++illegal_;
-        t_rollout_.fetch_add(now() - t);
-        note_fruitless();
-        continue;
-      }
-      w->bit_exact = tile_bit_exact(tc);
-      w->rtol = tc.kind == ISPC_TILE_SGEMM_TC && tc.engine == ISPC_ENGINE_TF32X3 ? 1e-5 : space_->tiles->rtol();
-      rc = ispc_emit_tiles(&tc, nullptr, nullptr, 0, &len, &w->launch);
-      if (rc == ISPC_OK) {
-        w->src.assign(len + 1, '\0');
-        rc = ispc_emit_tiles(&tc, nullptr, w->src.data(), w->src.size(), &len, &w->launch);
-        w->src.resize(len);
-      }
-    } else {
-      try {
-        LoopNest l = reconstruct(space_->kernel, *space_->ctx, w->leaf);
-        w->nest = flatten(space_->kernel, l);
-      } catch (const std::exception&) {
-        ++illegal_;
-        t_rollout_.fetch_add(now() - t);
-        note_fruitless();
-        continue;
-      }
-      rc = ispc_emit_cuda(&w->nest->nest, &eo, nullptr, nullptr, 0, &len, &w->launch);
-      if (rc == ISPC_OK) {
-        w->src.assign(len + 1, '\0');
-        rc = ispc_emit_cuda(&w->nest->nest, &eo, nullptr, w->src.data(), w->src.size(), &len, &w->launch);
-        w->src.resize(len);
-      }
-    }
-    t_rollout_.fetch_add(now() - t);
-    if (rc != ISPC_OK) {
-      if (trace_) std::fprintf(stderr, "[ispc] illegal leaf: %s\n", ispc_last_error(nullptr));
-      ++illegal_;
-      note_fruitless();
-      continue;
-    }
-    w->digest = digest(*space_->ctx, w->leaf);
-    std::unique_lock<std::mutex> lk(mu_);
-    if (!seen_hash_.insert(w->launch.source_hash).second) {
-      ++duplicates_;
-      lk.unlock();
-      note_fruitless();
-      if (exhausted_) std::this_thread::sleep_for(std::chrono::milliseconds(1));
-      continue;
-    }
-    fruitless_ = 0;
-    exhausted_ = false;
-    work_q_.push_back(std::move(w));
-    cv_batch_.notify_all();
-  }
-}
-
-void Search::compile_worker(int tid) {
-  (void)tid;
-  const size_t cap = size_t(cfg_.compile_threads) * 2 + 2;
+  eo.max_reg_elems = B200Machine::kMaxRegElems;  // register arrays beyond this spill on a 255-register thread anyway
+  const size_t batch = size_t(cfg_.batch);
+  const size_t cap_w = batch * size_t(workers_) * 2;  // emitted kernels waiting for NVRTC
+  const size_t cap_b = size_t(workers_) / 2 + 4;      // compiled batches waiting for the device
   while (!stop_) {
     std::vector<std::unique_ptr<Work>> items;
     {
       std::unique_lock<std::mutex> lk(mu_);
-      cv_batch_.wait(lk, [&] { return stop_ || (!work_q_.empty() && batch_q_.size() < cap); });
-      if (stop_) return;
-      // give the rollouts a moment to fill a whole batch
-      if (work_q_.size() < size_t(cfg_.batch))
-        cv_batch_.wait_for(lk, std::chrono::milliseconds(5),
-                           [&] { return stop_ || work_q_.size() >= size_t(cfg_.batch); });
-      while (!work_q_.empty() && items.size() < size_t(cfg_.batch)) {
-        items.push_back(std::move(work_q_.front()));
-        work_q_.pop_front();
-      }
-      if (!items.empty()) ++compiling_;
-      cv_work_.notify_all();
-    }
-    if (items.empty()) continue;
-    double t = now();
-    std::vector<const char*> srcs;
-    for (auto& w : items) srcs.push_back(w->src.c_str());
-    ispc_module* m = nullptr;
-    int rc = ispc_compile(srcs.data(), int(srcs.size()), "sm_100a", &m);
-    if (trace_) {
-      size_t bytes = 0;
-      for (auto& w : items) bytes += w->src.size();
-      std::fprintf(stderr, "[ispc] compile %zu kernels (%zu B of source) in %.3f s rc=%d first=%s\n", items.size(), bytes,
-                   now() - t, rc, items.front()->launch.name);
-      std::fflush(stderr);
-    }
-    std::vector<std::unique_ptr<CompiledBatch>> out;
-    if (rc == ISPC_OK) {
-      auto b = std::make_unique<CompiledBatch>();
-      b->items = std::move(items);
-      b->module = m;
-      out.push_back(std::move(b));
-    } else {
-      // isolate the failing kernel(s)
-      for (auto& w : items) {
-        const char* one[] = {w->src.c_str()};
-        ispc_module* m1 = nullptr;
-        if (ispc_compile(one, 1, "sm_100a", &m1) != ISPC_OK) {
-          ++compile_errors_;
-          continue;
+      for (;;) {
+        if (stop_) return;
+        const bool room_b = batch_q_.size() < cap_b;
+        const bool starving = batch_q_.empty() && compiling_.load() == 0;
+        if (!work_q_.empty() && room_b && (work_q_.size() >= batch || starving || work_q_.size() >= cap_w)) {
+          // a backlog compiles in bigger programs: NVRTC's fixed cost per
+          // program (~25 ms) is then shared by up to 2 x batch kernels
+          const size_t take = work_q_.size() >= 2 * batch ? 2 * batch : batch;
+          while (!work_q_.empty() && items.size() < take) {
+            items.push_back(std::move(work_q_.front()));
+            work_q_.pop_front();
+          }
+          ++compiling_;
+          break;
         }
-        auto b = std::make_unique<CompiledBatch>();
-        b->items.push_back(std::move(w));
-        b->module = m1;
-        out.push_back(std::move(b));
+        if (work_q_.size() < cap_w) break;  // room: run a rollout
+        cv_work_.wait_for(lk, std::chrono::milliseconds(5));
       }
     }
-    t_compile_.fetch_add(now() - t);
-    std::lock_guard<std::mutex> lk(mu_);
-    for (auto& b : out) batch_q_.push_back(std::move(b));
-    --compiling_;
-    cv_done_.notify_all();
+    if (!items.empty()) {
+      compile_items(std::move(items));
+      cv_work_.notify_all();
+    } else {
+      rollout_one(tid, rng, k_roll, eo);
+    }
   }
 }
+
+
+bool Search::uniform_walk(std::mt19937_64& rng, Candidate& leaf) {
+  return random_walk(*space_->ctx, space_->root, rng, leaf, nullptr).ok;
+}
+
+void Search::log_dead(int tid, int64_t rollout_no, const char* reason) {
+  std::fprintf(log_, "{\"status\": \"%s\", \"seed\": %llu, \"tid\": %d, \"rollout\": %lld, \"t\": %.4f}\n",
+               reason, (unsigned long long)cfg_.seed, tid, (long long)rollout_no, now() - t0_);
+}
+
 
 void Search::launch_worker() {
   bool& step_open = step_open_;
@@ -758,144 +863,190 @@ void Search::launch_worker() {
       b = std::move(batch_q_.front());
       batch_q_.pop_front();
       cv_batch_.notify_all();
+      if (dev_ && !step_open) {
+        ispc_dev_mark(dev_, 0);
+        step_open = true;
+      }
     }
-    double t_busy = now();
-    int h = 0;
-    if (!dev_) {  // dry run: count the compiled kernels as evaluated
+    const double t_busy = now();
+    const int64_t n = int64_t(b->items.size());
+    if (!dev_ || b->load_rc != ISPC_OK) {
+      // dry run: the compiled kernels count as evaluated; a module that did
+      // not load: every kernel of it is a launch error (a sticky fault ends
+      // the search, as in ispc_launch_batch)
       std::lock_guard<std::mutex> lk(mu_);
-      st_.evaluations += int64_t(b->items.size());
+      st_.evaluations += n;
+      if (dev_) {
+        st_.launch_errors += n;
+        if (b->load_rc == ISPC_E_STICKY) {
+          err_ = b->load_err;
+          stop_ = true;
+        }
+      }
       ispc_module_free(b->module);
       launching_ = false;
       cv_done_.notify_all();
       continue;
     }
-    if (ispc_module_load(dev_, b->module, &h) != ISPC_OK) {
-      std::lock_guard<std::mutex> lk(mu_);
-      st_.launch_errors += int64_t(b->items.size());
-      st_.evaluations += int64_t(b->items.size());
-      ispc_module_free(b->module);
-      cv_done_.notify_all();
-      continue;
-    }
-    for (auto& w : b->items) {
-      if (stop_) break;
-      {
-        std::unique_lock<std::mutex> lk(mu_);
-        if (st_.evaluations >= target_.load()) {
-          launching_ = false;
-          cv_done_.notify_all();
-          while (!(stop_ || st_.evaluations < target_.load())) cv_done_.wait_for(lk, std::chrono::milliseconds(20));
-          if (stop_) break;
-          launching_ = true;
-        }
-        if (!step_open && st_.evaluations < target_.load()) {
-          ispc_dev_mark(dev_, 0);
-          step_open = true;
-        }
-      }
-      const double T = inc_.seconds();
+    const double T = inc_.seconds();
+    std::vector<ispc_batch_item> items(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      Work& w = *b->items[size_t(i)];
       if (trace_) {
-        std::fprintf(stderr, "[ispc] launch %lld %s grid=%llu block=%u,%u,%u smem=%u wd=%u\n",
-                     (long long)st_.evaluations + 1, w->launch.name, (unsigned long long)w->launch.grid_x,
-                     w->launch.block[0], w->launch.block[1], w->launch.block[2], w->launch.static_smem,
-                     w->launch.watchdog);
-        std::fflush(stderr);
+        std::fprintf(stderr, "[ispc] launch %s grid=%llu block=%u,%u,%u smem=%u wd=%u\n", w.launch.name,
+                     (unsigned long long)w.launch.grid_x, w.launch.block[0], w.launch.block[1], w.launch.block[2],
+                     w.launch.static_smem, w.launch.watchdog);
         if (const char* dir = std::getenv("ISPC_TRACE_DIR")) {  // the kernel source, for post-mortems
-          if (FILE* f = std::fopen((std::string(dir) + "/" + w->launch.name + ".cu").c_str(), "w")) {
-            std::fputs(w->src.c_str(), f);
+          if (FILE* f = std::fopen((std::string(dir) + "/" + w.launch.name + ".cu").c_str(), "w")) {
+            std::fputs(w.src.c_str(), f);
             std::fclose(f);
           }
         }
       }
-      ispc_time_opts to{};
+      ispc_time_opts& to = items[size_t(i)].opts;
+      items[size_t(i)].launch = &w.launch;
       to.warmup = uint32_t(std::max(0, cfg_.warmup));
       to.reps = uint32_t(cfg_.reps);
       to.flush_l2 = uint32_t(cfg_.flush_l2);
       to.rotate = cfg_.rotate > 1 ? uint32_t(cfg_.rotate) : 0u;
       to.check = 1;
-      to.bit_exact = w->bit_exact ? 1 : 0;
-      to.rtol = w->rtol;
+      to.bit_exact = w.bit_exact ? 1 : 0;
+      to.rtol = w.rtol;
       // before the first measurement: 50x the leaf's own bound (>= 2 ms) for
       // the first 64 evaluations, then the cap (a schedule 50x off its bound
       // is not worth waiting 50 ms for while any incumbent is missing)
       to.budget_ns = std::isfinite(T) ? std::min(cfg_.max_budget_ns, std::max(T * 1e9 * cfg_.budget_factor,
-                                                                                T * 1e9 + 20e3))
-                     : st_.evaluations < 64 ? std::min(cfg_.max_budget_ns, std::max(2e6, 50.0 * w->bound_s * 1e9))
+                                                                              T * 1e9 + 20e3))
+                     : st_.evaluations < 64 ? std::min(cfg_.max_budget_ns, std::max(2e6, 50.0 * w.bound_s * 1e9))
                                             : cfg_.max_budget_ns;
-      ispc_time_result r{};
-      int rc = ispc_launch_timed(dev_, h, &w->launch, &to, &r);
-      const double t_now = now() - t0_;
-      std::string status;
-      bool improved = false;
-      {
-        std::lock_guard<std::mutex> lk(mu_);
+    }
+    // screened kernels slower than factor x incumbent cannot become the
+    // incumbent: their single checked launch is their time
+    const double refine_below = std::isfinite(T) ? T * 1e9 * refine_factor_ : std::numeric_limits<double>::infinity();
+    std::vector<ispc_time_result> res(static_cast<size_t>(n));
+    const double t_dev0 = now();
+    const int brc = ispc_launch_batch(dev_, b->handle, int(n), items.data(), refine_below, res.data());
+    const double t_dev = now() - t_dev0;
+    const std::string berr = brc ? ispc_last_error(dev_) : std::string();
+    // cuModuleUnload measured 1.4-231 ms per call on the B200 (it waits on
+    // the context): modules stay loaded (a few hundred KiB of device memory
+    // each) and are unloaded in bulk, between steps or at close
+    retired_.push_back(b->handle);
+    ispc_module_free(b->module);
+    b->module = nullptr;
+    if (retired_.size() >= kMaxRetired) {
+      for (size_t k = 0; k < kMaxRetired / 2; ++k) ispc_module_unload(dev_, retired_[k]);
+      retired_.erase(retired_.begin(), retired_.begin() + long(kMaxRetired / 2));
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      for (int64_t i = 0; i < n; ++i) {
+        Work& w = *b->items[size_t(i)];
+        const ispc_time_result& r = res[size_t(i)];
+        // a device-level failure of the batch fails every item of it
+        const int rc = brc ? brc : (r.status == ISPC_OK || r.status == ISPC_E_TIMEOUT || r.status == ISPC_E_MISMATCH)
+                                       ? ISPC_OK
+                                       : r.status;
+        const double t_now = now() - t0_;
+        std::string status;
+        bool improved = false;
         ++st_.evaluations;
         if (rc != ISPC_OK) {
           ++st_.launch_errors;
           status = rc == ISPC_E_STICKY ? "sticky" : "launch_error";
           if (rc == ISPC_E_STICKY) {
-            err_ = ispc_last_error(dev_);
+            err_ = berr;
             stop_ = true;
           }
-        } else if (r.status == ISPC_E_MISMATCH) {
-          ++st_.mismatches;
-          status = "mismatch";
-        } else if (r.status == ISPC_E_TIMEOUT) {
-          ++st_.timeouts;
-          status = "timeout";
         } else {
-          ++st_.ok;
-          status = "ok";
-          if (w->bound_s * 1e9 > r.median_ns * (1 + 1e-9)) ++st_.bound_violations;
-          inc_.offer(uint64_t(std::llround(r.median_ns)));
-          if (r.median_ns < st_.best_ns) {
-            improved = true;
-            st_.best_ns = r.median_ns;
-            st_.best_bound_ns = w->bound_s * 1e9;
-            st_.time_to_best_s = t_now;
-            st_.best_hash = w->launch.source_hash;
-            best_text_ = serialize_text(*space_->ctx, w->leaf);
-            best_src_ = w->src;
-            best_launch_ = w->launch;
+          step_busy_ms_ += r.first_ns * 1e-6;
+          if (r.median_ns != r.first_ns || r.min_ns != r.first_ns) ++refined_;
+          if (r.status == ISPC_E_MISMATCH) {
+            ++st_.mismatches;
+            status = "mismatch";
+          } else if (r.status == ISPC_E_TIMEOUT) {
+            ++st_.timeouts;
+            status = "timeout";
+          } else {
+            ++st_.ok;
+            status = "ok";
+            if (w.bound_s * 1e9 > r.median_ns * (1 + 1e-9)) ++st_.bound_violations;
+            inc_.offer(uint64_t(std::llround(r.median_ns)));
+            if (r.median_ns < st_.best_ns) {
+              improved = true;
+              st_.best_ns = r.median_ns;
+              st_.best_bound_ns = w.bound_s * 1e9;
+              st_.time_to_best_s = t_now;
+              st_.best_hash = w.launch.source_hash;
+              best_text_ = serialize_text(*space_->ctx, w.leaf);
+              best_src_ = w.src;
+              best_launch_ = w.launch;
+            }
           }
         }
-        if (rc == ISPC_OK && r.status == ISPC_OK && std::isfinite(r.median_ns)) note_elite(r.median_ns, w->root, w->leaf);
-        if (!w->path.empty()) {
-          const double ns = (rc == ISPC_OK && r.status == ISPC_OK) ? r.median_ns
-                                                                  : std::numeric_limits<double>::infinity();
-          backprop(w->path, ns);
+        if (rc == ISPC_OK && r.status == ISPC_OK && std::isfinite(r.median_ns)) note_elite(r.median_ns, w.root, w.leaf);
+        if (!w.path.empty()) {
+          const double ns = (rc == ISPC_OK && r.status == ISPC_OK) ? r.median_ns : std::numeric_limits<double>::infinity();
+          backprop(w.path, ns);
         }
-        if (log_) {  // JSON: -1 for "no value" (no incumbent yet, no time)
-          std::string compact = improved ? best_text_ : std::string();
-          std::replace(compact.begin(), compact.end(), '\n', ' ');
-          const double logged_ns = rc == ISPC_OK && std::isfinite(r.median_ns) ? r.median_ns : -1.0;
-          std::fprintf(log_,
-                       "{\"i\": %lld, \"t\": %.4f, \"status\": \"%s\", \"median_ns\": %.1f, \"bound_ns\": %.1f, "
-                       "\"incumbent_ns\": %.1f, \"hash\": \"%016llx\", \"digest\": \"%016llx\", \"best\": %s%s%s}\n",
-                       (long long)st_.evaluations, t_now, status.c_str(), logged_ns,
-                       w->bound_s * 1e9, std::isfinite(inc_.seconds()) ? inc_.seconds() * 1e9 : -1.0,
-                       (unsigned long long)w->launch.source_hash,
-                       (unsigned long long)w->digest, improved ? "true" : "false",
-                       improved ? ", \"candidate\": " : "", compact.c_str());
-          std::fflush(log_);
-        }
-        if (step_open && st_.evaluations >= target_.load()) {
-          ispc_dev_mark(dev_, 1);
-          double ms = 0;
-          ispc_dev_mark_elapsed(dev_, 0, 1, &ms);
-          st_.device_step_ms = ms;
-          step_open = false;
-        }
+        if (log_) log_eval(w, r, rc, status, t_now, improved);
       }
-      cv_done_.notify_all();
+      if (log_) std::fflush(log_);  // once per batch
+      if (step_open && st_.evaluations >= target_.load()) close_step();
+      t_launch_host_ += (now() - t_busy) - t_dev;
+      st_.t_gpu_s += now() - t_busy;
+      launching_ = false;
     }
-    ispc_module_unload(dev_, h);
-    ispc_module_free(b->module);
-    std::lock_guard<std::mutex> lk(mu_);
-    st_.t_gpu_s += now() - t_busy;
-    launching_ = false;
     cv_done_.notify_all();
+    if (trace_) std::fflush(stderr);
   }
+}
+
+// One JSONL record per evaluated kernel (under mu_): where the rollout came
+// from (rollout thread, its rollout number, shard subtree, the tree edges
+// taken with the bound of each child on the path), what was measured, and
+// the candidate text whenever it improved the best. -1 = no value.
+void Search::log_eval(const Work& w, const ispc_time_result& r, int rc, const std::string& status, double t_now,
+                      bool improved) {
+  std::string path = "[", anc = "[";
+  {
+    std::lock_guard<std::mutex> lk(tree_mu_);
+    for (size_t k = 0; k < w.path.size(); ++k) {
+      const auto& [node, i] = w.path[k];
+      path += (k ? ", " : "") + std::to_string(i);
+      char b[48];
+      std::snprintf(b, sizeof(b), "%s%.1f", k ? ", " : "", node->kid_bound[size_t(i)] * 1e9);
+      anc += b;
+    }
+  }
+  path += "]";
+  anc += "]";
+  std::string compact = improved ? best_text_ : std::string();
+  std::replace(compact.begin(), compact.end(), '\n', ' ');
+  const bool timed = rc == ISPC_OK;
+  std::fprintf(log_,
+               "{\"i\": %lld, \"t\": %.4f, \"status\": \"%s\", \"median_ns\": %.1f, \"first_ns\": %.1f, "
+               "\"min_ns\": %.1f, \"bound_ns\": %.1f, \"incumbent_ns\": %.1f, \"hash\": \"%016llx\", "
+               "\"digest\": \"%016llx\", \"grid\": %llu, \"block\": %u, \"seed\": %llu, \"tid\": %d, \"rollout\": %lld, \"subtree\": %zu, "
+               "\"path\": %s, \"path_bounds_ns\": %s, \"best\": %s%s%s}\n",
+               (long long)st_.evaluations, t_now, status.c_str(), timed ? r.median_ns : -1.0,
+               timed ? r.first_ns : -1.0, timed ? r.min_ns : -1.0, w.bound_s * 1e9,
+               std::isfinite(inc_.seconds()) ? inc_.seconds() * 1e9 : -1.0, (unsigned long long)w.launch.source_hash,
+               (unsigned long long)w.digest, (unsigned long long)w.launch.grid_x,
+               w.launch.block[0] * w.launch.block[1] * w.launch.block[2], (unsigned long long)cfg_.seed, w.tid, (long long)w.rollout_no, w.root,
+               path.c_str(), anc.c_str(), improved ? "true" : "false", improved ? ", \"candidate\": " : "",
+               compact.c_str());
+}
+
+// Records the device-timeline end of the open step (under mu_).
+void Search::close_step() {
+  ispc_dev_mark(dev_, 1);
+  double ms = 0;
+  ispc_dev_mark_elapsed(dev_, 0, 1, &ms);
+  st_.device_step_ms = ms;
+  st_.device_busy_ms = step_busy_ms_;
+  step_busy_ms_ = 0;
+  step_open_ = false;
 }
 
 int Search::region_io(const char* name, void* host, size_t bytes, bool upload) {
@@ -905,8 +1056,7 @@ int Search::region_io(const char* name, void* host, size_t bytes, bool upload) {
 }
 
 void Search::start() {
-  for (int i = 0; i < cfg_.rollout_threads; ++i) threads_.emplace_back([this, i] { rollout_worker(i); });
-  for (int i = 0; i < cfg_.compile_threads; ++i) threads_.emplace_back([this, i] { compile_worker(i); });
+  for (int i = 0; i < workers_; ++i) threads_.emplace_back([this, i] { worker(i); });
   threads_.emplace_back([this] { launch_worker(); });
   pipeline_started_ = true;
 }
@@ -933,17 +1083,13 @@ int Search::step(int64_t evaluations, double max_seconds) {
     }
     cv_done_.wait_for(lk, std::chrono::milliseconds(50));
   }
-  if (late) {
-    // stop launching for this step once the in-flight kernel returns
-    cv_done_.wait(lk, [&] { return stop_ || !launching_; });
-  }
-  if (step_open_) {  // close the device-timeline step of an exhausted search
-    ispc_dev_mark(dev_, 1);
-    double ms = 0;
-    ispc_dev_mark_elapsed(dev_, 0, 1, &ms);
-    st_.device_step_ms = ms;
-    step_open_ = false;
-  }
+  // lower the target first: the launch thread then stops at its next batch
+  // boundary and releases launching_ (else it could keep taking batches while
+  // evaluations < the old target and starve this wait past the deadline)
+  target_ = st_.evaluations;
+  cv_done_.notify_all();
+  if (late) cv_done_.wait(lk, [&] { return stop_ || !launching_; });
+  if (step_open_) close_step();  // the device-timeline end of an exhausted / late step
   target_ = st_.evaluations;
   if (stop_ && !err_.empty()) return ISPC_E_STICKY;
   return late ? ISPC_E_TIMEOUT : ISPC_OK;
@@ -963,6 +1109,8 @@ ispc_search_stats Search::stats() const {
   s.incumbent_ns = inc_.seconds() * 1e9;
   s.exhausted = exhausted_ ? 1 : 0;
   s.elapsed_s = now() - t0_;
+  s.refined = refined_;
+  s.t_launch_host_s = t_launch_host_;
   return s;
 }
 
@@ -1022,6 +1170,8 @@ int ispc_bound(const ispc_space* s, const ispc_cand* c, int l2_flushed, ispc_bou
     out->dram_bytes = r.dram_bytes;
     out->blocks_max = r.blocks_max;
     out->threads_per_block_max = r.threads_per_block_max;
+    out->dispatch = r.dispatch;
+    out->l1 = r.l1;
     return ISPC_OK;
   } catch (const std::exception& e) {
     return set_err(ISPC_E_ARG, e.what());

@@ -41,11 +41,14 @@
 namespace ispc_host {
 
 struct Incumbent {
-  std::atomic<uint64_t>* cell = nullptr;  // best measured time, ns (UINT64_MAX: none)
+  std::atomic<uint64_t>* cell = nullptr;  // best measured time, ns (0: none yet)
   void* map = nullptr;
   size_t map_bytes = 0;
+  bool pinned = false;
+  std::string name;
   std::unique_ptr<std::atomic<uint64_t>> local;
   void open(const char* shm_name);
+  void pin();
   ~Incumbent();
   double seconds() const;
   bool offer(uint64_t ns);  // true when it became the new best
@@ -77,6 +80,8 @@ struct Work {
   double bound_s = 0;
   uint64_t digest = 0;
   size_t root = 0;  // index of the shard subtree the leaf came from
+  int tid = 0;             // rollout thread that produced it
+  int64_t rollout_no = 0;  // that thread's rollout counter
   bool bit_exact = true;  // parity-mode and FFMA sgemm outputs: identical bits
   double rtol = 1e-5;     // otherwise: |out - exp| <= rtol * sum |products|
 };
@@ -84,6 +89,44 @@ struct Work {
 struct CompiledBatch {
   std::vector<std::unique_ptr<Work>> items;
   ispc_module* module = nullptr;
+  int handle = 0;       // loaded on the device by the compile thread (0: not loaded)
+  int load_rc = 0;      // ispc_module_load status
+  std::string load_err;
+};
+
+// Digests of partial candidates every completion of which is pruned or was
+// already produced (a dead end a rollout ran into, or a leaf it emitted).
+// The pruning threshold only falls, so membership is permanent; descents skip
+// such children instead of walking into them again. Sharded for the rollout
+// threads.
+class DeadSet {
+ public:
+  bool has(uint64_t d) {
+    Shard& s = shards_[d % kShards];
+    std::lock_guard<std::mutex> lk(s.mu);
+    return s.set.count(d) != 0;
+  }
+  void add(uint64_t d) {
+    Shard& s = shards_[d % kShards];
+    std::lock_guard<std::mutex> lk(s.mu);
+    s.set.insert(d);
+  }
+  size_t size() {
+    size_t n = 0;
+    for (Shard& s : shards_) {
+      std::lock_guard<std::mutex> lk(s.mu);
+      n += s.set.size();
+    }
+    return n;
+  }
+
+ private:
+  static constexpr size_t kShards = 64;
+  struct Shard {
+    std::mutex mu;
+    std::unordered_set<uint64_t> set;
+  };
+  Shard shards_[kShards];
 };
 
 class Search {
@@ -129,6 +172,7 @@ class Search {
   // again backtracks to an untried sibling instead of re-emitting it
   std::unordered_set<uint64_t> seen_leaf_;
   std::mutex seen_leaf_mu_;
+  DeadSet dead_;
   static constexpr int kRolloutExpansions = 96;  // node expansions one rollout may spend backtracking
   std::vector<std::thread> threads_;
   std::atomic<bool> stop_{false};
@@ -194,6 +238,15 @@ class Search {
   std::atomic<int> compiling_{0};  // batches inside NVRTC right now
   void note_fruitless();
   std::atomic<double> t_rollout_{0}, t_compile_{0};
+  double t_launch_host_ = 0;     // launch thread outside device waits (under mu_)
+  double step_busy_ms_ = 0;      // device time of timed launches in the open step (under mu_)
+  int64_t refined_ = 0;          // under mu_
+  double refine_factor_ = 1.25;
+  bool uniform_ = false;         // ISPC_WALK_UNIFORM
+  std::vector<int> retired_;     // loaded modules already evaluated (launch thread only)
+  static constexpr size_t kMaxRetired = 4096;
+  bool log_dead_ = false;        // ISPC_LOG_DEADENDS=1: JSONL records of rollouts that queued no kernel
+  bool uniform_walk(std::mt19937_64& rng, ispace::Candidate& leaf);
   double t0_ = 0;
   std::string best_text_, best_src_;
   ispc_launch best_launch_{};
@@ -212,9 +265,15 @@ class Search {
   int tree_depth_ = 12;
   int select_child(MctsNode& n, double T, std::mt19937_64& rng);
   void backprop(const std::vector<std::pair<MctsNode*, int>>& path, double ns);
-  void rollout_worker(int tid);
-  void compile_worker(int tid);
+  void worker(int tid);
+  void rollout_one(int tid, std::mt19937_64& rng, int64_t& k_roll, const ispc_emit_opts& eo);
+  void compile_items(std::vector<std::unique_ptr<Work>> items);
+  int workers_ = 1;  // host threads sharing rollouts and NVRTC
   void launch_worker();
+  void close_step();
+  void log_eval(const Work& w, const ispc_time_result& r, int rc, const std::string& status, double t_now,
+                bool improved);
+  void log_dead(int tid, int64_t rollout_no, const char* reason);  // from the rollout threads (stdio locks)
   void start();
   double now() const;
 };

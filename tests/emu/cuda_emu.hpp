@@ -115,6 +115,7 @@ inline float ispc_dsmem_ld(const float* p, unsigned) { return *p; }
 inline float4 ispc_dsmem_ld4(const float* p, unsigned) { return emu_ld(reinterpret_cast<const float4*>(p)); }
 
 inline int ispc_timeout_flag = 0;
+inline unsigned long long ispc_deadline_at = ~0ull;  // the emulator never times out
 inline unsigned long long ispc_now() { return 0; }
 alignas(16) inline float ispc_smem[1 << 16];
 
