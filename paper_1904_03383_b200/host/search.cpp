@@ -745,6 +745,13 @@ void Search::compile_items(std::vector<std::unique_ptr<Work>> items) {
   for (auto& w : items) srcs.push_back(w->src.c_str());
   ispc_module* m = nullptr;
   int rc = ispc_compile(srcs.data(), int(srcs.size()), "sm_100a", &m);
+  if (const char* dir = std::getenv("ISPC_DUMP_DIR")) {  // the compiled programs, for compile-cost studies
+    static std::atomic<int> seq{0};
+    if (FILE* f = std::fopen((std::string(dir) + "/prog" + std::to_string(seq++) + ".cu").c_str(), "w")) {
+      for (const char* x : srcs) std::fputs(x, f);
+      std::fclose(f);
+    }
+  }
   if (trace_) {
     size_t bytes = 0;
     for (auto& w : items) bytes += w->src.size();

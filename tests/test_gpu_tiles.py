@@ -171,69 +171,81 @@ def test_batched_small_readback_bit_exact(dev):
 
 @pytest.mark.parametrize("engine", ["TF32", "TF32X3"])
 def test_tcgen05_sgemm(dev, engine):
+    """Random leaves of one engine: every leaf the emitter accepts runs and
+    checks on the device (the device never reports illegal what the host
+    emitted), and at least 8 of 40 descents reach such a leaf."""
+    from paper_1904_03383_b200 import EmitError, tile_cuda
     space = Space("sgemm_tc", m=512, n=512, k=256)
     dev.bind(space.problem())
+    root = space.root().decide("engine", ["kernel"], engine)
     ok = 0
-    for leaf in _leaves(space, 40):
+    for seed in range(40):
+        try:
+            leaf, _, _ = root.random_leaf(seed)
+        except DeadEnd:
+            continue
         t = leaf.tiles()
-        if N.ENGINES[t.engine] != engine:
-            continue
+        try:
+            tile_cuda(t, "probe")
+        except EmitError:
+            continue  # statically illegal (e.g. a ring deeper than 227 KiB)
         m = dev.evaluate_tiles(t, reps=1, warmup=0)
-        if m.status == "illegal":  # e.g. a ring deeper than 227 KiB
-            continue
         assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
         ok += 1
-    assert ok >= 1
+    assert ok >= 8, ok
 
 
+# static legality of the variants below (emitter rules, checked on the host):
+# 3xTF32 on one CTA with TMA-staged A cannot hold a BN 256 ring of 3 stages
+TC_ILLEGAL = {("TF32X3", "TMA", "1", "256")}
+
+
+@pytest.mark.parametrize("bn", ["64", "128", "256"])
 @pytest.mark.parametrize("engine", ["TF32", "TF32X3"])
 @pytest.mark.parametrize("staging", ["TMA", "SHARED"])
 @pytest.mark.parametrize("pair", ["1", "2"])
-def test_tcgen05_staging_and_pairs(dev, engine, staging, pair):
+def test_tcgen05_staging_and_pairs(dev, engine, staging, pair, bn):
     """A staged by TMA or through registers; one CTA per UMMA or a
-    cta_group::2 pair (M = 256 over two SMs, B split between them)."""
+    cta_group::2 pair (M = 256 over two SMs, B split between them). Every
+    variant outside TC_ILLEGAL must run and check."""
+    from paper_1904_03383_b200 import EmitError, tile_cuda
     space = Space("sgemm_tc", m=512, n=768, k=192)
     dev.bind(space.problem())
-    ok = 0
-    for bn in ("64", "128", "256"):
-        c = space.root()
-        try:
-            c.decide("engine", ["kernel"], engine).decide("staging", ["kernel"], staging)
-            c.decide("tile", ["split"], pair).decide("tile", ["bn"], bn).decide("tile", ["stages"], "3")
-        except (DeadEnd, ValueError):
-            continue
-        t = c.first_leaf().tiles()
-        m = dev.evaluate_tiles(t, reps=1, warmup=0)
-        if m.status == "illegal":
-            continue
-        assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
-        assert m.launch.cluster[0] == (2 if pair == "2" else 0)
-        ok += 1
-    assert ok >= 1
+    c = space.root()
+    c.decide("engine", ["kernel"], engine).decide("staging", ["kernel"], staging)
+    c.decide("tile", ["split"], pair).decide("tile", ["bn"], bn).decide("tile", ["stages"], "3")
+    t = c.first_leaf().tiles()
+    if (engine, staging, pair, bn) in TC_ILLEGAL:
+        with pytest.raises(EmitError):
+            tile_cuda(t, "probe")
+        return
+    m = dev.evaluate_tiles(t, reps=1, warmup=0)
+    assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
+    assert m.launch.cluster[0] == (2 if pair == "2" else 0)
 
 
 @pytest.mark.parametrize("engine", ["TF32", "TF32X3"])
 @pytest.mark.parametrize("pair", ["1", "2", "4"])
-def test_tcgen05_persistent(dev, engine, pair):
+@pytest.mark.parametrize("staging,bn", [("TMA", "64"), ("SHARED", "128")])
+def test_tcgen05_persistent(dev, engine, pair, staging, bn):
     """Persistent grid (148 CTAs): several tiles per CTA through one running
     ring and a double-buffered TMEM accumulator; split 4 = two pairs sharing
-    the A boxes by TMA multicast."""
+    the A boxes by TMA multicast (so it needs TMA-staged A)."""
+    from paper_1904_03383_b200 import EmitError, tile_cuda
     space = Space("sgemm_tc", m=2048, n=2048, k=96)
     dev.bind(space.problem())
-    ok = 0
-    for staging, bn in (("TMA", "64"), ("SHARED", "128")):
-        c = space.root()
-        c.decide("engine", ["kernel"], engine).decide("staging", ["kernel"], staging)
-        c.decide("tile", ["split"], pair).decide("tile", ["bn"], bn).decide("tile", ["stages"], "4")
-        c.decide("tile", ["grid"], "148")
-        t = c.first_leaf().tiles()
-        m = dev.evaluate_tiles(t, reps=2, warmup=1)
-        if m.status == "illegal":
-            continue
-        assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
-        assert m.launch.grid_x == 148
-        ok += 1
-    assert ok >= 1
+    c = space.root()
+    c.decide("engine", ["kernel"], engine).decide("staging", ["kernel"], staging)
+    c.decide("tile", ["split"], pair).decide("tile", ["bn"], bn).decide("tile", ["stages"], "4")
+    c.decide("tile", ["grid"], "148")
+    t = c.first_leaf().tiles()
+    if pair == "4" and staging == "SHARED":
+        with pytest.raises(EmitError, match="multicast"):
+            tile_cuda(t, "probe")
+        return
+    m = dev.evaluate_tiles(t, reps=2, warmup=1)
+    assert m.status == "ok" and m.mismatches == 0, (t.as_dict(), m, dev.error())
+    assert m.launch.grid_x == 148
 
 
 @pytest.mark.parametrize("split", ["2", "4", "8"])
