@@ -50,6 +50,8 @@ BoundModel::BoundModel(const Kernel& k, const SpaceContext& ctx, const B200Machi
   v_vector_ = vindex(ctx, kind_c, "VECTOR");
   v_merged_ = vindex(ctx, order_c_, "MERGED");
   v_global_ = vindex(ctx, space_c, "GLOBAL");
+  std::uint32_t cache_c = choice_id(ctx, "cache");
+  v_cache_l2_ = vindex(ctx, cache_c, "L2");
 
   std::map<ObjId, std::size_t> dim_index;
   for (const auto& [id, di] : k.dims) {
@@ -85,6 +87,7 @@ BoundModel::BoundModel(const Kernel& k, const SpaceContext& ctx, const B200Machi
     r.memory = ii.op == Op::Load || ii.op == Op::Store;
     r.load = ii.op == Op::Load;
     r.region = ii.region;
+    if (r.memory) r.cache_inst = ctx.table.find(cache_c, id);
     r.stride_terms.resize(ii.dims.size());
     if (r.memory && ii.ivar != kNoIndex)
       for (const AddrTerm& t : k.ivars[ii.ivar].terms)
@@ -187,6 +190,21 @@ BoundReport BoundModel::bound(const Candidate& c) const {
     for (auto& [r, e] : comp) blocks_lo *= e;
     if (blocks_lo > 2147483647.0) return illegal(Illegal::Grid);
   }
+  // threads per block every completion has at least (certainly-THREAD dims)
+  double threads_lo = 1;
+  {
+    UF pm(nd);
+    for (std::size_t a = 0; a < nd; ++a)
+      for (std::size_t b = a + 1; b < nd; ++b)
+        if (is(a, v_thread_) && is(b, v_thread_) && may_merge(a, b)) pm.unite(a, b);
+    std::map<std::size_t, double> comp;
+    for (std::size_t d = 0; d < nd; ++d)
+      if (is(d, v_thread_)) comp[pm.find(d)] = std::max(comp[pm.find(d)], lo[d]);
+    for (auto& [r, e] : comp) threads_lo *= e;
+  }
+  const double resident = std::max(1.0, std::min<double>(m_.max_blocks_per_sm,
+                                                         std::floor(m_.max_threads_per_sm / std::max(threads_lo, 1.0))));
+  const double waves = std::ceil(blocks_lo / (double(m_.sms) * resident));
   // per-thread register arrays and unrolled body
   {
     double regs = 0, unrolled = 0;
@@ -248,7 +266,8 @@ BoundReport BoundModel::bound(const Candidate& c) const {
       double trips = 1;
       for (std::size_t d : r.dims)
         if (is(d, v_loop_)) trips *= lo[d];
-      load_chain = std::max(load_chain, trips);
+      const bool cg = r.cache_inst != kNoInstance && c.dom[r.cache_inst] == bit(v_cache_l2_);
+      load_chain = std::max(load_chain, trips * (cg ? m_.l2_load_latency_cycles : m_.min_load_latency_cycles));
     }
     if (r.memory) {
       double& t = region_touch[r.region];
@@ -303,7 +322,7 @@ BoundReport BoundModel::bound(const Candidate& c) const {
   rep.dram = dram_bytes / m_.hbm_bytes_per_s;
   rep.sm_mem = (input_bytes + tmp_lsu) / (sms * m_.sm_bytes_per_cycle * f);
   rep.issue = warp_insts / (sms * m_.issue_per_sm_cycle * f);
-  rep.thread = std::max(thread_trips, load_chain * m_.min_load_latency_cycles) / f;
+  rep.thread = std::max(1.0, waves) * std::max(thread_trips, load_chain) / f;
   rep.launch = m_.launch_floor_s;
   rep.dispatch = blocks_lo * m_.block_dispatch_s;
   rep.l1 = l1_lines / (sms * m_.l1_lines_per_cycle * f);

@@ -18,7 +18,10 @@
 //           lanes)) / (active SMs x 4 schedulers x f_max)
 //   thread  the sequential trips of one thread: every dim that cannot become
 //           BLOCK/THREAD/VECTOR multiplies by its smallest possible extent;
-//           one instruction per cycle at f_max
+//           one instruction per cycle at f_max, and each trip of the LOOPs
+//           around a load waits for it (29 cycles, 234 for ld.global.cg);
+//           times the waves the grid needs (blocks / (148 x resident blocks
+//           per SM, <= 32 and <= 2048 / threads per block))
 //   launch  1 us launch floor
 //   dispatch  the blocks every completion launches x 0.5 ns: the B200's block
 //           dispatch rate, measured with empty blocks (0.517 ns/block for
@@ -68,6 +71,14 @@ struct B200Machine {
   // LOOP dimensions around a load waits at least the fastest load latency
   // (LDS 29 cycles, L1 hit 31.8; B300_MICROARCH.md)
   double min_load_latency_cycles = 29;
+  // an ld.global.cg (cache = L2) bypasses L1: at least an L2 hit (234 cycles
+  // near-die, B300_MICROARCH.md)
+  double l2_load_latency_cycles = 234;
+  // residency: at most 32 blocks and 2048 threads per SM, so a grid runs in
+  // waves of 148 x that many blocks, each wave at least one block's
+  // sequential time
+  int max_blocks_per_sm = 32;
+  int max_threads_per_sm = 2048;
   double block_dispatch_s = 0.5e-9;  // per block, whatever the block does
   double l1_lines_per_cycle = 2;     // per SM (the L1 serves ~1 wavefront/clk; 2 keeps a margin)
 };
@@ -104,6 +115,7 @@ class BoundModel {
     bool memory;
     bool load;
     ispace::ObjId region;
+    std::uint32_t cache_inst = ~0u;  // cache(inst), memory instructions
     // per position of `dims`: the address terms of that dim, (base, indices
     // of the dims whose sizes multiply it) - its element stride
     std::vector<std::vector<std::pair<double, std::vector<std::size_t>>>> stride_terms;
@@ -130,7 +142,7 @@ class BoundModel {
   std::vector<RegionRec> regions_;
   std::vector<std::vector<std::uint32_t>> pair_order_;  // order(a,b) instance per dim pair
   int v_loop_ = 0, v_block_ = 1, v_thread_ = 2, v_unroll_ = 3, v_vector_ = 4;
-  int v_merged_ = 4, v_global_ = 0;
+  int v_merged_ = 4, v_global_ = 0, v_cache_l2_ = 1;
   std::uint32_t order_c_ = 0;
 
   ispace::Mask kinds(const ispace::Candidate& c, std::size_t d) const;
