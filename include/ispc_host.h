@@ -106,6 +106,65 @@ int ispc_estimate_tree(const ispc_space* s, const ispc_cand* from, int64_t probe
 /* Exhaustive first-open enumeration; returns the number of leaves (capped). */
 int64_t ispc_count_leaves(const ispc_space* s, const ispc_cand* from, int64_t cap);
 
+/* ---- tree-size estimators, enumeration, dead ends, prune profile ----------
+ * The reference's tree_size.cpp is a stub (proj/core/src/tree_size.cpp:1);
+ * contract SPEC.md:516-567 and paper sections 5.2-5.4. The tree below `from`
+ * branches on the first open instance (or the first in `order`, comma
+ * separated choice names); children are the values surviving apply_decision. */
+typedef struct {
+  double leaves, leaves_stderr;  /* estimate of the leaf count, its standard error */
+  double nodes, nodes_stderr;    /* estimate of the node count                    */
+  double dead_ratio;             /* knuth: probes ending at a dead end;
+                                    chen: runs reaching no leaf                   */
+  int64_t iterations;            /* knuth probes / chen runs                      */
+  int32_t method;                /* 0 knuth, 1 chen                               */
+  int32_t _pad;
+} ispc_tree_estimate;
+/* method "knuth" (random descents, product of branching factors) or "chen"
+ * (heuristic sampling over strata; stratifier "depth_remaining" = the paper's
+ * (depth, remaining open instances) pair, "depth", "remaining", or "constant",
+ * which violates strict decrease and is reported as ISPC_E_ARG). */
+int ispc_estimate(const ispc_space* s, const ispc_cand* from, const char* method, int64_t iterations,
+                  uint64_t seed, const char* order, const char* stratifier, ispc_tree_estimate* out);
+/* The same estimators on closed-form trees (their known answers):
+ * "uniform:B,D", "caterpillar:D,H", "random:S,B,D". */
+int ispc_estimate_synthetic(const char* tree, const char* method, int64_t iterations, uint64_t seed,
+                            const char* stratifier, ispc_tree_estimate* out);
+typedef struct {
+  int64_t nodes, leaves, dead_ends, max_depth;
+} ispc_enum_report;
+/* Exact depth-first enumeration; ISPC_E_ARG (refusal) past node_budget nodes.
+ * per_depth[d] (d < depth_cap) = nodes at depth d. */
+int ispc_enumerate(const ispc_space* s, const ispc_cand* from, const char* order, int64_t node_budget,
+                   ispc_enum_report* out, int64_t* per_depth, int depth_cap);
+int ispc_enumerate_synthetic(const char* tree, int64_t node_budget, ispc_enum_report* out, int64_t* per_depth,
+                             int depth_cap);
+typedef struct {
+  int64_t trials, dead_ends;
+  double ratio, ci_lo, ci_hi;  /* 95% Wilson score interval */
+  double mean_decisions;
+} ispc_deadend_report;
+/* Uniform random descents without pruning (paper section 5.2, Table 2). */
+int ispc_deadend_rate(const ispc_space* s, const ispc_cand* from, int64_t trials, uint64_t seed, const char* order,
+                      ispc_deadend_report* out);
+/* A uniform partial descent of `steps` decisions among the surviving
+ * children (subtrees for the estimator oracles). 1: dead end or leaf first. */
+int ispc_cand_descend(const ispc_space* s, const ispc_cand* from, const char* order, uint64_t seed, int steps,
+                      ispc_cand** out);
+/* Exact probability that such a descent meets a dead end (small trees;
+ * ISPC_E_ARG past node_budget nodes): the oracle of ispc_deadend_rate. */
+int ispc_deadend_exact(const ispc_space* s, const ispc_cand* from, const char* order, int64_t node_budget,
+                       double* p_dead);
+/* The lowest-bound descent: children in ascending B200 bound (ties: value
+ * order), backtracking out of dead ends and infinite-bound subtrees; 1 when
+ * no leaf is found within its node budget. */
+int ispc_greedy_leaf(const ispc_space* s, const ispc_cand* from, const char* order, ispc_cand** out,
+                     double* bound_s);
+/* Paper section 5.4: nodes per depth of the first depth_cap levels and how
+ * many have a B200 bound >= threshold_s (prunable against incumbent T). */
+int ispc_prune_profile(const ispc_space* s, const ispc_cand* from, const char* order, double threshold_s,
+                       int depth_cap, int64_t node_budget, int64_t* nodes_per_depth, int64_t* pruned_per_depth);
+
 /* Building-block spaces: the decided tile configuration (ispc.h). */
 int ispc_cand_to_tiles(const ispc_space* s, const ispc_cand* c, ispc_tile_config* out);
 
@@ -120,6 +179,46 @@ int ispc_cand_reference_source(const ispc_space* s, const ispc_cand* c, char* bu
 int ispc_cand_simulate(const ispc_space* s, const ispc_cand* c, int64_t out[5]);
 int ispc_cand_serialize(const ispc_space* s, const ispc_cand* c, char* buf, size_t cap, size_t* len);
 int ispc_cand_deserialize(const ispc_space* s, const char* text, ispc_cand** out);
+
+/* ---- deterministic TAG-MCTS ------------------------------
+ * Single-threaded, no clocks: the same seed and configuration give the same
+ * evaluations, best candidate and byte-identical JSONL log (one record per
+ * rollout: seed, path of decision values, cost or DEADEND, ancestor bounds).
+ * Evaluators: BOUND = the B200 bound x (1 + u), u in [0, 0.5) hashed from the
+ * leaf digest (admissible by construction: pruning on and off must agree on
+ * the optimum); SIMULATE = the reference's reconstruct + evaluate cycles
+ * (simulate.cpp:131-133) with a zero bound. */
+enum ispc_spec_evaluator { ISPC_SPEC_EVAL_BOUND = 0, ISPC_SPEC_EVAL_SIMULATE = 1 };
+typedef struct {
+  int64_t budget;        /* evaluations (distinct leaves)                      */
+  int64_t max_rollouts;  /* 0: unlimited                                       */
+  uint64_t seed;
+  const char* order;     /* comma separated choice names; NULL: first open     */
+  int32_t pruning;       /* exclude / zero-weight children with bound >= T     */
+  int32_t evaluator;     /* ispc_spec_evaluator                                */
+  double delta;          /* TAG confidence (0: 0.05)                           */
+  int32_t bucket;        /* TAG top-s set size (0: 20)                         */
+  int32_t _pad;
+  const char* log_path;  /* JSONL per rollout, NULL: none                      */
+} ispc_spec_config;
+typedef struct {
+  int64_t evaluations, rollouts, dead_rollouts, expanded, duplicates;
+  int64_t time_to_best_evals;  /* evaluations when the best was first met     */
+  int32_t exhausted;           /* the whole tree was evaluated or excluded     */
+  int32_t _pad;
+  double best_cost;            /* seconds (BOUND) or cycles (SIMULATE); inf: none */
+  uint64_t best_digest;
+} ispc_spec_result;
+int ispc_explore_spec(const ispc_space* s, const ispc_spec_config* cfg, ispc_spec_result* out, char* best_text,
+                      size_t cap, size_t* len);
+/* The TAG rule: unvisited (t <= 0) non-excluded children first, lowest index;
+ * then argmax (s + a + sqrt(2 s a + a^2)) / t with a = ln(2 total k / delta);
+ * -1 when every child is excluded. */
+int ispc_tag_select(int k, const double* s, const double* t, const unsigned char* excluded, int64_t total,
+                    double delta, int bucket);
+/* Seeded uniform first-open descents sharing one mt19937_64(seed), the walk of
+ * oracle/ref_cpu_bench.cpp: leaf digest per walk, 0 for a dead end. */
+int ispc_walk_digests(const ispc_space* s, const ispc_cand* from, uint64_t seed, int64_t walks, uint64_t* digests);
 
 /* ---- B200 lower bound (seconds) ------------------------------------------- */
 typedef struct {

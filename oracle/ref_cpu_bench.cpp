@@ -9,7 +9,9 @@
 //
 // Usage: ref_cpu_bench <kind> <n|m> <n> <k> <seconds> <threads> <factor-list>...
 //   factor list: comma separated sizes per universe, e.g. 2,4 2,4,8,...,1024
-// Prints one JSON object.
+// Prints one JSON object. With REF_DUMP_WALKS=K in the environment it instead
+// runs thread 0's first K walks and prints their leaf digests (0 = dead end):
+// the walk ispc_walk_digests must reproduce (tests/test_spec_search.py).
 #include <atomic>
 #include <limits>
 #include <chrono>
@@ -60,6 +62,36 @@ int main(int argc, char** argv) {
   make_root(*br.ctx, root);
   double build_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 
+  if (const char* dump = std::getenv("REF_DUMP_WALKS")) {
+    std::mt19937_64 rng(0x190403383ull);  // thread 0's generator
+    const long long K = std::atoll(dump);
+    std::printf("{\"seed\": %llu, \"digests\": [", 0x190403383ull);
+    for (long long w = 0; w < K; ++w) {
+      Candidate cur = root;
+      bool ok = true;
+      for (;;) {
+        std::vector<std::uint32_t> open = open_choices(*br.ctx, cur);
+        if (open.empty()) break;
+        Mask m = cur.dom[open.front()];
+        int pick = int(rng() % std::uint64_t(mask_count(m)));
+        int v = 0;
+        for (int b = 0; b < kMaxDomainBits; ++b)
+          if (mask_has(m, b) && pick-- == 0) {
+            v = b;
+            break;
+          }
+        Candidate child;
+        if (apply_decision(*br.ctx, cur, open.front(), v, child) != PropStatus::Ok) {
+          ok = false;
+          break;
+        }
+        cur = std::move(child);
+      }
+      std::printf("%s\"%llu\"", w ? ", " : "", ok ? (unsigned long long)digest(*br.ctx, cur) : 0ull);
+    }
+    std::printf("]}\n");
+    return 0;
+  }
   std::atomic<long long> walks{0}, leaves{0}, decisions{0}, dead{0};
   std::atomic<long long> best{std::numeric_limits<long long>::max()};
   auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(seconds);

@@ -233,6 +233,37 @@ ISPC_SYMBOLS = {
                                       C.POINTER(TimeResult), C.POINTER(Launch)]),
 }
 
+class TreeEstimate(C.Structure):
+    _fields_ = [("leaves", C.c_double), ("leaves_stderr", C.c_double), ("nodes", C.c_double),
+                ("nodes_stderr", C.c_double), ("dead_ratio", C.c_double), ("iterations", C.c_int64),
+                ("method", C.c_int32), ("_pad", C.c_int32)]
+
+
+class EnumReport(C.Structure):
+    _fields_ = [("nodes", C.c_int64), ("leaves", C.c_int64), ("dead_ends", C.c_int64), ("max_depth", C.c_int64)]
+
+
+class DeadendReport(C.Structure):
+    _fields_ = [("trials", C.c_int64), ("dead_ends", C.c_int64), ("ratio", C.c_double), ("ci_lo", C.c_double),
+                ("ci_hi", C.c_double), ("mean_decisions", C.c_double)]
+
+
+class SpecConfig(C.Structure):
+    _fields_ = [("budget", C.c_int64), ("max_rollouts", C.c_int64), ("seed", C.c_uint64), ("order", C.c_char_p),
+                ("pruning", C.c_int32), ("evaluator", C.c_int32), ("delta", C.c_double), ("bucket", C.c_int32),
+                ("_pad", C.c_int32), ("log_path", C.c_char_p)]
+
+
+class SpecResult(C.Structure):
+    _fields_ = [("evaluations", C.c_int64), ("rollouts", C.c_int64), ("dead_rollouts", C.c_int64),
+                ("expanded", C.c_int64), ("duplicates", C.c_int64), ("time_to_best_evals", C.c_int64),
+                ("exhausted", C.c_int32), ("_pad", C.c_int32), ("best_cost", C.c_double),
+                ("best_digest", C.c_uint64)]
+
+
+SPEC_EVAL_BOUND, SPEC_EVAL_SIMULATE = 0, 1
+
+
 HOST_SYMBOLS = {
     "ispc_space_create": (C.c_int, [C.POINTER(KernelSpec), C.POINTER(C.c_void_p)]),
     "ispc_space_free": (None, [C.c_void_p]),
@@ -255,6 +286,28 @@ HOST_SYMBOLS = {
     "ispc_count_leaves": (C.c_int64, [C.c_void_p, C.c_void_p, C.c_int64]),
     "ispc_estimate_tree": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_uint64, C.c_char_p,
                                      C.POINTER(C.c_double)]),
+    "ispc_estimate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_int64, C.c_uint64, C.c_char_p,
+                                C.c_char_p, C.POINTER(TreeEstimate)]),
+    "ispc_estimate_synthetic": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int64, C.c_uint64, C.c_char_p,
+                                          C.POINTER(TreeEstimate)]),
+    "ispc_enumerate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_int64, C.POINTER(EnumReport),
+                                 C.POINTER(C.c_int64), C.c_int]),
+    "ispc_enumerate_synthetic": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(EnumReport), C.POINTER(C.c_int64),
+                                           C.c_int]),
+    "ispc_deadend_rate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_uint64, C.c_char_p,
+                                    C.POINTER(DeadendReport)]),
+    "ispc_deadend_exact": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_int64, C.POINTER(C.c_double)]),
+    "ispc_cand_descend": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_uint64, C.c_int,
+                                    C.POINTER(C.c_void_p)]),
+    "ispc_greedy_leaf": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p),
+                                   C.POINTER(C.c_double)]),
+    "ispc_prune_profile": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_double, C.c_int, C.c_int64,
+                                     C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "ispc_explore_spec": (C.c_int, [C.c_void_p, C.POINTER(SpecConfig), C.POINTER(SpecResult), C.c_char_p,
+                                    C.c_size_t, C.POINTER(C.c_size_t)]),
+    "ispc_tag_select": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_ubyte),
+                                  C.c_int64, C.c_double, C.c_int]),
+    "ispc_walk_digests": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int64, C.POINTER(C.c_uint64)]),
     "ispc_cand_to_nest": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
     "ispc_cand_to_tiles": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(TileConfig)]),
     "ispc_nest_buf_get": (C.POINTER(Nest), [C.c_void_p]),

@@ -16,6 +16,32 @@ from dataclasses import dataclass, field
 from . import _native as N
 
 
+def explore_spec(space: "Space", budget: int, *, seed: int = 1, order: str | None = None, pruning: bool = True,
+                 evaluator: str = "bound", delta: float = 0.05, bucket: int = 20, max_rollouts: int = 0,
+                 log_path: str | None = None) -> dict:
+    """Deterministic single-threaded TAG-MCTS with a CPU
+    evaluator: "bound" (the B200 bound x a digest-hashed factor in [1, 1.5),
+    admissible by construction) or "simulate" (the reference's cycles)."""
+    keep = [x.encode() if x else None for x in (order, log_path)]
+    cfg = N.SpecConfig(budget=budget, max_rollouts=max_rollouts, seed=seed, order=keep[0], pruning=int(pruning),
+                       evaluator={"bound": N.SPEC_EVAL_BOUND, "simulate": N.SPEC_EVAL_SIMULATE}[evaluator],
+                       delta=delta, bucket=bucket, log_path=keep[1])
+    r = N.SpecResult()
+    text = N.read_text(lambda *a: N.host().ispc_explore_spec(space._h, C.byref(cfg), C.byref(r), *a))
+    out = {f: getattr(r, f) for f, _ in N.SpecResult._fields_ if f != "_pad"}
+    out["exhausted"] = bool(out["exhausted"])
+    out["best"] = space.deserialize(text) if text else None
+    return out
+
+
+def tag_select(s: list[float], t: list[float], total: int, excluded: list[bool] | None = None,
+               delta: float = 0.05, bucket: int = 20) -> int:
+    """The TAG selection rule (ispc_tag_select); -1 when every child is excluded."""
+    k = len(s)
+    ex = (C.c_ubyte * k)(*[int(x) for x in (excluded or [False] * k)])
+    return N.host().ispc_tag_select(k, (C.c_double * k)(*s), (C.c_double * k)(*t), ex, total, delta, bucket)
+
+
 # ---------------------------------------------------------------- search space
 class Space:
     """A kernel backbone bound to the GPU decision space (gpu_space.hpp:15-18)."""
@@ -149,6 +175,93 @@ class Candidate:
     def count_leaves(self, cap: int = 10 ** 7) -> int:
         return N.host().ispc_count_leaves(self.space._h, self._h, cap)
 
+    def estimate(self, method: str = "knuth", iterations: int = 1000, seed: int = 1, order: str | None = None,
+                 stratifier: str = "depth_remaining") -> dict:
+        """Knuth's or Chen's estimate of the subtree below this candidate
+        (SPEC.md:516-567); ValueError for a stratifier that does not strictly
+        decrease along the tree."""
+        e = N.TreeEstimate()
+        rc = N.host().ispc_estimate(self.space._h, self._h, method.encode(), iterations, seed,
+                                    order.encode() if order else None, stratifier.encode(), C.byref(e))
+        if rc != 0:
+            raise ValueError(N.host_error())
+        return _estimate_dict(e)
+
+    def enumerate(self, node_budget: int = 10 ** 6, order: str | None = None, depth_cap: int = 64) -> dict:
+        """Exact node / leaf / dead-end counts and nodes per depth; ValueError
+        (a refusal) past `node_budget` nodes."""
+        r = N.EnumReport()
+        per = (C.c_int64 * depth_cap)()
+        rc = N.host().ispc_enumerate(self.space._h, self._h, order.encode() if order else None, node_budget,
+                                     C.byref(r), per, depth_cap)
+        if rc != 0:
+            raise ValueError(N.host_error())
+        return _enum_dict(r, per)
+
+    def deadend_rate(self, trials: int = 1000, seed: int = 1, order: str | None = None) -> dict:
+        """Share of uniform random descents ending at a dead end, 95% Wilson CI
+        (paper section 5.2)."""
+        r = N.DeadendReport()
+        rc = N.host().ispc_deadend_rate(self.space._h, self._h, trials, seed, order.encode() if order else None,
+                                        C.byref(r))
+        if rc != 0:
+            raise ValueError(N.host_error())
+        return {"trials": r.trials, "dead_ends": r.dead_ends, "ratio": r.ratio, "ci95": [r.ci_lo, r.ci_hi],
+                "mean_decisions": r.mean_decisions}
+
+    def greedy_leaf(self, order: str | None = None) -> tuple["Candidate", float]:
+        """The lowest-bound descent from here: (leaf, its bound in seconds)."""
+        h = C.c_void_p()
+        b = C.c_double()
+        rc = N.host().ispc_greedy_leaf(self.space._h, self._h, order.encode() if order else None, C.byref(h),
+                                       C.byref(b))
+        if rc == 1:
+            raise DeadEnd("greedy descent met a dead end")
+        if rc != 0:
+            raise ValueError(N.host_error())
+        return Candidate(self.space, h), b.value
+
+    def walk_digests(self, seed: int, walks: int) -> list[int]:
+        """Leaf digests of `walks` seeded uniform first-open descents sharing
+        one generator (oracle/ref_cpu_bench.cpp's walk); 0 = dead end."""
+        out = (C.c_uint64 * walks)()
+        if N.host().ispc_walk_digests(self.space._h, self._h, seed, walks, out) != 0:
+            raise ValueError(N.host_error())
+        return list(out)
+
+    def descend(self, steps: int, seed: int = 1, order: str | None = None) -> "Candidate":
+        """A uniform partial descent of `steps` decisions; DeadEnd when it
+        meets a dead end or a leaf first."""
+        h = C.c_void_p()
+        rc = N.host().ispc_cand_descend(self.space._h, self._h, order.encode() if order else None, seed, steps,
+                                        C.byref(h))
+        if rc == 1:
+            raise DeadEnd("partial descent ended early")
+        if rc != 0:
+            raise ValueError(N.host_error())
+        return Candidate(self.space, h)
+
+    def deadend_exact(self, node_budget: int = 10 ** 6, order: str | None = None) -> float:
+        """Exact dead-end probability of a uniform random descent from here."""
+        p = C.c_double()
+        if N.host().ispc_deadend_exact(self.space._h, self._h, order.encode() if order else None, node_budget,
+                                       C.byref(p)) != 0:
+            raise ValueError(N.host_error())
+        return p.value
+
+    def prune_profile(self, threshold_s: float, depth_cap: int, order: str | None = None,
+                      node_budget: int = 10 ** 6) -> dict:
+        """Nodes per depth of the first `depth_cap` levels and how many the B200
+        bound prunes against incumbent `threshold_s` (paper section 5.4)."""
+        nodes = (C.c_int64 * depth_cap)()
+        pruned = (C.c_int64 * depth_cap)()
+        rc = N.host().ispc_prune_profile(self.space._h, self._h, order.encode() if order else None, threshold_s,
+                                         depth_cap, node_budget, nodes, pruned)
+        if rc != 0:
+            raise ValueError(N.host_error())
+        return {"nodes": list(nodes), "pruned": list(pruned),
+                "fraction": [p / n if n else None for p, n in zip(pruned, nodes)]}
+
     def tiles(self) -> N.TileConfig:
         """Decided building-block configuration (tiles.space candidates)."""
         t = N.TileConfig()
@@ -180,6 +293,42 @@ class Candidate:
         if N.host().ispc_bound(self.space._h, self._h, int(l2_flushed), C.byref(r)) != 0:
             raise ValueError(N.host_error())
         return {f: getattr(r, f) for f, _ in N.BoundReport._fields_}
+
+
+def _estimate_dict(e) -> dict:
+    z = 1.959963984540054
+    return {"method": ("knuth", "chen")[e.method], "iterations": e.iterations, "leaves": e.leaves,
+            "leaves_stderr": e.leaves_stderr, "leaves_ci95": [e.leaves - z * e.leaves_stderr,
+                                                             e.leaves + z * e.leaves_stderr],
+            "nodes": e.nodes, "nodes_stderr": e.nodes_stderr, "dead_ratio": e.dead_ratio}
+
+
+def _enum_dict(r, per) -> dict:
+    depth = [int(v) for v in per]
+    while depth and depth[-1] == 0:
+        depth.pop()
+    return {"nodes": r.nodes, "leaves": r.leaves, "dead_ends": r.dead_ends, "max_depth": r.max_depth,
+            "nodes_per_depth": depth}
+
+
+def estimate_synthetic(tree: str, method: str = "knuth", iterations: int = 1000, seed: int = 1,
+                       stratifier: str = "depth_remaining") -> dict:
+    """The estimators on a closed-form tree ("uniform:B,D", "caterpillar:D,H",
+    "random:S,B,D"): their known answers."""
+    e = N.TreeEstimate()
+    rc = N.host().ispc_estimate_synthetic(tree.encode(), method.encode(), iterations, seed, stratifier.encode(),
+                                          C.byref(e))
+    if rc != 0:
+        raise ValueError(N.host_error())
+    return _estimate_dict(e)
+
+
+def enumerate_synthetic(tree: str, node_budget: int = 10 ** 7, depth_cap: int = 64) -> dict:
+    r = N.EnumReport()
+    per = (C.c_int64 * depth_cap)()
+    if N.host().ispc_enumerate_synthetic(tree.encode(), node_budget, C.byref(r), per, depth_cap) != 0:
+        raise ValueError(N.host_error())
+    return _enum_dict(r, per)
 
 
 class NestHandle:
@@ -372,6 +521,32 @@ class Device:
             return Measurement(N.STATUS.get(rc, str(rc)), float("inf"), float("inf"), float("inf"), 0.0, -1, L)
         return Measurement(N.STATUS.get(r.status, str(r.status)), r.median_ns, r.min_ns, r.first_ns, r.max_err,
                            r.mismatches, L)
+
+
+def explore_spec(space: "Space", budget: int, *, seed: int = 1, order: str | None = None, pruning: bool = True,
+                 evaluator: str = "bound", delta: float = 0.05, bucket: int = 20, max_rollouts: int = 0,
+                 log_path: str | None = None) -> dict:
+    """Deterministic single-threaded TAG-MCTS with a CPU
+    evaluator: "bound" (the B200 bound x a digest-hashed factor in [1, 1.5),
+    admissible by construction) or "simulate" (the reference's cycles)."""
+    keep = [x.encode() if x else None for x in (order, log_path)]
+    cfg = N.SpecConfig(budget=budget, max_rollouts=max_rollouts, seed=seed, order=keep[0], pruning=int(pruning),
+                       evaluator={"bound": N.SPEC_EVAL_BOUND, "simulate": N.SPEC_EVAL_SIMULATE}[evaluator],
+                       delta=delta, bucket=bucket, log_path=keep[1])
+    r = N.SpecResult()
+    text = N.read_text(lambda *a: N.host().ispc_explore_spec(space._h, C.byref(cfg), C.byref(r), *a))
+    out = {f: getattr(r, f) for f, _ in N.SpecResult._fields_ if f != "_pad"}
+    out["exhausted"] = bool(out["exhausted"])
+    out["best"] = space.deserialize(text) if text else None
+    return out
+
+
+def tag_select(s: list[float], t: list[float], total: int, excluded: list[bool] | None = None,
+               delta: float = 0.05, bucket: int = 20) -> int:
+    """The TAG selection rule (ispc_tag_select); -1 when every child is excluded."""
+    k = len(s)
+    ex = (C.c_ubyte * k)(*[int(x) for x in (excluded or [False] * k)])
+    return N.host().ispc_tag_select(k, (C.c_double * k)(*s), (C.c_double * k)(*t), ex, total, delta, bucket)
 
 
 # ---------------------------------------------------------------- search

@@ -103,59 +103,4 @@ void count_leaves(const SpaceContext& ctx, const Candidate& c, int64_t& n, int64
   }
 }
 
-// Knuth's estimator of the search-tree size (PAPER.md:
-// 1101-1133; the reference's tree_size.cpp is a stub): each probe descends
-// from `from`, branching on the next instance (by `order`, else the first
-// open one, the tree count_leaves walks), and multiplies the number of
-// children that survive propagation. A probe ending at a leaf estimates the
-// leaf count by that product, one ending at a dead end contributes 0; the
-// node estimate sums the partial products. Unbiased for both.
-TreeEstimate knuth_estimate(const SpaceContext& ctx, const Candidate& from, int64_t probes, std::mt19937_64& rng,
-                            const DecisionOrder* order) {
-  TreeEstimate e;
-  double sum = 0, sum2 = 0, nodes = 0;
-  int64_t dead = 0;
-  for (int64_t p = 0; p < probes; ++p) {
-    Candidate cur = from;
-    double w = 1, nd = 1, leaves = 0;
-    for (;;) {
-      std::uint32_t inst;
-      if (order) {
-        inst = order->pick(ctx, cur);
-      } else {
-        std::vector<std::uint32_t> open = open_choices(ctx, cur);
-        inst = open.empty() ? kNoInstance : open.front();
-      }
-      if (inst == kNoInstance) {
-        leaves = w;
-        break;
-      }
-      std::vector<Candidate> kids;
-      Mask m = cur.dom[inst];
-      for (int v = 0; v < kMaxDomainBits; ++v) {
-        if (!mask_has(m, v)) continue;
-        Candidate child;
-        if (apply_decision(ctx, cur, inst, v, child) == PropStatus::Ok) kids.push_back(std::move(child));
-      }
-      if (kids.empty()) {
-        ++dead;
-        break;
-      }
-      w *= double(kids.size());
-      nd += w;
-      cur = std::move(kids[size_t(rng() % kids.size())]);
-    }
-    sum += leaves;
-    sum2 += leaves * leaves;
-    nodes += nd;
-  }
-  const double n = double(std::max<int64_t>(probes, 1));
-  e.probes = probes;
-  e.leaves = sum / n;
-  e.leaves_stderr = probes > 1 ? std::sqrt(std::max(0.0, (sum2 / n - e.leaves * e.leaves) / (n - 1))) : 0;
-  e.nodes = nodes / n;
-  e.dead_probe_ratio = double(dead) / n;
-  return e;
-}
-
 }  // namespace ispc_host
