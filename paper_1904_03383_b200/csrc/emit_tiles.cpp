@@ -652,7 +652,148 @@ void gemm_copy_cp_async(std::ostringstream& o, const GemmShape& g, const ispc_ti
   o << indent << "}\n";
 }
 
+// Warp-tiled FFMA2 sgemm (CP_ASYNC staging, vec 4, tm and tn multiples of 4,
+// whole warps). The thr_m x thr_n threads form warps of LX x LY lanes
+// (LX = min(thr_m, 8)); a lane owns tm x tn outputs as (tm/4) x (tn/4)
+// blocks of 4 x 4, rows wm*LX*tm + (i/4)*LX*4 + lx*4 + i%4 and columns
+// wn*LY*tn + (j/4)*LY*4 + ly*4 + j%4, so a warp's fragment reads are LX (A)
+// and LY (B) distinct float4s: one shared-memory wavefront each. Both operands
+// are k-major in shared memory: As[bk][BM] by 16-byte cp.async, Bs[bk][BN+4]
+// by 4-byte cp.async (B transposed on the way in, lanes walking k, which is
+// contiguous in global). The per-k fragments are double buffered in
+// registers (the loads of step k+1 are issued before the FFMA2s of step k;
+// the last step of a tile loads the next tile's first fragment after the
+// tile barrier). FFMA2 (__ffma2_rn: two IEEE fmas per lane, the B value
+// broadcast) keeps each output one fmaf chain in ascending k: bit-identical
+// to the sequential oracle. B200 measurements behind this structure:
+// tools/sgemm_lab.cu (profiles/r2_sgemm_lab.md).
+bool sgemm_warp_tiled_ok(const ispc_tile_config& c) {
+  const int T = c.thr_m * c.thr_n;
+  return c.staging == ISPC_STAGE_CP_ASYNC && c.vec == 4 && c.tm % 4 == 0 && c.tn % 4 == 0 && c.tm <= 8 &&
+         c.tn <= 8 && T % 32 == 0 && c.stages >= 2 && c.bk >= 4 && c.thr_m >= 4 && 32 % std::min(c.thr_m, 8) == 0 &&
+         c.thr_n % (32 / std::min(c.thr_m, 8)) == 0;
+}
+
+std::string sgemm_warp_tiled(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
+  const int64_t M = c.m, N = c.n, K = c.k;
+  const int LX = std::min(c.thr_m, 8), LY = 32 / LX;
+  const int WX = c.thr_m / LX;
+  const int TM = c.tm, TN = c.tn, BK = c.bk, S = c.stages, T = c.thr_m * c.thr_n;
+  const int64_t BM = int64_t(c.thr_m) * TM, BN = int64_t(c.thr_n) * TN, LDB = BN + 4;
+  if (M % BM || N % BN) illegal("CTA tile does not divide the output");
+  const int SP = std::max(1, c.split);
+  if (SP > 8) illegal("cluster larger than 8 CTAs");
+  if (K % (int64_t(SP) * BK)) illegal("split-K slices do not divide K");
+  if ((BM * BN) % (4 * SP)) illegal("partial tile does not split across the cluster");
+  const int64_t KT = K / (int64_t(SP) * BK);
+  const int64_t a_tile = BK * BM, b_tile = BK * LDB, stage = a_tile + b_tile;
+  if (stage * S * 4 > 232448) illegal("shared-memory ring exceeds 227 KiB");
+  if (int64_t(TM) * TN > 64) illegal("more than 64 accumulators per thread");
+  std::ostringstream o;
+  o << "extern \"C\" __global__ void __launch_bounds__(" << T << ") " << fn
+    << "(const float* __restrict__ g_a, const float* __restrict__ g_b, float* __restrict__ g_c) {\n";
+  o << "  extern __shared__ __align__(16) float ispc_smem[];\n";
+  o << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n";
+  o << "  const int wm = warp % " << WX << ", wn = warp / " << WX << ", lx = lane % " << LX << ", ly = lane / " << LX
+    << ";\n";
+  o << "  const long long tile = blockIdx.x / " << SP << ";\n";
+  o << "  const int rank = " << (SP > 1 ? "(int)ispc_cluster_rank()" : "0") << ";\n";
+  o << "  const long long bm = tile % " << M / BM << ", bn = tile / " << M / BM << ";\n";
+  o << "  const long long kbase = (long long)rank * " << K / SP << "LL;\n";
+  o << "  const float* pa = g_a + bm * " << BM << "LL + kbase * " << M << "LL;\n";
+  o << "  const float* pb = g_b + bn * " << BN << "LL * " << K << "LL + kbase;\n";
+  o << "  const int arow = wm * " << LX * TM << " + lx * 4, bcol = wn * " << LY * TN << " + ly * 4;\n";
+  o << "  float acc[" << TN << "][" << TM << "];\n";
+  o << "  #pragma unroll\n  for (int j = 0; j < " << TN << "; ++j)\n    #pragma unroll\n    for (int i = 0; i < " << TM
+    << "; ++i) acc[j][i] = 0.0f;\n";
+  o << "  float fa[2][" << TM << "], fb[2][" << TN << "];\n";
+  // copies of k tile kt into ring slot `slot`
+  o << "  auto load = [&](int kt, int slot) {\n";
+  o << "    float* sA = ispc_smem + slot * " << stage << ";\n";
+  o << "    float* sB = sA + " << a_tile << ";\n";
+  o << "    const long long k0 = (long long)kt * " << BK << ";\n";
+  o << "    #pragma unroll\n    for (int ch = tid; ch < " << a_tile / 4 << "; ch += " << T << ") {\n";
+  o << "      const int kk = ch / " << BM / 4 << ", mm = (ch % " << BM / 4 << ") * 4;\n";
+  o << "      " << (c.cache == ISPC_CACHE_L1 ? "ispc_cp_async_ca16" : "ispc_cp_async_cg16") << "(sA + kk * " << BM
+    << " + mm, pa + mm + (k0 + kk) * " << M << "LL);\n    }\n";
+  o << "    #pragma unroll\n    for (int e = tid; e < " << BK * BN << "; e += " << T << ") {\n";
+  o << "      const int kk = e % " << BK << ", nn = e / " << BK << ";\n";
+  o << "      ispc_cp_async_ca4(sB + kk * " << LDB << " + nn, pb + k0 + kk + (long long)nn * " << K << "LL);\n    }\n";
+  o << "  };\n";
+  // the fragments of step k of a staged tile
+  o << "  auto frag = [&](int buf, const float* sA, const float* sB, int k) {\n";
+  for (int h = 0; h < TM / 4; ++h)
+    o << "    { const float4 t = *(const float4*)(sA + k * " << BM << " + arow + " << h * LX * 4 << "); fa[buf]["
+      << 4 * h << "] = t.x; fa[buf][" << 4 * h + 1 << "] = t.y; fa[buf][" << 4 * h + 2 << "] = t.z; fa[buf]["
+      << 4 * h + 3 << "] = t.w; }\n";
+  for (int h = 0; h < TN / 4; ++h)
+    o << "    { const float4 t = *(const float4*)(sB + k * " << LDB << " + bcol + " << h * LY * 4 << "); fb[buf]["
+      << 4 * h << "] = t.x; fb[buf][" << 4 * h + 1 << "] = t.y; fb[buf][" << 4 * h + 2 << "] = t.z; fb[buf]["
+      << 4 * h + 3 << "] = t.w; }\n";
+  o << "  };\n";
+  o << "  #pragma unroll\n  for (int s = 0; s < " << S - 1 << "; ++s) {\n    if (s < " << KT
+    << ") load(s, s);\n    ispc_cp_async_commit();\n  }\n";
+  o << "  ispc_cp_async_wait<" << S - 2 << ">();\n  __syncthreads();\n";
+  o << "  frag(0, ispc_smem, ispc_smem + " << a_tile << ", 0);\n";
+  o << "  #pragma unroll 1\n  for (int kt = 0; kt < " << KT << "; ++kt) {\n";
+  o << "    const float* sA = ispc_smem + (kt % " << S << ") * " << stage << ";\n";
+  o << "    const float* sB = sA + " << a_tile << ";\n";
+  o << "    #pragma unroll\n    for (int k = 0; k < " << BK << "; ++k) {\n";
+  o << "      if (k == " << BK - 1 << ") {  // the next tile's first fragment, after its barrier\n";
+  o << "        ispc_cp_async_wait<" << S - 2 << ">();\n        __syncthreads();\n";
+  o << "        const float* nA = ispc_smem + ((kt + 1) % " << S << ") * " << stage << ";\n";
+  o << "        frag((k + 1) & 1, nA, nA + " << a_tile << ", 0);\n";
+  o << "      } else {\n        frag((k + 1) & 1, sA, sB, k + 1);\n      }\n";
+  o << "      if (k == 0) {\n        const int nk = kt + " << S - 1 << ";\n        if (nk < " << KT
+    << ") load(nk, nk % " << S << ");\n        ispc_cp_async_commit();\n      }\n";
+  o << "      #pragma unroll\n      for (int j = 0; j < " << TN << "; ++j)\n";
+  o << "        #pragma unroll\n        for (int i = 0; i < " << TM << "; i += 2) {\n";
+  o << "          const float2 r = __ffma2_rn(make_float2(fa[k & 1][i], fa[k & 1][i + 1]), make_float2(fb[k & 1][j], "
+       "fb[k & 1][j]), make_float2(acc[j][i], acc[j][i + 1]));\n";
+  o << "          acc[j][i] = r.x; acc[j][i + 1] = r.y;\n        }\n";
+  o << "    }\n  }\n";
+  o << "  ispc_cp_async_wait<0>();\n";
+  if (SP == 1) {
+    o << "  #pragma unroll\n  for (int j = 0; j < " << TN << "; ++j) {\n";
+    o << "    const long long col = bn * " << BN << "LL + bcol + (j / 4) * " << LY * 4 << " + j % 4;\n";
+    o << "    #pragma unroll\n    for (int i = 0; i < " << TM << "; i += 4)\n";
+    o << "      *(float4*)(g_c + bm * " << BM << "LL + arow + (i / 4) * " << LX * 4
+      << " + col * " << M << "LL) = make_float4(acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]);\n  }\n";
+  } else {
+    // partial tile P[col][row] (rows contiguous) in this CTA's shared memory;
+    // CTA `rank` sums slice `rank` of every CTA's P in rank order and stores it
+    const int64_t slice = BM * BN / SP;
+    o << "  __syncthreads();\n  float* P = ispc_smem;\n";
+    o << "  #pragma unroll\n  for (int j = 0; j < " << TN << "; ++j)\n";
+    o << "    #pragma unroll\n    for (int i = 0; i < " << TM << "; i += 4)\n";
+    o << "      *(float4*)(P + (bcol + (j / 4) * " << LY * 4 << " + j % 4) * " << BM << " + arow + (i / 4) * " << LX * 4
+      << ") = make_float4(acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]);\n";
+    o << "  ispc_cluster_sync();\n";
+    o << "  for (int e = rank * " << slice << " + tid * 4; e < (rank + 1) * " << slice << "; e += " << 4 * T << ") {\n";
+    o << "    float4 s = ispc_dsmem_ld4(P + e, 0);\n";
+    o << "    #pragma unroll\n    for (int q = 1; q < " << SP << "; ++q) {\n";
+    o << "      const float4 t = ispc_dsmem_ld4(P + e, q);\n";
+    o << "      s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;\n    }\n";
+    o << "    const int col = e / " << BM << ", row = e % " << BM << ";\n";
+    o << "    *(float4*)(g_c + bm * " << BM << "LL + row + (bn * " << BN << "LL + col) * " << M << "LL) = s;\n  }\n";
+    o << "  ispc_cluster_sync();\n";
+    L.cluster[0] = uint32_t(SP);
+    L.cluster[1] = L.cluster[2] = 1;
+  }
+  o << "}\n";
+  L.grid_x = uint64_t(M / BM * (N / BN) * SP);
+  L.block[0] = uint32_t(T);
+  L.block[1] = L.block[2] = 1;
+  L.static_smem = uint32_t(std::max<int64_t>(stage * S, SP > 1 ? BM * BN : 0) * 4);
+  add_region(L, "a", M * K);
+  add_region(L, "b", K * N);
+  add_region(L, "c", M * N);
+  L.reg_elems = uint32_t(TM * TN);
+  return o.str();
+}
+
 std::string sgemm(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
+  if (sgemm_warp_tiled_ok(c)) return sgemm_warp_tiled(c, fn, L);
   const int64_t M = c.m, N = c.n, K = c.k;
   GemmShape g = gemm_shape(c, M, N, K);
   if (c.staging != ISPC_STAGE_SHARED && c.staging != ISPC_STAGE_CP_ASYNC)

@@ -79,6 +79,7 @@ inline float __fadd_rn(float a, float b) {
   return r;
 }
 inline float __fmaf_rn(float a, float b, float c) { return std::fmaf(a, b, c); }
+inline float2 __ffma2_rn(float2 a, float2 b, float2 c) { return {std::fmaf(a.x, b.x, c.x), std::fmaf(a.y, b.y, c.y)}; }
 
 #define __global__
 #define __device__

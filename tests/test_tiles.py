@@ -140,6 +140,29 @@ def test_sgemm_kernels_bit_exact_on_emulator():
     assert _emulate_all(s, want, root=s.root().decide("tile", ["split"], "1")) >= 5
 
 
+@pytest.mark.parametrize("cfg", [
+    dict(thr_m=8, thr_n=4, tm=4, tn=4, bk=8, stages=2),
+    dict(thr_m=4, thr_n=8, tm=8, tn=4, bk=4, stages=3),
+    dict(thr_m=16, thr_n=4, tm=4, tn=8, bk=16, stages=2),
+])
+def test_warp_tiled_ffma2_sgemm_bit_exact_on_emulator(cfg):
+    """The warp-tiled FFMA2 building block (CP_ASYNC, vec 4, tm/tn multiples of
+    4, whole warps): B transposed by 4-byte cp.async, fragments double
+    buffered, two fmas per FFMA2 in ascending k: bit-identical to the oracle."""
+    s = Space("sgemm", m=64, n=32, k=32)
+    c = s.root().decide("staging", ["kernel"], "CP_ASYNC")
+    for k, v in dict(cfg, vec=4, split=1).items():
+        c = c.decide("tile", [k], str(v))
+    t = c.first_leaf().tiles()
+    src, L = tile_cuda(t, "k_emu")
+    assert "__ffma2_rn" in src and "ispc_cp_async_ca4" in src
+    orc = Oracle()
+    r = _regions(orc, s.problem())
+    ref = orc.matmul(r["a"], r["b"], 64, 32, 32)
+    emu.run(src, L, r)
+    assert np.array_equal(r["c"].view(np.uint32), ref.view(np.uint32)), t.as_dict()
+
+
 def test_batched_kernels_bit_exact_on_emulator():
     s = Space("batched", m=8, n=8, k=16, batch=8)
     orc = Oracle()

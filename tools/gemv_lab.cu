@@ -1,0 +1,285 @@
+// Development probe (not product): what one launch can stream from HBM at the
+// gemv 4096^2 size (64 MiB), and gemv structures that approach it, timed like
+// the bench (back-to-back launches over rotating copies larger than L2).
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/gemv_lab tools/gemv_lab.cu -lcublas
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e = (x);                                                             \
+    if (e != cudaSuccess) {                                                          \
+      std::printf("CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+      std::exit(1);                                                                  \
+    }                                                                                \
+  } while (0)
+
+constexpr int M = 4096, N = 4096, NCOPY = 6, R = 48;
+
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// pure read: grid-stride over n4 float4s, U loads in flight per thread
+template <int U>
+__global__ void read_k(const float4* __restrict__ a, long long n4, float* out) {
+  float s = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < n4; i += U * stride) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld_stream(a + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) s += v[u].x + v[u].y + v[u].z + v[u].w;
+  }
+  for (; i < n4; i += stride) {
+    float4 v = ld_stream(a + i);
+    s += v.x + v.y + v.z + v.w;
+  }
+  if (s == 12345.678f) out[0] = s;
+}
+
+// pure read, contiguous chunk per CTA (each CTA walks its own 64 MiB / grid)
+template <int U>
+__global__ void read_chunk_k(const float4* __restrict__ a, long long n4, float* out) {
+  const long long per = n4 / gridDim.x;
+  const float4* p = a + per * blockIdx.x;
+  float s = 0;
+  long long i = threadIdx.x;
+  for (; i + (long long)(U - 1) * blockDim.x < per; i += (long long)U * blockDim.x) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld_stream(p + i + u * blockDim.x);
+#pragma unroll
+    for (int u = 0; u < U; ++u) s += v[u].x + v[u].y + v[u].z + v[u].w;
+  }
+  for (; i < per; i += blockDim.x) {
+    float4 v = ld_stream(p + i);
+    s += v.x + v.y + v.z + v.w;
+  }
+  if (s == 12345.678f) out[0] = s;
+}
+
+// gemv, column blocks: CTA c owns columns [c*CPB, (c+1)*CPB) for all M rows;
+// thread t owns rows 4t..4t+3 of each column of its slice (blockDim = M/4/RS
+// threads per row-slice... here: blockDim.x threads cover M rows as float4,
+// RS = M / (4 * blockDim.x) row groups per thread), U columns in flight.
+// Partial y of each CTA -> atomicAdd (norm-wise checked).
+template <int T, int U>
+__global__ void __launch_bounds__(T) gemv_cols_k(const float* __restrict__ A, const float* __restrict__ x,
+                                                 float* __restrict__ y, int cpb) {
+  constexpr int RG = M / 4 / T;  // float4 row groups per thread
+  float4 acc[RG];
+#pragma unroll
+  for (int r = 0; r < RG; ++r) acc[r] = make_float4(0, 0, 0, 0);
+  const int j0 = blockIdx.x * cpb;
+  for (int j = j0; j < j0 + cpb; j += U) {
+    float xs[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xs[u] = __ldg(x + j + u);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float4* col = (const float4*)(A + (long long)(j + u) * M);
+#pragma unroll
+      for (int r = 0; r < RG; ++r) {
+        float4 v = ld_stream(col + threadIdx.x + r * T);
+        acc[r].x = fmaf(v.x, xs[u], acc[r].x);
+        acc[r].y = fmaf(v.y, xs[u], acc[r].y);
+        acc[r].z = fmaf(v.z, xs[u], acc[r].z);
+        acc[r].w = fmaf(v.w, xs[u], acc[r].w);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RG; ++r) {
+    float* py = y + 4 * (threadIdx.x + r * T);
+    atomicAdd(py + 0, acc[r].x);
+    atomicAdd(py + 1, acc[r].y);
+    atomicAdd(py + 2, acc[r].z);
+    atomicAdd(py + 3, acc[r].w);
+  }
+}
+
+// pure read through a cp.async.bulk (TMA 1-D) ring: one elected thread per
+// CTA streams CH-byte chunks of the CTA's contiguous slice into S stages; all
+// threads consume each landed chunk
+template <int CH, int S>
+__global__ void __launch_bounds__(256) read_bulk_k(const float* __restrict__ a, long long n, float* out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) unsigned long long full[S], empty[S];
+  const long long per = n / gridDim.x;  // floats
+  const float* p = a + per * blockIdx.x;
+  const int nch = int(per * 4 / CH);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      unsigned fa = (unsigned)__cvta_generic_to_shared(&full[s]), ea = (unsigned)__cvta_generic_to_shared(&empty[s]);
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(fa));
+      asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(ea), "r"((int)blockDim.x));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  auto issue = [&](int c) {
+    const int s = c % S;
+    unsigned fa = (unsigned)__cvta_generic_to_shared(&full[s]);
+    unsigned dst = (unsigned)__cvta_generic_to_shared(smem + s * CH);
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(fa), "r"(CH));
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(p + (long long)c * (CH / 4)), "r"(CH), "r"(fa)
+                 : "memory");
+  };
+  if (threadIdx.x == 0)
+    for (int c = 0; c < S && c < nch; ++c) issue(c);
+  float sum = 0;
+  for (int c = 0; c < nch; ++c) {
+    const int s = c % S;
+    const unsigned ph = (c / S) & 1;
+    unsigned fa = (unsigned)__cvta_generic_to_shared(&full[s]);
+    asm volatile(
+        "{ .reg .pred P; W: mbarrier.try_wait.parity.shared.b64 P, [%0], %1; @!P bra W; }" ::"r"(fa), "r"(ph));
+    const float4* q = (const float4*)(smem + s * CH);
+    for (int i = threadIdx.x; i < CH / 16; i += blockDim.x) {
+      float4 v = q[i];
+      sum += v.x + v.y + v.z + v.w;
+    }
+    unsigned ea = (unsigned)__cvta_generic_to_shared(&empty[s]);
+    asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(ea));
+    if (threadIdx.x == 0 && c + S < nch) {
+      asm volatile(
+          "{ .reg .pred P; W2: mbarrier.try_wait.parity.shared.b64 P, [%0], %1; @!P bra W2; }" ::"r"(ea), "r"(ph));
+      issue(c + S);
+    }
+  }
+  if (sum == 12345.678f) out[0] = sum;
+}
+
+__global__ void zero_k(float* y, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = 0;
+}
+
+template <class F>
+float timeit(F launch, cudaStream_t st) {
+  for (int w = 0; w < 3; ++w) launch(w % NCOPY);
+  CK(cudaStreamSynchronize(st));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  std::vector<float> ts;
+  for (int t = 0; t < 7; ++t) {
+    cudaEventRecord(e0, st);
+    for (int r = 0; r < R; ++r) launch(r % NCOPY);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ts.push_back(ms * 1e3f / R);
+  }
+  CK(cudaGetLastError());
+  std::sort(ts.begin(), ts.end());
+  return ts[3];
+}
+
+int main() {
+  cudaStream_t st;
+  CK(cudaStreamCreate(&st));
+  const long long nA = (long long)M * N;
+  std::vector<float*> A(NCOPY), X(NCOPY), Y(NCOPY);
+  std::vector<float> h(nA);
+  srand(3);
+  for (auto& v : h) v = float(rand() % 2001 - 1000) / 1024.f;
+  for (int c = 0; c < NCOPY; ++c) {
+    CK(cudaMalloc(&A[c], nA * 4));
+    CK(cudaMalloc(&X[c], N * 4));
+    CK(cudaMalloc(&Y[c], M * 4));
+    CK(cudaMemcpy(A[c], h.data(), nA * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(X[c], h.data(), N * 4, cudaMemcpyHostToDevice));
+  }
+  float* out;
+  CK(cudaMalloc(&out, 64));
+  const double bytes_read = nA * 4.0, bytes_gemv = 4.0 * (nA + M + N);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  std::printf("SMs %d\n", sms);
+#define READ(U, G, T)                                                                                    \
+  {                                                                                                      \
+    float us = timeit([&](int c) { read_k<U><<<G, T, 0, st>>>((const float4*)A[c], nA / 4, out); }, st); \
+    std::printf("read grid-stride U%-2d grid %5d x %4d: %7.2f us  %7.1f GB/s\n", U, G, T, us, bytes_read / us / 1e3); \
+  }
+  READ(4, sms, 1024);
+  READ(8, sms, 1024);
+  READ(4, 2 * sms, 1024);
+  READ(8, 2 * sms, 512);
+  READ(16, 2 * sms, 512);
+  READ(8, 4 * sms, 512);
+  READ(4, 8 * sms, 256);
+  READ(8, 8 * sms, 256);
+  READ(16, 4 * sms, 256);
+  READ(8, 16 * sms, 128);
+  READ(16, 8 * sms, 128);
+#define CHUNK(U, G, T)                                                                                        \
+  {                                                                                                           \
+    float us = timeit([&](int c) { read_chunk_k<U><<<G, T, 0, st>>>((const float4*)A[c], nA / 4, out); }, st); \
+    std::printf("read chunked    U%-2d grid %5d x %4d: %7.2f us  %7.1f GB/s\n", U, G, T, us, bytes_read / us / 1e3); \
+  }
+  CHUNK(8, 2 * sms, 512);
+  CHUNK(8, 4 * sms, 256);
+  CHUNK(4, 1024, 256);
+  CHUNK(8, 512, 512);
+  CHUNK(4, 2048, 256);
+  CHUNK(8, 8 * sms, 256);
+  CHUNK(16, 8 * sms, 128);
+#define BULK(CH, S, G)                                                                                      \
+  {                                                                                                         \
+    auto k = read_bulk_k<CH, S>;                                                                            \
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, CH * S));                       \
+    float us = timeit([&](int c) { k<<<G, 256, CH * S, st>>>(A[c], nA, out); }, st);                        \
+    std::printf("read bulk  CH %6d S %d grid %4d: %7.2f us  %7.1f GB/s\n", CH, S, G, us, bytes_read / us / 1e3); \
+  }
+  BULK(16384, 8, 148);
+  BULK(32768, 6, 148);
+  BULK(16384, 6, 256);
+  BULK(16384, 4, 296);
+  BULK(8192, 8, 296);
+  BULK(32768, 3, 296);
+  BULK(16384, 12, 148);
+  // cuBLAS sgemv
+  {
+    cublasHandle_t hb;
+    cublasCreate(&hb);
+    cublasSetStream(hb, st);
+    const float one = 1, zero = 0;
+    float us = timeit([&](int c) { cublasSgemv(hb, CUBLAS_OP_N, M, N, &one, A[c], M, X[c], 1, &zero, Y[c], 1); }, st);
+    std::printf("cublas sgemv: %7.2f us  %7.1f GB/s\n", us, bytes_gemv / us / 1e3);
+  }
+#define COLS(T, U, G)                                                                                  \
+  {                                                                                                    \
+    const int cpb = N / G;                                                                             \
+    float us = timeit(                                                                                 \
+        [&](int c) {                                                                                   \
+          zero_k<<<M / 256, 256, 0, st>>>(Y[c], M);                                                    \
+          gemv_cols_k<T, U><<<G, T, 0, st>>>(A[c], X[c], Y[c], cpb);                                   \
+        },                                                                                             \
+        st);                                                                                           \
+    std::printf("gemv cols T%-4d U%-2d grid %4d (+zero kernel): %7.2f us  %7.1f GB/s\n", T, U, G, us, \
+                bytes_gemv / us / 1e3);                                                                \
+  }
+  COLS(1024, 2, 256);
+  COLS(1024, 4, 256);
+  COLS(512, 2, 256);
+  COLS(512, 4, 512);
+  COLS(1024, 2, 512);
+  COLS(256, 4, 1024);
+  return 0;
+}

@@ -1,0 +1,483 @@
+// Development probe (not product): FFMA sgemm 1024^3 variants on one B200
+// against cuBLAS, to find the kernel structure the emitter's sgemm building
+// block should generate. C = A B column-major, k ascending per output
+// (bit-exact against a sequential fmaf reference kernel).
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/sgemm_lab tools/sgemm_lab.cu -lcublas
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e = (x);                                                             \
+    if (e != cudaSuccess) {                                                          \
+      std::printf("CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+      std::exit(1);                                                                  \
+    }                                                                                \
+  } while (0)
+
+__device__ __forceinline__ void cp16(void* s, const void* g) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void wait_group() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// thread (tx, ty): rows (i/4)*TX*4 + tx*4 + i%4 (groups of 4), cols ty + j*TY
+// As[BK][BM + PADA], Bs[BN][BK + 4]; S-stage cp.async ring, one barrier per k tile.
+// FRAG: 0 = A fragment per k step, 1 = A fragments of 4 k steps at once
+template <int TX, int TY, int TM, int TN, int BK, int S, int PADA, int F2>
+__global__ void __launch_bounds__(TX* TY) sgemm_k(const float* __restrict__ A, const float* __restrict__ B,
+                                                  float* __restrict__ C, int M, int N, int K) {
+  constexpr int T = TX * TY, BM = TX * TM, BN = TY * TN, LDA = BM + PADA, LDB = BK + 4;
+  constexpr int A_T = BK * LDA, B_T = BN * LDB, ST = A_T + B_T;
+  extern __shared__ __align__(16) float sm[];
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  const int tiles_m = M / BM;
+  const int bm = blockIdx.x % tiles_m, bn = blockIdx.x / tiles_m;
+  const float* pa = A + (long long)bm * BM;
+  const float* pb = B + (long long)bn * BN * K;
+  const int KT = K / BK;
+  auto load = [&](int kt, int slot) {
+    float* sA = sm + slot * ST;
+    float* sB = sA + A_T;
+    const long long k0 = (long long)kt * BK;
+#pragma unroll
+    for (int ch = tid; ch < BK * BM / 4; ch += T) {
+      const int kk = ch / (BM / 4), mm = (ch % (BM / 4)) * 4;
+      cp16(sA + kk * LDA + mm, pa + mm + (k0 + kk) * M);
+    }
+#pragma unroll
+    for (int ch = tid; ch < BN * BK / 4; ch += T) {
+      const int nn = ch / (BK / 4), kk = (ch % (BK / 4)) * 4;
+      cp16(sB + nn * LDB + kk, pb + k0 + kk + (long long)nn * K);
+    }
+  };
+  float acc[TN][TM];
+#pragma unroll
+  for (int j = 0; j < TN; ++j)
+#pragma unroll
+    for (int i = 0; i < TM; ++i) acc[j][i] = 0.f;
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < KT) load(s, s);
+    commit();
+  }
+#pragma unroll 1
+  for (int kt = 0; kt < KT; ++kt) {
+    wait_group<S - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + S - 1;
+      if (nk < KT) load(nk, nk % S);
+      commit();
+    }
+    const float* sA = sm + (kt % S) * ST;
+    const float* sB = sA + A_T;
+#pragma unroll
+    for (int kq = 0; kq < BK; kq += 4) {
+      float rb[TN][4];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        float4 t = *(const float4*)(sB + (ty + j * TY) * LDB + kq);
+        rb[j][0] = t.x, rb[j][1] = t.y, rb[j][2] = t.z, rb[j][3] = t.w;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float ra[TM];
+#pragma unroll
+        for (int i = 0; i < TM; i += 4) {
+          float4 t = *(const float4*)(sA + (kq + q) * LDA + (i / 4) * TX * 4 + tx * 4);
+          ra[i] = t.x, ra[i + 1] = t.y, ra[i + 2] = t.z, ra[i + 3] = t.w;
+        }
+        if constexpr (F2) {
+#pragma unroll
+          for (int j = 0; j < TN; ++j) {
+            const float2 bb = make_float2(rb[j][q], rb[j][q]);
+#pragma unroll
+            for (int i = 0; i < TM; i += 2) {
+              float2 c = make_float2(acc[j][i], acc[j][i + 1]);
+              c = __ffma2_rn(make_float2(ra[i], ra[i + 1]), bb, c);
+              acc[j][i] = c.x, acc[j][i + 1] = c.y;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < TN; ++j)
+#pragma unroll
+            for (int i = 0; i < TM; ++i) acc[j][i] = __fmaf_rn(ra[i], rb[j][q], acc[j][i]);
+        }
+      }
+    }
+  }
+  wait_group<0>();
+  float* pc = C + ((long long)bm * BM + tx * 4) + ((long long)bn * BN + ty) * M;
+#pragma unroll
+  for (int j = 0; j < TN; ++j)
+#pragma unroll
+    for (int i = 0; i < TM; i += 4)
+      *(float4*)(pc + (i / 4) * TX * 4 + (long long)j * TY * M) =
+          make_float4(acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]);
+}
+
+// peak probe: 16 independent chains per thread (8 float2 pairs for FFMA2)
+template <int F2>
+__global__ void peak_k(float* out, int iters, float a, float b) {
+  float acc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i] = threadIdx.x * 1e-3f + i;
+  for (int it = 0; it < iters; ++it) {
+    if constexpr (F2) {
+#pragma unroll
+      for (int i = 0; i < 16; i += 2) {
+        float2 c = __ffma2_rn(make_float2(acc[i], acc[i + 1]), make_float2(a, b), make_float2(b, a));
+        acc[i] = c.x, acc[i + 1] = c.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] = __fmaf_rn(acc[i], a, b);
+    }
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += acc[i];
+  if (s == 1.2345f) out[0] = s;
+}
+
+__global__ void ref_k(const float* A, const float* B, float* C, int M, int N, int K) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (i >= M) return;
+  float s = 0.f;
+  for (int k = 0; k < K; ++k) s = __fmaf_rn(A[i + (long long)k * M], B[k + (long long)j * K], s);
+  C[i + (long long)j * M] = s;
+}
+
+struct Bufs {
+  std::vector<float*> a, b, c;
+};
+
+template <int TX, int TY, int TM, int TN, int BK, int S, int PADA, int F2>
+void run(const char* tag, Bufs& bf, const float* ref, int M, int N, int K, int R, cudaStream_t st) {
+  constexpr int T = TX * TY, BM = TX * TM, BN = TY * TN;
+  constexpr int ST = BK * (BM + PADA) + BN * (BK + 4);
+  const size_t smem = size_t(ST) * S * 4;
+  auto kern = sgemm_k<TX, TY, TM, TN, BK, S, PADA, F2>;
+  if (smem > 232448) return;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const int grid = (M / BM) * (N / BN);
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T, smem));
+  for (int w = 0; w < 3; ++w) kern<<<grid, T, smem, st>>>(bf.a[0], bf.b[0], bf.c[0], M, N, K);
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  // check bits against the sequential reference
+  std::vector<float> h(size_t(M) * N), r(size_t(M) * N);
+  CK(cudaMemcpy(h.data(), bf.c[0], h.size() * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(r.data(), ref, r.size() * 4, cudaMemcpyDeviceToHost));
+  const bool exact = std::memcmp(h.data(), r.data(), h.size() * 4) == 0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  std::vector<float> ts;
+  for (int trial = 0; trial < 7; ++trial) {
+    cudaEventRecord(e0, st);
+    for (int r2 = 0; r2 < R; ++r2) {
+      const int x = r2 % int(bf.a.size());
+      kern<<<grid, T, smem, st>>>(bf.a[x], bf.b[x], bf.c[x], M, N, K);
+    }
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ts.push_back(ms * 1e3f / R);
+  }
+  std::sort(ts.begin(), ts.end());
+  std::printf("%-4s F2=%d TX%-3d TY%-3d TM%-2d TN%-2d BK%-2d S%d PAD%d  grid %5d thr %4d regs %3d occ %d spill %zu  %8.2f us  %6.1f TF/s  %s\n",
+              tag, F2, TX, TY, TM, TN, BK, S, PADA, grid, T, fa.numRegs, occ, (size_t)fa.localSizeBytes, ts[3],
+              2.0 * M * N * double(K) / (ts[3] * 1e-6) / 1e12, exact ? "bit-exact" : "MISMATCH");
+}
+
+
+__device__ __forceinline__ void cp4(void* s, const void* g) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(g));
+}
+
+__device__ unsigned long long* g_trace = nullptr;
+// v3: warp-tiled, k-major smem for both operands (B transposed by 4-byte
+// cp.async), per-k register fragments double buffered, FFMA2 with the B value
+// broadcast. Warps WX x WY, lanes LX x LY, 8 x 8 outputs per lane as 2 x 2
+// blocks of 4 x 4: row = wm*LX*8 + (i/4)*LX*4 + lx*4 + i%4, same for columns.
+template <int WX, int WY, int LX, int LY, int BK, int S, int PADB, int TM, int TN, int F2, int MINB, int SPLIT = 1>
+__global__ void __launch_bounds__(WX* WY * 32, MINB) sgemm_v3(const float* __restrict__ A, const float* __restrict__ B,
+                                                      float* __restrict__ C, int M, int N, int K) {
+  constexpr int T = WX * WY * 32;
+  static_assert(TM % 4 == 0 && TN % 4 == 0 && TM <= 8 && TN <= 8, "thread tile");
+  constexpr int BM = WX * LX * TM, BN = WY * LY * TN, LDB = BN + PADB;
+  constexpr int A_T = BK * BM, B_T = BK * LDB, ST = A_T + B_T;
+  static_assert(LX * LY == 32, "lanes");
+  extern __shared__ __align__(16) float sm[];
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WX, wn = warp / WX, lx = lane % LX, ly = lane / LX;
+  const int tiles_m = M / BM;
+  const int half = blockIdx.x % SPLIT, tile = blockIdx.x / SPLIT;
+  const int bm = tile % tiles_m, bn = tile / tiles_m;
+  const float* pa = A + (long long)bm * BM + (long long)half * (K / SPLIT) * M;
+  const float* pb = B + (long long)bn * BN * K + half * (K / SPLIT);
+  C += (long long)half * M * N;
+  const int KT = K / SPLIT / BK;
+  auto load = [&](int kt, int slot) {
+    float* sA = sm + slot * ST;
+    float* sB = sA + A_T;
+    const long long k0 = (long long)kt * BK;
+#pragma unroll
+    for (int ch = tid; ch < BK * BM / 4; ch += T) {
+      const int kk = ch / (BM / 4), mm = (ch % (BM / 4)) * 4;
+      cp16(sA + kk * BM + mm, pa + mm + (k0 + kk) * M);
+    }
+#pragma unroll
+    for (int e = tid; e < BK * BN; e += T) {  // lanes walk k (contiguous in global)
+      const int kk = e % BK, nn = e / BK;
+      cp4(sB + kk * LDB + nn, pb + k0 + kk + (long long)nn * K);
+    }
+  };
+  float acc[TN][TM];
+#pragma unroll
+  for (int j = 0; j < TN; ++j)
+#pragma unroll
+    for (int i = 0; i < TM; ++i) acc[j][i] = 0.f;
+  const int arow = wm * LX * TM + lx * 4, bcol = wn * LY * TN + ly * 4;
+  float fa[2][TM], fb[2][TN];
+  auto frag = [&](int buf, const float* sA, const float* sB, int k) {
+#pragma unroll
+    for (int h = 0; h < TM / 4; ++h) {
+      const float4 a0 = *(const float4*)(sA + k * BM + arow + h * LX * 4);
+      fa[buf][4 * h] = a0.x, fa[buf][4 * h + 1] = a0.y, fa[buf][4 * h + 2] = a0.z, fa[buf][4 * h + 3] = a0.w;
+    }
+#pragma unroll
+    for (int h = 0; h < TN / 4; ++h) {
+      const float4 b0 = *(const float4*)(sB + k * LDB + bcol + h * LY * 4);
+      fb[buf][4 * h] = b0.x, fb[buf][4 * h + 1] = b0.y, fb[buf][4 * h + 2] = b0.z, fb[buf][4 * h + 3] = b0.w;
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < KT) load(s, s);
+    commit();
+  }
+  wait_group<S - 2>();
+  __syncthreads();
+  frag(0, sm, sm + A_T, 0);
+#pragma unroll 1
+  for (int kt = 0; kt < KT; ++kt) {
+    const float* sA = sm + (kt % S) * ST;
+    const float* sB = sA + A_T;
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      if (k == BK - 1) {
+        wait_group<S - 2>();
+        __syncthreads();
+        const float* nA = sm + ((kt + 1) % S) * ST;
+        frag((k + 1) & 1, nA, nA + A_T, 0);  // past the end: reads a stale slot, unused
+      } else {
+        frag((k + 1) & 1, sA, sB, k + 1);
+      }
+      if (k == 0) {
+        const int nk = kt + S - 1;
+        if (nk < KT) load(nk, nk % S);
+        commit();
+      }
+      if constexpr (F2) {
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+          for (int i = 0; i < TM; i += 2) {
+            float2 c = make_float2(acc[j][i], acc[j][i + 1]);
+            c = __ffma2_rn(make_float2(fa[k & 1][i], fa[k & 1][i + 1]), make_float2(fb[k & 1][j], fb[k & 1][j]), c);
+            acc[j][i] = c.x, acc[j][i + 1] = c.y;
+          }
+      } else {
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+          for (int i = 0; i < TM; ++i) acc[j][i] = __fmaf_rn(fa[k & 1][i], fb[k & 1][j], acc[j][i]);
+      }
+    }
+  }
+  wait_group<0>();
+#pragma unroll
+  for (int j = 0; j < TN; ++j) {
+    const long long col = (long long)bn * BN + bcol + (j / 4) * LY * 4 + j % 4;
+#pragma unroll
+    for (int i = 0; i < TM; i += 4) {
+      const long long row = (long long)bm * BM + arow + (i / 4) * LX * 4;
+      *(float4*)(C + row + col * M) = make_float4(acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]);
+    }
+  }
+  if (g_trace && tid == 0) {
+    unsigned long long t_end;
+    unsigned smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_trace[3 * blockIdx.x] = t_start;
+    g_trace[3 * blockIdx.x + 1] = t_end;
+    g_trace[3 * blockIdx.x + 2] = smid;
+  }
+}
+
+template <int WX, int WY, int LX, int LY, int BK, int S, int PADB, int TM = 8, int TN = 8, int F2 = 1, int MINB = 1, int SPLIT = 1>
+void run3(Bufs& bf, const float* ref, int M, int N, int K, int R, cudaStream_t st) {
+  constexpr int T = WX * WY * 32, BM = WX * LX * TM, BN = WY * LY * TN;
+  constexpr int ST = BK * BM + BK * (BN + PADB);
+  const size_t smem = size_t(ST) * S * 4;
+  auto kern = sgemm_v3<WX, WY, LX, LY, BK, S, PADB, TM, TN, F2, MINB, SPLIT>;
+  if (smem > 232448) return;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const int grid = (M / BM) * (N / BN) * SPLIT;
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T, smem));
+  for (int w = 0; w < 3; ++w) kern<<<grid, T, smem, st>>>(bf.a[0], bf.b[0], bf.c[0], M, N, K);
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  std::vector<float> h(size_t(M) * N), r(size_t(M) * N);
+  CK(cudaMemcpy(h.data(), bf.c[0], h.size() * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(r.data(), ref, r.size() * 4, cudaMemcpyDeviceToHost));
+  const bool exact = std::memcmp(h.data(), r.data(), h.size() * 4) == 0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  std::vector<float> ts;
+  for (int trial = 0; trial < 7; ++trial) {
+    cudaEventRecord(e0, st);
+    for (int r2 = 0; r2 < R; ++r2) {
+      const int x = r2 % int(bf.a.size());
+      kern<<<grid, T, smem, st>>>(bf.a[x], bf.b[x], bf.c[x], M, N, K);
+    }
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ts.push_back(ms * 1e3f / R);
+  }
+  {
+    unsigned long long* tr;
+    CK(cudaMalloc(&tr, grid * 3 * 8));
+    CK(cudaMemcpyToSymbol(g_trace, &tr, sizeof(tr)));
+    kern<<<grid, T, smem, st>>>(bf.a[1], bf.b[1], bf.c[1], M, N, K);
+    CK(cudaStreamSynchronize(st));
+    std::vector<unsigned long long> h3(grid * 3);
+    CK(cudaMemcpy(h3.data(), tr, grid * 3 * 8, cudaMemcpyDeviceToHost));
+    unsigned long long* z = nullptr;
+    CK(cudaMemcpyToSymbol(g_trace, &z, sizeof(z)));
+    unsigned long long t0 = ~0ull, t1 = 0;
+    std::vector<int> per_sm(200, 0);
+    double dmin = 1e30, dmax = 0, dsum = 0;
+    for (int b = 0; b < grid; ++b) {
+      t0 = std::min(t0, h3[3 * b]);
+      t1 = std::max(t1, h3[3 * b + 1]);
+      per_sm[h3[3 * b + 2]]++;
+      const double d = double(h3[3 * b + 1] - h3[3 * b]);
+      dmin = std::min(dmin, d), dmax = std::max(dmax, d), dsum += d;
+    }
+    int shared = 0, used = 0;
+    for (int c : per_sm) used += c > 0, shared += c > 1;
+    double smax = 0;
+    for (int b = 0; b < grid; ++b) smax = std::max(smax, double(h3[3 * b] - t0));
+    std::printf("   trace: span %.2f us, CTA dur min %.2f avg %.2f max %.2f us, last start +%.2f us, SMs used %d (shared by >1 CTA: %d)\n",
+                (t1 - t0) / 1e3, dmin / 1e3, dsum / grid / 1e3, dmax / 1e3, smax / 1e3, used, shared);
+    cudaFree(tr);
+  }
+  std::sort(ts.begin(), ts.end());
+  std::printf("v3 SPLIT=%d F2=%d MINB=%d T%dx%d W%dx%d L%dx%d tile %dx%d BK%-2d S%d PADB%d grid %5d thr %4d regs %3d occ %d spill %zu  %8.2f us  %6.1f TF/s  %s\n",
+              SPLIT, F2, MINB, TM, TN, WX, WY, LX, LY, BM, BN, BK, S, PADB, grid, T, fa.numRegs, occ, (size_t)fa.localSizeBytes, ts[3],
+              2.0 * M * N * double(K) / (ts[3] * 1e-6) / 1e12, exact ? "bit-exact" : "MISMATCH");
+}
+
+int main() {
+  const int M = 1024, N = 1024, K = 1024, NB = 16, R = 32;
+  cudaStream_t st;
+  CK(cudaStreamCreate(&st));
+  Bufs bf;
+  std::vector<float> h(size_t(M) * K);
+  srand(7);
+  for (auto& x : h) x = float(rand() % 2001 - 1000) / 1024.0f;
+  for (int i = 0; i < NB; ++i) {
+    float *a, *b, *c;
+    CK(cudaMalloc(&a, size_t(M) * K * 4));
+    CK(cudaMalloc(&b, size_t(K) * N * 4));
+    CK(cudaMalloc(&c, size_t(M) * N * 4 * 4));
+    CK(cudaMemcpy(a, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(b, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    bf.a.push_back(a), bf.b.push_back(b), bf.c.push_back(c);
+  }
+  float* ref;
+  CK(cudaMalloc(&ref, size_t(M) * N * 4));
+  ref_k<<<dim3(M / 128, N), 128, 0, st>>>(bf.a[0], bf.b[0], ref, M, N, K);
+  CK(cudaStreamSynchronize(st));
+  // cuBLAS FP32 (default math)
+  {
+    cublasHandle_t hb;
+    cublasCreate(&hb);
+    cublasSetStream(hb, st);
+    const float one = 1.f, zero = 0.f;
+    for (int w = 0; w < 3; ++w)
+      cublasSgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, M, N, K, &one, bf.a[0], M, bf.b[0], K, &zero, bf.c[0], M);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    std::vector<float> ts;
+    for (int trial = 0; trial < 7; ++trial) {
+      cudaEventRecord(e0, st);
+      for (int r2 = 0; r2 < R; ++r2) {
+        const int x = r2 % NB;
+        cublasSgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, M, N, K, &one, bf.a[x], M, bf.b[x], K, &zero, bf.c[x], M);
+      }
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ts.push_back(ms * 1e3f / R);
+    }
+    std::sort(ts.begin(), ts.end());
+    std::printf("cublas       %8.2f us  %6.1f TF/s\n", ts[3], 2.0 * M * N * double(K) / (ts[3] * 1e-6) / 1e12);
+  }
+  for (int f2 = 0; f2 < 2; ++f2) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 8192, blocks = 148 * 8, thr = 256;
+    for (int w = 0; w < 2; ++w) (f2 ? peak_k<1> : peak_k<0>)<<<blocks, thr, 0, st>>>(ref, iters, 0.999f, 1e-3f);
+    cudaEventRecord(e0, st);
+    (f2 ? peak_k<1> : peak_k<0>)<<<blocks, thr, 0, st>>>(ref, iters, 0.999f, 1e-3f);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    std::printf("peak %s: %.1f TF/s\n", f2 ? "FFMA2" : "FFMA", 2.0 * 16 * iters * double(blocks) * thr / (ms * 1e-3) / 1e12);
+  }
+  ref_k<<<dim3(M / 128, N), 128, 0, st>>>(bf.a[0], bf.b[0], ref, M, N, K);
+#define RUN3(WX, WY, LX, LY, BK, S, P, ...) run3<WX, WY, LX, LY, BK, S, P, ##__VA_ARGS__>(bf, ref, M, N, K, R, st)
+  RUN3(2, 2, 8, 4, 16, 3, 4);   // 128x64, 128 thr (cuBLAS's tile)
+  RUN3(2, 2, 8, 4, 16, 3, 4, 8, 8, 1, 1, 2);
+  RUN3(2, 2, 8, 4, 16, 3, 4, 8, 8, 0, 1, 2);
+  RUN3(2, 2, 8, 4, 32, 3, 4, 8, 8, 1, 1, 2);
+  RUN3(2, 2, 8, 4, 16, 3, 4, 8, 8, 1, 1, 4);
+  RUN3(4, 2, 8, 4, 16, 3, 4, 4, 8, 1, 1, 2);
+  RUN3(2, 1, 8, 4, 16, 3, 4, 8, 8, 1, 1, 2);
+  return 0;
+}
