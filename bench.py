@@ -274,6 +274,76 @@ def run_configs(kinds, args, local, world, rank) -> dict:
     return out
 
 
+def replay_failures(log_path, space, ordinal, budget_s=120.0, max_threads=1 << 20) -> list[dict]:
+    """Every mismatch / launch error the search logged, re-emitted from its
+    candidate and executed on the CPU emulator (tests/emu) with the problem's
+    own inputs, against the device's golden outputs (pinned to the oracle by
+    the tests): "emulator agrees" means the schedule computes the right values
+    and the device run failed; "emulator differs" convicts the schedule or the
+    emitter. Bounded: at most budget_s seconds, kernels of <= max_threads threads."""
+    import numpy as np
+    if not log_path or not os.path.exists(log_path):
+        return []
+    rows = []
+    for line in open(log_path):
+        try:
+            r = json.loads(line)
+        except ValueError:
+            continue
+        if r.get("status") in ("mismatch", "launch_error", "sticky") and "candidate" in r:
+            rows.append(r)
+    if not rows:
+        return []
+    from paper_1904_03383_b200 import Device
+    from tests import emu
+    out = []
+    dev = Device(ordinal)
+    dev.bind(space.problem())
+    t0 = time.perf_counter()
+    for r in rows:
+        rec = {"i": r["i"], "status": r["status"], "hash": r.get("hash")}
+        if time.perf_counter() - t0 > budget_s:
+            rec["verdict"] = "not replayed (time budget)"
+            out.append(rec)
+            continue
+        try:
+            cand = space.deserialize(json.dumps(r["candidate"]) if not isinstance(r["candidate"], str)
+                                     else r["candidate"])
+            src, L = cand.nest().cuda("k_emu")
+            threads = int(L.grid_x) * L.block[0] * L.block[1] * L.block[2]
+            if threads > max_threads:
+                rec["verdict"] = f"not replayed ({threads} threads > {max_threads})"
+                out.append(rec)
+                continue
+            regions, outputs = {}, []
+            for i in range(L.num_params):
+                prm = L.params[i]
+                if prm.kind != 0 or not prm.is_input:  # is_input: bound to a problem region (else scratch)
+                    continue
+                name, n = prm.name.decode(), int(prm.elems)
+                try:  # an output: NaN-filled like the device run, compared with the golden values
+                    outputs.append((name, n, dev.read(name, n, expected=True)))
+                    regions[name] = np.full(n, np.nan, dtype=np.float32)
+                except RuntimeError:
+                    regions[name] = dev.read(name, n)
+            try:
+                emu.run(src, L, regions, space.problem().alpha)
+            except emu.TooLong:
+                rec["verdict"] = "not replayed (emulation budget)"
+                out.append(rec)
+                continue
+            bad = 0
+            for name, n, want in outputs:
+                bad += int(np.count_nonzero(regions[name].view(np.uint32) != want.view(np.uint32)))
+            rec["verdict"] = "emulator differs (schedule/emitter)" if bad else "emulator agrees (device-side failure)"
+            rec["emulator_mismatches"] = bad
+        except Exception as e:  # noqa: BLE001 - a verdict, not a crash
+            rec["verdict"] = f"replay error: {str(e)[:200]}"
+        out.append(rec)
+    dev.close()
+    return out
+
+
 def run_uniform(space, local, rank, world, args) -> dict:
     """Our evaluator on the reference baseline's walk: seeded uniform
     first-open descents from the root (oracle/ref_cpu_bench.cpp's), every
@@ -373,6 +443,7 @@ def run_ours(args, world, rank, local):
     best_src = search.best_source()
     search_error = N_error(search)
     search.close()
+    replays = replay_failures(log, space, local)
     uniform = None
     if args.uniform_evals > 0:
         uniform = run_uniform(space, local, rank, world, args)
@@ -453,6 +524,7 @@ def run_ours(args, world, rank, local):
                    "note": "busy = the timed kernel launches' own event time; the rest of the device "
                            "timeline is fills, checks, arm kernels and host gaps"},
         "uniform_walk": uniform,
+        "failure_replays": replays,
         "wall_s": round(wall, 3),
         "stalled_steps": stalled,
         "search_error": search_error,

@@ -1028,7 +1028,11 @@ void Search::log_eval(const Work& w, const ispc_time_result& r, int rc, const st
   }
   path += "]";
   anc += "]";
-  std::string compact = improved ? best_text_ : std::string();
+  // the candidate text rides along when it improved the best, and on every
+  // mismatch / launch error (bench.py replays those on the CPU emulator)
+  const bool failed = status == "mismatch" || status == "launch_error" || status == "sticky";
+  const bool with_cand = improved || failed;
+  std::string compact = improved ? best_text_ : failed ? serialize_text(*space_->ctx, w.leaf) : std::string();
   std::replace(compact.begin(), compact.end(), '\n', ' ');
   const bool timed = rc == ISPC_OK;
   std::fprintf(log_,
@@ -1041,7 +1045,7 @@ void Search::log_eval(const Work& w, const ispc_time_result& r, int rc, const st
                std::isfinite(inc_.seconds()) ? inc_.seconds() * 1e9 : -1.0, (unsigned long long)w.launch.source_hash,
                (unsigned long long)w.digest, (unsigned long long)w.launch.grid_x,
                w.launch.block[0] * w.launch.block[1] * w.launch.block[2], (unsigned long long)cfg_.seed, w.tid, (long long)w.rollout_no, w.root,
-               path.c_str(), anc.c_str(), improved ? "true" : "false", improved ? ", \"candidate\": " : "",
+               path.c_str(), anc.c_str(), improved ? "true" : "false", with_cand ? ", \"candidate\": " : "",
                compact.c_str());
 }
 
