@@ -131,12 +131,29 @@ def barrier(world: int):
         dist.barrier()
 
 
-def cpu_baseline(seconds: float, threads: int) -> dict | None:
+MATMUL_FACTORS = [[2, 4, 8, 16, 32], [2, 4]]
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(seconds: float, threads: int, kind: str = "axpy") -> dict | None:
     """The reference's own CPU search + evaluation (oracle/_ref), bounded sample."""
     if not os.path.exists(REF_CPU_BENCH):
         return None
-    args = [REF_CPU_BENCH, "axpy", "0", str(N_AXPY), "0", f"{seconds}", str(threads)]
-    args += [",".join(str(v) for v in u) for u in FACTORS]
+    if kind == "axpy":
+        args = [REF_CPU_BENCH, "axpy", "0", str(N_AXPY), "0", f"{seconds}", str(threads)]
+        args += [",".join(str(v) for v in u) for u in FACTORS]
+    else:
+        args = [REF_CPU_BENCH, "matmul", "1024", "1024", "1024", f"{seconds}", str(threads)]
+        args += [",".join(str(v) for v in u) for u in MATMUL_FACTORS]
     out = subprocess.run(args, capture_output=True, text=True, timeout=seconds * 4 + 120)
     if out.returncode != 0:
         return None
@@ -185,6 +202,11 @@ CONFIG_SPACES = {
     # the 1024^3 sgemm on the tensor pipe with fp32-level accuracy (3xTF32,
     # checked at 1e-5 of sum |a||b|), beside the FFMA search and cuBLAS FP32
     "sgemm_1024_x3": ("sgemm_tc_x3", dict(m=1024, n=1024, k=1024), 96, False),
+    # the reference's own matmul space at the paper's Table 2 shape:
+    # make_matmul(1024, 1024, 1024, {{2..32}, {2, 4}}) in gpu.space with the
+    # reference's MachineParams (kernels.cpp:435-488), every leaf lowered by
+    # the loop-nest emitter, bit-exact against the golden kernel
+    "matmul": ("matmul", dict(m=1024, n=1024, k=1024, factors=[[2, 4, 8, 16, 32], [2, 4]]), 256, False),
 }
 
 
@@ -244,7 +266,11 @@ def config_worker(args) -> None:
            "bound_violations": st["bound_violations"], "search_s": round(time.perf_counter() - t0, 2)}
     if best is not None:
         res["best"] = retime_best(space, best, reps=20, ordinal=args.ordinal)
-        res["best_config"] = best.tiles().as_dict()
+        if space.tiles:
+            res["best_config"] = best.tiles().as_dict()
+        else:
+            res["best_bound_us"] = round(best.bound()["total"] * 1e6, 3)
+            res["best_simulated_cycles"] = best.simulate()["total"]
         save_best(name, kw, best, kind)
     if args.with_cublas:
         res["cublas"] = cublas_reference(space)
@@ -494,8 +520,17 @@ def run_ours(args, world, rank, local):
         res = cpu_baseline(args.cpu_seconds, os.cpu_count() or 1)
         if res:
             cpu = {"value": res["leaves_per_s"], "unit": "candidates/s", "cores": res["threads"],
-                   "kind": "reference",
+                   "kind": "reference", "cpu_model": cpu_model(),
                    "sample": f"reference CPU search+simulate: {res['leaves']} leaves in {res['seconds']:.1f}s"}
+            # also one thread, and the matmul 1024^3 space
+            extra = {}
+            for kind, th in (("axpy", 1), ("matmul", os.cpu_count() or 1), ("matmul", 1)):
+                r2 = cpu_baseline(3.0, th, kind)
+                if r2:
+                    extra[f"{kind}_{th}t"] = {"leaves_per_s": r2["leaves_per_s"], "walks_per_s": r2["walks_per_s"],
+                                              "dead_ends": r2["dead_ends"], "leaves": r2["leaves"],
+                                              "best_simulated_cycles": r2["best_simulated_cycles"]}
+            cpu["more"] = extra
     # per evaluation: ispc_arm + the kernel + the check kernel; per re-timed
     # one: (warmup + reps) x (ispc_arm + kernel + flag collect)
     gpu_launches = int(evals_total * 3 + refined_here * (1 + 3) * 3)

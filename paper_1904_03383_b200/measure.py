@@ -171,7 +171,7 @@ def cublas_reference(space, reps: int = 20) -> dict | None:
         out["axpy"] = _time_rotating(mk([(n,), (n,)], lambda x, y: y.add_(x, alpha=1.5)), rot)
     elif kind == "gemv":
         out["sgemv"] = _time_rotating(mk([(n, m), (n,)], lambda at, x: torch.mv(at.t(), x)), rot)
-    elif kind == "sgemm":
+    elif kind in ("sgemm", "matmul"):
         out["sgemm"] = _time_rotating(mk([(k, m), (n, k)], lambda a, bb: torch.mm(a.t(), bb.t())), rot)
     elif kind == "batched":
         out["sgemm_strided_batched"] = _time_rotating(

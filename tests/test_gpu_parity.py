@@ -165,3 +165,33 @@ def test_matmul_scaled_fused_bit_exact(dev, orc):
     assert m.status == "ok" and m.mismatches == 0, (m, dev.error())
     got = dev.read("c", 64 * 64)
     assert np.array_equal(_bits(got), _bits(orc.expected(p)["c"]))
+
+
+def test_b200_mode_shared_staging_bit_exact(dev, orc):
+    """B200 MachineParams mode (227 KiB of shared memory per block instead of
+    the reference's 48 KiB, host_api.cpp machine_for): single-block axpy
+    schedules whose 64 KiB temporaries live in shared memory run bit-exact."""
+    from paper_1904_03383_b200 import _native as N
+    space = Space("axpy", n=16384, factors=[[4], [64]], mode=N.SPACE_B200)
+    dev.bind(space.problem())
+    p = space.problem()
+    ref = orc.axpy(orc.fill(p.n, p.seed, "x"), orc.fill(p.n, p.seed, "y"), p.alpha)
+    ok = 0
+    for seed in range(1, 300):
+        try:
+            leaf, _, _ = space.root().random_leaf(seed)
+            nest = leaf.nest()
+            src, _ = nest.cuda()
+        except (DeadEnd, EmitError, ValueError):
+            continue
+        if "__shared__" not in src:
+            continue
+        m = dev.evaluate(nest, reps=1, warmup=0)
+        if m.status == "timeout":
+            continue
+        assert m.status == "ok", (seed, m, dev.error())
+        assert np.array_equal(_bits(dev.read("z", p.n)), _bits(ref)), seed
+        ok += 1
+        if ok == 4:
+            break
+    assert ok >= 2

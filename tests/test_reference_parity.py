@@ -103,3 +103,28 @@ def test_knuth_estimate_matches_exact_count():
     est = s.root().estimate_tree(20000, seed=3)
     assert abs(est["leaves"] - 768) <= 4 * est["leaves_stderr"] + 1e-9
     assert est["dead_probe_ratio"] == 0.0
+
+
+def test_b200_mode_admits_shared_staging_the_parity_machine_cannot():
+    """machine_for(ISPC_SPACE_B200) raises shared_capacity to 227 KiB: at
+    axpy n = 16384 (64 KiB temporaries) no parity-mode leaf stages in shared
+    memory, most B200-mode leaves do; both spaces keep the reference's
+    instance table (same choices, same counts)."""
+    from paper_1904_03383_b200 import DeadEnd, EmitError
+    from paper_1904_03383_b200 import _native as N
+    counts = {}
+    for mode in (N.SPACE_PARITY, N.SPACE_B200):
+        s = Space("axpy", n=16384, factors=[[4], [64]], mode=mode)
+        assert s.stats()["instances"] == Space("axpy", n=16384, factors=[[4], [64]]).stats()["instances"]
+        shared = total = 0
+        for seed in range(1, 300):
+            try:
+                leaf, _, _ = s.root().random_leaf(seed)
+                src, _ = leaf.nest().cuda()
+            except (DeadEnd, EmitError, ValueError):
+                continue
+            total += 1
+            shared += "__shared__" in src
+        counts[mode] = (shared, total)
+    assert counts[N.SPACE_PARITY][0] == 0 and counts[N.SPACE_PARITY][1] > 20
+    assert counts[N.SPACE_B200][0] > counts[N.SPACE_B200][1] // 2
