@@ -233,7 +233,8 @@ int ispc_bound(const ispc_space* s, const ispc_cand* c, int l2_flushed, ispc_bou
 typedef struct ispc_search ispc_search;
 
 typedef struct {
-  int32_t device;           /* CUDA ordinal of this worker's B200               */
+  int32_t device;           /* CUDA ordinal of this worker's B200; -1 dry run (NVRTC,
+                               no device), -2 dry run without NVRTC (host pipeline) */
   int32_t rollout_threads;  /* 0: auto                                          */
   int32_t compile_threads;  /* 0: auto                                          */
   int32_t batch;            /* kernels per NVRTC program (0: 8)                 */
@@ -284,6 +285,9 @@ typedef struct {
   double device_busy_ms;    /* device time of the timed launches in the last step */
   double t_launch_host_s;   /* launch thread: host time spent per batch outside the
                                device waits (binding, enqueue, result processing) */
+  int64_t frontier_total;   /* subtree roots of the whole (all-shard) frontier     */
+  int64_t stealing_since;   /* rollouts when this shard's own subtrees were spent and
+                               it began stealing from the whole frontier (-1: never) */
 } ispc_search_stats;
 
 int ispc_search_create(const ispc_space* s, const ispc_search_config* cfg, ispc_search** out);

@@ -190,7 +190,8 @@ class SearchStats(C.Structure):
                                              "elapsed_s", "device_step_ms", "t_rollout_s", "t_compile_s",
                                              "t_gpu_s")]
                 + [("best_hash", C.c_uint64), ("frontier", C.c_int64), ("exhausted", C.c_int64),
-                   ("refined", C.c_int64), ("device_busy_ms", C.c_double), ("t_launch_host_s", C.c_double)])
+                   ("refined", C.c_int64), ("device_busy_ms", C.c_double), ("t_launch_host_s", C.c_double),
+                   ("frontier_total", C.c_int64), ("stealing_since", C.c_int64)])
 
 
 # Every symbol include/ispc.h declares, with its ctypes signature.

@@ -239,6 +239,7 @@ void Search::expand_frontier() {
     for (size_t i = 0; i < subtrees_.size(); ++i) mine_.push_back(i);
   }
   st_.frontier = int64_t(mine_.size());
+  st_.frontier_total = int64_t(subtrees_.size());
 }
 
 double Search::bound_total(const Candidate& c) const {
@@ -630,6 +631,7 @@ void Search::note_fruitless() {
   if (++fruitless_ < kExhaust) return;
   if (cfg_.shard_count > 1 && mine_.size() < subtrees_.size() && !stealing_.exchange(true)) {
     fruitless_ = 0;  // own shard spent: steal from the whole frontier before giving up
+    stealing_since_ = rollouts_.load();
     if (trace_) std::fprintf(stderr, "[ispc] shard %d spent, stealing from %zu subtrees\n", cfg_.shard_index,
                              subtrees_.size());
     return;
@@ -744,7 +746,9 @@ void Search::compile_items(std::vector<std::unique_ptr<Work>> items) {
   std::vector<const char*> srcs;
   for (auto& w : items) srcs.push_back(w->src.c_str());
   ispc_module* m = nullptr;
-  int rc = ispc_compile(srcs.data(), int(srcs.size()), "sm_100a", &m);
+  // device -2: a dry run of the host pipeline alone (no NVRTC, no device):
+  // the tests of sharding and stealing
+  int rc = cfg_.device == -2 ? ISPC_OK : ispc_compile(srcs.data(), int(srcs.size()), "sm_100a", &m);
   if (const char* dir = std::getenv("ISPC_DUMP_DIR")) {  // the compiled programs, for compile-cost studies
     static std::atomic<int> seq{0};
     if (FILE* f = std::fopen((std::string(dir) + "/prog" + std::to_string(seq++) + ".cu").c_str(), "w")) {
@@ -882,6 +886,14 @@ void Search::launch_worker() {
       // not load: every kernel of it is a launch error (a sticky fault ends
       // the search, as in ispc_launch_batch)
       std::lock_guard<std::mutex> lk(mu_);
+      if (!dev_ && log_) {
+        for (int64_t i = 0; i < n; ++i) {
+          const Work& w = *b->items[size_t(i)];
+          std::fprintf(log_, "{\"i\": %lld, \"status\": \"dry\", \"digest\": \"%016llx\", \"subtree\": %zu, \"shard\": %d}\n",
+                       (long long)(st_.evaluations + i + 1), (unsigned long long)w.digest, w.root, cfg_.shard_index);
+        }
+        std::fflush(log_);
+      }
       st_.evaluations += n;
       if (dev_) {
         st_.launch_errors += n;
@@ -1119,6 +1131,7 @@ ispc_search_stats Search::stats() const {
   s.t_compile_s = t_compile_;
   s.incumbent_ns = inc_.seconds() * 1e9;
   s.exhausted = exhausted_ ? 1 : 0;
+  s.stealing_since = stealing_since_;
   s.elapsed_s = now() - t0_;
   s.refined = refined_;
   s.t_launch_host_s = t_launch_host_;

@@ -157,6 +157,7 @@ class Search {
   std::vector<ispace::Candidate> subtrees_;  // the whole frontier
   std::vector<size_t> mine_;
   std::atomic<bool> stealing_{false};
+  std::atomic<int64_t> stealing_since_{-1};  // rollout count when stealing began (-1: never)
   Incumbent inc_;
   ispc_dev* dev_ = nullptr;
   std::string err_;

@@ -100,3 +100,57 @@ def test_bench_reports_the_best_kernel_over_ranks():
     got = dict(q.get() for _ in range(2))
     assert got[0] == got[1] == (117.0, "fast", 88.0, 4.5)
 
+
+
+def _steal_worker(rank, world, port, q, logdir):
+    import json
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1904_03383_b200 import Search, Space
+        space = Space("outer_product", m=4096, n=4096)
+        log = os.path.join(logdir, f"r{rank}.jsonl")
+        # device -2: the host pipeline alone (rollouts, emission; no NVRTC, no device)
+        s = Search(space, device=-2, seed=7 + rank, shard_index=rank, shard_count=world, rollout_threads=1,
+                   compile_threads=1, log_path=log)
+        mine = s.frontier()
+        s.step(100000, max_seconds=60)  # runs until every shard is spent (own subtrees, then stolen ones)
+        st = s.stats()
+        s.close()
+        rows = [json.loads(x) for x in open(log)]
+        q.put((rank, mine, st["frontier"], st["frontier_total"], st["stealing_since"], st["exhausted"],
+               sorted({r["subtree"] for r in rows}), sorted({r["digest"] for r in rows})))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_four_rank_frontier_partition_and_stealing(tmp_path):
+    """World 4 (gloo): the four shards partition one frontier (disjoint,
+    union = the whole frontier); once a shard's own subtrees are spent it
+    steals, producing leaves from other shards' subtrees; and the leaves the
+    ranks produce together include every leaf any single rank found."""
+    world = 4
+    port = 28000 + (uuid.uuid4().int % 1500)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_steal_worker, args=(r, world, port, q, str(tmp_path))) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    total = res[0][3]
+    sets = [set(r[1]) for r in res]
+    assert all(r[3] == total for r in res)
+    assert sum(r[2] for r in res) == total == len(set().union(*sets))
+    for i in range(world):
+        for j in range(i + 1, world):
+            assert not (sets[i] & sets[j]), "shards own disjoint subtrees"
+    for rank, _, _, _, stealing_since, exhausted, subtrees, _ in res:
+        assert exhausted == 1 and stealing_since >= 0, rank
+        assert any(t % world != rank for t in subtrees), f"rank {rank} never stole"
+    union = set().union(*(set(r[7]) for r in res))
+    assert all(set(r[7]) <= union for r in res) and len(union) >= max(len(r[7]) for r in res)
