@@ -13,6 +13,13 @@ import torch.multiprocessing as mp
 from tests.conftest import ROOT
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def _worker(rank, world, port, shm, kind, kw, q):
     import sys
     sys.path.insert(0, ROOT)
@@ -132,7 +139,7 @@ def test_four_rank_frontier_partition_and_stealing(tmp_path):
     steals, producing leaves from other shards' subtrees; and the leaves the
     ranks produce together include every leaf any single rank found."""
     world = 4
-    port = 28000 + (uuid.uuid4().int % 1500)
+    port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=_steal_worker, args=(r, world, port, q, str(tmp_path))) for r in range(world)]
