@@ -225,6 +225,7 @@ typedef struct {
   double total, dram, sm_mem, issue, thread, launch; /* seconds */
   double dram_bytes, blocks_max, threads_per_block_max;
   double dispatch, l1;      /* seconds: block dispatch floor, L1 lines of scattered warp accesses */
+  double lsu;               /* seconds: memory warp-instructions at 1 per SM cycle */
 } ispc_bound_report;
 /* l2_flushed: inputs start outside L2 (the timing flushes L2 between runs). */
 int ispc_bound(const ispc_space* s, const ispc_cand* c, int l2_flushed, ispc_bound_report* out);

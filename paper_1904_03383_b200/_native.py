@@ -167,7 +167,7 @@ class SpaceStats(C.Structure):
 
 class BoundReport(C.Structure):
     _fields_ = [(f, C.c_double) for f in ("total", "dram", "sm_mem", "issue", "thread", "launch", "dram_bytes",
-                                          "blocks_max", "threads_per_block_max", "dispatch", "l1")]
+                                          "blocks_max", "threads_per_block_max", "dispatch", "l1", "lsu")]
 
 
 class SearchConfig(C.Structure):

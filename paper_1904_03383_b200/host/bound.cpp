@@ -248,7 +248,7 @@ BoundReport BoundModel::bound(const Candidate& c) const {
   const double lanes = std::min(32.0, threads);
 
   // instructions that exist in every completion
-  double warp_insts = 0, thread_trips = 0, load_chain = 0;
+  double warp_insts = 0, mem_warp_insts = 0, thread_trips = 0, load_chain = 0;
   std::map<ObjId, double> region_touch;  // bytes each input region must move
   for (const InstRec& r : insts_) {
     if (r.lowering != kNoLowering && !((c.fired >> r.lowering) & 1u)) continue;
@@ -261,6 +261,7 @@ BoundReport BoundModel::bound(const Candidate& c) const {
     }
     double pack = packable ? (r.memory ? 4.0 : 2.0) : 1.0;
     warp_insts += std::ceil(r.instances / (lanes * pack));
+    if (r.memory) mem_warp_insts += std::ceil(r.instances / (lanes * pack));
     thread_trips += seq / pack;
     if (r.load) {  // trips of the dimensions certainly rolled loops around this load
       double trips = 1;
@@ -326,7 +327,8 @@ BoundReport BoundModel::bound(const Candidate& c) const {
   rep.launch = m_.launch_floor_s;
   rep.dispatch = blocks_lo * m_.block_dispatch_s;
   rep.l1 = l1_lines / (sms * m_.l1_lines_per_cycle * f);
-  rep.total = std::max({rep.dram, rep.sm_mem, rep.issue, rep.thread, rep.launch, rep.dispatch, rep.l1});
+  rep.lsu = mem_warp_insts / (sms * m_.lsu_per_cycle * f);
+  rep.total = std::max({rep.dram, rep.sm_mem, rep.issue, rep.thread, rep.launch, rep.dispatch, rep.l1, rep.lsu});
   return rep;
 }
 

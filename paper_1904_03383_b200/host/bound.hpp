@@ -32,6 +32,9 @@
 //           ceil(lanes x min(s, 32) / 32) 128-byte lines; lines / (active SMs
 //           x 2 lines/cycle x f_max) (the reference's coalescing rule,
 //           simulate.cpp:46-60, priced as L1 wavefronts)
+//   lsu     memory warp-instructions (instances / (active lanes x vector
+//           lanes), as in `issue`) / (active SMs x 1 per cycle x f_max): the
+//           load/store unit's issue floor (measured 1.82 cycles per LDG)
 // bound = max of the terms. All domain reads take the most optimistic value
 // still possible, so narrowing a domain can only raise a term (monotone), and
 // a leaf's bound is below its measured time (admissible; checked on every
@@ -80,6 +83,12 @@ struct B200Machine {
   int max_blocks_per_sm = 32;
   int max_threads_per_sm = 2048;
   double block_dispatch_s = 0.5e-9;  // per block, whatever the block does
+  // memory warp-instructions (global or shared, any width, any number of
+  // active lanes) an SM's load/store unit accepts per cycle: measured LDG
+  // issue floor 1.82 cycles per instruction (B300_MICROARCH.md "LDG"), 1 keeps
+  // the term admissible; a warp of a 1-thread block moves one vector per
+  // instruction, so tiny blocks pay it per element
+  double lsu_per_cycle = 1;
   double l1_lines_per_cycle = 2;     // per SM (the L1 serves ~1 wavefront/clk; 2 keeps a margin)
 };
 
@@ -88,7 +97,7 @@ enum class Illegal : int { None = 0, Grid, CrossBlock, Registers, Unrolled };
 
 struct BoundReport {
   Illegal illegal = Illegal::None;
-  double total = 0, dram = 0, sm_mem = 0, issue = 0, thread = 0, launch = 0, dispatch = 0, l1 = 0;
+  double total = 0, dram = 0, sm_mem = 0, issue = 0, thread = 0, launch = 0, dispatch = 0, l1 = 0, lsu = 0;
   double dram_bytes = 0;
   double blocks_max = 0, threads_per_block_max = 0;
 };

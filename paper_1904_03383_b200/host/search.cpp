@@ -1196,6 +1196,7 @@ int ispc_bound(const ispc_space* s, const ispc_cand* c, int l2_flushed, ispc_bou
     out->threads_per_block_max = r.threads_per_block_max;
     out->dispatch = r.dispatch;
     out->l1 = r.l1;
+    out->lsu = r.lsu;
     return ISPC_OK;
   } catch (const std::exception& e) {
     return set_err(ISPC_E_ARG, e.what());

@@ -118,9 +118,10 @@ template <int CH, int S>
 __global__ void __launch_bounds__(256) read_bulk_k(const float* __restrict__ a, long long n, float* out) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) unsigned long long full[S], empty[S];
-  const long long per = n / gridDim.x;  // floats
-  const float* p = a + per * blockIdx.x;
-  const int nch = int(per * 4 / CH);
+  // chunks b, b + G, b + 2G, ... of the whole array
+  const long long total = n * 4 / CH;
+  const int nch = int((total - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  const float* p = a;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       unsigned fa = (unsigned)__cvta_generic_to_shared(&full[s]), ea = (unsigned)__cvta_generic_to_shared(&empty[s]);
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(256) read_bulk_k(const float* __restrict__ a, 
     unsigned dst = (unsigned)__cvta_generic_to_shared(smem + s * CH);
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(fa), "r"(CH));
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(p + (long long)c * (CH / 4)), "r"(CH), "r"(fa)
+                 "l"(p + ((long long)c * gridDim.x + blockIdx.x) * (CH / 4)), "r"(CH), "r"(fa)
                  : "memory");
   };
   if (threadIdx.x == 0)
@@ -240,6 +241,12 @@ int main() {
   CHUNK(4, 2048, 256);
   CHUNK(8, 8 * sms, 256);
   CHUNK(16, 8 * sms, 128);
+  CHUNK(4, 4096, 256);
+  CHUNK(2, 4096, 256);
+  CHUNK(4, 2048, 512);
+  CHUNK(2, 8192, 256);
+  CHUNK(4, 1024, 1024);
+  CHUNK(1, 16384, 256);
 #define BULK(CH, S, G)                                                                                      \
   {                                                                                                         \
     auto k = read_bulk_k<CH, S>;                                                                            \
