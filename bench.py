@@ -206,8 +206,13 @@ CONFIG_SPACES = {
     # make_matmul(1024, 1024, 1024, {{2..32}, {2, 4}}) in gpu.space with the
     # reference's MachineParams (kernels.cpp:435-488), every leaf lowered by
     # the loop-nest emitter, bit-exact against the golden kernel
-    "matmul": ("matmul", dict(m=1024, n=1024, k=1024, factors=[[2, 4, 8, 16, 32], [2, 4]]), 256, False),
+    "matmul": ("matmul", dict(m=1024, n=1024, k=1024, factors=[[2, 4, 8, 16, 32], [2, 4]]), 96, False),
 }
+# per-config search options: the reference's matmul schedules at 1024^3 run
+# for milliseconds (its gpu.space has no shared-memory staging at this size,
+# SURVEY 0.5; the best leaf's bound is ~70 ms by the greedy descent), so their
+# watchdog budget is seconds rather than the headline's 50 ms
+CONFIG_SEARCH_KW = {"matmul": dict(max_budget_ns=3e9)}
 
 
 def safe_step(search, evals, seconds) -> bool:
@@ -255,12 +260,13 @@ def config_worker(args) -> None:
         import torch
         rot = rotation(space, torch.cuda.get_device_properties(args.ordinal).L2_cache_size)
     s = Search(space, device=args.ordinal, seed=0x1904 + args.ordinal, reps=3, warmup=1,
-               flush_l2=flush and rot < 2, rotate=rot)
+               flush_l2=flush and rot < 2, rotate=rot, **CONFIG_SEARCH_KW.get(name, {}))
     done = s.step(evals, max_seconds=4 * args.step_timeout)
     st = s.stats()
     best = s.best()
     s.close()
-    res = {"shape": kw, "evaluated": st["evaluations"], "ok": st["ok"], "mismatches": st["mismatches"],
+    res = {"shape": kw, "evaluated": st["evaluations"], "ok": st["ok"], "timeouts": st["timeouts"],
+           "mismatches": st["mismatches"],
            "illegal": st["illegal"], "launch_errors": st["launch_errors"], "exhausted": bool(st["exhausted"]),
            "deadline_hit": not done, "time_to_best_s": round(st["time_to_best_s"], 3),
            "bound_violations": st["bound_violations"], "search_s": round(time.perf_counter() - t0, 2)}
