@@ -171,15 +171,25 @@ def cublas_reference(space, reps: int = 20) -> dict | None:
         out["axpy"] = _time_rotating(mk([(n,), (n,)], lambda x, y: y.add_(x, alpha=1.5)), rot)
     elif kind == "gemv":
         out["sgemv"] = _time_rotating(mk([(n, m), (n,)], lambda at, x: torch.mv(at.t(), x)), rot)
-    elif kind in ("sgemm", "matmul"):
-        out["sgemm"] = _time_rotating(mk([(k, m), (n, k)], lambda a, bb: torch.mm(a.t(), bb.t())), rot)
+    # our problem's layout: A column-major M x K (storage = a (k, m) row-major),
+    # B column-major K x N (storage = bb (n, k)), C column-major M x N; in torch
+    # C's storage is torch.mm(bb, a) of shape (n, m): cuBLAS then solves
+    # exactly C = A B with A m-contiguous ("nn"). The "_tt" entries time the
+    # transposed product torch.mm(a.t(), bb.t()) (both operands k-contiguous
+    # for cuBLAS, kernel name ..._ttn_...): same flops, an easier layout for
+    # the TF32 tensor cores, reported for context only.
+    nn = lambda a, bb: torch.mm(bb, a)  # noqa: E731
+    tt = lambda a, bb: torch.mm(a.t(), bb.t())  # noqa: E731
+    if kind in ("sgemm", "matmul"):
+        out["sgemm"] = _time_rotating(mk([(k, m), (n, k)], nn), rot)
+        out["sgemm_tt"] = _time_rotating(mk([(k, m), (n, k)], tt), rot)
     elif kind == "batched":
-        out["sgemm_strided_batched"] = _time_rotating(
-            mk([(b, k, m), (b, n, k)], lambda a, bb: torch.bmm(a.transpose(1, 2), bb.transpose(1, 2))), rot)
+        out["sgemm_strided_batched"] = _time_rotating(mk([(b, k, m), (b, n, k)], lambda a, bb: torch.bmm(bb, a)), rot)
     elif kind in ("sgemm_tc", "sgemm_tc_x3"):
-        out["sgemm_fp32"] = _time_rotating(mk([(k, m), (n, k)], lambda a, bb: torch.mm(a.t(), bb.t())), rot, 3)
+        out["sgemm_fp32"] = _time_rotating(mk([(k, m), (n, k)], nn), rot, 3)
         torch.backends.cuda.matmul.allow_tf32 = True
-        out["sgemm_tf32"] = _time_rotating(mk([(k, m), (n, k)], lambda a, bb: torch.mm(a.t(), bb.t())), rot)
+        out["sgemm_tf32"] = _time_rotating(mk([(k, m), (n, k)], nn), rot)
+        out["sgemm_tf32_tt"] = _time_rotating(mk([(k, m), (n, k)], tt), rot)
         torch.backends.cuda.matmul.allow_tf32 = False
     res = {}
     for name, ns in out.items():
