@@ -160,6 +160,11 @@ int ispc_deadend_exact(const ispc_space* s, const ispc_cand* from, const char* o
  * no leaf is found within its node budget. */
 int ispc_greedy_leaf(const ispc_space* s, const ispc_cand* from, const char* order, ispc_cand** out,
                      double* bound_s);
+/* The reference's order round trip (nest_test.cpp:309-334) over every leaf
+ * below `from`: derive_orders(reconstruct(leaf)) against the leaf's order
+ * decisions. Counts leaves, derived pairs and pairs that disagree. */
+int ispc_order_round_trip(const ispc_space* s, const ispc_cand* from, int64_t node_budget, int64_t* leaves,
+                          int64_t* pairs, int64_t* mismatches);
 /* Paper section 5.4: nodes per depth of the first depth_cap levels and how
  * many have a B200 bound >= threshold_s (prunable against incumbent T). */
 int ispc_prune_profile(const ispc_space* s, const ispc_cand* from, const char* order, double threshold_s,
@@ -200,10 +205,14 @@ typedef struct {
   int32_t bucket;        /* TAG top-s set size (0: 20)                         */
   int32_t _pad;
   const char* log_path;  /* JSONL per rollout, NULL: none                      */
+  const char* resume_log; /* checkpoint: a log of an earlier run (same seed and
+                             configuration); its records are re-derived and must
+                             match, then the run continues to `budget` (NULL: none) */
 } ispc_spec_config;
 typedef struct {
   int64_t evaluations, rollouts, dead_rollouts, expanded, duplicates;
   int64_t time_to_best_evals;  /* evaluations when the best was first met     */
+  int64_t replayed;            /* resume-log records re-derived and matched    */
   int32_t exhausted;           /* the whole tree was evaluated or excluded     */
   int32_t _pad;
   double best_cost;            /* seconds (BOUND) or cycles (SIMULATE); inf: none */

@@ -252,12 +252,13 @@ class DeadendReport(C.Structure):
 class SpecConfig(C.Structure):
     _fields_ = [("budget", C.c_int64), ("max_rollouts", C.c_int64), ("seed", C.c_uint64), ("order", C.c_char_p),
                 ("pruning", C.c_int32), ("evaluator", C.c_int32), ("delta", C.c_double), ("bucket", C.c_int32),
-                ("_pad", C.c_int32), ("log_path", C.c_char_p)]
+                ("_pad", C.c_int32), ("log_path", C.c_char_p), ("resume_log", C.c_char_p)]
 
 
 class SpecResult(C.Structure):
     _fields_ = [("evaluations", C.c_int64), ("rollouts", C.c_int64), ("dead_rollouts", C.c_int64),
                 ("expanded", C.c_int64), ("duplicates", C.c_int64), ("time_to_best_evals", C.c_int64),
+                ("replayed", C.c_int64),
                 ("exhausted", C.c_int32), ("_pad", C.c_int32), ("best_cost", C.c_double),
                 ("best_digest", C.c_uint64)]
 
@@ -300,6 +301,8 @@ HOST_SYMBOLS = {
     "ispc_deadend_exact": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_int64, C.POINTER(C.c_double)]),
     "ispc_cand_descend": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_uint64, C.c_int,
                                     C.POINTER(C.c_void_p)]),
+    "ispc_order_round_trip": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
+                                        C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "ispc_greedy_leaf": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p),
                                    C.POINTER(C.c_double)]),
     "ispc_prune_profile": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_double, C.c_int, C.c_int64,

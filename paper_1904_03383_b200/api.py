@@ -18,16 +18,22 @@ from . import _native as N
 
 def explore_spec(space: "Space", budget: int, *, seed: int = 1, order: str | None = None, pruning: bool = True,
                  evaluator: str = "bound", delta: float = 0.05, bucket: int = 20, max_rollouts: int = 0,
-                 log_path: str | None = None) -> dict:
+                 log_path: str | None = None, resume_log: str | None = None) -> dict:
     """Deterministic single-threaded TAG-MCTS with a CPU
     evaluator: "bound" (the B200 bound x a digest-hashed factor in [1, 1.5),
-    admissible by construction) or "simulate" (the reference's cycles)."""
-    keep = [x.encode() if x else None for x in (order, log_path)]
+    admissible by construction) or "simulate" (the reference's cycles).
+    `resume_log`: the log of an earlier run is its checkpoint; it is replayed
+    (ValueError if a record differs) and the search continues to `budget`."""
+    keep = [x.encode() if x else None for x in (order, log_path, resume_log)]
     cfg = N.SpecConfig(budget=budget, max_rollouts=max_rollouts, seed=seed, order=keep[0], pruning=int(pruning),
                        evaluator={"bound": N.SPEC_EVAL_BOUND, "simulate": N.SPEC_EVAL_SIMULATE}[evaluator],
-                       delta=delta, bucket=bucket, log_path=keep[1])
+                       delta=delta, bucket=bucket, log_path=keep[1], resume_log=keep[2])
     r = N.SpecResult()
-    text = N.read_text(lambda *a: N.host().ispc_explore_spec(space._h, C.byref(cfg), C.byref(r), *a))
+    buf = C.create_string_buffer(1 << 20)
+    n = C.c_size_t(0)
+    if N.host().ispc_explore_spec(space._h, C.byref(cfg), C.byref(r), buf, len(buf), C.byref(n)) != 0:
+        raise ValueError(N.host_error())
+    text = buf.value.decode()
     out = {f: getattr(r, f) for f, _ in N.SpecResult._fields_ if f != "_pad"}
     out["exhausted"] = bool(out["exhausted"])
     out["best"] = space.deserialize(text) if text else None
@@ -240,6 +246,15 @@ class Candidate:
         if rc != 0:
             raise ValueError(N.host_error())
         return Candidate(self.space, h)
+
+    def order_round_trip(self, node_budget: int = 10 ** 6) -> dict:
+        """derive_orders over every leaf below here against the leaves' order
+        decisions (nest_test.cpp:309-334)."""
+        lv, pr, bad = C.c_int64(), C.c_int64(), C.c_int64()
+        if N.host().ispc_order_round_trip(self.space._h, self._h, node_budget, C.byref(lv), C.byref(pr),
+                                          C.byref(bad)) != 0:
+            raise ValueError(N.host_error())
+        return {"leaves": lv.value, "pairs": pr.value, "mismatches": bad.value}
 
     def deadend_exact(self, node_budget: int = 10 ** 6, order: str | None = None) -> float:
         """Exact dead-end probability of a uniform random descent from here."""
@@ -525,16 +540,22 @@ class Device:
 
 def explore_spec(space: "Space", budget: int, *, seed: int = 1, order: str | None = None, pruning: bool = True,
                  evaluator: str = "bound", delta: float = 0.05, bucket: int = 20, max_rollouts: int = 0,
-                 log_path: str | None = None) -> dict:
+                 log_path: str | None = None, resume_log: str | None = None) -> dict:
     """Deterministic single-threaded TAG-MCTS with a CPU
     evaluator: "bound" (the B200 bound x a digest-hashed factor in [1, 1.5),
-    admissible by construction) or "simulate" (the reference's cycles)."""
-    keep = [x.encode() if x else None for x in (order, log_path)]
+    admissible by construction) or "simulate" (the reference's cycles).
+    `resume_log`: the log of an earlier run is its checkpoint; it is replayed
+    (ValueError if a record differs) and the search continues to `budget`."""
+    keep = [x.encode() if x else None for x in (order, log_path, resume_log)]
     cfg = N.SpecConfig(budget=budget, max_rollouts=max_rollouts, seed=seed, order=keep[0], pruning=int(pruning),
                        evaluator={"bound": N.SPEC_EVAL_BOUND, "simulate": N.SPEC_EVAL_SIMULATE}[evaluator],
-                       delta=delta, bucket=bucket, log_path=keep[1])
+                       delta=delta, bucket=bucket, log_path=keep[1], resume_log=keep[2])
     r = N.SpecResult()
-    text = N.read_text(lambda *a: N.host().ispc_explore_spec(space._h, C.byref(cfg), C.byref(r), *a))
+    buf = C.create_string_buffer(1 << 20)
+    n = C.c_size_t(0)
+    if N.host().ispc_explore_spec(space._h, C.byref(cfg), C.byref(r), buf, len(buf), C.byref(n)) != 0:
+        raise ValueError(N.host_error())
+    text = buf.value.decode()
     out = {f: getattr(r, f) for f, _ in N.SpecResult._fields_ if f != "_pad"}
     out["exhausted"] = bool(out["exhausted"])
     out["best"] = space.deserialize(text) if text else None

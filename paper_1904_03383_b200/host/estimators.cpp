@@ -30,6 +30,7 @@
 
 #include "bound.hpp"
 #include "host_internal.hpp"
+#include "ispace/loop_nest.hpp"
 
 namespace ispc_host {
 
@@ -517,6 +518,50 @@ int ispc_deadend_exact(const ispc_space* s, const ispc_cand* from, const char* o
     } catch (const std::range_error&) {
       return set_err(ISPC_E_ARG, "exact dead-end probability refused: more than " + std::to_string(node_budget) +
                                      " nodes");
+    }
+    return ISPC_OK;
+  } catch (const std::exception& e) {
+    return set_err(ISPC_E_ARG, e.what());
+  }
+}
+
+// The reference's order round trip (nest_test.cpp:309-334) over every leaf
+// below `from`: reconstruct -> derive_orders (loop_nest.cpp:359-385), and each
+// derived pair's relation must be the single value the leaf's order(a, b)
+// instance holds (oriented like the reference test).
+int ispc_order_round_trip(const ispc_space* s, const ispc_cand* from, int64_t node_budget, int64_t* leaves,
+                          int64_t* pairs, int64_t* mismatches) {
+  try {
+    if (!s || !from || !leaves || !pairs || !mismatches || node_budget <= 0) return set_err(ISPC_E_ARG, "bad argument");
+    if (s->tiles) return set_err(ISPC_E_ARG, "order round trip: loop-nest spaces only");
+    const SpaceContext& ctx = *s->ctx;
+    const std::uint32_t order_c = ctx.table.find_choice("order");
+    if (order_c == kNoInstance) return set_err(ISPC_E_ARG, "space has no order choice");
+    *leaves = *pairs = *mismatches = 0;
+    SpaceTree t(ctx, from->c, nullptr);
+    std::vector<SpaceNode> stack{t.root()}, kids;
+    int64_t seen = 0;
+    while (!stack.empty()) {
+      SpaceNode n = std::move(stack.back());
+      stack.pop_back();
+      if (++seen > node_budget) return set_err(ISPC_E_ARG, "order round trip refused: node budget exceeded");
+      if (t.children(n, kids)) {
+        for (auto& k : kids) stack.push_back(std::move(k));
+        continue;
+      }
+      ++*leaves;
+      LoopNest l = reconstruct(s->kernel, ctx, n.c);
+      for (const auto& [pr, name] : derive_orders(l)) {
+        ++*pairs;
+        ObjId ids[2] = {pr.first, pr.second};
+        InstanceRef ref = ctx.table.resolve(order_c, ids, 2);
+        bool ok = ref.inst != kNoInstance;
+        if (ok) {
+          Mask m = ctx.table.oriented(order_c, n.c.dom[ref.inst], ref.swapped);
+          ok = mask_single(m) && ctx.table.choices[order_c].values[mask_first(m)] == name;
+        }
+        if (!ok) ++*mismatches;
+      }
     }
     return ISPC_OK;
   } catch (const std::exception& e) {

@@ -87,6 +87,16 @@ class SpecExplorer {
     }
     delta_ = cfg.delta > 0 ? cfg.delta : 0.05;
     bucket_ = cfg.bucket > 0 ? size_t(cfg.bucket) : 20;
+    // resume: the log of an earlier run with the same seed and configuration
+    // is the checkpoint; its records are re-derived (and must match byte for
+    // byte) before new ones are appended
+    if (cfg.resume_log && *cfg.resume_log) {
+      FILE* f = std::fopen(cfg.resume_log, "r");
+      if (!f) throw std::invalid_argument(std::string("cannot read resume log ") + cfg.resume_log);
+      char buf[1 << 16];
+      while (std::fgets(buf, sizeof(buf), f)) resume_.emplace_back(buf);
+      std::fclose(f);
+    }
     if (cfg.log_path && *cfg.log_path) log_ = std::fopen(cfg.log_path, "w");
     root_ = std::make_unique<SNode>();
     root_->cand = s->root;
@@ -98,10 +108,14 @@ class SpecExplorer {
   }
 
   void run(ispc_spec_result& res) {
-    while (st_.evaluations < cfg_.budget && !root_->exhausted) {
+    while ((st_.evaluations < cfg_.budget || replayed_ < resume_.size()) && !root_->exhausted) {
       if (cfg_.max_rollouts > 0 && st_.rollouts >= cfg_.max_rollouts) break;
       iterate();
     }
+    if (replayed_ < resume_.size() || diverged_)
+      throw std::runtime_error("resume log does not replay under this seed and configuration (record " +
+                               std::to_string(diverged_ ? first_diverged_ : replayed_ + 1) + ")");
+    st_.replayed = int64_t(replayed_);
     st_.exhausted = root_->exhausted ? 1 : 0;
     st_.best_cost = best_;
     st_.best_digest = best_digest_;
@@ -126,6 +140,10 @@ class SpecExplorer {
   uint64_t best_digest_ = 0;
   std::string best_text_;
   ispc_spec_result st_{};
+  std::vector<std::string> resume_;
+  size_t replayed_ = 0;
+  bool diverged_ = false;
+  size_t first_diverged_ = 0;
 
   double T() const { return cfg_.pruning ? best_ : kInf; }
 
@@ -294,7 +312,7 @@ class SpecExplorer {
 
   void log_rollout(const std::vector<int>& values, const std::vector<double>& bounds, double cost,
                    const char* tag) {
-    if (!log_) return;
+    if (!log_ && resume_.empty()) return;
     std::string p = "[", b = "[";
     for (size_t i = 0; i < values.size(); ++i) p += (i ? "," : "") + std::to_string(values[i]);
     for (size_t i = 0; i < bounds.size(); ++i) {
@@ -302,13 +320,21 @@ class SpecExplorer {
       std::snprintf(x, sizeof(x), "%s%.9g", i ? "," : "", bounds[i]);
       b += x;
     }
-    std::fprintf(log_, "{\"rollout\": %lld, \"seed\": %llu, \"path\": %s], \"ancestor_bounds\": %s], ",
-                 (long long)st_.rollouts, (unsigned long long)cfg_.seed, p.c_str(), b.c_str());
+    char head[160], tail[160];
+    std::snprintf(head, sizeof(head), "{\"rollout\": %lld, \"seed\": %llu, \"path\": ", (long long)st_.rollouts,
+                  (unsigned long long)cfg_.seed);
     if (tag)
-      std::fprintf(log_, "\"cost\": \"%s\", ", tag);
+      std::snprintf(tail, sizeof(tail), "\"cost\": \"%s\", ", tag);
     else
-      std::fprintf(log_, "\"cost\": %.9g, ", cost);
-    std::fprintf(log_, "\"best\": %.9g, \"evaluations\": %lld}\n", best_, (long long)st_.evaluations);
+      std::snprintf(tail, sizeof(tail), "\"cost\": %.9g, ", cost);
+    char fin[96];
+    std::snprintf(fin, sizeof(fin), "\"best\": %.9g, \"evaluations\": %lld}\n", best_, (long long)st_.evaluations);
+    const std::string rec = std::string(head) + p + "], \"ancestor_bounds\": " + b + "], " + tail + fin;
+    if (replayed_ < resume_.size()) {
+      if (resume_[replayed_] != rec && !diverged_) diverged_ = true, first_diverged_ = replayed_ + 1;
+      ++replayed_;
+    }
+    if (log_) std::fputs(rec.c_str(), log_);
   }
 };
 

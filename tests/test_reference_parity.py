@@ -128,3 +128,11 @@ def test_b200_mode_admits_shared_staging_the_parity_machine_cannot():
         counts[mode] = (shared, total)
     assert counts[N.SPACE_PARITY][0] == 0 and counts[N.SPACE_PARITY][1] > 20
     assert counts[N.SPACE_B200][0] > counts[N.SPACE_B200][1] // 2
+
+
+def test_order_decisions_round_trip_through_the_schedule_tree():
+    """nest_test.cpp:309-334: for all 768 leaves of outer_product(2, 2),
+    derive_orders(reconstruct(leaf)) yields 15 pairs, each the value of the
+    leaf's order decision."""
+    r = Space("outer_product", m=2, n=2).root().order_round_trip()
+    assert r == {"leaves": 768, "pairs": 768 * 15, "mismatches": 0}

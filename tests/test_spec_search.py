@@ -116,3 +116,23 @@ def test_uniform_walk_equals_the_reference_cpu_bench(kind, args, factors):
     ours = space.root().walk_digests(0x190403383, 24)
     assert ours == ref
     assert any(d == 0 for d in ref) and any(d != 0 for d in ref)  # both leaves and dead ends compared
+
+
+def test_checkpoint_resume_by_replay(tmp_path):
+    """SPEC.md:509 checkpoint/resume: the log of a run is its checkpoint. A run
+    resumed from it re-derives every logged record (refusing a log that does
+    not replay) and continues; the result equals one uninterrupted run."""
+    space = Space("outer_product", m=4096, n=4096)
+    a, b, c = (tmp_path / f"{x}.jsonl" for x in "abc")
+    first = explore_spec(space, 60, seed=3, log_path=str(a))
+    resumed = explore_spec(space, 150, seed=3, log_path=str(b), resume_log=str(a))
+    fresh = explore_spec(space, 150, seed=3, log_path=str(c))
+    assert resumed["replayed"] == first["rollouts"] > 0
+    assert b.read_bytes() == c.read_bytes()
+    assert resumed["best_digest"] == fresh["best_digest"] and resumed["evaluations"] == fresh["evaluations"]
+    lines = a.read_text().splitlines()
+    lines[5] = lines[5].replace('"seed": 3', '"seed": 4')
+    bad = tmp_path / "bad.jsonl"
+    bad.write_text("\n".join(lines) + "\n")
+    with pytest.raises(ValueError, match="record 6"):
+        explore_spec(space, 150, seed=3, resume_log=str(bad))
