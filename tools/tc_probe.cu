@@ -74,6 +74,7 @@ struct __align__(64) TMap { unsigned long long v[16]; };
 //       4 = SW128 by threads, 5 = SW128 by TMA (dump = landed bytes)
 __global__ void __launch_bounds__(128, 1) probe(int mode, const float* A, const float* B, float* out, int M, int N,
                                                 int K, const __grid_constant__ TMap tma, const __grid_constant__ TMap tmb,
+                                                const __grid_constant__ TMap tma32,
                                                 unsigned* dump) {
   extern __shared__ __align__(1024) unsigned char raw[];
   unsigned base = (saddr(raw) + 1023u) & ~1023u;
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(128, 1) probe(int mode, const float* A, const 
     ST32(tmem + ((unsigned)(warp * 32) << 16), r);
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   } else {
-    if (mode == 5) {
+    if (mode == 5 || mode == 10) {
       if (tid == 0) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fullb), "r"(16384u + 64u * 128u)
                      : "memory");
@@ -112,7 +113,7 @@ __global__ void __launch_bounds__(128, 1) probe(int mode, const float* A, const 
           asm volatile(
               "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
                   base + i * 4096u),
-              "l"(&tma), "r"(i * 32), "r"(0), "r"(fullb)
+              "l"(mode == 10 ? &tma32 : &tma), "r"(i * 32), "r"(0), "r"(fullb)
               : "memory");
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -129,7 +130,9 @@ __global__ void __launch_bounds__(128, 1) probe(int mode, const float* A, const 
           unsigned off;
           if (mode == 2) off = (m / 8) * 256 + (k / 4) * 128 + (m % 8) * 16 + (k % 4) * 4;
           else if (mode == 3) off = (m / 4) * 128 + (k % 8) * 16 + (m % 4) * 4;
-          else if (mode == 6) off = (m / 8) * 1024 + (m % 8) * 128 + ((((k % 32) / 4) ^ (m % 8)) * 16) + (k % 4) * 4;
+          else if (mode == 6 || mode == 7 || mode == 9) off = (m / 8) * 1024 + (m % 8) * 128 + ((((k % 32) / 4) ^ (m % 8)) * 16) + (k % 4) * 4;
+          else if (mode == 8)  // MN-major, 128-B swizzle with 32-B atoms: 4-row groups of 128-B rows
+            off = (m / 32) * 4096 + (k / 4) * 512 + (k % 4) * 128 + ((((m % 32) / 8) ^ (k % 4)) * 32) + (m % 8) * 4;
           else off = (m / 32) * 4096 + (k / 8) * 1024 + (k % 8) * 128 + ((((m % 32) / 4) ^ (k % 8)) * 16) + (m % 4) * 4;
           *(float*)(gen + off) = v;
         }
@@ -138,6 +141,8 @@ __global__ void __launch_bounds__(128, 1) probe(int mode, const float* A, const 
           float v = B[k + n * K];
           unsigned off;
           if (mode == 2 || mode == 3) off = (n / 8) * 256 + (k / 4) * 128 + (n % 8) * 16 + (k % 4) * 4;
+          else if (mode == 7) off = (n / 32) * 4096 + (k / 8) * 1024 + (k % 8) * 128 + ((((n % 32) / 4) ^ (k % 8)) * 16) + (n % 4) * 4;
+          else if (mode == 9) off = (n / 32) * 4096 + (k / 4) * 512 + (k % 4) * 128 + ((((n % 32) / 8) ^ (k % 4)) * 32) + (n % 8) * 4;
           else off = (n / 8) * 1024 + (n % 8) * 128 + ((((k % 32) / 4) ^ (n % 8)) * 16) + (k % 4) * 4;
           *(float*)(gen + 16384 + off) = v;
         }
@@ -146,8 +151,9 @@ __global__ void __launch_bounds__(128, 1) probe(int mode, const float* A, const 
     }
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const unsigned amaj = (mode == 3 || mode == 4 || mode == 5) ? 1u : 0u;
-      const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (amaj << 15) | (0u << 16) | ((64u >> 3) << 17) |
+      const unsigned amaj = (mode == 3 || mode == 4 || mode == 5 || mode == 8 || mode == 10) ? 1u : 0u;
+      const unsigned bmaj = (mode == 7 || mode == 9) ? 1u : 0u;
+      const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (amaj << 15) | (bmaj << 16) | ((64u >> 3) << 17) |
                              ((128u >> 4) << 24);
       if (mode == 2) {
         mma(tmem, desc(base, 128, 256, 0), desc(base + 16384, 128, 256, 0), idesc, 0);
@@ -157,6 +163,15 @@ __global__ void __launch_bounds__(128, 1) probe(int mode, const float* A, const 
       } else if (mode == 6) {
         for (int kk = 0; kk < 4; ++kk)
           mma(tmem, desc(base + kk * 32u, 16, 1024, 2), desc(base + 16384 + kk * 32u, 16, 1024, 2), idesc, kk != 0);
+      } else if (mode == 8 || mode == 10) {  // A MN-major, SWIZZLE_128B_BASE32B (layout 1): LBO 4 KiB per 32 m, SBO 512 B per 4 k
+        for (int kk = 0; kk < 4; ++kk)
+          mma(tmem, desc(base + kk * 1024u, 4096, 512, 1), desc(base + 16384 + kk * 32u, 16, 1024, 2), idesc, kk != 0);
+      } else if (mode == 9) {  // B MN-major, SWIZZLE_128B_BASE32B
+        for (int kk = 0; kk < 4; ++kk)
+          mma(tmem, desc(base + kk * 32u, 16, 1024, 2), desc(base + 16384 + kk * 1024u, 4096, 512, 1), idesc, kk != 0);
+      } else if (mode == 7) {  // A K-major (as P6), B MN-major: LBO 4 KiB between 32-n groups, SBO 1 KiB per 8 k
+        for (int kk = 0; kk < 4; ++kk)
+          mma(tmem, desc(base + kk * 32u, 16, 1024, 2), desc(base + 16384 + kk * 1024u, 4096, 1024, 2), idesc, kk != 0);
       } else {
         for (int kk = 0; kk < 4; ++kk)
           mma(tmem, desc(base + kk * 1024u, 4096, 1024, 2), desc(base + 16384 + kk * 32u, 16, 1024, 2), idesc,
@@ -193,7 +208,7 @@ int main() {
   CK(cudaMalloc(&dD, 65536 * 4));
   CK(cudaMemcpy(dA, hA.data(), hA.size() * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dB, hB.data(), hB.size() * 4, cudaMemcpyHostToDevice));
-  TMap ta{}, tb{};
+  TMap ta{}, tb{}, ta32{};
   {
     cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)K}, str[1] = {(cuuint64_t)M * 4};
     cuuint32_t box[2] = {32, 32}, es[2] = {1, 1};
@@ -201,6 +216,10 @@ int main() {
                                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     std::printf("encode A: %d\n", int(r));
+    r = cuTensorMapEncodeTiled((CUtensorMap*)&ta32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dA, dims, str, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    std::printf("encode A (128B, 32B atoms): %d\n", int(r));
     cuuint64_t dims2[2] = {(cuuint64_t)K, (cuuint64_t)N}, str2[1] = {(cuuint64_t)K * 4};
     cuuint32_t box2[2] = {32, 64};
     r = cuTensorMapEncodeTiled((CUtensorMap*)&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dB, dims2, str2, box2, es,
@@ -210,10 +229,10 @@ int main() {
   }
   CK(cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000));
   std::vector<unsigned> land4(16384 / 4 + 64 * 32);
-  for (int mode = 1; mode <= 6; ++mode) {
+  for (int mode = 1; mode <= 10; ++mode) {
     CK(cudaMemset(dO, 0xff, M * N * 4));
     CK(cudaMemset(dD, 0, 65536 * 4));
-    probe<<<1, 128, 70000>>>(mode, dA, dB, dO, M, N, K, ta, tb, dD);
+    probe<<<1, 128, 70000>>>(mode, dA, dB, dO, M, N, K, ta, tb, ta32, dD);
     cudaError_t e = cudaDeviceSynchronize();
     std::vector<float> o(M * N);
     std::vector<unsigned> dd(65536);
@@ -251,6 +270,18 @@ int main() {
           float v = hB[k + n * K];
           std::memcpy(&land4[(16384 + off) / 4], &v, 4);
         }
+    }
+    if (mode == 10) {
+      int diffA = 0;
+      for (int m = 0; m < 128; ++m)
+        for (int k = 0; k < 32; ++k) {
+          unsigned off = (m / 32) * 4096 + (k / 4) * 512 + (k % 4) * 128 + ((((m % 32) / 8) ^ (k % 4)) * 32) + (m % 8) * 4;
+          float v = hA[m + k * M];
+          unsigned u;
+          std::memcpy(&u, &v, 4);
+          diffA += dd[8192 + off / 4] != u;
+        }
+      std::printf("P10 landed A (TMA 128B_ATOM_32B) vs the BASE32B layout: %d/4096 words differ\n", diffA);
     }
     if (mode == 5) {
       int diffA = 0, diffB = 0;
