@@ -197,7 +197,7 @@ typedef struct {
 typedef struct {
   uint32_t param;        /* index of the kernel parameter it fills          */
   uint32_t rank;         /* 2 or 3                                          */
-  uint32_t swizzle;      /* 0 none, 1 32B, 2 64B, 3 128B                    */
+  uint32_t swizzle;      /* 0 none, 1 32B, 2 64B, 3 128B, 4 128B with 32-B atoms */
   uint32_t _pad;
   char region[24];       /* problem region name                             */
   uint64_t dims[3];      /* elements, innermost first                       */

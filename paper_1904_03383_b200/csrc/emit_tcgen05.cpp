@@ -2,31 +2,32 @@
 // matmul contraction (BASELINE.json config 5), C = A B with fp32 column-major
 // operands on the TF32 tensor pipe, fp32 accumulation in tensor memory.
 //
-// One CTA (split = 1) or a cluster pair (split = 2, cta_group::2, UMMA M = 256
-// over two SMs) computes a UMMA_M x BN tile of C with 256 threads per CTA:
-//   warp 0 lane 0  producer: per k block (32 deep) TMA boxes of this CTA's
-//                  B rows (BN / split of them) and, for staging TMA, its 128
-//                  A rows into stage s of a `stages`-deep ring; full[s]
-//                  counts the bytes (mbarrier expect_tx)
-//   warps 4-7      converters, row m = thread: tf32 UMMA reads K-major
-//                  operands only (MN-major reads zeros on sm_100a,
-//                  tools/tc_probe.cu) and A is m-contiguous, so each k block
-//                  of A is written K-major (128-B swizzle) into the stage:
-//                  staging TMA transposes the landed box, staging SHARED
-//                  loads A from global memory one k block ahead in
-//                  registers. TF32X3 also splits x -> big = cvt.rna.tf32(x),
-//                  small = x - big for A and (in place) B. They fence to the
-//                  async proxy and arrive on conv[s] (the leader's, remotely,
-//                  for a pair)
-//   warp 1         allocates BN TMEM columns; lane 0 of the (leader) CTA
-//                  issues 4 (x3 for TF32X3) tcgen05.mma per k block and
-//                  commits empty[s] (multicast to both CTAs of a pair), then
-//                  the accumulator barrier
-//   warps 0-7      epilogue: tcgen05.ld 32x32b.x32 (lane group = warp % 4,
-//                  column half = warp / 4), coalesced column-major stores
-// Operand descriptors: K-major, 128-B swizzle, rows of 32 tf32 (128 B),
-// 8-row atoms, SBO = 1 KiB; the k step inside the row advances the start
-// address by 32 B.
+// Both operands reach the UMMA straight from shared memory (kind::tf32, SS):
+//   A  column-major, so m-contiguous = MN-major. The TF32 UMMA reads an
+//      MN-major operand only in the 128-B swizzle with 32-B atoms
+//      (descriptor layout SWIZZLE_128B_BASE32B; with the plain 128-B swizzle it
+//      reads zeros), and TMA lands exactly that layout with
+//      CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B (tools/tc_probe.cu P8-P10): a
+//      {32 m x 32 k} box is 32 rows of 128 B (one per k), 32-B chunks XOR'd
+//      with k % 4; four boxes hold a CTA's 128 rows, LBO = 4 KiB between them,
+//      SBO = 512 B between groups of 4 k rows, +1 KiB per K = 8 MMA step.
+//   B  column-major K x N, so k-contiguous = K-major: one {32 k x BN/split n}
+//      box in the plain 128-B swizzle (SBO 1 KiB, +32 B per K = 8 step).
+// No thread touches the operands on the TF32 path: the MMA waits for the TMA
+// bytes. Converter warps run only where values must change or move:
+// TF32X3 splits A and B in place (big = cvt.rna.tf32(x), small = x - big
+// beside it, same layout), and staging SHARED brings A from global memory
+// through registers (one k block ahead) into the same MN-major layout.
+//
+// One-tile kernel (grid = 0): one CTA (split = 1) or a cluster pair
+// (split = 2, cta_group::2, UMMA M = 256 over two SMs, each CTA landing its
+// own 128 rows of A and half of B's BN rows) per UMMA_M x BN tile, 256 threads:
+//   warp 0 lane 0  producer: TMA ring of `stages` stages (full[s] expect_tx)
+//   warp 1         TMEM allocation (BN columns); lane 0 of the leader issues
+//                  4 (x3 for TF32X3) tcgen05.mma per k block and commits
+//                  empty[s] (multicast to both CTAs of a pair), then acc
+//   warps 4-7      converters (TF32X3 / staging SHARED only): conv[s]
+//   warps 0-7      epilogue: tcgen05.ld 32x32b.x32, coalesced column stores
 #include <cstdio>
 #include <cstring>
 #include <sstream>
@@ -68,6 +69,11 @@ static __device__ __forceinline__ unsigned long long ispc_umma_desc(unsigned add
   return (unsigned long long)((addr >> 4) & 0x3FFF) | ((unsigned long long)((lbo >> 4) & 0x3FFF) << 16) |
          ((unsigned long long)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
 }
+// MN-major operand, 128-B swizzle with 32-B atoms (layout type 1)
+static __device__ __forceinline__ unsigned long long ispc_umma_desc_mn32(unsigned addr, unsigned lbo, unsigned sbo) {
+  return (unsigned long long)((addr >> 4) & 0x3FFF) | ((unsigned long long)((lbo >> 4) & 0x3FFF) << 16) |
+         ((unsigned long long)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (1ull << 61);
+}
 static __device__ __forceinline__ void ispc_mbar_arrive(unsigned bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -86,6 +92,21 @@ static __device__ __forceinline__ void ispc_mma_tf32_ts(unsigned tmem, unsigned 
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem), "r"(ta), "l"(db), "r"(idesc),
+      "r"(accumulate) : "memory");
+}
+static __device__ __forceinline__ void ispc_mma_tf32_ss(unsigned tmem, unsigned long long da, unsigned long long db,
+                                                        unsigned idesc, unsigned accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem), "l"(da), "l"(db), "r"(idesc),
+      "r"(accumulate) : "memory");
+}
+static __device__ __forceinline__ void ispc_mma_tf32_ss_pair(unsigned tmem, unsigned long long da,
+                                                             unsigned long long db, unsigned idesc,
+                                                             unsigned accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem), "l"(da), "l"(db), "r"(idesc),
       "r"(accumulate) : "memory");
 }
 static __device__ __forceinline__ void ispc_mma_tf32_ts_pair(unsigned tmem, unsigned ta, unsigned long long db,
@@ -143,6 +164,7 @@ static __device__ __forceinline__ void ispc_mma_commit(unsigned bar) {
 )";
 }
 
+
 void tc_params(ispc_launch& L, int64_t M, int64_t N, int64_t K, int BNL) {
   // parameters: tensor maps over a and b, region a (register-staged A), region c
   L.num_params = 4;
@@ -166,7 +188,7 @@ void tc_params(ispc_launch& L, int64_t M, int64_t N, int64_t K, int BNL) {
   ispc_tmap& ta = L.tmaps[0];
   ta.param = 0;
   ta.rank = 2;
-  ta.swizzle = 3;
+  ta.swizzle = 4;  // 128-B swizzle, 32-B atoms: the MN-major TF32 operand layout
   std::snprintf(ta.region, sizeof(ta.region), "a");
   ta.dims[0] = uint64_t(M), ta.dims[1] = uint64_t(K);
   ta.strides[0] = uint64_t(M) * 4;
@@ -181,6 +203,90 @@ void tc_params(ispc_launch& L, int64_t M, int64_t N, int64_t K, int BNL) {
   tb.box[0] = 32, tb.box[1] = uint32_t(BNL);
 }
 
+// Stage layout and the pieces both kernels emit.
+struct TcStage {
+  int64_t a_bytes = 128 * 32 * 4, b_bytes = 0;
+  int64_t off_a = 0, off_b = 0, off_as = 0, off_bs = 0, stage = 0, tma_bytes = 0;
+};
+
+TcStage tc_stage(int BNL, bool X3, bool A_TMA) {
+  TcStage t;
+  t.b_bytes = int64_t(BNL) * 32 * 4;
+  t.off_a = 0;
+  t.off_b = t.a_bytes;
+  t.off_as = t.off_b + t.b_bytes;
+  t.off_bs = t.off_as + t.a_bytes;
+  t.stage = X3 ? t.off_bs + t.b_bytes : t.off_as;
+  t.tma_bytes = (A_TMA ? t.a_bytes : 0) + t.b_bytes;
+  return t;
+}
+
+// kind::tf32, fp32 accumulate, A MN-major, B K-major, N, M
+unsigned tc_idesc(int n, int um) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (unsigned(n >> 3) << 17) | (unsigned(um >> 4) << 24);
+}
+
+// The 4 (x3) MMAs of one k block from stage base `sa` into accumulator `acc`.
+void tc_emit_mmas(std::ostringstream& o, const TcStage& t, bool X3, const char* mma, const std::string& acc,
+                  const std::string& idesc, const std::string& first, const char* ind) {
+  o << ind << "#pragma unroll\n";
+  o << ind << "for (int kk = 0; kk < 4; ++kk) {\n";
+  o << ind << "  const unsigned long long da = ispc_umma_desc_mn32(sa + " << t.off_a << "u + kk * 1024u, 4096u, 512u);\n";
+  o << ind << "  const unsigned long long db = ispc_umma_desc(sa + " << t.off_b << "u + kk * 32u, 16u, 1024u);\n";
+  if (X3) {
+    o << ind << "  const unsigned long long das = ispc_umma_desc_mn32(sa + " << t.off_as
+      << "u + kk * 1024u, 4096u, 512u);\n";
+    o << ind << "  const unsigned long long dbs = ispc_umma_desc(sa + " << t.off_bs << "u + kk * 32u, 16u, 1024u);\n";
+    o << ind << "  " << mma << "(" << acc << ", das, db, " << idesc << ", (" << first << ") != 0);\n";
+    o << ind << "  " << mma << "(" << acc << ", da, dbs, " << idesc << ", 1u);\n";
+    o << ind << "  " << mma << "(" << acc << ", da, db, " << idesc << ", 1u);\n";
+  } else {
+    o << ind << "  " << mma << "(" << acc << ", da, db, " << idesc << ", (" << first << ") != 0);\n";
+  }
+  o << ind << "}\n";
+}
+
+// Converter work on stage `st` (generic pointer) of k block kb: thread `ct`
+// of `nct` converter threads. Staging SHARED: row m = ct % 128 stores its k
+// values v[] (16 or 32 of them, k0 = first k) into the MN-major layout.
+// TF32X3: every converter thread splits its share of the A and B float4s.
+void tc_emit_convert(std::ostringstream& o, const TcStage& t, bool X3, bool A_TMA, int nct, int kper,
+                     const char* ind) {
+  if (!A_TMA) {
+    // element (m, k) of the stage: (m / 32) 4 KiB + (k / 4) 512 B + (k % 4) 128 B + ((m % 32 / 8) ^ (k % 4)) 32 B + (m % 8) 4 B
+    o << ind << "#pragma unroll\n";
+    o << ind << "for (int q = 0; q < " << kper << "; ++q) {\n";
+    o << ind << "  const int k = k0 + q;\n";
+    o << ind << "  const unsigned off = (unsigned)(m >> 5) * 4096u + (unsigned)(k >> 2) * 512u + (unsigned)(k & 3) * 128u + "
+         "((((unsigned)(m & 31) >> 3) ^ (unsigned)(k & 3)) << 5) + (unsigned)(m & 7) * 4u;\n";
+    if (X3) {
+      o << ind << "  const float h = ispc_tf32_rna(v[q]);\n";
+      o << ind << "  *(float*)(st + " << t.off_a << " + off) = h;\n";
+      o << ind << "  *(float*)(st + " << t.off_as << " + off) = v[q] - h;\n";
+    } else {
+      o << ind << "  *(float*)(st + " << t.off_a << " + off) = v[q];\n";
+    }
+    o << ind << "}\n";
+  }
+  if (X3) {
+    auto split = [&](int64_t off, int64_t off_small, int64_t bytes) {
+      o << ind << "#pragma unroll 4\n";
+      o << ind << "for (int q = ct; q < " << bytes / 16 << "; q += " << nct << ") {\n";
+      o << ind << "  float4* px = (float4*)(st + " << off << ") + q;\n";
+      o << ind << "  const float4 x = *px;\n";
+      o << ind << "  float4 hi, lo;\n";
+      o << ind << "  hi.x = ispc_tf32_rna(x.x); hi.y = ispc_tf32_rna(x.y); hi.z = ispc_tf32_rna(x.z); hi.w = ispc_tf32_rna(x.w);\n";
+      o << ind << "  lo.x = x.x - hi.x; lo.y = x.y - hi.y; lo.z = x.z - hi.z; lo.w = x.w - hi.w;\n";
+      o << ind << "  *px = hi;\n";
+      o << ind << "  *((float4*)(st + " << off_small << ") + q) = lo;\n";
+      o << ind << "}\n";
+    };
+    if (A_TMA) split(t.off_a, t.off_as, t.a_bytes);
+    split(t.off_b, t.off_bs, t.b_bytes);
+  }
+  o << ind << "asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");  // the UMMA reads through the async proxy\n";
+}
+
 std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string& fn, ispc_launch& L);
 
 std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
@@ -191,7 +297,13 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
     illegal("the tensor-core tile stages A by TMA or through registers, B by TMA");
   if (c.engine != ISPC_ENGINE_TF32 && c.engine != ISPC_ENGINE_TF32X3) illegal("tcgen05 kernel needs a tensor engine");
   const bool X3 = c.engine == ISPC_ENGINE_TF32X3, A_TMA = c.staging == ISPC_STAGE_TMA;
+  const bool CONV = X3 || !A_TMA;
   const int T = 256;
+  const int PAIR0 = c.split > 1 ? c.split : 1;
+  // a pair's MMA (issued by the leader) reads both CTAs' stages: without
+  // converters, warp 2 lane 0 of each CTA relays its stage's TMA completion
+  // to the leader's conv barrier, which counts both CTAs
+  const bool RELAY = !CONV && PAIR0 == 2;
   if (!(BN == 64 || BN == 128 || BN == 256)) illegal("UMMA N must be 64, 128 or 256");
   if (PAIR != 1 && PAIR != 2) illegal("tcgen05 pairs at most two CTAs (cta_group::2)");
   if (S < 2 || S > 8) illegal("TMA ring depth must be 2..8");
@@ -199,27 +311,19 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   if (M % UM || N % BN || K % 32) illegal("shape not divisible by the UMMA_M x BN x 32 tile");
   if (M > (int64_t(1) << 31) || K > (int64_t(1) << 31) || N > (int64_t(1) << 31))
     illegal("shape too large for the tensor maps");
-  // tensor memory: accumulator in columns [0, BN), then one A slot per ring
-  // stage (32 columns = 32 k of this CTA's 128 rows; 64 with A small)
-  const int a_cols = X3 ? 64 : 32;
-  const int need_cols = BN + S * a_cols;
-  if (need_cols > 512) illegal("accumulator + A slots exceed 512 TMEM columns");
   int tcols = 32;
-  while (tcols < need_cols) tcols *= 2;
-  // smem ring stage (1 KiB aligned parts): ([A as landed, m contiguous]) [B rows, k contiguous] ([B small])
-  const int64_t a_bytes = 128 * 32 * 4, b_bytes = int64_t(BNL) * 32 * 4;
-  const int64_t off_b = A_TMA ? a_bytes : 0, off_bs = off_b + b_bytes;
-  const int64_t tma_bytes = off_b + b_bytes;
-  const int64_t stage = tma_bytes + (X3 ? b_bytes : 0);
-  const int64_t bar_off = S * stage;
+  while (tcols < BN) tcols *= 2;
+  const TcStage t = tc_stage(BNL, X3, A_TMA);
+  const int64_t bar_off = S * t.stage;
   const int nbar = 3 * S + 1;  // full[S], empty[S], conv[S], acc
   const int64_t smem = bar_off + (nbar + 1) * 8 + 1024;  // + slack to 1 KiB-align the base
   if (smem > 232448) illegal("TMA ring exceeds 227 KiB of shared memory");
-  // kind::tf32, fp32 accumulate, K-major operands, N = BN, M = UMMA_M
-  const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(UM >> 4) << 24);
+  const unsigned idesc = tc_idesc(BN, UM);
   const int64_t KB = K / 32, MB = M / UM;
-  const unsigned FULL = 0, EMPTY = 8u * S, CONV = 16u * S, ACC = 24u * S;
+  const unsigned FULL = 0, EMPTY = 8u * S, CONV_B = 16u * S, ACC = 24u * S;
   const char* cg = PAIR == 2 ? "2" : "1";
+  const char* mma = PAIR == 2 ? "ispc_mma_tf32_ss_pair" : "ispc_mma_tf32_ss";
+  const char* commit = PAIR == 2 ? "ispc_mma_commit_pair" : "ispc_mma_commit";
 
   std::ostringstream o;
   o << tcgen05_prelude();
@@ -270,103 +374,63 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   o << "      const int s = kb % " << S << ";\n";
   o << "      if (kb >= " << S << ") ispc_mbar_wait(bars + " << EMPTY << "u + 8u * s, ((kb / " << S << ") + 1) & 1);\n";
   o << "      const unsigned full = bars + " << FULL << "u + 8u * s;\n";
-  o << "      const unsigned sa = base + s * " << stage << "u;\n";
-  o << "      ispc_mbar_expect_tx(full, " << tma_bytes << "u);\n";
+  o << "      const unsigned sa = base + s * " << t.stage << "u;\n";
+  o << "      ispc_mbar_expect_tx(full, " << t.tma_bytes << "u);\n";
   if (A_TMA) {
     o << "      #pragma unroll\n";
-    o << "      for (int i = 0; i < 4; ++i) ispc_tma_2d(sa + i * 4096u, &tm_a, m_base + i * 32, kb * 32, full);\n";
+    o << "      for (int i = 0; i < 4; ++i) ispc_tma_2d(sa + " << t.off_a << "u + i * 4096u, &tm_a, m_base + i * 32, kb * 32, full);\n";
   }
-  o << "      ispc_tma_2d(sa + " << off_b << "u, &tm_b, kb * 32, n_blk * " << BN << " + rank * " << BNL
-    << ", full);\n";
+  o << "      ispc_tma_2d(sa + " << t.off_b << "u, &tm_b, kb * 32, n_blk * " << BN << " + rank * " << BNL << ", full);\n";
   o << "    }\n";
   o << "  } else if (warp == 1 && lane == 0 && rank == 0) {\n";
-  // MMA issuer (the pair's leader): A from tensor memory (slot s), B from the
-  // smem stage (K-major, 128-B swizzle); with cta_group::2 the same TMEM and
-  // smem addresses in the peer CTA supply rows 128..255 and the second half of B
-  const char* mma = PAIR == 2 ? "ispc_mma_tf32_ts_pair" : "ispc_mma_tf32_ts";
-  const char* commit = PAIR == 2 ? "ispc_mma_commit_pair" : "ispc_mma_commit";
+  // MMA issuer (the pair's leader): with cta_group::2 the same smem offsets in
+  // the peer CTA supply rows 128..255 of A and the second half of B
   o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
   o << "      const int s = kb % " << S << ";\n";
-  o << "      ispc_mbar_wait(bars + " << CONV << "u + 8u * s, (kb / " << S << ") & 1);\n";
+  o << "      ispc_mbar_wait(bars + " << (CONV || RELAY ? CONV_B : FULL) << "u + 8u * s, (kb / " << S << ") & 1);\n";
   o << "      asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
-  o << "      const unsigned sb = base + s * " << stage << "u + " << off_b << "u;\n";
-  o << "      const unsigned ta = tmem + " << BN << "u + s * " << a_cols << "u;\n";
-  o << "      #pragma unroll\n";
-  o << "      for (int kk = 0; kk < 4; ++kk) {\n";
-  o << "        const unsigned long long db = ispc_umma_desc(sb + kk * 32u, 16u, 1024u);\n";
-  if (X3) {
-    o << "        const unsigned long long dbs = ispc_umma_desc(sb + " << off_bs - off_b << "u + kk * 32u, 16u, 1024u);\n";
-    o << "        " << mma << "(tmem, ta + 32u + kk * 8u, db, " << idesc << "u, (kb | kk) != 0);\n";
-    o << "        " << mma << "(tmem, ta + kk * 8u, dbs, " << idesc << "u, 1u);\n";
-    o << "        " << mma << "(tmem, ta + kk * 8u, db, " << idesc << "u, 1u);\n";
-  } else {
-    o << "        " << mma << "(tmem, ta + kk * 8u, db, " << idesc << "u, (kb | kk) != 0);\n";
-  }
-  o << "      }\n";
-  o << "      " << commit << "(bars + " << EMPTY << "u + 8u * s);   // stage + A slot free (both CTAs of a pair)\n";
+  o << "      const unsigned sa = base + s * " << t.stage << "u;\n";
+  tc_emit_mmas(o, t, X3, mma, "tmem", std::to_string(idesc) + "u", "kb | kk", "      ");
+  o << "      " << commit << "(bars + " << EMPTY << "u + 8u * s);   // the stage is free (both CTAs of a pair)\n";
   o << "    }\n";
   o << "    " << commit << "(bars + " << ACC << "u);\n";
-  o << "  } else if (warp >= 4) {\n";
-  // converters, row m = thread = TMEM lane: A is m-contiguous, so each thread
-  // holds its row's 32 k values of a k block in registers (a transposed read
-  // of the landed TMA box, or straight from global memory one k block ahead)
-  // and tcgen05.st's them into the stage's A slot (TF32X3: big and small)
-  o << "    const int m = threadIdx.x - 128;\n";
-  o << "    const unsigned trow = (unsigned)((warp & 3) * 32) << 16;\n";
-  o << "    float v[32];\n";
-  if (!A_TMA) {
-    o << "    const float* pa = g_a + m_base + m;\n";
-    o << "    #pragma unroll\n";
-    o << "    for (int k = 0; k < 32; ++k) v[k] = __ldg(pa + (long long)k * " << M << "LL);\n";
+  if (RELAY) {
+    o << "  } else if (warp == 2 && lane == 0) {\n";
+    o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
+    o << "      const int s = kb % " << S << ";\n";
+    o << "      ispc_mbar_wait(bars + " << FULL << "u + 8u * s, (kb / " << S << ") & 1);\n";
+    o << "      ispc_mbar_arrive_rank(bars + " << CONV_B << "u + 8u * s, 0u);\n";
+    o << "    }\n";
   }
-  o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
-  o << "      const int s = kb % " << S << ";\n";
-  o << "      ispc_mbar_wait(bars + " << FULL << "u + 8u * s, (kb / " << S << ") & 1);\n";
-  o << "      unsigned char* st = gen + s * " << stage << ";\n";
-  if (A_TMA) {
-    o << "      const unsigned src_row = (m >> 5) * 4096u + (m & 3) * 4u;\n";
-    o << "      #pragma unroll\n";
-    o << "      for (int k = 0; k < 32; ++k)\n";
-    o << "        v[k] = *(const float*)(st + src_row + (k >> 3) * 1024u + (k & 7) * 128u + ((((m & 31) >> 2) ^ (k & 7)) << 4));\n";
+  if (CONV) {
+    o << "  } else if (warp >= 4) {\n";
+    o << "    const int m = threadIdx.x - 128, ct = m;\n";
+    if (!A_TMA) {
+      o << "    float v[32];\n";
+      o << "    const int k0 = 0;\n";
+      o << "    const float* pa = g_a + m_base + m;\n";
+      o << "    #pragma unroll\n";
+      o << "    for (int k = 0; k < 32; ++k) v[k] = __ldg(pa + (long long)k * " << M << "LL);\n";
+    }
+    o << "    for (int kb = 0; kb < " << KB << "; ++kb) {\n";
+    o << "      const int s = kb % " << S << ";\n";
+    o << "      ispc_mbar_wait(bars + " << FULL << "u + 8u * s, (kb / " << S << ") & 1);\n";
+    o << "      unsigned char* st = gen + s * " << t.stage << ";\n";
+    tc_emit_convert(o, t, X3, A_TMA, 128, 32, "      ");
+    o << "      asm volatile(\"bar.sync 1, 128;\" ::: \"memory\");\n";
+    if (PAIR == 2)  // the leader's conv barrier counts both CTAs
+      o << "      if (m == 0) ispc_mbar_arrive_rank(bars + " << CONV_B << "u + 8u * s, 0u);\n";
+    else
+      o << "      if (m == 0) ispc_mbar_arrive(bars + " << CONV_B << "u + 8u * s);\n";
+    if (!A_TMA) {  // next k block's A, issued after the arrive
+      o << "      if (kb + 1 < " << KB << ") {\n";
+      o << "        const float* pn = pa + (long long)(kb + 1) * 32 * " << M << "LL;\n";
+      o << "        #pragma unroll\n";
+      o << "        for (int k = 0; k < 32; ++k) v[k] = __ldg(pn + (long long)k * " << M << "LL);\n";
+      o << "      }\n";
+    }
+    o << "    }\n";
   }
-  o << "      const unsigned ta = tmem + trow + " << BN << "u + s * " << a_cols << "u;\n";
-  if (X3) {
-    o << "      float lo[32];\n";
-    o << "      #pragma unroll\n";
-    o << "      for (int k = 0; k < 32; ++k) { const float h = ispc_tf32_rna(v[k]); lo[k] = v[k] - h; v[k] = h; }\n";
-    o << "      ISPC_TMEM_ST32(ta, v);\n";
-    o << "      ISPC_TMEM_ST32(ta + 32u, lo);\n";
-    // B split in place (big) + small part beside it in the TMA stage
-    o << "      #pragma unroll 4\n";
-    o << "      for (int i = m; i < " << b_bytes / 16 << "; i += 128) {\n";
-    o << "        float4* pb = (float4*)(st + " << off_b << ") + i;\n";
-    o << "        const float4 x = *pb;\n";
-    o << "        float4 hi, l4;\n";
-    o << "        hi.x = ispc_tf32_rna(x.x); hi.y = ispc_tf32_rna(x.y); hi.z = ispc_tf32_rna(x.z); hi.w = ispc_tf32_rna(x.w);\n";
-    o << "        l4.x = x.x - hi.x; l4.y = x.y - hi.y; l4.z = x.z - hi.z; l4.w = x.w - hi.w;\n";
-    o << "        *pb = hi;\n";
-    o << "        *((float4*)(st + " << off_bs << ") + i) = l4;\n";
-    o << "      }\n";
-    o << "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
-  } else {
-    o << "      ISPC_TMEM_ST32(ta, v);\n";
-  }
-  o << "      asm volatile(\"tcgen05.wait::st.sync.aligned;\" ::: \"memory\");\n";
-  o << "      asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n";
-  // one arrive per CTA after the converter warps meet on named barrier 1
-  o << "      asm volatile(\"bar.sync 1, 128;\" ::: \"memory\");\n";
-  if (PAIR == 2)  // the leader's conv barrier counts both CTAs
-    o << "      if (m == 0) ispc_mbar_arrive_rank(bars + " << CONV << "u + 8u * s, 0u);\n";
-  else
-    o << "      if (m == 0) ispc_mbar_arrive(bars + " << CONV << "u + 8u * s);\n";
-  if (!A_TMA) {  // next k block's A, issued after the arrive so its release does not wait on the loads
-    o << "      if (kb + 1 < " << KB << ") {\n";
-    o << "        const float* pn = pa + (long long)(kb + 1) * 32 * " << M << "LL;\n";
-    o << "        #pragma unroll\n";
-    o << "        for (int k = 0; k < 32; ++k) v[k] = __ldg(pn + (long long)k * " << M << "LL);\n";
-    o << "      }\n";
-  }
-  o << "    }\n";
   o << "  }\n";
   o << "  __syncwarp();\n";
   // epilogue: TMEM lane group = warp % 4, column half = warp / 4
@@ -408,18 +472,6 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   L.reg_elems = 32;
   return o.str();
 }
-
-// Persistent variant (grid > 0): `grid` CTAs (grid / split clusters) walk the
-// UMMA_M x BN output tiles t = cluster, cluster + clusters, ... (m fastest);
-// every role keeps one running k-block counter across tiles, so the TMA ring
-// and the converters run ahead into the next tile, and the accumulator is
-// double-buffered in tensor memory: four dedicated epilogue warps (8-11)
-// drain tile i's buffer while the MMA lane fills the other with tile i+1.
-// Barriers: full[S], empty[S], conv[S] as in the one-tile kernel, plus
-// accfull[2] (MMA commit -> epilogue) and accempty[2] (epilogue -> the
-// leader's MMA lane; one arrive per CTA after the epilogue warps meet).
-// The 1 x 4 wave tail of a one-tile-per-CTA grid (512 tiles over 148 SMs =
-// 3.46 waves at 4096^3, BN 256) becomes 7 rounds of 74 pair tiles at BN 128.
 std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
   const int64_t M = c.m, N = c.n, K = c.k;
   // split: 1 = one CTA per tile, 2 = a cta_group::2 pair, 4 = two pairs in a
@@ -441,34 +493,30 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   if (M % UM || N % (BN * (QUAD ? 2 : 1)) || K % 32) illegal("shape not divisible by the UMMA_M x BN x 32 tile");
   if (M > (int64_t(1) << 31) || K > (int64_t(1) << 31) || N > (int64_t(1) << 31))
     illegal("shape too large for the tensor maps");
-  const int a_cols = X3 ? 64 : 32;
-  // two accumulator buffers when they fit beside the A slots, else one (the
-  // MMA of tile i + 1 then waits for the epilogue of tile i)
-  const int NB = 2 * BN + S * a_cols <= 512 ? 2 : 1;
-  const int need_cols = NB * BN + S * a_cols;
-  if (need_cols > 512) illegal("accumulator + A slots exceed 512 TMEM columns");
+  const bool CONV = X3 || !A_TMA;
+  const bool RELAY = !CONV && PAIR == 2;  // as in the one-tile kernel
+  // tensor memory holds only the accumulators, double buffered (2 x BN <= 512
+  // columns), so the epilogue of tile i overlaps the MMAs of tile i + 1
+  const int NB = 2;
   int tcols = 32;
-  while (tcols < need_cols) tcols *= 2;
-  const int64_t a_bytes = 128 * 32 * 4, b_bytes = int64_t(BNL) * 32 * 4;
-  const int64_t off_b = A_TMA ? a_bytes : 0, off_bs = off_b + b_bytes;
-  const int64_t tma_bytes = off_b + b_bytes;
-  const int64_t stage = tma_bytes + (X3 ? b_bytes : 0);
+  while (tcols < NB * BN) tcols *= 2;
+  const TcStage t = tc_stage(BNL, X3, A_TMA);
+  const int64_t stage = t.stage;
   const int64_t bar_off = S * stage;
   const int nbar = 3 * S + 4;  // full[S], empty[S], conv[S], accfull[2], accempty[2]
   const int64_t smem = bar_off + (nbar + 1) * 8 + 1024;
   if (smem > 232448) illegal("TMA ring exceeds 227 KiB of shared memory");
-  const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (unsigned(BN >> 3) << 17) | (unsigned(UM >> 4) << 24);
+  const unsigned idesc = tc_idesc(BN, UM);
   const int64_t KB = K / 32, MB = M / UM, TILES = MB * (N / BN / (QUAD ? 2 : 1));  // QUAD: tile pairs
   // tail split: when the last round of full tiles would leave most clusters
   // idle, its tiles are cut in half along n (UMMA N = BN / 2) and spread over
   // twice as many clusters
   const int64_t NCL = c.grid / CL, RFULL = TILES / NCL, REM = TILES - RFULL * NCL;
   const bool TS = !QUAD && BN == 256 && REM > 0 && 2 * REM <= NCL;
-  const unsigned idesc_half =
-      (1u << 4) | (2u << 7) | (2u << 10) | (unsigned((BN / 2) >> 3) << 17) | (unsigned(UM >> 4) << 24);
-  const unsigned FULL = 0, EMPTY = 8u * S, CONV = 16u * S, AFULL = 24u * S, AEMPTY = 24u * S + 16;
+  const unsigned idesc_half = tc_idesc(BN / 2, UM);
+  const unsigned FULL = 0, EMPTY = 8u * S, CONV_B = 16u * S, AFULL = 24u * S, AEMPTY = 24u * S + 16;
   const char* cg = PAIR == 2 ? "2" : "1";
-  const char* mma = PAIR == 2 ? "ispc_mma_tf32_ts_pair" : "ispc_mma_tf32_ts";
+  const char* mma = PAIR == 2 ? "ispc_mma_tf32_ss_pair" : "ispc_mma_tf32_ss";
   const char* commit = PAIR == 2 ? "ispc_mma_commit_pair" : "ispc_mma_commit";
   auto commit_to = [&](const std::string& bar, const char* mask) {  // both pairs (QUAD) or the own pair
     if (QUAD) return std::string("ispc_mma_commit_mask(") + bar + ", " + mask + ")";
@@ -553,18 +601,18 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   o << "        if (g >= " << S << ") ispc_mbar_wait(bars + " << EMPTY << "u + 8u * s, ((g / " << S << ") + 1) & 1);\n";
   o << "        const unsigned full = bars + " << FULL << "u + 8u * s;\n";
   o << "        const unsigned sa = base + s * " << stage << "u;\n";
-  o << "        ispc_mbar_expect_tx(full, " << tma_bytes << "u);\n";
+  o << "        ispc_mbar_expect_tx(full, " << t.tma_bytes << "u);\n";
   if (A_TMA && QUAD) {  // this CTA lands boxes 2 sub, 2 sub + 1 in itself and in the other pair's same-rank CTA
     o << "        const unsigned short amask = (unsigned short)((1u << rank) | (1u << (rank ^ 2u)));\n";
     o << "        #pragma unroll\n";
     o << "        for (int q = 2 * sub; q < 2 * sub + 2; ++q)\n";
-    o << "          ispc_tma_2d_mc(sa + q * 4096u, &tm_a, m_base + q * 32, kb * 32, full, amask);\n";
+    o << "          ispc_tma_2d_mc(sa + " << t.off_a << "u + q * 4096u, &tm_a, m_base + q * 32, kb * 32, full, amask);\n";
   } else if (A_TMA) {
     o << "        #pragma unroll\n";
-    o << "        for (int q = 0; q < 4; ++q) ispc_tma_2d(sa + q * 4096u, &tm_a, m_base + q * 32, kb * 32, full);\n";
+    o << "        for (int q = 0; q < 4; ++q) ispc_tma_2d(sa + " << t.off_a << "u + q * 4096u, &tm_a, m_base + q * 32, kb * 32, full);\n";
   }
   // the box always holds BN / PAIR rows; a half-width tile uses its first half
-  o << "        ispc_tma_2d(sa + " << off_b << "u, &tm_b, kb * 32, n_off + prank * (width / " << PAIR
+  o << "        ispc_tma_2d(sa + " << t.off_b << "u, &tm_b, kb * 32, n_off + prank * (width / " << PAIR
     << "), full);\n";
   o << "      }\n    }\n";
   o << "  } else if (warp == 1 && lane == 0 && prank == 0) {\n";
@@ -581,92 +629,61 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   o << "      const unsigned acc = tmem + ab * " << BN << "u;\n";
   o << "      for (int kb = 0; kb < " << KB << "; ++kb, ++g) {\n";
   o << "        const int s = g % " << S << ";\n";
-  o << "        ispc_mbar_wait(bars + " << CONV << "u + 8u * s, (g / " << S << ") & 1);\n";
+  o << "        ispc_mbar_wait(bars + " << (CONV || RELAY ? CONV_B : FULL) << "u + 8u * s, (g / " << S << ") & 1);\n";
   o << "        asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
-  o << "        const unsigned sb = base + s * " << stage << "u + " << off_b << "u;\n";
-  o << "        const unsigned ta = tmem + " << NB * BN << "u + s * " << a_cols << "u;\n";
-  o << "        #pragma unroll\n";
-  o << "        for (int kk = 0; kk < 4; ++kk) {\n";
-  o << "          const unsigned long long db = ispc_umma_desc(sb + kk * 32u, 16u, 1024u);\n";
-  if (X3) {
-    o << "          const unsigned long long dbs = ispc_umma_desc(sb + " << off_bs - off_b
-      << "u + kk * 32u, 16u, 1024u);\n";
-    o << "          " << mma << "(acc, ta + 32u + kk * 8u, db, " << idesc << "u, (kb | kk) != 0);\n";
-    o << "          " << mma << "(acc, ta + kk * 8u, dbs, " << idesc << "u, 1u);\n";
-    o << "          " << mma << "(acc, ta + kk * 8u, db, " << idesc << "u, 1u);\n";
-  } else {
-    o << "          " << mma << "(acc, ta + kk * 8u, db, " << idesc << "u, (kb | kk) != 0);\n";
-  }
-  o << "        }\n";
+  o << "        const unsigned sa = base + s * " << stage << "u;\n";
+  tc_emit_mmas(o, t, X3, mma, "acc", "idesc", "kb | kk", "        ");
   o << "        " << commit_to("bars + " + std::to_string(EMPTY) + "u + 8u * s", "(unsigned short)15") << ";\n";
   o << "      }\n";
   o << "      " << commit_to("bars + " + std::to_string(AFULL) + "u + 8u * ab", "pair_mask")
     << ";  // tile done: epilogue may drain\n";
   o << "    }\n";
-  o << "  } else if ((warp >= 4 && warp < 8) || warp >= 12) {\n";
-  // converters: two groups of 4 warps, group kh owns k = 16 kh .. 16 kh + 15
-  // of every k block (row m = TMEM lane of warp % 4)
-  o << "    const int m = threadIdx.x & 127, kh = warp >= 12 ? 1 : 0, ct = kh * 128 + m;\n";
-  o << "    const unsigned trow = (unsigned)((warp & 3) * 32) << 16;\n";
-  o << "    float v[16];\n";
-  o << "    int g = 0;\n";
-  o << "    for (int i = 0; i < my_tiles; ++i) {\n";
-  o << "      int m_blk, n_off, width;\n";
-  o << "      tile_of(i, m_blk, n_off, width);\n";
-  o << "      const int m_base = m_blk * " << UM << " + prank * 128;\n";
-  if (!A_TMA) {
-    o << "      const float* pa = g_a + m_base + m + (long long)kh * 16 * " << M << "LL;\n";
-    o << "      #pragma unroll\n";
-    o << "      for (int k = 0; k < 16; ++k) v[k] = __ldg(pa + (long long)k * " << M << "LL);\n";
+  if (RELAY) {
+    o << "  } else if (warp == 2 && lane == 0) {\n";
+    o << "    int g = 0;\n";
+    o << "    for (int i = 0; i < my_tiles; ++i)\n";
+    o << "      for (int kb = 0; kb < " << KB << "; ++kb, ++g) {\n";
+    o << "        const int s = g % " << S << ";\n";
+    o << "        ispc_mbar_wait(bars + " << FULL << "u + 8u * s, (g / " << S << ") & 1);\n";
+    o << "        ispc_mbar_arrive_rank(bars + " << CONV_B << "u + 8u * s, lead);\n";
+    o << "      }\n";
   }
-  o << "      for (int kb = 0; kb < " << KB << "; ++kb, ++g) {\n";
-  o << "        const int s = g % " << S << ";\n";
-  o << "        ispc_mbar_wait(bars + " << FULL << "u + 8u * s, (g / " << S << ") & 1);\n";
-  o << "        unsigned char* st = gen + s * " << stage << ";\n";
-  if (A_TMA) {
-    o << "        const unsigned src_row = (m >> 5) * 4096u + (m & 3) * 4u;\n";
-    o << "        #pragma unroll\n";
-    o << "        for (int q = 0; q < 16; ++q) {\n";
-    o << "          const int k = kh * 16 + q;\n";
-    o << "          v[q] = *(const float*)(st + src_row + (k >> 3) * 1024u + (k & 7) * 128u + ((((m & 31) >> 2) ^ (k & 7)) << 4));\n";
-    o << "        }\n";
+  if (CONV) {
+    // converters: two groups of 4 warps; staging SHARED: group kh brings k =
+    // 16 kh .. 16 kh + 15 of every k block of row m = thread; TF32X3: all 256
+    // threads split the landed A and B
+    o << "  } else if ((warp >= 4 && warp < 8) || warp >= 12) {\n";
+    o << "    const int m = threadIdx.x & 127, kh = warp >= 12 ? 1 : 0, ct = kh * 128 + m;\n";
+    if (!A_TMA) o << "    float v[16];\n    const int k0 = kh * 16;\n";
+    o << "    int g = 0;\n";
+    o << "    for (int i = 0; i < my_tiles; ++i) {\n";
+    o << "      int m_blk, n_off, width;\n";
+    o << "      tile_of(i, m_blk, n_off, width);\n";
+    o << "      const int m_base = m_blk * " << UM << " + prank * 128;\n";
+    if (!A_TMA) {
+      o << "      const float* pa = g_a + m_base + m + (long long)k0 * " << M << "LL;\n";
+      o << "      #pragma unroll\n";
+      o << "      for (int k = 0; k < 16; ++k) v[k] = __ldg(pa + (long long)k * " << M << "LL);\n";
+    }
+    o << "      for (int kb = 0; kb < " << KB << "; ++kb, ++g) {\n";
+    o << "        const int s = g % " << S << ";\n";
+    o << "        ispc_mbar_wait(bars + " << FULL << "u + 8u * s, (g / " << S << ") & 1);\n";
+    o << "        unsigned char* st = gen + s * " << stage << ";\n";
+    tc_emit_convert(o, t, X3, A_TMA, 256, 16, "        ");
+    o << "        asm volatile(\"bar.sync 1, 256;\" ::: \"memory\");\n";
+    if (PAIR == 2)
+      o << "        if (ct == 0) ispc_mbar_arrive_rank(bars + " << CONV_B << "u + 8u * s, lead);\n";
+    else
+      o << "        if (ct == 0) ispc_mbar_arrive(bars + " << CONV_B << "u + 8u * s);\n";
+    if (!A_TMA) {
+      o << "        if (kb + 1 < " << KB << ") {\n";
+      o << "          const float* pn = pa + (long long)(kb + 1) * 32 * " << M << "LL;\n";
+      o << "          #pragma unroll\n";
+      o << "          for (int k = 0; k < 16; ++k) v[k] = __ldg(pn + (long long)k * " << M << "LL);\n";
+      o << "        }\n";
+    }
+    o << "      }\n    }\n";
   }
-  o << "        const unsigned ta = tmem + trow + " << NB * BN << "u + s * " << a_cols << "u + kh * 16u;\n";
-  if (X3) {
-    o << "        float lo[16];\n";
-    o << "        #pragma unroll\n";
-    o << "        for (int k = 0; k < 16; ++k) { const float h = ispc_tf32_rna(v[k]); lo[k] = v[k] - h; v[k] = h; }\n";
-    o << "        ISPC_TMEM_ST16(ta, v);\n";
-    o << "        ISPC_TMEM_ST16(ta + 32u, lo);\n";
-    o << "        #pragma unroll 4\n";
-    o << "        for (int q = ct; q < " << b_bytes / 16 << "; q += 256) {\n";
-    o << "          float4* pb = (float4*)(st + " << off_b << ") + q;\n";
-    o << "          const float4 x = *pb;\n";
-    o << "          float4 hi, l4;\n";
-    o << "          hi.x = ispc_tf32_rna(x.x); hi.y = ispc_tf32_rna(x.y); hi.z = ispc_tf32_rna(x.z); hi.w = ispc_tf32_rna(x.w);\n";
-    o << "          l4.x = x.x - hi.x; l4.y = x.y - hi.y; l4.z = x.z - hi.z; l4.w = x.w - hi.w;\n";
-    o << "          *pb = hi;\n";
-    o << "          *((float4*)(st + " << off_bs << ") + q) = l4;\n";
-    o << "        }\n";
-    o << "        asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
-  } else {
-    o << "        ISPC_TMEM_ST16(ta, v);\n";
-  }
-  o << "        asm volatile(\"tcgen05.wait::st.sync.aligned;\" ::: \"memory\");\n";
-  o << "        asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n";
-  o << "        asm volatile(\"bar.sync 1, 256;\" ::: \"memory\");\n";
-  if (PAIR == 2)
-    o << "        if (ct == 0) ispc_mbar_arrive_rank(bars + " << CONV << "u + 8u * s, lead);\n";
-  else
-    o << "        if (ct == 0) ispc_mbar_arrive(bars + " << CONV << "u + 8u * s);\n";
-  if (!A_TMA) {
-    o << "        if (kb + 1 < " << KB << ") {\n";
-    o << "          const float* pn = pa + (long long)(kb + 1) * 32 * " << M << "LL;\n";
-    o << "          #pragma unroll\n";
-    o << "          for (int k = 0; k < 16; ++k) v[k] = __ldg(pn + (long long)k * " << M << "LL);\n";
-    o << "        }\n";
-  }
-  o << "      }\n    }\n";
   o << "  } else if (warp >= 8 && warp < 12) {\n";
   // epilogue warps: lane group = warp % 4
   o << "    const int lg = warp & 3;\n";

@@ -1220,7 +1220,13 @@ std::string emit_tile_kernel(const ispc_tile_config& c, const std::string& fn, i
     default: throw NestError(ISPC_E_ARG, "unknown tile kind");
   }
   if (L.static_smem > 232448) illegal("shared memory exceeds 227 KiB");
-  L.source_hash = fnv1a(src);
+  // the launch configuration is part of the candidate: two configurations
+  // whose sources coincide (a persistent grid reads gridDim) are different
+  // kernels to time, and get different names
+  char launch_sig[160];
+  std::snprintf(launch_sig, sizeof(launch_sig), "\n// launch grid %llu block %u cluster %u smem %u\n",
+                (unsigned long long)L.grid_x, L.block[0], L.cluster[0], L.static_smem);
+  L.source_hash = fnv1a(src + launch_sig);
   return src;
 }
 

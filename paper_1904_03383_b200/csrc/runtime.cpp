@@ -690,12 +690,14 @@ int bind_kernel(ispc_dev* d, Loaded& mod, const ispc_launch* L, uint32_t rotate,
       cuuint64_t strides[2] = {tm->strides[0], tm->strides[1]};
       cuuint32_t box[3] = {tm->box[0], tm->box[1], tm->box[2]};
       cuuint32_t estr[3] = {1, 1, 1};
-      static const CUtensorMapSwizzle sw[4] = {CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
-                                               CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_SWIZZLE_128B};
+      static const CUtensorMapSwizzle sw[5] = {CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                                               CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_SWIZZLE_128B,
+                                               CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B};
+      if (tm->swizzle > 4) return fail(d, ISPC_E_ARG, "tensor map swizzle mode");
       for (uint32_t c = 0; c < B.R; ++c)
         CU(d, drv.TensorMapEncodeTiled(&B.tmaps[c][ti], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, tm->rank,
                                        region_ptr(c, tm->region), dims, strides, box, estr,
-                                       CU_TENSOR_MAP_INTERLEAVE_NONE, sw[tm->swizzle & 3],
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE, sw[tm->swizzle],
                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
       B.tmap_of[i] = int(ti);
     } else {

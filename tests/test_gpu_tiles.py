@@ -195,9 +195,22 @@ def test_tcgen05_sgemm(dev, engine):
     assert ok >= 8, ok
 
 
+def tc_ring_fits(engine, pair, bn, stages):
+    """The emitter's shared-memory rule (emit_tcgen05.cpp tc_stage): a stage
+    holds A (16 KiB, 128 rows x 32 k) and this CTA's B rows (BN / pair x 128 B),
+    3xTF32 adds the small halves of both; the ring plus its barriers must fit
+    in 227 KiB."""
+    bnl = int(bn) // (2 if int(pair) >= 2 else 1)
+    stage = 16384 + bnl * 128
+    if engine == "TF32X3":
+        stage *= 2
+    return int(stages) * stage + 1024 + 8 * (3 * int(stages) + 6) <= 232448
+
+
 # static legality of the variants below (emitter rules, checked on the host):
-# 3xTF32 on one CTA with TMA-staged A cannot hold a BN 256 ring of 3 stages
-TC_ILLEGAL = {("TF32X3", "TMA", "1", "256")}
+# at 3 stages, 3xTF32 on one CTA cannot hold a BN 256 ring (96 KiB stages)
+TC_ILLEGAL = {(e, s, p, b) for e in ("TF32", "TF32X3") for s in ("TMA", "SHARED") for p in ("1", "2")
+              for b in ("64", "128", "256") if not tc_ring_fits(e, p, b, 3)}
 
 
 @pytest.mark.parametrize("bn", ["64", "128", "256"])
@@ -241,6 +254,10 @@ def test_tcgen05_persistent(dev, engine, pair, staging, bn):
     t = c.first_leaf().tiles()
     if pair == "4" and staging == "SHARED":
         with pytest.raises(EmitError, match="multicast"):
+            tile_cuda(t, "probe")
+        return
+    if not tc_ring_fits(engine, pair, bn, 4):
+        with pytest.raises(EmitError, match="227 KiB"):
             tile_cuda(t, "probe")
         return
     m = dev.evaluate_tiles(t, reps=2, warmup=1)
@@ -311,7 +328,7 @@ def test_search_policy_knobs(monkeypatch, capsys, knobs):
 @pytest.mark.parametrize("engine", ["TF32", "TF32X3"])
 @pytest.mark.parametrize("pair", ["1", "2"])
 def test_tcgen05_persistent_tail_split(dev, engine, pair):
-    """BN 256 persistent grid with one accumulator: the last, partial round of
+    """BN 256 persistent grid: the last, partial round of
     tiles is cut into half-width tiles (UMMA N = 128) spread over twice as many
     clusters (160 / 320 tiles over 74 / 148 clusters)."""
     space = Space("sgemm_tc", m=4096, n=2560, k=64)

@@ -473,11 +473,14 @@ int main() {
   ref_k<<<dim3(M / 128, N), 128, 0, st>>>(bf.a[0], bf.b[0], ref, M, N, K);
 #define RUN3(WX, WY, LX, LY, BK, S, P, ...) run3<WX, WY, LX, LY, BK, S, P, ##__VA_ARGS__>(bf, ref, M, N, K, R, st)
   RUN3(2, 2, 8, 4, 16, 3, 4);   // 128x64, 128 thr (cuBLAS's tile)
-  RUN3(2, 2, 8, 4, 16, 3, 4, 8, 8, 1, 1, 2);
-  RUN3(2, 2, 8, 4, 16, 3, 4, 8, 8, 0, 1, 2);
-  RUN3(2, 2, 8, 4, 32, 3, 4, 8, 8, 1, 1, 2);
-  RUN3(2, 2, 8, 4, 16, 3, 4, 8, 8, 1, 1, 4);
-  RUN3(4, 2, 8, 4, 16, 3, 4, 4, 8, 1, 1, 2);
-  RUN3(2, 1, 8, 4, 16, 3, 4, 8, 8, 1, 1, 2);
+  RUN3(4, 2, 8, 4, 16, 3, 4, 4, 8, 0);      // 128x64, 256 thr 4x8, FFMA
+  RUN3(4, 2, 8, 4, 32, 3, 4, 4, 8, 0);
+  RUN3(2, 4, 8, 4, 16, 3, 4, 8, 4, 0);      // 128x64, 256 thr 8x4, FFMA
+  RUN3(4, 2, 8, 4, 16, 4, 4, 4, 8, 0);
+  RUN3(2, 2, 8, 4, 16, 3, 4, 8, 8, 0, 1, 2);  // split-K 2: 2 CTAs/SM, FFMA
+  RUN3(4, 2, 8, 4, 16, 3, 4, 4, 8, 0, 1, 2);  // split-K 2, 256 thr 4x8 FFMA
+  RUN3(4, 2, 8, 4, 16, 3, 4, 4, 8, 1, 1, 2);  // same FFMA2
+  RUN3(4, 4, 8, 4, 16, 3, 4, 4, 4, 0);      // 128x64 512 thr 4x4 FFMA
+  RUN3(2, 2, 8, 4, 16, 3, 4, 4, 8, 0);      // 64x64 128 thr 4x8 FFMA (256 CTAs)
   return 0;
 }
