@@ -184,6 +184,8 @@ __global__ void flush_read_kernel(const uint4* __restrict__ p, int64_t n, unsign
   if (acc == 0x9e3779b9u) *sink = acc;  // practically never: keeps the loads alive
 }
 
+__global__ void fault_kernel(float* bad) { bad[threadIdx.x] = 1.0f; }
+
 __global__ void timer_kernel(unsigned long long* out) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -255,6 +257,11 @@ cudaError_t launch_flush_read(const void* p, size_t bytes, void* sink, cudaStrea
 
 cudaError_t launch_timer(unsigned long long* out, cudaStream_t s) {
   timer_kernel<<<1, 1, 0, s>>>(out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fault(cudaStream_t s) {
+  fault_kernel<<<1, 32, 0, s>>>(reinterpret_cast<float*>(uintptr_t(8)));
   return cudaGetLastError();
 }
 

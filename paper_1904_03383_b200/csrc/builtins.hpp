@@ -31,5 +31,8 @@ cudaError_t launch_check(const float* out, const float* exp, const float* scale,
 cudaError_t launch_collect(const int* timeout_flag, void* slot, cudaStream_t s);
 cudaError_t launch_timer(unsigned long long* out, cudaStream_t s);
 cudaError_t launch_flush_read(const void* p, size_t bytes, void* sink, cudaStream_t s);
+// Fault injection (tests of the context-respawn path): a store through an
+// invalid address, i.e. a context-killing illegal-address fault.
+cudaError_t launch_fault(cudaStream_t s);
 
 }  // namespace ispc

@@ -332,6 +332,27 @@ void ispc_dev_close(ispc_dev* d) {
   delete d;
 }
 
+int ispc_device_reset(int ordinal) {
+  // a sticky fault poisons the primary context of the whole process: destroy
+  // it and create a fresh one (every ispc_dev of this ordinal must have been
+  // closed first; their handles died with the old context)
+  cudaError_t e = cudaSetDevice(ordinal);
+  if (e != cudaSuccess && !sticky(e)) return cuda_fail(nullptr, e, "cudaSetDevice");
+  (void)cudaGetLastError();
+  if ((e = cudaDeviceReset()) != cudaSuccess) return cuda_fail(nullptr, e, "cudaDeviceReset");
+  if ((e = cudaFree(nullptr)) != cudaSuccess) return cuda_fail(nullptr, e, "cudaFree after the reset");
+  return ISPC_OK;
+}
+
+int ispc_dev_inject_fault(ispc_dev* d) {
+  if (!d) return ISPC_E_ARG;
+  int rc = bind_ctx(d);
+  if (rc) return rc;
+  CK(d, ispc::launch_fault(d->stream));
+  CK(d, cudaStreamSynchronize(d->stream));
+  return fail(d, ISPC_E_CUDA, "the injected fault did not fault");
+}
+
 int ispc_dev_info(const ispc_dev* d, int* sm_count, int64_t* l2_bytes, int64_t* hbm_bytes, int* sm_clock_khz) {
   if (!d) return ISPC_E_ARG;
   if (sm_count) *sm_count = d->sm_count;

@@ -49,6 +49,12 @@ void Incumbent::pin() {
   if (map && !pinned) pinned = ispc_host_register(map, map_bytes) == ISPC_OK;
 }
 
+// after a device reset the registration died with the old context
+void Incumbent::repin() {
+  pinned = false;
+  pin();
+}
+
 Incumbent::~Incumbent() {
   if (map) {
     if (pinned) ispc_host_unregister(map);
@@ -143,6 +149,7 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
   order_ = DecisionOrder::from_names(*space_->ctx, split(order_text_));
   inc_.open(shm_text_.empty() ? nullptr : shm_text_.c_str());
   trace_ = std::getenv("ISPC_TRACE") != nullptr;
+  if (const char* e = std::getenv("ISPC_INJECT_FAULT_AT")) inject_fault_at_ = std::atoll(e);
   if (const char* ld = std::getenv("ISPC_LOG_DEADENDS")) log_dead_ = std::atoi(ld) != 0;
   if (const char* g = std::getenv("ISPC_GREEDY")) {
     const std::string v(g);
@@ -786,11 +793,14 @@ void Search::compile_items(std::vector<std::unique_ptr<Work>> items) {
   }
   // load the cubins here, off the launch thread (module load and the eager
   // upload of its kernels overlap the device's work on earlier batches)
-  if (dev_)
-    for (auto& b : out) {
-      b->load_rc = ispc_module_load(dev_, b->module, &b->handle);
-      if (b->load_rc != ISPC_OK) b->load_err = ispc_last_error(dev_);
-    }
+  {
+    std::shared_lock<std::shared_mutex> dl(dev_mu_);
+    if (dev_)
+      for (auto& b : out) {
+        b->load_rc = ispc_module_load(dev_, b->module, &b->handle);
+        if (b->load_rc != ISPC_OK) b->load_err = ispc_last_error(dev_);
+      }
+  }
   t_compile_.fetch_add(now() - t);
   std::lock_guard<std::mutex> lk(mu_);
   for (auto& b : out) batch_q_.push_back(std::move(b));
@@ -859,6 +869,38 @@ void Search::log_dead(int tid, int64_t rollout_no, const char* reason) {
 }
 
 
+bool Search::respawn() {
+  std::unique_lock<std::shared_mutex> dl(dev_mu_);  // no module loads meanwhile
+  retired_.clear();                                 // their handles died with the context
+  ispc_dev_close(dev_);
+  dev_ = nullptr;
+  if (ispc_device_reset(cfg_.device) != ISPC_OK) {
+    err_ += std::string("; device reset failed: ") + ispc_last_error(nullptr);
+    return false;
+  }
+  ispc_problem p{};
+  if (ispc_dev_open(cfg_.device, &dev_) != ISPC_OK || ispc_space_problem(space_, &p) != 0 ||
+      ispc_bind_problem(dev_, &p) != ISPC_OK) {
+    err_ += std::string("; device reopen failed: ") + ispc_last_error(dev_);
+    return false;
+  }
+  inc_.repin();
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (auto& q : batch_q_) {  // compiled against the old context: load the cubins again
+      q->handle = 0;
+      q->load_rc = q->module ? ispc_module_load(dev_, q->module, &q->handle) : ISPC_E_ARG;
+      if (q->load_rc != ISPC_OK) q->load_err = ispc_last_error(dev_);
+    }
+    step_open_ = false;
+    ++respawns_;
+    err_.clear();
+  }
+  if (trace_) std::fprintf(stderr, "[ispc] sticky fault: device %d respawned (%lld)\n", cfg_.device,
+                           (long long)respawns_);
+  return true;
+}
+
 void Search::launch_worker() {
   bool& step_open = step_open_;
   while (!stop_) {
@@ -885,6 +927,8 @@ void Search::launch_worker() {
       // dry run: the compiled kernels count as evaluated; a module that did
       // not load: every kernel of it is a launch error (a sticky fault ends
       // the search, as in ispc_launch_batch)
+      bool respawn_needed = false;
+      {
       std::lock_guard<std::mutex> lk(mu_);
       if (!dev_ && log_) {
         for (int64_t i = 0; i < n; ++i) {
@@ -899,11 +943,19 @@ void Search::launch_worker() {
         st_.launch_errors += n;
         if (b->load_rc == ISPC_E_STICKY) {
           err_ = b->load_err;
-          stop_ = true;
+          respawn_needed = true;
         }
       }
       ispc_module_free(b->module);
-      launching_ = false;
+      }
+      if (respawn_needed && !respawn()) {
+        std::lock_guard<std::mutex> lk(mu_);
+        stop_ = true;
+      }
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        launching_ = false;
+      }
       cv_done_.notify_all();
       continue;
     }
@@ -944,7 +996,10 @@ void Search::launch_worker() {
     const double refine_below = std::isfinite(T) ? T * 1e9 * refine_factor_ : std::numeric_limits<double>::infinity();
     std::vector<ispc_time_result> res(static_cast<size_t>(n));
     const double t_dev0 = now();
-    const int brc = ispc_launch_batch(dev_, b->handle, int(n), items.data(), refine_below, res.data());
+    ++batches_launched_;
+    const int brc = batches_launched_ == inject_fault_at_
+                        ? ispc_dev_inject_fault(dev_)  // test hook: the batch dies with the context
+                        : ispc_launch_batch(dev_, b->handle, int(n), items.data(), refine_below, res.data());
     const double t_dev = now() - t_dev0;
     const std::string berr = brc ? ispc_last_error(dev_) : std::string();
     // cuModuleUnload measured 1.4-231 ms per call on the B200 (it waits on
@@ -957,6 +1012,7 @@ void Search::launch_worker() {
       for (size_t k = 0; k < kMaxRetired / 2; ++k) ispc_module_unload(dev_, retired_[k]);
       retired_.erase(retired_.begin(), retired_.begin() + long(kMaxRetired / 2));
     }
+    bool sticky_batch = false;
     {
       std::lock_guard<std::mutex> lk(mu_);
       for (int64_t i = 0; i < n; ++i) {
@@ -975,7 +1031,7 @@ void Search::launch_worker() {
           status = rc == ISPC_E_STICKY ? "sticky" : "launch_error";
           if (rc == ISPC_E_STICKY) {
             err_ = berr;
-            stop_ = true;
+            sticky_batch = true;
           }
         } else {
           step_busy_ms_ += r.first_ns * 1e-6;
@@ -1011,9 +1067,20 @@ void Search::launch_worker() {
         if (log_) log_eval(w, r, rc, status, t_now, improved);
       }
       if (log_) std::fflush(log_);  // once per batch
-      if (step_open && st_.evaluations >= target_.load()) close_step();
+      if (step_open && st_.evaluations >= target_.load() && !sticky_batch) close_step();
       t_launch_host_ += (now() - t_busy) - t_dev;
       st_.t_gpu_s += now() - t_busy;
+      if (!sticky_batch) launching_ = false;
+    }
+    if (sticky_batch) {
+      // a context-killing fault: replace the device (new primary context,
+      // the problem re-bound, queued modules reloaded) and go on, unless the
+      // fault is a kernel that still runs (a reset would wait on it)
+      const bool hung = err_.find("still running") != std::string::npos;
+      const bool ok = !hung && respawn();
+      std::lock_guard<std::mutex> lk(mu_);
+      if (!ok) stop_ = true;
+      if (step_open && st_.evaluations >= target_.load()) step_open = false;
       launching_ = false;
     }
     cv_done_.notify_all();
@@ -1132,6 +1199,7 @@ ispc_search_stats Search::stats() const {
   s.incumbent_ns = inc_.seconds() * 1e9;
   s.exhausted = exhausted_ ? 1 : 0;
   s.stealing_since = stealing_since_;
+  s.respawns = respawns_;
   s.elapsed_s = now() - t0_;
   s.refined = refined_;
   s.t_launch_host_s = t_launch_host_;

@@ -27,6 +27,7 @@
 #include <deque>
 #include <memory>
 #include <mutex>
+#include <shared_mutex>
 #include <string>
 #include <thread>
 #include <unordered_set>
@@ -49,6 +50,7 @@ struct Incumbent {
   std::unique_ptr<std::atomic<uint64_t>> local;
   void open(const char* shm_name);
   void pin();
+  void repin();
   ~Incumbent();
   double seconds() const;
   bool offer(uint64_t ns);  // true when it became the new best
@@ -160,6 +162,13 @@ class Search {
   std::atomic<int64_t> stealing_since_{-1};  // rollout count when stealing began (-1: never)
   Incumbent inc_;
   ispc_dev* dev_ = nullptr;
+  // exclusive while the launch thread replaces a device whose context a
+  // sticky fault killed; the compile threads' module loads hold it shared
+  std::shared_mutex dev_mu_;
+  int64_t respawns_ = 0;             // launch thread only
+  int64_t inject_fault_at_ = -1;     // ISPC_INJECT_FAULT_AT: batch number (tests of the respawn)
+  int64_t batches_launched_ = 0;     // launch thread only
+  bool respawn();                    // the launch thread's recovery from a sticky fault
   std::string err_;
   FILE* log_ = nullptr;
 
