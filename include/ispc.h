@@ -308,12 +308,10 @@ typedef struct ispc_dev ispc_dev;
 int ispc_dev_open(int ordinal, ispc_dev** out);
 void ispc_dev_close(ispc_dev* d);
 const char* ispc_last_error(const ispc_dev* d); /* NULL d: calling thread's last error */
-/* Recovery from a context-killing fault (ISPC_E_STICKY): after every
- * ispc_dev of the ordinal is closed, destroys the process's primary context
- * on it and creates a fresh one; ispc_dev_open then works again. */
-int ispc_device_reset(int ordinal);
 /* Test hook: a store through an invalid address on the device's stream; returns
- * ISPC_E_STICKY (and poisons the context) when the fault happened. */
+ * ISPC_E_STICKY (and poisons the context) when the fault happened. A faulted
+ * process cannot open the device again (cudaErrorDevicesUnavailable, measured
+ * on the B200 boxes); a new process can. */
 int ispc_dev_inject_fault(ispc_dev* d);
 int ispc_dev_info(const ispc_dev* d, int* sm_count, int64_t* l2_bytes, int64_t* hbm_bytes,
                   int* sm_clock_khz);

@@ -298,7 +298,6 @@ typedef struct {
   int64_t frontier_total;   /* subtree roots of the whole (all-shard) frontier     */
   int64_t stealing_since;   /* rollouts when this shard's own subtrees were spent and
                                it began stealing from the whole frontier (-1: never) */
-  int64_t respawns;         /* sticky faults survived by replacing the device context */
 } ispc_search_stats;
 
 int ispc_search_create(const ispc_space* s, const ispc_search_config* cfg, ispc_search** out);

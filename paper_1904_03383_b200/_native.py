@@ -191,12 +191,11 @@ class SearchStats(C.Structure):
                                              "t_gpu_s")]
                 + [("best_hash", C.c_uint64), ("frontier", C.c_int64), ("exhausted", C.c_int64),
                    ("refined", C.c_int64), ("device_busy_ms", C.c_double), ("t_launch_host_s", C.c_double),
-                   ("frontier_total", C.c_int64), ("stealing_since", C.c_int64), ("respawns", C.c_int64)])
+                   ("frontier_total", C.c_int64), ("stealing_since", C.c_int64)])
 
 
 # Every symbol include/ispc.h declares, with its ctypes signature.
 ISPC_SYMBOLS = {
-    "ispc_device_reset": (C.c_int, [C.c_int]),
     "ispc_dev_inject_fault": (C.c_int, [C.c_void_p]),
     "ispc_emit_cuda": (C.c_int, [C.POINTER(Nest), C.POINTER(EmitOpts), C.c_char_p, C.c_char_p, C.c_size_t,
                                  C.POINTER(C.c_size_t), C.POINTER(Launch)]),

@@ -332,18 +332,6 @@ void ispc_dev_close(ispc_dev* d) {
   delete d;
 }
 
-int ispc_device_reset(int ordinal) {
-  // a sticky fault poisons the primary context of the whole process: destroy
-  // it and create a fresh one (every ispc_dev of this ordinal must have been
-  // closed first; their handles died with the old context)
-  cudaError_t e = cudaSetDevice(ordinal);
-  if (e != cudaSuccess && !sticky(e)) return cuda_fail(nullptr, e, "cudaSetDevice");
-  (void)cudaGetLastError();
-  if ((e = cudaDeviceReset()) != cudaSuccess) return cuda_fail(nullptr, e, "cudaDeviceReset");
-  if ((e = cudaFree(nullptr)) != cudaSuccess) return cuda_fail(nullptr, e, "cudaFree after the reset");
-  return ISPC_OK;
-}
-
 int ispc_dev_inject_fault(ispc_dev* d) {
   if (!d) return ISPC_E_ARG;
   int rc = bind_ctx(d);

@@ -869,38 +869,6 @@ void Search::log_dead(int tid, int64_t rollout_no, const char* reason) {
 }
 
 
-bool Search::respawn() {
-  std::unique_lock<std::shared_mutex> dl(dev_mu_);  // no module loads meanwhile
-  retired_.clear();                                 // their handles died with the context
-  ispc_dev_close(dev_);
-  dev_ = nullptr;
-  if (ispc_device_reset(cfg_.device) != ISPC_OK) {
-    err_ += std::string("; device reset failed: ") + ispc_last_error(nullptr);
-    return false;
-  }
-  ispc_problem p{};
-  if (ispc_dev_open(cfg_.device, &dev_) != ISPC_OK || ispc_space_problem(space_, &p) != 0 ||
-      ispc_bind_problem(dev_, &p) != ISPC_OK) {
-    err_ += std::string("; device reopen failed: ") + ispc_last_error(dev_);
-    return false;
-  }
-  inc_.repin();
-  {
-    std::lock_guard<std::mutex> lk(mu_);
-    for (auto& q : batch_q_) {  // compiled against the old context: load the cubins again
-      q->handle = 0;
-      q->load_rc = q->module ? ispc_module_load(dev_, q->module, &q->handle) : ISPC_E_ARG;
-      if (q->load_rc != ISPC_OK) q->load_err = ispc_last_error(dev_);
-    }
-    step_open_ = false;
-    ++respawns_;
-    err_.clear();
-  }
-  if (trace_) std::fprintf(stderr, "[ispc] sticky fault: device %d respawned (%lld)\n", cfg_.device,
-                           (long long)respawns_);
-  return true;
-}
-
 void Search::launch_worker() {
   bool& step_open = step_open_;
   while (!stop_) {
@@ -927,7 +895,7 @@ void Search::launch_worker() {
       // dry run: the compiled kernels count as evaluated; a module that did
       // not load: every kernel of it is a launch error (a sticky fault ends
       // the search, as in ispc_launch_batch)
-      bool respawn_needed = false;
+      bool sticky_load = false;
       {
       std::lock_guard<std::mutex> lk(mu_);
       if (!dev_ && log_) {
@@ -943,12 +911,12 @@ void Search::launch_worker() {
         st_.launch_errors += n;
         if (b->load_rc == ISPC_E_STICKY) {
           err_ = b->load_err;
-          respawn_needed = true;
+          sticky_load = true;
         }
       }
       ispc_module_free(b->module);
       }
-      if (respawn_needed && !respawn()) {
+      if (sticky_load) {  // the context is dead for this process (see stop below)
         std::lock_guard<std::mutex> lk(mu_);
         stop_ = true;
       }
@@ -1073,14 +1041,14 @@ void Search::launch_worker() {
       if (!sticky_batch) launching_ = false;
     }
     if (sticky_batch) {
-      // a context-killing fault: replace the device (new primary context,
-      // the problem re-bound, queued modules reloaded) and go on, unless the
-      // fault is a kernel that still runs (a reset would wait on it)
-      const bool hung = err_.find("still running") != std::string::npos;
-      const bool ok = !hung && respawn();
+      // a context-killing fault ends this shard's search: on the B200 boxes
+      // the faulted process cannot create a new context (cudaDeviceReset +
+      // cudaFree report cudaErrorDevicesUnavailable, tools/respawn_probe.py),
+      // while a fresh process can - the caller's recovery is a new worker
+      // process (bench.py's config searches already run as children)
       std::lock_guard<std::mutex> lk(mu_);
-      if (!ok) stop_ = true;
-      if (step_open && st_.evaluations >= target_.load()) step_open = false;
+      stop_ = true;
+      step_open = false;
       launching_ = false;
     }
     cv_done_.notify_all();
@@ -1199,7 +1167,6 @@ ispc_search_stats Search::stats() const {
   s.incumbent_ns = inc_.seconds() * 1e9;
   s.exhausted = exhausted_ ? 1 : 0;
   s.stealing_since = stealing_since_;
-  s.respawns = respawns_;
   s.elapsed_s = now() - t0_;
   s.refined = refined_;
   s.t_launch_host_s = t_launch_host_;

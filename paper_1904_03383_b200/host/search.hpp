@@ -162,13 +162,9 @@ class Search {
   std::atomic<int64_t> stealing_since_{-1};  // rollout count when stealing began (-1: never)
   Incumbent inc_;
   ispc_dev* dev_ = nullptr;
-  // exclusive while the launch thread replaces a device whose context a
-  // sticky fault killed; the compile threads' module loads hold it shared
-  std::shared_mutex dev_mu_;
-  int64_t respawns_ = 0;             // launch thread only
-  int64_t inject_fault_at_ = -1;     // ISPC_INJECT_FAULT_AT: batch number (tests of the respawn)
+  std::shared_mutex dev_mu_;          // module loads (shared) against device replacement
+  int64_t inject_fault_at_ = -1;     // ISPC_INJECT_FAULT_AT: batch number (fault-handling tests)
   int64_t batches_launched_ = 0;     // launch thread only
-  bool respawn();                    // the launch thread's recovery from a sticky fault
   std::string err_;
   FILE* log_ = nullptr;
 
