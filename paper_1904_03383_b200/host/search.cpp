@@ -164,6 +164,13 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
   // spaces (whose leaves mostly share one bound)
   aspire_ = space_->tiles ? 0.0 : 1.5;
   if (const char* as = std::getenv("ISPC_ASPIRE")) aspire_ = std::max(0.0, std::atof(as));
+  // elite-guided rollouts (local search around the best measured leaves): on
+  // for the building-block spaces, whose leaves share one bound, so the tree
+  // statistics alone choose among ~10^5 of them (sgemm 1024^3: 53.3 us with
+  // q = 0.5 against 56.5 us without, same seed and budget; batched unchanged;
+  // profiles/r2h_elite.log); off for the loop-nest spaces (measured worse,
+  // section 5 of DESIGN.md)
+  elite_q_ = space_->tiles ? 0.5 : 0.0;
   if (const char* q = std::getenv("ISPC_ELITE_Q")) elite_q_ = std::clamp(std::atof(q), 0.0, 1.0);
   if (const char* mu = std::getenv("ISPC_ELITE_MUT")) elite_mut_ = std::max(0.0, std::atof(mu));
   if (const char* r = std::getenv("ISPC_ROLLOUT")) {

@@ -220,7 +220,7 @@ class Search {
   // deviating at ~mut randomly drawn decisions (local search around the
   // incumbents; the rest explore through the tree as before)
   static constexpr size_t kElite = 8;
-  double elite_q_ = 0.0, elite_mut_ = 2.0;  // off: measured worse
+  double elite_q_ = 0.0, elite_mut_ = 2.0;  // tiles 0.5, loop nests off (constructor)
   struct Elite {
     double ns;
     size_t root;
