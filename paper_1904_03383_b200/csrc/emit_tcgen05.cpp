@@ -29,6 +29,8 @@
 //   warps 4-7      converters (TF32X3 / staging SHARED only): conv[s]
 //   warps 0-7      epilogue: tcgen05.ld 32x32b.x32, coalesced column stores
 #include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <sstream>
 #include <string>
@@ -287,6 +289,29 @@ void tc_emit_convert(std::ostringstream& o, const TcStage& t, bool X3, bool A_TM
   o << ind << "asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");  // the UMMA reads through the async proxy\n";
 }
 
+// Tile rasterisation: tile t -> (m block, n tile). Groups of G m-blocks walk
+// the n tiles together, so the tiles in flight at once share A panels and B
+// panels (G = 1: m fastest over the whole column of m-blocks). ISPC_TC_GROUP
+// overrides the default (development knob).
+int tc_group(int64_t MB) {
+  int G = 8;
+  if (const char* e = std::getenv("ISPC_TC_GROUP")) G = std::max(1, std::atoi(e));
+  while (G > 1 && MB % G) G /= 2;
+  return int(std::min<int64_t>(G, MB));
+}
+
+std::string tc_tile_map(const std::string& t, const std::string& m, const std::string& nt, int64_t MB, int64_t NT,
+                        int G) {
+  std::ostringstream o;
+  if (G <= 1) {
+    o << m << " = " << t << " % " << MB << "; " << nt << " = " << t << " / " << MB << ";";
+  } else {
+    o << "{ const int g_ = " << t << " / " << G * NT << ", r_ = " << t << " % " << G * NT << "; " << m << " = g_ * " << G
+      << " + r_ % " << G << "; " << nt << " = r_ / " << G << "; }";
+  }
+  return o.str();
+}
+
 std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string& fn, ispc_launch& L);
 
 std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn, ispc_launch& L) {
@@ -343,7 +368,7 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
     o << "  const unsigned rank = 0;\n";
     o << "  const int pair = blockIdx.x;\n";
   }
-  o << "  const int m_blk = pair % " << MB << ", n_blk = pair / " << MB << ";\n";
+  o << "  int m_blk, n_blk;\n  " << tc_tile_map("pair", "m_blk", "n_blk", MB, N / BN, tc_group(MB)) << "\n";
   o << "  const int m_base = m_blk * " << UM << " + rank * 128;\n";
   o << "  unsigned char* gen = ispc_smem_raw + (base - raw);\n";
   o << "  unsigned* tmem_slot = (unsigned*)(gen + " << bar_off + nbar * 8 << ");\n";
@@ -552,15 +577,15 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   if (TS) {
     o << "    if (i >= " << RFULL << ") {\n";
     o << "      const int t = " << RFULL * NCL << " + cl / 2;\n";
-    o << "      m_blk = t % " << MB << ";\n";
-    o << "      n_off = (t / " << MB << ") * " << BN << " + (cl & 1) * " << BN / 2 << ";\n";
+    o << "      int nt;\n      " << tc_tile_map("t", "m_blk", "nt", MB, N / BN, tc_group(MB)) << "\n";
+    o << "      n_off = nt * " << BN << " + (cl & 1) * " << BN / 2 << ";\n";
     o << "      width = " << BN / 2 << ";\n";
     o << "      return;\n";
     o << "    }\n";
   }
   o << "    const int t = cl + i * ncl;\n";
-  o << "    m_blk = t % " << MB << ";\n";
-  o << "    n_off = " << (QUAD ? "((t / " + std::to_string(MB) + ") * 2 + sub)" : "(t / " + std::to_string(MB) + ")") << " * "
+  o << "    int nt;\n    " << tc_tile_map("t", "m_blk", "nt", MB, N / BN / (QUAD ? 2 : 1), tc_group(MB)) << "\n";
+  o << "    n_off = " << (QUAD ? "(nt * 2 + sub)" : "nt") << " * "
     << BN << ";\n";
   o << "    width = " << BN << ";\n";
   o << "  };\n";
