@@ -165,6 +165,68 @@ __global__ void __launch_bounds__(256) read_bulk_k(const float* __restrict__ a, 
   if (sum == 12345.678f) out[0] = sum;
 }
 
+
+// gemv "chunk" layout: CTA (rb, cb) reads rows [rb*R, rb*R+R) of columns
+// [cb*C, cb*C+C) (C segments of R*4 bytes); thread t owns rows 4t..4t+3 and
+// keeps one float4 per column in flight. Clusters of CL CTAs along columns
+// sum their partials through DSMEM; each cluster's partial goes to a
+// workspace; the last cluster of a row block (atomic counter) sums the
+// workspace column and writes y, then resets the counter.
+template <int R, int C, int CL>
+__global__ void __launch_bounds__(R / 4) gemv_chunk_k(const float* __restrict__ A, const float* __restrict__ x,
+                                                    float* __restrict__ y, float* __restrict__ ws,
+                                                    unsigned* __restrict__ counters) {
+  constexpr int T = R / 4, NCB = N / C, NCL = NCB / CL;  // column blocks, clusters per row block
+  __shared__ __align__(16) float4 part[T];
+  __shared__ bool last;
+  const int rb = blockIdx.x / NCB, cb = blockIdx.x % NCB;
+  const int t = threadIdx.x;
+  const float4* col = (const float4*)(A + (long long)cb * C * M + rb * R) + t;
+  float4 v[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) v[c] = ld_stream(col + (long long)c * (M / 4));
+  float4 acc = make_float4(0, 0, 0, 0);
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const float xc = __ldg(x + cb * C + c);
+    acc.x = fmaf(v[c].x, xc, acc.x); acc.y = fmaf(v[c].y, xc, acc.y);
+    acc.z = fmaf(v[c].z, xc, acc.z); acc.w = fmaf(v[c].w, xc, acc.w);
+  }
+  part[t] = acc;
+  unsigned rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (rank == 0) {
+    float4 s = acc;
+    const unsigned a = (unsigned)__cvta_generic_to_shared(&part[t]);
+#pragma unroll
+    for (unsigned q = 1; q < CL; ++q) {
+      unsigned r;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(q));
+      float4 o;
+      asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(o.x), "=f"(o.y), "=f"(o.z), "=f"(o.w) : "r"(r));
+      s.x += o.x; s.y += o.y; s.z += o.z; s.w += o.w;
+    }
+    const int cl = cb / CL;
+    ((float4*)(ws + ((long long)rb * NCL + cl) * R))[t] = s;
+    __threadfence();
+    __syncthreads();
+    if (t == 0) last = atomicAdd(counters + rb, 1u) == NCL - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      float4 tot = make_float4(0, 0, 0, 0);
+      for (int q = 0; q < NCL; ++q) {
+        const float4 o = __ldcg((const float4*)(ws + ((long long)rb * NCL + q) * R) + t);
+        tot.x += o.x; tot.y += o.y; tot.z += o.z; tot.w += o.w;
+      }
+      ((float4*)(y + rb * R))[t] = tot;
+      if (t == 0) counters[rb] = 0;
+    }
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __global__ void zero_k(float* y, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = 0;
@@ -282,6 +344,42 @@ int main() {
     std::printf("gemv cols T%-4d U%-2d grid %4d (+zero kernel): %7.2f us  %7.1f GB/s\n", T, U, G, us, \
                 bytes_gemv / us / 1e3);                                                                \
   }
+#define CHUNKG(R, C, CL)                                                                                  \
+  {                                                                                                        \
+    float* ws;                                                                                             \
+    unsigned* cnt;                                                                                         \
+    CK(cudaMalloc(&ws, sizeof(float) * M * (N / C / CL)));                                                 \
+    CK(cudaMalloc(&cnt, 4096));                                                                            \
+    CK(cudaMemset(cnt, 0, 4096));                                                                          \
+    cudaLaunchConfig_t cfg = {};                                                                           \
+    cfg.gridDim = dim3((M / R) * (N / C));                                                                 \
+    cfg.blockDim = dim3(R / 4);                                                                            \
+    cfg.stream = st;                                                                                       \
+    cudaLaunchAttribute at[1];                                                                             \
+    at[0].id = cudaLaunchAttributeClusterDimension;                                                        \
+    at[0].val.clusterDim.x = CL, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;                  \
+    cfg.attrs = at, cfg.numAttrs = 1;                                                                      \
+    auto k = gemv_chunk_k<R, C, CL>;                                                                       \
+    float us = timeit([&](int c) { CK(cudaLaunchKernelEx(&cfg, k, (const float*)A[c], (const float*)X[c], Y[c], ws, cnt)); }, st); \
+    std::vector<float> hy(M), hx(N);                                                                       \
+    CK(cudaMemcpy(hy.data(), Y[0], M * 4, cudaMemcpyDeviceToHost));                                        \
+    double maxerr = 0;                                                                                     \
+    for (int i = 0; i < M; i += 97) {                                                                      \
+      double s = 0, sa = 0;                                                                                \
+      for (int j = 0; j < N; ++j) { s += double(h[i + (long long)j * M]) * h[j]; sa += std::fabs(double(h[i + (long long)j * M]) * h[j]); } \
+      maxerr = std::max(maxerr, std::fabs(s - hy[i]) / sa);                                                \
+    }                                                                                                      \
+    std::printf("gemv chunk R%-4d C%-3d CL%d grid %5d: %7.2f us  %7.1f GB/s  maxerr %.2e\n", R, C, CL, (M / R) * (N / C), us, bytes_gemv / us / 1e3, maxerr); \
+    cudaFree(ws); cudaFree(cnt);                                                                           \
+  }
+  CHUNKG(1024, 8, 8);
+  CHUNKG(1024, 4, 8);
+  CHUNKG(1024, 16, 8);
+  CHUNKG(512, 8, 8);
+  CHUNKG(512, 16, 8);
+  CHUNKG(2048, 8, 8);
+  CHUNKG(1024, 8, 4);
+  CHUNKG(512, 4, 8);
   COLS(1024, 2, 256);
   COLS(1024, 4, 256);
   COLS(512, 2, 256);
