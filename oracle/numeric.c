@@ -10,7 +10,8 @@
  * there are no numeric golden vectors upstream; these functions are pinned
  * instead by tests/golden/*.json, outputs of an interpreter that executes the
  * reference's own Kernel objects instance by instance through the reference's
- * eval_addr/dim_extent (oracle/ref_interp.cpp, generator committed beside it).
+ * eval_addr/dim_extent (oracle/ref_golden.cpp, built from /root/reference by
+ * oracle/Makefile; tests/test_oracle_golden.py checks these functions against it).
  *
  *   axpy    kernels.cpp:373-408  z[i] = add(mul(alpha, x[i]), y[i]) — two
  *           separately rounded fp32 operations
