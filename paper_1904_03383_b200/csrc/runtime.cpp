@@ -72,6 +72,7 @@ struct DriverTable {
   decltype(&::cuModuleGetFunctionCount) ModuleGetFunctionCount = nullptr;
   decltype(&::cuModuleEnumerateFunctions) ModuleEnumerateFunctions = nullptr;
   decltype(&::cuFuncLoad) FuncLoad = nullptr;
+  decltype(&::cuFuncGetAttribute) FuncGetAttribute = nullptr;
 };
 DriverTable drv;
 
@@ -110,6 +111,7 @@ bool resolve_driver(std::string& why) {
     opt("cuModuleGetFunctionCount", reinterpret_cast<void**>(&drv.ModuleGetFunctionCount));
     opt("cuModuleEnumerateFunctions", reinterpret_cast<void**>(&drv.ModuleEnumerateFunctions));
     opt("cuFuncLoad", reinterpret_cast<void**>(&drv.FuncLoad));
+    opt("cuFuncGetAttribute", reinterpret_cast<void**>(&drv.FuncGetAttribute));
   });
   if (!ok) why = "CUDA driver entry points unavailable: " + err;
   return ok;
@@ -646,6 +648,19 @@ int bind_kernel(ispc_dev* d, Loaded& mod, const ispc_launch* L, uint32_t rotate,
   int rc = get_function(d, mod, L, &B.fn);
   if (rc) return rc;
   if (L->grid_x == 0 || L->grid_x > 0x7fffffffull) return fail(d, ISPC_E_ILLEGAL, "grid out of range");
+  // the block the candidate asks for must fit the registers ptxas gave the
+  // kernel (a static property of the compiled candidate, not a launch error)
+  if (drv.FuncGetAttribute) {
+    int max_threads = 0, regs = 0;
+    if (drv.FuncGetAttribute(&max_threads, CU_FUNC_ATTRIBUTE_MAX_THREADS_PER_BLOCK, B.fn) == CUDA_SUCCESS &&
+        drv.FuncGetAttribute(&regs, CU_FUNC_ATTRIBUTE_NUM_REGS, B.fn) == CUDA_SUCCESS) {
+      const uint64_t threads = uint64_t(L->block[0]) * std::max(1u, L->block[1]) * std::max(1u, L->block[2]);
+      if (max_threads > 0 && threads > uint64_t(max_threads))
+        return fail(d, ISPC_E_ILLEGAL, "block of " + std::to_string(threads) + " threads exceeds the " +
+                                           std::to_string(max_threads) + " that " + std::to_string(regs) +
+                                           " registers per thread allow");
+    }
+  }
   B.L = L;
   B.R = std::max<uint32_t>(1, std::min<uint32_t>(rotate, 16));
   if ((rc = ensure_rotation(d, B.R))) return rc;
@@ -898,7 +913,13 @@ int ispc_launch_batch(ispc_dev* d, int handle, int n, const ispc_batch_item* ite
     first_ev[size_t(i)] = ev;
     ev += 2;
     CK(d, cudaEventRecord(e0, d->stream));
-    if ((rc = enqueue(d, B[size_t(i)], 0, dl))) return rc;
+    if ((rc = enqueue(d, B[size_t(i)], 0, dl))) {
+      if (rc == ISPC_E_STICKY) return rc;
+      res[i].status = rc;  // this kernel alone cannot launch; the batch goes on
+      first_ev[size_t(i)] = SIZE_MAX;
+      ev -= 2;
+      continue;
+    }
     CK(d, cudaEventRecord(e1, d->stream));
     guard_ns += std::max(5e9, 40.0 * budget);
     ispc::CmpResult* slot = slots + i;

@@ -1000,6 +1000,10 @@ void Search::launch_worker() {
         const double t_now = now() - t0_;
         std::string status;
         bool improved = false;
+        if (rc == ISPC_E_ILLEGAL) {  // the compiled kernel cannot run its block (registers): never launched
+          ++illegal_;
+          continue;
+        }
         ++st_.evaluations;
         if (rc != ISPC_OK) {
           ++st_.launch_errors;
