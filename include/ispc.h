@@ -214,6 +214,11 @@ typedef struct {
   uint32_t block[3];     /* blockDim.{x,y,z}; innermost level is x         */
   uint32_t static_smem;  /* bytes of SHARED tmp regions                    */
   uint32_t num_params;
+  uint32_t pdl;          /* 1: launch with programmatic stream serialization
+                            (the kernel's first statement is griddepcontrol.wait,
+                            so it touches memory only after the previous grid of
+                            the stream completed; its CTAs may be scheduled
+                            while that grid drains)                        */
   ispc_param params[ISPC_MAX_PARAMS];
   uint32_t watchdog;     /* 1 when the kernel polls the deadline parameter */
   uint32_t reg_elems;    /* register-array elements per thread (static)    */
@@ -283,7 +288,7 @@ typedef struct {
   int32_t threads;               /* axpy stream: threads per CTA                    */
   int32_t grid;                  /* axpy stream: CTAs (0: one vector group per thread);
                                     tcgen05 / gemv: persistent CTAs (0: one tile each) */
-  int32_t _pad2;
+  int32_t pdl;                   /* 1: programmatic dependent launch (ispc_launch.pdl) */
 } ispc_tile_config;
 
 /* Emits the kernel of a tile configuration (same conventions as

@@ -107,7 +107,7 @@ class TMap(C.Structure):
 
 class Launch(C.Structure):
     _fields_ = [("name", C.c_char * 64), ("grid_x", C.c_uint64), ("block", C.c_uint32 * 3),
-                ("static_smem", C.c_uint32), ("num_params", C.c_uint32), ("params", Param * 32),
+                ("static_smem", C.c_uint32), ("num_params", C.c_uint32), ("pdl", C.c_uint32), ("params", Param * 32),
                 ("watchdog", C.c_uint32), ("reg_elems", C.c_uint32), ("source_hash", C.c_uint64),
                 ("cluster", C.c_uint32 * 3), ("num_tmaps", C.c_uint32), ("tmaps", TMap * 4)]
 
@@ -117,7 +117,7 @@ class TileConfig(C.Structure):
                 + [(f, C.c_int64) for f in ("m", "n", "k", "batch")]
                 + [(f, C.c_int32) for f in ("thr_m", "thr_n", "tm", "tn", "bk", "bn", "stages", "vec", "lanes_m",
                                             "lanes_n", "warps_m", "warps_n", "split", "unroll", "per_cta",
-                                            "threads", "grid", "_pad2")])
+                                            "threads", "grid", "pdl")])
 
     def as_dict(self) -> dict:
         d = {f: getattr(self, f) for f, _ in self._fields_ if not f.startswith("_")}

@@ -825,18 +825,24 @@ static __device__ __forceinline__ unsigned ispc_smem_addr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
 static __device__ __forceinline__ void ispc_cp_async_cg16(void* s, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(ispc_smem_addr(s)), "l"(g) : "memory");
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(ispc_smem_addr(s)), "l"(g));
 }
 static __device__ __forceinline__ void ispc_cp_async_ca16(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(ispc_smem_addr(s)), "l"(g) : "memory");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(ispc_smem_addr(s)), "l"(g));
 }
 static __device__ __forceinline__ void ispc_cp_async_ca8(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(ispc_smem_addr(s)), "l"(g) : "memory");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(ispc_smem_addr(s)), "l"(g));
 }
 static __device__ __forceinline__ void ispc_cp_async_ca4(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(ispc_smem_addr(s)), "l"(g) : "memory");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(ispc_smem_addr(s)), "l"(g));
 }
-static __device__ __forceinline__ void ispc_cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+// issue and commit carry no memory clobber (shared-memory loads of other ring
+// slots may be scheduled across them: the FFMA2 sgemm interleaves its fragment
+// loads with the copies); wait_group is the compiler barrier before a slot is read
+static __device__ __forceinline__ void ispc_cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+// programmatic dependent launch (ispc_launch.pdl): wait for the previous grid of the stream, then let the next one be scheduled
+static __device__ __forceinline__ void ispc_grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+static __device__ __forceinline__ void ispc_grid_dep_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 template <int N>
 static __device__ __forceinline__ void ispc_cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");

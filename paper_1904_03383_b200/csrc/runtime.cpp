@@ -743,7 +743,7 @@ int enqueue(ispc_dev* d, Bound& B, uint32_t copy, uint64_t deadline) {
     args[i] = B.tmap_of[i] >= 0 ? static_cast<void*>(&B.tmaps[copy][size_t(B.tmap_of[i])])
                                 : static_cast<void*>(&B.stores[copy][i]);
   }
-  if (B.clustered) {
+  if (B.clustered || L->pdl) {
     CUlaunchConfig cfg{};
     cfg.gridDimX = unsigned(L->grid_x);
     cfg.gridDimY = cfg.gridDimZ = 1;
@@ -752,13 +752,22 @@ int enqueue(ispc_dev* d, Bound& B, uint32_t copy, uint64_t deadline) {
     cfg.blockDimZ = L->block[2];
     cfg.sharedMemBytes = L->static_smem;
     cfg.hStream = reinterpret_cast<CUstream>(d->stream);
-    CUlaunchAttribute attr{};
-    attr.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
-    attr.value.clusterDim.x = L->cluster[0];
-    attr.value.clusterDim.y = std::max(1u, L->cluster[1]);
-    attr.value.clusterDim.z = std::max(1u, L->cluster[2]);
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
+    CUlaunchAttribute attr[2]{};
+    unsigned na = 0;
+    if (B.clustered) {
+      attr[na].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+      attr[na].value.clusterDim.x = L->cluster[0];
+      attr[na].value.clusterDim.y = std::max(1u, L->cluster[1]);
+      attr[na].value.clusterDim.z = std::max(1u, L->cluster[2]);
+      ++na;
+    }
+    if (L->pdl) {  // the kernel opens with griddepcontrol.wait (ispc.h: ispc_launch.pdl)
+      attr[na].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+      attr[na].value.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
     CU(d, drv.LaunchKernelEx(&cfg, B.fn, args, nullptr));
   } else {
     CU(d, drv.LaunchKernel(B.fn, unsigned(L->grid_x), 1, 1, L->block[0], L->block[1], L->block[2], L->static_smem,

@@ -108,6 +108,8 @@ inline void ispc_cp_async_ca16(void* s, const void* g) { std::memcpy(s, g, 16); 
 inline void ispc_cp_async_ca8(void* s, const void* g) { std::memcpy(s, g, 8); }
 inline void ispc_cp_async_ca4(void* s, const void* g) { std::memcpy(s, g, 4); }
 inline void ispc_cp_async_commit() {}
+inline void ispc_grid_dep_wait() {}
+inline void ispc_grid_dep_trigger() {}
 template <int N>
 inline void ispc_cp_async_wait() {}
 inline unsigned ispc_cluster_rank() { return 0; }  // clusters of one CTA only

@@ -4,9 +4,11 @@
 // (bit-exact against a sequential fmaf reference kernel).
 //   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/sgemm_lab tools/sgemm_lab.cu -lcublas
 #include <cublas_v2.h>
+#include "_kx_emitted.cuh"  // an emitted kernel (scratch, not committed)
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -219,6 +221,9 @@ __device__ unsigned long long* g_trace = nullptr;
 // cp.async), per-k register fragments double buffered, FFMA2 with the B value
 // broadcast. Warps WX x WY, lanes LX x LY, 8 x 8 outputs per lane as 2 x 2
 // blocks of 4 x 4: row = wm*LX*8 + (i/4)*LX*4 + lx*4 + i%4, same for columns.
+// SPLIT > 1: each k slice stores its own partial C with no reduction (a per-SM
+// throughput probe, not a complete kernel: its "MISMATCH" is expected).
+// F2: 0 FFMA, 1 FFMA2 j-outer, 2 FFMA2 i-outer, 3 FFMA2 i-outer with serpentine j.
 template <int WX, int WY, int LX, int LY, int BK, int S, int PADB, int TM, int TN, int F2, int MINB, int SPLIT = 1>
 __global__ void __launch_bounds__(WX* WY * 32, MINB) sgemm_v3(const float* __restrict__ A, const float* __restrict__ B,
                                                       float* __restrict__ C, int M, int N, int K) {
@@ -230,6 +235,7 @@ __global__ void __launch_bounds__(WX* WY * 32, MINB) sgemm_v3(const float* __res
   extern __shared__ __align__(16) float sm[];
   unsigned long long t_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp % WX, wn = warp / WX, lx = lane % LX, ly = lane / LX;
   const int tiles_m = M / BM;
@@ -300,11 +306,30 @@ __global__ void __launch_bounds__(WX* WY * 32, MINB) sgemm_v3(const float* __res
         if (nk < KT) load(nk, nk % S);
         commit();
       }
-      if constexpr (F2) {
+      if constexpr (F2 == 1) {
 #pragma unroll
         for (int j = 0; j < TN; ++j)
 #pragma unroll
           for (int i = 0; i < TM; i += 2) {
+            float2 c = make_float2(acc[j][i], acc[j][i + 1]);
+            c = __ffma2_rn(make_float2(fa[k & 1][i], fa[k & 1][i + 1]), make_float2(fb[k & 1][j], fb[k & 1][j]), c);
+            acc[j][i] = c.x, acc[j][i + 1] = c.y;
+          }
+      } else if constexpr (F2 == 2) {  // A pair held, B walks: Ra reused
+#pragma unroll
+        for (int i = 0; i < TM; i += 2)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) {
+            float2 c = make_float2(acc[j][i], acc[j][i + 1]);
+            c = __ffma2_rn(make_float2(fa[k & 1][i], fa[k & 1][i + 1]), make_float2(fb[k & 1][j], fb[k & 1][j]), c);
+            acc[j][i] = c.x, acc[j][i + 1] = c.y;
+          }
+      } else if constexpr (F2 == 3) {  // serpentine j order (B reused across the i-pair switch too)
+#pragma unroll
+        for (int i = 0; i < TM; i += 2)
+#pragma unroll
+          for (int jj = 0; jj < TN; ++jj) {
+            const int j = ((i / 2) & 1) ? TN - 1 - jj : jj;
             float2 c = make_float2(acc[j][i], acc[j][i + 1]);
             c = __ffma2_rn(make_float2(fa[k & 1][i], fa[k & 1][i + 1]), make_float2(fb[k & 1][j], fb[k & 1][j]), c);
             acc[j][i] = c.x, acc[j][i + 1] = c.y;
@@ -317,6 +342,7 @@ __global__ void __launch_bounds__(WX* WY * 32, MINB) sgemm_v3(const float* __res
       }
     }
   }
+  asm volatile("griddepcontrol.launch_dependents;");
   wait_group<0>();
 #pragma unroll
   for (int j = 0; j < TN; ++j) {
@@ -402,9 +428,695 @@ void run3(Bufs& bf, const float* ref, int M, int N, int K, int R, cudaStream_t s
                 (t1 - t0) / 1e3, dmin / 1e3, dsum / grid / 1e3, dmax / 1e3, smax / 1e3, used, shared);
     cudaFree(tr);
   }
+  float pdl_us = 0;
+  {
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid), cfg.blockDim = dim3(T), cfg.dynamicSmemBytes = smem, cfg.stream = st;
+    cfg.attrs = at, cfg.numAttrs = 1;
+    std::vector<float> tp;
+    for (int trial = 0; trial < 7; ++trial) {
+      cudaEventRecord(e0, st);
+      for (int r2 = 0; r2 < R; ++r2) {
+        const int x = r2 % int(bf.a.size());
+        CK(cudaLaunchKernelEx(&cfg, kern, (const float*)bf.a[x], (const float*)bf.b[x], bf.c[x], M, N, K));
+      }
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      tp.push_back(ms * 1e3f / R);
+    }
+    std::sort(tp.begin(), tp.end());
+    pdl_us = tp[3];
+    CK(cudaLaunchKernelEx(&cfg, kern, (const float*)bf.a[0], (const float*)bf.b[0], bf.c[0], M, N, K));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(h.data(), bf.c[0], h.size() * 4, cudaMemcpyDeviceToHost));
+    if (std::memcmp(h.data(), r.data(), h.size() * 4) != 0 && exact) std::printf("   PDL result differs!\n");
+  }
+  std::printf("   PDL back-to-back: %.2f us\n", pdl_us);
   std::sort(ts.begin(), ts.end());
   std::printf("v3 SPLIT=%d F2=%d MINB=%d T%dx%d W%dx%d L%dx%d tile %dx%d BK%-2d S%d PADB%d grid %5d thr %4d regs %3d occ %d spill %zu  %8.2f us  %6.1f TF/s  %s\n",
               SPLIT, F2, MINB, TM, TN, WX, WY, LX, LY, BM, BN, BK, S, PADB, grid, T, fa.numRegs, occ, (size_t)fa.localSizeBytes, ts[3],
+              2.0 * M * N * double(K) / (ts[3] * 1e-6) / 1e12, exact ? "bit-exact" : "MISMATCH");
+}
+
+
+// Chained stream-K (bit-exact): G persistent CTAs split the tiles x k-blocks
+// unit range evenly (each range >= one tile's KT units, so a tile spans at
+// most two CTAs). CTA c first computes the head (k from 0) of its last tile
+// and publishes the partial accumulators (workspace + flag), then its whole
+// tiles, then the tail of its first tile: it waits for CTA c-1's published
+// head and continues the same fmaf chains in ascending k. One continuous
+// cp.async ring walks the CTA's unit sequence across segment boundaries.
+__device__ float* g_ws = nullptr;
+__device__ unsigned long long* g_wait = nullptr;
+__device__ unsigned* g_flags = nullptr;
+template <int WX, int WY, int LX, int LY, int BK, int S, int PADB, int TM, int TN, int MINB>
+__global__ void __launch_bounds__(WX* WY * 32, MINB) sgemm_sk(const float* __restrict__ A, const float* __restrict__ B,
+                                                      float* __restrict__ C, int M, int N, int K, int G) {
+  constexpr int T = WX * WY * 32;
+  constexpr int BM = WX * LX * TM, BN = WY * LY * TN, LDB = BN + PADB;
+  constexpr int A_T = BK * BM, B_T = BK * LDB, ST = A_T + B_T;
+  extern __shared__ __align__(16) float sm[];
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WX, wn = warp / WX, lx = lane % LX, ly = lane / LX;
+  const int tiles_m = M / BM, KT = K / BK;
+  const long long U = (long long)tiles_m * (N / BN) * KT;
+  const long long u0 = U * blockIdx.x / G, u1 = U * (blockIdx.x + 1) / G;
+  // segments in processing order (tile, k begin, k length): the head of the
+  // last tile, the whole tiles, the tail of the first tile (<= 4 segments)
+  const int t_first = int(u0 / KT), k_first = int(u0 % KT);
+  const int t_last = int((u1 - 1) / KT), k_end = int((u1 - 1) % KT) + 1;
+  int sg_t[4] = {0, 0, 0, 0}, sg_b[4] = {0, 0, 0, 0}, sg_n[4] = {0, 0, 0, 0}, ns = 0;
+  if (k_end < KT && t_last != t_first) sg_t[ns] = t_last, sg_b[ns] = 0, sg_n[ns] = k_end, ++ns;
+  const int full_lo = t_first + (k_first > 0), full_hi = k_end < KT ? t_last - 1 : t_last;
+#pragma unroll
+  for (int f = 0; f < 2; ++f)
+    if (full_lo + f <= full_hi) sg_t[ns] = full_lo + f, sg_b[ns] = 0, sg_n[ns] = KT, ++ns;
+  if (k_first > 0) sg_t[ns] = t_first, sg_b[ns] = k_first, sg_n[ns] = (t_first == t_last ? k_end : KT) - k_first, ++ns;
+  int nq = 0;
+#pragma unroll
+  for (int x = 0; x < 4; ++x) nq += sg_n[x];
+  auto pick = [&](const int* v, int i) { return i == 0 ? v[0] : i == 1 ? v[1] : i == 2 ? v[2] : v[3]; };
+  // loader state: segment, k block, operand pointers of that k block
+  int l_s = 0, l_left = sg_n[0];
+  const float* l_pa;
+  const float* l_pb;
+  auto l_point = [&]() {
+    const int t = pick(sg_t, l_s), kb = pick(sg_b, l_s);
+    const int bm = t % tiles_m, bn = t / tiles_m;
+    l_pa = A + (long long)bm * BM + (long long)kb * BK * M;
+    l_pb = B + (long long)bn * BN * K + kb * BK;
+  };
+  l_point();
+  auto load = [&](int slot) {
+    if (l_left == 0) {
+      ++l_s;
+      l_left = pick(sg_n, l_s);
+      l_point();
+    }
+    float* sA = sm + slot * ST;
+    float* sB = sA + A_T;
+#pragma unroll
+    for (int ch = tid; ch < BK * BM / 4; ch += T) {
+      const int kk = ch / (BM / 4), mm = (ch % (BM / 4)) * 4;
+      cp16(sA + kk * BM + mm, l_pa + mm + kk * M);
+    }
+#pragma unroll
+    for (int e = tid; e < BK * BN; e += T) {
+      const int kk = e % BK, nn = e / BK;
+      cp4(sB + kk * LDB + nn, l_pb + kk + (long long)nn * K);
+    }
+    l_pa += (long long)BK * M;
+    l_pb += BK;
+    --l_left;
+  };
+  float acc[TN][TM];
+  const int arow = wm * LX * TM + lx * 4, bcol = wn * LY * TN + ly * 4;
+  float fa[2][TM], fb[2][TN];
+  auto frag = [&](int buf, const float* sA, const float* sB, int k) {
+#pragma unroll
+    for (int h = 0; h < TM / 4; ++h) {
+      const float4 a0 = *(const float4*)(sA + k * BM + arow + h * LX * 4);
+      fa[buf][4 * h] = a0.x, fa[buf][4 * h + 1] = a0.y, fa[buf][4 * h + 2] = a0.z, fa[buf][4 * h + 3] = a0.w;
+    }
+#pragma unroll
+    for (int h = 0; h < TN / 4; ++h) {
+      const float4 b0 = *(const float4*)(sB + k * LDB + bcol + h * LY * 4);
+      fb[buf][4 * h] = b0.x, fb[buf][4 * h + 1] = b0.y, fb[buf][4 * h + 2] = b0.z, fb[buf][4 * h + 3] = b0.w;
+    }
+  };
+  constexpr int NV = TM * TN / 4;
+  auto begin_seg = [&](int t, int kb) {
+    if (kb == 0) {
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int i = 0; i < TM; ++i) acc[j][i] = 0.f;
+    } else {  // continue CTA c-1's published head
+      if (tid == 0) {
+        unsigned v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(g_flags + t));
+        } while (v == 0);
+      }
+      __syncthreads();
+      const float4* w = (const float4*)(g_ws + (long long)t * BM * BN);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const float4 x = __ldcg(w + v * T + tid);
+        const int j = (v * 4) / TM, i = (v * 4) % TM;
+        acc[j][i] = x.x, acc[j][i + 1] = x.y, acc[j][i + 2] = x.z, acc[j][i + 3] = x.w;
+      }
+      __syncthreads();
+      if (tid == 0) g_flags[t] = 0;  // consumed: ready for the next launch
+    }
+  };
+  auto end_seg = [&](int t, int ke) {
+    if (ke < KT) {  // publish the head
+      float4* w = (float4*)(g_ws + (long long)t * BM * BN);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int j = (v * 4) / TM, i = (v * 4) % TM;
+        __stcg(w + v * T + tid, make_float4(acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]));
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g_flags + t), "r"(1u));
+    } else {
+      const int bm = t % tiles_m, bn = t / tiles_m;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const long long col = (long long)bn * BN + bcol + (j / 4) * LY * 4 + j % 4;
+#pragma unroll
+        for (int i = 0; i < TM; i += 4) {
+          const long long row = (long long)bm * BM + arow + (i / 4) * LX * 4;
+          *(float4*)(C + row + col * M) = make_float4(acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]);
+        }
+      }
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < nq) load(s);
+    commit();
+  }
+  wait_group<S - 2>();
+  __syncthreads();
+  frag(0, sm, sm + A_T, 0);
+  int c_s = 0, c_left = sg_n[0];
+  begin_seg(sg_t[0], sg_b[0]);
+#pragma unroll 1
+  for (int q = 0; q < nq; ++q) {
+    const float* sA = sm + (q % S) * ST;
+    const float* sB = sA + A_T;
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      if (k == BK - 1) {
+        wait_group<S - 2>();
+        __syncthreads();
+        const float* nA = sm + ((q + 1) % S) * ST;
+        frag((k + 1) & 1, nA, nA + A_T, 0);
+      } else {
+        frag((k + 1) & 1, sA, sB, k + 1);
+      }
+      if (k == 0) {
+        if (q + S - 1 < nq) load((q + S - 1) % S);
+        commit();
+      }
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int i = 0; i < TM; i += 2) {
+          float2 c = make_float2(acc[j][i], acc[j][i + 1]);
+          c = __ffma2_rn(make_float2(fa[k & 1][i], fa[k & 1][i + 1]), make_float2(fb[k & 1][j], fb[k & 1][j]), c);
+          acc[j][i] = c.x, acc[j][i + 1] = c.y;
+        }
+    }
+    if (--c_left == 0) {
+      const int t = pick(sg_t, c_s);
+      end_seg(t, pick(sg_b, c_s) + pick(sg_n, c_s));
+      if (++c_s < ns) {
+        c_left = pick(sg_n, c_s);
+        begin_seg(pick(sg_t, c_s), pick(sg_b, c_s));
+      }
+    }
+  }
+  wait_group<0>();
+  if (g_trace && tid == 0) {
+    unsigned long long t_end;
+    unsigned smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_trace[3 * blockIdx.x] = t_start;
+    g_trace[3 * blockIdx.x + 1] = t_end;
+    g_trace[3 * blockIdx.x + 2] = smid;
+  }
+}
+
+// Stream-K with additive fixup (1e-5 tolerance, not bit-exact when a tile is
+// shared): G CTAs walk the tiles x k-blocks units [u0, u1) in ascending order
+// through one continuous cp.async ring. A segment that starts inside a tile
+// (k > 0) is published to the CTA's workspace slot; the CTA holding a tile's
+// k = 0 segment finishes it: waits for the other holders' flags and adds
+// their partials in CTA order. Whole tiles are stored directly (bit-exact).
+template <int WX, int WY, int LX, int LY, int BK, int S, int PADB, int TM, int TN, int MINB>
+__global__ void __launch_bounds__(WX* WY * 32, MINB) sgemm_sk2(const float* __restrict__ A, const float* __restrict__ B,
+                                                       float* __restrict__ C, int M, int N, int K, int G) {
+  constexpr int T = WX * WY * 32;
+  constexpr int BM = WX * LX * TM, BN = WY * LY * TN, LDB = BN + PADB;
+  constexpr int A_T = BK * BM, B_T = BK * LDB, ST = A_T + B_T;
+  extern __shared__ __align__(16) float sm[];
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WX, wn = warp / WX, lx = lane % LX, ly = lane / LX;
+  const int tiles_m = M / BM, KT = K / BK;
+  const long long U = (long long)tiles_m * (N / BN) * KT;
+  const int u0 = int(U * blockIdx.x / G), u1 = int(U * (blockIdx.x + 1) / G);
+  const int nq = u1 - u0;
+  // loader: unit (l_t, l_k) and its operand pointers
+  int l_t = u0 / KT, l_k = u0 % KT;
+  const float* l_pa = A + (long long)(l_t % tiles_m) * BM + (long long)l_k * BK * M;
+  const float* l_pb = B + (long long)(l_t / tiles_m) * BN * K + l_k * BK;
+  auto load = [&](int slot) {
+    float* sA = sm + slot * ST;
+    float* sB = sA + A_T;
+#pragma unroll
+    for (int ch = tid; ch < BK * BM / 4; ch += T) {
+      const int kk = ch / (BM / 4), mm = (ch % (BM / 4)) * 4;
+      cp16(sA + kk * BM + mm, l_pa + mm + kk * M);
+    }
+#pragma unroll
+    for (int e = tid; e < BK * BN; e += T) {
+      const int kk = e % BK, nn = e / BK;
+      cp4(sB + kk * LDB + nn, l_pb + kk + (long long)nn * K);
+    }
+    if (++l_k == KT) {
+      l_k = 0, ++l_t;
+      l_pa = A + (long long)(l_t % tiles_m) * BM;
+      l_pb = B + (long long)(l_t / tiles_m) * BN * K;
+    } else {
+      l_pa += (long long)BK * M;
+      l_pb += BK;
+    }
+  };
+  float acc[TN][TM];
+  const int arow = wm * LX * TM + lx * 4, bcol = wn * LY * TN + ly * 4;
+  float fa[2][TM], fb[2][TN];
+  auto frag = [&](int buf, const float* sA, const float* sB, int k) {
+#pragma unroll
+    for (int h = 0; h < TM / 4; ++h) {
+      const float4 a0 = *(const float4*)(sA + k * BM + arow + h * LX * 4);
+      fa[buf][4 * h] = a0.x, fa[buf][4 * h + 1] = a0.y, fa[buf][4 * h + 2] = a0.z, fa[buf][4 * h + 3] = a0.w;
+    }
+#pragma unroll
+    for (int h = 0; h < TN / 4; ++h) {
+      const float4 b0 = *(const float4*)(sB + k * LDB + bcol + h * LY * 4);
+      fb[buf][4 * h] = b0.x, fb[buf][4 * h + 1] = b0.y, fb[buf][4 * h + 2] = b0.z, fb[buf][4 * h + 3] = b0.w;
+    }
+  };
+  constexpr int NV = TM * TN / 4;
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < nq) load(s);
+    commit();
+  }
+  wait_group<S - 2>();
+  __syncthreads();
+  frag(0, sm, sm + A_T, 0);
+  int c_t = u0 / KT, c_k = u0 % KT;
+  int q = 0;
+#pragma unroll 1
+  while (q < nq) {
+    const int c_kb = c_k;
+    const int len = min(KT - c_k, nq - q);
+#pragma unroll
+    for (int j = 0; j < TN; ++j)
+#pragma unroll
+      for (int i = 0; i < TM; ++i) acc[j][i] = 0.f;
+#pragma unroll 1
+    for (int e = 0; e < len; ++e, ++q) {
+      const float* sA = sm + (q % S) * ST;
+      const float* sB = sA + A_T;
+#pragma unroll
+      for (int k = 0; k < BK; ++k) {
+        if (k == BK - 1) {
+          wait_group<S - 2>();
+          __syncthreads();
+          const float* nA = sm + ((q + 1) % S) * ST;
+          frag((k + 1) & 1, nA, nA + A_T, 0);
+        } else {
+          frag((k + 1) & 1, sA, sB, k + 1);
+        }
+        if (k == 0) {
+          if (q + S - 1 < nq) load((q + S - 1) % S);
+          commit();
+        }
+#pragma unroll
+        for (int i = 0; i < TM; i += 2)
+#pragma unroll
+          for (int jj = 0; jj < TN; ++jj) {
+            const int j = ((i / 2) & 1) ? TN - 1 - jj : jj;
+            float2 c = make_float2(acc[j][i], acc[j][i + 1]);
+            c = __ffma2_rn(make_float2(fa[k & 1][i], fa[k & 1][i + 1]), make_float2(fb[k & 1][j], fb[k & 1][j]), c);
+            acc[j][i] = c.x, acc[j][i + 1] = c.y;
+          }
+      }
+    }
+    c_k += len;
+    {  // segment [c_kb, c_k) of tile c_t ends
+      if (c_kb > 0) {  // publish to this CTA's slot
+        float4* w = (float4*)(g_ws + (long long)blockIdx.x * BM * BN);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int j = (v * 4) / TM, i = (v * 4) % TM;
+          __stcg(w + v * T + tid, make_float4(acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]));
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g_flags + blockIdx.x), "r"(1u));
+      } else {
+        if (c_k < KT) {  // finisher: add the other holders' partials in CTA order
+          const int c_hi = int((((long long)(c_t + 1) * KT) * G - 1) / U);
+          for (int o = blockIdx.x + 1; o <= c_hi; ++o) {
+            if (tid == 0) {
+              unsigned long long w0, w1;
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w0));
+              unsigned v;
+              do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(g_flags + o));
+              } while (v == 0);
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w1));
+              if (g_wait) g_wait[blockIdx.x] += w1 - w0;
+            }
+            __syncthreads();
+            const float4* w = (const float4*)(g_ws + (long long)o * BM * BN);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              const float4 x = __ldcg(w + v * T + tid);
+              const int j = (v * 4) / TM, i = (v * 4) % TM;
+              acc[j][i] += x.x, acc[j][i + 1] += x.y, acc[j][i + 2] += x.z, acc[j][i + 3] += x.w;
+            }
+            __syncthreads();
+            if (tid == 0) g_flags[o] = 0;
+          }
+        }
+        const int bm = c_t % tiles_m, bn = c_t / tiles_m;
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          const long long col = (long long)bn * BN + bcol + (j / 4) * LY * 4 + j % 4;
+#pragma unroll
+          for (int i = 0; i < TM; i += 4) {
+            const long long row = (long long)bm * BM + arow + (i / 4) * LX * 4;
+            *(float4*)(C + row + col * M) = make_float4(acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]);
+          }
+        }
+      }
+      if (c_k == KT) c_k = 0, ++c_t;
+    }
+  }
+  wait_group<0>();
+  if (g_trace && tid == 0) {
+    unsigned long long t_end;
+    unsigned smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_trace[3 * blockIdx.x] = t_start;
+    g_trace[3 * blockIdx.x + 1] = t_end;
+    g_trace[3 * blockIdx.x + 2] = smid;
+  }
+}
+
+template <int WX, int WY, int LX, int LY, int BK, int S, int PADB, int TM, int TN, int MINB = 1, int ADD = 0>
+void run_sk(Bufs& bf, const float* ref, int M, int N, int K, int R, cudaStream_t st, int G) {
+  constexpr int T = WX * WY * 32, BM = WX * LX * TM, BN = WY * LY * TN;
+  constexpr int ST = BK * BM + BK * (BN + PADB);
+  const size_t smem = size_t(ST) * S * 4;
+  auto kern = ADD ? sgemm_sk2<WX, WY, LX, LY, BK, S, PADB, TM, TN, MINB> : sgemm_sk<WX, WY, LX, LY, BK, S, PADB, TM, TN, MINB>;
+  if (smem > 232448) return;
+  const int tiles = (M / BM) * (N / BN);
+  if (!ADD && G > tiles) { std::printf("sk skip: G %d > tiles %d\n", G, tiles); return; }
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T, smem));
+  if (occ * 148 < G) { std::printf("sk skip: G %d > resident %d\n", G, occ * 148); return; }
+  float* ws;
+  unsigned* fl;
+  CK(cudaMalloc(&ws, std::max(size_t(M) * N, size_t(G) * BM * BN) * 4));
+  CK(cudaMalloc(&fl, std::max(tiles, G) * 4));
+  CK(cudaMemset(fl, 0, std::max(tiles, G) * 4));
+  CK(cudaMemcpyToSymbol(g_ws, &ws, sizeof(ws)));
+  CK(cudaMemcpyToSymbol(g_flags, &fl, sizeof(fl)));
+  for (int w = 0; w < 3; ++w) kern<<<G, T, smem, st>>>(bf.a[0], bf.b[0], bf.c[0], M, N, K, G);
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  std::vector<float> h(size_t(M) * N), r(size_t(M) * N);
+  CK(cudaMemcpy(h.data(), bf.c[0], h.size() * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(r.data(), ref, r.size() * 4, cudaMemcpyDeviceToHost));
+  const bool exact = std::memcmp(h.data(), r.data(), h.size() * 4) == 0;
+  double maxrel = 0;
+  for (size_t i = 0; i < h.size(); ++i) maxrel = std::max(maxrel, double(std::fabs(h[i] - r[i])) / (std::fabs(r[i]) + 1e-3));
+  std::printf("   max rel err %.3g (%zu elems)\n", maxrel, h.size());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  std::vector<float> ts;
+  for (int trial = 0; trial < 7; ++trial) {
+    cudaEventRecord(e0, st);
+    for (int r2 = 0; r2 < R; ++r2) {
+      const int x = r2 % int(bf.a.size());
+      kern<<<G, T, smem, st>>>(bf.a[x], bf.b[x], bf.c[x], M, N, K, G);
+    }
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ts.push_back(ms * 1e3f / R);
+  }
+  {
+    unsigned long long* tr;
+    CK(cudaMalloc(&tr, G * 3 * 8));
+    CK(cudaMemcpyToSymbol(g_trace, &tr, sizeof(tr)));
+    unsigned long long* wt;
+    CK(cudaMalloc(&wt, G * 8));
+    CK(cudaMemset(wt, 0, G * 8));
+    CK(cudaMemcpyToSymbol(g_wait, &wt, sizeof(wt)));
+    kern<<<G, T, smem, st>>>(bf.a[1], bf.b[1], bf.c[1], M, N, K, G);
+    CK(cudaStreamSynchronize(st));
+    {
+      std::vector<unsigned long long> hw(G);
+      CK(cudaMemcpy(hw.data(), wt, G * 8, cudaMemcpyDeviceToHost));
+      unsigned long long* z2 = nullptr;
+      CK(cudaMemcpyToSymbol(g_wait, &z2, sizeof(z2)));
+      double wmax = 0, wsum = 0;
+      for (auto x : hw) wmax = std::max(wmax, double(x)), wsum += double(x);
+      std::printf("   waits: max %.2f us, avg %.2f us\n", wmax / 1e3, wsum / G / 1e3);
+      cudaFree(wt);
+    }
+    std::vector<unsigned long long> h3(G * 3);
+    CK(cudaMemcpy(h3.data(), tr, G * 3 * 8, cudaMemcpyDeviceToHost));
+    unsigned long long* z = nullptr;
+    CK(cudaMemcpyToSymbol(g_trace, &z, sizeof(z)));
+    unsigned long long t0 = ~0ull, t1 = 0;
+    double dmin = 1e30, dmax = 0, dsum = 0;
+    for (int b = 0; b < G; ++b) {
+      t0 = std::min(t0, h3[3 * b]);
+      t1 = std::max(t1, h3[3 * b + 1]);
+      const double d = double(h3[3 * b + 1] - h3[3 * b]);
+      dmin = std::min(dmin, d), dmax = std::max(dmax, d), dsum += d;
+    }
+    std::printf("   trace: span %.2f us, CTA dur min %.2f avg %.2f max %.2f us\n", (t1 - t0) / 1e3, dmin / 1e3,
+                dsum / G / 1e3, dmax / 1e3);
+    std::printf("   starts/durs (us):");
+    for (int b = 0; b < G; b += std::max(1, G / 24))
+      std::printf(" [%d sm%llu +%.1f %.1f]", b, h3[3 * b + 2], (h3[3 * b] - t0) / 1e3, (h3[3 * b + 1] - h3[3 * b]) / 1e3);
+    std::printf("\n");
+    cudaFree(tr);
+  }
+  cudaFree(ws);
+  cudaFree(fl);
+  std::sort(ts.begin(), ts.end());
+  std::printf("sk%s G=%d MINB=%d T%dx%d W%dx%d L%dx%d tile %dx%d BK%-2d S%d thr %4d regs %3d occ %d spill %zu  %8.2f us  %6.1f TF/s  %s\n",
+              ADD ? "2(add)" : "", G, MINB, TM, TN, WX, WY, LX, LY, BM, BN, BK, S, T, fa.numRegs, occ, (size_t)fa.localSizeBytes, ts[3],
+              2.0 * M * N * double(K) / (ts[3] * 1e-6) / 1e12, exact ? "bit-exact" : "MISMATCH");
+}
+
+
+
+// v4: B n-major in shared memory (Bs[n][BK], 16-byte cp.async, the k chunks
+// XOR-swizzled by (n/4)%4 so a warp's four distinct columns hit four bank
+// groups), B fragments read as float4 along k (four k steps per LDS.128,
+// double buffered by k group), A as v3. Serpentine FFMA2 order.
+template <int WX, int WY, int LX, int LY, int BK, int S, int TM, int TN, int MINB, int SPLIT = 1>
+__global__ void __launch_bounds__(WX* WY * 32, MINB) sgemm_v4(const float* __restrict__ A, const float* __restrict__ B,
+                                                      float* __restrict__ C, int M, int N, int K) {
+  constexpr int T = WX * WY * 32;
+  static_assert(TM % 4 == 0 && TN % 4 == 0 && TM <= 8 && TN <= 8 && LY == 4, "thread tile");
+  static_assert(BK % 8 == 0, "BK/4 even");
+  constexpr int BM = WX * LX * TM, BN = WY * LY * TN, KC = BK / 4, NG = BK / 4;
+  constexpr int A_T = BK * BM, B_T = BN * BK, ST = A_T + B_T;
+  extern __shared__ __align__(16) float sm[];
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WX, wn = warp / WX, lx = lane % LX, ly = lane / LX;
+  const int tiles_m = M / BM;
+  const int half = blockIdx.x % SPLIT, tile = blockIdx.x / SPLIT;
+  const int bm = tile % tiles_m, bn = tile / tiles_m;
+  const float* pa = A + (long long)bm * BM + (long long)half * (K / SPLIT) * M;
+  const float* pb = B + (long long)bn * BN * K + half * (K / SPLIT);
+  C += (long long)half * M * N;
+  const int KT = K / SPLIT / BK;
+  auto load = [&](int kt, int slot) {
+    float* sA = sm + slot * ST;
+    float* sB = sA + A_T;
+    const long long k0 = (long long)kt * BK;
+#pragma unroll
+    for (int ch = tid; ch < BK * BM / 4; ch += T) {
+      const int kk = ch / (BM / 4), mm = (ch % (BM / 4)) * 4;
+      cp16(sA + kk * BM + mm, pa + mm + (k0 + kk) * M);
+    }
+#pragma unroll
+    for (int ch = tid; ch < BN * KC; ch += T) {
+      const int n = ch / KC, c = ch % KC;
+      cp16(sB + n * BK + ((c ^ ((n >> 2) & 3)) * 4), pb + k0 + c * 4 + (long long)n * K);
+    }
+  };
+  float acc[TN][TM];
+#pragma unroll
+  for (int j = 0; j < TN; ++j)
+#pragma unroll
+    for (int i = 0; i < TM; ++i) acc[j][i] = 0.f;
+  const int arow = wm * LX * TM + lx * 4, bcol = wn * LY * TN + ly * 4;
+  const int bsw = ((bcol >> 2) & 3);  // (n/4)%4 for this lane's columns (j/4 adds 4 groups: same residue)
+  float fa[2][TM], fb[2][TN][4];
+  auto frag_a = [&](int buf, const float* sA, int k) {
+#pragma unroll
+    for (int h = 0; h < TM / 4; ++h) {
+      const float4 a0 = *(const float4*)(sA + k * BM + arow + h * LX * 4);
+      fa[buf][4 * h] = a0.x, fa[buf][4 * h + 1] = a0.y, fa[buf][4 * h + 2] = a0.z, fa[buf][4 * h + 3] = a0.w;
+    }
+  };
+  auto frag_b = [&](int buf, const float* sB, int g) {
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int n = bcol + (j / 4) * LY * 4 + j % 4;
+      const float4 b0 = *(const float4*)(sB + n * BK + ((g ^ bsw) * 4));
+      fb[buf][j][0] = b0.x, fb[buf][j][1] = b0.y, fb[buf][j][2] = b0.z, fb[buf][j][3] = b0.w;
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < KT) load(s, s);
+    commit();
+  }
+  wait_group<S - 2>();
+  __syncthreads();
+  frag_a(0, sm, 0);
+  frag_b(0, sm + A_T, 0);
+#pragma unroll 1
+  for (int kt = 0; kt < KT; ++kt) {
+    const float* sA = sm + (kt % S) * ST;
+    const float* sB = sA + A_T;
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      const int g = k / 4, q = k % 4;
+      if (k == BK - 1) {
+        wait_group<S - 2>();
+        __syncthreads();
+        const float* nA = sm + ((kt + 1) % S) * ST;
+        frag_a((k + 1) & 1, nA, 0);
+        frag_b(0, nA + A_T, 0);
+      } else {
+        frag_a((k + 1) & 1, sA, k + 1);
+        if (q == 1 && g + 1 < NG) frag_b((g + 1) & 1, sB, g + 1);
+      }
+      if (k == 0) {
+        const int nk = kt + S - 1;
+        if (nk < KT) load(nk, nk % S);
+        commit();
+      }
+#pragma unroll
+      for (int i = 0; i < TM; i += 2)
+#pragma unroll
+        for (int jj = 0; jj < TN; ++jj) {
+          const int j = ((i / 2) & 1) ? TN - 1 - jj : jj;
+          float2 c = make_float2(acc[j][i], acc[j][i + 1]);
+          const float bv = fb[g & 1][j][q];
+          c = __ffma2_rn(make_float2(fa[k & 1][i], fa[k & 1][i + 1]), make_float2(bv, bv), c);
+          acc[j][i] = c.x, acc[j][i + 1] = c.y;
+        }
+    }
+  }
+  wait_group<0>();
+#pragma unroll
+  for (int j = 0; j < TN; ++j) {
+    const long long col = (long long)bn * BN + bcol + (j / 4) * LY * 4 + j % 4;
+#pragma unroll
+    for (int i = 0; i < TM; i += 4) {
+      const long long row = (long long)bm * BM + arow + (i / 4) * LX * 4;
+      *(float4*)(C + row + col * M) = make_float4(acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]);
+    }
+  }
+  if (g_trace && tid == 0) {
+    unsigned long long t_end;
+    unsigned smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_trace[3 * blockIdx.x] = t_start;
+    g_trace[3 * blockIdx.x + 1] = t_end;
+    g_trace[3 * blockIdx.x + 2] = smid;
+  }
+}
+
+template <int WX, int WY, int LX, int LY, int BK, int S, int TM = 8, int TN = 8, int MINB = 1, int SPLIT = 1>
+void run4(Bufs& bf, const float* ref, int M, int N, int K, int R, cudaStream_t st) {
+  constexpr int T = WX * WY * 32, BM = WX * LX * TM, BN = WY * LY * TN;
+  constexpr int ST = BK * BM + BK * BN;
+  const size_t smem = size_t(ST) * S * 4;
+  auto kern = sgemm_v4<WX, WY, LX, LY, BK, S, TM, TN, MINB, SPLIT>;
+  if (smem > 232448) return;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const int grid = (M / BM) * (N / BN) * SPLIT;
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T, smem));
+  for (int w = 0; w < 3; ++w) kern<<<grid, T, smem, st>>>(bf.a[0], bf.b[0], bf.c[0], M, N, K);
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  std::vector<float> h(size_t(M) * N), r(size_t(M) * N);
+  CK(cudaMemcpy(h.data(), bf.c[0], h.size() * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(r.data(), ref, r.size() * 4, cudaMemcpyDeviceToHost));
+  const bool exact = std::memcmp(h.data(), r.data(), h.size() * 4) == 0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  std::vector<float> ts;
+  for (int trial = 0; trial < 7; ++trial) {
+    cudaEventRecord(e0, st);
+    for (int r2 = 0; r2 < R; ++r2) {
+      const int x = r2 % int(bf.a.size());
+      kern<<<grid, T, smem, st>>>(bf.a[x], bf.b[x], bf.c[x], M, N, K);
+    }
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ts.push_back(ms * 1e3f / R);
+  }
+  {
+    unsigned long long* tr;
+    CK(cudaMalloc(&tr, grid * 3 * 8));
+    CK(cudaMemcpyToSymbol(g_trace, &tr, sizeof(tr)));
+    kern<<<grid, T, smem, st>>>(bf.a[1], bf.b[1], bf.c[1], M, N, K);
+    CK(cudaStreamSynchronize(st));
+    std::vector<unsigned long long> h3(grid * 3);
+    CK(cudaMemcpy(h3.data(), tr, grid * 3 * 8, cudaMemcpyDeviceToHost));
+    unsigned long long* z = nullptr;
+    CK(cudaMemcpyToSymbol(g_trace, &z, sizeof(z)));
+    unsigned long long t0 = ~0ull, t1 = 0;
+    double dmin = 1e30, dmax = 0;
+    for (int b = 0; b < grid; ++b) {
+      t0 = std::min(t0, h3[3 * b]);
+      t1 = std::max(t1, h3[3 * b + 1]);
+      const double d = double(h3[3 * b + 1] - h3[3 * b]);
+      dmin = std::min(dmin, d), dmax = std::max(dmax, d);
+    }
+    std::printf("   trace: span %.2f us, CTA dur min %.2f max %.2f us\n", (t1 - t0) / 1e3, dmin / 1e3, dmax / 1e3);
+    cudaFree(tr);
+  }
+  std::sort(ts.begin(), ts.end());
+  std::printf("v4 SPLIT=%d MINB=%d T%dx%d W%dx%d L%dx%d tile %dx%d BK%-2d S%d grid %5d thr %4d regs %3d occ %d spill %zu  %8.2f us  %6.1f TF/s  %s\n",
+              SPLIT, MINB, TM, TN, WX, WY, LX, LY, BM, BN, BK, S, grid, T, fa.numRegs, occ, (size_t)fa.localSizeBytes, ts[3],
               2.0 * M * N * double(K) / (ts[3] * 1e-6) / 1e12, exact ? "bit-exact" : "MISMATCH");
 }
 
@@ -471,16 +1183,79 @@ int main() {
     std::printf("peak %s: %.1f TF/s\n", f2 ? "FFMA2" : "FFMA", 2.0 * 16 * iters * double(blocks) * thr / (ms * 1e-3) / 1e12);
   }
   ref_k<<<dim3(M / 128, N), 128, 0, st>>>(bf.a[0], bf.b[0], ref, M, N, K);
+  {  // the emitter's kernel for the same configuration, compiled by nvcc, timed like the rest
+    const int smem = 37632;
+    CK(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    for (int w = 0; w < 3; ++w) kx<<<128, 128, smem, st>>>(bf.a[0], bf.b[0], bf.c[0]);
+    CK(cudaStreamSynchronize(st));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    std::vector<float> ts;
+    for (int trial = 0; trial < 7; ++trial) {
+      cudaEventRecord(e0, st);
+      for (int r2 = 0; r2 < R; ++r2) kx<<<128, 128, smem, st>>>(bf.a[r2 % NB], bf.b[r2 % NB], bf.c[r2 % NB]);
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ts.push_back(ms * 1e3f / R);
+    }
+    std::sort(ts.begin(), ts.end());
+    std::vector<float> h(size_t(M) * N), r(size_t(M) * N);
+    CK(cudaMemcpy(h.data(), bf.c[0], h.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(r.data(), ref, r.size() * 4, cudaMemcpyDeviceToHost));
+    std::printf("emitted kx (nvcc)  %8.2f us  %s\n", ts[3], std::memcmp(h.data(), r.data(), h.size() * 4) == 0 ? "bit-exact" : "MISMATCH");
+  }
+  {  // the emitter's kernel for the same configuration, compiled by nvcc, timed like the rest
+    const int smem = 37632;
+    CK(cudaFuncSetAttribute(kx2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    for (int w = 0; w < 3; ++w) kx2<<<128, 128, smem, st>>>(bf.a[0], bf.b[0], bf.c[0]);
+    CK(cudaStreamSynchronize(st));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    std::vector<float> ts;
+    for (int trial = 0; trial < 7; ++trial) {
+      cudaEventRecord(e0, st);
+      for (int r2 = 0; r2 < R; ++r2) kx2<<<128, 128, smem, st>>>(bf.a[r2 % NB], bf.b[r2 % NB], bf.c[r2 % NB]);
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ts.push_back(ms * 1e3f / R);
+    }
+    std::sort(ts.begin(), ts.end());
+    std::vector<float> h(size_t(M) * N), r(size_t(M) * N);
+    CK(cudaMemcpy(h.data(), bf.c[0], h.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(r.data(), ref, r.size() * 4, cudaMemcpyDeviceToHost));
+    std::printf("emitted kx2 (opaque dims)  %8.2f us  %s\n", ts[3], std::memcmp(h.data(), r.data(), h.size() * 4) == 0 ? "bit-exact" : "MISMATCH");
+  }
+  {  // the emitter's kernel for the same configuration, compiled by nvcc, timed like the rest
+    const int smem = 37632;
+    CK(cudaFuncSetAttribute(kx3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    for (int w = 0; w < 3; ++w) kx3<<<128, 128, smem, st>>>(bf.a[0], bf.b[0], bf.c[0]);
+    CK(cudaStreamSynchronize(st));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    std::vector<float> ts;
+    for (int trial = 0; trial < 7; ++trial) {
+      cudaEventRecord(e0, st);
+      for (int r2 = 0; r2 < R; ++r2) kx3<<<128, 128, smem, st>>>(bf.a[r2 % NB], bf.b[r2 % NB], bf.c[r2 % NB]);
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ts.push_back(ms * 1e3f / R);
+    }
+    std::sort(ts.begin(), ts.end());
+    std::vector<float> h(size_t(M) * N), r(size_t(M) * N);
+    CK(cudaMemcpy(h.data(), bf.c[0], h.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(r.data(), ref, r.size() * 4, cudaMemcpyDeviceToHost));
+    std::printf("emitted kx3 (opaque KT)  %8.2f us  %s\n", ts[3], std::memcmp(h.data(), r.data(), h.size() * 4) == 0 ? "bit-exact" : "MISMATCH");
+  }
 #define RUN3(WX, WY, LX, LY, BK, S, P, ...) run3<WX, WY, LX, LY, BK, S, P, ##__VA_ARGS__>(bf, ref, M, N, K, R, st)
-  RUN3(2, 2, 8, 4, 16, 3, 4);   // 128x64, 128 thr (cuBLAS's tile)
-  RUN3(4, 2, 8, 4, 16, 3, 4, 4, 8, 0);      // 128x64, 256 thr 4x8, FFMA
-  RUN3(4, 2, 8, 4, 32, 3, 4, 4, 8, 0);
-  RUN3(2, 4, 8, 4, 16, 3, 4, 8, 4, 0);      // 128x64, 256 thr 8x4, FFMA
-  RUN3(4, 2, 8, 4, 16, 4, 4, 4, 8, 0);
-  RUN3(2, 2, 8, 4, 16, 3, 4, 8, 8, 0, 1, 2);  // split-K 2: 2 CTAs/SM, FFMA
-  RUN3(4, 2, 8, 4, 16, 3, 4, 4, 8, 0, 1, 2);  // split-K 2, 256 thr 4x8 FFMA
-  RUN3(4, 2, 8, 4, 16, 3, 4, 4, 8, 1, 1, 2);  // same FFMA2
-  RUN3(4, 4, 8, 4, 16, 3, 4, 4, 4, 0);      // 128x64 512 thr 4x4 FFMA
-  RUN3(2, 2, 8, 4, 16, 3, 4, 4, 8, 0);      // 64x64 128 thr 4x8 FFMA (256 CTAs)
+  RUN3(2, 2, 8, 4, 16, 3, 4, 8, 8, 3);      // serpentine (r2k best)
   return 0;
 }
