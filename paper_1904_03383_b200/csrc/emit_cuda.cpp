@@ -836,6 +836,24 @@ static __device__ __forceinline__ void ispc_cp_async_ca8(void* s, const void* g)
 static __device__ __forceinline__ void ispc_cp_async_ca4(void* s, const void* g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(ispc_smem_addr(s)), "l"(g));
 }
+// the same copies to a 32-bit shared-memory address (NVRTC keeps a generic ->
+// shared conversion per copy otherwise: 64-bit cvt pairs nvcc does not emit)
+static __device__ __forceinline__ void ispc_cp_async_cg16_s(unsigned s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g));
+}
+static __device__ __forceinline__ void ispc_cp_async_ca16_s(unsigned s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g));
+}
+static __device__ __forceinline__ void ispc_cp_async_ca4_s(unsigned s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(g));
+}
+// a 16-byte shared-memory load by 32-bit address (volatile: never moved
+// across the ring's barriers)
+static __device__ __forceinline__ float4 ispc_lds4(unsigned a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
 // issue and commit carry no memory clobber (shared-memory loads of other ring
 // slots may be scheduled across them: the FFMA2 sgemm interleaves its fragment
 // loads with the copies); wait_group is the compiler barrier before a slot is read
@@ -878,6 +896,12 @@ static __device__ __forceinline__ float4 ispc_dsmem_ld4(const float* p, unsigned
   asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "r"(r) : "memory");
   return v;
+}
+static __device__ __forceinline__ void ispc_dsmem_st4(float* p, unsigned rank, float4 v) {
+  unsigned a = ispc_smem_addr(p), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(r), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
 }
 static __device__ __forceinline__ float ispc_dsmem_ld(const float* p, unsigned rank) {
   unsigned a = ispc_smem_addr(p), r;

@@ -712,41 +712,45 @@ std::string sgemm_warp_tiled(const ispc_tile_config& c, const std::string& fn, i
     << "; ++i) acc[j][i] = 0.0f;\n";
   o << "  float fa[2][" << TM << "], fb[2][" << TN << "];\n";
   // copies of k tile kt into ring slot `slot`
+  // copies address shared memory as 32-bit offsets from one converted base
+  o << "  const unsigned ispc_sbase = ispc_smem_addr(ispc_smem);\n";
   o << "  auto load = [&](int kt, int slot) {\n";
-  o << "    float* sA = ispc_smem + slot * " << stage << ";\n";
-  o << "    float* sB = sA + " << a_tile << ";\n";
+  o << "    const unsigned sA = ispc_sbase + slot * " << stage * 4 << "u;\n";
+  o << "    const unsigned sB = sA + " << a_tile * 4 << "u;\n";
   o << "    const long long k0 = (long long)kt * " << BK << ";\n";
   o << "    #pragma unroll\n    for (int ch = tid; ch < " << a_tile / 4 << "; ch += " << T << ") {\n";
   o << "      const int kk = ch / " << BM / 4 << ", mm = (ch % " << BM / 4 << ") * 4;\n";
-  o << "      " << (c.cache == ISPC_CACHE_L1 ? "ispc_cp_async_ca16" : "ispc_cp_async_cg16") << "(sA + kk * " << BM
-    << " + mm, pa + mm + (k0 + kk) * " << M << "LL);\n    }\n";
+  o << "      " << (c.cache == ISPC_CACHE_L1 ? "ispc_cp_async_ca16_s" : "ispc_cp_async_cg16_s") << "(sA + (kk * "
+    << BM << " + mm) * 4u, pa + mm + (k0 + kk) * " << M << "LL);\n    }\n";
   o << "    #pragma unroll\n    for (int e = tid; e < " << BK * BN << "; e += " << T << ") {\n";
   o << "      const int kk = e % " << BK << ", nn = e / " << BK << ";\n";
-  o << "      ispc_cp_async_ca4(sB + kk * " << LDB << " + nn, pb + k0 + kk + (long long)nn * " << K << "LL);\n    }\n";
+  o << "      ispc_cp_async_ca4_s(sB + (kk * " << LDB << " + nn) * 4u, pb + k0 + kk + (long long)nn * " << K
+    << "LL);\n    }\n";
   o << "  };\n";
-  // the fragments of step k of a staged tile
-  o << "  auto frag = [&](int buf, const float* sA, const float* sB, int k) {\n";
+  // the fragments of step k of a staged tile, read by 32-bit shared-memory
+  // address (ld.shared.v4; generic pointer arithmetic stays 64-bit under NVRTC)
+  o << "  auto frag = [&](int buf, unsigned sA, unsigned sB, int k) {\n";
   for (int h = 0; h < TM / 4; ++h)
-    o << "    { const float4 t = *(const float4*)(sA + k * " << BM << " + arow + " << h * LX * 4 << "); fa[buf]["
+    o << "    { const float4 t = ispc_lds4(sA + (k * " << BM << " + arow + " << h * LX * 4 << ") * 4u); fa[buf]["
       << 4 * h << "] = t.x; fa[buf][" << 4 * h + 1 << "] = t.y; fa[buf][" << 4 * h + 2 << "] = t.z; fa[buf]["
       << 4 * h + 3 << "] = t.w; }\n";
   for (int h = 0; h < TN / 4; ++h)
-    o << "    { const float4 t = *(const float4*)(sB + k * " << LDB << " + bcol + " << h * LY * 4 << "); fb[buf]["
+    o << "    { const float4 t = ispc_lds4(sB + (k * " << LDB << " + bcol + " << h * LY * 4 << ") * 4u); fb[buf]["
       << 4 * h << "] = t.x; fb[buf][" << 4 * h + 1 << "] = t.y; fb[buf][" << 4 * h + 2 << "] = t.z; fb[buf]["
       << 4 * h + 3 << "] = t.w; }\n";
   o << "  };\n";
   o << "  #pragma unroll\n  for (int s = 0; s < " << S - 1 << "; ++s) {\n    if (s < ispc_kt"
     << ") load(s, s);\n    ispc_cp_async_commit();\n  }\n";
   o << "  ispc_cp_async_wait<" << S - 2 << ">();\n  __syncthreads();\n";
-  o << "  frag(0, ispc_smem, ispc_smem + " << a_tile << ", 0);\n";
+  o << "  frag(0, ispc_sbase, ispc_sbase + " << a_tile * 4 << "u, 0);\n";
   o << "  #pragma unroll 1\n  for (int kt = 0; kt < ispc_kt; ++kt) {\n";
-  o << "    const float* sA = ispc_smem + (kt % " << S << ") * " << stage << ";\n";
-  o << "    const float* sB = sA + " << a_tile << ";\n";
+  o << "    const unsigned sA = ispc_sbase + (kt % " << S << ") * " << stage * 4 << "u;\n";
+  o << "    const unsigned sB = sA + " << a_tile * 4 << "u;\n";
   o << "    #pragma unroll\n    for (int k = 0; k < " << BK << "; ++k) {\n";
   o << "      if (k == " << BK - 1 << ") {  // the next tile's first fragment, after its barrier\n";
   o << "        ispc_cp_async_wait<" << S - 2 << ">();\n        __syncthreads();\n";
-  o << "        const float* nA = ispc_smem + ((kt + 1) % " << S << ") * " << stage << ";\n";
-  o << "        frag((k + 1) & 1, nA, nA + " << a_tile << ", 0);\n";
+  o << "        const unsigned nA = ispc_sbase + ((kt + 1) % " << S << ") * " << stage * 4 << "u;\n";
+  o << "        frag((k + 1) & 1, nA, nA + " << a_tile * 4 << "u, 0);\n";
   o << "      } else {\n        frag((k + 1) & 1, sA, sB, k + 1);\n      }\n";
   o << "      if (k == 0) {\n        const int nk = kt + " << S - 1 << ";\n        if (nk < ispc_kt"
     << ") load(nk, nk % " << S << ");\n        ispc_cp_async_commit();\n      }\n";
@@ -767,6 +771,40 @@ std::string sgemm_warp_tiled(const ispc_tile_config& c, const std::string& fn, i
     o << "    #pragma unroll\n    for (int i = 0; i < " << TM << "; i += 4)\n";
     o << "      *(float4*)(g_c + bm * " << BM << "LL + arow + (i / 4) * " << LX * 4
       << " + col * " << M << "LL) = make_float4(acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]);\n  }\n";
+  } else if ((TM * TN / 4) % SP == 0) {
+    // exchange: the thread's float4 vectors v (column j, rows i..i+3) are
+    // finished by CTA v % SP of the cluster; after a cluster barrier (every
+    // CTA is done with its ring) each CTA stores the vectors others finish
+    // into slot X[its rank][v / SP][tid] of the finisher's shared memory
+    // (DSMEM), and after a second barrier each finisher sums the SP partials
+    // of its vectors in rank order (as the slice reduction below does) and
+    // stores them: one remote store per foreign vector, no local staging
+    const int NV = TM * TN / 4, NU = NV / SP;
+    o << "  ispc_cluster_sync();\n";
+    o << "  float* X = ispc_smem;\n";
+    for (int v = 0; v < NV; ++v) {
+      const int j = v / (TM / 4), i = (v % (TM / 4)) * 4;
+      o << "  if (rank != " << v % SP << ") ispc_dsmem_st4(X + ((rank * " << NU << " + " << v / SP << ") * " << T
+        << " + tid) * 4, " << v % SP << ", make_float4(acc[" << j << "][" << i << "], acc[" << j << "][" << i + 1
+        << "], acc[" << j << "][" << i + 2 << "], acc[" << j << "][" << i + 3 << "]));\n";
+    }
+    o << "  ispc_cluster_sync();\n";
+    for (int v = 0; v < NV; ++v) {
+      const int j = v / (TM / 4), i = (v % (TM / 4)) * 4;
+      o << "  if (rank == " << v % SP << ") {\n";
+      o << "    const float4 own = make_float4(acc[" << j << "][" << i << "], acc[" << j << "][" << i + 1 << "], acc["
+        << j << "][" << i + 2 << "], acc[" << j << "][" << i + 3 << "]);\n";
+      o << "    float4 s = " << v % SP << " == 0 ? own : *(const float4*)(X + ((0 * " << NU << " + " << v / SP << ") * "
+        << T << " + tid) * 4);\n";
+      for (int q = 1; q < SP; ++q) {
+        o << "    { const float4 t = rank == " << q << " ? own : *(const float4*)(X + ((" << q << " * " << NU << " + "
+          << v / SP << ") * " << T << " + tid) * 4); s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w; }\n";
+      }
+      o << "    *(float4*)(g_c + bm * " << BM << "LL + arow + " << (i / 4) * LX * 4 << " + (bn * " << BN
+        << "LL + bcol + " << (j / 4) * LY * 4 + j % 4 << ") * " << M << "LL) = s;\n  }\n";
+    }
+    L.cluster[0] = uint32_t(SP);
+    L.cluster[1] = L.cluster[2] = 1;
   } else {
     // partial tile P[col][row] (rows contiguous) in this CTA's shared memory;
     // CTA `rank` sums slice `rank` of every CTA's P in rank order and stores it

@@ -116,11 +116,21 @@ inline unsigned ispc_cluster_rank() { return 0; }  // clusters of one CTA only
 inline void ispc_cluster_sync() { emu_yield_barrier(); }
 inline float ispc_dsmem_ld(const float* p, unsigned) { return *p; }
 inline float4 ispc_dsmem_ld4(const float* p, unsigned) { return emu_ld(reinterpret_cast<const float4*>(p)); }
+inline void ispc_dsmem_st4(float* p, unsigned, float4 v) { emu_st(reinterpret_cast<float4*>(p), v); }
 
 inline int ispc_timeout_flag = 0;
 inline unsigned long long ispc_deadline_at = ~0ull;  // the emulator never times out
 inline unsigned long long ispc_now() { return 0; }
 alignas(16) inline float ispc_smem[1 << 16];
+inline unsigned ispc_smem_addr(const void* p) {
+  return unsigned(static_cast<const char*>(p) - reinterpret_cast<const char*>(ispc_smem));
+}
+inline float4 ispc_lds4(unsigned a) {
+  return emu_ld(reinterpret_cast<const float4*>(reinterpret_cast<const char*>(ispc_smem) + a));
+}
+inline void ispc_cp_async_cg16_s(unsigned s, const void* g) { std::memcpy(reinterpret_cast<char*>(ispc_smem) + s, g, 16); }
+inline void ispc_cp_async_ca16_s(unsigned s, const void* g) { std::memcpy(reinterpret_cast<char*>(ispc_smem) + s, g, 16); }
+inline void ispc_cp_async_ca4_s(unsigned s, const void* g) { std::memcpy(reinterpret_cast<char*>(ispc_smem) + s, g, 4); }
 
 inline void emu_fiber_entry() {
   emu_s->kernel();

@@ -137,7 +137,7 @@ def test_sgemm_kernels_bit_exact_on_emulator():
         assert np.array_equal(regs["c"].view(np.uint32), ref.view(np.uint32)), t.as_dict()
 
     # clusters (split-K) need concurrent CTAs: checked on the GPU
-    assert _emulate_all(s, want, root=s.root().decide("tile", ["split"], "1")) >= 5
+    assert _emulate_all(s, want, n=80, root=s.root().decide("tile", ["split"], "1")) >= 5
 
 
 @pytest.mark.parametrize("cfg", [

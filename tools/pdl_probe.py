@@ -25,6 +25,24 @@ CASES = [
                                         warps_n=16, split=4, unroll=16)),
     ("gemv", dict(m=4096, n=4096), dict(cache="STREAM", bk=1, stages=1, vec=4, lanes_m=16, lanes_n=2, warps_m=1,
                                         warps_n=16, split=8, unroll=8)),
+    ("gemv", dict(m=4096, n=4096), dict(cache="STREAM", bk=1, stages=1, vec=4, lanes_m=32, lanes_n=1, warps_m=1,
+                                        warps_n=32, split=4, unroll=16)),
+    ("gemv", dict(m=4096, n=4096), dict(cache="STREAM", bk=1, stages=1, vec=4, lanes_m=32, lanes_n=1, warps_m=2,
+                                        warps_n=16, split=4, unroll=16)),
+    ("gemv", dict(m=4096, n=4096), dict(cache="STREAM", bk=1, stages=1, vec=4, lanes_m=32, lanes_n=1, warps_m=4,
+                                        warps_n=8, split=8, unroll=16)),
+    ("gemv", dict(m=4096, n=4096), dict(cache="STREAM", bk=1, stages=1, vec=4, lanes_m=16, lanes_n=2, warps_m=1,
+                                        warps_n=32, split=8, unroll=8)),
+    ("gemv", dict(m=4096, n=4096), dict(cache="STREAM", bk=1, stages=1, vec=4, lanes_m=16, lanes_n=2, warps_m=2,
+                                        warps_n=16, split=4, unroll=16)),
+    ("gemv", dict(m=4096, n=4096), dict(cache="STREAM", bk=1, stages=1, vec=4, lanes_m=8, lanes_n=4, warps_m=1,
+                                        warps_n=32, split=4, unroll=16)),
+    ("gemv", dict(m=4096, n=4096), dict(cache="STREAM", bk=1, stages=1, vec=4, lanes_m=16, lanes_n=2, warps_m=1,
+                                        warps_n=32, split=2, unroll=16)),
+    ("gemv", dict(m=4096, n=4096), dict(cache="STREAM", bk=1, stages=1, vec=4, lanes_m=32, lanes_n=1, warps_m=1,
+                                        warps_n=32, split=2, unroll=16)),
+    ("gemv", dict(m=4096, n=4096), dict(cache="STREAM", bk=1, stages=1, vec=4, lanes_m=16, lanes_n=2, warps_m=1,
+                                        warps_n=16, split=4, unroll=16)),
     ("batched", dict(m=32, n=32, k=64, batch=512), dict(staging="CP_ASYNC", tm=2, tn=8, bk=16, vec=4, per_cta=1)),
     ("batched", dict(m=32, n=32, k=64, batch=512), dict(staging="CP_ASYNC", tm=4, tn=4, bk=32, vec=4, per_cta=1)),
     ("axpy_stream", dict(n=1 << 26), dict(vec=2, unroll=2, threads=512)),
@@ -57,7 +75,10 @@ def main():
     from paper_1904_03383_b200.measure import rotation
     dev = Device(0)
     l2 = dev.info()["l2_bytes"]
+    kinds = os.environ.get("PROBE_KINDS")
     for kind, shape, fields in CASES:
+        if kinds and kind not in kinds.split(","):
+            continue
         space = Space(kind, **shape)
         dev.bind(space.problem())
         rot = rotation(space, l2)
