@@ -369,3 +369,45 @@ def test_gemv_grid_variants_through_the_abi(dev, cfg):
     y64, scale = orc.gemv_f64(a, x, 4096, 4096)
     y = dev.read("y", 4096).astype(np.float64)
     assert np.max(np.abs(y - y64) / np.maximum(scale, 1e-30)) <= 1e-5
+
+
+@pytest.mark.parametrize("kind,kw", [
+    ("gemv", dict(m=512, n=256)),
+    ("sgemm", dict(m=256, n=256, k=128)),
+    ("batched", dict(m=32, n=32, k=64, batch=64)),
+    ("sgemm_tc", dict(m=256, n=256, k=256)),
+    ("axpy_stream", dict(n=1 << 20)),
+])
+def test_pdl_kernels_match_their_plain_twins(dev, kind, kw):
+    """Programmatic dependent launch (tile decision `pdl`): the same
+    configuration with pdl = 1, launched back to back with the PDL attribute
+    over rotating input copies, passes the on-device check and leaves exactly
+    the output its pdl = 0 twin leaves (griddepcontrol.wait orders every
+    memory access after the previous grid)."""
+    space = Space(kind, **kw)
+    dev.bind(space.problem())
+    out_name, out_n = {"gemv": ("y", kw.get("m", 0)), "axpy_stream": ("z", kw.get("n", 0))}.get(
+        kind, ("c", kw.get("m", 0) * kw.get("n", 0) * kw.get("batch", 1)))
+    checked = 0
+    root = space.root().decide("tile", ["pdl"], "1")
+    for seed in range(40):
+        try:
+            leaf, _, _ = root.random_leaf(seed)
+        except DeadEnd:
+            continue
+        t1 = leaf.tiles()
+        m1 = dev.evaluate_tiles(t1, reps=4, warmup=1, rotate=3)
+        if m1.status == "illegal":
+            continue
+        assert m1.status == "ok" and m1.mismatches == 0, (t1.as_dict(), m1, dev.error())
+        got1 = dev.read(out_name, out_n)
+        t0 = leaf.tiles()
+        t0.pdl = 0
+        m0 = dev.evaluate_tiles(t0, reps=1, warmup=0)
+        assert m0.status == "ok", (t0.as_dict(), m0, dev.error())
+        got0 = dev.read(out_name, out_n)
+        assert np.array_equal(got1.view(np.uint32), got0.view(np.uint32)), t1.as_dict()
+        checked += 1
+        if checked >= 3:
+            break
+    assert checked >= 1, kind

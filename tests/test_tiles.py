@@ -264,3 +264,48 @@ def test_gemv_grid_requires_a_streaming_staging():
     t.bk, t.stages, t.grid = 64, 2, 296
     with pytest.raises(EmitError):
         tile_cuda(t)
+
+
+def test_pdl_is_a_decision_of_every_family_and_shapes_the_kernel():
+    """`pdl` (programmatic dependent launch) is a tile decision of every
+    building-block family; pdl = 1 makes griddepcontrol.wait the kernel's first
+    statement and sets ispc_launch.pdl, pdl = 0 emits neither, and the two are
+    different kernels to time (different source hashes). The emulator runs a
+    pdl = 1 sgemm bit-exactly (the wait and trigger are no-ops there)."""
+    for kind, kw in [("gemv", dict(m=256, n=128)), ("sgemm", dict(m=64, n=64, k=32)),
+                     ("batched", dict(m=8, n=16, k=32, batch=6)), ("sgemm_tc", dict(m=256, n=256, k=128)),
+                     ("axpy_stream", dict(n=1 << 12))]:
+        s = Space(kind, **kw)
+        leaves = {}
+        for v in ("0", "1"):
+            for leaf in _leaves(s, 40, root=s.root().decide("tile", ["pdl"], v)):
+                try:
+                    src, L = tile_cuda(leaf.tiles(), "k_pdl")
+                except EmitError:
+                    continue
+                leaves[v] = (leaf.tiles(), src, L)
+                break
+        assert set(leaves) == {"0", "1"}, kind
+        t1, src1, L1 = leaves["1"]
+        t0, src0, L0 = leaves["0"]
+        assert t1.pdl == 1 and L1.pdl == 1 and t0.pdl == 0 and L0.pdl == 0
+        sig = src1.index(" k_pdl(")
+        body = src1[src1.index(") {\n", sig) + 4:]
+        assert body.startswith("  ispc_grid_dep_wait();\n  ispc_grid_dep_trigger();\n"), kind
+        assert "ispc_grid_dep" not in src0
+        t0.pdl = 1
+        src01, L01 = tile_cuda(t0, "k_pdl")
+        assert L01.source_hash != L0.source_hash and src01.replace("  ispc_grid_dep_wait();\n  ispc_grid_dep_trigger();\n", "") == src0
+    # bit-exact on the emulator with pdl
+    s = Space("sgemm", m=32, n=32, k=32)
+    orc = Oracle()
+    p = s.problem()
+    r = _regions(orc, p)
+    ref = orc.matmul(r["a"], r["b"], 32, 32, 32)
+
+    def want(regs, t):
+        assert t.pdl == 1
+        assert np.array_equal(regs["c"].view(np.uint32), ref.view(np.uint32)), t.as_dict()
+
+    root = s.root().decide("tile", ["split"], "1").decide("tile", ["pdl"], "1")
+    assert _emulate_all(s, want, n=80, root=root) >= 3
