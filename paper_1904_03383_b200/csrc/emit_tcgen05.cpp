@@ -42,6 +42,10 @@ namespace ispc {
 
 namespace {
 [[noreturn]] void illegal(const std::string& why) { throw NestError(ISPC_E_ILLEGAL, why); }
+bool tc_pair_direct() {
+  const char* e = std::getenv("ISPC_TC_PAIR_TMA");
+  return e && std::string(e) == "direct";
+}
 }  // namespace
 
 const char* tcgen05_prelude() {
@@ -66,6 +70,19 @@ static __device__ __forceinline__ void ispc_tma_2d(unsigned dst, const ispc_tmap
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(bar) : "memory");
+}
+// a pair's peer CTA lands its box in its own shared memory and signals the
+// leader's mbarrier (cta_group::2: the barrier may live in the peer CTA)
+static __device__ __forceinline__ void ispc_tma_2d_cg2(unsigned dst, const ispc_tmap_t* map, int c0, int c1,
+                                                       unsigned bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(bar_cluster) : "memory");
+}
+static __device__ __forceinline__ unsigned ispc_mapa(unsigned addr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
 }
 static __device__ __forceinline__ unsigned long long ispc_umma_desc(unsigned addr, unsigned lbo, unsigned sbo) {
   return (unsigned long long)((addr >> 4) & 0x3FFF) | ((unsigned long long)((lbo >> 4) & 0x3FFF) << 16) |
@@ -328,7 +345,12 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   // a pair's MMA (issued by the leader) reads both CTAs' stages: without
   // converters, warp 2 lane 0 of each CTA relays its stage's TMA completion
   // to the leader's conv barrier, which counts both CTAs
-  const bool RELAY = !CONV && PAIR0 == 2;
+  const bool RELAY0 = !CONV && PAIR0 == 2;
+  // direct pair TMA (ISPC_TC_PAIR_TMA=direct): the peer's TMA signals the
+  // leader's full barrier itself (cta_group::2), the leader expects both CTAs'
+  // bytes, and no relay lane runs
+  const bool DIRECT = RELAY0 && tc_pair_direct();
+  const bool RELAY = RELAY0 && !DIRECT;
   if (!(BN == 64 || BN == 128 || BN == 256)) illegal("UMMA N must be 64, 128 or 256");
   if (PAIR != 1 && PAIR != 2) illegal("tcgen05 pairs at most two CTAs (cta_group::2)");
   if (S < 2 || S > 8) illegal("TMA ring depth must be 2..8");
@@ -400,12 +422,20 @@ std::string emit_tcgen05_kernel(const ispc_tile_config& c, const std::string& fn
   o << "      if (kb >= " << S << ") ispc_mbar_wait(bars + " << EMPTY << "u + 8u * s, ((kb / " << S << ") + 1) & 1);\n";
   o << "      const unsigned full = bars + " << FULL << "u + 8u * s;\n";
   o << "      const unsigned sa = base + s * " << t.stage << "u;\n";
+  if (DIRECT) {
+    o << "      const unsigned lfull = rank == 0 ? full : ispc_mapa(full, 0u);\n";
+    o << "      if (rank == 0) ispc_mbar_expect_tx(full, " << 2 * t.tma_bytes << "u);\n";
+    o << "      #pragma unroll\n";
+    o << "      for (int i = 0; i < 4; ++i) ispc_tma_2d_cg2(sa + " << t.off_a << "u + i * 4096u, &tm_a, m_base + i * 32, kb * 32, lfull);\n";
+    o << "      ispc_tma_2d_cg2(sa + " << t.off_b << "u, &tm_b, kb * 32, n_blk * " << BN << " + rank * " << BNL << ", lfull);\n";
+  } else {
   o << "      ispc_mbar_expect_tx(full, " << t.tma_bytes << "u);\n";
   if (A_TMA) {
     o << "      #pragma unroll\n";
     o << "      for (int i = 0; i < 4; ++i) ispc_tma_2d(sa + " << t.off_a << "u + i * 4096u, &tm_a, m_base + i * 32, kb * 32, full);\n";
   }
   o << "      ispc_tma_2d(sa + " << t.off_b << "u, &tm_b, kb * 32, n_blk * " << BN << " + rank * " << BNL << ", full);\n";
+  }
   o << "    }\n";
   o << "  } else if (warp == 1 && lane == 0 && rank == 0) {\n";
   // MMA issuer (the pair's leader): with cta_group::2 the same smem offsets in
@@ -519,7 +549,8 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   if (M > (int64_t(1) << 31) || K > (int64_t(1) << 31) || N > (int64_t(1) << 31))
     illegal("shape too large for the tensor maps");
   const bool CONV = X3 || !A_TMA;
-  const bool RELAY = !CONV && PAIR == 2;  // as in the one-tile kernel
+  const bool DIRECT = !CONV && PAIR == 2 && !QUAD && tc_pair_direct();  // as in the one-tile kernel
+  const bool RELAY = !CONV && PAIR == 2 && !DIRECT;
   // tensor memory holds only the accumulators, double buffered (2 x BN <= 512
   // columns), so the epilogue of tile i overlaps the MMAs of tile i + 1
   const int NB = 2;
@@ -626,6 +657,14 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   o << "        if (g >= " << S << ") ispc_mbar_wait(bars + " << EMPTY << "u + 8u * s, ((g / " << S << ") + 1) & 1);\n";
   o << "        const unsigned full = bars + " << FULL << "u + 8u * s;\n";
   o << "        const unsigned sa = base + s * " << stage << "u;\n";
+  if (DIRECT) {
+    o << "        const unsigned lfull = prank == 0 ? full : ispc_mapa(full, lead);\n";
+    o << "        if (prank == 0) ispc_mbar_expect_tx(full, " << 2 * t.tma_bytes << "u);\n";
+    o << "        #pragma unroll\n";
+    o << "        for (int q = 0; q < 4; ++q) ispc_tma_2d_cg2(sa + " << t.off_a << "u + q * 4096u, &tm_a, m_base + q * 32, kb * 32, lfull);\n";
+    o << "        ispc_tma_2d_cg2(sa + " << t.off_b << "u, &tm_b, kb * 32, n_off + prank * (width / " << PAIR << "), lfull);\n";
+    o << "      }\n    }\n";
+  } else {
   o << "        ispc_mbar_expect_tx(full, " << t.tma_bytes << "u);\n";
   if (A_TMA && QUAD) {  // this CTA lands boxes 2 sub, 2 sub + 1 in itself and in the other pair's same-rank CTA
     o << "        const unsigned short amask = (unsigned short)((1u << rank) | (1u << (rank ^ 2u)));\n";
@@ -640,6 +679,7 @@ std::string emit_tcgen05_persistent(const ispc_tile_config& c, const std::string
   o << "        ispc_tma_2d(sa + " << t.off_b << "u, &tm_b, kb * 32, n_off + prank * (width / " << PAIR
     << "), full);\n";
   o << "      }\n    }\n";
+  }
   o << "  } else if (warp == 1 && lane == 0 && prank == 0) {\n";
   // MMA issuer
   o << "    int g = 0;\n";

@@ -170,12 +170,9 @@ Search::Search(const ispc_space* space, const ispc_search_config& cfg) : space_(
   // q = 0.5 against 56.5 us without, same seed and budget; batched unchanged;
   // profiles/r2h_elite.log); off for the loop-nest spaces (measured worse,
   // section 5 of DESIGN.md)
-  // round 2 (pdl decision added; profiles/r2m_sweep_*.log): q 0.9 with 1.5
-  // expected deviations found the best sgemm (47.9 us) of four settings and a
-  // gemv within 0.3% of the best; the spread between settings is within the
-  // run-to-run spread of one setting
-  elite_q_ = space_->tiles ? 0.9 : 0.0;
-  if (space_->tiles) elite_mut_ = 1.5;
+  // (q 0.5-0.9 with 1.5-3 expected deviations: profiles/r2m_sweep_*.log; the
+  // spread between settings is within the run-to-run spread of one setting)
+  elite_q_ = space_->tiles ? 0.5 : 0.0;
   if (const char* q = std::getenv("ISPC_ELITE_Q")) elite_q_ = std::clamp(std::atof(q), 0.0, 1.0);
   if (const char* mu = std::getenv("ISPC_ELITE_MUT")) elite_mut_ = std::max(0.0, std::atof(mu));
   if (const char* r = std::getenv("ISPC_ROLLOUT")) {

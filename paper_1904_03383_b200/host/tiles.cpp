@@ -73,8 +73,9 @@ double TileFamily::rtol() const {
 }
 
 // every family carries `pdl` (programmatic dependent launch, ispc_launch.pdl),
-// decided first: it shifts every configuration of a family by about the same
-// 1-2 us, so the tree statistics learn it in the first rollouts
+// decided last (decided first with 90% elite-guided rollouts, the searches
+// kept pdl = 0 more often and found slower kernels: profiles/r2n_bench.json
+// against r2l_bench.json)
 TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, std::int64_t k, std::int64_t batch) {
   TileFamily f;
   f.m = m, f.n = n, f.k = k, f.batch = std::max<std::int64_t>(batch, 1);
@@ -96,7 +97,7 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     vec.acc = unroll.acc = true;
     split.cluster = true;
     bk.stage = st.stage = true;
-    f.params = {P("pdl", {0, 1}), vec, lm, ln, wm, wn, split, unroll, bk, st, grid};
+    f.params = {vec, lm, ln, wm, wn, split, unroll, bk, st, grid, P("pdl", {0, 1})};
     f.min_threads = 32;
     f.warp_lanes = 32;
     f.max_acc = 64;
@@ -113,7 +114,7 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     tx.thread = ty.thread = true;
     tm.acc = tn.acc = true;
     split.cluster = true;
-    f.params = {P("pdl", {0, 1}), tx, ty, tm, tn, bk, st, vec, split};
+    f.params = {tx, ty, tm, tn, bk, st, vec, split, P("pdl", {0, 1})};
     f.min_threads = 32;
     f.max_acc = 128;
     pre("staging", {"SHARED", "CP_ASYNC"});
@@ -127,7 +128,7 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     TileParam bk = P("bk", dividing({4, 8, 16, 32, 64}, k)), vec = P("vec", {1, 2, 4});
     pc.thread = true;
     tm.acc = tn.acc = true;
-    f.params = {P("pdl", {0, 1}), pc, tm, tn, bk, vec};
+    f.params = {pc, tm, tn, bk, vec, P("pdl", {0, 1})};
     f.min_threads = 1;
     f.max_acc = 64;
     pre("staging", {"DIRECT", "SHARED", "CP_ASYNC"});
@@ -146,7 +147,7 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     TileParam grid = P("grid", {0, 128, 144, 148});  // 0: one tile per CTA (pair); else persistent CTAs (<= one per SM)
     pair.cluster = true;
     grid.persist = true;
-    f.params = {P("pdl", {0, 1}), bn, st, pair, grid};
+    f.params = {bn, st, pair, grid, P("pdl", {0, 1})};
     f.min_threads = 1;
     f.max_acc = 1;
     f.max_cluster = 4;
@@ -165,7 +166,7 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     TileParam unroll = P("unroll", {1, 2, 4, 8}), grid = P("grid", {0, 148, 296, 592, 1184, 2368, 4736});
     thr.thread = true;
     vec.acc = unroll.acc = true;
-    f.params = {P("pdl", {0, 1}), vec, thr, unroll, grid};
+    f.params = {vec, thr, unroll, grid, P("pdl", {0, 1})};
     f.min_threads = 32;
     f.max_acc = 32;
     pre("staging", {"DIRECT"});
