@@ -268,12 +268,24 @@ def config_worker(args) -> None:
     done = s.step(evals, max_seconds=4 * args.step_timeout)
     st = s.stats()
     best = s.best()
+    elites = s.elites() if space.tiles else []
     s.close()
+    polish_report = None
+    if best is not None and space.tiles and not args.no_polish:
+        # hill-climbing over the incumbent's single-decision (then reshaping
+        # pair) neighbours, same evaluation path (paper_1904_03383_b200/polish.py)
+        from paper_1904_03383_b200 import Device
+        from paper_1904_03383_b200.polish import polish_many
+        dev = Device(args.ordinal)
+        best, polish_report = polish_many(space, [best] + elites, dev, rotation(space, dev.info()["l2_bytes"]))
+        dev.close()
     res = {"shape": kw, "evaluated": st["evaluations"], "ok": st["ok"], "timeouts": st["timeouts"],
            "mismatches": st["mismatches"],
            "illegal": st["illegal"], "launch_errors": st["launch_errors"], "exhausted": bool(st["exhausted"]),
            "deadline_hit": not done, "time_to_best_s": round(st["time_to_best_s"], 3),
            "bound_violations": st["bound_violations"], "search_s": round(time.perf_counter() - t0, 2)}
+    if polish_report is not None:
+        res["polish"] = polish_report
     if best is not None and name == "matmul":  # seconds per launch: the search's own single timing
         res["best"] = {"status": "ok", "kernel_us": round(st["best_ns"] / 1e3, 1),
                        "timing": "one checked launch during the search"}
@@ -303,6 +315,8 @@ def run_configs(kinds, args, local, world, rank) -> dict:
                "--batch-div", str(world), "--step-timeout", str(args.step_timeout)]
         if rank == 0:
             cmd.append("--with-cublas")
+        if args.no_polish:
+            cmd.append("--no-polish")
         try:
             p = subprocess.run(cmd, capture_output=True, text=True, timeout=8 * args.step_timeout + 300)
             lines = [l for l in p.stdout.splitlines() if l.startswith("CONFIG_RESULT ")]
@@ -605,6 +619,7 @@ def main():
     ap.add_argument("--ordinal", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--batch-div", type=int, default=1, help=argparse.SUPPRESS)
     ap.add_argument("--with-cublas", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--no-polish", action="store_true", help="config searches without the hill-climbing polish")
     args = ap.parse_args()
     if args.config_worker:
         import torch

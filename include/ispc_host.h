@@ -311,6 +311,10 @@ int ispc_search_stats_get(const ispc_search* h, ispc_search_stats* out);
 /* Best candidate (reference text serialization) and its CUDA source. */
 int ispc_search_best(const ispc_search* h, char* buf, size_t cap, size_t* len);
 int ispc_search_best_source(const ispc_search* h, char* buf, size_t cap, size_t* len);
+/* The i-th best measured leaf the search keeps for its elite-guided rollouts
+ * (fastest first; at most 8, only when elite guidance is on: the building-block
+ * spaces), reference text serialization; "" past the last. */
+int ispc_search_elite(const ispc_search* h, int i, char* buf, size_t cap, size_t* len);
 const char* ispc_search_error(const ispc_search* h);
 /* Host <-> device copies of the search's bound problem between steps (the
  * end-to-end measurement uploads inputs and reads the output every step). */

@@ -329,6 +329,7 @@ HOST_SYMBOLS = {
     "ispc_search_stats_get": (C.c_int, [C.c_void_p, C.POINTER(SearchStats)]),
     "ispc_search_best": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "ispc_search_best_source": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "ispc_search_elite": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "ispc_search_error": (C.c_char_p, [C.c_void_p]),
     "ispc_search_free": (None, [C.c_void_p]),
     "ispc_search_write_region": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t]),

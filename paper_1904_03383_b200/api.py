@@ -617,6 +617,17 @@ class Search:
         text = N.read_text(N.host().ispc_search_best, self._h)
         return self.space.deserialize(text) if text else None
 
+    def elites(self) -> list[Candidate]:
+        """The best measured leaves kept for elite-guided rollouts, fastest
+        first (building-block spaces; empty for the loop-nest spaces)."""
+        out = []
+        for i in range(64):
+            text = N.read_text(N.host().ispc_search_elite, self._h, i)
+            if not text:
+                break
+            out.append(self.space.deserialize(text))
+        return out
+
     def best_source(self) -> str:
         return N.read_text(N.host().ispc_search_best_source, self._h)
 

@@ -1197,6 +1197,11 @@ std::string Search::best_candidate() const {
   return best_text_;
 }
 
+std::string Search::elite_candidate(size_t i) const {
+  std::lock_guard<std::mutex> lk(const_cast<std::mutex&>(elite_mu_));
+  return i < elites_.size() ? serialize_text(*space_->ctx, elites_[i].leaf) : std::string();
+}
+
 std::string Search::best_source() const {
   std::lock_guard<std::mutex> lk(const_cast<std::mutex&>(mu_));
   return best_src_;
@@ -1292,6 +1297,11 @@ static int put(const std::string& s, char* buf, size_t cap, size_t* len) {
 int ispc_search_best(const ispc_search* h, char* buf, size_t cap, size_t* len) {
   if (!h) return set_err(ISPC_E_ARG, "null search");
   return put(h->s->best_candidate(), buf, cap, len);
+}
+
+int ispc_search_elite(const ispc_search* h, int i, char* buf, size_t cap, size_t* len) {
+  if (!h || i < 0) return set_err(ISPC_E_ARG, "null search or negative index");
+  return put(h->s->elite_candidate(size_t(i)), buf, cap, len);
 }
 
 int ispc_search_best_source(const ispc_search* h, char* buf, size_t cap, size_t* len) {

@@ -138,6 +138,8 @@ class Search {
   int step(int64_t evaluations, double max_seconds = 0);
   ispc_search_stats stats() const;
   std::string best_candidate() const;
+  // the i-th of the best measured leaves (elite-guided rollouts keep 8), "" past the end
+  std::string elite_candidate(size_t i) const;
   std::string best_source() const;
   ispc_launch best_launch() const;
   std::string error() const { return err_; }

@@ -309,3 +309,26 @@ def test_pdl_is_a_decision_of_every_family_and_shapes_the_kernel():
 
     root = s.root().decide("tile", ["split"], "1").decide("tile", ["pdl"], "1")
     assert _emulate_all(s, want, n=80, root=root) >= 3
+
+
+def test_polish_neighbours_are_leaves_of_the_space():
+    """The config searches' hill-climbing polish (paper_1904_03383_b200/polish.py)
+    only ever measures leaves of the same space: every single-decision and
+    reshaping-pair neighbour is a fully specified candidate decided through the
+    reference engine, differs from the incumbent, and round-trips its
+    decisions."""
+    from paper_1904_03383_b200 import polish as P
+    for kind, kw in [("sgemm", dict(m=1024, n=1024, k=1024)), ("gemv", dict(m=4096, n=4096)),
+                     ("batched", dict(m=32, n=32, k=64, batch=512)), ("sgemm_tc", dict(m=4096, n=4096, k=4096))]:
+        s = Space(kind, **kw)
+        leaf = _leaves(s, 10)[0]
+        enums, params = P._decisions(s, leaf)
+        assert "pdl" in params
+        singles, pairs = P.neighbours(s, enums, params), P.neighbours(s, enums, params, pairs=True)
+        assert singles, kind
+        for why, e, q in singles + pairs:
+            assert (e, q) != (enums, params), why
+            c = P._leaf(s, e, q)
+            assert c is not None and c.fully_specified
+            e2, q2 = P._decisions(s, c)
+            assert (e2, q2) == (e, q), why
