@@ -11,7 +11,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 
-CFGS = [dict(staging="TMA", engine="TF32", bn=256, stages=4, split=2, grid=0),
+CFGS = [dict(staging="TMA", engine="TF32", bn=256, stages=7, split=2, grid=148),
+        dict(staging="TMA", engine="TF32", bn=256, stages=7, split=2, grid=128),
+        dict(staging="TMA", engine="TF32", bn=256, stages=7, split=4, grid=128),
+        dict(staging="TMA", engine="TF32", bn=256, stages=7, split=2, grid=0),
+        dict(staging="TMA", engine="TF32", bn=256, stages=4, split=2, grid=0),
         dict(staging="TMA", engine="TF32", bn=256, stages=5, split=2, grid=148),
         dict(staging="TMA", engine="TF32", bn=256, stages=6, split=2, grid=128),
         dict(staging="TMA", engine="TF32", bn=256, stages=6, split=2, grid=148),
@@ -34,7 +38,7 @@ def main():
         rot = rotation(space, l2)
         for f in CFGS:
             row = {"shape": shape["m"], **f}
-            for mode in ("relay", "direct"):
+            for mode in os.environ.get("TC_MODES", "relay,direct").split(","):
                 os.environ["ISPC_TC_PAIR_TMA"] = mode
                 m = dev.evaluate_tiles(config(N, "sgemm_tc", shape, f, 1), reps=reps, warmup=2, rotate=rot)
                 row[mode] = [m.status, round(m.median_ns / 1e3, 2), m.max_err]
