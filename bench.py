@@ -193,8 +193,8 @@ CONFIG_SPACES = {
     "axpy_stream": ("axpy_stream", dict(n=1 << 26), 256, False),
     # budgets: ~2 ms of host + device time per gemv / batched evaluation,
     # ~12 ms per sgemm one (a larger space whose leaves share one bound)
-    "gemv": ("gemv", dict(m=4096, n=4096), 12288, True),
-    "sgemm": ("sgemm", dict(m=1024, n=1024, k=1024), 8192, False),
+    "gemv": ("gemv", dict(m=4096, n=4096), 8192, True),
+    "sgemm": ("sgemm", dict(m=1024, n=1024, k=1024), 6144, False),
     "batched": ("batched", dict(m=32, n=32, k=64, batch=512), 4096, True),
     # the tcgen05 spaces hold ~400 / ~200 runnable leaves (staging x engine x
     # bn x stages x cluster x persistent grid); the bound prunes 3xTF32 leaves

@@ -4,7 +4,7 @@
 // (bit-exact against a sequential fmaf reference kernel).
 //   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/sgemm_lab tools/sgemm_lab.cu -lcublas
 #include <cublas_v2.h>
-#include "_kx_emitted.cuh"  // an emitted kernel (scratch, not committed)
+
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1183,79 +1183,12 @@ int main() {
     std::printf("peak %s: %.1f TF/s\n", f2 ? "FFMA2" : "FFMA", 2.0 * 16 * iters * double(blocks) * thr / (ms * 1e-3) / 1e12);
   }
   ref_k<<<dim3(M / 128, N), 128, 0, st>>>(bf.a[0], bf.b[0], ref, M, N, K);
-  {  // the emitter's kernel for the same configuration, compiled by nvcc, timed like the rest
-    const int smem = 37632;
-    CK(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    for (int w = 0; w < 3; ++w) kx<<<128, 128, smem, st>>>(bf.a[0], bf.b[0], bf.c[0]);
-    CK(cudaStreamSynchronize(st));
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    std::vector<float> ts;
-    for (int trial = 0; trial < 7; ++trial) {
-      cudaEventRecord(e0, st);
-      for (int r2 = 0; r2 < R; ++r2) kx<<<128, 128, smem, st>>>(bf.a[r2 % NB], bf.b[r2 % NB], bf.c[r2 % NB]);
-      cudaEventRecord(e1, st);
-      cudaEventSynchronize(e1);
-      float ms;
-      cudaEventElapsedTime(&ms, e0, e1);
-      ts.push_back(ms * 1e3f / R);
-    }
-    std::sort(ts.begin(), ts.end());
-    std::vector<float> h(size_t(M) * N), r(size_t(M) * N);
-    CK(cudaMemcpy(h.data(), bf.c[0], h.size() * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(r.data(), ref, r.size() * 4, cudaMemcpyDeviceToHost));
-    std::printf("emitted kx (nvcc)  %8.2f us  %s\n", ts[3], std::memcmp(h.data(), r.data(), h.size() * 4) == 0 ? "bit-exact" : "MISMATCH");
-  }
-  {  // the emitter's kernel for the same configuration, compiled by nvcc, timed like the rest
-    const int smem = 37632;
-    CK(cudaFuncSetAttribute(kx2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    for (int w = 0; w < 3; ++w) kx2<<<128, 128, smem, st>>>(bf.a[0], bf.b[0], bf.c[0]);
-    CK(cudaStreamSynchronize(st));
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    std::vector<float> ts;
-    for (int trial = 0; trial < 7; ++trial) {
-      cudaEventRecord(e0, st);
-      for (int r2 = 0; r2 < R; ++r2) kx2<<<128, 128, smem, st>>>(bf.a[r2 % NB], bf.b[r2 % NB], bf.c[r2 % NB]);
-      cudaEventRecord(e1, st);
-      cudaEventSynchronize(e1);
-      float ms;
-      cudaEventElapsedTime(&ms, e0, e1);
-      ts.push_back(ms * 1e3f / R);
-    }
-    std::sort(ts.begin(), ts.end());
-    std::vector<float> h(size_t(M) * N), r(size_t(M) * N);
-    CK(cudaMemcpy(h.data(), bf.c[0], h.size() * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(r.data(), ref, r.size() * 4, cudaMemcpyDeviceToHost));
-    std::printf("emitted kx2 (opaque dims)  %8.2f us  %s\n", ts[3], std::memcmp(h.data(), r.data(), h.size() * 4) == 0 ? "bit-exact" : "MISMATCH");
-  }
-  {  // the emitter's kernel for the same configuration, compiled by nvcc, timed like the rest
-    const int smem = 37632;
-    CK(cudaFuncSetAttribute(kx3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    for (int w = 0; w < 3; ++w) kx3<<<128, 128, smem, st>>>(bf.a[0], bf.b[0], bf.c[0]);
-    CK(cudaStreamSynchronize(st));
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    std::vector<float> ts;
-    for (int trial = 0; trial < 7; ++trial) {
-      cudaEventRecord(e0, st);
-      for (int r2 = 0; r2 < R; ++r2) kx3<<<128, 128, smem, st>>>(bf.a[r2 % NB], bf.b[r2 % NB], bf.c[r2 % NB]);
-      cudaEventRecord(e1, st);
-      cudaEventSynchronize(e1);
-      float ms;
-      cudaEventElapsedTime(&ms, e0, e1);
-      ts.push_back(ms * 1e3f / R);
-    }
-    std::sort(ts.begin(), ts.end());
-    std::vector<float> h(size_t(M) * N), r(size_t(M) * N);
-    CK(cudaMemcpy(h.data(), bf.c[0], h.size() * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(r.data(), ref, r.size() * 4, cudaMemcpyDeviceToHost));
-    std::printf("emitted kx3 (opaque KT)  %8.2f us  %s\n", ts[3], std::memcmp(h.data(), r.data(), h.size() * 4) == 0 ? "bit-exact" : "MISMATCH");
-  }
 #define RUN3(WX, WY, LX, LY, BK, S, P, ...) run3<WX, WY, LX, LY, BK, S, P, ##__VA_ARGS__>(bf, ref, M, N, K, R, st)
-  RUN3(2, 2, 8, 4, 16, 3, 4, 8, 8, 3);      // serpentine (r2k best)
+  RUN3(4, 2, 8, 4, 16, 4, 4, 8, 8, 3, 1, 2);  // 256x64 split-K 2 (slices not reduced: probe)
+#define RUNSK(G, WX, WY, LX, LY, BK, S, P, ...) run_sk<WX, WY, LX, LY, BK, S, P, ##__VA_ARGS__>(bf, ref, M, N, K, R, st, G)
+  RUNSK(128, 4, 2, 8, 4, 16, 4, 4, 8, 8, 1, 1);   // 256x64 tiles, stream-K over 128 CTAs (= split 2)
+  RUNSK(148, 4, 2, 8, 4, 16, 4, 4, 8, 8, 1, 1);   // 256x64 tiles, stream-K over 148 CTAs
+  RUNSK(148, 4, 2, 8, 4, 16, 3, 4, 8, 8, 1, 1);
+  RUNSK(148, 2, 2, 8, 4, 16, 4, 4, 8, 8, 1, 1);   // 128x64 tiles, 148 CTAs
   return 0;
 }
