@@ -208,7 +208,7 @@ CONFIG_SPACES = {
     # make_matmul(1024, 1024, 1024, {{2..32}, {2, 4}}) in gpu.space with the
     # reference's MachineParams (kernels.cpp:435-488), every leaf lowered by
     # the loop-nest emitter, bit-exact against the golden kernel
-    "matmul": ("matmul", dict(m=1024, n=1024, k=1024, factors=[[2, 4, 8, 16, 32], [2, 4]]), 8, False),
+    "matmul": ("matmul", dict(m=1024, n=1024, k=1024, factors=[[2, 4, 8, 16, 32], [2, 4]]), 6, False),
 }
 # per-config search options: the reference's matmul schedules at 1024^3 run
 # for seconds (its gpu.space has no shared-memory staging at this size,
@@ -264,7 +264,10 @@ def config_worker(args) -> None:
         rot = rotation(space, torch.cuda.get_device_properties(args.ordinal).L2_cache_size)
     skw = dict(reps=3, warmup=1)
     skw.update(CONFIG_SEARCH_KW.get(name, {}))
-    s = Search(space, device=args.ordinal, seed=0x1904 + args.ordinal, flush_l2=flush and rot < 2, rotate=rot, **skw)
+    clog = os.path.join(ROOT, "gpurun_out", f"config_{name}.jsonl") if os.path.isdir(
+        os.path.join(ROOT, "gpurun_out")) else None
+    s = Search(space, device=args.ordinal, seed=0x1904 + args.ordinal, flush_l2=flush and rot < 2, rotate=rot,
+               log_path=clog, **skw)
     done = s.step(evals, max_seconds=4 * args.step_timeout)
     st = s.stats()
     best = s.best()

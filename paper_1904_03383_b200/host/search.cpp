@@ -962,11 +962,16 @@ void Search::launch_worker() {
       to.rtol = w.rtol;
       // before the first measurement: 50x the leaf's own bound (>= 2 ms) for
       // the first 64 evaluations, then the cap (a schedule 50x off its bound
-      // is not worth waiting 50 ms for while any incumbent is missing)
+      // is not worth waiting 50 ms for while any incumbent is missing); a
+      // caller that raised the cap above the default (the reference's matmul
+      // space, whose schedules run for seconds ~100x above their bounds) gets
+      // the cap from the start
+      const bool long_cap = cfg_.max_budget_ns > 50e6;
       to.budget_ns = std::isfinite(T) ? std::min(cfg_.max_budget_ns, std::max(T * 1e9 * cfg_.budget_factor,
                                                                               T * 1e9 + 20e3))
-                     : st_.evaluations < 64 ? std::min(cfg_.max_budget_ns, std::max(2e6, 50.0 * w.bound_s * 1e9))
-                                            : cfg_.max_budget_ns;
+                     : st_.evaluations < 64 && !long_cap
+                         ? std::min(cfg_.max_budget_ns, std::max(2e6, 50.0 * w.bound_s * 1e9))
+                         : cfg_.max_budget_ns;
     }
     // screened kernels slower than factor x incumbent cannot become the
     // incumbent: their single checked launch is their time
