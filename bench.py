@@ -289,6 +289,8 @@ def config_worker(args) -> None:
            "bound_violations": st["bound_violations"], "search_s": round(time.perf_counter() - t0, 2)}
     if polish_report is not None:
         res["polish"] = polish_report
+    if st["mismatches"] and not space.tiles:
+        res["failure_replays"] = replay_scaled(clog, kind, kw)
     if best is not None and name == "matmul":  # seconds per launch: the search's own single timing
         res["best"] = {"status": "ok", "kernel_us": round(st["best_ns"] / 1e3, 1),
                        "timing": "one checked launch during the search"}
@@ -327,6 +329,58 @@ def run_configs(kinds, args, local, world, rank) -> dict:
                 "error": (p.stderr.strip().splitlines() or ["no output"])[-1][:300], "rc": p.returncode}
         except subprocess.TimeoutExpired:
             out[kind] = {"error": "config search timed out"}
+    return out
+
+
+def replay_scaled(log_path, kind, kw, size=128, budget_s=180.0) -> list[dict]:
+    """Every mismatch a config search logged, re-decided at a small shape of
+    the same space (the same decision values; the reference's matmul space at
+    1024^3 runs for seconds and exceeds the emulator) and run on the CPU
+    emulator against the CPU oracle: "emulator differs" means the schedule
+    itself computes other values (e.g. an accumulator initialised inside its
+    reduction loop, a temporary read before it is written - schedules the
+    reference space admits), "emulator agrees" a device-side or
+    size-dependent failure."""
+    import numpy as np
+
+    from paper_1904_03383_b200 import Space
+    from tests import emu
+    from tests.oracle_lib import Oracle
+    out = []
+    if not log_path or not os.path.exists(log_path):
+        return out
+    small = dict(kw, m=size, n=size, k=size) if "k" in kw else dict(kw, m=size, n=size)
+    sp = Space(kind, **small)
+    p = sp.problem()
+    orc = Oracle()
+    exp = orc.expected(p)
+    t0 = time.perf_counter()
+    for line in open(log_path):
+        r = json.loads(line)
+        if r.get("status") != "mismatch" or "candidate" not in r:
+            continue
+        rec = {"i": r["i"], "status": r["status"], "hash": r.get("hash"), "replayed_at": size}
+        if time.perf_counter() - t0 > budget_s:
+            rec["verdict"] = "not replayed (time budget)"
+            out.append(rec)
+            continue
+        try:
+            cand = sp.deserialize(json.dumps(r["candidate"]))
+            src, L = cand.nest().cuda("k_emu", watchdog=0)  # no deadline polls (barrier phases) on the emulator
+            regions = {}
+            for i in range(L.num_params):
+                prm = L.params[i]
+                if prm.kind != 0 or not prm.is_input:
+                    continue
+                name, n = prm.name.decode(), int(prm.elems)
+                regions[name] = np.full(n, np.nan, dtype=np.float32) if name in exp else orc.fill(n, p.seed, name)
+            emu.run(src, L, regions, p.alpha)
+            bad = sum(int(np.count_nonzero(regions[nm].view(np.uint32) != w.view(np.uint32))) for nm, w in exp.items())
+            rec["verdict"] = "emulator differs (schedule/emitter)" if bad else "emulator agrees (device-side failure)"
+            rec["emulator_mismatches"] = bad
+        except Exception as e:  # noqa: BLE001 - a verdict, not a crash
+            rec["verdict"] = f"replay error: {str(e)[:200]}"
+        out.append(rec)
     return out
 
 

@@ -411,3 +411,27 @@ def test_pdl_kernels_match_their_plain_twins(dev, kind, kw):
         if checked >= 3:
             break
     assert checked >= 1, kind
+
+
+def test_polish_keeps_the_search_in_its_space_and_checked(dev):
+    """The config searches' polish (hill climbing from the search's best
+    measured leaves): every kernel it ends on is a leaf of the space that passes
+    the on-device check, and it never returns something slower than where it
+    started by more than the timing noise."""
+    from paper_1904_03383_b200 import Search
+    from paper_1904_03383_b200.measure import rotation
+    from paper_1904_03383_b200.polish import polish_many
+    space = Space("batched", m=32, n=32, k=64, batch=128)
+    s = Search(space, device=0, seed=11, reps=3, warmup=1)
+    s.step(48, max_seconds=120)
+    best, elites = s.best(), s.elites()
+    s.close()
+    assert best is not None and elites, "the search measured nothing"
+    rot = rotation(space, dev.info()["l2_bytes"])
+    end, rep = polish_many(space, [best] + elites, dev, rot, budget=60)
+    assert end.fully_specified and rep["evaluated"] <= 60 + 3 * 3 + 3
+    dev.bind(space.problem())
+    m = dev.evaluate_tiles(end.tiles(), reps=8, warmup=2, rotate=rot)
+    assert m.status == "ok" and m.mismatches == 0, (end.tiles().as_dict(), m)
+    for run in rep["starts"]:
+        assert run["end_us"] <= run["start_us"] * 1.001, run
