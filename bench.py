@@ -412,6 +412,8 @@ def replay_failures(log_path, space, ordinal, budget_s=120.0, max_threads=1 << 2
     t0 = time.perf_counter()
     for r in rows:
         rec = {"i": r["i"], "status": r["status"], "hash": r.get("hash")}
+        if r.get("error"):
+            rec["error"] = r["error"]
         if time.perf_counter() - t0 > budget_s:
             rec["verdict"] = "not replayed (time budget)"
             out.append(rec)

@@ -1099,6 +1099,12 @@ void Search::log_eval(const Work& w, const ispc_time_result& r, int rc, const st
   const bool with_cand = improved || failed;
   std::string compact = improved ? best_text_ : failed ? serialize_text(*space_->ctx, w.leaf) : std::string();
   std::replace(compact.begin(), compact.end(), '\n', ' ');
+  if (status == "launch_error" || status == "sticky") {  // the device's last error message rides along
+    std::string e;
+    for (const char* q = dev_ ? ispc_last_error(dev_) : nullptr; q && *q && e.size() < 300; ++q)
+      e += (*q == '"' || *q == '\\') ? '\'' : (static_cast<unsigned char>(*q) < 0x20) ? ' ' : *q;
+    compact += (compact.empty() ? "" : ", ") + std::string("\"error\": \"") + e + "\"";
+  }
   const bool timed = rc == ISPC_OK;
   std::fprintf(log_,
                "{\"i\": %lld, \"t\": %.4f, \"status\": \"%s\", \"median_ns\": %.1f, \"first_ns\": %.1f, "
