@@ -33,6 +33,8 @@ __device__ __forceinline__ float4 ld_stream(const float4* p) {
 // pure read: grid-stride over n4 float4s, U loads in flight per thread
 template <int U>
 __global__ void read_k(const float4* __restrict__ a, long long n4, float* out) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // no-ops unless launched with PDL
+  asm volatile("griddepcontrol.launch_dependents;");
   float s = 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -53,6 +55,8 @@ __global__ void read_k(const float4* __restrict__ a, long long n4, float* out) {
 // pure read, contiguous chunk per CTA (each CTA walks its own 64 MiB / grid)
 template <int U>
 __global__ void read_chunk_k(const float4* __restrict__ a, long long n4, float* out) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   const long long per = n4 / gridDim.x;
   const float4* p = a + per * blockIdx.x;
   float s = 0;
@@ -254,6 +258,17 @@ float timeit(F launch, cudaStream_t st) {
   return ts[3];
 }
 
+template <class K>
+void launch_pdl(K kern, int g, int t, cudaStream_t st, const float4* a, long long n4, float* out) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g), cfg.blockDim = dim3(t), cfg.dynamicSmemBytes = 0, cfg.stream = st;
+  cfg.attrs = at, cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kern, a, n4, out));
+}
+
 int main() {
   cudaStream_t st;
   CK(cudaStreamCreate(&st));
@@ -280,6 +295,27 @@ int main() {
     float us = timeit([&](int c) { read_k<U><<<G, T, 0, st>>>((const float4*)A[c], nA / 4, out); }, st); \
     std::printf("read grid-stride U%-2d grid %5d x %4d: %7.2f us  %7.1f GB/s\n", U, G, T, us, bytes_read / us / 1e3); \
   }
+#define READP(U, G, T)                                                                                   \
+  {                                                                                                      \
+    float us = timeit([&](int c) { launch_pdl(read_k<U>, G, T, st, (const float4*)A[c], nA / 4, out); }, st); \
+    std::printf("read grid-stride U%-2d grid %5d x %4d PDL: %7.2f us  %7.1f GB/s\n", U, G, T, us, bytes_read / us / 1e3); \
+  }
+#define CHUNKP(U, G, T)                                                                                   \
+  {                                                                                                      \
+    float us = timeit([&](int c) { launch_pdl(read_chunk_k<U>, G, T, st, (const float4*)A[c], nA / 4, out); }, st); \
+    std::printf("read chunked    U%-2d grid %5d x %4d PDL: %7.2f us  %7.1f GB/s\n", U, G, T, us, bytes_read / us / 1e3); \
+  }
+  READP(8, 16 * sms, 128);
+  READP(8, 8 * sms, 256);
+  READP(4, 8 * sms, 256);
+  READP(16, 4 * sms, 256);
+  READP(8, 2 * sms, 512);
+  CHUNKP(4, 2048, 256);
+  CHUNKP(4, 4096, 256);
+  CHUNKP(8, 2048, 256);
+  CHUNKP(8, 1184, 256);
+  CHUNKP(4, 1024, 512);
+  READ(8, 16 * sms, 128);
   READ(4, sms, 1024);
   READ(8, sms, 1024);
   READ(4, 2 * sms, 1024);
