@@ -270,7 +270,8 @@ typedef struct {
   uint32_t kind;                 /* ispc_tile_kind                                  */
   uint32_t staging, engine;      /* ispc_staging, ispc_engine                       */
   uint32_t xreduce, cache;       /* ispc_xreduce, ispc_cache (global operand loads) */
-  uint32_t _pad;
+  uint32_t lds;                  /* FFMA2 sgemm: 1 = fragments by 32-bit ld.shared.v4,
+                                    0 = by generic pointers                         */
   int64_t m, n, k, batch;        /* problem shape (column-major operands)           */
   /* decided tile parameters; 0 = not a parameter of this kind                    */
   int32_t thr_m, thr_n;          /* sgemm: CTA threads along m / n                  */

@@ -113,7 +113,7 @@ class Launch(C.Structure):
 
 
 class TileConfig(C.Structure):
-    _fields_ = ([(f, C.c_uint32) for f in ("kind", "staging", "engine", "xreduce", "cache", "_pad")]
+    _fields_ = ([(f, C.c_uint32) for f in ("kind", "staging", "engine", "xreduce", "cache", "lds")]
                 + [(f, C.c_int64) for f in ("m", "n", "k", "batch")]
                 + [(f, C.c_int32) for f in ("thr_m", "thr_n", "tm", "tn", "bk", "bn", "stages", "vec", "lanes_m",
                                             "lanes_n", "warps_m", "warps_n", "split", "unroll", "per_cta",

@@ -727,17 +727,32 @@ std::string sgemm_warp_tiled(const ispc_tile_config& c, const std::string& fn, i
   o << "      ispc_cp_async_ca4_s(sB + (kk * " << LDB << " + nn) * 4u, pb + k0 + kk + (long long)nn * " << K
     << "LL);\n    }\n";
   o << "  };\n";
-  // the fragments of step k of a staged tile, read by 32-bit shared-memory
-  // address (ld.shared.v4; generic pointer arithmetic stays 64-bit under NVRTC)
+  // the fragments of step k of a staged tile (sA / sB: 32-bit shared-memory
+  // addresses of the stage). Decision `lds`: 1 reads them by ld.shared.v4 at
+  // 32-bit addresses (NVRTC keeps generic pointer arithmetic 64-bit), 0 by
+  // generic float4 pointers - each is faster for some shapes (256 x 64 split-K
+  // 2: 46.97 vs 48.13 us; 128 x 64 split 1: 53.2 vs 49.8 us with pdl,
+  // profiles/r2m_pdl_probe2.log, r2m_pdl_probe.log)
+  const bool LDS = c.lds != 0;
   o << "  auto frag = [&](int buf, unsigned sA, unsigned sB, int k) {\n";
-  for (int h = 0; h < TM / 4; ++h)
-    o << "    { const float4 t = ispc_lds4(sA + (k * " << BM << " + arow + " << h * LX * 4 << ") * 4u); fa[buf]["
-      << 4 * h << "] = t.x; fa[buf][" << 4 * h + 1 << "] = t.y; fa[buf][" << 4 * h + 2 << "] = t.z; fa[buf]["
-      << 4 * h + 3 << "] = t.w; }\n";
-  for (int h = 0; h < TN / 4; ++h)
-    o << "    { const float4 t = ispc_lds4(sB + (k * " << LDB << " + bcol + " << h * LY * 4 << ") * 4u); fb[buf]["
-      << 4 * h << "] = t.x; fb[buf][" << 4 * h + 1 << "] = t.y; fb[buf][" << 4 * h + 2 << "] = t.z; fb[buf]["
-      << 4 * h + 3 << "] = t.w; }\n";
+  for (int h = 0; h < TM / 4; ++h) {
+    if (LDS)
+      o << "    { const float4 t = ispc_lds4(sA + (k * " << BM << " + arow + " << h * LX * 4 << ") * 4u); ";
+    else
+      o << "    { const float4 t = *(const float4*)(ispc_smem + (sA - ispc_sbase) / 4u + k * " << BM << " + arow + "
+        << h * LX * 4 << "); ";
+    o << "fa[buf][" << 4 * h << "] = t.x; fa[buf][" << 4 * h + 1 << "] = t.y; fa[buf][" << 4 * h + 2
+      << "] = t.z; fa[buf][" << 4 * h + 3 << "] = t.w; }\n";
+  }
+  for (int h = 0; h < TN / 4; ++h) {
+    if (LDS)
+      o << "    { const float4 t = ispc_lds4(sB + (k * " << LDB << " + bcol + " << h * LY * 4 << ") * 4u); ";
+    else
+      o << "    { const float4 t = *(const float4*)(ispc_smem + (sB - ispc_sbase) / 4u + k * " << LDB << " + bcol + "
+        << h * LY * 4 << "); ";
+    o << "fb[buf][" << 4 * h << "] = t.x; fb[buf][" << 4 * h + 1 << "] = t.y; fb[buf][" << 4 * h + 2
+      << "] = t.z; fb[buf][" << 4 * h + 3 << "] = t.w; }\n";
+  }
   o << "  };\n";
   o << "  #pragma unroll\n  for (int s = 0; s < " << S - 1 << "; ++s) {\n    if (s < ispc_kt"
     << ") load(s, s);\n    ispc_cp_async_commit();\n  }\n";

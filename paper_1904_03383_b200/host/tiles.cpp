@@ -114,7 +114,7 @@ TileFamily make_family(const std::string& kind, std::int64_t m, std::int64_t n, 
     tx.thread = ty.thread = true;
     tm.acc = tn.acc = true;
     split.cluster = true;
-    f.params = {tx, ty, tm, tn, bk, st, vec, split, P("pdl", {0, 1})};
+    f.params = {tx, ty, tm, tn, bk, st, vec, split, P("lds", {0, 1}), P("pdl", {0, 1})};
     f.min_threads = 32;
     f.max_acc = 128;
     pre("staging", {"SHARED", "CP_ASYNC"});
@@ -311,6 +311,7 @@ ispc_tile_config tile_config(const TileFamily& f, const SpaceContext& ctx, const
   t.threads = v("threads");
   t.grid = v("grid");
   t.pdl = v("pdl");
+  t.lds = uint32_t(v("lds"));
   return t;
 }
 

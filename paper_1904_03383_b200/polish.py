@@ -19,7 +19,7 @@ from . import _native as N
 from .api import Candidate, DeadEnd, Device, Space
 
 TILE_PARAMS = ("thr_m", "thr_n", "tm", "tn", "bk", "bn", "stages", "vec", "lanes_m", "lanes_n", "warps_m",
-               "warps_n", "split", "unroll", "per_cta", "threads", "grid", "pdl")
+               "warps_n", "split", "unroll", "per_cta", "threads", "grid", "lds", "pdl")
 ENUMS = {"staging": N.STAGINGS, "engine": N.ENGINES, "xreduce": N.XREDUCES, "cache": N.CACHES}
 
 

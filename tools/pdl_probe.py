@@ -19,6 +19,12 @@ CASES = [
                                                  bk=16, stages=3, vec=4, split=1)),
     ("sgemm", dict(m=1024, n=1024, k=1024), dict(staging="CP_ASYNC", cache="STREAM", thr_m=32, thr_n=8, tm=8, tn=8,
                                                  bk=16, stages=4, vec=4, split=2)),
+    ("sgemm", dict(m=1024, n=1024, k=1024), dict(staging="CP_ASYNC", cache="STREAM", thr_m=32, thr_n=8, tm=8, tn=8,
+                                                 bk=16, stages=4, vec=4, split=2, lds=1)),
+    ("sgemm", dict(m=1024, n=1024, k=1024), dict(staging="CP_ASYNC", cache="STREAM", thr_m=16, thr_n=8, tm=8, tn=8,
+                                                 bk=16, stages=3, vec=4, split=1, lds=1)),
+    ("sgemm", dict(m=1024, n=1024, k=1024), dict(staging="CP_ASYNC", cache="STREAM", thr_m=16, thr_n=8, tm=8, tn=8,
+                                                 bk=16, stages=4, vec=4, split=2, lds=1)),
     ("gemv", dict(m=4096, n=4096), dict(cache="STREAM", bk=1, stages=1, vec=4, lanes_m=16, lanes_n=2, warps_m=1,
                                         warps_n=32, split=4, unroll=16)),
     ("gemv", dict(m=4096, n=4096), dict(cache="STREAM", bk=1, stages=1, vec=4, lanes_m=32, lanes_n=1, warps_m=1,
