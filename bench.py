@@ -192,9 +192,10 @@ CONFIG_SPACES = {
     # searches the reference's own gpu.space for the same computation)
     "axpy_stream": ("axpy_stream", dict(n=1 << 26), 256, False),
     # budgets: ~2 ms of host + device time per gemv / batched evaluation,
-    # ~12 ms per sgemm one (a larger space whose leaves share one bound)
+    # ~35 ms per sgemm one (NVRTC of the unrolled FFMA2 tiles); the polish
+    # (paper_1904_03383_b200/polish.py) follows every building-block search
     "gemv": ("gemv", dict(m=4096, n=4096), 8192, True),
-    "sgemm": ("sgemm", dict(m=1024, n=1024, k=1024), 6144, False),
+    "sgemm": ("sgemm", dict(m=1024, n=1024, k=1024), 4096, False),
     "batched": ("batched", dict(m=32, n=32, k=64, batch=512), 4096, True),
     # the tcgen05 spaces hold ~400 / ~200 runnable leaves (staging x engine x
     # bn x stages x cluster x persistent grid); the bound prunes 3xTF32 leaves
