@@ -55,3 +55,19 @@ def test_replay_verdicts(tmp_path, monkeypatch):
         monkeypatch.setattr(P, "Device", StubDevice)
         out = bench.replay_failures(str(log), space, 0)
         assert len(out) == 1 and out[0]["i"] == 7 and out[0]["verdict"].startswith(verdict), out
+
+
+def test_config_mismatch_replayed_at_a_small_shape(tmp_path):
+    """A mismatch the reference's matmul 1024^3 space produced on the B200
+    (tests/golden/matmul_invalid_schedule.json: the accumulator initialised
+    inside the k loop, the staged temporary read before it is written) is
+    re-decided at 128^3 and run on the emulator against the CPU oracle: the
+    schedule itself computes other values ("emulator differs")."""
+    rec = json.load(open(os.path.join(ROOT, "tests", "golden", "matmul_invalid_schedule.json")))["record"]
+    kw = dict(m=1024, n=1024, k=1024, factors=[[2, 4, 8, 16, 32], [2, 4]])
+    log = tmp_path / "config_matmul.jsonl"
+    log.write_text(json.dumps(rec) + "\n" + json.dumps({"i": 9, "status": "ok"}) + "\n")
+    out = bench.replay_scaled(str(log), "matmul", kw)
+    assert len(out) == 1 and out[0]["i"] == rec["i"] and out[0]["replayed_at"] == 128
+    assert out[0]["verdict"].startswith("emulator differs"), out
+    assert out[0]["emulator_mismatches"] > 0
