@@ -239,6 +239,10 @@ class CudaEmitter {
     const ispc_nest& n = v_.n;
     int64_t threads = v_.threads_per_block();
     if (threads > 1024) throw NestError(ISPC_E_ILLEGAL, "more than 1024 threads per block");
+    // the outermost of three thread levels is threadIdx.z, which the hardware
+    // caps at 64 (the launch fails with CUDA_ERROR_INVALID_VALUE otherwise)
+    if (n.num_thread_levels == 3 && n.thread_shape[0] > 64)
+      throw NestError(ISPC_E_ILLEGAL, "threadIdx.z level of " + std::to_string(n.thread_shape[0]) + " threads (max 64)");
     if (v_.blocks() > 0x7fffffffLL) throw NestError(ISPC_E_ILLEGAL, "grid exceeds 2^31-1 blocks");
     uint32_t max_regs = opts_.max_reg_elems ? opts_.max_reg_elems : 512;
     uint32_t max_unr = opts_.max_unrolled ? opts_.max_unrolled : 16384;

@@ -648,6 +648,11 @@ int bind_kernel(ispc_dev* d, Loaded& mod, const ispc_launch* L, uint32_t rotate,
   int rc = get_function(d, mod, L, &B.fn);
   if (rc) return rc;
   if (L->grid_x == 0 || L->grid_x > 0x7fffffffull) return fail(d, ISPC_E_ILLEGAL, "grid out of range");
+  // the hardware's per-dimension block limits (a schedule mapping a thread
+  // level of 128 to threadIdx.z is not launchable: CUDA_ERROR_INVALID_VALUE)
+  if (L->block[0] > 1024 || L->block[1] > 1024 || L->block[2] > 64)
+    return fail(d, ISPC_E_ILLEGAL, "block dims " + std::to_string(L->block[0]) + " x " + std::to_string(L->block[1]) +
+                                       " x " + std::to_string(L->block[2]) + " exceed x, y <= 1024, z <= 64");
   // the block the candidate asks for must fit the registers ptxas gave the
   // kernel (a static property of the compiled candidate, not a launch error)
   if (drv.FuncGetAttribute) {

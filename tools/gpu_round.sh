@@ -11,6 +11,7 @@ if [ "${2:-}" != "skip-tests" ]; then
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/${TAG}_smoke.log 2>&1; echo "smoke=$?" >> $OUT/${TAG}_smoke.log
 fi
 timeout 1500 python bench.py --steps 5 --warmup 3 > $OUT/${TAG}_bench.log 2>&1; echo "bench=$?" >> $OUT/${TAG}_bench.log
+cp $OUT/search_r0.jsonl $OUT/${TAG}_search_r0.jsonl 2>/dev/null  # the later runs below reuse the name
 nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/${TAG}_smi_after.csv 2>&1
 # the sharded path end to end: 2 ranks (sharing this one GPU), headline only
 BENCH_NO_SAVE_BEST=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29531 \
