@@ -136,3 +136,17 @@ def test_order_decisions_round_trip_through_the_schedule_tree():
     leaf's order decision."""
     r = Space("outer_product", m=2, n=2).root().order_round_trip()
     assert r == {"leaves": 768, "pairs": 768 * 15, "mismatches": 0}
+
+
+def test_threadidx_z_above_64_is_illegal():
+    """The reference space holds schedules whose outermost of three thread
+    levels has 128 or 256 threads; threadIdx.z is capped at 64, so the
+    emitter rejects them (ISPC_E_ILLEGAL) instead of the launch failing with
+    CUDA_ERROR_INVALID_VALUE (one such launch error in the r2u headline)."""
+    import pytest
+
+    from paper_1904_03383_b200 import EmitError
+    sp = Space("axpy", n=1 << 26, factors=[[2, 4], [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024]])
+    leaf = sp.root().random_leaf(117)[0]
+    with pytest.raises(EmitError, match="threadIdx.z"):
+        leaf.nest().cuda("k")
