@@ -89,6 +89,7 @@ def retime_best(space, cand, reps: int = 20, dev=None, ordinal: int = 0) -> dict
     dev = dev or Device(ordinal)
     dev.bind(space.problem())
     rot = rotation(space, dev.info()["l2_bytes"])
+    reps = max(reps, 8 * rot)  # at least 8 groups of back-to-back launches (median over groups)
     if space.tiles:
         m = dev.evaluate_tiles(cand.tiles(), reps=reps, warmup=3, rotate=rot)
     else:
