@@ -1,7 +1,7 @@
 // Development probe (not product): what one launch can stream from HBM at the
 // gemv 4096^2 size (64 MiB), and gemv structures that approach it, timed like
 // the bench (back-to-back launches over rotating copies larger than L2).
-//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/gemv_lab tools/gemv_lab.cu -lcublas
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tools/gemv_lab tools/gemv_lab.cu -lcublas -lcuda
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 

@@ -2,7 +2,7 @@
 // against cuBLAS, to find the kernel structure the emitter's sgemm building
 // block should generate. C = A B column-major, k ascending per output
 // (bit-exact against a sequential fmaf reference kernel).
-//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/sgemm_lab tools/sgemm_lab.cu -lcublas
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tools/sgemm_lab tools/sgemm_lab.cu -lcublas
 #include <cublas_v2.h>
 
 #include <cuda_runtime.h>
