@@ -51,8 +51,10 @@ def _leaf(space: Space, enums: dict, params: dict) -> Candidate | None:
 
 
 def neighbours(space: Space, enums: dict, params: dict, pairs: bool = False) -> list[tuple[str, dict, dict]]:
-    """Single-decision neighbours (each parameter x2, /2, x4, /4 or set to
-    0 / 1 / 148 / 296; each enum changed), or with `pairs` the moves that
+    """Single-decision neighbours (each parameter x2, /2, x4, /4, +-1 when
+    small, or set to 0 / 1, a persistent grid to any SM-shaped size; each
+    enum changed), or
+    with `pairs` the moves that
     double one parameter and halve another (a CTA or warp reshaped at the
     same thread count, a tile traded for split-K depth)."""
     out, seen = [], set()
@@ -70,7 +72,11 @@ def neighbours(space: Space, enums: dict, params: dict, pairs: bool = False) -> 
                     add(f"{p}={v * 2},{r}={w // 2}", enums, dict(params, **{p: v * 2, r: w // 2}))
     else:
         for p, v in params.items():
-            for w in sorted({v * 2, v // 2, v * 4, v // 4, 0, 1, 148, 296} - {v}):
+            # persistent grid sizes are SM-count shaped, not powers of two
+            extra = {0, 128, 144, 148, 296, 592, 1184, 2368, 4736} if p == "grid" else {0, 1}
+            if 1 < v <= 16:  # ring depths and other small counts are not powers of two
+                extra |= {v - 1, v + 1}
+            for w in sorted(({v * 2, v // 2, v * 4, v // 4} | extra) - {v}):
                 if w >= 0:
                     add(f"{p}={w}", enums, dict(params, **{p: w}))
         for ch, values in ENUMS.items():
