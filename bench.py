@@ -194,8 +194,8 @@ CONFIG_SPACES = {
     # budgets: ~2 ms of host + device time per gemv / batched evaluation,
     # ~35 ms per sgemm one (NVRTC of the unrolled FFMA2 tiles); the polish
     # (paper_1904_03383_b200/polish.py) follows every building-block search
-    "gemv": ("gemv", dict(m=4096, n=4096), 8192, True),
-    "sgemm": ("sgemm", dict(m=1024, n=1024, k=1024), 4096, False),
+    "gemv": ("gemv", dict(m=4096, n=4096), 6144, True),
+    "sgemm": ("sgemm", dict(m=1024, n=1024, k=1024), 3072, False),
     "batched": ("batched", dict(m=32, n=32, k=64, batch=512), 4096, True),
     # the tcgen05 spaces hold ~400 / ~200 runnable leaves (staging x engine x
     # bn x stages x cluster x persistent grid); the bound prunes 3xTF32 leaves
@@ -209,7 +209,7 @@ CONFIG_SPACES = {
     # make_matmul(1024, 1024, 1024, {{2..32}, {2, 4}}) in gpu.space with the
     # reference's MachineParams (kernels.cpp:435-488), every leaf lowered by
     # the loop-nest emitter, bit-exact against the golden kernel
-    "matmul": ("matmul", dict(m=1024, n=1024, k=1024, factors=[[2, 4, 8, 16, 32], [2, 4]]), 6, False),
+    "matmul": ("matmul", dict(m=1024, n=1024, k=1024, factors=[[2, 4, 8, 16, 32], [2, 4]]), 4, False),
 }
 # per-config search options: the reference's matmul schedules at 1024^3 run
 # for seconds (its gpu.space has no shared-memory staging at this size,
