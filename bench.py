@@ -216,7 +216,10 @@ CONFIG_SPACES = {
 # SURVEY 0.5; the greedy descent's lowest-bound leaf - bound 70 ms - runs
 # 6.6 s on 2 blocks of 4 threads, profiles/r2f_matmul_parity.log), so the
 # config measures a handful of leaves once each under an 8 s watchdog
-CONFIG_SEARCH_KW = {"matmul": dict(max_budget_ns=8e9, reps=1, warmup=0)}
+CONFIG_SEARCH_KW = {"matmul": dict(max_budget_ns=5e9, reps=1, warmup=0)}
+# wall-clock caps of the config searches (the default bench run stays near
+# 6-7 minutes; NVRTC of the unrolled FFMA2 tiles varies 2x between boxes)
+CONFIG_SECONDS = {"sgemm": 120.0, "gemv": 45.0, "batched": 60.0}
 
 
 def safe_step(search, evals, seconds) -> bool:
@@ -269,7 +272,7 @@ def config_worker(args) -> None:
         os.path.join(ROOT, "gpurun_out")) else None
     s = Search(space, device=args.ordinal, seed=0x1904 + args.ordinal, flush_l2=flush and rot < 2, rotate=rot,
                log_path=clog, **skw)
-    done = s.step(evals, max_seconds=4 * args.step_timeout)
+    done = s.step(evals, max_seconds=min(4 * args.step_timeout, CONFIG_SECONDS.get(name, float("inf"))))
     st = s.stats()
     best = s.best()
     elites = s.elites() if space.tiles else []
