@@ -137,8 +137,8 @@ def polish(space: Space, leaf: Candidate, dev: Device, rotate: int, budget: int 
                   "moves": moves}
 
 
-def polish_many(space: Space, starts: list[Candidate], dev: Device, rotate: int, budget: int = 320,
-                max_starts: int = 3) -> tuple[Candidate, dict]:
+def polish_many(space: Space, starts: list[Candidate], dev: Device, rotate: int, budget: int = 400,
+                max_starts: int = 4) -> tuple[Candidate, dict]:
     """Hill-climbs from up to `max_starts` distinct starting leaves (the
     search's best measured ones, fastest first), splitting the budget, and
     returns the fastest end point by a final paired re-time."""
