@@ -429,7 +429,7 @@ def test_polish_keeps_the_search_in_its_space_and_checked(dev):
     assert best is not None and elites, "the search measured nothing"
     rot = rotation(space, dev.info()["l2_bytes"])
     end, rep = polish_many(space, [best] + elites, dev, rot, budget=60)
-    assert end.fully_specified and rep["evaluated"] <= 60 + 3 * 3 + 3
+    assert end.fully_specified and rep["evaluated"] <= 60 + 4 * 3 + 4  # each start may overshoot by a confirm pair
     dev.bind(space.problem())
     m = dev.evaluate_tiles(end.tiles(), reps=8, warmup=2, rotate=rot)
     assert m.status == "ok" and m.mismatches == 0, (end.tiles().as_dict(), m)
